@@ -56,7 +56,7 @@ $(OBJ)/cuda/%.o: $(PKG)/csrc/cuda/%.cpp $(CU_HDR) $(wildcard include/c3sim/*.hpp
 $(LIB)/libc3cuda.so: $(CU_OBJ) $(CC_OBJ) $(LIB)/libc3sim.so
 	@mkdir -p $(@D)
 	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $(CU_OBJ) $(CC_OBJ) -L$(LIB) -lc3sim \
-	    -L$(CUDA)/lib64/stubs -lcuda -lcudart_static -Xlinker -rpath,'$$ORIGIN'
+	    -lcudart_static -Xlinker -rpath,'$$ORIGIN'
 
 $(BIN)/c3sim: $(PKG)/csrc/tools/c3sim_cli.cpp $(LIB)/libc3sim.so
 	@mkdir -p $(@D)

@@ -1,0 +1,221 @@
+/* c3cuda.h — C ABI of libc3cuda.so, the B200 execution layer of the C3 hot path:
+ * a GEMM running concurrently with an all-gather / reduce-scatter across the
+ * GPUs of one node, under the paper's strategies.
+ *
+ * Plain C: opaque handles, POD structs, int status codes, no exceptions and no
+ * torch types across the boundary. Status codes mirror the reference error
+ * taxonomy (/root/reference/proj/include/c3sim/errors.hpp:8-28): 0 ok,
+ * 2 I/O, 3 unknown entity, 4 validation, 5 fit; >= 100 CUDA runtime / driver
+ * failures, message in c3_last_error() (thread-local).
+ *
+ * Which reference interface each entry point stands in for (file:line under
+ * /root/reference/proj) is given next to it. The reference never executes a
+ * collective or a GEMM — it models them — so "replaces" means: this call
+ * executes on B200 what that declaration describes/costs.
+ *
+ * Process model: one process per GPU (torchrun), or a LOOPBACK world in which
+ * all n ranks are virtual and live on one device (parity tests, and the 1-GPU
+ * bench, where the peers are stand-in HBM buffers and no NVLink is involved).
+ * Peer memory is mapped with CUDA IPC: export a handle, exchange handles with
+ * any host transport (the tests and bench use torch.distributed), import.
+ */
+#ifndef C3CUDA_H
+#define C3CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define C3_OK 0
+#define C3_ERR_IO 2
+#define C3_ERR_UNKNOWN 3
+#define C3_ERR_VALIDATION 4
+#define C3_ERR_FIT 5
+#define C3_ERR_CUDA 100
+#define C3_ERR_DRIVER 101
+#define C3_ERR_UNSUPPORTED 102
+
+#define C3_MAX_RANKS 8
+#define C3_IPC_HANDLE_BYTES 64
+
+/* c3sim::CollectiveKind (workload.hpp:14) + the ReduceScatter extension. */
+#define C3_ALL_GATHER 0
+#define C3_ALL_TO_ALL 1
+#define C3_REDUCE_SCATTER 2
+
+/* c3sim::Strategy ordinals (sim.hpp:15). */
+#define C3_SERIAL 0
+#define C3_C3_BASE 1
+#define C3_C3_SP 2
+#define C3_C3_RP 3
+#define C3_C3_SP_RP 4
+#define C3_CONCCL 5
+#define C3_CONCCL_RP 6
+/* extra execution-only modes (not reference strategies): */
+#define C3_GEMM_ONLY 100 /* isolated GEMM */
+#define C3_COMM_ONLY_CU 101 /* isolated SM-driven collective */
+#define C3_COMM_ONLY_DMA 102 /* isolated copy-engine collective */
+
+/* c3sim::CommBackend (interference.hpp:14). */
+#define C3_BACKEND_CU 0
+#define C3_BACKEND_DMA 1
+
+typedef struct c3_world c3_world;
+typedef struct c3_session c3_session;
+
+/* Mirror of c3sim::Transfer (conccl.hpp:15-23). */
+typedef struct c3_transfer {
+    int32_t src_gpu, dst_gpu;
+    int64_t src_offset, dst_offset, length;
+    int32_t engine_id, seq;
+} c3_transfer;
+
+typedef struct c3_world_info {
+    int rank, n_ranks, device, loopback;
+    int sm_count;            /* cus_per_gpu of the B200 machine descriptor */
+    int async_engines;       /* dma_engines_per_gpu */
+    int l2_bytes;            /* llc_capacity */
+    int cc_major, cc_minor;
+    int green_ctx;           /* 1 when SM partitioning via green contexts works */
+    int sm_grain;            /* min_cu_grain: green-context SM split granularity */
+    int stream_prio_lo, stream_prio_hi;
+} c3_world_info;
+
+/* One C3 scenario (c3sim::C3Scenario, workload.hpp:37-43), executable form:
+ * GEMM C[m,n] = A[m,k] B[n,k]^T in bf16 with fp32 accumulation, plus one
+ * collective of `payload_bytes` per rank (all-gather: gathered bytes;
+ * reduce-scatter: input bytes, bf16 elements) over n_ranks. */
+typedef struct c3_scenario_desc {
+    int64_t m, n, k;
+    int32_t collective;
+    int32_t n_ranks;
+    int64_t payload_bytes;
+} c3_scenario_desc;
+
+/* c3sim::Allocation (sim.hpp:25-31), in SMs. */
+typedef struct c3_alloc {
+    int32_t cus_gemm, cus_comm, cus_idle;
+    int32_t backend;
+    int32_t comm_first;
+} c3_alloc;
+
+/* Device-event timing of one C3 step on this rank, milliseconds from the
+ * step's start event. partition: 0 none/CTA caps, 1 green contexts. */
+typedef struct c3_timing {
+    double gemm_start_ms, gemm_end_ms;
+    double comm_start_ms, comm_end_ms;
+    double total_ms;
+    int32_t gemm_ctas, comm_ctas, partition, launches;
+} c3_timing;
+
+typedef struct c3_session_ptrs {
+    void* a;          /* bf16 [m,k] */
+    void* b;          /* bf16 [n,k] */
+    void* c;          /* bf16 [m,n] */
+    void* send;       /* AG: chunk bytes; RS: payload bytes (n slots) */
+    void* recv;       /* AG: payload bytes (n slots); RS: payload/n bytes */
+    void* staging;    /* RS copy-engine staging: payload bytes */
+    int64_t a_bytes, b_bytes, c_bytes, send_bytes, recv_bytes, staging_bytes;
+    int32_t virtual_ranks; /* loopback: n; else 1. ptrs above are rank 0's */
+} c3_session_ptrs;
+
+/* ---------------------------------------------------------------- errors */
+const char* c3_last_error(void);
+int c3_version(void);
+
+/* ----------------------------------------------------------------- world
+ * Replaces the reference's static machine model MachineDescriptor
+ * (machine.hpp:13-28) with the live device: c3_world_get_info reports the
+ * numbers a B200 machine file is generated from. */
+int c3_world_create(int rank, int n_ranks, int device, int loopback, c3_world** out);
+int c3_world_destroy(c3_world* w);
+int c3_world_get_info(const c3_world* w, c3_world_info* out);
+/* barrier-free device memory helpers (setup only; hot calls never allocate) */
+int c3_malloc(c3_world* w, int64_t bytes, void** ptr);
+int c3_free(c3_world* w, void* ptr);
+int c3_memcpy(void* dst, const void* src, int64_t bytes, int kind /*cudaMemcpyKind*/, void* stream);
+int c3_stream_sync(void* stream);
+int c3_device_sync(void);
+/* CUDA IPC mapping of a c3_malloc'ed buffer into peers. */
+int c3_ipc_export(c3_world* w, void* ptr, void* handle_out);
+int c3_ipc_import(c3_world* w, const void* handle, void** peer_ptr);
+int c3_ipc_close(c3_world* w, void* peer_ptr);
+
+/* --------------------------------------------------- synthetic inputs
+ * Counter-hash data shared bit-for-bit with oracle/c3oracle.c. */
+int c3_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor, void* stream);
+int c3_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor, void* stream);
+
+/* ------------------------------------------------------------------ GEMM
+ * Executes c3sim::GemmKernel (workload.hpp:18-25) whose cost
+ * roofline_gemm_time (workload.hpp:62-63) models; max_ctas caps the
+ * persistent grid = the GEMM's SM allocation (Allocation::cus_gemm). */
+int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
+                 int64_t k, int max_ctas, void* stream);
+
+/* ----------------------------------------------------------- collectives
+ * SM-driven ("CU backend") direct algorithm over mapped peer memory.
+ * recv[p] = rank p's receive base (peer-mapped, or local in loopback);
+ * rank `self` writes its chunk to recv[p] + self*chunk for every p (its own
+ * slot too, unless send already aliases it). n_ctas = the comm kernel's SM
+ * allocation (Allocation::cus_comm). These standalone calls carry no
+ * cross-rank completion signal: in a multi-process world pair them with a
+ * host barrier (a c3_session's collectives signal through peer flags).
+ * Replaces: CollectiveOp{AllGather} execution (workload.hpp:27-35) whose
+ * wire time roofline_collective_time (workload.hpp:66-67) models. */
+int c3_allgather_p2p(c3_world* w, int self, const void* send, void* const* recv,
+                     int64_t chunk_bytes, int n_ctas, void* stream);
+/* Direct reduce-scatter, pull form: out = sum_{g=0..n-1} in[g][self*count ..],
+ * fp32 accumulation in rank order, one bf16 rounding. in[g] = rank g's
+ * input (peer-mapped or local). Extension: no reference counterpart. */
+int c3_reduce_scatter_p2p(c3_world* w, int self, const void* const* in, void* out,
+                          int64_t count, int n_ctas, void* stream);
+/* Local n-slot reduce (copy-engine reduce-scatter second phase). */
+int c3_reduce_local_bf16(const void* const* slots, int n_slots, void* out, int64_t count,
+                         int n_ctas, void* stream);
+/* Copy-engine ("DMA backend", ConCCL) executor: each transfer with
+ * src_gpu == src_filter (or every transfer when src_filter < 0) becomes one
+ * cudaMemcpyAsync dst[t.dst_gpu]+dst_offset <- src[t.src_gpu]+src_offset on
+ * the world's copy stream for t.engine_id; no SM runs a kernel for it.
+ * Replaces: executing c3sim::TransferPlan (conccl.hpp:33-39) produced by
+ * plan_all_gather / plan_all_to_all (conccl.hpp:44-50), whose cost plan_cost
+ * (conccl.hpp:72-73) models. The plan must pass validate_plan first. */
+int c3_ce_execute(c3_world* w, const c3_transfer* t, int n_transfers, const void* const* src,
+                  void* const* dst, int src_filter, void* stream);
+
+/* The ConCCL plan itself, from the product model layer (libc3sim): the
+ * reference plan_all_gather / plan_all_to_all (conccl.hpp:44-50) plus the
+ * reduce-scatter copy phase, validated with validate_plan (conccl.hpp:60)
+ * before it is returned. out may be NULL to query *count. */
+int c3_plan_transfers(int kind, int n_ranks, int64_t chunk_bytes, int dma_engines,
+                      c3_transfer* out, int capacity, int* count);
+
+/* ------------------------------------------------------------ C3 runtime
+ * A session owns one scenario's operands and executes it under a strategy.
+ * Replaces (executes) c3sim::simulate (sim.hpp:70-73) for the strategy the
+ * reference's allocate_cus (sim.hpp:38-40) describes; alloc == NULL means
+ * "use the model's own allocation for this machine". */
+int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** out);
+int c3_session_destroy(c3_session* s);
+int c3_session_pointers(const c3_session* s, int virtual_rank, c3_session_ptrs* out);
+int c3_session_fill(c3_session* s, uint64_t seed);
+/* multi-process: export this rank's recv/send/staging/signal handles
+ * (C3_SESSION_HANDLE_BYTES), then import every rank's blob (rank order). */
+#define C3_SESSION_HANDLE_BYTES (4 * C3_IPC_HANDLE_BYTES)
+int c3_session_export(c3_session* s, void* blob_out);
+int c3_session_import(c3_session* s, const void* all_blobs);
+/* One C3 step (synchronous on the host at the end; device-event timed). */
+int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);
+/* Loopback parity form: every virtual rank's share of the collective runs (the
+ * plain call runs rank 0's share only, the per-GPU load of a real world). */
+int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);
+/* The allocation c3_session_run uses for (strategy, alloc == NULL). */
+int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* C3CUDA_H */

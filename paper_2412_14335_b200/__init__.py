@@ -1,0 +1,119 @@
+"""c3-b200: B200-native execution of the C3 hot path of arXiv 2412.14335 —
+a GEMM concurrent with an all-gather / reduce-scatter across one node's GPUs,
+under the paper's strategies (serial, c3_base, c3_sp, c3_rp, c3_sp_rp, conccl,
+conccl_rp).
+
+The product is native: ``lib/libc3sim.so`` (the reference's c3sim C++ API,
+``include/c3sim/*.hpp``) and ``lib/libc3cuda.so`` (sm_100a kernels + runtime
+behind the C ABI ``include/c3cuda.h``). This package is the thin Python host
+mirror used by bench.py and the tests; it owns no compute.
+"""
+import ctypes as C
+
+from . import _capi
+from ._capi import (ALL_GATHER, ALL_TO_ALL, REDUCE_SCATTER, SERIAL, C3_BASE, C3_SP, C3_RP,
+                    C3_SP_RP, CONCCL, CONCCL_RP, GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA,
+                    STRATEGY_NAMES, BACKEND_CU, BACKEND_DMA, C3Error, check, lib, ptr_array)
+
+__all__ = ["World", "Session", "plan_transfers", "ideal_speedup", "fraction_of_ideal",
+           "STRATEGY_NAMES", "C3Error"]
+
+
+def ideal_speedup(t_gemm, t_comm):
+    """(t_g + t_c) / max(t_g, t_c) — reference taxonomy.cpp:23-27."""
+    if not (t_gemm > 0 and t_comm > 0):
+        raise ValueError("ideal_speedup: times must be positive")
+    return (t_gemm + t_comm) / max(t_gemm, t_comm)
+
+
+def fraction_of_ideal(speedup, ideal):
+    """(speedup - 1) / (ideal - 1), 0 for a slowdown, not capped — taxonomy.cpp:29-33."""
+    if not ideal > 1:
+        raise ValueError("fraction_of_ideal: ideal must be > 1")
+    return 0.0 if speedup < 1.0 else (speedup - 1.0) / (ideal - 1.0)
+
+
+def plan_transfers(kind, n_ranks, chunk_bytes, dma_engines):
+    """The validated ConCCL plan from the product model layer (libc3sim)."""
+    L = lib()
+    n = C.c_int(0)
+    check(L.c3_plan_transfers(kind, n_ranks, chunk_bytes, dma_engines, None, 0, C.byref(n)))
+    arr = (_capi.Transfer * max(1, n.value))()
+    check(L.c3_plan_transfers(kind, n_ranks, chunk_bytes, dma_engines, arr, n.value, C.byref(n)))
+    return arr, n.value
+
+
+class World:
+    """One device; `loopback=True` hosts all n ranks virtually on it."""
+
+    def __init__(self, rank=0, n_ranks=1, device=0, loopback=False):
+        self.h = C.c_void_p()
+        check(lib().c3_world_create(rank, n_ranks, device, int(bool(loopback)), C.byref(self.h)))
+        info = _capi.WorldInfo()
+        check(lib().c3_world_get_info(self.h, C.byref(info)))
+        self.info = info
+        self.rank, self.n_ranks = info.rank, info.n_ranks
+
+    def close(self):
+        if self.h:
+            check(lib().c3_world_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def gemm(self, a, b, c, m, n, k, max_ctas=0, stream=None):
+        check(lib().c3_gemm_bf16(self.h, a, b, c, m, n, k, max_ctas, stream))
+
+    def allgather_p2p(self, self_rank, send, recv_ptrs, chunk_bytes, n_ctas=32, stream=None):
+        check(lib().c3_allgather_p2p(self.h, self_rank, send, ptr_array(recv_ptrs), chunk_bytes,
+                                     n_ctas, stream))
+
+    def reduce_scatter_p2p(self, self_rank, in_ptrs, out, count, n_ctas=32, stream=None):
+        check(lib().c3_reduce_scatter_p2p(self.h, self_rank, ptr_array(in_ptrs), out, count,
+                                          n_ctas, stream))
+
+    def ce_execute(self, transfers, n_transfers, src_ptrs, dst_ptrs, src_filter=-1, stream=None):
+        check(lib().c3_ce_execute(self.h, transfers, n_transfers, ptr_array(src_ptrs),
+                                  ptr_array(dst_ptrs), src_filter, stream))
+
+
+class Session:
+    """One C3 scenario's operands, executed under a strategy (c3_session_*)."""
+
+    def __init__(self, world, m, n, k, collective, payload_bytes):
+        self.world = world
+        d = _capi.ScenarioDesc(m, n, k, collective, world.n_ranks, payload_bytes)
+        self.desc = d
+        self.h = C.c_void_p()
+        check(lib().c3_session_create(world.h, C.byref(d), C.byref(self.h)))
+
+    def close(self):
+        if self.h:
+            check(lib().c3_session_destroy(self.h))
+            self.h = C.c_void_p()
+
+    def pointers(self, virtual_rank=0):
+        p = _capi.SessionPtrs()
+        check(lib().c3_session_pointers(self.h, virtual_rank, C.byref(p)))
+        return p
+
+    def fill(self, seed=20241217):
+        check(lib().c3_session_fill(self.h, seed))
+
+    def export_handles(self):
+        buf = C.create_string_buffer(_capi.SESSION_HANDLE_BYTES)
+        check(lib().c3_session_export(self.h, buf))
+        return buf.raw
+
+    def import_handles(self, blobs):
+        joined = b"".join(blobs)
+        check(lib().c3_session_import(self.h, C.create_string_buffer(joined, len(joined))))
+
+    def default_alloc(self, strategy):
+        a = _capi.Alloc()
+        check(lib().c3_session_default_alloc(self.h, strategy, C.byref(a)))
+        return a
+
+    def run(self, strategy, alloc=None, all_ranks=False):
+        t = _capi.Timing()
+        fn = lib().c3_session_run_all_ranks if all_ranks else lib().c3_session_run
+        check(fn(self.h, strategy, C.byref(alloc) if alloc is not None else None, C.byref(t)))
+        return t

@@ -1,0 +1,104 @@
+// Internal declarations shared by the CUDA translation units and the host
+// runtime of libc3cuda.so. Nothing here crosses the C ABI.
+#pragma once
+
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdint>
+#include <string>
+
+#include "c3cuda.h"
+
+namespace c3k {
+
+// ------------------------------------------------------- driver entry points
+// Resolved lazily via cudaGetDriverEntryPoint (driver.cpp); nullptr when the
+// driver lacks the symbol. No link-time libcuda dependency.
+struct Driver {
+    PFN_cuGetErrorName_v6000 GetErrorName;
+    PFN_cuInit_v2000 Init;
+    PFN_cuDeviceGet_v2000 DeviceGet;
+    PFN_cuDeviceGetDevResource_v12040 DeviceGetDevResource;
+    PFN_cuDevSmResourceSplitByCount_v12040 DevSmResourceSplitByCount;
+    PFN_cuDevResourceGenerateDesc_v12040 DevResourceGenerateDesc;
+    PFN_cuGreenCtxCreate_v12040 GreenCtxCreate;
+    PFN_cuGreenCtxDestroy_v12040 GreenCtxDestroy;
+    PFN_cuGreenCtxStreamCreate_v12050 GreenCtxStreamCreate;
+    PFN_cuStreamDestroy_v4000 StreamDestroy;
+    PFN_cuStreamWriteValue32_v11070 StreamWriteValue32;
+    PFN_cuStreamWaitValue32_v11070 StreamWaitValue32;
+    PFN_cuTensorMapEncodeTiled_v12000 TensorMapEncodeTiled;
+};
+const Driver& drv();
+
+// ----------------------------------------------------------------- errors
+int set_error(int code, const std::string& msg);
+const char* last_error_cstr();
+int set_cuda_error(cudaError_t e, const char* what);
+int set_driver_error(CUresult r, const char* what);
+
+#define C3_TRY(expr)                   \
+    do {                               \
+        const int _rc = (expr);        \
+        if (_rc != C3_OK) return _rc;  \
+    } while (0)
+#define C3_CUDA(expr)                                                   \
+    do {                                                                \
+        const cudaError_t _e = (expr);                                  \
+        if (_e != cudaSuccess) return ::c3k::set_cuda_error(_e, #expr); \
+    } while (0)
+// Calls drv().fn(args...), failing cleanly when the entry point is missing.
+#define C3_CU(fn, ...)                                                                  \
+    do {                                                                                \
+        if (!::c3k::drv().fn)                                                           \
+            return ::c3k::set_error(C3_ERR_UNSUPPORTED, "driver entry point cu" #fn " missing"); \
+        const CUresult _r = ::c3k::drv().fn(__VA_ARGS__);                               \
+        if (_r != CUDA_SUCCESS) return ::c3k::set_driver_error(_r, "cu" #fn);           \
+    } while (0)
+
+// ------------------------------------------------------------------- GEMM
+struct GemmPlan {
+    CUtensorMap map_a;
+    CUtensorMap map_b;
+    void* c = nullptr;
+    int64_t m = 0, n = 0, k = 0;
+    int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;
+};
+int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
+                   int64_t k);
+int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream);
+
+// ------------------------------------------------------------ collectives
+// Cross-process completion signalling for the SM-driven collectives.
+// `mine` is this rank's flag array (C3_MAX_RANKS x 2 words: [entry, exit]
+// per source rank), `peers[p]` rank p's array (peer-mapped). `done` is a
+// device counter (one per launch site) used to elect the last CTA.
+struct Signals {
+    uint32_t* mine = nullptr;
+    uint32_t* peers[C3_MAX_RANKS] = {};
+    uint32_t* done = nullptr;
+    uint32_t epoch = 0;
+    bool enabled = false;
+};
+
+struct PtrTable {
+    const void* p[C3_MAX_RANKS];
+};
+struct MutPtrTable {
+    void* p[C3_MAX_RANKS];
+};
+
+int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
+                          int64_t chunk_bytes, int n_ctas, const Signals& sig,
+                          cudaStream_t stream);
+int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
+                               int n_ctas, const Signals& sig, cudaStream_t stream);
+int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor,
+                     cudaStream_t stream);
+int launch_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor,
+                       cudaStream_t stream);
+
+}  // namespace c3k

@@ -1,0 +1,300 @@
+// SM-driven direct collectives over NVSwitch peer memory (the paper's "CU
+// backend", executed instead of modeled) and the synthetic-input generators.
+//
+//  * all-gather, push form: rank `self` loads each 16-byte vector of its chunk
+//    once and stores it into slot `self` of every rank's receive buffer — the
+//    same (src, dst, offset) mapping as the reference's plan_all_gather
+//    (/root/reference/proj/src/conccl.cpp:35-51), one step, no ring (every
+//    peer is one NVSwitch hop away).
+//  * reduce-scatter, pull form (extension): rank `self`
+//    reads slot `self` of every rank's input, sums in fp32 in rank order
+//    0..n-1 and rounds once to bf16 — bit-identical to the oracle
+//    (oracle/c3oracle.c c3o_reduce_scatter_bf16). The same kernel, fed with
+//    local staging slots, is the copy-engine path's local reduce.
+//
+// Multi-process completion uses per-rank flag words written with
+// st.release.sys into peers' signal arrays (monotonic epochs; no reset).
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "c3cuda_internal.hpp"
+#include "ptx.cuh"
+
+namespace c3k {
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kUnroll = 4;
+
+// Last-CTA election + cross-rank exit barrier. Called by every thread of every
+// CTA after its stores; returns after this rank has seen `epoch` from all peers
+// (only the elected CTA waits; the other CTAs exit).
+__device__ void exit_barrier(const Signals& sig, int self, int n, int slot_base) {
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    fence_sys();
+    const uint32_t ticket = atomicAdd(sig.done, 1u);
+    if (ticket != gridDim.x - 1) return;
+    fence_sys();
+    for (int p = 0; p < n; ++p)
+        if (p != self) st_release_sys(sig.peers[p] + slot_base + self, sig.epoch);
+    for (int p = 0; p < n; ++p)
+        if (p != self)
+            while (ld_acquire_sys(sig.mine + slot_base + p) < sig.epoch) {
+            }
+    *sig.done = 0;  // next launch on this stream starts from zero
+}
+
+// Entry barrier: every peer has reached this collective (its inputs are ready).
+__device__ void entry_barrier(const Signals& sig, int self, int n, int slot_base) {
+    if (threadIdx.x == 0) {
+        if (blockIdx.x == 0) {
+            fence_sys();
+            for (int p = 0; p < n; ++p)
+                if (p != self) st_release_sys(sig.peers[p] + slot_base + self, sig.epoch);
+        }
+        for (int p = 0; p < n; ++p)
+            if (p != self)
+                while (ld_acquire_sys(sig.mine + slot_base + p) < sig.epoch) {
+                }
+    }
+    __syncthreads();
+}
+
+// Signal-array layout (words): [0,8) all-gather exit, [8,16) reduce-scatter
+// entry, [16,24) reduce-scatter exit, [24,32) copy-engine exit.
+constexpr int kAgExit = 0, kRsEntry = 8, kRsExit = 16;
+
+__global__ void __launch_bounds__(kThreads)
+ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, int n,
+                   int64_t nvec, int64_t slot_vec, int copy_self, Signals sig) {
+    uint4* dst[C3_MAX_RANKS];
+#pragma unroll
+    for (int j = 0; j < C3_MAX_RANKS; ++j)
+        dst[j] = j < n ? static_cast<uint4*>(recv.p[j]) + slot_vec * self : nullptr;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
+         base < nvec; base += step) {
+        uint4 v[kUnroll];
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+            const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+            if (i < nvec) v[u] = ld_nc_v4(src + i);
+        }
+        // peers in rotated order so the ranks do not all start on the same target
+        for (int j = 1; j <= n; ++j) {
+            const int p = (self + j) % n;
+            if (p == self && !copy_self) continue;
+            uint4* d = dst[p];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+                if (i < nvec) st_v4(d + i, v[u]);
+            }
+        }
+    }
+    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+}
+
+// Byte-granular fallback shape for chunks that are not 16-byte multiples or
+// 16-byte aligned (tiny parity cases only; large runs always take the vector path).
+__global__ void __launch_bounds__(kThreads)
+ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self, int n,
+                    int64_t chunk, int copy_self, Signals sig) {
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < chunk; i += step) {
+        const uint8_t v = src[i];
+        for (int p = 0; p < n; ++p) {
+            if (p == self && !copy_self) continue;
+            static_cast<uint8_t*>(recv.p[p])[chunk * self + i] = v;
+        }
+    }
+    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+}
+
+__device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& v) {
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float2 f = __bfloat1622float2(h[j]);
+        acc[2 * j] = __fadd_rn(acc[2 * j], f.x);
+        acc[2 * j + 1] = __fadd_rn(acc[2 * j + 1], f.y);
+    }
+}
+
+template <int N>
+__global__ void __launch_bounds__(kThreads)
+rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
+                   int64_t slot_vec, Signals sig) {
+    if (sig.enabled) entry_barrier(sig, self, N, kRsEntry);
+    const uint4* src[N];
+#pragma unroll
+    for (int g = 0; g < N; ++g) src[g] = static_cast<const uint4*>(in.p[g]) + slot_vec * self;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * 2;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * 2 + threadIdx.x; base < nvec;
+         base += step) {
+        uint4 v[2][N];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+            if (i < nvec)
+#pragma unroll
+                for (int g = 0; g < N; ++g) v[u][g] = ld_v4(src[g] + i);
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+            if (i >= nvec) continue;
+            float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+            for (int g = 0; g < N; ++g) acc_bf16x8(acc, v[u][g]);  // rank order 0..N-1
+            uint4 o;
+            __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
+            st_v4(out + i, o);
+        }
+    }
+    if (sig.enabled) exit_barrier(sig, self, N, kRsExit);
+}
+
+__global__ void __launch_bounds__(kThreads)
+rs_pull_scalar_kernel(PtrTable in, __nv_bfloat16* __restrict__ out, int self, int n, int64_t count,
+                      Signals sig) {
+    if (sig.enabled) entry_barrier(sig, self, n, kRsEntry);
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < count; i += step) {
+        float acc = 0.f;
+        for (int g = 0; g < n; ++g)
+            acc = __fadd_rn(acc, __bfloat162float(static_cast<const __nv_bfloat16*>(in.p[g])[count * self + i]));
+        out[i] = __float2bfloat16_rn(acc);
+    }
+    if (sig.enabled) exit_barrier(sig, self, n, kRsExit);
+}
+
+// ------------------------------------------------------ synthetic inputs ---
+
+__device__ __forceinline__ uint64_t hash64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+__device__ __forceinline__ uint64_t label_word(uint64_t key, uint64_t w) { return hash64(key ^ w); }
+
+__global__ void fill_bf16_kernel(__nv_bfloat16* dst, int64_t count, uint64_t key) {
+    const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += step) {
+        const uint64_t h = label_word(key, static_cast<uint64_t>(i));
+        const int32_t r24 = static_cast<int32_t>(h >> 40);
+        const float u = static_cast<float>(r24 - (1 << 23)) * (1.0f / 8388608.0f);
+        dst[i] = __float2bfloat16_rn(u * 0.125f);
+    }
+}
+
+__global__ void fill_labels_kernel(uint8_t* dst, int64_t bytes, uint64_t key) {
+    const int64_t words = bytes / 8;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
+    const bool aligned = (reinterpret_cast<uintptr_t>(dst) & 7) == 0;
+    for (int64_t w = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; w <= words; w += step) {
+        const uint64_t v = label_word(key, static_cast<uint64_t>(w));
+        const int64_t at = w * 8;
+        const int64_t nbytes = w < words ? 8 : bytes - at;
+        if (nbytes == 8 && aligned) {
+            *reinterpret_cast<uint64_t*>(dst + at) = v;
+        } else {
+            for (int64_t b = 0; b < nbytes; ++b) dst[at + b] = static_cast<uint8_t>(v >> (8 * b));
+        }
+    }
+}
+
+uint64_t label_key(uint64_t seed, int rank, int tensor) {
+    return seed ^ (static_cast<uint64_t>(static_cast<uint32_t>(rank)) << 56) ^
+           (static_cast<uint64_t>(static_cast<uint32_t>(tensor)) << 48);
+}
+
+int grid_for(int64_t work_items, int threads, int cap) {
+    const int64_t g = (work_items + threads - 1) / threads;
+    return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, cap)));
+}
+
+}  // namespace
+
+int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
+                          int64_t chunk_bytes, int n_ctas, const Signals& sig,
+                          cudaStream_t stream) {
+    if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
+        return set_error(C3_ERR_VALIDATION, "allgather: bad rank/world");
+    if (chunk_bytes < 0) return set_error(C3_ERR_VALIDATION, "allgather: negative chunk");
+    if (n_ctas < 1) return set_error(C3_ERR_VALIDATION, "allgather: n_ctas must be >= 1");
+    // send may alias slot `self` of recv[self] (in-place): then skip the self copy
+    const bool in_place = send == static_cast<const uint8_t*>(recv.p[self]) + chunk_bytes * self;
+    uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(chunk_bytes);
+    for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
+    if (chunk_bytes == 0 && !sig.enabled) return C3_OK;
+    if ((align & 15) == 0) {
+        const int64_t nvec = chunk_bytes / 16;
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
+        ag_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
+                                                         n, nvec, nvec, in_place ? 0 : 1, sig);
+    } else {
+        const int grid = grid_for(std::max<int64_t>(chunk_bytes, 1), kThreads, n_ctas);
+        ag_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
+                                                          self, n, chunk_bytes, in_place ? 0 : 1, sig);
+    }
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
+                               int n_ctas, const Signals& sig, cudaStream_t stream) {
+    if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
+        return set_error(C3_ERR_VALIDATION, "reduce_scatter: bad rank/world");
+    if (count < 0) return set_error(C3_ERR_VALIDATION, "reduce_scatter: negative count");
+    if (n_ctas < 1) return set_error(C3_ERR_VALIDATION, "reduce_scatter: n_ctas must be >= 1");
+    if (count == 0 && !sig.enabled) return C3_OK;
+    uintptr_t align = reinterpret_cast<uintptr_t>(out) | static_cast<uintptr_t>(count * 2);
+    for (int g = 0; g < n; ++g) align |= reinterpret_cast<uintptr_t>(in.p[g]);
+    if ((align & 15) == 0) {
+        const int64_t nvec = count / 8;
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * 2, n_ctas);
+        uint4* o = static_cast<uint4*>(out);
+        switch (n) {
+#define C3_RS_CASE(N)                                                                          \
+    case N:                                                                                    \
+        rs_pull_vec_kernel<N><<<grid, kThreads, 0, stream>>>(in, o, self, nvec, nvec, sig);    \
+        break;
+            C3_RS_CASE(1) C3_RS_CASE(2) C3_RS_CASE(3) C3_RS_CASE(4)
+            C3_RS_CASE(5) C3_RS_CASE(6) C3_RS_CASE(7) C3_RS_CASE(8)
+#undef C3_RS_CASE
+        }
+    } else {
+        const int grid = grid_for(std::max<int64_t>(count, 1), kThreads, n_ctas);
+        rs_pull_scalar_kernel<<<grid, kThreads, 0, stream>>>(in, static_cast<__nv_bfloat16*>(out),
+                                                             self, n, count, sig);
+    }
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor,
+                     cudaStream_t stream) {
+    if (count <= 0) return C3_OK;
+    fill_bf16_kernel<<<grid_for(count, 256, 148 * 16), 256, 0, stream>>>(
+        static_cast<__nv_bfloat16*>(dst), count, label_key(seed, rank, tensor));
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor,
+                       cudaStream_t stream) {
+    if (bytes <= 0) return C3_OK;
+    fill_labels_kernel<<<grid_for(bytes / 8 + 1, 256, 148 * 16), 256, 0, stream>>>(
+        static_cast<uint8_t*>(dst), bytes, label_key(seed, rank, tensor));
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+}  // namespace c3k

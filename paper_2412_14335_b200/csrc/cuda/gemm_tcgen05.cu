@@ -1,0 +1,288 @@
+// Persistent bf16 GEMM for sm_100a: TMA -> shared memory (4-stage mbarrier
+// ring) -> tcgen05.mma (single-thread issue, fp32 accumulators in TMEM,
+// double-buffered) -> tcgen05.ld epilogue -> bf16 global stores.
+//
+//   C[M,N] = A[M,K] * B[N,K]^T      (A, B K-major bf16; C row-major bf16)
+//
+// This is the "compute" half of a C3 pair (reference GemmKernel,
+// /root/reference/proj/include/c3sim/workload.hpp:18-25; its cost model
+// roofline_gemm_time, src/workload.cpp:72-78). The grid is capped at
+// `max_ctas` CTAs (one per SM, persistent over output tiles): the B200
+// counterpart of the paper's CU allocation to the GEMM (allocate_cus
+// cus_gemm, src/sim.cpp:40-100) and of ConCCL_rp's idle grain
+// (src/strategy.cpp:96-113).
+//
+// Warp roles (256 threads): warp 0 = TMA producer (one thread), warp 1 = MMA
+// issuer (one thread), warp 2 = TMEM allocator, warps 4..7 = epilogue (warp
+// 4+q reads TMEM lanes 32q..32q+31, i.e. output rows 32q.. of the tile).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "c3cuda_internal.hpp"
+#include "ptx.cuh"
+
+namespace c3k {
+
+namespace gemm {
+
+constexpr int BM = 128;          // UMMA M (one CTA)
+constexpr int BN = 256;          // UMMA N
+constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
+constexpr int UK = 16;           // UMMA K for 16-bit inputs
+constexpr int STAGES = 4;
+constexpr int ACC_BUFS = 2;
+constexpr uint32_t TMEM_COLS = 512;  // ACC_BUFS x BN fp32 columns
+constexpr int THREADS = 256;
+constexpr int GROUP_M = 16;      // tile raster: 16 M-tiles per band for L2 reuse
+
+constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
+constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
+constexpr uint32_t STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
+constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+struct Params {
+    int m, n, k;
+    int tiles_m, tiles_n, num_tiles, k_blocks;
+    __nv_bfloat16* c;
+    int ldc;
+};
+
+__device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
+    const int band = GROUP_M * p.tiles_n;
+    const int first_m = (tile / band) * GROUP_M;
+    const int rows = min(p.tiles_m - first_m, GROUP_M);
+    const int in_band = tile % band;
+    tm = first_m + in_band % rows;
+    tn = in_band / rows;
+}
+
+__global__ void __launch_bounds__(THREADS, 1)
+gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
+                    const __grid_constant__ CUtensorMap map_b, const Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1024-byte alignment for the 128B-swizzle atoms.
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+    uint64_t* full = bars;                       // [STAGES]  TMA -> MMA
+    uint64_t* empty = bars + STAGES;             // [STAGES]  MMA -> TMA
+    uint64_t* acc_full = bars + 2 * STAGES;      // [ACC_BUFS] MMA -> epilogue
+    uint64_t* acc_empty = acc_full + ACC_BUFS;   // [ACC_BUFS] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + ACC_BUFS);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_a);
+        tma_prefetch_desc(&map_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < ACC_BUFS; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 128);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ---------------- TMA producer ----------------
+        const uint64_t keep = policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            int tm, tn;
+            tile_coords(p, tile, tm, tn);
+            for (int kb = 0; kb < p.k_blocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
+                tma_load_2d(smem_a + stage * A_STAGE_BYTES, &map_a, &full[stage], kb * BK, tm * BM, keep);
+                tma_load_2d(smem_b + stage * B_STAGE_BYTES, &map_b, &full[stage], kb * BK, tn * BN, keep);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+        }
+    } else if (warp == 1 && lane == 0) {
+        // ---------------- MMA issuer ----------------
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+        const uint32_t a0 = smem_u32(smem_a), b0 = smem_u32(smem_b);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+            for (int kb = 0; kb < p.k_blocks; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t a_addr = a0 + stage * A_STAGE_BYTES;
+                const uint32_t b_addr = b0 + stage * B_STAGE_BYTES;
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k) {
+                    // advancing K inside the 128-byte swizzle atom = +32 B per UMMA_K
+                    umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * UK * 2),
+                              smem_desc_k_sw128(b_addr + k * UK * 2), idesc, (kb | k) != 0);
+                }
+                umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            umma_commit(&acc_full[acc]);  // accumulator tile complete
+            if (++acc == ACC_BUFS) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ---------------- epilogue: TMEM -> registers -> bf16 -> global ----------------
+        const int q = warp - 4;                 // TMEM lane quarter
+        const int row_in_tile = q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+            int tm, tn;
+            tile_coords(p, tile, tm, tn);
+            mbar_wait(&acc_full[acc], acc_phase);
+            tc_fence_after();
+            const int row = tm * BM + row_in_tile;
+            const bool row_ok = row < p.m;
+            __nv_bfloat16* crow = p.c + static_cast<size_t>(row) * p.ldc;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(t_row + c, v);
+                tmem_ld_wait();
+                const int col = tn * BN + c;
+                if (row_ok) {
+                    if (col + 32 <= p.n) {
+                        uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            uint4 o;
+                            __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                            __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                            __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                            __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                            o.x = *reinterpret_cast<uint32_t*>(&h0);
+                            o.y = *reinterpret_cast<uint32_t*>(&h1);
+                            o.z = *reinterpret_cast<uint32_t*>(&h2);
+                            o.w = *reinterpret_cast<uint32_t*>(&h3);
+                            dst[j] = o;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[acc]);
+            if (++acc == ACC_BUFS) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc<TMEM_COLS>(tmem_base);
+    }
+}
+
+}  // namespace gemm
+
+// ----------------------------------------------------------------- host ---
+
+namespace {
+
+CUresult encode_kmajor_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t k,
+                            uint32_t box_rows) {
+    const cuuint64_t dims[2] = {k, rows};
+    const cuuint64_t strides[1] = {k * 2};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(gemm::BK), box_rows};
+    const cuuint32_t estr[2] = {1, 1};
+    if (!drv().TensorMapEncodeTiled) return CUDA_ERROR_NOT_SUPPORTED;
+    return drv().TensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
+                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+}
+
+}  // namespace
+
+int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
+                   int64_t k) {
+    if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
+    if (k % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: K must be a multiple of 8 (16-byte rows)");
+    if (n % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: N must be a multiple of 8 (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+        return set_error(C3_ERR_VALIDATION, "gemm: operands must be 16-byte aligned");
+    if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return set_error(C3_ERR_VALIDATION, "gemm: dimension too large");
+    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), gemm::BM);
+    if (r == CUDA_SUCCESS)
+        r = encode_kmajor_bf16(&plan->map_b, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), gemm::BN);
+    if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
+    plan->m = m;
+    plan->n = n;
+    plan->k = k;
+    plan->c = C;
+    plan->tiles_m = static_cast<int>((m + gemm::BM - 1) / gemm::BM);
+    plan->tiles_n = static_cast<int>((n + gemm::BN - 1) / gemm::BN);
+    plan->num_tiles = plan->tiles_m * plan->tiles_n;
+    plan->k_blocks = static_cast<int>((k + gemm::BK - 1) / gemm::BK);
+    return C3_OK;
+}
+
+int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel,
+                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             static_cast<int>(gemm::SMEM_BYTES));
+        if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
+        attr_done = true;
+    }
+    int grid = max_ctas > 0 ? max_ctas : sm_count;
+    grid = std::min(grid, sm_count);
+    grid = std::min(grid, plan->num_tiles);
+    gemm::Params p;
+    p.m = static_cast<int>(plan->m);
+    p.n = static_cast<int>(plan->n);
+    p.k = static_cast<int>(plan->k);
+    p.tiles_m = plan->tiles_m;
+    p.tiles_n = plan->tiles_n;
+    p.num_tiles = plan->num_tiles;
+    p.k_blocks = plan->k_blocks;
+    p.c = static_cast<__nv_bfloat16*>(plan->c);
+    p.ldc = static_cast<int>(plan->n);
+    gemm::gemm_bf16_tn_kernel<<<grid, gemm::THREADS, gemm::SMEM_BYTES, stream>>>(plan->map_a,
+                                                                                 plan->map_b, p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
+    return C3_OK;
+}
+
+}  // namespace c3k

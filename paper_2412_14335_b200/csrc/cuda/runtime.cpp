@@ -1,0 +1,934 @@
+// libc3cuda host runtime: error state, worlds (one device; real or loopback
+// ranks), CUDA-IPC peer mapping, the copy-engine plan executor, and the C3
+// session that executes one scenario under the paper's strategies.
+//
+// Strategy semantics are the reference's allocate_cus
+// (/root/reference/proj/src/sim.cpp:40-100), turned into launch mechanics:
+//   serial     GEMM then collective, back to back on one stream
+//   c3_base    GEMM launched first (every SM), SM collective second with the
+//              one grain the model leaves it, default priorities
+//   c3_sp      SM collective launched first on the highest-priority stream
+//              with its saturation CTAs; GEMM capped at cus_gemm CTAs
+//   c3_rp      SM partition: green contexts (cuGreenCtx*) split the GPU into a
+//              comm group of cus_comm SMs and a GEMM group (falls back to CTA
+//              caps, reported in c3_timing.partition, if green contexts fail)
+//   c3_sp_rp   c3_rp with the collective first on a high-priority stream
+//   conccl     copy-engine collective (each TransferPlan transfer becomes a
+//              cudaMemcpyAsync on the stream of its engine) + GEMM on all SMs
+//   conccl_rp  copy-engine collective + GEMM capped at cus_gemm (one grain
+//              idle for memory-bound GEMMs; conccl_rp_plan, strategy.cpp:96-113)
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cstring>
+#include <map>
+#include <string>
+#include <vector>
+
+#include "c3cuda_internal.hpp"
+#include "c3sim/conccl.hpp"
+#include "c3sim/errors.hpp"
+#include "c3sim/sim.hpp"
+
+namespace c3k {
+
+namespace {
+thread_local std::string g_last_error;
+}
+
+const char* last_error_cstr() { return g_last_error.c_str(); }
+
+int set_error(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+int set_cuda_error(cudaError_t e, const char* what) {
+    return set_error(C3_ERR_CUDA, std::string(what) + ": " + cudaGetErrorName(e) + " (" +
+                                      cudaGetErrorString(e) + ")");
+}
+int set_driver_error(CUresult r, const char* what) {
+    const char* name = nullptr;
+    if (drv().GetErrorName) drv().GetErrorName(r, &name);
+    return set_error(C3_ERR_DRIVER,
+                     std::string(what) + ": " + (name ? name : std::to_string(static_cast<int>(r))));
+}
+
+// Runs a model-layer call, mapping c3sim exceptions to status codes.
+template <class F>
+int guarded(F&& f) {
+    try {
+        return f();
+    } catch (const c3sim::IoError& e) {
+        return set_error(C3_ERR_IO, e.what());
+    } catch (const c3sim::UnknownEntityError& e) {
+        return set_error(C3_ERR_UNKNOWN, e.what());
+    } catch (const c3sim::FitError& e) {
+        return set_error(C3_ERR_FIT, e.what());
+    } catch (const c3sim::Error& e) {
+        return set_error(C3_ERR_VALIDATION, e.what());
+    } catch (const std::exception& e) {
+        return set_error(C3_ERR_VALIDATION, e.what());
+    }
+}
+
+}  // namespace c3k
+
+using namespace c3k;
+
+// ------------------------------------------------------------------ world
+
+struct GreenPartition {
+    int comm_sms = 0, gemm_sms = 0;
+    CUgreenCtx comm_ctx = nullptr, gemm_ctx = nullptr;
+    CUstream comm_stream = nullptr, gemm_stream = nullptr;
+};
+
+struct c3_world {
+    int rank = 0, n_ranks = 1, device = 0, loopback = 0;
+    cudaDeviceProp prop{};
+    int prio_lo = 0, prio_hi = 0;
+    int green_ok = 0, green_grain = 0;
+    CUdevice cu_dev = 0;
+    std::vector<cudaStream_t> ce_streams;  // one per copy-engine index
+    std::vector<cudaEvent_t> ce_events;
+    cudaEvent_t fork_event = nullptr;
+    std::map<int, GreenPartition> partitions;  // keyed by requested comm SMs
+};
+
+namespace {
+
+int probe_green(c3_world* w) {
+    // The SM split granularity on sm_100 is not documented in the 12.9
+    // headers: ask for a 1-SM group and read back what the driver grants.
+    CUdevResource all{};
+    const Driver& d = drv();
+    if (!d.DeviceGetDevResource || !d.DevSmResourceSplitByCount || !d.GreenCtxCreate ||
+        !d.GreenCtxStreamCreate || !d.DevResourceGenerateDesc)
+        return 0;
+    if (d.DeviceGetDevResource(w->cu_dev, &all, CU_DEV_RESOURCE_TYPE_SM) != CUDA_SUCCESS) return 0;
+    CUdevResource grp[1] = {};
+    CUdevResource rest{};
+    unsigned int nb = 1;
+    if (d.DevSmResourceSplitByCount(grp, &nb, &all, &rest, 0, 1) != CUDA_SUCCESS || nb < 1) return 0;
+    w->green_grain = static_cast<int>(grp[0].sm.smCount);
+    return 1;
+}
+
+int ce_stream(c3_world* w, int engine, std::size_t* idx_out) {
+    const int n_eng = std::max(1, w->prop.asyncEngineCount);
+    const std::size_t idx = static_cast<std::size_t>(engine % n_eng);
+    while (w->ce_streams.size() <= idx) {
+        cudaStream_t s;
+        cudaEvent_t e;
+        C3_CUDA(cudaStreamCreateWithPriority(&s, cudaStreamNonBlocking, w->prio_hi));
+        C3_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        w->ce_streams.push_back(s);
+        w->ce_events.push_back(e);
+    }
+    *idx_out = idx;
+    return C3_OK;
+}
+
+int green_partition(c3_world* w, int comm_sms, GreenPartition** out) {
+    auto it = w->partitions.find(comm_sms);
+    if (it != w->partitions.end()) {
+        *out = &it->second;
+        return C3_OK;
+    }
+    if (!w->green_ok) return set_error(C3_ERR_UNSUPPORTED, "green contexts unavailable on this device");
+    CUdevResource all{};
+    C3_CU(DeviceGetDevResource, w->cu_dev, &all, CU_DEV_RESOURCE_TYPE_SM);
+    CUdevResource comm[1] = {};
+    CUdevResource rest{};
+    unsigned int nb = 1;
+    C3_CU(DevSmResourceSplitByCount, comm, &nb, &all, &rest, 0, static_cast<unsigned>(comm_sms));
+    if (nb < 1) return set_error(C3_ERR_UNSUPPORTED, "green context split produced no group");
+    GreenPartition gp;
+    gp.comm_sms = static_cast<int>(comm[0].sm.smCount);
+    gp.gemm_sms = static_cast<int>(rest.sm.smCount);
+    CUdevResourceDesc dc, dg;
+    C3_CU(DevResourceGenerateDesc, &dc, comm, 1);
+    C3_CU(DevResourceGenerateDesc, &dg, &rest, 1);
+    C3_CU(GreenCtxCreate, &gp.comm_ctx, dc, w->cu_dev, CU_GREEN_CTX_DEFAULT_STREAM);
+    C3_CU(GreenCtxCreate, &gp.gemm_ctx, dg, w->cu_dev, CU_GREEN_CTX_DEFAULT_STREAM);
+    C3_CU(GreenCtxStreamCreate, &gp.comm_stream, gp.comm_ctx, CU_STREAM_NON_BLOCKING, w->prio_hi);
+    C3_CU(GreenCtxStreamCreate, &gp.gemm_stream, gp.gemm_ctx, CU_STREAM_NON_BLOCKING, 0);
+    *out = &w->partitions.emplace(comm_sms, gp).first->second;
+    return C3_OK;
+}
+
+// Copy-engine executor: fork from `parent`, one cudaMemcpyAsync per selected
+// transfer on its engine's stream, join back into `parent`.
+int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, void* const* dst,
+           int src_filter, cudaStream_t parent) {
+    if (!w->fork_event) C3_CUDA(cudaEventCreateWithFlags(&w->fork_event, cudaEventDisableTiming));
+    std::vector<char> used;
+    bool forked = false;
+    for (int i = 0; i < nt; ++i) {
+        const c3_transfer& x = t[i];
+        if (src_filter >= 0 && x.src_gpu != src_filter) continue;
+        if (x.length <= 0) continue;
+        std::size_t idx = 0;
+        C3_TRY(ce_stream(w, x.engine_id, &idx));
+        if (!forked) {
+            C3_CUDA(cudaEventRecord(w->fork_event, parent));
+            forked = true;
+        }
+        if (used.size() <= idx) used.resize(idx + 1, 0);
+        if (!used[idx]) {
+            C3_CUDA(cudaStreamWaitEvent(w->ce_streams[idx], w->fork_event, 0));
+            used[idx] = 1;
+        }
+        C3_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst[x.dst_gpu]) + x.dst_offset,
+                                static_cast<const uint8_t*>(src[x.src_gpu]) + x.src_offset,
+                                static_cast<size_t>(x.length), cudaMemcpyDeviceToDevice,
+                                w->ce_streams[idx]));
+    }
+    for (std::size_t idx = 0; idx < used.size(); ++idx) {
+        if (!used[idx]) continue;
+        C3_CUDA(cudaEventRecord(w->ce_events[idx], w->ce_streams[idx]));
+        C3_CUDA(cudaStreamWaitEvent(parent, w->ce_events[idx], 0));
+    }
+    return C3_OK;
+}
+
+// B200 machine descriptor for a world of `n` ranks, from the live device.
+// Peaks are the driver-measured MEASURED_PEAKS.json figures of this pool.
+c3sim::MachineDescriptor b200_machine(const c3_world* w, int n) {
+    c3sim::MachineDescriptor md;
+    md.gpus_per_node = n;
+    md.cus_per_gpu = w->prop.multiProcessorCount;
+    md.xcds_per_gpu = md.cus_per_gpu % 2 == 0 ? 2 : 1;
+    md.cus_per_xcd = md.cus_per_gpu / md.xcds_per_gpu;
+    md.min_cu_grain = md.cus_per_gpu % 4 == 0 ? 4 : (md.cus_per_gpu % 2 == 0 ? 2 : 1);
+    md.dma_engines_per_gpu = std::max(1, w->prop.asyncEngineCount);
+    md.peak_compute_flops = 1.6097e15;
+    md.hbm_bandwidth = 6.5383e12;
+    md.llc_capacity = w->prop.l2CacheSize;
+    md.link_bandwidth_unidir = n > 1 ? 900e9 / (n - 1) : 900e9;
+    md.links_per_gpu = n - 1;
+    md.cpu_launch_overhead = 2e-6;
+    md.dma_sync_overhead = 1e-5;
+    c3sim::validate(md);
+    return md;
+}
+
+// Placeholder interference tables until measured B200 tables are loaded:
+// GEMMs scale with SMs (compute-bound: C/c; memory-bound saturating at C/2),
+// collectives use the reference's bandwidth-proportional default.
+c3sim::SlowdownTableSet default_tables(const c3sim::MachineDescriptor& md) {
+    c3sim::SlowdownTableSet t;
+    const int C = md.cus_per_gpu, g = md.min_cu_grain;
+    auto& cb = t.at(c3sim::KernelClass::GemmComputeBound);
+    auto& mb = t.at(c3sim::KernelClass::GemmMemoryBound);
+    cb.kernel_class = c3sim::KernelClass::GemmComputeBound;
+    mb.kernel_class = c3sim::KernelClass::GemmMemoryBound;
+    for (int c = g; c < C; c += g) {
+        cb.points.push_back({c, static_cast<double>(C) / c});
+        mb.points.push_back({c, std::max(1.0, 0.5 * C / c)});
+    }
+    cb.points.push_back({C, 1.0});
+    mb.points.push_back({C, 1.0});
+    t.at(c3sim::KernelClass::AllGather) = c3sim::default_comm_table(c3sim::CollectiveKind::AllGather, md);
+    t.at(c3sim::KernelClass::AllToAll) = c3sim::default_comm_table(c3sim::CollectiveKind::AllToAll, md);
+    return t;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- session
+
+namespace {
+constexpr int kSigWords = 64;  // signal array: see collectives.cu for the layout
+constexpr int kCeExit = 24, kCeEntry = 32;
+constexpr int kRunAllRanks = 1;
+}  // namespace
+
+struct c3_session {
+    c3_world* w = nullptr;
+    c3_scenario_desc d{};
+    int vr = 1;             // virtual ranks held by this process
+    int n = 1;              // collective ranks
+    int64_t chunk = 0;      // payload / n (bytes)
+    GemmPlan gemm;
+    void *a = nullptr, *b = nullptr, *c = nullptr;
+    // per virtual rank: AG recv (payload, own chunk in place); RS in (payload),
+    // out (chunk), staging (payload)
+    std::vector<void*> recv, in, out, staging;
+    // multi-process peer views, indexed by rank ([rank] = local)
+    void* peer_coll[C3_MAX_RANKS] = {};     // AG recv / RS in
+    void* peer_staging[C3_MAX_RANKS] = {};
+    uint32_t* peer_sig[C3_MAX_RANKS] = {};
+    std::vector<void*> imported;            // to close on destroy
+    uint32_t* sig = nullptr;                // local signal array
+    uint32_t* done = nullptr;               // [0] AG counter, [1] RS counter
+    uint32_t epoch = 0;
+    bool ready = false;                     // peers imported (or loopback)
+    std::vector<c3_transfer> plan;          // validated ConCCL plan
+    cudaStream_t main = nullptr, gemm_s = nullptr, comm_s = nullptr, comm_hi = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
+                ev_ce = nullptr, ev_end = nullptr;
+    c3sim::MachineDescriptor md;
+    c3sim::SlowdownTableSet tables;
+    c3sim::C3Scenario scenario;
+};
+
+namespace {
+
+int session_alloc(c3_session* s) {
+    const c3_scenario_desc& d = s->d;
+    C3_CUDA(cudaMalloc(&s->a, static_cast<size_t>(d.m * d.k * 2)));
+    C3_CUDA(cudaMalloc(&s->b, static_cast<size_t>(d.n * d.k * 2)));
+    C3_CUDA(cudaMalloc(&s->c, static_cast<size_t>(d.m * d.n * 2)));
+    C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k));
+    const size_t payload = static_cast<size_t>(d.payload_bytes);
+    for (int v = 0; v < s->vr; ++v) {
+        void* p = nullptr;
+        if (d.collective == C3_ALL_GATHER) {
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
+            s->recv.push_back(p);
+        } else {
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
+            s->in.push_back(p);
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(static_cast<size_t>(s->chunk), 16)));
+            s->out.push_back(p);
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
+            s->staging.push_back(p);
+        }
+    }
+    C3_CUDA(cudaMalloc(&s->sig, kSigWords * sizeof(uint32_t)));
+    C3_CUDA(cudaMemset(s->sig, 0, kSigWords * sizeof(uint32_t)));
+    C3_CUDA(cudaMalloc(&s->done, 4 * sizeof(uint32_t)));
+    C3_CUDA(cudaMemset(s->done, 0, 4 * sizeof(uint32_t)));
+    C3_CUDA(cudaStreamCreateWithFlags(&s->main, cudaStreamNonBlocking));
+    C3_CUDA(cudaStreamCreateWithPriority(&s->gemm_s, cudaStreamNonBlocking, s->w->prio_lo));
+    C3_CUDA(cudaStreamCreateWithPriority(&s->comm_s, cudaStreamNonBlocking, s->w->prio_lo));
+    C3_CUDA(cudaStreamCreateWithPriority(&s->comm_hi, cudaStreamNonBlocking, s->w->prio_hi));
+    for (cudaEvent_t* e : {&s->ev_start, &s->ev_gs, &s->ev_ge, &s->ev_cs, &s->ev_ce, &s->ev_end})
+        C3_CUDA(cudaEventCreate(e));
+    return C3_OK;
+}
+
+Signals make_signals(c3_session* s, int which) {
+    Signals g;
+    if (s->w->loopback || s->n == 1) return g;
+    g.enabled = true;
+    g.mine = s->sig;
+    for (int p = 0; p < s->n; ++p) g.peers[p] = s->peer_sig[p];
+    g.done = s->done + which;
+    g.epoch = s->epoch;
+    return g;
+}
+
+// Stream-memop barrier (copy-engine path; no SM involvement): tell every
+// peer we reached `slot`, then wait until every peer told us.
+int memop_barrier(c3_session* s, int slot, cudaStream_t st) {
+    for (int p = 0; p < s->n; ++p) {
+        if (p == s->w->rank) continue;
+        C3_CU(StreamWriteValue32, reinterpret_cast<CUstream>(st),
+                                   reinterpret_cast<CUdeviceptr>(s->peer_sig[p] + slot + s->w->rank),
+                                   s->epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+    }
+    for (int p = 0; p < s->n; ++p) {
+        if (p == s->w->rank) continue;
+        C3_CU(StreamWaitValue32, reinterpret_cast<CUstream>(st),
+                                  reinterpret_cast<CUdeviceptr>(s->sig + slot + p), s->epoch,
+                                  CU_STREAM_WAIT_VALUE_GEQ);
+    }
+    return C3_OK;
+}
+
+// Enqueue this rank's share of the collective on `st`. Returns the number of
+// kernels launched via *launches.
+int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaStream_t st,
+                       int* launches) {
+    c3_world* w = s->w;
+    const int n = s->n;
+    const int64_t chunk = s->chunk;
+    const bool loop = w->loopback != 0;
+    const bool all = loop && (flags & kRunAllRanks);
+    const int first = loop ? 0 : w->rank;
+    const int last = loop ? (all ? n - 1 : 0) : w->rank;
+    if (n == 1) return C3_OK;
+    if (s->d.collective == C3_ALL_GATHER) {
+        MutPtrTable recv{};
+        std::vector<const void*> src(static_cast<size_t>(n));
+        std::vector<void*> dst(static_cast<size_t>(n));
+        for (int p = 0; p < n; ++p) {
+            void* base = loop ? s->recv[static_cast<size_t>(p)] : s->peer_coll[p];
+            recv.p[p] = base;
+            dst[static_cast<size_t>(p)] = base;
+            src[static_cast<size_t>(p)] = static_cast<uint8_t*>(base) + chunk * p;
+        }
+        if (backend == C3_BACKEND_CU) {
+            const Signals sig = make_signals(s, 0);
+            for (int v = first; v <= last; ++v) {
+                C3_TRY(launch_allgather_push(v, n, static_cast<uint8_t*>(recv.p[v]) + chunk * v, recv,
+                                             chunk, n_ctas, sig, st));
+                ++*launches;
+            }
+        } else {
+            C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
+                          all ? -1 : first, st));
+            if (!loop) C3_TRY(memop_barrier(s, kCeExit, st));
+        }
+        return C3_OK;
+    }
+    // reduce-scatter
+    const int64_t count = chunk / 2;
+    if (backend == C3_BACKEND_CU) {
+        PtrTable in{};
+        for (int p = 0; p < n; ++p) in.p[p] = loop ? s->in[static_cast<size_t>(p)] : s->peer_coll[p];
+        const Signals sig = make_signals(s, 1);
+        for (int v = first; v <= last; ++v) {
+            void* out = loop ? s->out[static_cast<size_t>(v)] : s->out[0];
+            C3_TRY(launch_reduce_scatter_pull(v, n, in, out, count, n_ctas, sig, st));
+            ++*launches;
+        }
+        return C3_OK;
+    }
+    // copy phase: rank g's slot p -> rank p's staging slot g (plan_reduce_scatter)
+    std::vector<const void*> src(static_cast<size_t>(n));
+    std::vector<void*> dst(static_cast<size_t>(n));
+    for (int p = 0; p < n; ++p) {
+        src[static_cast<size_t>(p)] = loop ? s->in[static_cast<size_t>(p)] : s->peer_coll[p];
+        dst[static_cast<size_t>(p)] = loop ? s->staging[static_cast<size_t>(p)] : s->peer_staging[p];
+    }
+    if (!loop) {
+        src[static_cast<size_t>(w->rank)] = s->in[0];
+        C3_TRY(memop_barrier(s, kCeEntry, st));  // peers done with their staging
+    }
+    C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
+                  all ? -1 : first, st));
+    if (!loop) C3_TRY(memop_barrier(s, kCeExit, st));
+    // local reduce of the n slots (own slot straight from the input)
+    for (int v = first; v <= last; ++v) {
+        PtrTable slots{};
+        const size_t lv = loop ? static_cast<size_t>(v) : 0;
+        for (int g = 0; g < n; ++g)
+            slots.p[g] = g == v ? static_cast<const uint8_t*>(s->in[lv]) + chunk * v
+                                : static_cast<const uint8_t*>(s->staging[lv]) + chunk * g;
+        C3_TRY(launch_reduce_scatter_pull(0, n, slots, s->out[lv], count, std::max(1, n_ctas),
+                                          Signals{}, st));
+        ++*launches;
+    }
+    return C3_OK;
+}
+
+float elapsed(cudaEvent_t a, cudaEvent_t b) {
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* c3_last_error(void) { return last_error_cstr(); }
+int c3_version(void) { return 1; }
+
+int c3_world_create(int rank, int n_ranks, int device, int loopback, c3_world** out) {
+    if (!out) return set_error(C3_ERR_VALIDATION, "c3_world_create: null out");
+    if (n_ranks < 1 || n_ranks > C3_MAX_RANKS)
+        return set_error(C3_ERR_VALIDATION, "c3_world_create: n_ranks must be in [1, 8]");
+    if (rank < 0 || rank >= n_ranks) return set_error(C3_ERR_VALIDATION, "c3_world_create: bad rank");
+    auto* w = new c3_world;
+    w->rank = loopback ? 0 : rank;
+    w->n_ranks = n_ranks;
+    w->device = device;
+    w->loopback = loopback ? 1 : 0;
+    const auto fail = [&](int rc) {
+        delete w;
+        return rc;
+    };
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return fail(set_cuda_error(e, "cudaSetDevice"));
+    e = cudaGetDeviceProperties(&w->prop, device);
+    if (e != cudaSuccess) return fail(set_cuda_error(e, "cudaGetDeviceProperties"));
+    if (w->prop.major != 10)
+        return fail(set_error(C3_ERR_UNSUPPORTED, "libc3cuda is built for sm_100a (B200); device is sm_" +
+                                                      std::to_string(w->prop.major * 10 + w->prop.minor)));
+    cudaDeviceGetStreamPriorityRange(&w->prio_lo, &w->prio_hi);
+    if (!drv().Init || !drv().DeviceGet || drv().Init(0) != CUDA_SUCCESS ||
+        drv().DeviceGet(&w->cu_dev, device) != CUDA_SUCCESS)
+        return fail(set_error(C3_ERR_DRIVER, "cuInit/cuDeviceGet failed"));
+    w->green_ok = probe_green(w);
+    *out = w;
+    return C3_OK;
+}
+
+int c3_world_destroy(c3_world* w) {
+    if (!w) return C3_OK;
+    cudaSetDevice(w->device);
+    for (auto& [k, gp] : w->partitions) {
+        if (gp.comm_stream && drv().StreamDestroy) drv().StreamDestroy(gp.comm_stream);
+        if (gp.gemm_stream && drv().StreamDestroy) drv().StreamDestroy(gp.gemm_stream);
+        if (gp.comm_ctx && drv().GreenCtxDestroy) drv().GreenCtxDestroy(gp.comm_ctx);
+        if (gp.gemm_ctx && drv().GreenCtxDestroy) drv().GreenCtxDestroy(gp.gemm_ctx);
+    }
+    for (auto s : w->ce_streams) cudaStreamDestroy(s);
+    for (auto e : w->ce_events) cudaEventDestroy(e);
+    if (w->fork_event) cudaEventDestroy(w->fork_event);
+    delete w;
+    return C3_OK;
+}
+
+int c3_world_get_info(const c3_world* w, c3_world_info* o) {
+    if (!w || !o) return set_error(C3_ERR_VALIDATION, "c3_world_get_info: null argument");
+    o->rank = w->rank;
+    o->n_ranks = w->n_ranks;
+    o->device = w->device;
+    o->loopback = w->loopback;
+    o->sm_count = w->prop.multiProcessorCount;
+    o->async_engines = w->prop.asyncEngineCount;
+    o->l2_bytes = w->prop.l2CacheSize;
+    o->cc_major = w->prop.major;
+    o->cc_minor = w->prop.minor;
+    o->green_ctx = w->green_ok;
+    o->sm_grain = w->green_grain;
+    o->stream_prio_lo = w->prio_lo;
+    o->stream_prio_hi = w->prio_hi;
+    return C3_OK;
+}
+
+int c3_malloc(c3_world* w, int64_t bytes, void** ptr) {
+    if (!w || !ptr || bytes < 0) return set_error(C3_ERR_VALIDATION, "c3_malloc: bad argument");
+    C3_CUDA(cudaSetDevice(w->device));
+    C3_CUDA(cudaMalloc(ptr, static_cast<size_t>(std::max<int64_t>(bytes, 16))));
+    return C3_OK;
+}
+
+int c3_free(c3_world* w, void* ptr) {
+    if (!w) return set_error(C3_ERR_VALIDATION, "c3_free: null world");
+    C3_CUDA(cudaFree(ptr));
+    return C3_OK;
+}
+
+int c3_memcpy(void* dst, const void* src, int64_t bytes, int kind, void* stream) {
+    if (bytes <= 0) return C3_OK;
+    C3_CUDA(cudaMemcpyAsync(dst, src, static_cast<size_t>(bytes), static_cast<cudaMemcpyKind>(kind),
+                            static_cast<cudaStream_t>(stream)));
+    return C3_OK;
+}
+
+int c3_stream_sync(void* stream) {
+    C3_CUDA(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return C3_OK;
+}
+
+int c3_device_sync(void) {
+    C3_CUDA(cudaDeviceSynchronize());
+    return C3_OK;
+}
+
+int c3_ipc_export(c3_world* w, void* ptr, void* handle_out) {
+    if (!w || !ptr || !handle_out) return set_error(C3_ERR_VALIDATION, "c3_ipc_export: null argument");
+    static_assert(sizeof(cudaIpcMemHandle_t) == C3_IPC_HANDLE_BYTES, "IPC handle size");
+    cudaIpcMemHandle_t h;
+    C3_CUDA(cudaIpcGetMemHandle(&h, ptr));
+    std::memcpy(handle_out, &h, sizeof h);
+    return C3_OK;
+}
+
+int c3_ipc_import(c3_world* w, const void* handle, void** peer_ptr) {
+    if (!w || !handle || !peer_ptr) return set_error(C3_ERR_VALIDATION, "c3_ipc_import: null argument");
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    C3_CUDA(cudaSetDevice(w->device));
+    C3_CUDA(cudaIpcOpenMemHandle(peer_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+    return C3_OK;
+}
+
+int c3_ipc_close(c3_world* w, void* peer_ptr) {
+    if (!w) return set_error(C3_ERR_VALIDATION, "c3_ipc_close: null world");
+    C3_CUDA(cudaIpcCloseMemHandle(peer_ptr));
+    return C3_OK;
+}
+
+int c3_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor, void* stream) {
+    return launch_fill_bf16(dst, count, seed, rank, tensor, static_cast<cudaStream_t>(stream));
+}
+
+int c3_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor, void* stream) {
+    return launch_fill_labels(dst, bytes, seed, rank, tensor, static_cast<cudaStream_t>(stream));
+}
+
+int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
+                 int64_t k, int max_ctas, void* stream) {
+    if (!w) return set_error(C3_ERR_VALIDATION, "c3_gemm_bf16: null world");
+    GemmPlan plan;
+    C3_TRY(gemm_plan_init(&plan, A, B, C, m, n, k));
+    return gemm_plan_launch(&plan, max_ctas, w->prop.multiProcessorCount,
+                            static_cast<cudaStream_t>(stream));
+}
+
+int c3_allgather_p2p(c3_world* w, int self, const void* send, void* const* recv,
+                     int64_t chunk_bytes, int n_ctas, void* stream) {
+    if (!w || !recv) return set_error(C3_ERR_VALIDATION, "c3_allgather_p2p: null argument");
+    MutPtrTable t{};
+    for (int p = 0; p < w->n_ranks; ++p) t.p[p] = recv[p];
+    return launch_allgather_push(self, w->n_ranks, send, t, chunk_bytes, n_ctas, Signals{},
+                                 static_cast<cudaStream_t>(stream));
+}
+
+int c3_reduce_scatter_p2p(c3_world* w, int self, const void* const* in, void* out, int64_t count,
+                          int n_ctas, void* stream) {
+    if (!w || !in) return set_error(C3_ERR_VALIDATION, "c3_reduce_scatter_p2p: null argument");
+    PtrTable t{};
+    for (int p = 0; p < w->n_ranks; ++p) t.p[p] = in[p];
+    return launch_reduce_scatter_pull(self, w->n_ranks, t, out, count, n_ctas, Signals{},
+                                      static_cast<cudaStream_t>(stream));
+}
+
+int c3_reduce_local_bf16(const void* const* slots, int n_slots, void* out, int64_t count, int n_ctas,
+                         void* stream) {
+    if (!slots || n_slots < 1 || n_slots > C3_MAX_RANKS)
+        return set_error(C3_ERR_VALIDATION, "c3_reduce_local_bf16: bad slots");
+    PtrTable t{};
+    for (int g = 0; g < n_slots; ++g) t.p[g] = slots[g];
+    return launch_reduce_scatter_pull(0, n_slots, t, out, count, n_ctas, Signals{},
+                                      static_cast<cudaStream_t>(stream));
+}
+
+int c3_ce_execute(c3_world* w, const c3_transfer* t, int n_transfers, const void* const* src,
+                  void* const* dst, int src_filter, void* stream) {
+    if (!w || (n_transfers > 0 && (!t || !src || !dst)))
+        return set_error(C3_ERR_VALIDATION, "c3_ce_execute: null argument");
+    for (int i = 0; i < n_transfers; ++i)
+        if (t[i].src_gpu < 0 || t[i].src_gpu >= w->n_ranks || t[i].dst_gpu < 0 ||
+            t[i].dst_gpu >= w->n_ranks || t[i].length < 0 || t[i].src_offset < 0 || t[i].dst_offset < 0)
+            return set_error(C3_ERR_VALIDATION, "c3_ce_execute: transfer " + std::to_string(i) + " out of range");
+    return ce_run(w, t, n_transfers, src, dst, src_filter, static_cast<cudaStream_t>(stream));
+}
+
+// ------------------------------------------------------------- sessions
+
+int c3_plan_transfers(int kind, int n_ranks, int64_t chunk_bytes, int dma_engines, c3_transfer* out,
+                      int capacity, int* count) {
+    if (!count) return set_error(C3_ERR_VALIDATION, "c3_plan_transfers: null count");
+    return guarded([&] {
+        c3sim::MachineDescriptor md;
+        md.gpus_per_node = std::max(1, n_ranks);
+        md.dma_engines_per_gpu = dma_engines;
+        c3sim::TransferPlan plan;
+        switch (kind) {
+            case C3_ALL_GATHER: plan = c3sim::plan_all_gather(n_ranks, chunk_bytes, md); break;
+            case C3_ALL_TO_ALL: plan = c3sim::plan_all_to_all(n_ranks, chunk_bytes, md); break;
+            case C3_REDUCE_SCATTER: plan = c3sim::plan_reduce_scatter(n_ranks, chunk_bytes, md); break;
+            default: throw c3sim::UnknownEntityError("unknown collective kind " + std::to_string(kind));
+        }
+        if (dma_engines < 1) throw c3sim::ValidationError("dma_engines must be >= 1");
+        const c3sim::PlanCheck chk = c3sim::validate_plan(plan, md);
+        if (!chk.ok) throw c3sim::ValidationError("transfer plan invalid: " + chk.error);
+        *count = static_cast<int>(plan.transfers.size());
+        if (out) {
+            if (capacity < *count) throw c3sim::ValidationError("c3_plan_transfers: capacity too small");
+            for (int i = 0; i < *count; ++i) {
+                const auto& t = plan.transfers[static_cast<std::size_t>(i)];
+                out[i] = {t.src_gpu, t.dst_gpu, t.src_offset, t.dst_offset, t.length, t.engine_id, t.seq};
+            }
+        }
+        return C3_OK;
+    });
+}
+
+int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** out) {
+    if (!w || !desc || !out) return set_error(C3_ERR_VALIDATION, "c3_session_create: null argument");
+    const c3_scenario_desc& d = *desc;
+    if (d.n_ranks != w->n_ranks)
+        return set_error(C3_ERR_VALIDATION, "c3_session_create: scenario n_ranks != world n_ranks");
+    if (d.collective != C3_ALL_GATHER && d.collective != C3_REDUCE_SCATTER)
+        return set_error(C3_ERR_UNSUPPORTED, "c3_session_create: collective must be all-gather or reduce-scatter");
+    if (d.payload_bytes < 0 || d.payload_bytes % d.n_ranks)
+        return set_error(C3_ERR_VALIDATION, "collective: payload_bytes must be divisible by n_ranks");
+    if (d.collective == C3_REDUCE_SCATTER && (d.payload_bytes / d.n_ranks) % 2)
+        return set_error(C3_ERR_VALIDATION, "reduce-scatter: per-rank slot must hold whole bf16 elements");
+    auto* s = new c3_session;
+    s->w = w;
+    s->d = d;
+    s->n = d.n_ranks;
+    s->vr = w->loopback ? d.n_ranks : 1;
+    s->chunk = d.payload_bytes / d.n_ranks;
+    const auto fail = [&](int rc) {
+        c3_session_destroy(s);
+        return rc;
+    };
+    cudaSetDevice(w->device);
+    int rc = session_alloc(s);
+    if (rc != C3_OK) return fail(rc);
+    rc = guarded([&] {
+        s->md = b200_machine(w, s->n);
+        s->tables = default_tables(s->md);
+        c3sim::C3Scenario& sc = s->scenario;
+        sc.id = "session";
+        sc.gemm.tag = "gemm";
+        sc.gemm.m = d.m;
+        sc.gemm.n = d.n;
+        sc.gemm.k = d.k;
+        sc.gemm.dtype_bytes = 2;
+        sc.collective.kind = d.collective == C3_ALL_GATHER ? c3sim::CollectiveKind::AllGather
+                                                           : c3sim::CollectiveKind::ReduceScatter;
+        sc.collective.payload_bytes = d.payload_bytes;
+        sc.collective.n_ranks = d.n_ranks;
+        if (s->n > 1) {
+            const c3sim::TransferPlan tp =
+                d.collective == C3_ALL_GATHER ? c3sim::plan_all_gather(s->n, s->chunk, s->md)
+                                              : c3sim::plan_reduce_scatter(s->n, s->chunk, s->md);
+            const c3sim::PlanCheck chk = c3sim::validate_plan(tp, s->md);
+            if (!chk.ok) throw c3sim::ValidationError("transfer plan invalid: " + chk.error);
+            for (const auto& t : tp.transfers)
+                s->plan.push_back({t.src_gpu, t.dst_gpu, t.src_offset, t.dst_offset, t.length,
+                                   t.engine_id, t.seq});
+        }
+        return C3_OK;
+    });
+    if (rc != C3_OK) return fail(rc);
+    if (w->loopback || s->n == 1) {
+        s->ready = true;
+        if (!w->loopback) {
+            s->peer_coll[0] = d.collective == C3_ALL_GATHER ? s->recv[0] : s->in[0];
+            s->peer_sig[0] = s->sig;
+        }
+    }
+    *out = s;
+    return C3_OK;
+}
+
+int c3_session_destroy(c3_session* s) {
+    if (!s) return C3_OK;
+    cudaSetDevice(s->w->device);
+    cudaDeviceSynchronize();
+    for (void* p : s->imported) cudaIpcCloseMemHandle(p);
+    for (auto* v : {&s->recv, &s->in, &s->out, &s->staging})
+        for (void* p : *v) cudaFree(p);
+    for (void* p : {s->a, s->b, s->c, static_cast<void*>(s->sig), static_cast<void*>(s->done)})
+        if (p) cudaFree(p);
+    for (cudaStream_t st : {s->main, s->gemm_s, s->comm_s, s->comm_hi})
+        if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end})
+        if (e) cudaEventDestroy(e);
+    delete s;
+    return C3_OK;
+}
+
+int c3_session_pointers(const c3_session* s, int v, c3_session_ptrs* o) {
+    if (!s || !o) return set_error(C3_ERR_VALIDATION, "c3_session_pointers: null argument");
+    if (v < 0 || v >= s->vr) return set_error(C3_ERR_VALIDATION, "c3_session_pointers: bad virtual rank");
+    std::memset(o, 0, sizeof *o);
+    const c3_scenario_desc& d = s->d;
+    o->a = s->a;
+    o->b = s->b;
+    o->c = s->c;
+    o->a_bytes = d.m * d.k * 2;
+    o->b_bytes = d.n * d.k * 2;
+    o->c_bytes = d.m * d.n * 2;
+    const size_t sv = static_cast<size_t>(v);
+    const int self = s->w->loopback ? v : s->w->rank;
+    if (d.collective == C3_ALL_GATHER) {
+        o->recv = s->recv[sv];
+        o->recv_bytes = d.payload_bytes;
+        o->send = static_cast<uint8_t*>(s->recv[sv]) + s->chunk * self;
+        o->send_bytes = s->chunk;
+    } else {
+        o->send = s->in[sv];
+        o->send_bytes = d.payload_bytes;
+        o->recv = s->out[sv];
+        o->recv_bytes = s->chunk;
+        o->staging = s->staging[sv];
+        o->staging_bytes = d.payload_bytes;
+    }
+    o->virtual_ranks = s->vr;
+    return C3_OK;
+}
+
+int c3_session_fill(c3_session* s, uint64_t seed) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_fill: null session");
+    const c3_scenario_desc& d = s->d;
+    cudaStream_t st = s->main;
+    const int r0 = s->w->loopback ? 0 : s->w->rank;
+    C3_TRY(launch_fill_bf16(s->a, d.m * d.k, seed, r0, 0, st));
+    C3_TRY(launch_fill_bf16(s->b, d.n * d.k, seed, r0, 1, st));
+    for (int v = 0; v < s->vr; ++v) {
+        const int rank = s->w->loopback ? v : s->w->rank;
+        const size_t sv = static_cast<size_t>(v);
+        if (d.collective == C3_ALL_GATHER) {
+            C3_CUDA(cudaMemsetAsync(s->recv[sv], 0, static_cast<size_t>(d.payload_bytes), st));
+            C3_TRY(launch_fill_labels(static_cast<uint8_t*>(s->recv[sv]) + s->chunk * rank, s->chunk,
+                                      seed, rank, 2, st));
+        } else {
+            C3_TRY(launch_fill_bf16(s->in[sv], d.payload_bytes / 2, seed, rank, 3, st));
+        }
+    }
+    C3_CUDA(cudaStreamSynchronize(st));
+    return C3_OK;
+}
+
+int c3_session_export(c3_session* s, void* blob) {
+    if (!s || !blob) return set_error(C3_ERR_VALIDATION, "c3_session_export: null argument");
+    if (s->w->loopback) return set_error(C3_ERR_VALIDATION, "c3_session_export: loopback session");
+    std::memset(blob, 0, C3_SESSION_HANDLE_BYTES);
+    uint8_t* b = static_cast<uint8_t*>(blob);
+    void* coll = s->d.collective == C3_ALL_GATHER ? s->recv[0] : s->in[0];
+    C3_TRY(c3_ipc_export(s->w, coll, b));
+    if (!s->staging.empty()) C3_TRY(c3_ipc_export(s->w, s->staging[0], b + C3_IPC_HANDLE_BYTES));
+    C3_TRY(c3_ipc_export(s->w, s->sig, b + 2 * C3_IPC_HANDLE_BYTES));
+    return C3_OK;
+}
+
+int c3_session_import(c3_session* s, const void* all) {
+    if (!s || !all) return set_error(C3_ERR_VALIDATION, "c3_session_import: null argument");
+    if (s->w->loopback) return set_error(C3_ERR_VALIDATION, "c3_session_import: loopback session");
+    const uint8_t* b = static_cast<const uint8_t*>(all);
+    for (int p = 0; p < s->n; ++p) {
+        const uint8_t* blob = b + static_cast<size_t>(p) * C3_SESSION_HANDLE_BYTES;
+        if (p == s->w->rank) {
+            s->peer_coll[p] = s->d.collective == C3_ALL_GATHER ? s->recv[0] : s->in[0];
+            s->peer_staging[p] = s->staging.empty() ? nullptr : s->staging[0];
+            s->peer_sig[p] = s->sig;
+            continue;
+        }
+        void* ptr = nullptr;
+        C3_TRY(c3_ipc_import(s->w, blob, &ptr));
+        s->imported.push_back(ptr);
+        s->peer_coll[p] = ptr;
+        if (!s->staging.empty()) {
+            C3_TRY(c3_ipc_import(s->w, blob + C3_IPC_HANDLE_BYTES, &ptr));
+            s->imported.push_back(ptr);
+            s->peer_staging[p] = ptr;
+        }
+        C3_TRY(c3_ipc_import(s->w, blob + 2 * C3_IPC_HANDLE_BYTES, &ptr));
+        s->imported.push_back(ptr);
+        s->peer_sig[p] = static_cast<uint32_t*>(ptr);
+    }
+    s->ready = true;
+    return C3_OK;
+}
+
+int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
+    if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_default_alloc: null argument");
+    const int C = s->md.cus_per_gpu;
+    if (strategy >= C3_GEMM_ONLY) {
+        *out = {C, strategy == C3_COMM_ONLY_CU ? 32 : 0, 0,
+                strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA : C3_BACKEND_CU, 0};
+        return C3_OK;
+    }
+    if (strategy < C3_SERIAL || strategy > C3_CONCCL_RP)
+        return set_error(C3_ERR_UNKNOWN, "unknown strategy " + std::to_string(strategy));
+    return guarded([&] {
+        const c3sim::Allocation a =
+            c3sim::allocate_cus(s->scenario, static_cast<c3sim::Strategy>(strategy), s->md, s->tables,
+                                c3sim::EfficiencyParams{});
+        out->cus_gemm = a.cus_gemm;
+        out->cus_comm = a.cus_comm;
+        out->cus_idle = a.cus_idle;
+        out->backend = a.comm_backend == c3sim::CommBackend::DMA ? C3_BACKEND_DMA : C3_BACKEND_CU;
+        out->comm_first = a.comm_first ? 1 : 0;
+        if (strategy == C3_SERIAL) out->cus_comm = 32;  // isolated SM collective width
+        return C3_OK;
+    });
+}
+
+static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_in, int flags,
+                            c3_timing* t) {
+    if (!s->ready) return set_error(C3_ERR_VALIDATION, "c3_session_run: peers not imported");
+    c3_alloc a;
+    if (alloc_in)
+        a = *alloc_in;
+    else
+        C3_TRY(c3_session_default_alloc(s, strategy, &a));
+    c3_world* w = s->w;
+    const int C = w->prop.multiProcessorCount;
+    std::memset(t, 0, sizeof *t);
+    ++s->epoch;
+
+    cudaStream_t gs = s->gemm_s, cs = s->comm_s;
+    int gemm_ctas = std::max(1, std::min(a.cus_gemm > 0 ? a.cus_gemm : C, C));
+    int comm_ctas = std::max(1, a.cus_comm > 0 ? a.cus_comm : 32);
+    const bool sp = strategy == C3_C3_SP || strategy == C3_C3_SP_RP;
+    const bool rp = strategy == C3_C3_RP || strategy == C3_C3_SP_RP;
+    if (sp) cs = s->comm_hi;
+    if (rp && w->green_ok) {
+        GreenPartition* gp = nullptr;
+        if (green_partition(w, comm_ctas, &gp) == C3_OK) {
+            gs = reinterpret_cast<cudaStream_t>(gp->gemm_stream);
+            cs = reinterpret_cast<cudaStream_t>(gp->comm_stream);
+            comm_ctas = gp->comm_sms;
+            gemm_ctas = std::min(gemm_ctas, gp->gemm_sms);
+            t->partition = 1;
+        }
+    }
+    t->gemm_ctas = gemm_ctas;
+    t->comm_ctas = a.backend == C3_BACKEND_CU ? comm_ctas : 0;
+    int launches = 0;
+
+    C3_CUDA(cudaEventRecord(s->ev_start, s->main));
+    const bool do_gemm = strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;
+    const bool do_comm = strategy != C3_GEMM_ONLY;
+    const int backend = strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA
+                        : strategy == C3_COMM_ONLY_CU ? C3_BACKEND_CU
+                                                      : a.backend;
+    if (strategy == C3_SERIAL) {
+        C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
+        C3_CUDA(cudaEventRecord(s->ev_gs, gs));
+        C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs));
+        ++launches;
+        C3_CUDA(cudaEventRecord(s->ev_ge, gs));
+        C3_CUDA(cudaEventRecord(s->ev_cs, gs));
+        C3_TRY(enqueue_collective(s, C3_BACKEND_CU, comm_ctas, flags, gs, &launches));
+        C3_CUDA(cudaEventRecord(s->ev_ce, gs));
+        C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ce, 0));
+    } else {
+        C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
+        C3_CUDA(cudaStreamWaitEvent(cs, s->ev_start, 0));
+        const auto launch_gemm = [&]() -> int {
+            C3_CUDA(cudaEventRecord(s->ev_gs, gs));
+            if (do_gemm) {
+                C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs));
+                ++launches;
+            }
+            C3_CUDA(cudaEventRecord(s->ev_ge, gs));
+            return C3_OK;
+        };
+        const auto launch_comm = [&]() -> int {
+            C3_CUDA(cudaEventRecord(s->ev_cs, cs));
+            if (do_comm) C3_TRY(enqueue_collective(s, backend, comm_ctas, flags, cs, &launches));
+            C3_CUDA(cudaEventRecord(s->ev_ce, cs));
+            return C3_OK;
+        };
+        if (a.comm_first) {
+            C3_TRY(launch_comm());
+            C3_TRY(launch_gemm());
+        } else {
+            C3_TRY(launch_gemm());
+            C3_TRY(launch_comm());
+        }
+        C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ge, 0));
+        C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ce, 0));
+    }
+    C3_CUDA(cudaEventRecord(s->ev_end, s->main));
+    C3_CUDA(cudaEventSynchronize(s->ev_end));
+    C3_CUDA(cudaGetLastError());
+    t->gemm_start_ms = elapsed(s->ev_start, s->ev_gs);
+    t->gemm_end_ms = elapsed(s->ev_start, s->ev_ge);
+    t->comm_start_ms = elapsed(s->ev_start, s->ev_cs);
+    t->comm_end_ms = elapsed(s->ev_start, s->ev_ce);
+    t->total_ms = elapsed(s->ev_start, s->ev_end);
+    t->launches = launches;
+    return C3_OK;
+}
+
+int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out) {
+    if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_run: null argument");
+    C3_CUDA(cudaSetDevice(s->w->device));
+    return session_run_impl(s, strategy, alloc, 0, out);
+}
+
+// Loopback parity helper: run every virtual rank's share of the collective.
+int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out) {
+    if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_run_all_ranks: null argument");
+    C3_CUDA(cudaSetDevice(s->w->device));
+    return session_run_impl(s, strategy, alloc, kRunAllRanks, out);
+}
+
+}  // extern "C"

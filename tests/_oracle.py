@@ -1,0 +1,112 @@
+"""ctypes binding of the TEST-ONLY oracle (oracle/lib/libc3oracle.so).
+
+Only tests/, __graft_entry__.smoke() and bench.py's CPU-baseline legs import
+this module; the product never does.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(REPO, "oracle", "lib", "libc3oracle.so")
+
+
+class Transfer(C.Structure):
+    _fields_ = [("src_gpu", C.c_int32), ("dst_gpu", C.c_int32), ("src_offset", C.c_int64),
+                ("dst_offset", C.c_int64), ("length", C.c_int64), ("engine_id", C.c_int32),
+                ("seq", C.c_int32)]
+
+
+_L = None
+
+
+def lib():
+    global _L
+    if _L is None:
+        L = C.CDLL(LIB)
+        L.c3o_label_word.restype = C.c_uint64
+        L.c3o_label_word.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_uint64]
+        L.c3o_fill_labels.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_int]
+        L.c3o_fill_bf16.argtypes = [C.c_void_p, C.c_int64, C.c_uint64, C.c_int, C.c_int]
+        L.c3o_bf16_value.restype = C.c_uint16
+        L.c3o_bf16_value.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_uint64]
+        L.c3o_f32_to_bf16_rne.restype = C.c_uint16
+        L.c3o_f32_to_bf16_rne.argtypes = [C.c_float]
+        L.c3o_bf16_to_f32.restype = C.c_float
+        L.c3o_bf16_to_f32.argtypes = [C.c_uint16]
+        L.c3o_replay_plan.argtypes = [C.POINTER(Transfer), C.c_int, C.c_int, C.c_void_p,
+                                      C.c_int64, C.c_void_p, C.c_int64]
+        L.c3o_byte_oracle.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
+                                      C.POINTER(Transfer), C.c_int, C.c_char_p, C.c_size_t]
+        L.c3o_expected_allgather.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_int]
+        L.c3o_reduce_scatter_bf16.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p]
+        L.c3o_gemm_bf16_ref_samples.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                                C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
+                                                C.c_void_p, C.c_void_p]
+        L.c3o_gemm_f32.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
+                                   C.c_int64, C.c_int]
+        L.c3o_cpu_c3.argtypes = [C.c_int64, C.c_int64, C.c_int64, C.c_int, C.POINTER(Transfer),
+                                 C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                 C.c_void_p]
+        _L = L
+    return _L
+
+
+def _p(a):
+    return a.ctypes.data_as(C.c_void_p)
+
+
+def labels(nbytes, seed, rank, tensor):
+    out = np.empty(nbytes, np.uint8)
+    lib().c3o_fill_labels(_p(out), nbytes, seed, rank, tensor)
+    return out
+
+
+def bf16(count, seed, rank, tensor):
+    out = np.empty(count, np.uint16)
+    lib().c3o_fill_bf16(_p(out), count, seed, rank, tensor)
+    return out
+
+
+def bf16_to_f32(bits):
+    return (bits.astype(np.uint32) << 16).view(np.float32)
+
+
+def expected_allgather(n, chunk, seed, tensor):
+    out = np.empty(n * chunk, np.uint8)
+    lib().c3o_expected_allgather(_p(out), n, chunk, seed, tensor)
+    return out
+
+
+def reduce_scatter(inputs, rank, count):
+    """inputs: list of uint16 arrays (n*count each)."""
+    n = len(inputs)
+    arr = (C.c_void_p * n)(*[i.ctypes.data for i in inputs])
+    out = np.empty(count, np.uint16)
+    lib().c3o_reduce_scatter_bf16(arr, n, rank, count, _p(out))
+    return out
+
+
+def gemm_samples(A, B, M, N, K, rows, cols):
+    rows = np.ascontiguousarray(rows, np.int64)
+    cols = np.ascontiguousarray(cols, np.int64)
+    ref = np.empty(len(rows), np.float64)
+    mag = np.empty(len(rows), np.float64)
+    lib().c3o_gemm_bf16_ref_samples(_p(A), _p(B), M, N, K, _p(rows), _p(cols), len(rows),
+                                    _p(ref), _p(mag))
+    return ref, mag
+
+
+def to_transfers(plan_json_transfers):
+    arr = (Transfer * max(1, len(plan_json_transfers)))()
+    for i, t in enumerate(plan_json_transfers):
+        arr[i] = Transfer(t["src"], t["dst"], t["src_off"], t["dst_off"], t["len"], t["engine"],
+                          t["seq"])
+    return arr
+
+
+def byte_oracle(kind, n, chunk, src_bytes, dst_bytes, transfers, count):
+    why = C.create_string_buffer(256)
+    rc = lib().c3o_byte_oracle(kind, n, chunk, src_bytes, dst_bytes, transfers, count, why, 256)
+    return rc, why.value.decode()
