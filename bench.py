@@ -1,0 +1,385 @@
+#!/usr/bin/env python3
+"""C3 bench: GEMM concurrent with an all-gather (or reduce-scatter) under the
+paper's strategies, on B200, through the product's C ABI (libc3cuda.so).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2]
+                    [--strategy conccl] [--impl ours|reference]
+
+Metric (BASELINE.json): C3 speedup over serial and % of ideal speedup.
+  speedup = (t_gemm_iso + t_comm_iso) / t_concurrent   (reference sim.cpp:143,212)
+  ideal   = (t_gemm_iso + t_comm_iso) / max(...)        (taxonomy.cpp:23-27)
+  % ideal = 100 (speedup - 1) / (ideal - 1)             (taxonomy.cpp:29-33)
+t_comm_iso is the isolated time of the SAME backend the strategy uses
+(north_star); the conservative variant (vs the best isolated collective) is
+reported beside it.
+
+World: at N=1 the 8-rank scenario of configs[1] is EMULATED on one GPU
+("loopback"): this GPU runs its own GEMM and its own share of the 8-rank
+collective, with the 7 peers' buffers as stand-in HBM buffers — per-GPU HBM
+traffic is that of the real collective, but no NVLink is involved, so the
+collective is faster than on a real node (stated in config.world). Under
+torchrun (N>1) every rank is a real GPU and peers are mapped with CUDA IPC.
+
+Timing: W warm-up steps, then exactly K timed steps between a barrier +
+device synchronize; per-step device time from CUDA events on the launching
+streams (inside c3_session_run), max over ranks; inputs (A 128 MiB, B 448 MiB,
+AG 896 MiB) exceed the 126 MB L2, so no flush is needed between steps.
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+from paper_2412_14335_b200.dist import Dist  # noqa: E402
+
+MIB = 1 << 20
+# BASELINE.json configs: (M, N, K), collective, payload per rank
+CONFIGS = {
+    "cfg2": dict(desc="LLaMA-70B FSDP layer: FFN up-proj GEMM 8192x28672x8192 bf16 || "
+                      "next-layer weight all-gather 896 MiB (gate+up) across 8 GPUs",
+                 m=8192, n=28672, k=8192, coll="all-gather", payload=896 * MIB),
+    "cfg2_448": dict(desc="LLaMA-70B FFN up GEMM || all-gather 448 MiB (up only)",
+                     m=8192, n=28672, k=8192, coll="all-gather", payload=448 * MIB),
+    "cfg3": dict(desc="LLaMA-70B backward: weight-grad GEMM 8192x28672x8192 bf16 || "
+                      "gradient reduce-scatter 896 MiB",
+                 m=8192, n=28672, k=8192, coll="reduce-scatter", payload=896 * MIB),
+    "cfg4": dict(desc="LLaMA-405B FSDP layer: GEMM 8192x53248x16384 bf16 || all-gather 1664 MiB",
+                 m=8192, n=53248, k=16384, coll="all-gather", payload=1664 * MIB),
+    "cfg4_mb": dict(desc="LLaMA-405B small-token (memory-bound) GEMM 128x53248x16384 || "
+                         "all-gather 1664 MiB",
+                    m=128, n=53248, k=16384, coll="all-gather", payload=1664 * MIB),
+}
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def load_peaks():
+    path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            p = json.load(f)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+# ------------------------------------------------------------- clocks ------
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sms, maxs, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sms.append(float(parts[0]))
+                maxs.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        loaded = [s for s in sms if s > 300] or sms
+        return {"sm_mhz": statistics.median(loaded) if loaded else None,
+                "sm_max_mhz": max(maxs) if maxs else None,
+                "reasons": sorted(reasons), "samples": len(sms)}
+
+
+# ------------------------------------------------------------ ours ------
+
+def median(xs):
+    return statistics.median(xs) if xs else float("nan")
+
+
+def run_ours(args, dist):
+    import ctypes as C
+
+    import torch
+
+    import paper_2412_14335_b200 as c3
+
+    cfg = CONFIGS[args.config]
+    n = 8 if dist.world == 1 else dist.world
+    loopback = dist.world == 1
+    torch.cuda.set_device(dist.local_rank)
+    world = c3.World(dist.rank, n, dist.local_rank, loopback=loopback)
+    coll = c3.ALL_GATHER if cfg["coll"] == "all-gather" else c3.REDUCE_SCATTER
+    sess = c3.Session(world, cfg["m"], cfg["n"], cfg["k"], coll, cfg["payload"])
+    if not loopback:
+        sess.import_handles(dist.allgather_bytes(sess.export_handles()))
+    sess.fill(20241217)
+    strategies = [c3.STRATEGY_NAMES.index(s) for s in args.strategies]
+    head = c3.STRATEGY_NAMES.index(args.strategy)
+
+    def timed(strategy, steps, alloc=None):
+        """steps runs; per-step device times, max over ranks."""
+        rows = []
+        for _ in range(steps):
+            t = sess.run(strategy, alloc)
+            rows.append([t.total_ms, t.gemm_end_ms - t.gemm_start_ms, t.comm_end_ms - t.comm_start_ms,
+                         float(t.launches)])
+        flat = dist.max_list([v for r in rows for v in r])
+        return [flat[i * 4:(i + 1) * 4] for i in range(steps)]
+
+    # isolated kernel times (outside the timed region), own-backend collectives
+    W, K = args.warmup, args.steps
+    timed(c3.GEMM_ONLY, W)
+    t_g = median([r[1] for r in timed(c3.GEMM_ONLY, K)])
+    iso_comm = {}
+    for name, mode in (("cu", c3.COMM_ONLY_CU), ("dma", c3.COMM_ONLY_DMA)):
+        a = sess.default_alloc(mode)
+        if mode == c3.COMM_ONLY_CU:
+            a.cus_comm = 32 if coll == c3.ALL_GATHER else 64  # comm_saturation_cus
+        timed(mode, 2, a)
+        iso_comm[name] = median([r[2] for r in timed(mode, K, a)])
+
+    results = {}
+    for st in strategies:
+        if st == c3.SERIAL:
+            continue
+        timed(st, max(1, W // 2))
+        rows = timed(st, K)
+        t_conc = median([r[0] for r in rows])
+        backend = sess.default_alloc(st).backend
+        t_c = iso_comm["dma" if backend == c3.BACKEND_DMA else "cu"]
+        sp = (t_g + t_c) / t_conc
+        ideal = c3.ideal_speedup(t_g, t_c)
+        best_c = min(iso_comm.values())
+        results[c3.STRATEGY_NAMES[st]] = {
+            "t_concurrent_ms": t_conc, "t_comm_iso_ms": t_c, "speedup": sp, "ideal": ideal,
+            "fraction_of_ideal": c3.fraction_of_ideal(sp, ideal),
+            "speedup_vs_best_comm": (t_g + best_c) / t_conc,
+            "fraction_vs_best_comm": c3.fraction_of_ideal((t_g + best_c) / t_conc,
+                                                          c3.ideal_speedup(t_g, best_c)),
+            "gemm_ms_in_step": median([r[1] for r in rows])}
+
+    # ---- the timed region: K steps of the headline strategy ----
+    for _ in range(W):
+        sess.run(head)
+    torch.cuda.synchronize()
+    dist.barrier()
+    clocks = ClockSampler(dist.local_rank) if dist.rank == 0 else None
+    if clocks:
+        clocks.start()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rows = timed(head, K)
+    torch.cuda.synchronize()
+    dist.barrier()
+    wall = time.perf_counter() - t0
+    clk = clocks.stop() if clocks else None
+    step_ms = [r[0] for r in rows]
+    gemm_ms = [r[1] for r in rows]
+    launches = int(sum(r[3] for r in rows))
+    t_conc = median(step_ms)
+    backend = sess.default_alloc(head).backend
+    t_c = iso_comm["dma" if backend == c3.BACKEND_DMA else "cu"]
+    speedup = (t_g + t_c) / t_conc
+    ideal = c3.ideal_speedup(t_g, t_c)
+    frac = c3.fraction_of_ideal(speedup, ideal)
+
+    # ---- e2e through the C ABI with host buffers ----
+    p = sess.pointers(0)
+    h2d = p.a_bytes + p.send_bytes
+    d2h = 4096
+    pin_a = torch.empty(p.a_bytes, dtype=torch.uint8, pin_memory=True)
+    pin_s = torch.empty(p.send_bytes, dtype=torch.uint8, pin_memory=True)
+    pin_o = torch.empty(d2h, dtype=torch.uint8, pin_memory=True)
+    L = c3.lib()
+
+    def e2e_step(strategy):
+        t0 = time.perf_counter()
+        c3.check(L.c3_memcpy(p.a, pin_a.data_ptr(), p.a_bytes, 1, None))
+        c3.check(L.c3_memcpy(p.send, pin_s.data_ptr(), p.send_bytes, 1, None))
+        c3.check(L.c3_stream_sync(None))
+        sess.run(strategy)
+        c3.check(L.c3_memcpy(pin_o.data_ptr(), p.c, d2h, 2, None))
+        c3.check(L.c3_stream_sync(None))
+        return (time.perf_counter() - t0) * 1e3
+
+    for _ in range(2):
+        e2e_step(head)
+    e2e_conc = median(dist.max_list([e2e_step(head) for _ in range(K)]))
+    e2e_g = median(dist.max_list([e2e_step(c3.GEMM_ONLY) for _ in range(K)]))
+    e2e_c = median(dist.max_list(
+        [e2e_step(c3.COMM_ONLY_DMA if backend == c3.BACKEND_DMA else c3.COMM_ONLY_CU)
+         for _ in range(K)]))
+    # serial e2e = inputs in, GEMM, collective, result out (copies counted once)
+    io_ms = e2e_g - t_g
+    e2e_speedup = (e2e_g + e2e_c - io_ms) / e2e_conc
+
+    peaks, peak_src = load_peaks()
+    flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
+    gemm_avg = sum(gemm_ms) / len(gemm_ms)
+    achieved = flops / (gemm_avg * 1e-3) / 1e12
+    traffic = None
+    prof = os.path.join(REPO, "profiles", "ncu_gemm_summary.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(f"{cfg['m']}x{cfg['n']}x{cfg['k']}", {}).get("dram_bytes")
+        except Exception:
+            traffic = None
+    out = {
+        "metric": "C3 speedup over serial and % of ideal speedup (GEMM+all-gather) at 2/4/8 B200",
+        "value": speedup, "unit": "x (t_serial / t_concurrent)",
+        "fraction_of_ideal_pct": 100.0 * frac, "ideal": ideal,
+        "n_gpus": dist.world, "steps": K, "warmup": W,
+        "ms_per_step": sum(step_ms) / len(step_ms), "ms_per_step_median": t_conc,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16", "data": "synthetic (counter-hash bf16 U(-1,1)/8 and byte labels)",
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "strategy": args.strategy,
+                   "collective": cfg["coll"], "payload_bytes": cfg["payload"],
+                   "gemm_mnk": [cfg["m"], cfg["n"], cfg["k"]], "ranks": n,
+                   "world": ("loopback: 8-rank collective emulated on 1 GPU (peer buffers in local "
+                             "HBM, no NVLink)") if loopback else f"{n} GPUs, CUDA-IPC peer memory",
+                   "l2": "inputs > 126 MB L2 (no flush needed)",
+                   "isolated_ms": {"gemm": t_g, "comm_cu": iso_comm["cu"],
+                                   "comm_dma": iso_comm["dma"]},
+                   "timed_region_wall_s": wall},
+        "strategies": results,
+        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tn_kernel (tcgen05)",
+                     "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                     "frac": achieved / peaks["bf16_tflops"],
+                     "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", 1365.0),
+                     "peak_source": peak_src + " burst bf16 (cuBLAS)",
+                     "algorithmic_flops_per_launch": flops, "traffic": traffic},
+        "e2e": {"value": e2e_speedup, "unit": "x (t_serial / t_concurrent, host buffers)",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                "concurrent_ms": e2e_conc},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(quick=True)
+    sess.close()
+    world.close()
+    return out
+
+
+# ---------------------------------------------------------- CPU arms ------
+
+def ref_cpu_c3(m, n, k, ranks, payload, warmup, iters):
+    exe = os.path.join(REPO, "oracle", "_ref", "c3sim_ref_cpu_c3")
+    machine = os.path.join(REPO, "tests", "golden", "ref_data", "mi300x-node.json")
+    threads = os.cpu_count() or 1
+    r = subprocess.run([exe, str(m), str(n), str(k), str(ranks), str(payload), str(threads),
+                        str(warmup), str(iters), machine], capture_output=True, text=True,
+                       check=True)
+    return json.loads(r.stdout)
+
+
+def cpu_baseline(quick=True):
+    """configs[0] on the host cores: fp32 GEMM 1024^3 || 16 MiB all-gather at
+    world 2 (the reference planner's transfers, memcpy replay)."""
+    res = ref_cpu_c3(1024, 1024, 1024, 2, 16 * MIB, 2 if quick else 6, 3 if quick else 9)
+    return {"value": res["speedup"], "unit": "x (t_serial / t_concurrent)",
+            "cores": res["threads"], "kind": "port",
+            "fraction_of_ideal_pct": 100 * res["fraction_of_ideal"],
+            "sample": ("configs[0]: fp32 GEMM 1024x1024x1024 on all host threads || 16 MiB "
+                       "all-gather (reference plan_all_gather, world 2) replayed by memcpy on one "
+                       "thread; oracle/c3oracle.c restatement driven by oracle/_ref; medians"),
+            "t_gemm_ms": 1e3 * res["t_gemm_s"], "t_comm_ms": 1e3 * res["t_comm_s"],
+            "t_concurrent_ms": 1e3 * res["t_concurrent_s"]}
+
+
+def run_reference(args, dist):
+    """--impl reference: the reference's CPU path on the host cores, on a
+    bounded sample of the same workload (M scaled to 256 tokens and the
+    payload by the same factor), rank 0 only."""
+    cfg = CONFIGS[args.config]
+    scale = max(1, cfg["m"] // 256)
+    m = cfg["m"] // scale
+    payload = cfg["payload"] // scale
+    payload -= payload % 8
+    t0 = time.perf_counter()
+    res = ref_cpu_c3(m, cfg["n"], cfg["k"], 8, payload, 1, max(1, min(args.steps, 3)))
+    wall = time.perf_counter() - t0
+    sample = (f"bounded sample of {args.config} (1/{scale} of its tokens and payload): fp32 GEMM "
+              f"{m}x{cfg['n']}x{cfg['k']} on all host threads || all-gather of {payload / MIB:.0f} "
+              "MiB over 8 host ranks (reference plan_all_gather replayed by memcpy on one thread); "
+              "medians")
+    return {"metric": "C3 speedup over serial and % of ideal speedup (GEMM+all-gather) at 2/4/8 B200",
+            "impl": "reference", "value": res["speedup"], "unit": "x (t_serial / t_concurrent)",
+            "fraction_of_ideal_pct": 100 * res["fraction_of_ideal"],
+            "n_gpus": dist.world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1e3 * res["t_concurrent_s"], "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "fp32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: {cfg['desc']}", "sample": sample},
+            "cpu_baseline": {"value": res["speedup"], "unit": "x", "cores": res["threads"],
+                             "kind": "port", "sample": sample},
+            "e2e": {"value": res["speedup"], "unit": "x", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+            "wall_s": wall}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=9)
+    ap.add_argument("--warmup", type=int, default=6)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--strategy", default="conccl")
+    ap.add_argument("--strategies", default="c3_base,c3_sp,c3_rp,c3_sp_rp,conccl,conccl_rp")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.strategies = [s for s in args.strategies.split(",") if s]
+    args.warmup = max(3, args.warmup)
+    dist = Dist()
+    try:
+        if args.impl == "reference":
+            if dist.rank == 0:
+                print(json.dumps(run_reference(args, dist)))
+            return
+        out = run_ours(args, dist)
+        if dist.rank == 0:
+            print(json.dumps(out))
+    finally:
+        dist.close()
+
+
+if __name__ == "__main__":
+    main()
