@@ -150,6 +150,8 @@ def run_ours(args, dist):
     if not loopback:
         sess.import_handles(dist.allgather_bytes(sess.export_handles()))
     sess.fill(20241217)
+    if not loopback:
+        sess.set_barrier(dist.barrier)
     strategies = [c3.STRATEGY_NAMES.index(s) for s in args.strategies]
     head = c3.STRATEGY_NAMES.index(args.strategy)
 

@@ -212,6 +212,14 @@ int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing
 /* Loopback parity form: every virtual rank's share of the collective runs (the
  * plain call runs rank 0's share only, the per-GPU load of a real world). */
 int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);
+/* Cross-rank completion of the copy-engine collective is host-side (the
+ * copies are host-issued, as in the paper's ConCCL): a multi-process session
+ * running a DMA strategy calls `fn(ctx)` (e.g. a torch.distributed barrier)
+ * once per step after its own copies drained, and before the local reduce of
+ * a reduce-scatter. Return 0 on success. Not needed for loopback worlds or
+ * the SM (P2P) collectives, which signal through peer flags on the device. */
+typedef int (*c3_barrier_fn)(void* ctx);
+int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
 /* The allocation c3_session_run uses for (strategy, alloc == NULL). */
 int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out);
 

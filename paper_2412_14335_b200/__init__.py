@@ -107,6 +107,18 @@ class Session:
         joined = b"".join(blobs)
         check(lib().c3_session_import(self.h, C.create_string_buffer(joined, len(joined))))
 
+    def set_barrier(self, fn):
+        """Host barrier for copy-engine collectives across processes:
+        fn() -> None (e.g. torch.distributed.barrier)."""
+        def _cb(_ctx):
+            try:
+                fn()
+                return 0
+            except Exception:
+                return 1
+        self._barrier_cb = _capi.BARRIER_FN(_cb)  # keep alive
+        check(lib().c3_session_set_barrier(self.h, C.cast(self._barrier_cb, C.c_void_p), None))
+
     def default_alloc(self, strategy):
         a = _capi.Alloc()
         check(lib().c3_session_default_alloc(self.h, strategy, C.byref(a)))

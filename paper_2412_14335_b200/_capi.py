@@ -25,6 +25,7 @@ BACKEND_CU, BACKEND_DMA = 0, 1
 IPC_HANDLE_BYTES = 64
 SESSION_HANDLE_BYTES = 4 * IPC_HANDLE_BYTES
 MAX_RANKS = 8
+BARRIER_FN = C.CFUNCTYPE(C.c_int, C.c_void_p)
 
 
 class Transfer(C.Structure):
@@ -99,6 +100,7 @@ SIGNATURES = {
     "c3_session_run": (I, [P, I, C.POINTER(Alloc), C.POINTER(Timing)]),
     "c3_session_run_all_ranks": (I, [P, I, C.POINTER(Alloc), C.POINTER(Timing)]),
     "c3_session_default_alloc": (I, [P, I, C.POINTER(Alloc)]),
+    "c3_session_set_barrier": (I, [P, C.c_void_p, P]),
 }
 
 

@@ -158,7 +158,13 @@ int green_partition(c3_world* w, int comm_sms, GreenPartition** out) {
 }
 
 // Copy-engine executor: fork from `parent`, one cudaMemcpyAsync per selected
-// transfer on its engine's stream, join back into `parent`.
+// transfer on the stream of its engine_id, join back into `parent`.
+// Measured on B200 (profiles/r01_ce_probe2.json): copies between two devices
+// and host<->device copies run on copy engines; a copy whose source and
+// destination are on the SAME device runs as a driver copy kernel on SMs
+// (every runtime path, including cudaMemcpyBatchAsync with
+// PreferOverlapWithCompute). So the DMA backend is copy-engine only across
+// devices; in a loopback world its "transfers" are SM copies.
 int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, void* const* dst,
            int src_filter, cudaStream_t parent) {
     if (!w->fork_event) C3_CUDA(cudaEventCreateWithFlags(&w->fork_event, cudaEventDisableTiming));
@@ -166,8 +172,7 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
     bool forked = false;
     for (int i = 0; i < nt; ++i) {
         const c3_transfer& x = t[i];
-        if (src_filter >= 0 && x.src_gpu != src_filter) continue;
-        if (x.length <= 0) continue;
+        if ((src_filter >= 0 && x.src_gpu != src_filter) || x.length <= 0) continue;
         std::size_t idx = 0;
         C3_TRY(ce_stream(w, x.engine_id, &idx));
         if (!forked) {
@@ -240,7 +245,6 @@ c3sim::SlowdownTableSet default_tables(const c3sim::MachineDescriptor& md) {
 
 namespace {
 constexpr int kSigWords = 64;  // signal array: see collectives.cu for the layout
-constexpr int kCeExit = 24, kCeEntry = 32;
 constexpr int kRunAllRanks = 1;
 }  // namespace
 
@@ -263,6 +267,8 @@ struct c3_session {
     uint32_t* sig = nullptr;                // local signal array
     uint32_t* done = nullptr;               // [0] AG counter, [1] RS counter
     uint32_t epoch = 0;
+    c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
+    void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
     std::vector<c3_transfer> plan;          // validated ConCCL plan
     cudaStream_t main = nullptr, gemm_s = nullptr, comm_s = nullptr, comm_hi = nullptr;
@@ -320,21 +326,16 @@ Signals make_signals(c3_session* s, int which) {
     return g;
 }
 
-// Stream-memop barrier (copy-engine path; no SM involvement): tell every
-// peer we reached `slot`, then wait until every peer told us.
-int memop_barrier(c3_session* s, int slot, cudaStream_t st) {
-    for (int p = 0; p < s->n; ++p) {
-        if (p == s->w->rank) continue;
-        C3_CU(StreamWriteValue32, reinterpret_cast<CUstream>(st),
-                                   reinterpret_cast<CUdeviceptr>(s->peer_sig[p] + slot + s->w->rank),
-                                   s->epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
-    }
-    for (int p = 0; p < s->n; ++p) {
-        if (p == s->w->rank) continue;
-        C3_CU(StreamWaitValue32, reinterpret_cast<CUstream>(st),
-                                  reinterpret_cast<CUdeviceptr>(s->sig + slot + p), s->epoch,
-                                  CU_STREAM_WAIT_VALUE_GEQ);
-    }
+// Host barrier across ranks for the copy-engine path: the copies are
+// host-issued (as in the paper's ConCCL) and so is their cross-rank
+// completion; `local` work on `st` is drained first. No stream-wait memops:
+// a blocked cuStreamWaitValue32 can hold a hardware queue other work needs.
+int host_barrier(c3_session* s, cudaStream_t st) {
+    if (s->w->loopback || s->n == 1) return C3_OK;
+    if (!s->barrier) return set_error(C3_ERR_VALIDATION, "copy-engine collective across processes needs "
+                                                         "c3_session_set_barrier");
+    C3_CUDA(cudaStreamSynchronize(st));
+    if (s->barrier(s->barrier_ctx) != 0) return set_error(C3_ERR_IO, "host barrier callback failed");
     return C3_OK;
 }
 
@@ -368,9 +369,10 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
                 ++*launches;
             }
         } else {
+            // completion across ranks: every rank's outgoing copies done = all
+            // data delivered (host barrier at the end of the step, outside timing)
             C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
                           all ? -1 : first, st));
-            if (!loop) C3_TRY(memop_barrier(s, kCeExit, st));
         }
         return C3_OK;
     }
@@ -394,13 +396,10 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         src[static_cast<size_t>(p)] = loop ? s->in[static_cast<size_t>(p)] : s->peer_coll[p];
         dst[static_cast<size_t>(p)] = loop ? s->staging[static_cast<size_t>(p)] : s->peer_staging[p];
     }
-    if (!loop) {
-        src[static_cast<size_t>(w->rank)] = s->in[0];
-        C3_TRY(memop_barrier(s, kCeEntry, st));  // peers done with their staging
-    }
+    if (!loop) src[static_cast<size_t>(w->rank)] = s->in[0];
     C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
                   all ? -1 : first, st));
-    if (!loop) C3_TRY(memop_barrier(s, kCeExit, st));
+    C3_TRY(host_barrier(s, st));  // every peer's slot has landed in my staging
     // local reduce of the n slots (own slot straight from the input)
     for (int v = first; v <= last; ++v) {
         PtrTable slots{};
@@ -805,6 +804,13 @@ int c3_session_import(c3_session* s, const void* all) {
     return C3_OK;
 }
 
+int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_barrier: null session");
+    s->barrier = fn;
+    s->barrier_ctx = ctx;
+    return C3_OK;
+}
+
 int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
     if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_default_alloc: null argument");
     const int C = s->md.cus_per_gpu;
@@ -914,6 +920,10 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     t->comm_start_ms = elapsed(s->ev_start, s->ev_cs);
     t->comm_end_ms = elapsed(s->ev_start, s->ev_ce);
     t->total_ms = elapsed(s->ev_start, s->ev_end);
+    // copy-engine collectives complete across ranks at a host barrier after
+    // the step (each rank's device time is its own copies; callers take the
+    // max over ranks, which is when every chunk has landed)
+    if (do_comm && backend == C3_BACKEND_DMA) C3_TRY(host_barrier(s, s->main));
     t->launches = launches;
     return C3_OK;
 }

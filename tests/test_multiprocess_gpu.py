@@ -1,0 +1,88 @@
+"""Multi-process C3 world on ONE GPU: two processes (ranks 0, 1) share device 0,
+exchange CUDA-IPC handles of their session buffers over gloo, and run the
+non-loopback code path — P2P kernels that signal completion through peer
+flag words (st.release.sys / ld.acquire.sys), and the copy-engine executor
+with its host barrier — checked bit-exactly against the oracle.
+
+This is the same code a one-process-per-GPU torchrun world executes; only the
+peer mapping is same-device IPC instead of NVLink (the box gives one GPU).
+Kernels of the two processes time-slice on the device, so barrier waits here
+cost scheduler slices: this test checks correctness, not speed.
+"""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch.multiprocessing as mp
+
+pytestmark = pytest.mark.gpu
+SEED = 20241217
+
+
+def _free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+def _worker(rank, world, port, coll, q):
+    try:
+        os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                           "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+        import paper_2412_14335_b200 as c3
+        from paper_2412_14335_b200.dist import Dist
+        from tests import _oracle as orc
+        d = Dist()
+        w = c3.World(rank, world, 0, loopback=False)
+        M, N, K = 256, 512, 256
+        chunk = 256 << 10
+        payload = world * chunk
+        s = c3.Session(w, M, N, K, coll, payload)
+        s.import_handles(d.allgather_bytes(s.export_handles()))
+        s.set_barrier(d.barrier)
+        results = {}
+        for strat in (c3.C3_SP, c3.CONCCL, c3.COMM_ONLY_CU, c3.COMM_ONLY_DMA, c3.SERIAL):
+            s.fill(SEED)
+            d.barrier()  # every rank's inputs are written before anyone reads/pushes
+            t = s.run(strat)
+            d.barrier()  # every rank's collective done before checking
+            p = s.pointers(0)
+            if coll == c3.ALL_GATHER:
+                got = np.empty(payload, np.uint8)
+                c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
+                c3.check(c3.lib().c3_stream_sync(None))
+                ok = np.array_equal(got, orc.expected_allgather(world, chunk, SEED, 2))
+            else:
+                count = chunk // 2
+                host_in = [orc.bf16(world * count, SEED, g, 3) for g in range(world)]
+                got = np.empty(count, np.uint16)
+                c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, count * 2, 2, None))
+                c3.check(c3.lib().c3_stream_sync(None))
+                ok = np.array_equal(got, orc.reduce_scatter(host_in, rank, count))
+            results[strat] = (ok, t.total_ms)
+        s.close()
+        w.close()
+        d.close()
+        q.put((rank, results, None))
+    except Exception as e:  # report instead of hanging the parent
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("coll", [0, 2], ids=["all-gather", "reduce-scatter"])
+def test_two_processes_one_gpu(coll):
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, coll, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = [q.get(timeout=240) for _ in procs]
+    for p in procs:
+        p.join(timeout=60)
+    for rank, res, err in out:
+        assert err is None, f"rank {rank}: {err}"
+        for strat, (ok, ms) in res.items():
+            assert ok, f"rank {rank} strategy {strat} wrong output"
