@@ -152,8 +152,9 @@ def run_ours(args, dist):
     sess.fill(20241217)
     if not loopback:
         sess.set_barrier(dist.barrier)
+    tables = os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv")
+    sess.load_tables(tables)
     strategies = [c3.STRATEGY_NAMES.index(s) for s in args.strategies]
-    head = c3.STRATEGY_NAMES.index(args.strategy)
 
     def timed(strategy, steps, alloc=None):
         """steps runs; per-step device times, max over ranks."""
@@ -165,41 +166,58 @@ def run_ours(args, dist):
         flat = dist.max_list([v for r in rows for v in r])
         return [flat[i * 4:(i + 1) * 4] for i in range(steps)]
 
-    # isolated kernel times (outside the timed region), own-backend collectives
+    # isolated kernel times on the whole GPU (outside the timed region): the
+    # reference's t_gemm / t_comm (sim.cpp:136-138), per backend
     W, K = args.warmup, args.steps
+    full = world.info.sm_count
     timed(c3.GEMM_ONLY, W)
     t_g = median([r[1] for r in timed(c3.GEMM_ONLY, K)])
     iso_comm = {}
     for name, mode in (("cu", c3.COMM_ONLY_CU), ("dma", c3.COMM_ONLY_DMA)):
         a = sess.default_alloc(mode)
-        if mode == c3.COMM_ONLY_CU:
-            a.cus_comm = 32 if coll == c3.ALL_GATHER else 64  # comm_saturation_cus
+        a.cus_comm = full
         timed(mode, 2, a)
         iso_comm[name] = median([r[2] for r in timed(mode, K, a)])
+    dma_ok = not loopback  # same-device copies run on SMs
+
+    def summarise(name, rows, t_c):
+        t_conc = median([r[0] for r in rows])
+        sp = (t_g + t_c) / t_conc
+        ideal = c3.ideal_speedup(t_g, t_c)
+        best_c = min(iso_comm["cu"], iso_comm["dma"]) if dma_ok else iso_comm["cu"]
+        return {"t_concurrent_ms": t_conc, "t_comm_iso_ms": t_c, "speedup": sp, "ideal": ideal,
+                "fraction_of_ideal": c3.fraction_of_ideal(sp, ideal),
+                "speedup_vs_best_comm": (t_g + best_c) / t_conc,
+                "fraction_vs_best_comm": c3.fraction_of_ideal((t_g + best_c) / t_conc,
+                                                              c3.ideal_speedup(t_g, best_c)),
+                "gemm_ms_in_step": median([r[1] for r in rows])}
 
     results = {}
     for st in strategies:
         if st == c3.SERIAL:
             continue
-        timed(st, max(1, W // 2))
-        rows = timed(st, K)
-        t_conc = median([r[0] for r in rows])
-        backend = sess.default_alloc(st).backend
-        t_c = iso_comm["dma" if backend == c3.BACKEND_DMA else "cu"]
-        sp = (t_g + t_c) / t_conc
-        ideal = c3.ideal_speedup(t_g, t_c)
-        best_c = min(iso_comm.values())
-        results[c3.STRATEGY_NAMES[st]] = {
-            "t_concurrent_ms": t_conc, "t_comm_iso_ms": t_c, "speedup": sp, "ideal": ideal,
-            "fraction_of_ideal": c3.fraction_of_ideal(sp, ideal),
-            "speedup_vs_best_comm": (t_g + best_c) / t_conc,
-            "fraction_vs_best_comm": c3.fraction_of_ideal((t_g + best_c) / t_conc,
-                                                          c3.ideal_speedup(t_g, best_c)),
-            "gemm_ms_in_step": median([r[1] for r in rows])}
+        a = sess.default_alloc(st)
+        timed(st, max(1, W // 2), a)
+        res = summarise(c3.STRATEGY_NAMES[st], timed(st, K, a),
+                        iso_comm["dma" if a.backend == c3.BACKEND_DMA else "cu"])
+        res["alloc"] = {"cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm, "cus_idle": a.cus_idle,
+                        "backend": "DMA" if a.backend == c3.BACKEND_DMA else "CU"}
+        if a.backend == c3.BACKEND_DMA and loopback:
+            res["note"] = "loopback: same-device copies run on SMs, not copy engines"
+        results[c3.STRATEGY_NAMES[st]] = res
+
+    # the runtime heuristic's pick (model layer simulate() on measured tables)
+    if args.strategy == "auto":
+        head, head_alloc, predicted = sess.choose(t_g, iso_comm["cu"], iso_comm["dma"], dma_ok)
+    else:
+        head = c3.STRATEGY_NAMES.index(args.strategy)
+        head_alloc, predicted = sess.default_alloc(head), None
+    head_name = c3.STRATEGY_NAMES[head]
+    measured_best = max(results, key=lambda k: results[k]["speedup"]) if results else None
 
     # ---- the timed region: K steps of the headline strategy ----
     for _ in range(W):
-        sess.run(head)
+        sess.run(head, head_alloc)
     torch.cuda.synchronize()
     dist.barrier()
     clocks = ClockSampler(dist.local_rank) if dist.rank == 0 else None
@@ -207,7 +225,7 @@ def run_ours(args, dist):
         clocks.start()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rows = timed(head, K)
+    rows = timed(head, K, head_alloc)
     torch.cuda.synchronize()
     dist.barrier()
     wall = time.perf_counter() - t0
@@ -215,12 +233,18 @@ def run_ours(args, dist):
     step_ms = [r[0] for r in rows]
     gemm_ms = [r[1] for r in rows]
     launches = int(sum(r[3] for r in rows))
-    t_conc = median(step_ms)
-    backend = sess.default_alloc(head).backend
+    backend = head_alloc.backend
     t_c = iso_comm["dma" if backend == c3.BACKEND_DMA else "cu"]
-    speedup = (t_g + t_c) / t_conc
-    ideal = c3.ideal_speedup(t_g, t_c)
-    frac = c3.fraction_of_ideal(speedup, ideal)
+    head_res = summarise(head_name, rows, t_c)
+    t_conc = head_res["t_concurrent_ms"]
+    speedup, ideal, frac = head_res["speedup"], head_res["ideal"], head_res["fraction_of_ideal"]
+    choice = {"strategy": head_name, "selected_by": "runtime heuristic (c3_session_choose)"
+              if args.strategy == "auto" else "--strategy",
+              "alloc": {"cus_gemm": head_alloc.cus_gemm, "cus_comm": head_alloc.cus_comm,
+                        "cus_idle": head_alloc.cus_idle,
+                        "backend": "DMA" if backend == c3.BACKEND_DMA else "CU"},
+              "predicted_ms": predicted, "measured_ms": t_conc,
+              "measured_best_default_alloc": measured_best, "tables": os.path.relpath(tables, REPO)}
 
     # ---- e2e through the C ABI with host buffers ----
     p = sess.pointers(0)
@@ -236,7 +260,7 @@ def run_ours(args, dist):
         c3.check(L.c3_memcpy(p.a, pin_a.data_ptr(), p.a_bytes, 1, None))
         c3.check(L.c3_memcpy(p.send, pin_s.data_ptr(), p.send_bytes, 1, None))
         c3.check(L.c3_stream_sync(None))
-        sess.run(strategy)
+        sess.run(strategy, head_alloc if strategy == head else None)
         c3.check(L.c3_memcpy(pin_o.data_ptr(), p.c, d2h, 2, None))
         c3.check(L.c3_stream_sync(None))
         return (time.perf_counter() - t0) * 1e3
@@ -245,9 +269,21 @@ def run_ours(args, dist):
         e2e_step(head)
     e2e_conc = median(dist.max_list([e2e_step(head) for _ in range(K)]))
     e2e_g = median(dist.max_list([e2e_step(c3.GEMM_ONLY) for _ in range(K)]))
-    e2e_c = median(dist.max_list(
-        [e2e_step(c3.COMM_ONLY_DMA if backend == c3.BACKEND_DMA else c3.COMM_ONLY_CU)
-         for _ in range(K)]))
+    comm_mode = c3.COMM_ONLY_DMA if backend == c3.BACKEND_DMA else c3.COMM_ONLY_CU
+    comm_alloc = sess.default_alloc(comm_mode)
+    comm_alloc.cus_comm = full
+
+    def e2e_comm():
+        t0 = time.perf_counter()
+        c3.check(L.c3_memcpy(p.a, pin_a.data_ptr(), p.a_bytes, 1, None))
+        c3.check(L.c3_memcpy(p.send, pin_s.data_ptr(), p.send_bytes, 1, None))
+        c3.check(L.c3_stream_sync(None))
+        sess.run(comm_mode, comm_alloc)
+        c3.check(L.c3_memcpy(pin_o.data_ptr(), p.c, d2h, 2, None))
+        c3.check(L.c3_stream_sync(None))
+        return (time.perf_counter() - t0) * 1e3
+
+    e2e_c = median(dist.max_list([e2e_comm() for _ in range(K)]))
     # serial e2e = inputs in, GEMM, collective, result out (copies counted once)
     io_ms = e2e_g - t_g
     e2e_speedup = (e2e_g + e2e_c - io_ms) / e2e_conc
@@ -272,7 +308,8 @@ def run_ours(args, dist):
         "ms_per_step": sum(step_ms) / len(step_ms), "ms_per_step_median": t_conc,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16", "data": "synthetic (counter-hash bf16 U(-1,1)/8 and byte labels)",
-        "config": {"workload": f"{args.config}: {cfg['desc']}", "strategy": args.strategy,
+        "config": {"workload": f"{args.config}: {cfg['desc']}", "strategy": head_name,
+                   "strategy_choice": choice,
                    "collective": cfg["coll"], "payload_bytes": cfg["payload"],
                    "gemm_mnk": [cfg["m"], cfg["n"], cfg["k"]], "ranks": n,
                    "world": ("loopback: 8-rank collective emulated on 1 GPU (peer buffers in local "
@@ -363,7 +400,8 @@ def main():
     ap.add_argument("--steps", type=int, default=9)
     ap.add_argument("--warmup", type=int, default=6)
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
-    ap.add_argument("--strategy", default="conccl")
+    ap.add_argument("--strategy", default="auto",
+                    help="auto = the runtime heuristic's pick, or a strategy name")
     ap.add_argument("--strategies", default="c3_base,c3_sp,c3_rp,c3_sp_rp,conccl,conccl_rp")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -220,6 +220,16 @@ int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc,
  * the SM (P2P) collectives, which signal through peer flags on the device. */
 typedef int (*c3_barrier_fn)(void* ctx);
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
+/* Runtime heuristic (the paper's strategy choice, on the product model layer):
+ * load measured interference tables (reference SlowdownTable CSV,
+ * interference.hpp:57-61; data/b200-*-slowdown-tables.csv), then predict every
+ * strategy with simulate() (sim.hpp:70-73) from this GPU's measured isolated
+ * times and return the fastest (serial if nothing beats it) with its
+ * allocation. allow_dma = 0 excludes conccl/conccl_rp (e.g. loopback worlds,
+ * where same-device copies are SM copies). */
+int c3_session_load_tables(c3_session* s, const char* csv_path);
+int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, double t_comm_dma_ms,
+                      int allow_dma, int* strategy, c3_alloc* alloc, double* predicted_ms);
 /* The allocation c3_session_run uses for (strategy, alloc == NULL). */
 int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out);
 

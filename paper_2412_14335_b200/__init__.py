@@ -119,6 +119,16 @@ class Session:
         self._barrier_cb = _capi.BARRIER_FN(_cb)  # keep alive
         check(lib().c3_session_set_barrier(self.h, C.cast(self._barrier_cb, C.c_void_p), None))
 
+    def load_tables(self, csv_path):
+        check(lib().c3_session_load_tables(self.h, csv_path.encode()))
+
+    def choose(self, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms=0.0, allow_dma=True):
+        """Runtime heuristic: (strategy, alloc, predicted_ms)."""
+        st, a, pred = C.c_int(), _capi.Alloc(), C.c_double()
+        check(lib().c3_session_choose(self.h, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms,
+                                      int(bool(allow_dma)), C.byref(st), C.byref(a), C.byref(pred)))
+        return st.value, a, pred.value
+
     def default_alloc(self, strategy):
         a = _capi.Alloc()
         check(lib().c3_session_default_alloc(self.h, strategy, C.byref(a)))

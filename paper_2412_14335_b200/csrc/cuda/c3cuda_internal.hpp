@@ -64,11 +64,13 @@ struct GemmPlan {
     CUtensorMap map_a;
     CUtensorMap map_b;
     void* c = nullptr;
+    int* counters = nullptr;  // device [tile claims, CTA exits]; zero between launches
     int64_t m = 0, n = 0, k = 0;
+    int bn = 256;             // tile width: 256, or 128 when tiles are scarce
     int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;
 };
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k);
+                   int64_t k, int* counters, int sm_count);
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream);
 
 // ------------------------------------------------------------ collectives

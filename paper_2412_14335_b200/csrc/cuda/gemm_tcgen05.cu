@@ -1,23 +1,33 @@
-// Persistent bf16 GEMM for sm_100a: TMA -> shared memory (4-stage mbarrier
-// ring) -> tcgen05.mma (single-thread issue, fp32 accumulators in TMEM,
-// double-buffered) -> tcgen05.ld epilogue -> bf16 global stores.
+// Persistent bf16 GEMM for sm_100a: TMA -> shared memory (mbarrier ring) ->
+// tcgen05.mma (single-thread issue, fp32 accumulators in TMEM, double
+// buffered) -> tcgen05.ld epilogue -> bf16 global stores.
 //
 //   C[M,N] = A[M,K] * B[N,K]^T      (A, B K-major bf16; C row-major bf16)
 //
 // This is the "compute" half of a C3 pair (reference GemmKernel,
 // /root/reference/proj/include/c3sim/workload.hpp:18-25; its cost model
 // roofline_gemm_time, src/workload.cpp:72-78). The grid is capped at
-// `max_ctas` CTAs (one per SM, persistent over output tiles): the B200
-// counterpart of the paper's CU allocation to the GEMM (allocate_cus
-// cus_gemm, src/sim.cpp:40-100) and of ConCCL_rp's idle grain
-// (src/strategy.cpp:96-113).
+// `max_ctas` CTAs (one per SM): the B200 counterpart of the paper's CU
+// allocation to the GEMM (allocate_cus cus_gemm, src/sim.cpp:40-100) and of
+// ConCCL_rp's idle grain (src/strategy.cpp:96-113).
 //
-// Warp roles (256 threads): warp 0 = TMA producer (one thread), warp 1 = MMA
-// issuer (one thread), warp 2 = TMEM allocator, warps 4..7 = epilogue (warp
-// 4+q reads TMEM lanes 32q..32q+31, i.e. output rows 32q.. of the tile).
+// Tiles are CLAIMED dynamically (global atomic counter, claimed by the TMA
+// warp a few k-blocks before the MMA needs them, handed to the MMA and
+// epilogue warps through a small shared-memory ring). Under C3 a co-running
+// collective slows some SMs more than others (co-resident comm CTAs, HBM
+// contention); with static round-robin tiles the slowest CTA sets the GEMM's
+// end, with claiming the other SMs absorb the work (measured: profiles/
+// r01_strategy_grid_*.json).
+//
+// Warp roles (256 threads): warp 0 = tile claimer + TMA producer (one
+// thread), warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator,
+// warps 4..7 = epilogue (warp 4+q reads TMEM lanes 32q..32q+31 = tile rows).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
+
+#include <cstdlib>
+#include <string>
 
 #include "c3cuda_internal.hpp"
 #include "ptx.cuh"
@@ -27,25 +37,30 @@ namespace c3k {
 namespace gemm {
 
 constexpr int BM = 128;          // UMMA M (one CTA)
-constexpr int BN = 256;          // UMMA N
 constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
 constexpr int UK = 16;           // UMMA K for 16-bit inputs
-constexpr int STAGES = 4;
 constexpr int ACC_BUFS = 2;
-constexpr uint32_t TMEM_COLS = 512;  // ACC_BUFS x BN fp32 columns
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;      // tile raster: 16 M-tiles per band for L2 reuse
+constexpr int TILE_RING = 4;     // claimed-tile hand-off depth
 
-constexpr uint32_t A_STAGE_BYTES = BM * BK * 2;   // 16 KiB
-constexpr uint32_t B_STAGE_BYTES = BN * BK * 2;   // 32 KiB
-constexpr uint32_t STAGE_BYTES = A_STAGE_BYTES + B_STAGE_BYTES;
-constexpr uint32_t SMEM_BYTES = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+template <int BN>
+struct Cfg {
+    static constexpr int STAGES = BN == 256 ? 4 : 6;
+    static constexpr uint32_t A_STAGE = BM * BK * 2;
+    static constexpr uint32_t B_STAGE = BN * BK * 2;
+    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+    static constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;  // 512 or 256
+    static constexpr uint32_t SMEM = STAGES * STAGE + 1024 /*align*/ + 512 /*barriers, ring*/;
+};
 
 struct Params {
     int m, n, k;
     int tiles_m, tiles_n, num_tiles, k_blocks;
     __nv_bfloat16* c;
     int ldc;
+    int* tile_counter;  // claims; reset to 0 by the last CTA to exit
+    int* exit_counter;
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
@@ -57,21 +72,27 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
     tn = in_band / rows;
 }
 
+template <int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, const Params p) {
+    using K = Cfg<BN>;
+    constexpr int STAGES = K::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms.
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
     uint8_t* smem_a = smem;
-    uint8_t* smem_b = smem + STAGES * A_STAGE_BYTES;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-    uint64_t* full = bars;                       // [STAGES]  TMA -> MMA
-    uint64_t* empty = bars + STAGES;             // [STAGES]  MMA -> TMA
+    uint8_t* smem_b = smem + STAGES * K::A_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * K::STAGE);
+    uint64_t* full = bars;                       // [STAGES]   TMA -> MMA
+    uint64_t* empty = bars + STAGES;             // [STAGES]   MMA -> TMA
     uint64_t* acc_full = bars + 2 * STAGES;      // [ACC_BUFS] MMA -> epilogue
     uint64_t* acc_empty = acc_full + ACC_BUFS;   // [ACC_BUFS] epilogue -> MMA
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + ACC_BUFS);
+    uint64_t* tile_full = acc_empty + ACC_BUFS;  // [TILE_RING] claimer -> MMA, epilogue
+    uint64_t* tile_empty = tile_full + TILE_RING;
+    int* tile_ring = reinterpret_cast<int*>(tile_empty + TILE_RING);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + TILE_RING);
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -87,32 +108,48 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_init(&acc_full[b], 1);
             mbar_init(&acc_empty[b], 128);
         }
+        for (int r = 0; r < TILE_RING; ++r) {
+            mbar_init(&tile_full[r], 1);
+            mbar_init(&tile_empty[r], 1 + 4);  // MMA thread + one lane per epilogue warp
+        }
         fence_mbar_init();
     }
-    if (warp == 2) tmem_alloc<TMEM_COLS>(tmem_slot);
+    if (warp == 2) tmem_alloc<K::TMEM_COLS>(tmem_slot);
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 
     if (warp == 0 && lane == 0) {
-        // ---------------- TMA producer ----------------
+        // ---------------- tile claimer + TMA producer ----------------
         const uint64_t keep = policy_evict_last();
         int stage = 0;
         uint32_t phase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        // dynamic claiming, or static round-robin when no counter is given
+        const bool dyn = p.tile_counter != nullptr;
+        int tile = dyn ? atomicAdd(p.tile_counter, 1) : static_cast<int>(blockIdx.x);
+        for (int i = 0;; ++i) {
+            const int r = i % TILE_RING;
+            if (tile >= p.num_tiles) tile = -1;
+            mbar_wait(&tile_empty[r], ((i / TILE_RING) & 1) ^ 1);
+            tile_ring[r] = tile;
+            mbar_arrive(&tile_full[r]);  // release: consumers read tile_ring[r] after their wait
+            if (tile < 0) break;
+            // claim the next tile now; its round trip overlaps this tile's loads
+            const int next = dyn ? atomicAdd(p.tile_counter, 1) : tile + static_cast<int>(gridDim.x);
             int tm, tn;
             tile_coords(p, tile, tm, tn);
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
-                mbar_arrive_expect_tx(&full[stage], STAGE_BYTES);
-                tma_load_2d(smem_a + stage * A_STAGE_BYTES, &map_a, &full[stage], kb * BK, tm * BM, keep);
-                tma_load_2d(smem_b + stage * B_STAGE_BYTES, &map_b, &full[stage], kb * BK, tn * BN, keep);
+                mbar_arrive_expect_tx(&full[stage], K::STAGE);
+                tma_load_2d(smem_a + stage * K::A_STAGE, &map_a, &full[stage], kb * BK, tm * BM, keep);
+                tma_load_2d(smem_b + stage * K::B_STAGE, &map_b, &full[stage], kb * BK, tn * BN, keep);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
                 }
             }
+            tile = next;
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
@@ -122,15 +159,20 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
         uint32_t phase = 0;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int i = 0;; ++i) {
+            const int r = i % TILE_RING;
+            mbar_wait(&tile_full[r], (i / TILE_RING) & 1);
+            const int tile = tile_ring[r];
+            mbar_arrive(&tile_empty[r]);
+            if (tile < 0) break;
             mbar_wait(&acc_empty[acc], acc_phase ^ 1);
             tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
-                const uint32_t a_addr = a0 + stage * A_STAGE_BYTES;
-                const uint32_t b_addr = b0 + stage * B_STAGE_BYTES;
+                const uint32_t a_addr = a0 + stage * K::A_STAGE;
+                const uint32_t b_addr = b0 + stage * K::B_STAGE;
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k) {
                     // advancing K inside the 128-byte swizzle atom = +32 B per UMMA_K
@@ -155,7 +197,13 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
         const int row_in_tile = q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
-        for (int tile = blockIdx.x; tile < p.num_tiles; tile += gridDim.x) {
+        for (int i = 0;; ++i) {
+            const int r = i % TILE_RING;
+            mbar_wait(&tile_full[r], (i / TILE_RING) & 1);
+            const int tile = tile_ring[r];
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tile_empty[r]);
+            if (tile < 0) break;
             int tm, tn;
             tile_coords(p, tile, tm, tn);
             mbar_wait(&acc_full[acc], acc_phase);
@@ -207,7 +255,17 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
     __syncthreads();
     if (warp == 2) {
         tc_fence_after();
-        tmem_dealloc<TMEM_COLS>(tmem_base);
+        tmem_dealloc<K::TMEM_COLS>(tmem_base);
+    }
+    // Last CTA out resets the claim counter for the next launch (every CTA's
+    // claimer has drawn its terminal ticket before its CTA reaches here).
+    if (threadIdx.x == 0 && p.tile_counter != nullptr) {
+        __threadfence();
+        if (atomicAdd(p.exit_counter, 1) == static_cast<int>(gridDim.x) - 1) {
+            *p.tile_counter = 0;
+            *p.exit_counter = 0;
+            __threadfence();
+        }
     }
 }
 
@@ -225,49 +283,22 @@ CUresult encode_kmajor_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, ui
     const cuuint32_t estr[2] = {1, 1};
     if (!drv().TensorMapEncodeTiled) return CUDA_ERROR_NOT_SUPPORTED;
     return drv().TensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
-                                  dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                  CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                                      dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                      CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-}  // namespace
-
-int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k) {
-    if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
-    if (k % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: K must be a multiple of 8 (16-byte rows)");
-    if (n % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: N must be a multiple of 8 (16-byte rows)");
-    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
-        return set_error(C3_ERR_VALIDATION, "gemm: operands must be 16-byte aligned");
-    if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
-        return set_error(C3_ERR_VALIDATION, "gemm: dimension too large");
-    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), gemm::BM);
-    if (r == CUDA_SUCCESS)
-        r = encode_kmajor_bf16(&plan->map_b, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), gemm::BN);
-    if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
-    plan->m = m;
-    plan->n = n;
-    plan->k = k;
-    plan->c = C;
-    plan->tiles_m = static_cast<int>((m + gemm::BM - 1) / gemm::BM);
-    plan->tiles_n = static_cast<int>((n + gemm::BN - 1) / gemm::BN);
-    plan->num_tiles = plan->tiles_m * plan->tiles_n;
-    plan->k_blocks = static_cast<int>((k + gemm::BK - 1) / gemm::BK);
-    return C3_OK;
-}
-
-int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream) {
+template <int BN>
+int launch_bn(const GemmPlan* plan, int grid, cudaStream_t stream) {
+    using K = gemm::Cfg<BN>;
     static bool attr_done = false;
     if (!attr_done) {
-        cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel,
-                                             cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             static_cast<int>(gemm::SMEM_BYTES));
+        const cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel<BN>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(K::SMEM));
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
         attr_done = true;
     }
-    int grid = max_ctas > 0 ? max_ctas : sm_count;
-    grid = std::min(grid, sm_count);
-    grid = std::min(grid, plan->num_tiles);
     gemm::Params p;
     p.m = static_cast<int>(plan->m);
     p.n = static_cast<int>(plan->n);
@@ -278,11 +309,56 @@ int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStrea
     p.k_blocks = plan->k_blocks;
     p.c = static_cast<__nv_bfloat16*>(plan->c);
     p.ldc = static_cast<int>(plan->n);
-    gemm::gemm_bf16_tn_kernel<<<grid, gemm::THREADS, gemm::SMEM_BYTES, stream>>>(plan->map_a,
-                                                                                 plan->map_b, p);
+    static const bool static_sched = [] {
+        const char* e = std::getenv("C3_GEMM_SCHED");  // development A/B switch
+        return e != nullptr && std::string(e) == "static";
+    }();
+    p.tile_counter = static_sched ? nullptr : plan->counters;
+    p.exit_counter = plan->counters + 1;
+    gemm::gemm_bf16_tn_kernel<BN><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, plan->map_b, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
     return C3_OK;
+}
+
+}  // namespace
+
+int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
+                   int64_t k, int* counters, int sm_count) {
+    if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
+    if (k % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: K must be a multiple of 8 (16-byte rows)");
+    if (n % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: N must be a multiple of 8 (16-byte rows)");
+    if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
+        return set_error(C3_ERR_VALIDATION, "gemm: operands must be 16-byte aligned");
+    if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
+        return set_error(C3_ERR_VALIDATION, "gemm: dimension too large");
+    if (!counters) return set_error(C3_ERR_VALIDATION, "gemm: missing tile-claim counters");
+    // Wide 128x256 tiles unless that leaves fewer than two tiles per SM, where
+    // 128x128 tiles cut the last-wave loss (e.g. M=128: 208 -> 416 tiles).
+    const int64_t tm = (m + gemm::BM - 1) / gemm::BM;
+    plan->bn = tm * ((n + 255) / 256) < 2 * static_cast<int64_t>(std::max(sm_count, 1)) ? 128 : 256;
+    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), gemm::BM);
+    if (r == CUDA_SUCCESS)
+        r = encode_kmajor_bf16(&plan->map_b, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k),
+                               static_cast<uint32_t>(plan->bn));
+    if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
+    plan->m = m;
+    plan->n = n;
+    plan->k = k;
+    plan->c = C;
+    plan->counters = counters;
+    plan->tiles_m = static_cast<int>(tm);
+    plan->tiles_n = static_cast<int>((n + plan->bn - 1) / plan->bn);
+    plan->num_tiles = plan->tiles_m * plan->tiles_n;
+    plan->k_blocks = static_cast<int>((k + gemm::BK - 1) / gemm::BK);
+    return C3_OK;
+}
+
+int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream) {
+    int grid = max_ctas > 0 ? max_ctas : sm_count;
+    grid = std::min(grid, sm_count);
+    grid = std::min(grid, plan->num_tiles);
+    return plan->bn == 128 ? launch_bn<128>(plan, grid, stream) : launch_bn<256>(plan, grid, stream);
 }
 
 }  // namespace c3k

@@ -93,7 +93,10 @@ struct c3_world {
     std::vector<cudaEvent_t> ce_events;
     cudaEvent_t fork_event = nullptr;
     std::map<int, GreenPartition> partitions;  // keyed by requested comm SMs
+    int* gemm_counters = nullptr;              // pool for standalone c3_gemm_bf16 calls
+    int gemm_counter_next = 0;
 };
+static constexpr int kGemmCounterSlots = 64;
 
 namespace {
 
@@ -255,6 +258,7 @@ struct c3_session {
     int n = 1;              // collective ranks
     int64_t chunk = 0;      // payload / n (bytes)
     GemmPlan gemm;
+    int* gemm_counters = nullptr;
     void *a = nullptr, *b = nullptr, *c = nullptr;
     // per virtual rank: AG recv (payload, own chunk in place); RS in (payload),
     // out (chunk), staging (payload)
@@ -286,7 +290,10 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaMalloc(&s->a, static_cast<size_t>(d.m * d.k * 2)));
     C3_CUDA(cudaMalloc(&s->b, static_cast<size_t>(d.n * d.k * 2)));
     C3_CUDA(cudaMalloc(&s->c, static_cast<size_t>(d.m * d.n * 2)));
-    C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k));
+    C3_CUDA(cudaMalloc(&s->gemm_counters, 2 * sizeof(int)));
+    C3_CUDA(cudaMemset(s->gemm_counters, 0, 2 * sizeof(int)));
+    C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k, s->gemm_counters,
+                          s->w->prop.multiProcessorCount));
     const size_t payload = static_cast<size_t>(d.payload_bytes);
     for (int v = 0; v < s->vr; ++v) {
         void* p = nullptr;
@@ -453,6 +460,9 @@ int c3_world_create(int rank, int n_ranks, int device, int loopback, c3_world** 
         drv().DeviceGet(&w->cu_dev, device) != CUDA_SUCCESS)
         return fail(set_error(C3_ERR_DRIVER, "cuInit/cuDeviceGet failed"));
     w->green_ok = probe_green(w);
+    e = cudaMalloc(&w->gemm_counters, 2 * kGemmCounterSlots * sizeof(int));
+    if (e == cudaSuccess) e = cudaMemset(w->gemm_counters, 0, 2 * kGemmCounterSlots * sizeof(int));
+    if (e != cudaSuccess) return fail(set_cuda_error(e, "cudaMalloc(gemm counters)"));
     *out = w;
     return C3_OK;
 }
@@ -469,6 +479,7 @@ int c3_world_destroy(c3_world* w) {
     for (auto s : w->ce_streams) cudaStreamDestroy(s);
     for (auto e : w->ce_events) cudaEventDestroy(e);
     if (w->fork_event) cudaEventDestroy(w->fork_event);
+    if (w->gemm_counters) cudaFree(w->gemm_counters);
     delete w;
     return C3_OK;
 }
@@ -557,7 +568,9 @@ int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, 
                  int64_t k, int max_ctas, void* stream) {
     if (!w) return set_error(C3_ERR_VALIDATION, "c3_gemm_bf16: null world");
     GemmPlan plan;
-    C3_TRY(gemm_plan_init(&plan, A, B, C, m, n, k));
+    // round-robin claim-counter pairs: up to kGemmCounterSlots GEMMs in flight
+    int* ctr = w->gemm_counters + 2 * (w->gemm_counter_next++ % kGemmCounterSlots);
+    C3_TRY(gemm_plan_init(&plan, A, B, C, m, n, k, ctr, w->prop.multiProcessorCount));
     return gemm_plan_launch(&plan, max_ctas, w->prop.multiProcessorCount,
                             static_cast<cudaStream_t>(stream));
 }
@@ -701,7 +714,8 @@ int c3_session_destroy(c3_session* s) {
     for (void* p : s->imported) cudaIpcCloseMemHandle(p);
     for (auto* v : {&s->recv, &s->in, &s->out, &s->staging})
         for (void* p : *v) cudaFree(p);
-    for (void* p : {s->a, s->b, s->c, static_cast<void*>(s->sig), static_cast<void*>(s->done)})
+    for (void* p : {s->a, s->b, s->c, static_cast<void*>(s->sig), static_cast<void*>(s->done),
+                    static_cast<void*>(s->gemm_counters)})
         if (p) cudaFree(p);
     for (cudaStream_t st : {s->main, s->gemm_s, s->comm_s, s->comm_hi})
         if (st) cudaStreamDestroy(st);
@@ -802,6 +816,72 @@ int c3_session_import(c3_session* s, const void* all) {
     }
     s->ready = true;
     return C3_OK;
+}
+
+int c3_session_load_tables(c3_session* s, const char* csv_path) {
+    if (!s || !csv_path) return set_error(C3_ERR_VALIDATION, "c3_session_load_tables: null argument");
+    return guarded([&] {
+        s->tables = c3sim::load_slowdown_tables(csv_path, s->md.min_cu_grain);
+        return C3_OK;
+    });
+}
+
+// Runtime strategy heuristic: predict every strategy's makespan with the
+// model layer's simulate() (sim.cpp:121-215) fed with this GPU's measured
+// isolated times (GemmKernel/CollectiveOp::measured_time, workload.hpp:23,34)
+// and the loaded (measured) interference tables; rp splits come from
+// partition_heuristic (strategy.cpp:48-94). The DMA backend's link bandwidth
+// is set so that plan_cost reproduces the measured copy-engine time. Serial
+// wins when no concurrent strategy is predicted to beat it.
+int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, double t_comm_dma_ms,
+                      int allow_dma, int* strategy, c3_alloc* alloc, double* predicted_ms) {
+    if (!s || !strategy || !alloc || !predicted_ms)
+        return set_error(C3_ERR_VALIDATION, "c3_session_choose: null argument");
+    if (!(t_gemm_ms > 0 && t_comm_cu_ms > 0))
+        return set_error(C3_ERR_VALIDATION, "c3_session_choose: isolated times must be positive");
+    return guarded([&] {
+        c3sim::EfficiencyParams eff;
+        eff.comm_launch_overhead_cu = 0.0;  // measured times include launch
+        const c3sim::CoRunPenalty pen = c3sim::CoRunPenalty::ones();
+        c3sim::C3Scenario sc = s->scenario;
+        sc.gemm.measured_time = t_gemm_ms * 1e-3;
+        sc.gemm.boundedness_override =
+            c3sim::classify_gemm_boundedness(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
+        double best = (t_gemm_ms + std::min(t_comm_cu_ms, allow_dma && t_comm_dma_ms > 0
+                                                               ? t_comm_dma_ms : t_comm_cu_ms)) * 1e-3;
+        int best_st = C3_SERIAL;
+        for (int st = C3_C3_BASE; st <= C3_CONCCL_RP; ++st) {
+            const bool dma = st == C3_CONCCL || st == C3_CONCCL_RP;
+            if (dma && (!allow_dma || !(t_comm_dma_ms > 0))) continue;
+            c3sim::C3Scenario x = sc;
+            x.collective.measured_time = (dma ? t_comm_dma_ms : t_comm_cu_ms) * 1e-3;
+            c3sim::MachineDescriptor md = s->md;
+            if (dma && s->chunk > 0) {
+                md.cpu_launch_overhead = 0.0;
+                md.dma_sync_overhead = 0.0;
+                md.link_bandwidth_unidir = static_cast<double>(s->chunk) /
+                                           (eff.efficiency * t_comm_dma_ms * 1e-3);
+            }
+            const c3sim::SimTimeline tl =
+                c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff);
+            if (tl.makespan < best) {
+                best = tl.makespan;
+                best_st = st;
+            }
+        }
+        *strategy = best_st;
+        *predicted_ms = best * 1e3;
+        c3sim::C3Scenario x = sc;
+        x.collective.measured_time = t_comm_cu_ms * 1e-3;
+        const c3sim::Allocation a =
+            c3sim::allocate_cus(x, static_cast<c3sim::Strategy>(best_st), s->md, s->tables, eff);
+        alloc->cus_gemm = a.cus_gemm;
+        alloc->cus_comm = best_st == C3_SERIAL ? 32 : a.cus_comm;
+        alloc->cus_idle = a.cus_idle;
+        alloc->backend = a.comm_backend == c3sim::CommBackend::DMA ? C3_BACKEND_DMA : C3_BACKEND_CU;
+        alloc->comm_first = a.comm_first ? 1 : 0;
+        return C3_OK;
+    });
 }
 
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
