@@ -61,13 +61,15 @@ int set_driver_error(CUresult r, const char* what);
 
 // ------------------------------------------------------------------- GEMM
 struct GemmPlan {
-    CUtensorMap map_a;
-    CUtensorMap map_b;
+    enum Kind { kWide = 0, kNarrow = 1, kPair = 2 };  // 128x256, 128x128, pair 256x256
+    CUtensorMap map_a;     // 128-row boxes
+    CUtensorMap map_b128;  // 128-row boxes (pair half tile, narrow kernel)
+    CUtensorMap map_b256;  // 256-row boxes (wide kernel)
     void* c = nullptr;
     int* counters = nullptr;  // device [tile claims, CTA exits]; zero between launches
     int64_t m = 0, n = 0, k = 0;
-    int bn = 256;             // tile width: 256, or 128 when tiles are scarce
-    int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;
+    Kind kind = kWide;
+    int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;  // of the chosen kernel
 };
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
                    int64_t k, int* counters, int sm_count);

@@ -289,7 +289,7 @@ CUresult encode_kmajor_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, ui
 }
 
 template <int BN>
-int launch_bn(const GemmPlan* plan, int grid, cudaStream_t stream) {
+int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStream_t stream) {
     using K = gemm::Cfg<BN>;
     static bool attr_done = false;
     if (!attr_done) {
@@ -303,9 +303,9 @@ int launch_bn(const GemmPlan* plan, int grid, cudaStream_t stream) {
     p.m = static_cast<int>(plan->m);
     p.n = static_cast<int>(plan->n);
     p.k = static_cast<int>(plan->k);
-    p.tiles_m = plan->tiles_m;
-    p.tiles_n = plan->tiles_n;
-    p.num_tiles = plan->num_tiles;
+    p.tiles_m = static_cast<int>((plan->m + gemm::BM - 1) / gemm::BM);
+    p.tiles_n = static_cast<int>((plan->n + BN - 1) / BN);
+    p.num_tiles = p.tiles_m * p.tiles_n;
     p.k_blocks = plan->k_blocks;
     p.c = static_cast<__nv_bfloat16*>(plan->c);
     p.ldc = static_cast<int>(plan->n);
@@ -315,13 +315,16 @@ int launch_bn(const GemmPlan* plan, int grid, cudaStream_t stream) {
     }();
     p.tile_counter = static_sched ? nullptr : plan->counters;
     p.exit_counter = plan->counters + 1;
-    gemm::gemm_bf16_tn_kernel<BN><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, plan->map_b, p);
+    grid = std::min(grid, p.num_tiles);
+    gemm::gemm_bf16_tn_kernel<BN><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, map_b, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
     return C3_OK;
 }
 
 }  // namespace
+
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream);
 
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
                    int64_t k, int* counters, int sm_count) {
@@ -333,32 +336,50 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
         return set_error(C3_ERR_VALIDATION, "gemm: dimension too large");
     if (!counters) return set_error(C3_ERR_VALIDATION, "gemm: missing tile-claim counters");
-    // Wide 128x256 tiles unless that leaves fewer than two tiles per SM, where
-    // 128x128 tiles cut the last-wave loss (e.g. M=128: 208 -> 416 tiles).
-    const int64_t tm = (m + gemm::BM - 1) / gemm::BM;
-    plan->bn = tm * ((n + 255) / 256) < 2 * static_cast<int64_t>(std::max(sm_count, 1)) ? 128 : 256;
-    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), gemm::BM);
+    // Kernel choice: CTA-pair 256x256 tiles when there is at least one pair
+    // tile per SM pair; else single-CTA 128x256 tiles, or 128x128 when that
+    // leaves fewer than two tiles per SM (e.g. M=128: 208 -> 416 tiles).
+    const int64_t sms = std::max(sm_count, 2);
+    const int64_t tm1 = (m + 127) / 128;
+    const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
+    plan->kind = m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
+                 : tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow
+                                                     : GemmPlan::kWide;
+    if (const char* f = std::getenv("C3_GEMM_KERNEL")) {  // tests force each variant
+        const std::string v(f);
+        if (v == "pair") plan->kind = GemmPlan::kPair;
+        if (v == "wide") plan->kind = GemmPlan::kWide;
+        if (v == "narrow") plan->kind = GemmPlan::kNarrow;
+    }
+    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), 128);
+    if (r == CUDA_SUCCESS)  // 128-row B boxes: the pair kernel's half tile and the narrow kernel
+        r = encode_kmajor_bf16(&plan->map_b128, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 128);
     if (r == CUDA_SUCCESS)
-        r = encode_kmajor_bf16(&plan->map_b, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k),
-                               static_cast<uint32_t>(plan->bn));
+        r = encode_kmajor_bf16(&plan->map_b256, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 256);
     if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
     plan->m = m;
     plan->n = n;
     plan->k = k;
     plan->c = C;
     plan->counters = counters;
-    plan->tiles_m = static_cast<int>(tm);
-    plan->tiles_n = static_cast<int>((n + plan->bn - 1) / plan->bn);
-    plan->num_tiles = plan->tiles_m * plan->tiles_n;
     plan->k_blocks = static_cast<int>((k + gemm::BK - 1) / gemm::BK);
+    const int bm = plan->kind == GemmPlan::kPair ? 256 : 128;
+    const int bn = plan->kind == GemmPlan::kNarrow ? 128 : 256;
+    plan->tiles_m = static_cast<int>((m + bm - 1) / bm);
+    plan->tiles_n = static_cast<int>((n + bn - 1) / bn);
+    plan->num_tiles = plan->tiles_m * plan->tiles_n;
     return C3_OK;
 }
 
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream) {
     int grid = max_ctas > 0 ? max_ctas : sm_count;
     grid = std::min(grid, sm_count);
-    grid = std::min(grid, plan->num_tiles);
-    return plan->bn == 128 ? launch_bn<128>(plan, grid, stream) : launch_bn<256>(plan, grid, stream);
+    if (plan->kind == GemmPlan::kPair && grid >= 2) {
+        grid = std::min(grid / 2, plan->num_tiles) * 2;  // whole CTA pairs
+        return gemm_pair_launch(plan, grid, stream);
+    }
+    if (plan->kind == GemmPlan::kWide) return launch_bn<256>(plan, plan->map_b256, grid, stream);
+    return launch_bn<128>(plan, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap
 }
 
 }  // namespace c3k

@@ -1,0 +1,308 @@
+// CTA-pair variant of the persistent bf16 GEMM (tcgen05 cta_group::2).
+//
+// A cluster of two CTAs on one TPC computes a 256 x 256 output tile. Each CTA
+// TMA-loads its own 128 rows of A and its half (128 rows) of the tile's B
+// rows; the even ("leader") CTA issues tcgen05.mma.cta_group::2 with M = 256,
+// which reads A and B from BOTH CTAs' shared memory (identical offsets) and
+// accumulates each CTA's 128 rows x 256 columns into that CTA's own TMEM.
+// Versus the single-CTA 128 x 256 tile this halves the B bytes each SM pulls
+// from L2 per MMA (32 KiB instead of 48 KiB per 64-deep k-block): the
+// single-CTA kernel's tensor pipe sat at 88% with ~2.9 GB of DRAM traffic
+// per cfg2 launch (profiles/ncu_gemm_summary.json).
+//
+// Synchronisation (all mbarriers, no __syncthreads in the main loop):
+//   full[s]     leader only; leader arms expect_tx(2 x stage bytes), both CTAs'
+//               TMA loads complete_tx on it (peer bit of the address cleared)
+//   empty[s]    both CTAs; the leader's tcgen05.commit multicasts to both
+//   acc_full[b] both CTAs; multicast commit after a tile's last k-block
+//   acc_empty[b] leader; 4 local + 4 remote epilogue-warp arrivals
+//   tile ring   leader claims tiles (global atomic, one tile ahead), writes
+//               the id into both CTAs' rings (st.shared::cluster) and arrives
+//               on both tile_full; consumers of both CTAs release the slot on
+//               the leader's tile_empty (1 MMA + 4 + 1 peer producer + 4).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "c3cuda_internal.hpp"
+#include "ptx.cuh"
+
+namespace c3k {
+namespace gemm2 {
+
+constexpr int BM = 256;        // pair tile rows (128 per CTA)
+constexpr int BN = 256;        // pair tile cols (B: 128 rows per CTA)
+constexpr int BK = 64;
+constexpr int UK = 16;
+constexpr int STAGES = 6;
+constexpr int ACC_BUFS = 2;
+constexpr int THREADS = 256;
+constexpr int GROUP_M = 8;     // 8 pair-rows (2048 rows of A) per raster band
+constexpr int RING = 4;
+constexpr uint32_t A_STAGE = 128 * BK * 2;  // this CTA's 128 rows of A
+constexpr uint32_t B_STAGE = 128 * BK * 2;  // this CTA's 128 rows of B
+constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;
+constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 512;
+
+struct Params {
+    int m, n, k;
+    int tiles_m, tiles_n, num_tiles, k_blocks;
+    __nv_bfloat16* c;
+    int ldc;
+    int* tile_counter;
+    int* exit_counter;
+};
+
+__device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
+    const int band = GROUP_M * p.tiles_n;
+    const int first_m = (tile / band) * GROUP_M;
+    const int rows = min(p.tiles_m - first_m, GROUP_M);
+    const int in_band = tile % band;
+    tm = first_m + in_band % rows;
+    tn = in_band / rows;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
+                         const __grid_constant__ CUtensorMap map_b, const Params p) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = reinterpret_cast<uint8_t*>(
+        (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
+    uint8_t* smem_a = smem;
+    uint8_t* smem_b = smem + STAGES * A_STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
+    uint64_t* full = bars;
+    uint64_t* empty = bars + STAGES;
+    uint64_t* acc_full = bars + 2 * STAGES;
+    uint64_t* acc_empty = acc_full + ACC_BUFS;
+    uint64_t* tile_full = acc_empty + ACC_BUFS;
+    uint64_t* tile_empty = tile_full + RING;
+    int* tile_ring = reinterpret_cast<int*>(tile_empty + RING);
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + RING);
+
+    const int warp = threadIdx.x / 32;
+    const int lane = threadIdx.x % 32;
+    const uint32_t rank = cluster_ctarank();
+    const bool leader = rank == 0;
+
+    if (warp == 0 && lane == 0) {
+        tma_prefetch_desc(&map_a);
+        tma_prefetch_desc(&map_b);
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < ACC_BUFS; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 8);
+        }
+        for (int r = 0; r < RING; ++r) {
+            mbar_init(&tile_full[r], 1);
+            mbar_init(&tile_empty[r], 10);
+        }
+        fence_mbar_init();
+    }
+    if (warp == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
+    tc_fence_before();
+    cluster_sync();  // barrier inits and TMEM allocation visible across the pair
+    tc_fence_after();
+    const uint32_t tmem_base = *tmem_slot;
+
+    if (warp == 0 && lane == 0) {
+        // ------------- tile claims (leader) + TMA producer (both CTAs) -------------
+        const uint64_t keep = policy_evict_last();
+        int stage = 0;
+        uint32_t phase = 0;
+        int tile = leader ? atomicAdd(p.tile_counter, 1) : 0;
+        for (int i = 0;; ++i) {
+            const int r = i % RING;
+            const uint32_t par = (i / RING) & 1;
+            if (leader) {
+                if (tile >= p.num_tiles) tile = -1;
+                mbar_wait(&tile_empty[r], par ^ 1);
+                tile_ring[r] = tile;
+                st_cluster_u32(mapa(smem_u32(&tile_ring[r]), 1), static_cast<uint32_t>(tile));
+                mbar_arrive(&tile_full[r]);
+                mbar_arrive_cluster(mapa(smem_u32(&tile_full[r]), 1));
+            } else {
+                mbar_wait_cluster(&tile_full[r], par);
+                tile = tile_ring[r];
+                mbar_arrive_cluster(mapa(smem_u32(&tile_empty[r]), 0));
+            }
+            if (tile < 0) break;
+            const int next = leader ? atomicAdd(p.tile_counter, 1) : 0;
+            int tm, tn;
+            tile_coords(p, tile, tm, tn);
+            const int a_row = tm * BM + static_cast<int>(rank) * 128;
+            const int b_row = tn * BN + static_cast<int>(rank) * 128;
+            for (int kb = 0; kb < p.k_blocks; ++kb) {
+                mbar_wait(&empty[stage], phase ^ 1);
+                if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
+                tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, keep);
+                tma_load_2d_pair(smem_b + stage * B_STAGE, &map_b, &full[stage], kb * BK, b_row, keep);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            tile = next;
+        }
+    } else if (warp == 1 && lane == 0 && leader) {
+        // ------------- MMA issuer (leader only) -------------
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+        const uint32_t a0 = smem_u32(smem_a), b0 = smem_u32(smem_b);
+        int stage = 0;
+        uint32_t phase = 0;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int i = 0;; ++i) {
+            const int r = i % RING;
+            mbar_wait(&tile_full[r], (i / RING) & 1);
+            const int tile = tile_ring[r];
+            mbar_arrive(&tile_empty[r]);
+            if (tile < 0) break;
+            mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+            tc_fence_after();
+            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+            for (int kb = 0; kb < p.k_blocks; ++kb) {
+                mbar_wait(&full[stage], phase);
+                tc_fence_after();
+                const uint32_t a_addr = a0 + stage * A_STAGE;
+                const uint32_t b_addr = b0 + stage * B_STAGE;
+#pragma unroll
+                for (int k = 0; k < BK / UK; ++k)
+                    umma_bf16_pair(d_tmem, smem_desc_k_sw128(a_addr + k * UK * 2),
+                                   smem_desc_k_sw128(b_addr + k * UK * 2), idesc, (kb | k) != 0);
+                umma_commit_pair(&empty[stage], 0x3);
+                if (++stage == STAGES) {
+                    stage = 0;
+                    phase ^= 1;
+                }
+            }
+            umma_commit_pair(&acc_full[acc], 0x3);
+            if (++acc == ACC_BUFS) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    } else if (warp >= 4) {
+        // ------------- epilogue (both CTAs): own 128 rows x 256 columns -------------
+        const int q = warp - 4;
+        const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
+        int acc = 0;
+        uint32_t acc_phase = 0;
+        for (int i = 0;; ++i) {
+            const int r = i % RING;
+            if (leader)
+                mbar_wait(&tile_full[r], (i / RING) & 1);
+            else
+                mbar_wait_cluster(&tile_full[r], (i / RING) & 1);
+            const int tile = tile_ring[r];
+            __syncwarp();
+            if (lane == 0) {
+                if (leader)
+                    mbar_arrive(&tile_empty[r]);
+                else
+                    mbar_arrive_cluster(mapa(smem_u32(&tile_empty[r]), 0));
+            }
+            if (tile < 0) break;
+            int tm, tn;
+            tile_coords(p, tile, tm, tn);
+            mbar_wait(&acc_full[acc], acc_phase);
+            tc_fence_after();
+            const int row = tm * BM + row_in_tile;
+            const bool row_ok = row < p.m;
+            __nv_bfloat16* crow = p.c + static_cast<size_t>(row) * p.ldc;
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                   static_cast<uint32_t>(acc * BN);
+#pragma unroll 1
+            for (int c = 0; c < BN; c += 32) {
+                uint32_t v[32];
+                tmem_ld_32x32b_x32(t_row + c, v);
+                tmem_ld_wait();
+                const int col = tn * BN + c;
+                if (!row_ok) continue;
+                if (col + 32 <= p.n) {
+                    uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        uint4 o;
+                        __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                        __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                        __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                        o.x = *reinterpret_cast<uint32_t*>(&h0);
+                        o.y = *reinterpret_cast<uint32_t*>(&h1);
+                        o.z = *reinterpret_cast<uint32_t*>(&h2);
+                        o.w = *reinterpret_cast<uint32_t*>(&h3);
+                        dst[j] = o;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 32; ++j)
+                        if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) {
+                if (leader)
+                    mbar_arrive(&acc_empty[acc]);
+                else
+                    mbar_arrive_cluster(mapa(smem_u32(&acc_empty[acc]), 0));
+            }
+            if (++acc == ACC_BUFS) {
+                acc = 0;
+                acc_phase ^= 1;
+            }
+        }
+    }
+
+    tc_fence_before();
+    cluster_sync();  // no CTA leaves while its peer may still signal into it
+    if (warp == 2) {
+        tc_fence_after();
+        tmem_dealloc_pair<TMEM_COLS>(tmem_base);
+    }
+    if (threadIdx.x == 0 && leader) {
+        __threadfence();
+        if (atomicAdd(p.exit_counter, 1) == static_cast<int>(gridDim.x / 2) - 1) {
+            *p.tile_counter = 0;
+            *p.exit_counter = 0;
+            __threadfence();
+        }
+    }
+}
+
+}  // namespace gemm2
+
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream) {
+    static bool attr_done = false;
+    if (!attr_done) {
+        const cudaError_t e = cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(gemm2::SMEM));
+        if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm pair)");
+        attr_done = true;
+    }
+    gemm2::Params p;
+    p.m = static_cast<int>(plan->m);
+    p.n = static_cast<int>(plan->n);
+    p.k = static_cast<int>(plan->k);
+    p.tiles_m = plan->tiles_m;
+    p.tiles_n = plan->tiles_n;
+    p.num_tiles = plan->num_tiles;
+    p.k_blocks = plan->k_blocks;
+    p.c = static_cast<__nv_bfloat16*>(plan->c);
+    p.ldc = static_cast<int>(plan->n);
+    p.tile_counter = plan->counters;
+    p.exit_counter = plan->counters + 1;
+    gemm2::gemm_bf16_tn_pair_kernel<<<grid, gemm2::THREADS, gemm2::SMEM, stream>>>(plan->map_a,
+                                                                                   plan->map_b128, p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm pair launch");
+    return C3_OK;
+}
+
+}  // namespace c3k

@@ -86,6 +86,30 @@ def test_gemm_small_full(torch_mod, c3, M, N, K):
     w.close()
 
 
+@pytest.mark.parametrize("kernel", ["pair", "wide", "narrow"])
+@pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 768, 1024), (1000, 2056, 136),
+                                   (300, 520, 200)])
+def test_gemm_kernel_variants_full(torch_mod, c3, monkeypatch, kernel, M, N, K):
+    """Each GEMM kernel variant (CTA-pair 256x256, single-CTA 128x256 and
+    128x128 tiles), forced, on full outputs including ragged M/N/K tails."""
+    monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
+    torch = torch_mod
+    w = c3.World()
+    A = torch.empty(M * K, dtype=torch.int16, device="cuda")
+    B = torch.empty(N * K, dtype=torch.int16, device="cuda")
+    Cm = torch.zeros(M * N, dtype=torch.int16, device="cuda")
+    c3.check(c3.lib().c3_fill_bf16(A.data_ptr(), M * K, SEED, 0, 0, None))
+    c3.check(c3.lib().c3_fill_bf16(B.data_ptr(), N * K, SEED, 0, 1, None))
+    for cap in (0, 6):
+        Cm.zero_()
+        w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, cap)
+        torch.cuda.synchronize()
+        Ah, Bh = orc.bf16(M * K, SEED, 0, 0), orc.bf16(N * K, SEED, 0, 1)
+        rows, cols = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+        gemm_check(Cm.cpu().numpy().view(np.uint16), Ah, Bh, M, N, K, rows.ravel(), cols.ravel())
+    w.close()
+
+
 @pytest.mark.parametrize("max_ctas", [1, 7, 148])
 def test_gemm_cta_cap_same_result(torch_mod, c3, max_ctas):
     """The CTA cap (SM allocation) must not change a single output bit."""
