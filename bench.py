@@ -166,45 +166,57 @@ def run_ours(args, dist):
         flat = dist.max_list([v for r in rows for v in r])
         return [flat[i * 4:(i + 1) * 4] for i in range(steps)]
 
-    # isolated kernel times on the whole GPU (outside the timed region): the
-    # reference's t_gemm / t_comm (sim.cpp:136-138), per backend
+    # Isolated kernel times on the whole GPU are the reference's t_gemm /
+    # t_comm (sim.cpp:136-138). They are measured INTERLEAVED with the
+    # concurrent runs (round-robin within each round) so clock / power-cap
+    # drift over the run affects serial and concurrent alike.
     W, K = args.warmup, args.steps
     full = world.info.sm_count
-    timed(c3.GEMM_ONLY, W)
-    t_g = median([r[1] for r in timed(c3.GEMM_ONLY, K)])
-    iso_comm = {}
-    for name, mode in (("cu", c3.COMM_ONLY_CU), ("dma", c3.COMM_ONLY_DMA)):
-        a = sess.default_alloc(mode)
-        a.cus_comm = full
-        timed(mode, 2, a)
-        iso_comm[name] = median([r[2] for r in timed(mode, K, a)])
     dma_ok = not loopback  # same-device copies run on SMs
+    iso_modes = {"gemm": (c3.GEMM_ONLY, sess.default_alloc(c3.GEMM_ONLY)),
+                 "cu": (c3.COMM_ONLY_CU, sess.default_alloc(c3.COMM_ONLY_CU)),
+                 "dma": (c3.COMM_ONLY_DMA, sess.default_alloc(c3.COMM_ONLY_DMA))}
+    iso_modes["cu"][1].cus_comm = full
+    col = {"gemm": 1, "cu": 2, "dma": 2}
 
-    def summarise(name, rows, t_c):
+    def rounds(jobs, n):
+        """n round-robin rounds over jobs {name: (strategy, alloc)}; per-job rows."""
+        out = {k: [] for k in jobs}
+        for _ in range(n):
+            for name, (st, a) in jobs.items():
+                out[name] += timed(st, 1, a)
+        return out
+
+    rounds(iso_modes, W)  # warm-up
+    strat_jobs = {}
+    for st in strategies:
+        if st != c3.SERIAL:
+            strat_jobs[c3.STRATEGY_NAMES[st]] = (st, sess.default_alloc(st))
+    sweep_rows = rounds({**iso_modes, **strat_jobs}, K)
+    iso_comm = {k: median([r[col[k]] for r in sweep_rows[k]]) for k in ("cu", "dma")}
+    t_g = median([r[1] for r in sweep_rows["gemm"]])
+
+    def summarise(rows, t_g, t_c, best_c):
         t_conc = median([r[0] for r in rows])
         sp = (t_g + t_c) / t_conc
         ideal = c3.ideal_speedup(t_g, t_c)
-        best_c = min(iso_comm["cu"], iso_comm["dma"]) if dma_ok else iso_comm["cu"]
-        return {"t_concurrent_ms": t_conc, "t_comm_iso_ms": t_c, "speedup": sp, "ideal": ideal,
-                "fraction_of_ideal": c3.fraction_of_ideal(sp, ideal),
+        return {"t_concurrent_ms": t_conc, "t_gemm_iso_ms": t_g, "t_comm_iso_ms": t_c,
+                "speedup": sp, "ideal": ideal, "fraction_of_ideal": c3.fraction_of_ideal(sp, ideal),
                 "speedup_vs_best_comm": (t_g + best_c) / t_conc,
                 "fraction_vs_best_comm": c3.fraction_of_ideal((t_g + best_c) / t_conc,
                                                               c3.ideal_speedup(t_g, best_c)),
                 "gemm_ms_in_step": median([r[1] for r in rows])}
 
+    best_iso = min(iso_comm.values()) if dma_ok else iso_comm["cu"]
     results = {}
-    for st in strategies:
-        if st == c3.SERIAL:
-            continue
-        a = sess.default_alloc(st)
-        timed(st, max(1, W // 2), a)
-        res = summarise(c3.STRATEGY_NAMES[st], timed(st, K, a),
-                        iso_comm["dma" if a.backend == c3.BACKEND_DMA else "cu"])
+    for name, (st, a) in strat_jobs.items():
+        res = summarise(sweep_rows[name], t_g, iso_comm["dma" if a.backend == c3.BACKEND_DMA else "cu"],
+                        best_iso)
         res["alloc"] = {"cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm, "cus_idle": a.cus_idle,
                         "backend": "DMA" if a.backend == c3.BACKEND_DMA else "CU"}
         if a.backend == c3.BACKEND_DMA and loopback:
-            res["note"] = "loopback: same-device copies run on SMs, not copy engines"
-        results[c3.STRATEGY_NAMES[st]] = res
+            res["note"] = "loopback: same-device copies run on SMs (driver copy kernels), not copy engines"
+        results[name] = res
 
     # the runtime heuristic's pick (model layer simulate() on measured tables)
     if args.strategy == "auto":
@@ -214,8 +226,12 @@ def run_ours(args, dist):
         head_alloc, predicted = sess.default_alloc(head), None
     head_name = c3.STRATEGY_NAMES[head]
     measured_best = max(results, key=lambda k: results[k]["speedup"]) if results else None
+    backend = head_alloc.backend
+    comm_key = "dma" if backend == c3.BACKEND_DMA else "cu"
 
-    # ---- the timed region: K steps of the headline strategy ----
+    # ---- the timed region: K C3 steps of the headline strategy; the isolated
+    # GEMM and collective reference runs are interleaved between steps (their
+    # device times are not part of ms_per_step) ----
     for _ in range(W):
         sess.run(head, head_alloc)
     torch.cuda.synchronize()
@@ -225,17 +241,19 @@ def run_ours(args, dist):
         clocks.start()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    rows = timed(head, K, head_alloc)
+    timed_rows = rounds({"gemm": iso_modes["gemm"], comm_key: iso_modes[comm_key],
+                         "step": (head, head_alloc)}, K)
     torch.cuda.synchronize()
     dist.barrier()
     wall = time.perf_counter() - t0
     clk = clocks.stop() if clocks else None
+    rows = timed_rows["step"]
     step_ms = [r[0] for r in rows]
     gemm_ms = [r[1] for r in rows]
     launches = int(sum(r[3] for r in rows))
-    backend = head_alloc.backend
-    t_c = iso_comm["dma" if backend == c3.BACKEND_DMA else "cu"]
-    head_res = summarise(head_name, rows, t_c)
+    t_g_timed = median([r[1] for r in timed_rows["gemm"]])
+    t_c = median([r[col[comm_key]] for r in timed_rows[comm_key]])
+    head_res = summarise(rows, t_g_timed, t_c, t_c)
     t_conc = head_res["t_concurrent_ms"]
     speedup, ideal, frac = head_res["speedup"], head_res["ideal"], head_res["fraction_of_ideal"]
     choice = {"strategy": head_name, "selected_by": "runtime heuristic (c3_session_choose)"
@@ -269,9 +287,7 @@ def run_ours(args, dist):
         e2e_step(head)
     e2e_conc = median(dist.max_list([e2e_step(head) for _ in range(K)]))
     e2e_g = median(dist.max_list([e2e_step(c3.GEMM_ONLY) for _ in range(K)]))
-    comm_mode = c3.COMM_ONLY_DMA if backend == c3.BACKEND_DMA else c3.COMM_ONLY_CU
-    comm_alloc = sess.default_alloc(comm_mode)
-    comm_alloc.cus_comm = full
+    comm_mode, comm_alloc = iso_modes[comm_key]
 
     def e2e_comm():
         t0 = time.perf_counter()
@@ -285,7 +301,7 @@ def run_ours(args, dist):
 
     e2e_c = median(dist.max_list([e2e_comm() for _ in range(K)]))
     # serial e2e = inputs in, GEMM, collective, result out (copies counted once)
-    io_ms = e2e_g - t_g
+    io_ms = e2e_g - t_g_timed
     e2e_speedup = (e2e_g + e2e_c - io_ms) / e2e_conc
 
     peaks, peak_src = load_peaks()
@@ -315,8 +331,11 @@ def run_ours(args, dist):
                    "world": ("loopback: 8-rank collective emulated on 1 GPU (peer buffers in local "
                              "HBM, no NVLink)") if loopback else f"{n} GPUs, CUDA-IPC peer memory",
                    "l2": "inputs > 126 MB L2 (no flush needed)",
-                   "isolated_ms": {"gemm": t_g, "comm_cu": iso_comm["cu"],
-                                   "comm_dma": iso_comm["dma"]},
+                   "isolated_ms": {"gemm": t_g_timed, "comm": t_c, "backend": comm_key,
+                                   "sweep_gemm": t_g, "sweep_comm_cu": iso_comm["cu"],
+                                   "sweep_comm_dma": iso_comm["dma"]},
+                   "protocol": ("W warm-up, then K rounds of [isolated GEMM, isolated collective, "
+                                "C3 step]; medians; ms_per_step = C3 steps only"),
                    "timed_region_wall_s": wall},
         "strategies": results,
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tn_kernel (tcgen05)",

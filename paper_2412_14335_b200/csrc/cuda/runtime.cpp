@@ -876,7 +876,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
         const c3sim::Allocation a =
             c3sim::allocate_cus(x, static_cast<c3sim::Strategy>(best_st), s->md, s->tables, eff);
         alloc->cus_gemm = a.cus_gemm;
-        alloc->cus_comm = best_st == C3_SERIAL ? 32 : a.cus_comm;
+        alloc->cus_comm = best_st == C3_SERIAL ? s->md.cus_per_gpu : a.cus_comm;
         alloc->cus_idle = a.cus_idle;
         alloc->backend = a.comm_backend == c3sim::CommBackend::DMA ? C3_BACKEND_DMA : C3_BACKEND_CU;
         alloc->comm_first = a.comm_first ? 1 : 0;
@@ -910,7 +910,7 @@ int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
         out->cus_idle = a.cus_idle;
         out->backend = a.comm_backend == c3sim::CommBackend::DMA ? C3_BACKEND_DMA : C3_BACKEND_CU;
         out->comm_first = a.comm_first ? 1 : 0;
-        if (strategy == C3_SERIAL) out->cus_comm = 32;  // isolated SM collective width
+        if (strategy == C3_SERIAL) out->cus_comm = C;  // each kernel alone on the whole GPU
         return C3_OK;
     });
 }
