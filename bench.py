@@ -180,11 +180,12 @@ def run_ours(args, dist):
     col = {"gemm": 1, "cu": 2, "dma": 2}
 
     def rounds(jobs, n):
-        """n round-robin rounds over jobs {name: (strategy, alloc)}; per-job rows."""
+        """n round-robin rounds over jobs {name: (strategy, alloc) | callable};
+        per-job rows [total, gemm, comm, launches] (device ms, max over ranks)."""
         out = {k: [] for k in jobs}
         for _ in range(n):
-            for name, (st, a) in jobs.items():
-                out[name] += timed(st, 1, a)
+            for name, job in jobs.items():
+                out[name] += [job()] if callable(job) else timed(job[0], 1, job[1])
         return out
 
     rounds(iso_modes, W)  # warm-up
@@ -219,8 +220,24 @@ def run_ours(args, dist):
         results[name] = res
 
     # the runtime heuristic's pick (model layer simulate() on measured tables)
+    tune = None
     if args.strategy == "auto":
         head, head_alloc, predicted = sess.choose(t_g, iso_comm["cu"], iso_comm["dma"], dma_ok)
+        # measured refinement over the model's pick, serial, and B200
+        # co-resident SM variants (the GEMM keeps every SM; comm CTAs share SMs
+        # with the GEMM's CTAs — 512 threads, no smem, fits beside 193 KB)
+        cands = [(head, head_alloc), (c3.SERIAL, sess.default_alloc(c3.SERIAL))]
+        for st in (c3.C3_BASE, c3.C3_SP):
+            for ctas in (8, 16, 32, 64):
+                a = sess.default_alloc(st)
+                a.cus_gemm, a.cus_comm = full, ctas
+                cands.append((st, a))
+        if dma_ok:
+            cands += [(st, sess.default_alloc(st)) for st in (c3.CONCCL, c3.CONCCL_RP)]
+        best_i, best_ms = sess.autotune(cands, rounds=3)
+        tune = {"candidates": len(cands), "model_pick": c3.STRATEGY_NAMES[head],
+                "picked_index": best_i, "picked_ms": best_ms}
+        head, head_alloc = cands[best_i]
     else:
         head = c3.STRATEGY_NAMES.index(args.strategy)
         head_alloc, predicted = sess.default_alloc(head), None
@@ -241,8 +258,14 @@ def run_ours(args, dist):
         clocks.start()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    timed_rows = rounds({"gemm": iso_modes["gemm"], comm_key: iso_modes[comm_key],
-                         "step": (head, head_alloc)}, K)
+    lib = None
+    if not args.no_library_baseline:
+        lib = LibraryBaseline(cfg, dist, loopback)
+        rounds({"lg": lib.gemm_only, "lc": lib.comm_only, "lb": lib.both}, W)
+    jobs = {"gemm": iso_modes["gemm"], comm_key: iso_modes[comm_key], "step": (head, head_alloc)}
+    if lib:
+        jobs.update({"lib_gemm": lib.gemm_only, "lib_comm": lib.comm_only, "lib_both": lib.both})
+    timed_rows = rounds(jobs, K)
     torch.cuda.synchronize()
     dist.barrier()
     wall = time.perf_counter() - t0
@@ -256,12 +279,12 @@ def run_ours(args, dist):
     head_res = summarise(rows, t_g_timed, t_c, t_c)
     t_conc = head_res["t_concurrent_ms"]
     speedup, ideal, frac = head_res["speedup"], head_res["ideal"], head_res["fraction_of_ideal"]
-    choice = {"strategy": head_name, "selected_by": "runtime heuristic (c3_session_choose)"
-              if args.strategy == "auto" else "--strategy",
+    choice = {"strategy": head_name, "selected_by": "runtime: model prediction (c3_session_choose) + "
+              "measured autotune (c3_session_autotune)" if args.strategy == "auto" else "--strategy",
               "alloc": {"cus_gemm": head_alloc.cus_gemm, "cus_comm": head_alloc.cus_comm,
                         "cus_idle": head_alloc.cus_idle,
                         "backend": "DMA" if backend == c3.BACKEND_DMA else "CU"},
-              "predicted_ms": predicted, "measured_ms": t_conc,
+              "predicted_ms": predicted, "measured_ms": t_conc, "autotune": tune,
               "measured_best_default_alloc": measured_best, "tables": os.path.relpath(tables, REPO)}
 
     # ---- e2e through the C ABI with host buffers ----
@@ -350,11 +373,100 @@ def run_ours(args, dist):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if lib:
+        tg_l = median([r[1] for r in timed_rows["lib_gemm"]])
+        tc_l = median([r[2] for r in timed_rows["lib_comm"]])
+        tb_l = median([r[0] for r in timed_rows["lib_both"]])
+        sp_l = (tg_l + tc_l) / tb_l
+        ideal_l = (tg_l + tc_l) / max(tg_l, tc_l)
+        out["library_baseline"] = {
+            "what": lib.label, "t_gemm_ms": tg_l, "t_comm_ms": tc_l, "t_concurrent_ms": tb_l,
+            "speedup": sp_l, "ideal": ideal_l,
+            "fraction_of_ideal": 0.0 if sp_l < 1 else (sp_l - 1) / (ideal_l - 1),
+            "library_concurrent_over_ours": tb_l / t_conc,
+            "note": "interleaved with our steps in the same timed rounds"}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(quick=True)
     sess.close()
     world.close()
     return out
+
+
+# ------------------------------------------------- library baseline ------
+
+class LibraryBaseline:
+    """Same scenario with library kernels: cuBLAS GEMM (torch.matmul) concurrent
+    with NCCL all-gather / reduce-scatter (N>1), or — loopback — with torch
+    device copies moving this GPU's share of the 8-rank collective (7 chunks).
+    Each call returns [total, gemm, comm, 0] device ms (max over ranks)."""
+
+    def __init__(self, cfg, dist, loopback):
+        import torch
+        self.torch, self.dist = torch, dist
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.A = torch.randn(cfg["m"], cfg["k"], device=dev, dtype=torch.bfloat16)
+        self.B = torch.randn(cfg["n"], cfg["k"], device=dev, dtype=torch.bfloat16)
+        self.C = torch.empty(cfg["m"], cfg["n"], device=dev, dtype=torch.bfloat16)
+        n = 8 if loopback else dist.world
+        chunk = cfg["payload"] // n
+        self.s_g, self.s_c = torch.cuda.Stream(), torch.cuda.Stream()
+        self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        if loopback:
+            src = torch.empty(chunk, dtype=torch.uint8, device=dev)
+            dst = torch.empty(n * chunk, dtype=torch.uint8, device=dev)
+
+            def comm():
+                for p in range(1, n):
+                    dst[p * chunk:(p + 1) * chunk].copy_(src)
+            self.label = ("cuBLAS (torch.matmul) || torch device copies of 7 chunks "
+                          "(loopback; SM copy kernels)")
+        else:
+            import torch.distributed as tdist
+            pg = tdist.new_group(backend="nccl")
+            if cfg["coll"] == "all-gather":
+                src = torch.empty(chunk, dtype=torch.uint8, device=dev)
+                dst = torch.empty(n * chunk, dtype=torch.uint8, device=dev)
+
+                def comm():
+                    tdist.all_gather_into_tensor(dst, src, group=pg)
+            else:
+                src = torch.randn(cfg["payload"] // 2, device=dev).to(torch.bfloat16)
+                dst = torch.empty(cfg["payload"] // 2 // n, device=dev, dtype=torch.bfloat16)
+
+                def comm():
+                    tdist.reduce_scatter_tensor(dst, src, group=pg)
+            self.label = "cuBLAS (torch.matmul) || NCCL " + cfg["coll"]
+        self.comm = comm
+
+    def _run(self, g, c):
+        torch, ev = self.torch, self.ev
+        torch.cuda.synchronize()
+        ev[0].record()
+        self.s_g.wait_event(ev[0])
+        self.s_c.wait_event(ev[0])
+        if g:
+            with torch.cuda.stream(self.s_g):
+                torch.matmul(self.A, self.B.t(), out=self.C)
+        if c:
+            with torch.cuda.stream(self.s_c):
+                self.comm()
+        ev[1].record(self.s_g)
+        ev[2].record(self.s_c)
+        torch.cuda.current_stream().wait_event(ev[1])
+        torch.cuda.current_stream().wait_event(ev[2])
+        ev[3].record()
+        ev[3].synchronize()
+        tot = ev[0].elapsed_time(ev[3])
+        return self.dist.max_list([tot, tot if g else 0.0, tot if c else 0.0, 0.0])
+
+    def gemm_only(self):
+        return self._run(True, False)
+
+    def comm_only(self):
+        return self._run(False, True)
+
+    def both(self):
+        return self._run(True, True)
 
 
 # ---------------------------------------------------------- CPU arms ------
@@ -424,6 +536,7 @@ def main():
     ap.add_argument("--strategies", default="c3_base,c3_sp,c3_rp,c3_sp_rp,conccl,conccl_rp")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-library-baseline", action="store_true")
     args = ap.parse_args()
     args.strategies = [s for s in args.strategies.split(",") if s]
     args.warmup = max(3, args.warmup)

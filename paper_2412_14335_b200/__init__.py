@@ -129,6 +129,15 @@ class Session:
                                       int(bool(allow_dma)), C.byref(st), C.byref(a), C.byref(pred)))
         return st.value, a, pred.value
 
+    def autotune(self, candidates, rounds=3):
+        """candidates: [(strategy, Alloc)] -> (best index, median ms)."""
+        n = len(candidates)
+        sts = (C.c_int * n)(*[c[0] for c in candidates])
+        als = (_capi.Alloc * n)(*[c[1] for c in candidates])
+        best, ms = C.c_int(), C.c_double()
+        check(lib().c3_session_autotune(self.h, sts, als, n, rounds, C.byref(best), C.byref(ms)))
+        return best.value, ms.value
+
     def default_alloc(self, strategy):
         a = _capi.Alloc()
         check(lib().c3_session_default_alloc(self.h, strategy, C.byref(a)))

@@ -20,6 +20,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstring>
 #include <map>
 #include <string>
@@ -882,6 +883,31 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
         alloc->comm_first = a.comm_first ? 1 : 0;
         return C3_OK;
     });
+}
+
+int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* allocs, int n,
+                        int rounds, int* best, double* best_ms) {
+    if (!s || !strategies || !allocs || !best || !best_ms || n < 1 || rounds < 1)
+        return set_error(C3_ERR_VALIDATION, "c3_session_autotune: bad argument");
+    std::vector<std::vector<double>> t(static_cast<size_t>(n));
+    for (int r = 0; r < rounds; ++r)  // round-robin so clock drift hits all alike
+        for (int i = 0; i < n; ++i) {
+            c3_timing tm;
+            C3_TRY(c3_session_run(s, strategies[i], &allocs[i], &tm));
+            t[static_cast<size_t>(i)].push_back(tm.total_ms);
+        }
+    *best = 0;
+    *best_ms = 1e300;
+    for (int i = 0; i < n; ++i) {
+        auto v = t[static_cast<size_t>(i)];
+        std::sort(v.begin(), v.end());
+        const double med = v[v.size() / 2];
+        if (med < *best_ms) {
+            *best_ms = med;
+            *best = i;
+        }
+    }
+    return C3_OK;
 }
 
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
