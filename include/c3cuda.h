@@ -87,7 +87,8 @@ typedef struct c3_world_info {
 /* One C3 scenario (c3sim::C3Scenario, workload.hpp:37-43), executable form:
  * GEMM C[m,n] = A[m,k] B[n,k]^T in bf16 with fp32 accumulation, plus one
  * collective of `payload_bytes` per rank (all-gather: gathered bytes;
- * reduce-scatter: input bytes, bf16 elements) over n_ranks. */
+ * all-to-all: send-buffer bytes; reduce-scatter: input bytes, bf16 elements)
+ * over n_ranks. */
 typedef struct c3_scenario_desc {
     int64_t m, n, k;
     int32_t collective;
@@ -168,6 +169,11 @@ int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, 
  * wire time roofline_collective_time (workload.hpp:66-67) models. */
 int c3_allgather_p2p(c3_world* w, int self, const void* send, void* const* recv,
                      int64_t chunk_bytes, int n_ctas, void* stream);
+/* All-to-all, push form: slot p of `send` -> slot `self` of recv[p] (for every
+ * p, including self). Executes CollectiveOp{AllToAll} (workload.hpp:27-35)
+ * with plan_all_to_all's mapping (conccl.hpp:49-50). */
+int c3_alltoall_p2p(c3_world* w, int self, const void* send, void* const* recv,
+                    int64_t per_peer_bytes, int n_ctas, void* stream);
 /* Direct reduce-scatter, pull form: out = sum_{g=0..n-1} in[g][self*count ..],
  * fp32 accumulation in rank order, one bf16 rounding. in[g] = rank g's
  * input (peer-mapped or local). Extension: no reference counterpart. */

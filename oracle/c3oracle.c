@@ -137,6 +137,15 @@ void c3o_expected_allgather(void* out, int n, int64_t chunk, uint64_t seed, int 
     for (int g = 0; g < n; ++g) c3o_fill_labels((uint8_t*)out + (int64_t)g * chunk, chunk, seed, g, tensor);
 }
 
+void c3o_expected_alltoall(void* out, int n, int rank, int64_t slot, uint64_t seed, int tensor) {
+    uint8_t* buf = (uint8_t*)malloc((size_t)(n * slot) + 8);
+    for (int g = 0; g < n; ++g) {
+        c3o_fill_labels(buf, (int64_t)n * slot, seed, g, tensor);
+        memcpy((uint8_t*)out + (int64_t)g * slot, buf + (int64_t)rank * slot, (size_t)slot);
+    }
+    free(buf);
+}
+
 void c3o_reduce_scatter_bf16(const uint16_t* const* inputs, int n, int rank, int64_t count,
                              uint16_t* out) {
 #pragma omp parallel for schedule(static)

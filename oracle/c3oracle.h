@@ -68,6 +68,11 @@ int c3o_byte_oracle(int kind, int n_ranks, int64_t chunk, int64_t src_bytes, int
  * filled with c3o_fill_labels(seed, rank, tensor): slot g = rank g's chunk. */
 void c3o_expected_allgather(void* out, int n_ranks, int64_t chunk, uint64_t seed, int tensor);
 
+/* Expected all-to-all receive buffer of rank r when every rank g's send buffer
+ * (n slots of `slot` bytes) holds c3o_fill_labels(seed, g, tensor): slot g of
+ * rank r's receive = rank g's send slot r (test_conccl.cpp:63-64). */
+void c3o_expected_alltoall(void* out, int n_ranks, int rank, int64_t slot, uint64_t seed, int tensor);
+
 /* Reduce-scatter reference: inputs[g] is rank g's bf16 input of n*count
  * elements; out receives rank r's slot: sum_{g=0..n-1} inputs[g][r*count + i]
  * accumulated in fp32 in rank order, rounded once to bf16 (RNE). */

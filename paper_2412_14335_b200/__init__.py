@@ -66,6 +66,10 @@ class World:
         check(lib().c3_allgather_p2p(self.h, self_rank, send, ptr_array(recv_ptrs), chunk_bytes,
                                      n_ctas, stream))
 
+    def alltoall_p2p(self, self_rank, send, recv_ptrs, per_peer_bytes, n_ctas=32, stream=None):
+        check(lib().c3_alltoall_p2p(self.h, self_rank, send, ptr_array(recv_ptrs), per_peer_bytes,
+                                    n_ctas, stream))
+
     def reduce_scatter_p2p(self, self_rank, in_ptrs, out, count, n_ctas=32, stream=None):
         check(lib().c3_reduce_scatter_p2p(self.h, self_rank, ptr_array(in_ptrs), out, count,
                                           n_ctas, stream))

@@ -87,6 +87,7 @@ SIGNATURES = {
     "c3_fill_labels": (I, [P, I64, U64, I, I, P]),
     "c3_gemm_bf16": (I, [P, P, P, P, I64, I64, I64, I, P]),
     "c3_allgather_p2p": (I, [P, I, P, PP, I64, I, P]),
+    "c3_alltoall_p2p": (I, [P, I, P, PP, I64, I, P]),
     "c3_reduce_scatter_p2p": (I, [P, I, PP, P, I64, I, P]),
     "c3_reduce_local_bf16": (I, [PP, I, P, I64, I, P]),
     "c3_ce_execute": (I, [P, C.POINTER(Transfer), I, PP, PP, I, P]),

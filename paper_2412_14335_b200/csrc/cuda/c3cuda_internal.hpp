@@ -98,6 +98,8 @@ struct MutPtrTable {
 int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
                           int64_t chunk_bytes, int n_ctas, const Signals& sig,
                           cudaStream_t stream);
+int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
+                         int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream);
 int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
                                int n_ctas, const Signals& sig, cudaStream_t stream);
 int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor,

@@ -113,6 +113,44 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
     if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
 }
 
+// All-to-all, push form (plan_all_to_all's mapping, conccl.cpp:55-84): slot p
+// of rank `self`'s send buffer goes to slot `self` of rank p's receive buffer.
+__global__ void __launch_bounds__(kThreads)
+a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, int n,
+                    int64_t slot_vec, Signals sig) {
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
+    for (int j = 0; j < n; ++j) {
+        const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
+        const uint4* src = send + slot_vec * p;
+        uint4* dst = static_cast<uint4*>(recv.p[p]) + slot_vec * self;
+        for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
+             base < slot_vec; base += step) {
+            uint4 v[kUnroll];
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+                if (i < slot_vec) v[u] = ld_nc_v4(src + i);
+            }
+#pragma unroll
+            for (int u = 0; u < kUnroll; ++u) {
+                const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+                if (i < slot_vec) st_v4(dst + i, v[u]);
+            }
+        }
+    }
+    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+}
+
+__global__ void __launch_bounds__(kThreads)
+a2a_push_byte_kernel(const uint8_t* __restrict__ send, MutPtrTable recv, int self, int n,
+                     int64_t slot, Signals sig) {
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads;
+    for (int p = 0; p < n; ++p)
+        for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < slot; i += step)
+            static_cast<uint8_t*>(recv.p[p])[slot * self + i] = send[slot * p + i];
+    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+}
+
 __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& v) {
     const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v);
 #pragma unroll
@@ -243,6 +281,29 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
         const int grid = grid_for(std::max<int64_t>(chunk_bytes, 1), kThreads, n_ctas);
         ag_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
                                                           self, n, chunk_bytes, in_place ? 0 : 1, sig);
+    }
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
+                         int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream) {
+    if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
+        return set_error(C3_ERR_VALIDATION, "alltoall: bad rank/world");
+    if (per_peer_bytes < 0) return set_error(C3_ERR_VALIDATION, "alltoall: negative slot");
+    if (n_ctas < 1) return set_error(C3_ERR_VALIDATION, "alltoall: n_ctas must be >= 1");
+    if (per_peer_bytes == 0 && !sig.enabled) return C3_OK;
+    uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(per_peer_bytes);
+    for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
+    if ((align & 15) == 0) {
+        const int64_t nvec = per_peer_bytes / 16;
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
+        a2a_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
+                                                          n, nvec, sig);
+    } else {
+        const int grid = grid_for(std::max<int64_t>(per_peer_bytes, 1), kThreads, n_ctas);
+        a2a_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
+                                                           self, n, per_peer_bytes, sig);
     }
     C3_CUDA(cudaGetLastError());
     return C3_OK;

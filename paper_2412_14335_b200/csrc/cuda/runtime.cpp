@@ -301,6 +301,11 @@ int session_alloc(c3_session* s) {
         if (d.collective == C3_ALL_GATHER) {
             C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
             s->recv.push_back(p);
+        } else if (d.collective == C3_ALL_TO_ALL) {
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
+            s->in.push_back(p);
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
+            s->recv.push_back(p);
         } else {
             C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
             s->in.push_back(p);
@@ -381,6 +386,36 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             // data delivered (host barrier at the end of the step, outside timing)
             C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
                           all ? -1 : first, st));
+        }
+        return C3_OK;
+    }
+    if (s->d.collective == C3_ALL_TO_ALL) {
+        MutPtrTable recv{};
+        std::vector<const void*> src(static_cast<size_t>(n));
+        std::vector<void*> dst(static_cast<size_t>(n));
+        for (int p = 0; p < n; ++p) {
+            recv.p[p] = loop ? s->recv[static_cast<size_t>(p)] : s->peer_coll[p];
+            dst[static_cast<size_t>(p)] = recv.p[p];
+            src[static_cast<size_t>(p)] = loop ? s->in[static_cast<size_t>(p)] : s->in[0];
+        }
+        if (backend == C3_BACKEND_CU) {
+            const Signals sig = make_signals(s, 0);
+            for (int v = first; v <= last; ++v) {
+                C3_TRY(launch_alltoall_push(v, n, loop ? s->in[static_cast<size_t>(v)] : s->in[0], recv,
+                                            chunk, n_ctas, sig, st));
+                ++*launches;
+            }
+        } else {
+            // plan_all_to_all (conccl.cpp:55-84) on the copy engines; the self
+            // slot is a local copy, not part of the plan
+            C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
+                          all ? -1 : first, st));
+            for (int v = first; v <= last; ++v) {
+                const size_t lv = loop ? static_cast<size_t>(v) : 0;
+                C3_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(s->recv[lv]) + chunk * v,
+                                        static_cast<const uint8_t*>(s->in[lv]) + chunk * v,
+                                        static_cast<size_t>(chunk), cudaMemcpyDeviceToDevice, st));
+            }
         }
         return C3_OK;
     }
@@ -585,6 +620,15 @@ int c3_allgather_p2p(c3_world* w, int self, const void* send, void* const* recv,
                                  static_cast<cudaStream_t>(stream));
 }
 
+int c3_alltoall_p2p(c3_world* w, int self, const void* send, void* const* recv,
+                    int64_t per_peer_bytes, int n_ctas, void* stream) {
+    if (!w || !recv) return set_error(C3_ERR_VALIDATION, "c3_alltoall_p2p: null argument");
+    MutPtrTable t{};
+    for (int p = 0; p < w->n_ranks; ++p) t.p[p] = recv[p];
+    return launch_alltoall_push(self, w->n_ranks, send, t, per_peer_bytes, n_ctas, Signals{},
+                                static_cast<cudaStream_t>(stream));
+}
+
 int c3_reduce_scatter_p2p(c3_world* w, int self, const void* const* in, void* out, int64_t count,
                           int n_ctas, void* stream) {
     if (!w || !in) return set_error(C3_ERR_VALIDATION, "c3_reduce_scatter_p2p: null argument");
@@ -651,8 +695,8 @@ int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** ou
     const c3_scenario_desc& d = *desc;
     if (d.n_ranks != w->n_ranks)
         return set_error(C3_ERR_VALIDATION, "c3_session_create: scenario n_ranks != world n_ranks");
-    if (d.collective != C3_ALL_GATHER && d.collective != C3_REDUCE_SCATTER)
-        return set_error(C3_ERR_UNSUPPORTED, "c3_session_create: collective must be all-gather or reduce-scatter");
+    if (d.collective != C3_ALL_GATHER && d.collective != C3_REDUCE_SCATTER && d.collective != C3_ALL_TO_ALL)
+        return set_error(C3_ERR_UNKNOWN, "c3_session_create: unknown collective kind");
     if (d.payload_bytes < 0 || d.payload_bytes % d.n_ranks)
         return set_error(C3_ERR_VALIDATION, "collective: payload_bytes must be divisible by n_ranks");
     if (d.collective == C3_REDUCE_SCATTER && (d.payload_bytes / d.n_ranks) % 2)
@@ -680,14 +724,16 @@ int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** ou
         sc.gemm.n = d.n;
         sc.gemm.k = d.k;
         sc.gemm.dtype_bytes = 2;
-        sc.collective.kind = d.collective == C3_ALL_GATHER ? c3sim::CollectiveKind::AllGather
-                                                           : c3sim::CollectiveKind::ReduceScatter;
+        sc.collective.kind = d.collective == C3_ALL_GATHER   ? c3sim::CollectiveKind::AllGather
+                             : d.collective == C3_ALL_TO_ALL ? c3sim::CollectiveKind::AllToAll
+                                                             : c3sim::CollectiveKind::ReduceScatter;
         sc.collective.payload_bytes = d.payload_bytes;
         sc.collective.n_ranks = d.n_ranks;
         if (s->n > 1) {
             const c3sim::TransferPlan tp =
-                d.collective == C3_ALL_GATHER ? c3sim::plan_all_gather(s->n, s->chunk, s->md)
-                                              : c3sim::plan_reduce_scatter(s->n, s->chunk, s->md);
+                d.collective == C3_ALL_GATHER   ? c3sim::plan_all_gather(s->n, s->chunk, s->md)
+                : d.collective == C3_ALL_TO_ALL ? c3sim::plan_all_to_all(s->n, s->chunk, s->md)
+                                                : c3sim::plan_reduce_scatter(s->n, s->chunk, s->md);
             const c3sim::PlanCheck chk = c3sim::validate_plan(tp, s->md);
             if (!chk.ok) throw c3sim::ValidationError("transfer plan invalid: " + chk.error);
             for (const auto& t : tp.transfers)
@@ -700,7 +746,7 @@ int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** ou
     if (w->loopback || s->n == 1) {
         s->ready = true;
         if (!w->loopback) {
-            s->peer_coll[0] = d.collective == C3_ALL_GATHER ? s->recv[0] : s->in[0];
+            s->peer_coll[0] = d.collective == C3_REDUCE_SCATTER ? s->in[0] : s->recv[0];
             s->peer_sig[0] = s->sig;
         }
     }
@@ -744,6 +790,11 @@ int c3_session_pointers(const c3_session* s, int v, c3_session_ptrs* o) {
         o->recv_bytes = d.payload_bytes;
         o->send = static_cast<uint8_t*>(s->recv[sv]) + s->chunk * self;
         o->send_bytes = s->chunk;
+    } else if (d.collective == C3_ALL_TO_ALL) {
+        o->send = s->in[sv];
+        o->send_bytes = d.payload_bytes;
+        o->recv = s->recv[sv];
+        o->recv_bytes = d.payload_bytes;
     } else {
         o->send = s->in[sv];
         o->send_bytes = d.payload_bytes;
@@ -770,6 +821,9 @@ int c3_session_fill(c3_session* s, uint64_t seed) {
             C3_CUDA(cudaMemsetAsync(s->recv[sv], 0, static_cast<size_t>(d.payload_bytes), st));
             C3_TRY(launch_fill_labels(static_cast<uint8_t*>(s->recv[sv]) + s->chunk * rank, s->chunk,
                                       seed, rank, 2, st));
+        } else if (d.collective == C3_ALL_TO_ALL) {
+            C3_CUDA(cudaMemsetAsync(s->recv[sv], 0, static_cast<size_t>(d.payload_bytes), st));
+            C3_TRY(launch_fill_labels(s->in[sv], d.payload_bytes, seed, rank, 4, st));
         } else {
             C3_TRY(launch_fill_bf16(s->in[sv], d.payload_bytes / 2, seed, rank, 3, st));
         }
@@ -783,7 +837,7 @@ int c3_session_export(c3_session* s, void* blob) {
     if (s->w->loopback) return set_error(C3_ERR_VALIDATION, "c3_session_export: loopback session");
     std::memset(blob, 0, C3_SESSION_HANDLE_BYTES);
     uint8_t* b = static_cast<uint8_t*>(blob);
-    void* coll = s->d.collective == C3_ALL_GATHER ? s->recv[0] : s->in[0];
+    void* coll = s->d.collective == C3_REDUCE_SCATTER ? s->in[0] : s->recv[0];
     C3_TRY(c3_ipc_export(s->w, coll, b));
     if (!s->staging.empty()) C3_TRY(c3_ipc_export(s->w, s->staging[0], b + C3_IPC_HANDLE_BYTES));
     C3_TRY(c3_ipc_export(s->w, s->sig, b + 2 * C3_IPC_HANDLE_BYTES));
@@ -797,7 +851,7 @@ int c3_session_import(c3_session* s, const void* all) {
     for (int p = 0; p < s->n; ++p) {
         const uint8_t* blob = b + static_cast<size_t>(p) * C3_SESSION_HANDLE_BYTES;
         if (p == s->w->rank) {
-            s->peer_coll[p] = s->d.collective == C3_ALL_GATHER ? s->recv[0] : s->in[0];
+            s->peer_coll[p] = s->d.collective == C3_REDUCE_SCATTER ? s->in[0] : s->recv[0];
             s->peer_staging[p] = s->staging.empty() ? nullptr : s->staging[0];
             s->peer_sig[p] = s->sig;
             continue;

@@ -40,6 +40,8 @@ def lib():
         L.c3o_byte_oracle.argtypes = [C.c_int, C.c_int, C.c_int64, C.c_int64, C.c_int64,
                                       C.POINTER(Transfer), C.c_int, C.c_char_p, C.c_size_t]
         L.c3o_expected_allgather.argtypes = [C.c_void_p, C.c_int, C.c_int64, C.c_uint64, C.c_int]
+        L.c3o_expected_alltoall.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_uint64,
+                                            C.c_int]
         L.c3o_reduce_scatter_bf16.argtypes = [C.c_void_p, C.c_int, C.c_int, C.c_int64, C.c_void_p]
         L.c3o_gemm_bf16_ref_samples.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int64,
                                                 C.c_int64, C.c_void_p, C.c_void_p, C.c_int64,
@@ -76,6 +78,12 @@ def bf16_to_f32(bits):
 def expected_allgather(n, chunk, seed, tensor):
     out = np.empty(n * chunk, np.uint8)
     lib().c3o_expected_allgather(_p(out), n, chunk, seed, tensor)
+    return out
+
+
+def expected_alltoall(n, rank, slot, seed, tensor):
+    out = np.empty(n * slot, np.uint8)
+    lib().c3o_expected_alltoall(_p(out), n, rank, slot, seed, tensor)
     return out
 
 

@@ -278,3 +278,51 @@ def test_session_all_strategies_loopback(torch_mod, c3, collective, n):
                     f"strategy {strat} rank {v}"
     s.close()
     w.close()
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("slot", [1, 5, 4096, 1 << 20])
+def test_alltoall_p2p_and_ce_bit_exact(torch_mod, c3, n, slot):
+    """All-to-all (reference plan_all_to_all semantics, §8(f) F1): P2P push and
+    the copy-engine executor running the product's validated plan."""
+    torch = torch_mod
+    w = c3.World(0, n, 0, loopback=True)
+    send = [torch.from_numpy(orc.labels(n * slot, SEED, g, 4)).cuda() for g in range(n)]
+    for path in ("p2p", "ce"):
+        recv = [dev_bytes(torch, n * slot) for _ in range(n)]
+        for r in recv:
+            r.zero_()
+        rptr = [r.data_ptr() for r in recv]
+        if path == "p2p":
+            for g in range(n):
+                w.alltoall_p2p(g, send[g].data_ptr(), rptr, slot, n_ctas=8)
+        else:
+            plan, cnt = c3.plan_transfers(c3.ALL_TO_ALL, n, slot, max(1, w.info.async_engines))
+            w.ce_execute(plan, cnt, [s.data_ptr() for s in send], rptr)
+            for g in range(n):  # the self slot is local, not part of the plan
+                recv[g][g * slot:(g + 1) * slot] = send[g][g * slot:(g + 1) * slot]
+        torch.cuda.synchronize()
+        for r in range(n):
+            assert np.array_equal(to_host_u8(recv[r], n * slot),
+                                  orc.expected_alltoall(n, r, slot, SEED, 4)), f"{path} rank {r}"
+    w.close()
+
+
+@pytest.mark.parametrize("n", [2, 8])
+def test_session_alltoall_all_strategies(torch_mod, c3, n):
+    w = c3.World(0, n, 0, loopback=True)
+    payload = n * (32 << 10)
+    s = c3.Session(w, 256, 256, 128, c3.ALL_TO_ALL, payload)
+    for strat in SESSION_STRATS:
+        s.fill(SEED)
+        s.run(strat, all_ranks=True)
+        if strat == c3.GEMM_ONLY:
+            continue
+        for v in range(n):
+            got = np.empty(payload, np.uint8)
+            c3.check(c3.lib().c3_memcpy(got.ctypes.data, s.pointers(v).recv, payload, 2, None))
+            c3.check(c3.lib().c3_stream_sync(None))
+            assert np.array_equal(got, orc.expected_alltoall(n, v, payload // n, SEED, 4)), \
+                f"strategy {strat} rank {v}"
+    s.close()
+    w.close()

@@ -55,6 +55,11 @@ def _worker(rank, world, port, coll, q):
                 c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
                 c3.check(c3.lib().c3_stream_sync(None))
                 ok = np.array_equal(got, orc.expected_allgather(world, chunk, SEED, 2))
+            elif coll == c3.ALL_TO_ALL:
+                got = np.empty(payload, np.uint8)
+                c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
+                c3.check(c3.lib().c3_stream_sync(None))
+                ok = np.array_equal(got, orc.expected_alltoall(world, rank, chunk, SEED, 4))
             else:
                 count = chunk // 2
                 host_in = [orc.bf16(world * count, SEED, g, 3) for g in range(world)]
@@ -71,7 +76,7 @@ def _worker(rank, world, port, coll, q):
         q.put((rank, None, repr(e)))
 
 
-@pytest.mark.parametrize("coll", [0, 2], ids=["all-gather", "reduce-scatter"])
+@pytest.mark.parametrize("coll", [0, 1, 2], ids=["all-gather", "all-to-all", "reduce-scatter"])
 def test_two_processes_one_gpu(coll):
     world, port = 2, _free_port()
     ctx = mp.get_context("spawn")
