@@ -42,6 +42,9 @@ from paper_2412_14335_b200.dist import Dist  # noqa: E402
 MIB = 1 << 20
 # BASELINE.json configs: (M, N, K), collective, payload per rank
 CONFIGS = {
+    "cfg1": dict(desc="configs[0] on the GPU: GEMM 1024x1024x1024 (bf16 here; fp32 in the CPU "
+                      "reference) || 16 MiB all-gather", m=1024, n=1024, k=1024,
+                 coll="all-gather", payload=16 * MIB),
     "cfg2": dict(desc="LLaMA-70B FSDP layer: FFN up-proj GEMM 8192x28672x8192 bf16 || "
                       "next-layer weight all-gather 896 MiB (gate+up) across 8 GPUs",
                  m=8192, n=28672, k=8192, coll="all-gather", payload=896 * MIB),
@@ -129,6 +132,12 @@ class ClockSampler:
 
 # ------------------------------------------------------------ ours ------
 
+def log(msg):
+    if os.environ.get("C3_BENCH_VERBOSE"):
+        print(f"[bench rank {os.environ.get('RANK', '0')} {time.strftime('%H:%M:%S')}] {msg}",
+              file=sys.stderr, flush=True)
+
+
 def median(xs):
     return statistics.median(xs) if xs else float("nan")
 
@@ -143,12 +152,16 @@ def run_ours(args, dist):
     cfg = CONFIGS[args.config]
     n = 8 if dist.world == 1 else dist.world
     loopback = dist.world == 1
-    torch.cuda.set_device(dist.local_rank)
-    world = c3.World(dist.rank, n, dist.local_rank, loopback=loopback)
+    # C3_SHARED_DEVICE=1: every rank on device 0 (exercises the multi-process
+    # IPC path on a one-GPU box; not a performance configuration)
+    device = 0 if os.environ.get("C3_SHARED_DEVICE") else dist.local_rank
+    torch.cuda.set_device(device)
+    world = c3.World(dist.rank, n, device, loopback=loopback)
     coll = c3.ALL_GATHER if cfg["coll"] == "all-gather" else c3.REDUCE_SCATTER
     sess = c3.Session(world, cfg["m"], cfg["n"], cfg["k"], coll, cfg["payload"])
     if not loopback:
         sess.import_handles(dist.allgather_bytes(sess.export_handles()))
+    log("session ready")
     sess.fill(20241217)
     if not loopback:
         sess.set_barrier(dist.barrier)
@@ -189,12 +202,14 @@ def run_ours(args, dist):
         return out
 
     rounds(iso_modes, W)  # warm-up
+    log("isolated warm-up done")
     strat_jobs = {}
     for st in strategies:
         if st != c3.SERIAL:
             strat_jobs[c3.STRATEGY_NAMES[st]] = (st, sess.default_alloc(st))
     sweep_rows = rounds({**iso_modes, **strat_jobs}, K)
     iso_comm = {k: median([r[col[k]] for r in sweep_rows[k]]) for k in ("cu", "dma")}
+    log("strategy sweep done")
     t_g = median([r[1] for r in sweep_rows["gemm"]])
 
     def summarise(rows, t_g, t_c, best_c):
@@ -234,7 +249,8 @@ def run_ours(args, dist):
                 cands.append((st, a))
         if dma_ok:
             cands += [(st, sess.default_alloc(st)) for st in (c3.CONCCL, c3.CONCCL_RP)]
-        best_i, best_ms = sess.autotune(cands, rounds=3)
+        best_i, best_ms = sess.autotune(cands, rounds=3, reduce_max=dist.max_list)
+        log(f"autotune done: {best_i}")
         tune = {"candidates": len(cands), "model_pick": c3.STRATEGY_NAMES[head],
                 "picked_index": best_i, "picked_ms": best_ms}
         head, head_alloc = cands[best_i]
@@ -253,12 +269,14 @@ def run_ours(args, dist):
         sess.run(head, head_alloc)
     torch.cuda.synchronize()
     dist.barrier()
-    clocks = ClockSampler(dist.local_rank) if dist.rank == 0 else None
+    clocks = ClockSampler(device) if dist.rank == 0 else None
     if clocks:
         clocks.start()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     lib = None
+    if os.environ.get("C3_SHARED_DEVICE"):
+        args.no_library_baseline = True  # NCCL cannot place two ranks on one device
     if not args.no_library_baseline:
         lib = LibraryBaseline(cfg, dist, loopback)
         rounds({"lg": lib.gemm_only, "lc": lib.comm_only, "lb": lib.both}, W)
@@ -266,6 +284,7 @@ def run_ours(args, dist):
     if lib:
         jobs.update({"lib_gemm": lib.gemm_only, "lib_comm": lib.comm_only, "lib_both": lib.both})
     timed_rows = rounds(jobs, K)
+    log("timed region done")
     torch.cuda.synchronize()
     dist.barrier()
     wall = time.perf_counter() - t0

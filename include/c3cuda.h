@@ -237,11 +237,12 @@ int c3_session_load_tables(c3_session* s, const char* csv_path);
 int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, double t_comm_dma_ms,
                       int allow_dma, int* strategy, c3_alloc* alloc, double* predicted_ms);
 /* Measured refinement: run each (strategy, alloc) candidate `rounds` times in
- * round-robin order and return the index with the lowest median step time.
- * Multi-process: every rank must pass the same candidates (the runs are
- * collective). */
+ * round-robin order; medians[i] = candidate i's median step time, *best =
+ * this rank's fastest. Multi-process: every rank must pass the same
+ * candidates (the runs are collective) and must pick from the max over ranks
+ * of `medians`, not from its local *best. */
 int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* allocs, int n,
-                        int rounds, int* best, double* best_ms);
+                        int rounds, double* medians, int* best, double* best_ms);
 /* The allocation c3_session_run uses for (strategy, alloc == NULL). */
 int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out);
 

@@ -133,14 +133,22 @@ class Session:
                                       int(bool(allow_dma)), C.byref(st), C.byref(a), C.byref(pred)))
         return st.value, a, pred.value
 
-    def autotune(self, candidates, rounds=3):
-        """candidates: [(strategy, Alloc)] -> (best index, median ms)."""
+    def autotune(self, candidates, rounds=3, reduce_max=None):
+        """candidates: [(strategy, Alloc)] -> (best index, median ms). With
+        several ranks pass reduce_max (elementwise max over ranks of a list) so
+        every rank picks the same candidate."""
         n = len(candidates)
         sts = (C.c_int * n)(*[c[0] for c in candidates])
         als = (_capi.Alloc * n)(*[c[1] for c in candidates])
+        med = (C.c_double * n)()
         best, ms = C.c_int(), C.c_double()
-        check(lib().c3_session_autotune(self.h, sts, als, n, rounds, C.byref(best), C.byref(ms)))
-        return best.value, ms.value
+        check(lib().c3_session_autotune(self.h, sts, als, n, rounds, med, C.byref(best),
+                                        C.byref(ms)))
+        meds = list(med)
+        if reduce_max is not None:
+            meds = reduce_max(meds)
+        i = min(range(n), key=lambda j: meds[j])
+        return i, meds[i]
 
     def default_alloc(self, strategy):
         a = _capi.Alloc()

@@ -940,8 +940,8 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
 }
 
 int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* allocs, int n,
-                        int rounds, int* best, double* best_ms) {
-    if (!s || !strategies || !allocs || !best || !best_ms || n < 1 || rounds < 1)
+                        int rounds, double* medians, int* best, double* best_ms) {
+    if (!s || !strategies || !allocs || !medians || !best || !best_ms || n < 1 || rounds < 1)
         return set_error(C3_ERR_VALIDATION, "c3_session_autotune: bad argument");
     std::vector<std::vector<double>> t(static_cast<size_t>(n));
     for (int r = 0; r < rounds; ++r)  // round-robin so clock drift hits all alike
@@ -956,6 +956,7 @@ int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* al
         auto v = t[static_cast<size_t>(i)];
         std::sort(v.begin(), v.end());
         const double med = v[v.size() / 2];
+        medians[i] = med;
         if (med < *best_ms) {
             *best_ms = med;
             *best = i;

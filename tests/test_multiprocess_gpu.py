@@ -91,3 +91,22 @@ def test_two_processes_one_gpu(coll):
         assert err is None, f"rank {rank}: {err}"
         for strat, (ok, ms) in res.items():
             assert ok, f"rank {rank} strategy {strat} wrong output"
+
+
+def test_bench_two_ranks_shared_device(tmp_path):
+    """bench.py's N>1 path (torchrun, IPC handle exchange, max-over-ranks
+    timing, autotune agreed across ranks) on one GPU shared by two ranks."""
+    import json
+    import subprocess
+    import sys
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, C3_SHARED_DEVICE="1")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(_free_port()), os.path.join(repo, "bench.py"), "--gpus", "2",
+                        "--steps", "3", "--warmup", "3", "--config", "cfg1"],
+                       capture_output=True, text=True, env=env, timeout=400, cwd=repo)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] >= 1
+    assert "CUDA-IPC" in line["config"]["world"]

@@ -1,0 +1,77 @@
+"""Measured C3 sweep on this GPU (loopback worlds): every BASELINE config x
+collective x strategy, in the reference's sweep CSV schema
+(scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal;
+sim.cpp:319-334) plus measured columns. Isolated and concurrent runs are
+interleaved round-robin. usage: python tools/c3_sweep.py OUT.csv [rounds]"""
+import os
+import statistics
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import paper_2412_14335_b200 as c3  # noqa: E402
+from bench import CONFIGS  # noqa: E402
+
+KIND = {"all-gather": c3.ALL_GATHER, "all-to-all": c3.ALL_TO_ALL,
+        "reduce-scatter": c3.REDUCE_SCATTER}
+
+
+def main():
+    out_path = sys.argv[1]
+    R = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    rows = ["scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
+            "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world"]
+    for name in ("cfg2", "cfg2_448", "cfg3", "cfg4", "cfg4_mb"):
+        cfg = CONFIGS[name]
+        colls = [cfg["coll"]] + (["all-to-all"] if cfg["coll"] == "all-gather" else [])
+        for coll in colls:
+            w = c3.World(0, 8, 0, loopback=True)
+            s = c3.Session(w, cfg["m"], cfg["n"], cfg["k"], KIND[coll], cfg["payload"])
+            s.load_tables(os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv"))
+            s.fill()
+            full = w.info.sm_count
+            jobs = {"gemm": (c3.GEMM_ONLY, s.default_alloc(c3.GEMM_ONLY))}
+            a = s.default_alloc(c3.COMM_ONLY_CU)
+            a.cus_comm = full
+            jobs["comm"] = (c3.COMM_ONLY_CU, a)
+            for st in range(1, 7):
+                jobs[c3.STRATEGY_NAMES[st]] = (st, s.default_alloc(st))
+            for ctas in (16, 32, 64):  # B200 co-resident SM variants
+                a = s.default_alloc(c3.C3_BASE)
+                a.cus_gemm, a.cus_comm = full, ctas
+                jobs[f"c3_base_coresident{ctas}"] = (c3.C3_BASE, a)
+            t = {k: [] for k in jobs}
+            for r in range(R + 1):
+                for k, (st, al) in jobs.items():
+                    tm = s.run(st, al)
+                    if r:
+                        t[k].append(tm)
+            med = lambda k, f: statistics.median(f(x) for x in t[k])  # noqa: E731
+            tg = med("gemm", lambda x: x.gemm_end_ms - x.gemm_start_ms)
+            tc = med("comm", lambda x: x.comm_end_ms - x.comm_start_ms)
+            ideal = c3.ideal_speedup(tg, tc)
+            tax = "G-long" if tg > 1.15 * tc else "C-long" if tc > 1.15 * tg else "GC-equal"
+            sid = f"{name}_{cfg['payload'] >> 20}M"
+            flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
+            rows.append(f"{sid},{coll},{tax},serial,{(tg + tc) / 1e3:.6g},1,{ideal:.6g},0,{tg:.4f},"
+                        f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,loopback-8")
+            for k, (st, al) in jobs.items():
+                if k in ("gemm", "comm"):
+                    continue
+                mk = med(k, lambda x: x.total_ms)
+                gk = med(k, lambda x: x.gemm_end_ms - x.gemm_start_ms)
+                sp = (tg + tc) / mk
+                rows.append(f"{sid},{coll},{tax},{k},{mk / 1e3:.6g},{sp:.6g},{ideal:.6g},"
+                            f"{c3.fraction_of_ideal(sp, ideal):.6g},{tg:.4f},{tc:.4f},"
+                            f"{flops / gk / 1e9:.1f},{al.cus_gemm},{al.cus_comm},"
+                            f"{'DMA' if al.backend else 'CU'},loopback-8")
+            s.close()
+            w.close()
+            print(f"{sid} {coll} done", file=sys.stderr, flush=True)
+    with open(out_path, "w") as f:
+        f.write("\n".join(rows) + "\n")
+    print("\n".join(rows))
+
+
+if __name__ == "__main__":
+    main()
