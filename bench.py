@@ -167,6 +167,9 @@ def run_ours(args, dist):
         sess.set_barrier(dist.barrier)
     tables = os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv")
     sess.load_tables(tables)
+    params = os.path.join(REPO, "data", "b200-loopback-params.json")
+    if os.path.exists(params):
+        sess.load_params(params)
     strategies = [c3.STRATEGY_NAMES.index(s) for s in args.strategies]
 
     def timed(strategy, steps, alloc=None):
@@ -304,7 +307,8 @@ def run_ours(args, dist):
                         "cus_idle": head_alloc.cus_idle,
                         "backend": "DMA" if backend == c3.BACKEND_DMA else "CU"},
               "predicted_ms": predicted, "measured_ms": t_conc, "autotune": tune,
-              "measured_best_default_alloc": measured_best, "tables": os.path.relpath(tables, REPO)}
+              "measured_best_default_alloc": measured_best, "tables": os.path.relpath(tables, REPO),
+              "penalties": "data/b200-loopback-params.json (fitted, tools/calibrate_penalties.py)"}
 
     # ---- e2e through the C ABI with host buffers ----
     p = sess.pointers(0)

@@ -234,8 +234,15 @@ int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
  * allocation. allow_dma = 0 excludes conccl/conccl_rp (e.g. loopback worlds,
  * where same-device copies are SM copies). */
 int c3_session_load_tables(c3_session* s, const char* csv_path);
+/* Co-run penalties for the predictor from a params JSON (params_io.hpp:18-19),
+ * e.g. data/b200-loopback-params.json fitted by `c3sim calibrate` on measured
+ * B200 speedups (tools/calibrate_penalties.py). Default: unit penalties. */
+int c3_session_load_params(c3_session* s, const char* params_json_path);
 int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, double t_comm_dma_ms,
                       int allow_dma, int* strategy, c3_alloc* alloc, double* predicted_ms);
+/* The model's predicted makespan of one strategy (same inputs as choose). */
+int c3_session_predict(c3_session* s, int strategy, double t_gemm_ms, double t_comm_cu_ms,
+                       double t_comm_dma_ms, double* predicted_ms);
 /* Measured refinement: run each (strategy, alloc) candidate `rounds` times in
  * round-robin order; medians[i] = candidate i's median step time, *best =
  * this rank's fastest. Multi-process: every rank must pass the same

@@ -126,12 +126,22 @@ class Session:
     def load_tables(self, csv_path):
         check(lib().c3_session_load_tables(self.h, csv_path.encode()))
 
+    def load_params(self, json_path):
+        check(lib().c3_session_load_params(self.h, json_path.encode()))
+
     def choose(self, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms=0.0, allow_dma=True):
         """Runtime heuristic: (strategy, alloc, predicted_ms)."""
         st, a, pred = C.c_int(), _capi.Alloc(), C.c_double()
         check(lib().c3_session_choose(self.h, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms,
                                       int(bool(allow_dma)), C.byref(st), C.byref(a), C.byref(pred)))
         return st.value, a, pred.value
+
+    def predict(self, strategy, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms=0.0):
+        """Model-layer predicted makespan (ms) of one strategy."""
+        ms = C.c_double()
+        check(lib().c3_session_predict(self.h, strategy, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms,
+                                       C.byref(ms)))
+        return ms.value
 
     def autotune(self, candidates, rounds=3, reduce_max=None):
         """candidates: [(strategy, Alloc)] -> (best index, median ms). With

@@ -29,6 +29,7 @@
 #include "c3cuda_internal.hpp"
 #include "c3sim/conccl.hpp"
 #include "c3sim/errors.hpp"
+#include "c3sim/params_io.hpp"
 #include "c3sim/sim.hpp"
 
 namespace c3k {
@@ -281,6 +282,7 @@ struct c3_session {
                 ev_ce = nullptr, ev_end = nullptr;
     c3sim::MachineDescriptor md;
     c3sim::SlowdownTableSet tables;
+    c3sim::CoRunPenalty penalties = c3sim::CoRunPenalty::ones();  // c3_session_load_params
     c3sim::C3Scenario scenario;
 };
 
@@ -881,6 +883,56 @@ int c3_session_load_tables(c3_session* s, const char* csv_path) {
     });
 }
 
+namespace {
+
+// Model-layer prediction of one strategy's makespan (seconds) from measured
+// isolated times; see c3_session_choose.
+double predict_makespan(c3_session* s, int st, double t_gemm_ms, double t_comm_cu_ms,
+                        double t_comm_dma_ms) {
+    c3sim::EfficiencyParams eff;
+    eff.comm_launch_overhead_cu = 0.0;  // measured times include launch
+    const c3sim::CoRunPenalty& pen = s->penalties;
+    c3sim::C3Scenario x = s->scenario;
+    x.gemm.measured_time = t_gemm_ms * 1e-3;
+    x.gemm.boundedness_override =
+        c3sim::classify_gemm_boundedness(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
+    const bool dma = st == C3_CONCCL || st == C3_CONCCL_RP;
+    x.collective.measured_time = (dma ? t_comm_dma_ms : t_comm_cu_ms) * 1e-3;
+    if (st == C3_SERIAL) return (t_gemm_ms + t_comm_cu_ms) * 1e-3;
+    c3sim::MachineDescriptor md = s->md;
+    if (dma && s->chunk > 0) {
+        md.cpu_launch_overhead = 0.0;
+        md.dma_sync_overhead = 0.0;
+        md.link_bandwidth_unidir =
+            static_cast<double>(s->chunk) / (eff.efficiency * t_comm_dma_ms * 1e-3);
+    }
+    return c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff).makespan;
+}
+
+}  // namespace
+
+int c3_session_load_params(c3_session* s, const char* params_json_path) {
+    if (!s || !params_json_path) return set_error(C3_ERR_VALIDATION, "c3_session_load_params: null argument");
+    return guarded([&] {
+        s->penalties = c3sim::load_params_file(params_json_path).penalties;
+        return C3_OK;
+    });
+}
+
+int c3_session_predict(c3_session* s, int strategy, double t_gemm_ms, double t_comm_cu_ms,
+                       double t_comm_dma_ms, double* predicted_ms) {
+    if (!s || !predicted_ms) return set_error(C3_ERR_VALIDATION, "c3_session_predict: null argument");
+    if (strategy < C3_SERIAL || strategy > C3_CONCCL_RP)
+        return set_error(C3_ERR_UNKNOWN, "unknown strategy " + std::to_string(strategy));
+    const bool dma = strategy == C3_CONCCL || strategy == C3_CONCCL_RP;
+    if (!(t_gemm_ms > 0 && t_comm_cu_ms > 0) || (dma && !(t_comm_dma_ms > 0)))
+        return set_error(C3_ERR_VALIDATION, "c3_session_predict: isolated times must be positive");
+    return guarded([&] {
+        *predicted_ms = predict_makespan(s, strategy, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms) * 1e3;
+        return C3_OK;
+    });
+}
+
 // Runtime strategy heuristic: predict every strategy's makespan with the
 // model layer's simulate() (sim.cpp:121-215) fed with this GPU's measured
 // isolated times (GemmKernel/CollectiveOp::measured_time, workload.hpp:23,34)
@@ -895,38 +947,24 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
     if (!(t_gemm_ms > 0 && t_comm_cu_ms > 0))
         return set_error(C3_ERR_VALIDATION, "c3_session_choose: isolated times must be positive");
     return guarded([&] {
-        c3sim::EfficiencyParams eff;
-        eff.comm_launch_overhead_cu = 0.0;  // measured times include launch
-        const c3sim::CoRunPenalty pen = c3sim::CoRunPenalty::ones();
-        c3sim::C3Scenario sc = s->scenario;
-        sc.gemm.measured_time = t_gemm_ms * 1e-3;
-        sc.gemm.boundedness_override =
-            c3sim::classify_gemm_boundedness(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
-        double best = (t_gemm_ms + std::min(t_comm_cu_ms, allow_dma && t_comm_dma_ms > 0
-                                                               ? t_comm_dma_ms : t_comm_cu_ms)) * 1e-3;
+        const bool use_dma = allow_dma && t_comm_dma_ms > 0;
+        double best = (t_gemm_ms + std::min(t_comm_cu_ms, use_dma ? t_comm_dma_ms : t_comm_cu_ms)) * 1e-3;
         int best_st = C3_SERIAL;
         for (int st = C3_C3_BASE; st <= C3_CONCCL_RP; ++st) {
             const bool dma = st == C3_CONCCL || st == C3_CONCCL_RP;
-            if (dma && (!allow_dma || !(t_comm_dma_ms > 0))) continue;
-            c3sim::C3Scenario x = sc;
-            x.collective.measured_time = (dma ? t_comm_dma_ms : t_comm_cu_ms) * 1e-3;
-            c3sim::MachineDescriptor md = s->md;
-            if (dma && s->chunk > 0) {
-                md.cpu_launch_overhead = 0.0;
-                md.dma_sync_overhead = 0.0;
-                md.link_bandwidth_unidir = static_cast<double>(s->chunk) /
-                                           (eff.efficiency * t_comm_dma_ms * 1e-3);
-            }
-            const c3sim::SimTimeline tl =
-                c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff);
-            if (tl.makespan < best) {
-                best = tl.makespan;
+            if (dma && !use_dma) continue;
+            const double m = predict_makespan(s, st, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms);
+            if (m < best) {
+                best = m;
                 best_st = st;
             }
         }
         *strategy = best_st;
         *predicted_ms = best * 1e3;
-        c3sim::C3Scenario x = sc;
+        c3sim::EfficiencyParams eff;
+        eff.comm_launch_overhead_cu = 0.0;
+        c3sim::C3Scenario x = s->scenario;
+        x.gemm.measured_time = t_gemm_ms * 1e-3;
         x.collective.measured_time = t_comm_cu_ms * 1e-3;
         const c3sim::Allocation a =
             c3sim::allocate_cus(x, static_cast<c3sim::Strategy>(best_st), s->md, s->tables, eff);

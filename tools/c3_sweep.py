@@ -20,7 +20,8 @@ def main():
     out_path = sys.argv[1]
     R = int(sys.argv[2]) if len(sys.argv) > 2 else 5
     rows = ["scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
-            "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world"]
+            "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
+            "predicted_makespan_s"]
     for name in ("cfg2", "cfg2_448", "cfg3", "cfg4", "cfg4_mb"):
         cfg = CONFIGS[name]
         colls = [cfg["coll"]] + (["all-to-all"] if cfg["coll"] == "all-gather" else [])
@@ -28,12 +29,15 @@ def main():
             w = c3.World(0, 8, 0, loopback=True)
             s = c3.Session(w, cfg["m"], cfg["n"], cfg["k"], KIND[coll], cfg["payload"])
             s.load_tables(os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv"))
+            if os.path.exists(os.path.join(REPO, "data", "b200-loopback-params.json")):
+                s.load_params(os.path.join(REPO, "data", "b200-loopback-params.json"))
             s.fill()
             full = w.info.sm_count
             jobs = {"gemm": (c3.GEMM_ONLY, s.default_alloc(c3.GEMM_ONLY))}
             a = s.default_alloc(c3.COMM_ONLY_CU)
             a.cus_comm = full
             jobs["comm"] = (c3.COMM_ONLY_CU, a)
+            jobs["comm_dma"] = (c3.COMM_ONLY_DMA, s.default_alloc(c3.COMM_ONLY_DMA))
             for st in range(1, 7):
                 jobs[c3.STRATEGY_NAMES[st]] = (st, s.default_alloc(st))
             for ctas in (16, 32, 64):  # B200 co-resident SM variants
@@ -49,22 +53,25 @@ def main():
             med = lambda k, f: statistics.median(f(x) for x in t[k])  # noqa: E731
             tg = med("gemm", lambda x: x.gemm_end_ms - x.gemm_start_ms)
             tc = med("comm", lambda x: x.comm_end_ms - x.comm_start_ms)
+            td = med("comm_dma", lambda x: x.comm_end_ms - x.comm_start_ms)
             ideal = c3.ideal_speedup(tg, tc)
             tax = "G-long" if tg > 1.15 * tc else "C-long" if tc > 1.15 * tg else "GC-equal"
             sid = f"{name}_{cfg['payload'] >> 20}M"
             flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
             rows.append(f"{sid},{coll},{tax},serial,{(tg + tc) / 1e3:.6g},1,{ideal:.6g},0,{tg:.4f},"
-                        f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,loopback-8")
+                        f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,loopback-8,"
+                        f"{s.predict(c3.SERIAL, tg, tc, td) / 1e3:.6g}")
             for k, (st, al) in jobs.items():
-                if k in ("gemm", "comm"):
+                if k in ("gemm", "comm", "comm_dma"):
                     continue
+                pred = (s.predict(st, tg, tc, td) / 1e3) if "coresident" not in k else float("nan")
                 mk = med(k, lambda x: x.total_ms)
                 gk = med(k, lambda x: x.gemm_end_ms - x.gemm_start_ms)
                 sp = (tg + tc) / mk
                 rows.append(f"{sid},{coll},{tax},{k},{mk / 1e3:.6g},{sp:.6g},{ideal:.6g},"
                             f"{c3.fraction_of_ideal(sp, ideal):.6g},{tg:.4f},{tc:.4f},"
                             f"{flops / gk / 1e9:.1f},{al.cus_gemm},{al.cus_comm},"
-                            f"{'DMA' if al.backend else 'CU'},loopback-8")
+                            f"{'DMA' if al.backend else 'CU'},loopback-8,{pred:.6g}")
             s.close()
             w.close()
             print(f"{sid} {coll} done", file=sys.stderr, flush=True)
