@@ -53,6 +53,9 @@ CONFIGS = {
     "cfg3": dict(desc="LLaMA-70B backward: weight-grad GEMM 8192x28672x8192 bf16 || "
                       "gradient reduce-scatter 896 MiB",
                  m=8192, n=28672, k=8192, coll="reduce-scatter", payload=896 * MIB),
+    "cfg2_a2a": dict(desc="LLaMA-70B FFN GEMM 8192x28672x8192 || 896 MiB all-to-all (the "
+                          "reference dataset's second collective kind, SURVEY §8(f) F1)",
+                     m=8192, n=28672, k=8192, coll="all-to-all", payload=896 * MIB),
     "cfg4": dict(desc="LLaMA-405B FSDP layer: GEMM 8192x53248x16384 bf16 || all-gather 1664 MiB",
                  m=8192, n=53248, k=16384, coll="all-gather", payload=1664 * MIB),
     "cfg4_mb": dict(desc="LLaMA-405B small-token (memory-bound) GEMM 128x53248x16384 || "
@@ -157,7 +160,8 @@ def run_ours(args, dist):
     device = 0 if os.environ.get("C3_SHARED_DEVICE") else dist.local_rank
     torch.cuda.set_device(device)
     world = c3.World(dist.rank, n, device, loopback=loopback)
-    coll = c3.ALL_GATHER if cfg["coll"] == "all-gather" else c3.REDUCE_SCATTER
+    coll = {"all-gather": c3.ALL_GATHER, "all-to-all": c3.ALL_TO_ALL,
+            "reduce-scatter": c3.REDUCE_SCATTER}[cfg["coll"]]
     sess = c3.Session(world, cfg["m"], cfg["n"], cfg["k"], coll, cfg["payload"])
     if not loopback:
         sess.import_handles(dist.allgather_bytes(sess.export_handles()))
@@ -210,6 +214,15 @@ def run_ours(args, dist):
     for st in strategies:
         if st != c3.SERIAL:
             strat_jobs[c3.STRATEGY_NAMES[st]] = (st, sess.default_alloc(st))
+    # B200 extension: collective fused into the CTA-pair GEMM (TMA bulk copies)
+    fused_ok = coll != c3.REDUCE_SCATTER
+    if fused_ok:
+        try:
+            sess.run(c3.FUSED, sess.default_alloc(c3.FUSED))
+        except c3.C3Error:
+            fused_ok = False  # shape not on the CTA-pair kernel
+    if fused_ok:
+        strat_jobs["c3_fused"] = (c3.FUSED, sess.default_alloc(c3.FUSED))
     sweep_rows = rounds({**iso_modes, **strat_jobs}, K)
     iso_comm = {k: median([r[col[k]] for r in sweep_rows[k]]) for k in ("cu", "dma")}
     log("strategy sweep done")
@@ -231,8 +244,11 @@ def run_ours(args, dist):
     for name, (st, a) in strat_jobs.items():
         res = summarise(sweep_rows[name], t_g, iso_comm["dma" if a.backend == c3.BACKEND_DMA else "cu"],
                         best_iso)
+        if st == c3.FUSED:
+            res["note"] = ("collective moved inside the CTA-pair GEMM kernel by its copy warp "
+                           "(TMA bulk copies, 4 KiB pieces); t_comm_iso = SM collective")
         res["alloc"] = {"cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm, "cus_idle": a.cus_idle,
-                        "backend": "DMA" if a.backend == c3.BACKEND_DMA else "CU"}
+                        "backend": ["CU", "DMA", "TMA"][a.backend]}
         if a.backend == c3.BACKEND_DMA and loopback:
             res["note"] = "loopback: same-device copies run on SMs (driver copy kernels), not copy engines"
         results[name] = res
@@ -252,7 +268,9 @@ def run_ours(args, dist):
                 cands.append((st, a))
         if dma_ok:
             cands += [(st, sess.default_alloc(st)) for st in (c3.CONCCL, c3.CONCCL_RP)]
-        best_i, best_ms = sess.autotune(cands, rounds=3, reduce_max=dist.max_list)
+        if fused_ok:
+            cands.append((c3.FUSED, sess.default_alloc(c3.FUSED)))
+        best_i, best_ms = sess.autotune(cands, rounds=5, reduce_max=dist.max_list)
         log(f"autotune done: {best_i}")
         tune = {"candidates": len(cands), "model_pick": c3.STRATEGY_NAMES[head],
                 "picked_index": best_i, "picked_ms": best_ms}
@@ -263,7 +281,7 @@ def run_ours(args, dist):
     head_name = c3.STRATEGY_NAMES[head]
     measured_best = max(results, key=lambda k: results[k]["speedup"]) if results else None
     backend = head_alloc.backend
-    comm_key = "dma" if backend == c3.BACKEND_DMA else "cu"
+    comm_key = "dma" if backend == c3.BACKEND_DMA else "cu"  # fused (TMA) vs the SM collective
 
     # ---- the timed region: K C3 steps of the headline strategy; the isolated
     # GEMM and collective reference runs are interleaved between steps (their
@@ -304,8 +322,7 @@ def run_ours(args, dist):
     choice = {"strategy": head_name, "selected_by": "runtime: model prediction (c3_session_choose) + "
               "measured autotune (c3_session_autotune)" if args.strategy == "auto" else "--strategy",
               "alloc": {"cus_gemm": head_alloc.cus_gemm, "cus_comm": head_alloc.cus_comm,
-                        "cus_idle": head_alloc.cus_idle,
-                        "backend": "DMA" if backend == c3.BACKEND_DMA else "CU"},
+                        "cus_idle": head_alloc.cus_idle, "backend": ["CU", "DMA", "TMA"][backend]},
               "predicted_ms": predicted, "measured_ms": t_conc, "autotune": tune,
               "measured_best_default_alloc": measured_best, "tables": os.path.relpath(tables, REPO),
               "penalties": "data/b200-loopback-params.json (fitted, tools/calibrate_penalties.py)"}

@@ -54,6 +54,12 @@ extern "C" {
 #define C3_C3_SP_RP 4
 #define C3_CONCCL 5
 #define C3_CONCCL_RP 6
+/* B200 extension of the DMA-offload idea (not a reference strategy): the
+ * all-gather / all-to-all is moved INSIDE the CTA-pair GEMM kernel by its idle
+ * warp 3 driving the SM's own TMA unit (cp.async.bulk global -> smem -> local
+ * or NVLink-peer global), paced by the GEMM's load progress — no extra SMs,
+ * kernels or copy-engine round trips. */
+#define C3_FUSED 7
 /* extra execution-only modes (not reference strategies): */
 #define C3_GEMM_ONLY 100 /* isolated GEMM */
 #define C3_COMM_ONLY_CU 101 /* isolated SM-driven collective */
@@ -62,6 +68,7 @@ extern "C" {
 /* c3sim::CommBackend (interference.hpp:14). */
 #define C3_BACKEND_CU 0
 #define C3_BACKEND_DMA 1
+#define C3_BACKEND_TMA 2 /* C3_FUSED: the GEMM kernel's own TMA unit */
 
 typedef struct c3_world c3_world;
 typedef struct c3_session c3_session;
@@ -225,6 +232,11 @@ int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc,
  * a reduce-scatter. Return 0 on success. Not needed for loopback worlds or
  * the SM (P2P) collectives, which signal through peer flags on the device. */
 typedef int (*c3_barrier_fn)(void* ctx);
+/* C3_FUSED pacing: the copies of each CTA finish after this share of the
+ * GEMM's operand loads (default 0 = as fast as possible); piece_bytes =
+ * bytes per bulk copy (16..16384, multiple of 16; default 4096 — small pieces
+ * keep the SM's TMA queue short for the GEMM's operand loads). */
+int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes);
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
 /* Runtime heuristic (the paper's strategy choice, on the product model layer):
  * load measured interference tables (reference SlowdownTable CSV,

@@ -12,8 +12,9 @@ import ctypes as C
 
 from . import _capi
 from ._capi import (ALL_GATHER, ALL_TO_ALL, REDUCE_SCATTER, SERIAL, C3_BASE, C3_SP, C3_RP,
-                    C3_SP_RP, CONCCL, CONCCL_RP, GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA,
-                    STRATEGY_NAMES, BACKEND_CU, BACKEND_DMA, C3Error, check, lib, ptr_array)
+                    C3_SP_RP, CONCCL, CONCCL_RP, FUSED, GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA,
+                    STRATEGY_NAMES, BACKEND_CU, BACKEND_DMA, BACKEND_TMA, C3Error, check, lib,
+                    ptr_array)
 
 __all__ = ["World", "Session", "plan_transfers", "ideal_speedup", "fraction_of_ideal",
            "STRATEGY_NAMES", "C3Error"]
@@ -125,6 +126,9 @@ class Session:
 
     def load_tables(self, csv_path):
         check(lib().c3_session_load_tables(self.h, csv_path.encode()))
+
+    def set_fused_pace(self, pace=0.0, piece_bytes=4096):
+        check(lib().c3_session_set_fused_pace(self.h, pace, piece_bytes))
 
     def load_params(self, json_path):
         check(lib().c3_session_load_params(self.h, json_path.encode()))

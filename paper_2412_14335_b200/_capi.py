@@ -19,9 +19,11 @@ ERR_NAMES = {2: "IoError", 3: "UnknownEntityError", 4: "ValidationError", 5: "Fi
 
 ALL_GATHER, ALL_TO_ALL, REDUCE_SCATTER = 0, 1, 2
 SERIAL, C3_BASE, C3_SP, C3_RP, C3_SP_RP, CONCCL, CONCCL_RP = range(7)
+FUSED = 7  # B200 extension: collective moved inside the GEMM kernel by its TMA unit
 GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA = 100, 101, 102
-STRATEGY_NAMES = ["serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp"]
-BACKEND_CU, BACKEND_DMA = 0, 1
+STRATEGY_NAMES = ["serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp",
+                  "c3_fused"]
+BACKEND_CU, BACKEND_DMA, BACKEND_TMA = 0, 1, 2
 IPC_HANDLE_BYTES = 64
 SESSION_HANDLE_BYTES = 4 * IPC_HANDLE_BYTES
 MAX_RANKS = 8
@@ -102,6 +104,7 @@ SIGNATURES = {
     "c3_session_run_all_ranks": (I, [P, I, C.POINTER(Alloc), C.POINTER(Timing)]),
     "c3_session_default_alloc": (I, [P, I, C.POINTER(Alloc)]),
     "c3_session_set_barrier": (I, [P, C.c_void_p, P]),
+    "c3_session_set_fused_pace": (I, [P, C.c_float, I]),
     "c3_session_load_tables": (I, [P, C.c_char_p]),
     "c3_session_load_params": (I, [P, C.c_char_p]),
     "c3_session_predict": (I, [P, I, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),

@@ -73,7 +73,9 @@ struct GemmPlan {
 };
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
                    int64_t k, int* counters, int sm_count);
-int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream);
+struct FusedComm;
+int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
+                     const FusedComm* fc = nullptr);
 
 // ------------------------------------------------------------ collectives
 // Cross-process completion signalling for the SM-driven collectives.
@@ -86,6 +88,22 @@ struct Signals {
     uint32_t* done = nullptr;
     uint32_t epoch = 0;
     bool enabled = false;
+};
+
+// Fused C3 (collective moved by the GEMM's own copy warp + TMA unit).
+constexpr int kFusedExitSlot = 40;  // signal-array words [40,48)
+struct FusedComm {
+    int enabled = 0;
+    int kind = 0;                    // 0 all-gather, 1 all-to-all
+    int n = 1;                       // ranks
+    int self_begin = 0, self_end = 0;  // ranks whose share this launch moves
+    int skip_self = 1;               // AG: own slot already in place
+    int64_t chunk = 0;               // bytes per slot
+    const uint8_t* src[C3_MAX_RANKS] = {};  // AG: rank v's own chunk; A2A: send base
+    uint8_t* dst[C3_MAX_RANKS] = {};        // rank q's receive base
+    float pace = 0.0f;               // finish copies by this share of the GEMM's loads (0 = unpaced)
+    int64_t piece = 4096;            // bytes per bulk copy (<= 16 KiB buffer)
+    Signals sig;
 };
 
 struct PtrTable {

@@ -17,6 +17,9 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <string>
+
 #include "c3cuda_internal.hpp"
 #include "ptx.cuh"
 
@@ -68,7 +71,8 @@ constexpr int kAgExit = 0, kRsEntry = 8, kRsExit = 16;
 
 __global__ void __launch_bounds__(kThreads)
 ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, int n,
-                   int64_t nvec, int64_t slot_vec, int copy_self, Signals sig) {
+                   int64_t nvec, int64_t slot_vec, int copy_self, int stream_l2, Signals sig) {
+    const uint64_t pol = policy_evict_first();
     uint4* dst[C3_MAX_RANKS];
 #pragma unroll
     for (int j = 0; j < C3_MAX_RANKS; ++j)
@@ -80,7 +84,7 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
             const int64_t i = base + static_cast<int64_t>(u) * kThreads;
-            if (i < nvec) v[u] = ld_nc_v4(src + i);
+            if (i < nvec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
         }
         // peers in rotated order so the ranks do not all start on the same target
         for (int j = 1; j <= n; ++j) {
@@ -90,7 +94,12 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kThreads;
-                if (i < nvec) st_v4(d + i, v[u]);
+                if (i < nvec) {
+                    if (stream_l2)
+                        st_stream_v4(d + i, v[u], pol);
+                    else
+                        st_v4(d + i, v[u]);
+                }
             }
         }
     }
@@ -117,7 +126,8 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
 // of rank `self`'s send buffer goes to slot `self` of rank p's receive buffer.
 __global__ void __launch_bounds__(kThreads)
 a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, int n,
-                    int64_t slot_vec, Signals sig) {
+                    int64_t slot_vec, int stream_l2, Signals sig) {
+    const uint64_t pol = policy_evict_first();
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
     for (int j = 0; j < n; ++j) {
         const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
@@ -129,12 +139,17 @@ a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, 
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kThreads;
-                if (i < slot_vec) v[u] = ld_nc_v4(src + i);
+                if (i < slot_vec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kThreads;
-                if (i < slot_vec) st_v4(dst + i, v[u]);
+                if (i < slot_vec) {
+                    if (stream_l2)
+                        st_stream_v4(dst + i, v[u], pol);
+                    else
+                        st_v4(dst + i, v[u]);
+                }
             }
         }
     }
@@ -164,7 +179,8 @@ __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& v) {
 template <int N>
 __global__ void __launch_bounds__(kThreads)
 rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
-                   int64_t slot_vec, Signals sig) {
+                   int64_t slot_vec, int stream_l2, Signals sig) {
+    const uint64_t pol = policy_evict_first();
     if (sig.enabled) entry_barrier(sig, self, N, kRsEntry);
     const uint4* src[N];
 #pragma unroll
@@ -178,7 +194,8 @@ rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
             const int64_t i = base + static_cast<int64_t>(u) * kThreads;
             if (i < nvec)
 #pragma unroll
-                for (int g = 0; g < N; ++g) v[u][g] = ld_v4(src[g] + i);
+                for (int g = 0; g < N; ++g)
+                    v[u][g] = stream_l2 ? ld_stream_v4(src[g] + i, pol) : ld_v4(src[g] + i);
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -191,7 +208,10 @@ rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
             __nv_bfloat162* h = reinterpret_cast<__nv_bfloat162*>(&o);
 #pragma unroll
             for (int j = 0; j < 4; ++j) h[j] = __floats2bfloat162_rn(acc[2 * j], acc[2 * j + 1]);
-            st_v4(out + i, o);
+            if (stream_l2)
+                st_stream_v4(out + i, o, pol);
+            else
+                st_v4(out + i, o);
         }
     }
     if (sig.enabled) exit_barrier(sig, self, N, kRsExit);
@@ -253,6 +273,16 @@ uint64_t label_key(uint64_t seed, int rank, int tensor) {
            (static_cast<uint64_t>(static_cast<uint32_t>(tensor)) << 48);
 }
 
+// L2 evict-first streaming of collective payloads (default on; C3_COMM_L2=normal
+// switches it off for A/B measurements).
+int stream_l2_enabled() {
+    static const int on = [] {
+        const char* e = std::getenv("C3_COMM_L2");
+        return (e != nullptr && std::string(e) == "normal") ? 0 : 1;
+    }();
+    return on;
+}
+
 int grid_for(int64_t work_items, int threads, int cap) {
     const int64_t g = (work_items + threads - 1) / threads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, cap)));
@@ -276,7 +306,8 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
         const int64_t nvec = chunk_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
         ag_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
-                                                         n, nvec, nvec, in_place ? 0 : 1, sig);
+                                                         n, nvec, nvec, in_place ? 0 : 1,
+                                                         stream_l2_enabled(), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(chunk_bytes, 1), kThreads, n_ctas);
         ag_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
@@ -299,7 +330,7 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
         const int64_t nvec = per_peer_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
         a2a_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
-                                                          n, nvec, sig);
+                                                          n, nvec, stream_l2_enabled(), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(per_peer_bytes, 1), kThreads, n_ctas);
         a2a_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
@@ -325,7 +356,8 @@ int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, i
         switch (n) {
 #define C3_RS_CASE(N)                                                                          \
     case N:                                                                                    \
-        rs_pull_vec_kernel<N><<<grid, kThreads, 0, stream>>>(in, o, self, nvec, nvec, sig);    \
+        rs_pull_vec_kernel<N><<<grid, kThreads, 0, stream>>>(in, o, self, nvec, nvec,          \
+                                                             stream_l2_enabled(), sig);         \
         break;
             C3_RS_CASE(1) C3_RS_CASE(2) C3_RS_CASE(3) C3_RS_CASE(4)
             C3_RS_CASE(5) C3_RS_CASE(6) C3_RS_CASE(7) C3_RS_CASE(8)

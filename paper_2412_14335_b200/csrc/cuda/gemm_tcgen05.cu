@@ -324,7 +324,7 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStre
 
 }  // namespace
 
-int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream);
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc);
 
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
                    int64_t k, int* counters, int sm_count) {
@@ -371,12 +371,16 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     return C3_OK;
 }
 
-int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream) {
+int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
+                     const FusedComm* fc) {
     int grid = max_ctas > 0 ? max_ctas : sm_count;
     grid = std::min(grid, sm_count);
+    if (fc && (plan->kind != GemmPlan::kPair || grid < 2))
+        return set_error(C3_ERR_UNSUPPORTED, "fused C3 needs the CTA-pair GEMM (M >= 256, enough tiles)");
     if (plan->kind == GemmPlan::kPair && grid >= 2) {
-        grid = std::min(grid / 2, plan->num_tiles) * 2;  // whole CTA pairs
-        return gemm_pair_launch(plan, grid, stream);
+        // whole CTA pairs; a fused launch keeps every pair (its copy warps move data)
+        grid = fc ? grid / 2 * 2 : std::min(grid / 2, plan->num_tiles) * 2;
+        return gemm_pair_launch(plan, grid, stream, fc);
     }
     if (plan->kind == GemmPlan::kWide) return launch_bn<256>(plan, plan->map_b256, grid, stream);
     return launch_bn<128>(plan, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap

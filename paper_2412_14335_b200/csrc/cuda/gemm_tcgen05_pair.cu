@@ -44,6 +44,9 @@ constexpr uint32_t B_STAGE = 128 * BK * 2;  // this CTA's 128 rows of B
 constexpr uint32_t STAGE = A_STAGE + B_STAGE;
 constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;
 constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 512;
+// fused C3: two 16 KiB copy buffers in the shared memory the GEMM leaves free
+constexpr uint32_t PIECE = 16 * 1024;
+constexpr uint32_t SMEM_FUSED = SMEM + 2 * PIECE + 64;
 
 struct Params {
     int m, n, k;
@@ -52,6 +55,7 @@ struct Params {
     int ldc;
     int* tile_counter;
     int* exit_counter;
+    FusedComm fc;  // only read by the FUSED instantiation
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
@@ -63,6 +67,61 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
     tn = in_band / rows;
 }
 
+// Fused C3 copy engine (warp 3, one thread, FUSED only): this rank's share of
+// the collective moved by the SM's own TMA unit with bulk async copies —
+// global -> 16 KiB shared buffer -> every destination (local or NVLink peer) —
+// double-buffered, and paced so item k of this CTA's n items starts once the
+// CTA's producer has issued k/n * pace of its expected k-blocks. Work items
+// are spread round-robin over the grid. AG: item = (rank v, piece j), one load,
+// n-1 stores; A2A: item = (v, dest q, piece j), one load, one store.
+__device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
+                                const uint32_t* progress, const volatile uint32_t* producer_done) {
+    const FusedComm& fc = p.fc;
+    const uint64_t pol = policy_evict_first();
+    const int64_t piece = fc.piece;  // <= PIECE (the buffer size)
+    const int64_t pieces = (fc.chunk + piece - 1) / piece;
+    const int nv = fc.self_end - fc.self_begin;
+    const int64_t per_v = fc.kind == 0 ? pieces : pieces * fc.n;
+    const int64_t total = per_v * nv;
+    const int64_t G = gridDim.x;
+    const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + G - 1) / G : 0;
+    // expected producer k-blocks of this CTA over the GEMM (pair tiles / pairs)
+    const double est_kb = static_cast<double>((p.num_tiles + G / 2 - 1) / (G / 2)) * p.k_blocks;
+    int64_t k = 0;
+    for (int64_t w = blockIdx.x; w < total; w += G, ++k) {
+        const int b = static_cast<int>(k & 1);
+        if (k >= 2) bulk_wait_read<1>();  // buffer b's stores (group k-2) done reading
+        if (fc.pace > 0.f && mine > 0) {
+            const uint32_t target = static_cast<uint32_t>(est_kb * fc.pace * k / mine);
+            while (ld_volatile_shared(progress) < target && !*producer_done) __nanosleep(256);
+        }
+        const int v = fc.self_begin + static_cast<int>(w / per_v);
+        const int64_t r = w % per_v;
+        const int q = fc.kind == 0 ? -1 : static_cast<int>(r / pieces);
+        const int64_t j = fc.kind == 0 ? r : r % pieces;
+        const int64_t off = j * piece;
+        const int64_t left = fc.chunk - off;
+        const uint32_t len = static_cast<uint32_t>(left < piece ? left : piece);
+        const uint8_t* src = fc.src[v] + (fc.kind == 0 ? 0 : static_cast<int64_t>(q) * fc.chunk) + off;
+        mbar_arrive_expect_tx(&lbar[b], len);
+        bulk_load(buf + b * PIECE, src, len, &lbar[b], pol);
+        mbar_wait(&lbar[b], static_cast<uint32_t>((k >> 1) & 1));
+        if (fc.kind == 0) {
+            for (int t = 1; t <= fc.n; ++t) {
+                const int d = (v + t) % fc.n;  // rotated targets
+                if (d == v && fc.skip_self) continue;
+                bulk_store(fc.dst[d] + static_cast<int64_t>(v) * fc.chunk + off, buf + b * PIECE, len, pol);
+            }
+        } else {
+            bulk_store(fc.dst[q] + static_cast<int64_t>(v) * fc.chunk + off, buf + b * PIECE, len, pol);
+        }
+        bulk_commit();
+    }
+    bulk_wait_all();
+    fence_proxy_async_global();
+}
+
+template <bool FUSED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b, const Params p) {
@@ -80,6 +139,11 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     uint64_t* tile_empty = tile_full + RING;
     int* tile_ring = reinterpret_cast<int*>(tile_empty + RING);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + RING);
+    // fused C3 state (FUSED only): copy buffers after the ring, 1 KiB aligned
+    uint64_t* lbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [2] copy loads
+    uint32_t* progress = reinterpret_cast<uint32_t*>(lbar + 2);   // producer k-blocks issued
+    uint32_t* producer_done = progress + 1;
+    uint8_t* copy_buf = smem + STAGES * STAGE + 1024;
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -100,6 +164,12 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         for (int r = 0; r < RING; ++r) {
             mbar_init(&tile_full[r], 1);
             mbar_init(&tile_empty[r], 10);
+        }
+        if (FUSED) {
+            mbar_init(&lbar[0], 1);
+            mbar_init(&lbar[1], 1);
+            *progress = 0;
+            *producer_done = 0;
         }
         fence_mbar_init();
     }
@@ -141,6 +211,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
                 tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, keep);
                 tma_load_2d_pair(smem_b + stage * B_STAGE, &map_b, &full[stage], kb * BK, b_row, keep);
+                if (FUSED) st_volatile_shared(progress, ld_volatile_shared(progress) + 1);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -148,6 +219,9 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             }
             tile = next;
         }
+        if (FUSED) st_volatile_shared(producer_done, 1);
+    } else if (FUSED && warp == 3 && lane == 0) {
+        if (p.fc.enabled) fused_copy_loop(p, copy_buf, lbar, progress, producer_done);
     } else if (warp == 1 && lane == 0 && leader) {
         // ------------- MMA issuer (leader only) -------------
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
@@ -265,6 +339,22 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         tc_fence_after();
         tmem_dealloc_pair<TMEM_COLS>(tmem_base);
     }
+    // fused C3 across processes: once every CTA's copies are complete, the
+    // last CTA tells every peer and waits for all of them (peer flag words)
+    if (FUSED && p.fc.enabled && p.fc.sig.enabled && threadIdx.x == 0) {
+        const Signals& sig = p.fc.sig;
+        fence_sys();
+        if (atomicAdd(sig.done, 1u) == gridDim.x - 1) {
+            fence_sys();
+            for (int q = 0; q < p.fc.n; ++q)
+                if (q != p.fc.self_begin) st_release_sys(sig.peers[q] + kFusedExitSlot + p.fc.self_begin, sig.epoch);
+            for (int q = 0; q < p.fc.n; ++q)
+                if (q != p.fc.self_begin)
+                    while (ld_acquire_sys(sig.mine + kFusedExitSlot + q) < sig.epoch) {
+                    }
+            *sig.done = 0;
+        }
+    }
     if (threadIdx.x == 0 && leader) {
         __threadfence();
         if (atomicAdd(p.exit_counter, 1) == static_cast<int>(gridDim.x / 2) - 1) {
@@ -277,14 +367,19 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 
 }  // namespace gemm2
 
-int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream) {
-    static bool attr_done = false;
-    if (!attr_done) {
-        const cudaError_t e = cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel,
-                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                   static_cast<int>(gemm2::SMEM));
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc) {
+    static bool attr_done[2] = {false, false};
+    const int f = fc != nullptr ? 1 : 0;
+    if (!attr_done[f]) {
+        const cudaError_t e =
+            f ? cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel<true>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(gemm2::SMEM_FUSED))
+              : cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel<false>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     static_cast<int>(gemm2::SMEM));
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm pair)");
-        attr_done = true;
+        attr_done[f] = true;
     }
     gemm2::Params p;
     p.m = static_cast<int>(plan->m);
@@ -298,8 +393,17 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream) {
     p.ldc = static_cast<int>(plan->n);
     p.tile_counter = plan->counters;
     p.exit_counter = plan->counters + 1;
-    gemm2::gemm_bf16_tn_pair_kernel<<<grid, gemm2::THREADS, gemm2::SMEM, stream>>>(plan->map_a,
-                                                                                   plan->map_b128, p);
+    if (fc) {
+        if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
+        p.fc = *fc;
+        p.fc.piece = std::max<int64_t>(16, std::min<int64_t>(fc->piece, gemm2::PIECE)) / 16 * 16;
+        gemm2::gemm_bf16_tn_pair_kernel<true><<<grid, gemm2::THREADS, gemm2::SMEM_FUSED, stream>>>(
+            plan->map_a, plan->map_b128, p);
+    } else {
+        p.fc = FusedComm{};
+        gemm2::gemm_bf16_tn_pair_kernel<false><<<grid, gemm2::THREADS, gemm2::SMEM, stream>>>(
+            plan->map_a, plan->map_b128, p);
+    }
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "gemm pair launch");
     return C3_OK;

@@ -273,6 +273,8 @@ struct c3_session {
     uint32_t* sig = nullptr;                // local signal array
     uint32_t* done = nullptr;               // [0] AG counter, [1] RS counter
     uint32_t epoch = 0;
+    float fused_pace = 0.0f;                // C3_FUSED: copies finish by this share of the GEMM (0 = unpaced)
+    int64_t fused_piece = 4096;             // C3_FUSED: bytes per bulk copy
     c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
     void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
@@ -319,7 +321,7 @@ int session_alloc(c3_session* s) {
     }
     C3_CUDA(cudaMalloc(&s->sig, kSigWords * sizeof(uint32_t)));
     C3_CUDA(cudaMemset(s->sig, 0, kSigWords * sizeof(uint32_t)));
-    C3_CUDA(cudaMalloc(&s->done, 4 * sizeof(uint32_t)));
+    C3_CUDA(cudaMalloc(&s->done, 4 * sizeof(uint32_t)));  // [0] AG/A2A [1] RS [2] fused
     C3_CUDA(cudaMemset(s->done, 0, 4 * sizeof(uint32_t)));
     C3_CUDA(cudaStreamCreateWithFlags(&s->main, cudaStreamNonBlocking));
     C3_CUDA(cudaStreamCreateWithPriority(&s->gemm_s, cudaStreamNonBlocking, s->w->prio_lo));
@@ -1003,6 +1005,16 @@ int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* al
     return C3_OK;
 }
 
+int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_fused_pace: null session");
+    if (!(pace >= 0.f && pace <= 1.f)) return set_error(C3_ERR_VALIDATION, "pace must be in [0, 1]");
+    if (piece_bytes < 16 || piece_bytes > 16384 || piece_bytes % 16)
+        return set_error(C3_ERR_VALIDATION, "piece must be a multiple of 16 in [16, 16384]");
+    s->fused_pace = pace;
+    s->fused_piece = piece_bytes;
+    return C3_OK;
+}
+
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
     if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_barrier: null session");
     s->barrier = fn;
@@ -1016,6 +1028,10 @@ int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
     if (strategy >= C3_GEMM_ONLY) {
         *out = {C, strategy == C3_COMM_ONLY_CU ? 32 : 0, 0,
                 strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA : C3_BACKEND_CU, 0};
+        return C3_OK;
+    }
+    if (strategy == C3_FUSED) {
+        *out = {C, 0, 0, C3_BACKEND_TMA, 0};
         return C3_OK;
     }
     if (strategy < C3_SERIAL || strategy > C3_CONCCL_RP)
@@ -1066,6 +1082,47 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     t->gemm_ctas = gemm_ctas;
     t->comm_ctas = a.backend == C3_BACKEND_CU ? comm_ctas : 0;
     int launches = 0;
+
+    if (strategy == C3_FUSED) {
+        if (s->d.collective != C3_ALL_GATHER && s->d.collective != C3_ALL_TO_ALL)
+            return set_error(C3_ERR_UNSUPPORTED, "fused C3 moves all-gather / all-to-all data only");
+        FusedComm fc;
+        fc.enabled = s->n > 1 ? 1 : 0;
+        fc.kind = s->d.collective == C3_ALL_GATHER ? 0 : 1;
+        fc.n = s->n;
+        fc.chunk = s->chunk;
+        fc.pace = s->fused_pace;
+        fc.piece = s->fused_piece;
+        const bool loop = w->loopback != 0;
+        fc.self_begin = loop ? 0 : w->rank;
+        fc.self_end = loop ? ((flags & kRunAllRanks) ? s->n : 1) : w->rank + 1;
+        for (int q = 0; q < s->n; ++q) {
+            const size_t lq = loop ? static_cast<size_t>(q) : 0;
+            fc.dst[q] = static_cast<uint8_t*>(loop ? s->recv[lq] : s->peer_coll[q]);
+            if (loop || q == w->rank) {
+                fc.src[q] = fc.kind == 0 ? static_cast<const uint8_t*>(s->recv[lq]) + s->chunk * q
+                                         : static_cast<const uint8_t*>(s->in[lq]);
+            }
+        }
+        if (!loop && s->n > 1) {
+            fc.sig = make_signals(s, 2);
+        }
+        t->gemm_ctas = gemm_ctas;
+        C3_CUDA(cudaEventRecord(s->ev_start, s->main));
+        C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
+        C3_CUDA(cudaEventRecord(s->ev_gs, gs));
+        C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs, &fc));
+        C3_CUDA(cudaEventRecord(s->ev_ge, gs));
+        C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ge, 0));
+        C3_CUDA(cudaEventRecord(s->ev_end, s->main));
+        C3_CUDA(cudaEventSynchronize(s->ev_end));
+        C3_CUDA(cudaGetLastError());
+        t->gemm_start_ms = t->comm_start_ms = elapsed(s->ev_start, s->ev_gs);
+        t->gemm_end_ms = t->comm_end_ms = elapsed(s->ev_start, s->ev_ge);
+        t->total_ms = elapsed(s->ev_start, s->ev_end);
+        t->launches = 1;
+        return C3_OK;
+    }
 
     C3_CUDA(cudaEventRecord(s->ev_start, s->main));
     const bool do_gemm = strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;

@@ -326,3 +326,46 @@ def test_session_alltoall_all_strategies(torch_mod, c3, n):
                 f"strategy {strat} rank {v}"
     s.close()
     w.close()
+
+
+@pytest.mark.parametrize("collective", [0, 1], ids=["all-gather", "all-to-all"])
+@pytest.mark.parametrize("n", [2, 8])
+@pytest.mark.parametrize("pace", [0.0, 0.8])
+def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace):
+    """C3_FUSED: the collective moved inside the CTA-pair GEMM by its copy warp
+    (TMA bulk copies). Every virtual rank's output bit-exact; GEMM in tolerance."""
+    monkeypatch.setenv("C3_GEMM_KERNEL", "pair")
+    w = c3.World(0, n, 0, loopback=True)
+    M, N, K = 512, 1024, 512
+    payload = n * ((3 << 16) + 48)  # slots not a multiple of the 16 KiB piece
+    s = c3.Session(w, M, N, K, collective, payload)
+    s.set_fused_pace(pace)
+    s.fill(SEED)
+    t = s.run(c3.FUSED, all_ranks=True)
+    assert t.launches == 1
+    chunk = payload // n
+    for v in range(n):
+        got = np.empty(payload, np.uint8)
+        c3.check(c3.lib().c3_memcpy(got.ctypes.data, s.pointers(v).recv, payload, 2, None))
+        c3.check(c3.lib().c3_stream_sync(None))
+        want = (orc.expected_allgather(n, chunk, SEED, 2) if collective == 0
+                else orc.expected_alltoall(n, v, chunk, SEED, 4))
+        assert np.array_equal(got, want), f"rank {v}"
+    Ah, Bh = orc.bf16(M * K, SEED, 0, 0), orc.bf16(N * K, SEED, 0, 1)
+    Cbits = np.empty(M * N, np.uint16)
+    c3.check(c3.lib().c3_memcpy(Cbits.ctypes.data, s.pointers(0).c, M * N * 2, 2, None))
+    c3.check(c3.lib().c3_stream_sync(None))
+    rows, cols = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    gemm_check(Cbits, Ah, Bh, M, N, K, rows.ravel(), cols.ravel())
+    s.close()
+    w.close()
+
+
+def test_fused_rejects_reduce_scatter(c3):
+    w = c3.World(0, 2, 0, loopback=True)
+    s = c3.Session(w, 2048, 2048, 256, c3.REDUCE_SCATTER, 2 << 20)
+    with pytest.raises(c3.C3Error) as e:
+        s.run(c3.FUSED)
+    assert e.value.code == 102
+    s.close()
+    w.close()

@@ -37,14 +37,18 @@ def _worker(rank, world, port, coll, q):
         from tests import _oracle as orc
         d = Dist()
         w = c3.World(rank, world, 0, loopback=False)
-        M, N, K = 256, 512, 256
+        os.environ["C3_GEMM_KERNEL"] = "pair"  # the fused path needs the CTA-pair GEMM
+        M, N, K = 512, 1024, 256
         chunk = 256 << 10
         payload = world * chunk
         s = c3.Session(w, M, N, K, coll, payload)
         s.import_handles(d.allgather_bytes(s.export_handles()))
         s.set_barrier(d.barrier)
         results = {}
-        for strat in (c3.C3_SP, c3.CONCCL, c3.COMM_ONLY_CU, c3.COMM_ONLY_DMA, c3.SERIAL):
+        strats = [c3.C3_SP, c3.CONCCL, c3.COMM_ONLY_CU, c3.COMM_ONLY_DMA, c3.SERIAL]
+        if coll != c3.REDUCE_SCATTER:
+            strats.append(c3.FUSED)
+        for strat in strats:
             s.fill(SEED)
             d.barrier()  # every rank's inputs are written before anyone reads/pushes
             t = s.run(strat)

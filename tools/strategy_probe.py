@@ -27,16 +27,20 @@ def main():
     out = {}
     a = s.default_alloc(c3.GEMM_ONLY)
     out["gemm_only"] = med(c3.GEMM_ONLY, a)
-    for ctas in (8, 16, 32, 64, 148):
+    for ctas in (64, 148):
         a = s.default_alloc(c3.COMM_ONLY_CU)
         a.cus_comm = ctas
         out[f"comm_only_{ctas}"] = med(c3.COMM_ONLY_CU, a)
-    for strat in (c3.C3_BASE, c3.C3_SP):
-        for gemm in (148, 140, 132):
-            for ctas in (8, 16, 32, 64, 148):
+    for strat in (c3.C3_BASE,):
+        for gemm in (148,):
+            for ctas in (32, 64, 148):
                 a = s.default_alloc(strat)
                 a.cus_gemm, a.cus_comm = gemm, ctas
                 out[f"{c3.STRATEGY_NAMES[strat]}_g{gemm}_c{ctas}"] = med(strat, a)
+    for piece in (1024, 2048, 4096, 8192, 16384):
+        for pace in (0.0, 0.8):
+            s.set_fused_pace(pace, piece)
+            out[f"fused_piece{piece}_pace{pace}"] = med(c3.FUSED, s.default_alloc(c3.FUSED))
     for ctas in (8, 16, 32):
         a = s.default_alloc(c3.C3_RP)
         a.cus_gemm, a.cus_comm = 148 - ctas, ctas
