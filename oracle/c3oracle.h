@@ -19,7 +19,8 @@
  *     vectors; the data-movement semantics are pinned by the reference's own
  *     ByteOracle and validate_plan, see tests/test_oracle.py).
  *   - synthetic inputs: counter-based hash of (seed, rank, tensor, index) so the
- *     CUDA side regenerates bit-identical data (paper_2412_14335_b200/csrc/cuda/fill.cu).
+ *     CUDA side regenerates bit-identical data (fill kernels in
+ *     paper_2412_14335_b200/csrc/cuda/collectives.cu).
  */
 #ifndef C3ORACLE_H
 #define C3ORACLE_H

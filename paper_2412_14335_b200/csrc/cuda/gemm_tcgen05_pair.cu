@@ -24,6 +24,8 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "c3cuda_internal.hpp"
 #include "ptx.cuh"
 
@@ -37,7 +39,11 @@ constexpr int UK = 16;
 constexpr int STAGES = 6;
 constexpr int ACC_BUFS = 2;
 constexpr int THREADS = 256;
-constexpr int GROUP_M = 8;     // 8 pair-rows (2048 rows of A) per raster band
+// Pair-rows per raster band (C3_GEMM_BAND env overrides, dev A/B). Measured
+// DRAM reads per cfg2 launch: band 8 -> 2.39 GB, 16 -> 3.85 GB, 32 -> 12.3 GB
+// (profiles/r01_gemm_band_ab.txt): the L2 is split across the two dies, so a
+// band's A slice must stay well under the nominal 126 MB.
+constexpr int GROUP_M_DEFAULT = 8;
 constexpr int RING = 4;
 constexpr uint32_t A_STAGE = 128 * BK * 2;  // this CTA's 128 rows of A
 constexpr uint32_t B_STAGE = 128 * BK * 2;  // this CTA's 128 rows of B
@@ -55,13 +61,14 @@ struct Params {
     int ldc;
     int* tile_counter;
     int* exit_counter;
+    int group_m;
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
-    const int band = GROUP_M * p.tiles_n;
-    const int first_m = (tile / band) * GROUP_M;
-    const int rows = min(p.tiles_m - first_m, GROUP_M);
+    const int band = p.group_m * p.tiles_n;
+    const int first_m = (tile / band) * p.group_m;
+    const int rows = min(p.tiles_m - first_m, p.group_m);
     const int in_band = tile % band;
     tm = first_m + in_band % rows;
     tn = in_band / rows;
@@ -393,6 +400,12 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
     p.ldc = static_cast<int>(plan->n);
     p.tile_counter = plan->counters;
     p.exit_counter = plan->counters + 1;
+    static const int band = [] {
+        const char* e = std::getenv("C3_GEMM_BAND");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? v : gemm2::GROUP_M_DEFAULT;
+    }();
+    p.group_m = band;
     if (fc) {
         if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
         p.fc = *fc;
