@@ -469,6 +469,12 @@ class LibraryBaseline:
 
                 def comm():
                     tdist.all_gather_into_tensor(dst, src, group=pg)
+            elif cfg["coll"] == "all-to-all":
+                src = torch.empty(cfg["payload"], dtype=torch.uint8, device=dev)
+                dst = torch.empty(cfg["payload"], dtype=torch.uint8, device=dev)
+
+                def comm():
+                    tdist.all_to_all_single(dst, src, group=pg)
             else:
                 src = torch.randn(cfg["payload"] // 2, device=dev).to(torch.bfloat16)
                 dst = torch.empty(cfg["payload"] // 2 // n, device=dev, dtype=torch.bfloat16)

@@ -235,7 +235,9 @@ typedef int (*c3_barrier_fn)(void* ctx);
 /* C3_FUSED pacing: the copies of each CTA finish after this share of the
  * GEMM's operand loads (default 0 = as fast as possible); piece_bytes =
  * bytes per bulk copy (16..16384, multiple of 16; default 4096 — small pieces
- * keep the SM's TMA queue short for the GEMM's operand loads). */
+ * keep the SM's TMA queue short for the GEMM's operand loads). piece_bytes = 0
+ * selects the LSU mode instead: the copy warp's 32 lanes move 16-byte vectors
+ * with plain loads/stores, leaving the TMA unit to the GEMM (pace unused). */
 int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes);
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
 /* Runtime heuristic (the paper's strategy choice, on the product model layer):

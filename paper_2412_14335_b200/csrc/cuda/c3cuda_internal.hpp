@@ -103,6 +103,7 @@ struct FusedComm {
     uint8_t* dst[C3_MAX_RANKS] = {};        // rank q's receive base
     float pace = 0.0f;               // finish copies by this share of the GEMM's loads (0 = unpaced)
     int64_t piece = 4096;            // bytes per bulk copy (<= 16 KiB buffer)
+    int mode = 0;                    // 0: TMA bulk copies (lane 0), 1: LSU vectors (32 lanes)
     Signals sig;
 };
 

@@ -128,6 +128,52 @@ __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
     fence_proxy_async_global();
 }
 
+// Fused C3, LSU variant (all 32 lanes of warp 3): 16-byte vector loads and
+// stores (L2 evict-first), AG: one load, n-1 stores per vector; A2A: one
+// load, one store. Keeps the SM's TMA queue for the GEMM's operand loads.
+__device__ void fused_copy_loop_lsu(const Params& p, int lane) {
+    const FusedComm& fc = p.fc;
+    const uint64_t pol = policy_evict_first();
+    const int64_t vecs = fc.chunk / 16;
+    const int nv = fc.self_end - fc.self_begin;
+    const int64_t rows = fc.kind == 0 ? 1 : fc.n;  // (dest) sub-slots per rank
+    const int64_t per_v = rows * vecs;
+    const int64_t total = per_v * nv;
+    constexpr int U = 4;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * 32 * U;
+    for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32 * U + lane; base < total; base += step) {
+        uint4 v[U];
+        int vv[U], qq[U];
+        int64_t ii[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t w = base + u * 32;
+            if (w >= total) continue;
+            vv[u] = fc.self_begin + static_cast<int>(w / per_v);
+            const int64_t r = w % per_v;
+            qq[u] = static_cast<int>(r / vecs);
+            ii[u] = r % vecs;
+            const uint4* src = reinterpret_cast<const uint4*>(fc.src[vv[u]]) + (fc.kind == 0 ? 0 : qq[u] * vecs);
+            v[u] = ld_stream_v4(src + ii[u], pol);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (base + u * 32 >= total) continue;
+            const int64_t off = static_cast<int64_t>(vv[u]) * vecs + ii[u];
+            if (fc.kind == 0) {
+                for (int t = 1; t <= fc.n; ++t) {
+                    const int d = (vv[u] + t) % fc.n;
+                    if (d == vv[u] && fc.skip_self) continue;
+                    st_stream_v4(reinterpret_cast<uint4*>(fc.dst[d]) + off, v[u], pol);
+                }
+            } else {
+                st_stream_v4(reinterpret_cast<uint4*>(fc.dst[qq[u]]) + off, v[u], pol);
+            }
+        }
+    }
+    __threadfence_system();
+}
+
 template <bool FUSED>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
 gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
@@ -227,8 +273,13 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             tile = next;
         }
         if (FUSED) st_volatile_shared(producer_done, 1);
-    } else if (FUSED && warp == 3 && lane == 0) {
-        if (p.fc.enabled) fused_copy_loop(p, copy_buf, lbar, progress, producer_done);
+    } else if (FUSED && warp == 3) {
+        if (p.fc.enabled) {
+            if (p.fc.mode == 1)
+                fused_copy_loop_lsu(p, lane);
+            else if (lane == 0)
+                fused_copy_loop(p, copy_buf, lbar, progress, producer_done);
+        }
     } else if (warp == 1 && lane == 0 && leader) {
         // ------------- MMA issuer (leader only) -------------
         constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);

@@ -275,6 +275,7 @@ struct c3_session {
     uint32_t epoch = 0;
     float fused_pace = 0.0f;                // C3_FUSED: copies finish by this share of the GEMM (0 = unpaced)
     int64_t fused_piece = 4096;             // C3_FUSED: bytes per bulk copy
+    int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
     c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
     void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
@@ -1007,6 +1008,12 @@ int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* al
 
 int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes) {
     if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_fused_pace: null session");
+    if (piece_bytes == 0) {  // LSU mode: the copy warp's 32 lanes move 16-byte vectors
+        s->fused_mode = 1;
+        s->fused_pace = pace;
+        return C3_OK;
+    }
+    s->fused_mode = 0;
     if (!(pace >= 0.f && pace <= 1.f)) return set_error(C3_ERR_VALIDATION, "pace must be in [0, 1]");
     if (piece_bytes < 16 || piece_bytes > 16384 || piece_bytes % 16)
         return set_error(C3_ERR_VALIDATION, "piece must be a multiple of 16 in [16, 16384]");
@@ -1093,6 +1100,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         fc.chunk = s->chunk;
         fc.pace = s->fused_pace;
         fc.piece = s->fused_piece;
+        fc.mode = s->fused_mode;
         const bool loop = w->loopback != 0;
         fc.self_begin = loop ? 0 : w->rank;
         fc.self_end = loop ? ((flags & kRunAllRanks) ? s->n : 1) : w->rank + 1;

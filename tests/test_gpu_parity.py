@@ -330,8 +330,8 @@ def test_session_alltoall_all_strategies(torch_mod, c3, n):
 
 @pytest.mark.parametrize("collective", [0, 1], ids=["all-gather", "all-to-all"])
 @pytest.mark.parametrize("n", [2, 8])
-@pytest.mark.parametrize("pace", [0.0, 0.8])
-def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace):
+@pytest.mark.parametrize("pace,piece", [(0.0, 4096), (0.8, 16384), (0.0, 0)])
+def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace, piece):
     """C3_FUSED: the collective moved inside the CTA-pair GEMM by its copy warp
     (TMA bulk copies). Every virtual rank's output bit-exact; GEMM in tolerance."""
     monkeypatch.setenv("C3_GEMM_KERNEL", "pair")
@@ -339,7 +339,7 @@ def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace):
     M, N, K = 512, 1024, 512
     payload = n * ((3 << 16) + 48)  # slots not a multiple of the 16 KiB piece
     s = c3.Session(w, M, N, K, collective, payload)
-    s.set_fused_pace(pace)
+    s.set_fused_pace(pace, piece)
     s.fill(SEED)
     t = s.run(c3.FUSED, all_ranks=True)
     assert t.launches == 1

@@ -37,8 +37,8 @@ def main():
                 a = s.default_alloc(strat)
                 a.cus_gemm, a.cus_comm = gemm, ctas
                 out[f"{c3.STRATEGY_NAMES[strat]}_g{gemm}_c{ctas}"] = med(strat, a)
-    for piece in (1024, 2048, 4096, 8192, 16384):
-        for pace in (0.0, 0.8):
+    for piece in (0, 2048, 4096, 8192):
+        for pace in (0.0,):
             s.set_fused_pace(pace, piece)
             out[f"fused_piece{piece}_pace{pace}"] = med(c3.FUSED, s.default_alloc(c3.FUSED))
     for ctas in (8, 16, 32):
