@@ -229,6 +229,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     if (warp == 2) tmem_alloc_pair<TMEM_COLS>(tmem_slot);
     tc_fence_before();
     cluster_sync();  // barrier inits and TMEM allocation visible across the pair
+    __syncthreads();  // CTA-scope order for the TMEM address slot (explicit for racecheck)
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
 

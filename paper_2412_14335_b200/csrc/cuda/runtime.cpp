@@ -734,7 +734,7 @@ int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** ou
                                                              : c3sim::CollectiveKind::ReduceScatter;
         sc.collective.payload_bytes = d.payload_bytes;
         sc.collective.n_ranks = d.n_ranks;
-        if (s->n > 1) {
+        if (s->n > 1 && s->chunk > 0) {  // nothing to plan for an empty payload
             const c3sim::TransferPlan tp =
                 d.collective == C3_ALL_GATHER   ? c3sim::plan_all_gather(s->n, s->chunk, s->md)
                 : d.collective == C3_ALL_TO_ALL ? c3sim::plan_all_to_all(s->n, s->chunk, s->md)

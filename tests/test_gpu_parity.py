@@ -369,3 +369,22 @@ def test_fused_rejects_reduce_scatter(c3):
     assert e.value.code == 102
     s.close()
     w.close()
+
+
+@pytest.mark.parametrize("collective", [0, 1, 2])
+def test_degenerate_worlds(c3, collective):
+    """A 1-rank collective is an empty plan (conccl.hpp:30-32) and a zero-byte
+    payload moves nothing; every strategy still runs and the GEMM still runs."""
+    w1 = c3.World(0, 1, 0, loopback=False)
+    s = c3.Session(w1, 256, 256, 64, collective, 4096)
+    for strat in list(range(7)) + [100, 101, 102]:
+        t = s.run(strat)
+        assert t.total_ms >= 0
+    s.close()
+    w1.close()
+    w = c3.World(0, 4, 0, loopback=True)
+    s = c3.Session(w, 256, 256, 64, collective, 0)
+    for strat in (c3.SERIAL, c3.C3_SP, c3.CONCCL, c3.COMM_ONLY_CU, c3.COMM_ONLY_DMA):
+        s.run(strat, all_ranks=True)
+    s.close()
+    w.close()
