@@ -206,6 +206,13 @@ int c3_ce_execute(c3_world* w, const c3_transfer* t, int n_transfers, const void
 int c3_plan_transfers(int kind, int n_ranks, int64_t chunk_bytes, int dma_engines,
                       c3_transfer* out, int capacity, int* count);
 
+/* One transformer layer as C3 scenarios, from the product model layer's
+ * ingest_model (workload.hpp:80-94): the layer's forward GEMMs (qkv, attn
+ * out, gate+up, down) each with the FSDP all-gather of its weight as payload
+ * (0 when shards == 1). out may be NULL to query *count. */
+int c3_ingest_model(int64_t hidden, int64_t ffn, int64_t tokens, int dtype_bytes, int shards,
+                    c3_scenario_desc* out, int capacity, int* count);
+
 /* ------------------------------------------------------------ C3 runtime
  * A session owns one scenario's operands and executes it under a strategy.
  * Replaces (executes) c3sim::simulate (sim.hpp:70-73) for the strategy the

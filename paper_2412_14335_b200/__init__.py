@@ -44,6 +44,17 @@ def plan_transfers(kind, n_ranks, chunk_bytes, dma_engines):
     return arr, n.value
 
 
+def ingest_model(hidden, ffn, tokens, dtype_bytes=2, shards=8):
+    """The layer's C3 scenarios (model layer ingest_model): list of
+    (m, n, k, all-gather payload bytes of that GEMM's weight)."""
+    L = lib()
+    n = C.c_int(0)
+    check(L.c3_ingest_model(hidden, ffn, tokens, dtype_bytes, shards, None, 0, C.byref(n)))
+    arr = (_capi.ScenarioDesc * max(1, n.value))()
+    check(L.c3_ingest_model(hidden, ffn, tokens, dtype_bytes, shards, arr, n.value, C.byref(n)))
+    return [(d.m, d.n, d.k, d.payload_bytes) for d in arr[:n.value]]
+
+
 class World:
     """One device; `loopback=True` hosts all n ranks virtually on it."""
 

@@ -94,6 +94,7 @@ SIGNATURES = {
     "c3_reduce_local_bf16": (I, [PP, I, P, I64, I, P]),
     "c3_ce_execute": (I, [P, C.POINTER(Transfer), I, PP, PP, I, P]),
     "c3_plan_transfers": (I, [I, I, I64, I, C.POINTER(Transfer), I, C.POINTER(C.c_int)]),
+    "c3_ingest_model": (I, [I64, I64, I64, I, I, C.POINTER(ScenarioDesc), I, C.POINTER(C.c_int)]),
     "c3_session_create": (I, [P, C.POINTER(ScenarioDesc), PP]),
     "c3_session_destroy": (I, [P]),
     "c3_session_pointers": (I, [P, I, C.POINTER(SessionPtrs)]),

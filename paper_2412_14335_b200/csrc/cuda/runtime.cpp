@@ -695,6 +695,36 @@ int c3_plan_transfers(int kind, int n_ranks, int64_t chunk_bytes, int dma_engine
     });
 }
 
+int c3_ingest_model(int64_t hidden, int64_t ffn, int64_t tokens, int dtype_bytes, int shards,
+                    c3_scenario_desc* out, int capacity, int* count) {
+    if (!count) return set_error(C3_ERR_VALIDATION, "c3_ingest_model: null count");
+    return guarded([&] {
+        c3sim::ModelConfig cfg;
+        cfg.hidden = hidden;
+        cfg.ffn = ffn;
+        cfg.tokens = tokens;
+        cfg.dtype_bytes = dtype_bytes;
+        cfg.shards = shards;
+        const c3sim::ModelWorkload w = c3sim::ingest_model(cfg);
+        *count = static_cast<int>(w.gemms.size());
+        if (out) {
+            if (capacity < *count) throw c3sim::ValidationError("c3_ingest_model: capacity too small");
+            for (int i = 0; i < *count; ++i) {
+                const auto& g = w.gemms[static_cast<size_t>(i)];
+                c3_scenario_desc d{};
+                d.m = g.m;
+                d.n = g.n;
+                d.k = g.k;
+                d.collective = C3_ALL_GATHER;
+                d.n_ranks = shards;
+                d.payload_bytes = w.all_gathers.empty() ? 0 : w.all_gathers[static_cast<size_t>(i)].payload_bytes;
+                out[i] = d;
+            }
+        }
+        return C3_OK;
+    });
+}
+
 int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** out) {
     if (!w || !desc || !out) return set_error(C3_ERR_VALIDATION, "c3_session_create: null argument");
     const c3_scenario_desc& d = *desc;

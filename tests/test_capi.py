@@ -82,3 +82,14 @@ def _has_gpu():
         return torch.cuda.is_available()
     except Exception:
         return False
+
+
+def test_ingest_model_llama70b_layer():
+    """ingest_model (workload.cpp:217-251 semantics) through the C ABI."""
+    layer = c3.ingest_model(8192, 28672, 8192, 2, 8)
+    assert [(m, n, k) for m, n, k, _ in layer] == [
+        (8192, 3 * 8192, 8192), (8192, 8192, 8192), (8192, 2 * 28672, 8192), (8192, 8192, 28672)]
+    assert [p for *_, p in layer] == [3 * 8192 * 8192 * 2, 8192 * 8192 * 2, 2 * 28672 * 8192 * 2,
+                                      28672 * 8192 * 2]
+    assert all(p % 8 == 0 for *_, p in layer)
+    assert all(p == 0 for *_, p in c3.ingest_model(4096, 11008, 2048, 2, 1))

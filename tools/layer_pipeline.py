@@ -1,0 +1,112 @@
+"""Model-level C3: one FSDP transformer layer as a pipeline
+of C3 pairs on B200. The layer comes from the product model layer's
+ingest_model (reference workload.cpp:217-251): forward GEMMs qkv, attn-out,
+gate+up, down, each weight sharded over 8 ranks. Pair i = GEMM i concurrent
+with the all-gather of weight i+1 (prefetch; the last GEMM prefetches the next
+layer's first weight). Loopback world on one GPU, in two emulations: the
+collective at full local speed, and rate-matched to NVLink (770 GB/s per
+direction, as in bench.py). Isolated and concurrent runs interleaved.
+
+usage: python tools/layer_pipeline.py OUT.csv [rounds]
+"""
+import os
+import statistics
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+import paper_2412_14335_b200 as c3  # noqa: E402
+
+MODELS = {"llama70b": (8192, 28672), "llama405b": (16384, 53248)}
+TAGS = ["attn_qkv", "attn_out", "ffn_in", "ffn_out"]
+NVLINK_GBPS = 770.0
+
+
+def rate_matched_ctas(s, payload, n):
+    target = (n - 1) / n * payload / (NVLINK_GBPS * 1e9) * 1e3
+    best = None
+    for ctas in (2, 4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 148):
+        a = s.default_alloc(c3.COMM_ONLY_CU)
+        a.cus_comm = ctas
+        ms = statistics.median(s.run(c3.COMM_ONLY_CU, a).comm_end_ms for _ in range(3))
+        if best is None or abs(ms - target) < abs(best[1] - target):
+            best = (ctas, ms)
+        if ms < target:
+            break
+    return best[0]
+
+
+def main():
+    out_path = sys.argv[1]
+    R = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    n = 8
+    rows = ["model,pair,gemm_mnk,ag_weight,payload_mib,emulation,comm_ctas,t_gemm_ms,t_comm_ms,"
+            "serial_ms,best_strategy,concurrent_ms,speedup,ideal,fraction_of_ideal"]
+    for model, (hidden, ffn) in MODELS.items():
+        layer = c3.ingest_model(hidden, ffn, 8192, 2, n)
+        totals = {}
+        for i, (m, nn, kk, _) in enumerate(layer):
+            j = (i + 1) % len(layer)
+            payload = layer[j][3]
+            w = c3.World(0, n, 0, loopback=True)
+            s = c3.Session(w, m, nn, kk, c3.ALL_GATHER, payload)
+            s.fill()
+            full = w.info.sm_count
+            for emu in ("full-speed", "nvlink-rate"):
+                ctas = full if emu == "full-speed" else rate_matched_ctas(s, payload, n)
+                comm = s.default_alloc(c3.COMM_ONLY_CU)
+                comm.cus_comm = ctas
+                jobs = {"gemm": (c3.GEMM_ONLY, s.default_alloc(c3.GEMM_ONLY)),
+                        "comm": (c3.COMM_ONLY_CU, comm)}
+                for st in (c3.C3_BASE, c3.C3_SP):
+                    for cc in sorted({min(ctas, 64), 32} if emu == "full-speed" else {ctas}):
+                        a = s.default_alloc(st)
+                        a.cus_gemm, a.cus_comm = full, cc
+                        jobs[f"{c3.STRATEGY_NAMES[st]}_coresident{cc}"] = (st, a)
+                try:
+                    s.run(c3.FUSED, s.default_alloc(c3.FUSED))
+                    if emu == "full-speed":
+                        jobs["c3_fused"] = (c3.FUSED, s.default_alloc(c3.FUSED))
+                except c3.C3Error:
+                    pass
+                t = {k: [] for k in jobs}
+                names = list(jobs)
+                for r in range(R + 1):
+                    for job in names[r % len(names):] + names[:r % len(names)]:
+                        st, a = jobs[job]
+                        tm = s.run(st, a)
+                        if r:
+                            t[job].append(tm)
+                tg = statistics.median(x.gemm_end_ms - x.gemm_start_ms for x in t["gemm"])
+                tc = statistics.median(x.comm_end_ms - x.comm_start_ms for x in t["comm"])
+                conc = {name: statistics.median(x.total_ms for x in v) for name, v in t.items()
+                        if name not in ("gemm", "comm")}
+                best = min(conc, key=conc.get)
+                bc = min(conc[best], tg + tc)  # the runtime falls back to serial if nothing wins
+                if bc == tg + tc:
+                    best = "serial"
+                ideal = c3.ideal_speedup(tg, tc)
+                sp = (tg + tc) / bc
+                rows.append(f"{model},{i},{m}x{nn}x{kk},{TAGS[j]},{payload / 2**20:.1f},{emu},{ctas},"
+                            f"{tg:.4f},{tc:.4f},{tg + tc:.4f},{best},{bc:.4f},{sp:.4f},{ideal:.4f},"
+                            f"{c3.fraction_of_ideal(sp, ideal):.4f}")
+                acc = totals.setdefault(emu, [0.0, 0.0, 0.0, 0.0])
+                acc[0] += tg
+                acc[1] += tc
+                acc[2] += bc
+                acc[3] += max(tg, tc)
+            s.close()
+            w.close()
+            print(f"{model} pair {i} done", file=sys.stderr, flush=True)
+        for emu, (tg, tc, bc, ideal_ms) in totals.items():
+            ideal = (tg + tc) / ideal_ms
+            sp = (tg + tc) / bc
+            rows.append(f"{model},layer,all,all,,{emu},,{tg:.4f},{tc:.4f},{tg + tc:.4f},per-pair best,"
+                        f"{bc:.4f},{sp:.4f},{ideal:.4f},{c3.fraction_of_ideal(sp, ideal):.4f}")
+    with open(out_path, "w") as f:
+        f.write("\n".join(rows) + "\n")
+    print("\n".join(rows))
+
+
+if __name__ == "__main__":
+    main()
