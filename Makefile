@@ -29,11 +29,17 @@ CC_SRC    := $(wildcard $(PKG)/csrc/cuda/*.cpp)
 CC_OBJ    := $(patsubst $(PKG)/csrc/cuda/%.cpp,$(OBJ)/cuda/%.o,$(CC_SRC))
 CU_HDR    := $(wildcard $(PKG)/csrc/cuda/*.cuh) $(wildcard $(PKG)/csrc/cuda/*.hpp) include/c3cuda.h
 
-.PHONY: all model cuda cli oracle clean
-all: model cuda cli oracle
+PYINC    := $(shell python3 -c "import sysconfig; print(sysconfig.get_paths()['include'])")
+PYBIND   := $(shell python3 -c "import pybind11; print(pybind11.get_include())")
+PYEXT    := $(shell python3 -c "import sysconfig; print(sysconfig.get_config_var('EXT_SUFFIX'))")
+PYMOD    := $(PKG)/python/c3sim/_c3sim$(PYEXT)
+
+.PHONY: all model cuda cli python oracle clean
+all: model cuda cli python oracle
 model: $(LIB)/libc3sim.so
 cuda: $(LIB)/libc3cuda.so
 cli: $(BIN)/c3sim
+python: $(PYMOD)
 oracle:
 	$(MAKE) -C oracle -s
 
@@ -58,9 +64,15 @@ $(LIB)/libc3cuda.so: $(CU_OBJ) $(CC_OBJ) $(LIB)/libc3sim.so
 	$(NVCC) $(ARCH) -shared -ccbin $(CXX) -o $@ $(CU_OBJ) $(CC_OBJ) -L$(LIB) -lc3sim \
 	    -lcudart_static -Xlinker -rpath,'$$ORIGIN'
 
-$(BIN)/c3sim: $(PKG)/csrc/tools/c3sim_cli.cpp $(LIB)/libc3sim.so
+$(BIN)/c3sim: $(PKG)/csrc/tools/c3sim_cli.cpp $(LIB)/libc3sim.so $(LIB)/libc3cuda.so include/c3sim/exec.hpp
 	@mkdir -p $(@D)
-	$(CXX) $(CXXFLAGS) $< -L$(LIB) -lc3sim -Wl,-rpath,'$$ORIGIN/../lib' -o $@
+	$(CXX) $(CXXFLAGS) $< -L$(LIB) -lc3cuda -lc3sim -Wl,-rpath,'$$ORIGIN/../lib' -o $@
+
+# pybind11 module: the reference's Python surface over the product libraries
+$(PYMOD): $(PKG)/csrc/python/c3sim_module.cpp $(LIB)/libc3sim.so $(LIB)/libc3cuda.so $(wildcard include/c3sim/*.hpp)
+	@mkdir -p $(@D)
+	$(CXX) $(CXXFLAGS) -Wno-unused-parameter -shared -I$(PYINC) -I$(PYBIND) $< -L$(LIB) -lc3cuda -lc3sim \
+	    -Wl,-rpath,'$$ORIGIN/../../lib' -o $@
 
 clean:
 	rm -rf build $(LIB) $(BIN)

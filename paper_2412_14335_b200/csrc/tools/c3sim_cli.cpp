@@ -4,6 +4,14 @@
 // conccl-plan, sweep, calibrate; exit 0 ok, 2 I/O, 3 unknown entity,
 // 4 validation, 5 fit. Argument parsing is self-contained (no CLI11).
 // Reports are written atomically (temp file + rename).
+//
+// New subcommand `run` EXECUTES scenarios on the local B200 through the C++
+// execution API (include/c3sim/exec.hpp -> libc3cuda.so): measured isolated
+// times, the strategy's measured makespan, speedup / ideal / fraction of
+// ideal, and — given --machine and --tables — the model's prediction from the
+// same measured isolated times next to it. Single process, so the n ranks of
+// the scenario run as a loopback world on one GPU. Exit 6 = device error
+// (CUDA / driver / no B200).
 #include <cstdio>
 #include <filesystem>
 #include <fstream>
@@ -17,6 +25,7 @@
 #include "c3sim/calibrate.hpp"
 #include "c3sim/conccl.hpp"
 #include "c3sim/errors.hpp"
+#include "c3sim/exec.hpp"
 #include "c3sim/machine.hpp"
 #include "c3sim/params_io.hpp"
 #include "c3sim/sim.hpp"
@@ -276,10 +285,109 @@ int calibrate_cmd(const Args& a) {
     return 0;
 }
 
+C3Scenario run_scenario(const Args& a) {
+    if (a.has("scenario")) {
+        const auto all = load_dataset(a.need("dataset"));
+        std::optional<CollectiveKind> kind;
+        if (!a.get("filter-collective").empty()) kind = collective_kind_from_string(a.get("filter-collective"));
+        for (const auto& x : all)
+            if (x.id == a.get("scenario") && (!kind || x.collective.kind == *kind)) return x;
+        throw UnknownEntityError("unknown scenario id '" + a.get("scenario") + "'");
+    }
+    C3Scenario sc;
+    sc.id = a.get("id", "custom");
+    sc.gemm.tag = "gemm";
+    sc.gemm.m = std::stoll(a.need("m"));
+    sc.gemm.n = std::stoll(a.need("n"));
+    sc.gemm.k = std::stoll(a.need("k"));
+    sc.collective.kind = collective_kind_from_string(a.get("kind", "all-gather"));
+    sc.collective.n_ranks = std::stoi(a.need("ranks"));
+    sc.collective.payload_bytes = std::stoll(a.need("payload-bytes"));
+    validate(sc.gemm);
+    validate(sc.collective);
+    return sc;
+}
+
+int run_cmd(const Args& a) {
+    const std::string format = a.get("format", "csv");
+    check_format(format);
+    C3Scenario sc = run_scenario(a);
+    std::vector<ExecMode> modes;
+    const std::string name = a.get("strategy", "all");
+    if (name == "all") {
+        for (Strategy s : kAllStrategies) modes.push_back(to_mode(s));
+        modes.push_back(ExecMode::Fused);
+    } else {
+        modes.push_back(exec_mode_from_string(name));
+    }
+    ExecOptions o;
+    o.warmup = std::stoi(a.get("warmup", "6"));
+    o.reps = std::stoi(a.get("reps", "9"));
+    o.seed = std::stoull(a.get("seed", "20241217"));
+
+    // optional model side: predict every strategy from the measured isolated times
+    std::optional<Inputs> model;
+    if (a.has("machine") && a.has("tables")) model = load_inputs(a, false, true);
+
+    World world(0, sc.collective.n_ranks, std::stoi(a.get("device", "0")), /*loopback=*/true);
+    Session session(world, sc);
+    std::ostringstream csv;
+    csv << "scenario_id,collective,strategy,cus_gemm,cus_comm,backend,t_gemm_s,t_comm_s,t_comm_dma_s,"
+           "makespan_s,speedup,ideal,fraction_of_ideal,taxonomy,predicted_makespan_s,predicted_speedup\n";
+    json rows = json::array();
+    for (ExecMode m : modes) {
+        ExecResult r;
+        try {
+            r = execute(session, sc, m, o);
+            o.fill = false;  // operands stay resident across strategies
+        } catch (const ValidationError& e) {  // e.g. c3_fused on a shape without the pair GEMM
+            std::cerr << "skip " << to_string(m) << ": " << e.what() << "\n";
+            continue;
+        }
+        std::string pred_ms, pred_sp;
+        double pm = 0;
+        if (model && static_cast<int>(m) <= C3_CONCCL_RP) {
+            C3Scenario msc = sc;
+            msc.gemm.measured_time = r.t_gemm;
+            msc.collective.measured_time = r.t_comm;
+            SimOptions so;
+            so.freeze_phase2_allocation = model->params.freeze_phase2_allocation;
+            const SimTimeline tl = simulate(msc, static_cast<Strategy>(static_cast<int>(m)), model->md,
+                                            model->tables, model->params.penalties, model->params.eff, so);
+            pm = tl.makespan;
+            pred_ms = g12(tl.makespan);
+            pred_sp = g12(tl.speedup);
+        }
+        const char* backend = r.alloc.backend == C3_BACKEND_DMA ? "dma"
+                              : r.alloc.backend == C3_BACKEND_TMA ? "tma" : "cu";
+        csv << sc.id << ',' << to_string(sc.collective.kind) << ',' << to_string(m) << ','
+            << r.gemm_ctas << ',' << r.comm_ctas << ',' << backend << ',' << g12(r.t_gemm) << ','
+            << g12(r.t_comm) << ',' << g12(r.t_comm_dma) << ',' << g12(r.makespan) << ','
+            << g12(r.speedup) << ',' << g12(r.ideal) << ',' << g12(r.fraction_of_ideal) << ','
+            << to_string(r.taxonomy) << ',' << pred_ms << ',' << pred_sp << '\n';
+        json row = {{"scenario_id", sc.id}, {"collective", to_string(sc.collective.kind)},
+                    {"strategy", to_string(m)}, {"cus_gemm", r.gemm_ctas}, {"cus_comm", r.comm_ctas},
+                    {"backend", backend}, {"t_gemm_s", r.t_gemm}, {"t_comm_s", r.t_comm},
+                    {"t_comm_dma_s", r.t_comm_dma}, {"makespan_s", r.makespan}, {"speedup", r.speedup},
+                    {"ideal", r.ideal}, {"fraction_of_ideal", r.fraction_of_ideal},
+                    {"taxonomy", to_string(r.taxonomy)}, {"steps_s", r.steps}};
+        if (!pred_ms.empty()) row["predicted_makespan_s"] = pm;
+        rows.push_back(row);
+    }
+    if (rows.empty()) throw ValidationError("run: no strategy could execute this scenario");
+    write_report(a.out(), format == "csv" ? csv.str() : rows.dump(2) + "\n");
+    return 0;
+}
+
 void usage() {
     std::cerr << "usage: c3sim {classify|plan|conccl-plan|sweep|calibrate} --machine FILE "
                  "[--dataset FILE] [--tables FILE] [--params FILE] [--out FILE] "
-                 "[--zero-interference] [subcommand options]\n";
+                 "[--zero-interference] [subcommand options]\n"
+                 "       c3sim run {--dataset FILE --scenario ID | --m M --n N --k K --ranks R "
+                 "--payload-bytes P [--kind all-gather|all-to-all|reduce-scatter]} "
+                 "[--strategy NAME|all] [--warmup W] [--reps K] [--device D] "
+                 "[--machine FILE --tables FILE [--params FILE]] [--format csv|structured-text] "
+                 "[--out FILE]\n";
 }
 
 }  // namespace
@@ -319,8 +427,12 @@ int main(int argc, char** argv) {
         if (a.cmd == "conccl-plan") return conccl_plan_cmd(a);
         if (a.cmd == "sweep") return sweep_cmd(a);
         if (a.cmd == "calibrate") return calibrate_cmd(a);
+        if (a.cmd == "run") return run_cmd(a);
         usage();
         return 2;
+    } catch (const DeviceError& e) {
+        std::cerr << "error: " << e.what() << "\n";
+        return 6;
     } catch (const IoError& e) {
         std::cerr << "error: " << e.what() << "\n";
         return 2;

@@ -114,3 +114,48 @@ def test_bench_two_ranks_shared_device(tmp_path):
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] >= 1
     assert "CUDA-IPC" in line["config"]["world"]
+
+
+def _exec_worker(rank, world, port, strategy, q):
+    """C++ execution API (exec.hpp) through the pybind module in a real
+    multi-process world: the HostTransport is two Python callables over gloo."""
+    try:
+        import sys
+        os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                           "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+        repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+        sys.path.insert(0, os.path.join(repo, "paper_2412_14335_b200", "python"))
+        import c3sim
+        from paper_2412_14335_b200.dist import Dist
+        d = Dist()
+        w = c3sim.World(rank, world, 0, False)
+        s = c3sim.C3Scenario()
+        s.id = "mp"
+        s.gemm.m, s.gemm.n, s.gemm.k, s.gemm.dtype_bytes = 512, 1024, 256, 2
+        s.collective.kind = c3sim.CollectiveKind.ALL_GATHER
+        s.collective.n_ranks = world
+        s.collective.payload_bytes = world << 18
+        r = c3sim.execute(s, strategy, w, warmup=1, reps=3,
+                          allgather=lambda b: b"".join(d.allgather_bytes(b)), barrier=d.barrier)
+        q.put((rank, (r.makespan, list(r.steps), r.t_gemm, r.t_comm), None))
+        d.close()
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("strategy", ["c3_sp", "conccl"])
+def test_exec_api_two_processes_one_gpu(strategy):
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_exec_worker, args=(r, world, port, strategy, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=240) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+    for rank, res, err in out:
+        assert err is None, f"rank {rank}: {err}"
+    # execute() reports the max over ranks: both ranks agree on every number
+    assert out[0][1] == out[1][1]
+    assert out[0][1][0] > 0 and len(out[0][1][1]) == 3

@@ -1,0 +1,154 @@
+"""_c3sim, the pybind11 module over the product model layer + execution API
+(paper_2412_14335_b200/csrc/python/c3sim_module.cpp).
+
+- The reference's OWN Python smoke test (proj/tests/python/test_smoke.py) runs
+  unchanged through the reference's own `c3sim` package on top of our .so
+  (needs /root/reference: this container only).
+- The product `c3sim` package reproduces the golden sweep byte-for-byte, has
+  the reduce-scatter extension, and refuses to execute without a B200.
+- GPU: execute() / measure_isolated() on a loopback world, and `c3sim run`.
+"""
+import glob
+import hashlib
+import json
+import os
+import subprocess
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PYDIR = os.path.join(REPO, "paper_2412_14335_b200", "python")
+REF_DATA = os.path.join(REPO, "tests", "golden", "ref_data")
+REF_SMOKE = "/root/reference/proj/tests/python/test_smoke.py"
+GOLDEN_SWEEP_SHA = "5b82de0beac7015284e6007cf9cd710ab629dc6d8f1a0c9006b16c1c0c73159a"
+
+sys.path.insert(0, PYDIR)
+import c3sim  # noqa: E402
+
+
+def test_module_is_the_product_build():
+    so = c3sim._c3sim.__file__
+    assert so.startswith(PYDIR) and glob.glob(os.path.join(PYDIR, "c3sim", "_c3sim*.so"))
+
+
+@pytest.mark.skipif(not os.path.exists(REF_SMOKE), reason="reference tree not mounted")
+def test_reference_python_smoke_suite_against_product(tmp_path):
+    env = dict(os.environ, PYTHONPATH=os.path.join(PYDIR, "c3sim") + ":/root/reference/proj/python",
+               C3SIM_DATA_DIR=REF_DATA)
+    probe = subprocess.run([sys.executable, "-c", "import c3sim; print(c3sim._impl.__file__)"],
+                           env=env, cwd=tmp_path, capture_output=True, text=True)
+    assert probe.returncode == 0 and probe.stdout.strip().startswith(PYDIR), probe.stderr
+    r = subprocess.run([sys.executable, "-m", "pytest", "-p", "no:cacheprovider", "-q", REF_SMOKE],
+                       env=env, cwd=tmp_path, capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0 and "5 passed" in r.stdout, r.stdout + r.stderr
+
+
+def test_golden_sweep_through_python():
+    md = c3sim.load_machine_file(os.path.join(REF_DATA, "mi300x-node.json"))
+    tables = c3sim.load_slowdown_tables(os.path.join(REF_DATA, "slowdown-tables.csv"), md.min_cu_grain)
+    params = c3sim.load_params_file(os.path.join(REF_DATA, "default-params.json"))
+    scen = c3sim.load_dataset(os.path.join(REF_DATA, "c3-dataset.json"))
+    opt = c3sim.SimOptions()
+    opt.freeze_phase2_allocation = params.freeze_phase2_allocation
+    strategies = [getattr(c3sim.Strategy, n) for n in
+                  ("SERIAL", "C3_BASE", "C3_SP", "C3_RP", "C3_SP_RP", "CONCCL", "CONCCL_RP")]
+    res = c3sim.sweep(scen, strategies, md, tables, params.penalties, params.eff, opt)
+    csv = c3sim.sweep_to_csv(res)
+    assert hashlib.sha256(csv.encode()).hexdigest() == GOLDEN_SWEEP_SHA
+
+
+def test_reduce_scatter_extension():
+    md = c3sim.load_machine_file(os.path.join(REF_DATA, "mi300x-node.json"))
+    plan = c3sim.plan_reduce_scatter(8, 1 << 20, md)
+    assert plan.kind == c3sim.CollectiveKind.REDUCE_SCATTER and len(plan.transfers) == 56
+    assert c3sim.validate_plan(plan, md).ok
+    assert c3sim.collective_name(c3sim.CollectiveKind.REDUCE_SCATTER) == "reduce-scatter"
+
+
+def test_errors_map_to_reference_types():
+    with pytest.raises(c3sim.IoError):
+        c3sim.load_machine_file("/nonexistent/machine.json")
+    with pytest.raises(c3sim.ValidationError):
+        c3sim.classify_c3(-1.0, 1.0)
+
+
+def test_b200_machine_file_loads():
+    md = c3sim.load_machine_file(c3sim.data_path("b200-loopback-node.json"))
+    assert md.cus_per_gpu == 148
+
+
+def _has_gpu():
+    try:
+        import torch
+        return torch.cuda.is_available()
+    except Exception:
+        return False
+
+
+def test_execute_without_gpu_is_a_device_error():
+    if _has_gpu():
+        pytest.skip("GPU present")
+    with pytest.raises(c3sim.DeviceError):
+        c3sim.World(0, 2, 0, True)
+
+
+def _small_scenario(kind=None, n=2, m=2048, nn=2560):
+    s = c3sim.C3Scenario()
+    s.id = "small"
+    s.gemm.m, s.gemm.n, s.gemm.k, s.gemm.dtype_bytes = m, nn, 1024, 2  # 80 pair tiles: c3_fused runs
+    s.collective.kind = kind or c3sim.CollectiveKind.ALL_GATHER
+    s.collective.n_ranks = n
+    s.collective.payload_bytes = 16 << 20
+    return s
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["serial", "c3_sp", "c3_rp", "conccl", "c3_fused"])
+def test_execute_loopback(strategy):
+    w = c3sim.World(0, 2, 0, True)
+    r = c3sim.execute(_small_scenario(), strategy, w, warmup=2, reps=3)
+    assert r.strategy == strategy and len(r.steps) == 3
+    assert r.t_gemm > 0 and r.t_comm > 0 and r.makespan > 0
+    assert r.serial_time == pytest.approx(r.t_gemm + r.t_comm)
+    assert r.ideal == pytest.approx(c3sim.ideal_speedup(r.t_gemm, r.t_comm))
+    assert r.fraction_of_ideal == pytest.approx(c3sim.fraction_of_ideal(r.speedup, r.ideal))
+
+
+@pytest.mark.gpu
+def test_fused_on_a_small_gemm_is_unsupported():
+    w = c3sim.World(0, 2, 0, True)
+    with pytest.raises(c3sim.UnsupportedError):
+        c3sim.execute(_small_scenario(m=128, nn=1024), "c3_fused", w, warmup=1, reps=1)
+    with pytest.raises(c3sim.ValidationError):  # UnsupportedError is a ValidationError
+        c3sim.execute(_small_scenario(m=128, nn=1024), "c3_fused", w, warmup=1, reps=1)
+
+
+@pytest.mark.gpu
+def test_measure_isolated_feeds_the_model():
+    w = c3sim.World(0, 2, 0, True)
+    s = c3sim.measure_isolated(_small_scenario(c3sim.CollectiveKind.REDUCE_SCATTER), w, warmup=2, reps=3)
+    assert s.gemm.measured_time > 0 and s.collective.measured_time > 0
+    md = c3sim.load_machine_file(c3sim.data_path("b200-loopback-node.json"))
+    eff = c3sim.EfficiencyParams()
+    assert c3sim.roofline_gemm_time(s.gemm, md, eff) == s.gemm.measured_time
+
+
+@pytest.mark.gpu
+def test_cli_run_executes_and_predicts(tmp_path):
+    out = tmp_path / "run.json"
+    exe = os.path.join(REPO, "paper_2412_14335_b200", "bin", "c3sim")
+    r = subprocess.run([exe, "run", "--m", "2048", "--n", "2560", "--k", "1024", "--ranks", "2",
+                        "--payload-bytes", str(16 << 20), "--strategy", "all", "--warmup", "2", "--reps",
+                        "3", "--machine", os.path.join(REPO, "data", "b200-loopback-node.json"),
+                        "--tables", os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv"),
+                        "--format", "structured-text", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    rows = json.loads(out.read_text())
+    names = [x["strategy"] for x in rows]
+    assert names == ["serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp", "c3_fused"]
+    for x in rows:
+        assert x["makespan_s"] > 0 and x["t_gemm_s"] > 0 and len(x["steps_s"]) == 3
+        if x["strategy"] != "c3_fused":
+            assert x["predicted_makespan_s"] > 0
