@@ -246,6 +246,15 @@ typedef int (*c3_barrier_fn)(void* ctx);
  * selects the LSU mode instead: the copy warp's 32 lanes move 16-byte vectors
  * with plain loads/stores, leaving the TMA unit to the GEMM (pace unused). */
 int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes);
+/* Link-rate emulation (for loopback worlds, where the "peers" are local HBM
+ * buffers and no NVLink limits the collective): pace this rank's peer traffic
+ * per step to `gbps` GB/s (per direction), e.g. 770 for one B200's measured
+ * NVLink 5 peer bandwidth. Applies to the SM collectives (AG/A2A push bytes,
+ * RS pulled bytes) and to C3_FUSED's copy warps; each CTA waits on the global
+ * timer, so the collective's time does not depend on SM clocks or CTA count
+ * (given enough CTAs to reach the rate). 0 = off (default). Copy-engine
+ * transfers are not paced. */
+int c3_session_set_link_rate(c3_session* s, double gbps);
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
 /* Runtime heuristic (the paper's strategy choice, on the product model layer):
  * load measured interference tables (reference SlowdownTable CSV,

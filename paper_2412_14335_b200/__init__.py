@@ -141,6 +141,11 @@ class Session:
     def set_fused_pace(self, pace=0.0, piece_bytes=4096):
         check(lib().c3_session_set_fused_pace(self.h, pace, piece_bytes))
 
+    def set_link_rate(self, gbps):
+        """Link-rate emulation (loopback): pace the collective's peer traffic
+        to `gbps` GB/s per direction (0 = off)."""
+        check(lib().c3_session_set_link_rate(self.h, float(gbps)))
+
     def load_params(self, json_path):
         check(lib().c3_session_load_params(self.h, json_path.encode()))
 
@@ -158,10 +163,11 @@ class Session:
                                        C.byref(ms)))
         return ms.value
 
-    def autotune(self, candidates, rounds=3, reduce_max=None):
+    def autotune(self, candidates, rounds=3, reduce_max=None, medians=None):
         """candidates: [(strategy, Alloc)] -> (best index, median ms). With
         several ranks pass reduce_max (elementwise max over ranks of a list) so
-        every rank picks the same candidate."""
+        every rank picks the same candidate. `medians` (a list) receives every
+        candidate's median step time."""
         n = len(candidates)
         sts = (C.c_int * n)(*[c[0] for c in candidates])
         als = (_capi.Alloc * n)(*[c[1] for c in candidates])
@@ -172,6 +178,8 @@ class Session:
         meds = list(med)
         if reduce_max is not None:
             meds = reduce_max(meds)
+        if medians is not None:
+            medians[:] = meds
         i = min(range(n), key=lambda j: meds[j])
         return i, meds[i]
 

@@ -106,6 +106,7 @@ SIGNATURES = {
     "c3_session_default_alloc": (I, [P, I, C.POINTER(Alloc)]),
     "c3_session_set_barrier": (I, [P, C.c_void_p, P]),
     "c3_session_set_fused_pace": (I, [P, C.c_float, I]),
+    "c3_session_set_link_rate": (I, [P, C.c_double]),
     "c3_session_load_tables": (I, [P, C.c_char_p]),
     "c3_session_load_params": (I, [P, C.c_char_p]),
     "c3_session_predict": (I, [P, I, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),

@@ -104,6 +104,8 @@ struct FusedComm {
     float pace = 0.0f;               // finish copies by this share of the GEMM's loads (0 = unpaced)
     int64_t piece = 4096;            // bytes per bulk copy (<= 16 KiB buffer)
     int mode = 0;                    // 0: TMA bulk copies (lane 0), 1: LSU vectors (32 lanes)
+    double link_bpns = 0.0;          // > 0: the launch's peer-traffic budget, bytes/ns (link emulation)
+    float link_cta_bpns = 0.0f;      // per-CTA share, set by the launcher from the grid
     Signals sig;
 };
 
@@ -114,13 +116,17 @@ struct MutPtrTable {
     void* p[C3_MAX_RANKS];
 };
 
+// link_bpns > 0: pace the launch's peer traffic to that many bytes/ns in total
+// (= GB/s; NVLink emulation in loopback worlds, c3_session_set_link_rate).
 int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
                           int64_t chunk_bytes, int n_ctas, const Signals& sig,
-                          cudaStream_t stream);
+                          cudaStream_t stream, double link_bpns = 0.0);
 int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
-                         int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream);
+                         int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream,
+                         double link_bpns = 0.0);
 int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
-                               int n_ctas, const Signals& sig, cudaStream_t stream);
+                               int n_ctas, const Signals& sig, cudaStream_t stream,
+                               double link_bpns = 0.0);
 int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor,
                      cudaStream_t stream);
 int launch_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor,

@@ -14,6 +14,12 @@
 //
 // Multi-process completion uses per-rank flag words written with
 // st.release.sys into peers' signal arrays (monotonic epochs; no reset).
+//
+// Link-rate emulation (loopback only, off by default): with cta_bpns > 0 each
+// CTA paces its peer traffic to cta_bpns bytes/ns on the global timer
+// (link_wait, ptx.cuh), so a loopback collective takes the time the node's
+// NVLink would give it regardless of SM clocks or CTA count. The iteration
+// loops are CTA-uniform so the pacing barrier is legal.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -71,15 +77,24 @@ constexpr int kAgExit = 0, kRsEntry = 8, kRsExit = 16;
 
 __global__ void __launch_bounds__(kThreads)
 ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, int n,
-                   int64_t nvec, int64_t slot_vec, int copy_self, int stream_l2, Signals sig) {
+                   int64_t nvec, int64_t slot_vec, int copy_self, int stream_l2, float cta_bpns,
+                   Signals sig) {
     const uint64_t pol = policy_evict_first();
     uint4* dst[C3_MAX_RANKS];
 #pragma unroll
     for (int j = 0; j < C3_MAX_RANKS; ++j)
         dst[j] = j < n ? static_cast<uint4*>(recv.p[j]) + slot_vec * self : nullptr;
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
-         base < nvec; base += step) {
+    const uint64_t t0 = global_ns();
+    double sent = 0.0;  // peer bytes this CTA has pushed (pacing)
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll; blk < nvec; blk += step) {
+        if (cta_bpns > 0.f) {
+            if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
+            __syncthreads();
+            const int64_t left = nvec - blk;
+            sent += 16.0 * (n - 1) * static_cast<double>(left < kThreads * kUnroll ? left : kThreads * kUnroll);
+        }
+        const int64_t base = blk + threadIdx.x;
         uint4 v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
@@ -103,6 +118,7 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
             }
         }
     }
+    if (cta_bpns > 0.f && threadIdx.x == 0) link_wait(t0, sent, cta_bpns);  // the last bytes' link time
     if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
 }
 
@@ -126,15 +142,24 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
 // of rank `self`'s send buffer goes to slot `self` of rank p's receive buffer.
 __global__ void __launch_bounds__(kThreads)
 a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, int n,
-                    int64_t slot_vec, int stream_l2, Signals sig) {
+                    int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
+    const uint64_t t0 = global_ns();
+    double sent = 0.0;
     for (int j = 0; j < n; ++j) {
         const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
         const uint4* src = send + slot_vec * p;
         uint4* dst = static_cast<uint4*>(recv.p[p]) + slot_vec * self;
-        for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll + threadIdx.x;
-             base < slot_vec; base += step) {
+        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll; blk < slot_vec;
+             blk += step) {
+            if (cta_bpns > 0.f && p != self) {
+                if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
+                __syncthreads();
+                const int64_t left = slot_vec - blk;
+                sent += 16.0 * static_cast<double>(left < kThreads * kUnroll ? left : kThreads * kUnroll);
+            }
+            const int64_t base = blk + threadIdx.x;
             uint4 v[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
@@ -153,6 +178,7 @@ a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, 
             }
         }
     }
+    if (cta_bpns > 0.f && threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
     if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
 }
 
@@ -179,15 +205,23 @@ __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& v) {
 template <int N>
 __global__ void __launch_bounds__(kThreads)
 rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
-                   int64_t slot_vec, int stream_l2, Signals sig) {
+                   int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
     if (sig.enabled) entry_barrier(sig, self, N, kRsEntry);
     const uint4* src[N];
 #pragma unroll
     for (int g = 0; g < N; ++g) src[g] = static_cast<const uint4*>(in.p[g]) + slot_vec * self;
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * 2;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * kThreads * 2 + threadIdx.x; base < nvec;
-         base += step) {
+    const uint64_t t0 = global_ns();
+    double pulled = 0.0;  // peer bytes this CTA has read (pacing)
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreads * 2; blk < nvec; blk += step) {
+        if (cta_bpns > 0.f) {
+            if (threadIdx.x == 0) link_wait(t0, pulled, cta_bpns);
+            __syncthreads();
+            const int64_t left = nvec - blk;
+            pulled += 16.0 * (N - 1) * static_cast<double>(left < kThreads * 2 ? left : kThreads * 2);
+        }
+        const int64_t base = blk + threadIdx.x;
         uint4 v[2][N];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
@@ -214,6 +248,7 @@ rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
                 st_v4(out + i, o);
         }
     }
+    if (cta_bpns > 0.f && threadIdx.x == 0) link_wait(t0, pulled, cta_bpns);
     if (sig.enabled) exit_barrier(sig, self, N, kRsExit);
 }
 
@@ -292,7 +327,7 @@ int grid_for(int64_t work_items, int threads, int cap) {
 
 int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
                           int64_t chunk_bytes, int n_ctas, const Signals& sig,
-                          cudaStream_t stream) {
+                          cudaStream_t stream, double link_bpns) {
     if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
         return set_error(C3_ERR_VALIDATION, "allgather: bad rank/world");
     if (chunk_bytes < 0) return set_error(C3_ERR_VALIDATION, "allgather: negative chunk");
@@ -307,7 +342,8 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
         ag_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
                                                          n, nvec, nvec, in_place ? 0 : 1,
-                                                         stream_l2_enabled(), sig);
+                                                         stream_l2_enabled(),
+                                                         static_cast<float>(link_bpns / grid), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(chunk_bytes, 1), kThreads, n_ctas);
         ag_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
@@ -318,7 +354,8 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
 }
 
 int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
-                         int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream) {
+                         int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream,
+                         double link_bpns) {
     if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
         return set_error(C3_ERR_VALIDATION, "alltoall: bad rank/world");
     if (per_peer_bytes < 0) return set_error(C3_ERR_VALIDATION, "alltoall: negative slot");
@@ -330,7 +367,8 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
         const int64_t nvec = per_peer_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
         a2a_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
-                                                          n, nvec, stream_l2_enabled(), sig);
+                                                          n, nvec, stream_l2_enabled(),
+                                                          static_cast<float>(link_bpns / grid), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(per_peer_bytes, 1), kThreads, n_ctas);
         a2a_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
@@ -341,7 +379,7 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
 }
 
 int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
-                               int n_ctas, const Signals& sig, cudaStream_t stream) {
+                               int n_ctas, const Signals& sig, cudaStream_t stream, double link_bpns) {
     if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
         return set_error(C3_ERR_VALIDATION, "reduce_scatter: bad rank/world");
     if (count < 0) return set_error(C3_ERR_VALIDATION, "reduce_scatter: negative count");
@@ -356,8 +394,8 @@ int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, i
         switch (n) {
 #define C3_RS_CASE(N)                                                                          \
     case N:                                                                                    \
-        rs_pull_vec_kernel<N><<<grid, kThreads, 0, stream>>>(in, o, self, nvec, nvec,          \
-                                                             stream_l2_enabled(), sig);         \
+        rs_pull_vec_kernel<N><<<grid, kThreads, 0, stream>>>(                                  \
+            in, o, self, nvec, nvec, stream_l2_enabled(), static_cast<float>(link_bpns / grid), sig); \
         break;
             C3_RS_CASE(1) C3_RS_CASE(2) C3_RS_CASE(3) C3_RS_CASE(4)
             C3_RS_CASE(5) C3_RS_CASE(6) C3_RS_CASE(7) C3_RS_CASE(8)

@@ -94,6 +94,9 @@ __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
     const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + G - 1) / G : 0;
     // expected producer k-blocks of this CTA over the GEMM (pair tiles / pairs)
     const double est_kb = static_cast<double>((p.num_tiles + G / 2 - 1) / (G / 2)) * p.k_blocks;
+    const uint64_t t0 = global_ns();
+    double sent = 0.0;  // peer bytes stored (link emulation)
+    const int targets = fc.kind == 0 ? (fc.skip_self ? fc.n - 1 : fc.n) : 1;
     int64_t k = 0;
     for (int64_t w = blockIdx.x; w < total; w += G, ++k) {
         const int b = static_cast<int>(k & 1);
@@ -102,6 +105,7 @@ __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
             const uint32_t target = static_cast<uint32_t>(est_kb * fc.pace * k / mine);
             while (ld_volatile_shared(progress) < target && !*producer_done) __nanosleep(256);
         }
+        if (fc.link_cta_bpns > 0.f) link_wait(t0, sent, fc.link_cta_bpns);
         const int v = fc.self_begin + static_cast<int>(w / per_v);
         const int64_t r = w % per_v;
         const int q = fc.kind == 0 ? -1 : static_cast<int>(r / pieces);
@@ -109,6 +113,7 @@ __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
         const int64_t off = j * piece;
         const int64_t left = fc.chunk - off;
         const uint32_t len = static_cast<uint32_t>(left < piece ? left : piece);
+        sent += static_cast<double>(len) * (fc.kind == 0 ? targets : (q == v ? 0 : 1));
         const uint8_t* src = fc.src[v] + (fc.kind == 0 ? 0 : static_cast<int64_t>(q) * fc.chunk) + off;
         mbar_arrive_expect_tx(&lbar[b], len);
         bulk_load(buf + b * PIECE, src, len, &lbar[b], pol);
@@ -126,6 +131,7 @@ __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
     }
     bulk_wait_all();
     fence_proxy_async_global();
+    if (fc.link_cta_bpns > 0.f) link_wait(t0, sent, fc.link_cta_bpns);  // the last pieces' link time
 }
 
 // Fused C3, LSU variant (all 32 lanes of warp 3): 16-byte vector loads and
@@ -141,7 +147,17 @@ __device__ void fused_copy_loop_lsu(const Params& p, int lane) {
     const int64_t total = per_v * nv;
     constexpr int U = 4;
     const int64_t step = static_cast<int64_t>(gridDim.x) * 32 * U;
-    for (int64_t base = static_cast<int64_t>(blockIdx.x) * 32 * U + lane; base < total; base += step) {
+    const uint64_t t0 = global_ns();
+    double sent = 0.0;  // peer bytes stored by this warp (link emulation)
+    const double per_vec = 16.0 * (fc.kind == 0 ? (fc.skip_self ? fc.n - 1 : fc.n) : 1);
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * 32 * U; blk < total; blk += step) {
+        if (fc.link_cta_bpns > 0.f) {
+            if (lane == 0) link_wait(t0, sent, fc.link_cta_bpns);
+            __syncwarp();
+            const int64_t left = total - blk;
+            sent += per_vec * static_cast<double>(left < 32 * U ? left : 32 * U);
+        }
+        const int64_t base = blk + lane;
         uint4 v[U];
         int vv[U], qq[U];
         int64_t ii[U];
@@ -172,6 +188,7 @@ __device__ void fused_copy_loop_lsu(const Params& p, int lane) {
         }
     }
     __threadfence_system();
+    if (fc.link_cta_bpns > 0.f && lane == 0) link_wait(t0, sent, fc.link_cta_bpns);
 }
 
 template <bool FUSED>
@@ -461,6 +478,7 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
     if (fc) {
         if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
         p.fc = *fc;
+        p.fc.link_cta_bpns = static_cast<float>(fc->link_bpns / grid);
         p.fc.piece = std::max<int64_t>(16, std::min<int64_t>(fc->piece, gemm2::PIECE)) / 16 * 16;
         gemm2::gemm_bf16_tn_pair_kernel<true><<<grid, gemm2::THREADS, gemm2::SMEM_FUSED, stream>>>(
             plan->map_a, plan->map_b128, p);

@@ -306,6 +306,23 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+// Link-rate governor (NVLink emulation in loopback worlds, c3_session_set_link_rate):
+// the caller has moved `sent` bytes since `t0` at a budget of `bytes_per_ns`;
+// sleep until that volume fits under the budget. Global timer, so the pace does
+// not depend on SM clocks.
+__device__ __forceinline__ uint64_t global_ns() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+__device__ __forceinline__ void link_wait(uint64_t t0, double sent, float bytes_per_ns) {
+    const uint64_t due = t0 + static_cast<uint64_t>(sent / bytes_per_ns);
+    for (uint64_t now = global_ns(); now < due; now = global_ns()) {
+        const uint64_t gap = due - now;
+        __nanosleep(static_cast<unsigned>(gap < 4000 ? gap : 4000));
+    }
+}
+
 // 16-byte streaming load that bypasses L1 allocation; 16-byte store.
 __device__ __forceinline__ uint4 ld_nc_v4(const uint4* p) {
     uint4 v;

@@ -276,6 +276,7 @@ struct c3_session {
     float fused_pace = 0.0f;                // C3_FUSED: copies finish by this share of the GEMM (0 = unpaced)
     int64_t fused_piece = 4096;             // C3_FUSED: bytes per bulk copy
     int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
+    double link_gbps = 0.0;                 // link emulation: peer-traffic budget per step (0 = off)
     c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
     void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
@@ -383,7 +384,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             const Signals sig = make_signals(s, 0);
             for (int v = first; v <= last; ++v) {
                 C3_TRY(launch_allgather_push(v, n, static_cast<uint8_t*>(recv.p[v]) + chunk * v, recv,
-                                             chunk, n_ctas, sig, st));
+                                             chunk, n_ctas, sig, st, s->link_gbps));
                 ++*launches;
             }
         } else {
@@ -407,7 +408,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             const Signals sig = make_signals(s, 0);
             for (int v = first; v <= last; ++v) {
                 C3_TRY(launch_alltoall_push(v, n, loop ? s->in[static_cast<size_t>(v)] : s->in[0], recv,
-                                            chunk, n_ctas, sig, st));
+                                            chunk, n_ctas, sig, st, s->link_gbps));
                 ++*launches;
             }
         } else {
@@ -432,7 +433,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         const Signals sig = make_signals(s, 1);
         for (int v = first; v <= last; ++v) {
             void* out = loop ? s->out[static_cast<size_t>(v)] : s->out[0];
-            C3_TRY(launch_reduce_scatter_pull(v, n, in, out, count, n_ctas, sig, st));
+            C3_TRY(launch_reduce_scatter_pull(v, n, in, out, count, n_ctas, sig, st, s->link_gbps));
             ++*launches;
         }
         return C3_OK;
@@ -1052,6 +1053,13 @@ int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes) {
     return C3_OK;
 }
 
+int c3_session_set_link_rate(c3_session* s, double gbps) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_link_rate: null session");
+    if (!(gbps >= 0.0)) return set_error(C3_ERR_VALIDATION, "link rate must be >= 0 GB/s");
+    s->link_gbps = gbps;  // 1 GB/s = 1 byte/ns
+    return C3_OK;
+}
+
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
     if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_barrier: null session");
     s->barrier = fn;
@@ -1131,6 +1139,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         fc.pace = s->fused_pace;
         fc.piece = s->fused_piece;
         fc.mode = s->fused_mode;
+        fc.link_bpns = s->link_gbps;
         const bool loop = w->loopback != 0;
         fc.self_begin = loop ? 0 : w->rank;
         fc.self_end = loop ? ((flags & kRunAllRanks) ? s->n : 1) : w->rank + 1;

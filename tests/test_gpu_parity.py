@@ -388,3 +388,57 @@ def test_degenerate_worlds(c3, collective):
         s.run(strat, all_ranks=True)
     s.close()
     w.close()
+
+
+@pytest.mark.parametrize("collective", [0, 1, 2], ids=["all-gather", "all-to-all", "reduce-scatter"])
+def test_link_rate_emulation_exact_and_paced(torch_mod, c3, monkeypatch, collective):
+    """c3_session_set_link_rate: the paced SM collective (and the paced fused
+    copies) deliver bit-identical data, and the isolated collective takes the
+    link time (n-1)/n * P / rate, independent of the CTA count."""
+    monkeypatch.setenv("C3_GEMM_KERNEL", "pair")  # the fused path needs the CTA-pair GEMM
+    n, rate = 8, 200.0  # GB/s: slow enough that pacing, not HBM, sets the time
+    payload = n * (8 << 20)  # enough 32 KiB iterations per CTA for the pace to be smooth
+    w = c3.World(0, n, 0, loopback=True)
+    s = c3.Session(w, 512, 1024, 512, collective, payload)
+    chunk = payload // n
+    target_ms = (n - 1) / n * payload / (rate * 1e9) * 1e3
+    s.set_link_rate(rate)
+    for ctas in (16, 64):
+        a = s.default_alloc(c3.COMM_ONLY_CU)
+        a.cus_comm = ctas
+        ms = sorted(_comm_ms(s.run(c3.COMM_ONLY_CU, a)) for _ in range(3))[1]
+        assert 0.95 * target_ms <= ms <= 1.25 * target_ms, (ctas, ms, target_ms)
+    strats = [c3.C3_SP] + ([c3.FUSED] if collective != 2 else [])
+    for strat in strats:
+        s.fill(SEED)
+        t = s.run(strat, all_ranks=True)
+        assert t.total_ms > 0
+        for v in range(n):
+            p = s.pointers(v)
+            if collective == 2:
+                count = chunk // 2
+                host_in = [orc.bf16(n * count, SEED, g, 3) for g in range(n)]
+                got = np.empty(count, np.uint16)
+                c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, count * 2, 2, None))
+                c3.check(c3.lib().c3_stream_sync(None))
+                assert np.array_equal(got, orc.reduce_scatter(host_in, v, count))
+                continue
+            got = np.empty(payload, np.uint8)
+            c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
+            c3.check(c3.lib().c3_stream_sync(None))
+            want = (orc.expected_allgather(n, chunk, SEED, 2) if collective == 0
+                    else orc.expected_alltoall(n, v, chunk, SEED, 4))
+            assert np.array_equal(got, want), f"strategy {strat} rank {v}"
+    s.set_link_rate(0.0)
+    a = s.default_alloc(c3.COMM_ONLY_CU)
+    a.cus_comm = 32
+    fast = min(_comm_ms(s.run(c3.COMM_ONLY_CU, a)) for _ in range(3))
+    assert fast < 0.5 * target_ms  # unpaced is much faster: the pacing is what set the time
+    with pytest.raises(c3.C3Error):
+        s.set_link_rate(-1.0)
+    s.close()
+    w.close()
+
+
+def _comm_ms(t):
+    return t.comm_end_ms - t.comm_start_ms

@@ -1,6 +1,8 @@
 """One small, profiler-friendly invocation per kernel family for ncu:
 GEMM (cfg2 shape by default), loopback all-gather push and reduce-scatter
-pull, all through the C ABI. Usage: python tools/ncu_target.py [gemm|ag|rs|all] [M N K]"""
+pull, and the fused C3 pair GEMM next to the plain pair GEMM (cfg2 + 896 MiB
+all-gather, loopback), all through the C ABI.
+Usage: python tools/ncu_target.py [gemm|ag|rs|fused|all] [M N K]"""
 import os
 import sys
 
@@ -33,4 +35,14 @@ if what in ("ag", "rs", "all"):
         for _ in range(2):
             s.run(c3.COMM_ONLY_CU, a)
         s.close()
+    wl.close()
+if what == "fused":
+    n = 8
+    wl = c3.World(0, n, 0, loopback=True)
+    s = c3.Session(wl, M, N, K, c3.ALL_GATHER, 896 << 20)
+    s.fill()
+    for _ in range(2):
+        s.run(c3.GEMM_ONLY)
+        s.run(c3.FUSED)
+    s.close()
     wl.close()
