@@ -2,7 +2,12 @@
 collective x strategy, in the reference's sweep CSV schema
 (scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal;
 sim.cpp:319-334) plus measured columns. Isolated and concurrent runs are
-interleaved round-robin. usage: python tools/c3_sweep.py OUT.csv [rounds]"""
+interleaved round-robin.
+
+usage: python tools/c3_sweep.py OUT.csv [rounds] [link_gbps]
+link_gbps > 0 paces every SM collective (and the fused copies) to that NVLink
+rate with the session's link governor (c3_session_set_link_rate), so the
+loopback world has the real node's collective time; 0 = full local speed."""
 import os
 import statistics
 import sys
@@ -19,6 +24,8 @@ KIND = {"all-gather": c3.ALL_GATHER, "all-to-all": c3.ALL_TO_ALL,
 def main():
     out_path = sys.argv[1]
     R = int(sys.argv[2]) if len(sys.argv) > 2 else 5
+    link = float(sys.argv[3]) if len(sys.argv) > 3 else 0.0
+    world = f"loopback-8-link{link:.0f}" if link > 0 else "loopback-8"
     rows = ["scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
             "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
             "predicted_makespan_s"]
@@ -32,21 +39,32 @@ def main():
             if os.path.exists(os.path.join(REPO, "data", "b200-loopback-params.json")):
                 s.load_params(os.path.join(REPO, "data", "b200-loopback-params.json"))
             s.fill()
+            s.set_link_rate(link)
             full = w.info.sm_count
             jobs = {"gemm": (c3.GEMM_ONLY, s.default_alloc(c3.GEMM_ONLY))}
             a = s.default_alloc(c3.COMM_ONLY_CU)
             a.cus_comm = full
             jobs["comm"] = (c3.COMM_ONLY_CU, a)
             jobs["comm_dma"] = (c3.COMM_ONLY_DMA, s.default_alloc(c3.COMM_ONLY_DMA))
-            for st in range(1, 7):
+            # copy-engine strategies are not paced (nothing to pace in a DMA
+            # queue; in loopback they are SM copy kernels): full-speed sweep only
+            for st in (range(1, 7) if link == 0 else range(1, 5)):
                 jobs[c3.STRATEGY_NAMES[st]] = (st, s.default_alloc(st))
             for ctas in (16, 32, 64):  # B200 co-resident SM variants
                 a = s.default_alloc(c3.C3_BASE)
                 a.cus_gemm, a.cus_comm = full, ctas
                 jobs[f"c3_base_coresident{ctas}"] = (c3.C3_BASE, a)
+            if KIND[coll] != c3.REDUCE_SCATTER:
+                try:
+                    s.run(c3.FUSED, s.default_alloc(c3.FUSED))
+                    jobs["c3_fused"] = (c3.FUSED, s.default_alloc(c3.FUSED))
+                except c3.C3Error:
+                    pass  # shape not on the CTA-pair GEMM
             t = {k: [] for k in jobs}
+            names = list(jobs)
             for r in range(R + 1):
-                for k, (st, al) in jobs.items():
+                for k in names[r % len(names):] + names[:r % len(names)]:  # rotated order
+                    st, al = jobs[k]
                     tm = s.run(st, al)
                     if r:
                         t[k].append(tm)
@@ -59,19 +77,20 @@ def main():
             sid = f"{name}_{cfg['payload'] >> 20}M"
             flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
             rows.append(f"{sid},{coll},{tax},serial,{(tg + tc) / 1e3:.6g},1,{ideal:.6g},0,{tg:.4f},"
-                        f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,loopback-8,"
+                        f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,{world},"
                         f"{s.predict(c3.SERIAL, tg, tc, td) / 1e3:.6g}")
             for k, (st, al) in jobs.items():
                 if k in ("gemm", "comm", "comm_dma"):
                     continue
-                pred = (s.predict(st, tg, tc, td) / 1e3) if "coresident" not in k else float("nan")
+                pred = (s.predict(st, tg, tc, td) / 1e3) if st <= c3.CONCCL_RP and "coresident" not in k \
+                    else float("nan")
                 mk = med(k, lambda x: x.total_ms)
                 gk = med(k, lambda x: x.gemm_end_ms - x.gemm_start_ms)
                 sp = (tg + tc) / mk
                 rows.append(f"{sid},{coll},{tax},{k},{mk / 1e3:.6g},{sp:.6g},{ideal:.6g},"
                             f"{c3.fraction_of_ideal(sp, ideal):.6g},{tg:.4f},{tc:.4f},"
                             f"{flops / gk / 1e9:.1f},{al.cus_gemm},{al.cus_comm},"
-                            f"{'DMA' if al.backend else 'CU'},loopback-8,{pred:.6g}")
+                            f"{['CU', 'DMA', 'TMA'][al.backend]},{world},{pred:.6g}")
             s.close()
             w.close()
             print(f"{sid} {coll} done", file=sys.stderr, flush=True)

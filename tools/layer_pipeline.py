@@ -4,8 +4,9 @@ ingest_model (reference workload.cpp:217-251): forward GEMMs qkv, attn-out,
 gate+up, down, each weight sharded over 8 ranks. Pair i = GEMM i concurrent
 with the all-gather of weight i+1 (prefetch; the last GEMM prefetches the next
 layer's first weight). Loopback world on one GPU, in two emulations: the
-collective at full local speed, and rate-matched to NVLink (770 GB/s per
-direction, as in bench.py). Isolated and concurrent runs interleaved.
+collective at full local speed, and paced to NVLink (770 GB/s per direction)
+by the session's link governor (c3_session_set_link_rate, as in bench.py).
+Isolated and concurrent runs interleaved in rotated order.
 
 usage: python tools/layer_pipeline.py OUT.csv [rounds]
 """
@@ -22,18 +23,17 @@ TAGS = ["attn_qkv", "attn_out", "ffn_in", "ffn_out"]
 NVLINK_GBPS = 770.0
 
 
-def rate_matched_ctas(s, payload, n):
+def link_ctas(s, payload, n):
+    """Fewest CTAs with which the paced collective reaches the link time (+3%)."""
     target = (n - 1) / n * payload / (NVLINK_GBPS * 1e9) * 1e3
-    best = None
-    for ctas in (2, 4, 6, 8, 12, 16, 24, 32, 48, 64, 96, 148):
+    s.set_link_rate(NVLINK_GBPS)
+    for ctas in (8, 12, 16, 24, 32, 48, 64, 96, 148):
         a = s.default_alloc(c3.COMM_ONLY_CU)
         a.cus_comm = ctas
         ms = statistics.median(s.run(c3.COMM_ONLY_CU, a).comm_end_ms for _ in range(3))
-        if best is None or abs(ms - target) < abs(best[1] - target):
-            best = (ctas, ms)
-        if ms < target:
-            break
-    return best[0]
+        if ms <= 1.03 * target:
+            return ctas
+    return 148
 
 
 def main():
@@ -53,22 +53,23 @@ def main():
             s.fill()
             full = w.info.sm_count
             for emu in ("full-speed", "nvlink-rate"):
-                ctas = full if emu == "full-speed" else rate_matched_ctas(s, payload, n)
+                s.set_link_rate(0.0)
+                ctas = full if emu == "full-speed" else link_ctas(s, payload, n)
                 comm = s.default_alloc(c3.COMM_ONLY_CU)
-                comm.cus_comm = ctas
+                comm.cus_comm = ctas  # isolated: whole GPU, or the link-rate CTA count
                 jobs = {"gemm": (c3.GEMM_ONLY, s.default_alloc(c3.GEMM_ONLY)),
                         "comm": (c3.COMM_ONLY_CU, comm)}
                 for st in (c3.C3_BASE, c3.C3_SP):
-                    for cc in sorted({min(ctas, 64), 32} if emu == "full-speed" else {ctas}):
+                    for cc in sorted({32, 64} if emu == "full-speed" else {ctas, 2 * ctas}):
                         a = s.default_alloc(st)
                         a.cus_gemm, a.cus_comm = full, cc
                         jobs[f"{c3.STRATEGY_NAMES[st]}_coresident{cc}"] = (st, a)
                 try:
                     s.run(c3.FUSED, s.default_alloc(c3.FUSED))
-                    if emu == "full-speed":
-                        jobs["c3_fused"] = (c3.FUSED, s.default_alloc(c3.FUSED))
+                    jobs["c3_fused"] = (c3.FUSED, s.default_alloc(c3.FUSED))
                 except c3.C3Error:
                     pass
+                s.set_link_rate(NVLINK_GBPS if emu == "nvlink-rate" else 0.0)
                 t = {k: [] for k in jobs}
                 names = list(jobs)
                 for r in range(R + 1):
