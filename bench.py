@@ -452,6 +452,7 @@ def run_ours(args, dist):
     e2e_speedup = (e2e_g + e2e_c - io_ms) / e2e_conc
 
     peaks, peak_src = load_peaks()
+    peak_sus = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
     flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
     gemm_avg = sum(gemm_ms) / len(gemm_ms)
     achieved = flops / (gemm_avg * 1e-3) / 1e12
@@ -499,10 +500,11 @@ def run_ours(args, dist):
         "loopback_full_speed": full_speed,
         "strategies_full_speed": results,
         "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tn_pair_kernel (tcgen05 cta_group::2)",
-                     "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                     "frac": achieved / peaks["bf16_tflops"],
-                     "frac_of_sustained": achieved / peaks.get("bf16_tflops_sustained", 1365.0),
-                     "peak_source": peak_src + " burst bf16 (cuBLAS)",
+                     "achieved": achieved, "peak": peak_sus, "unit": "TFLOP/s",
+                     "frac": achieved / peak_sus,
+                     "frac_of_burst": achieved / peaks["bf16_tflops"],
+                     "peak_source": peak_src + " sustained bf16 (cuBLAS back to back under the "
+                                    "power cap): the GEMM is timed inside a long step",
                      "algorithmic_flops_per_launch": flops, "traffic": traffic},
         "e2e": {"value": e2e_speedup, "unit": "x (t_serial / t_concurrent, host buffers)",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

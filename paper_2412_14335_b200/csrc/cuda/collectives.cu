@@ -122,6 +122,66 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
     if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
 }
 
+// All-gather, push form on the SM's TMA unit: one thread per CTA streams this
+// CTA's pieces of the chunk global -> shared memory (nbuf buffers, loads
+// issued nbuf-1 pieces ahead) -> slot `self` of every rank with bulk stores
+// (cp.async.bulk), so a CTA moves `piece` bytes per instruction instead of 16.
+constexpr int kBulkMaxBufs = 8;
+__global__ void __launch_bounds__(32)
+ag_push_bulk_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self, int n, int64_t chunk,
+                    int copy_self, int piece, int nbuf, int stream_l2, float cta_bpns, Signals sig) {
+    extern __shared__ __align__(128) uint8_t bulk_buf[];
+    __shared__ __align__(8) uint64_t bar[kBulkMaxBufs];
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < nbuf; ++b) mbar_init(&bar[b], 1);
+        fence_mbar_init();
+        const uint64_t pol = stream_l2 ? policy_evict_first() : policy_evict_normal();
+        const int64_t G = gridDim.x;
+        const int64_t pieces = (chunk + piece - 1) / piece;
+        const int64_t mine = pieces > blockIdx.x ? (pieces - blockIdx.x + G - 1) / G : 0;
+        const int targets = copy_self ? n : n - 1;
+        auto piece_len = [&](int64_t k) {
+            const int64_t left = chunk - (blockIdx.x + k * G) * piece;
+            return static_cast<uint32_t>(left < piece ? left : piece);
+        };
+        auto issue_load = [&](int64_t k) {
+            const int b = static_cast<int>(k % nbuf);
+            const uint32_t len = piece_len(k);
+            mbar_arrive_expect_tx(&bar[b], len);
+            bulk_load(bulk_buf + static_cast<int64_t>(b) * piece, src + (blockIdx.x + k * G) * piece, len,
+                      &bar[b], pol);
+        };
+        for (int64_t k = 0; k < nbuf - 1 && k < mine; ++k) issue_load(k);
+        const uint64_t t0 = global_ns();
+        double sent = 0.0;
+        for (int64_t k = 0; k < mine; ++k) {
+            const int b = static_cast<int>(k % nbuf);
+            const uint32_t len = piece_len(k);
+            mbar_wait(&bar[b], static_cast<uint32_t>((k / nbuf) & 1));
+            if (cta_bpns > 0.f) link_wait(t0, sent, cta_bpns);
+            sent += static_cast<double>(len) * (n - 1);
+            const int64_t off = static_cast<int64_t>(self) * chunk + (blockIdx.x + k * G) * piece;
+            for (int j = 1; j <= n; ++j) {  // rotated targets
+                const int p = (self + j) % n;
+                if (p == self && !copy_self) continue;
+                bulk_store(static_cast<uint8_t*>(recv.p[p]) + off, bulk_buf + static_cast<int64_t>(b) * piece,
+                           len, pol);
+            }
+            bulk_commit();
+            // refill buffer (k-1) % nbuf (stores = group k-1) with piece k+nbuf-1
+            if (k + nbuf - 1 < mine) {
+                bulk_wait_read<1>();
+                issue_load(k + nbuf - 1);
+            }
+        }
+        bulk_wait_all();
+        fence_proxy_async_global();
+        if (cta_bpns > 0.f) link_wait(t0, sent, cta_bpns);
+        (void)targets;
+    }
+    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+}
+
 // Byte-granular fallback shape for chunks that are not 16-byte multiples or
 // 16-byte aligned (tiny parity cases only; large runs always take the vector path).
 __global__ void __launch_bounds__(kThreads)
@@ -318,6 +378,24 @@ int stream_l2_enabled() {
     return on;
 }
 
+// Bulk-copy (TMA) all-gather: C3_COMM_IMPL=bulk selects it, C3_COMM_PIECE /
+// C3_COMM_NBUF size its shared-memory ring (dev A/B).
+struct BulkCfg {
+    bool on;
+    int piece, nbuf;
+};
+const BulkCfg& bulk_cfg() {
+    static const BulkCfg c = [] {
+        BulkCfg b{false, 16384, 4};
+        const char* e = std::getenv("C3_COMM_IMPL");
+        b.on = e != nullptr && std::string(e) == "bulk";
+        if (const char* p = std::getenv("C3_COMM_PIECE")) b.piece = std::max(16, std::atoi(p) / 16 * 16);
+        if (const char* q = std::getenv("C3_COMM_NBUF")) b.nbuf = std::min(kBulkMaxBufs, std::max(2, std::atoi(q)));
+        return b;
+    }();
+    return c;
+}
+
 int grid_for(int64_t work_items, int threads, int cap) {
     const int64_t g = (work_items + threads - 1) / threads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, cap)));
@@ -337,7 +415,21 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
     uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(chunk_bytes);
     for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
     if (chunk_bytes == 0 && !sig.enabled) return C3_OK;
-    if ((align & 15) == 0) {
+    if ((align & 15) == 0 && bulk_cfg().on) {
+        const BulkCfg& bc = bulk_cfg();
+        const size_t smem = static_cast<size_t>(bc.piece) * bc.nbuf;
+        static bool attr = false;
+        if (!attr) {
+            C3_CUDA(cudaFuncSetAttribute(ag_push_bulk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(smem)));
+            attr = true;
+        }
+        const int grid = grid_for(std::max<int64_t>(chunk_bytes, 1), bc.piece, n_ctas);
+        ag_push_bulk_kernel<<<grid, 32, smem, stream>>>(static_cast<const uint8_t*>(send), recv, self, n,
+                                                        chunk_bytes, in_place ? 0 : 1, bc.piece, bc.nbuf,
+                                                        stream_l2_enabled(),
+                                                        static_cast<float>(link_bpns / grid), sig);
+    } else if ((align & 15) == 0) {
         const int64_t nvec = chunk_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
         ag_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,

@@ -62,6 +62,8 @@ struct Params {
     int* tile_counter;
     int* exit_counter;
     int group_m;
+    int pol_a, pol_b;  // L2 policy of the A / B operand loads (policy_by_kind)
+    int pol_c;         // C stores: 0 = plain, else an L2 cache hint (policy_by_kind)
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -252,7 +254,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 
     if (warp == 0 && lane == 0) {
         // ------------- tile claims (leader) + TMA producer (both CTAs) -------------
-        const uint64_t keep = policy_evict_last();
+        const uint64_t pol_a = policy_by_kind(p.pol_a);
+        const uint64_t pol_b = policy_by_kind(p.pol_b);
         int stage = 0;
         uint32_t phase = 0;
         int tile = leader ? atomicAdd(p.tile_counter, 1) : 0;
@@ -280,8 +283,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
-                tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, keep);
-                tma_load_2d_pair(smem_b + stage * B_STAGE, &map_b, &full[stage], kb * BK, b_row, keep);
+                tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, pol_a);
+                tma_load_2d_pair(smem_b + stage * B_STAGE, &map_b, &full[stage], kb * BK, b_row, pol_b);
                 if (FUSED) st_volatile_shared(progress, ld_volatile_shared(progress) + 1);
                 if (++stage == STAGES) {
                     stage = 0;
@@ -342,6 +345,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
         int acc = 0;
         uint32_t acc_phase = 0;
+        const uint64_t pol_c = policy_by_kind(p.pol_c);
         for (int i = 0;; ++i) {
             const int r = i % RING;
             if (leader)
@@ -386,7 +390,10 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                         o.y = *reinterpret_cast<uint32_t*>(&h1);
                         o.z = *reinterpret_cast<uint32_t*>(&h2);
                         o.w = *reinterpret_cast<uint32_t*>(&h3);
-                        dst[j] = o;
+                        if (p.pol_c)
+                            st_stream_v4(dst + j, o, pol_c);
+                        else
+                            dst[j] = o;
                     }
                 } else {
 #pragma unroll
@@ -475,6 +482,15 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return v > 0 ? v : gemm2::GROUP_M_DEFAULT;
     }();
     p.group_m = band;
+    // L2 policies of the operand loads, "<a><b>" digits (C3_GEMM_POL env, dev A/B)
+    // and of the C stores ("<a><b><c>", c = 0 plain)
+    static const int pol = [] {
+        const char* e = std::getenv("C3_GEMM_POL");
+        return e && e[0] && e[1] && e[2] ? (e[0] - '0') * 100 + (e[1] - '0') * 10 + (e[2] - '0') : 110;
+    }();
+    p.pol_a = pol / 100;
+    p.pol_b = pol / 10 % 10;
+    p.pol_c = pol % 10;
     if (fc) {
         if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
         p.fc = *fc;

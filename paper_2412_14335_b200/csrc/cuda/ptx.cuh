@@ -74,6 +74,15 @@ __device__ __forceinline__ uint64_t policy_evict_first() {
     asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
     return p;
 }
+__device__ __forceinline__ uint64_t policy_evict_normal() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+// 1 = evict_last, 2 = evict_first, anything else = evict_normal
+__device__ __forceinline__ uint64_t policy_by_kind(int kind) {
+    return kind == 1 ? policy_evict_last() : kind == 2 ? policy_evict_first() : policy_evict_normal();
+}
 
 // ------------------------------------------------------------- tcgen05 ---
 
