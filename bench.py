@@ -178,6 +178,9 @@ def run_ours(args, dist):
     params = os.path.join(REPO, "data", "b200-loopback-params.json")
     if os.path.exists(params):
         sess.load_params(params)
+    cores = os.path.join(REPO, "data", "b200-coresident.json")
+    if os.path.exists(cores):
+        sess.load_coresident(cores)  # B200 co-residency in the model (c3sim/coresident.hpp)
     strategies = [c3.STRATEGY_NAMES.index(s) for s in args.strategies]
 
     def timed(strategy, steps, alloc=None, link=0.0):
@@ -287,6 +290,11 @@ def run_ours(args, dist):
         warm = rounds(head_iso, 3)
         t_g_pick = median([r[1] for r in warm["gemm"]])
         t_c_pick = median([r[2] for r in warm["cu"]])
+        # the collective's measured time vs CTAs at the link rate (flat from
+        # nvl_ctas on) replaces the full-speed comm table in the model
+        curve = {c: t for c, t in nvl_probe.items() if c < nvl_ctas}
+        curve.update({nvl_ctas: t_c_pick, full: t_c_pick})
+        sess.set_comm_curve(sorted(curve.items()))
     else:
         t_g_pick, t_c_pick = t_g, iso_comm["cu"]
 
@@ -322,7 +330,7 @@ def run_ours(args, dist):
     tune = None
     if args.strategy == "auto":
         head, head_alloc, predicted = sess.choose(t_g_pick, t_c_pick, iso_comm["dma"], dma_ok)
-        if emulate:
+        if emulate and head_alloc.cus_gemm + head_alloc.cus_comm <= full:
             head_alloc.cus_comm = nvl_ctas  # the model's split, the collective at NVLink rate
         cands = [(head, head_alloc)] + (emulated_candidates() if emulate else full_speed_candidates())
         sess.set_link_rate(link)
@@ -332,7 +340,10 @@ def run_ours(args, dist):
         tune = {"candidates": [{"strategy": c3.STRATEGY_NAMES[st], "cus_gemm": a.cus_gemm,
                                 "cus_comm": a.cus_comm, "median_ms": ms}
                                for (st, a), ms in zip(cands, meds)],
-                "model_pick": c3.STRATEGY_NAMES[head], "picked_index": best_i, "picked_ms": best_ms}
+                "model_pick": c3.STRATEGY_NAMES[head], "model_alloc": {"cus_gemm": head_alloc.cus_gemm,
+                                                                      "cus_comm": head_alloc.cus_comm},
+                "model_pick_coresident": head_alloc.cus_gemm + head_alloc.cus_comm > full,
+                "picked_index": best_i, "picked_ms": best_ms}
         head, head_alloc = cands[best_i]
     else:
         head = c3.STRATEGY_NAMES.index(args.strategy)

@@ -273,6 +273,24 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
 /* The model's predicted makespan of one strategy (same inputs as choose). */
 int c3_session_predict(c3_session* s, int strategy, double t_gemm_ms, double t_comm_cu_ms,
                        double t_comm_dma_ms, double* predicted_ms);
+/* B200 extension: co-residency in the model (include/c3sim/coresident.hpp).
+ * set_comm_curve: the collective's measured isolated time (ms) at each CTA
+ * count (strictly increasing), under this world's real or emulated link rate;
+ * it replaces the collective's slowdown table in every prediction (n = 0
+ * restores the loaded table). load_coresident: co-residency penalties JSON
+ * ({"gemm-compute-bound", "gemm-memory-bound", "comm"}; fitted by
+ * tools/calibrate_coresident.py, e.g. data/b200-coresident.json); once loaded,
+ * c3_session_choose also predicts the co-resident execution (GEMM on every SM,
+ * the SM collective on c CTAs beside it) for c in {8,16,24,32,48,64} and the
+ * curve's points, and returns it as C3_C3_SP with cus_gemm = all SMs,
+ * cus_comm = c, comm_first = 1 when it is fastest. NULL path disables. */
+int c3_session_set_comm_curve(c3_session* s, const int* ctas, const double* ms, int n);
+int c3_session_load_coresident(c3_session* s, const char* json_path);
+/* Prediction for an explicit allocation: co-resident allocations (CU backend,
+ * cus_gemm + cus_comm > SMs) use the co-resident model, others as
+ * c3_session_predict. */
+int c3_session_predict_alloc(c3_session* s, int strategy, const c3_alloc* alloc, double t_gemm_ms,
+                             double t_comm_cu_ms, double t_comm_dma_ms, double* predicted_ms);
 /* Measured refinement: run each (strategy, alloc) candidate `rounds` times in
  * round-robin order; medians[i] = candidate i's median step time, *best =
  * this rank's fastest. Multi-process: every rank must pass the same

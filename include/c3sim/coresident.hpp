@@ -1,0 +1,74 @@
+// c3-b200 extension (no counterpart in the reference): co-residency in the
+// interference model.
+//
+// The reference partitions CUs: a kernel pair shares the GPU as
+// cus_gemm + cus_comm <= C (sim.cpp:40-100), and the SM strategies pay the
+// GEMM's CU-loss slowdown. On B200 a P2P collective's CTA (512 threads, no
+// shared memory) fits on the same SM as the persistent GEMM's CTA, so the
+// GEMM keeps all C SMs and the collective runs on `cus_comm` CTAs beside it
+// (DESIGN.md §5.4). This header models that execution mode with the same
+// two-phase fluid form as simulate() (sim.cpp:121-215):
+//   phase 1: GEMM rate 1/p_g, collective rate 1/(t_c(c)/t_c * p_c)
+//   phase 2: the survivor alone at rate 1.
+// t_c(c) comes from a measured CommCurve (collective time vs CTA count under
+// the world's link conditions), p_g / p_c are co-residency penalties fitted
+// on measured co-resident runs (tools/calibrate_coresident.py).
+#pragma once
+
+#include <filesystem>
+#include <string>
+#include <vector>
+
+#include "c3sim/interference.hpp"
+#include "c3sim/machine.hpp"
+#include "c3sim/sim.hpp"
+
+namespace c3sim {
+
+/// Measured isolated collective time (seconds) vs CTA count, under the world's
+/// real (or emulated) link rate. Points sorted by ctas, times > 0.
+struct CommCurve {
+    std::vector<int> ctas;
+    std::vector<double> seconds;
+
+    bool empty() const { return ctas.empty(); }
+    /// Linear between points; below the first point time scales as 1/ctas
+    /// (bandwidth per CTA), above the last it stays flat.
+    double time_at(int cus) const;
+    /// Slowdown table over grain multiples up to C: t(c) / t(C), last point 1.0.
+    SlowdownTable as_table(KernelClass cls, const MachineDescriptor& md) const;
+};
+
+void validate(const CommCurve& c);
+
+/// Co-residency penalties: residual slowdown of each kernel while both are
+/// resident on the same SMs (1.0 = no interference).
+struct CoResidentParams {
+    double gemm_compute_bound = 1.0;
+    double gemm_memory_bound = 1.0;
+    double comm = 1.0;
+
+    double gemm(KernelClass gemm_class) const {
+        return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
+    }
+};
+
+void validate(const CoResidentParams& p);
+
+/// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc}.
+CoResidentParams load_coresident_params(const std::filesystem::path& path);
+std::string save_coresident_params(const CoResidentParams& p);
+
+/// Two-phase fluid prediction of a co-resident run: GEMM on all CUs
+/// (t_gemm seconds alone), collective on cus_comm CTAs (t_comm_at_ctas
+/// seconds alone at that CTA count). serial_time / ideal use t_comm_full,
+/// the collective's isolated time on the whole GPU (the paper's t_comm).
+SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
+                                int cus_comm, KernelClass gemm_class, const CoResidentParams& p);
+
+/// Penalty p_g that makes simulate_coresident reproduce a measured makespan
+/// (collective finishing first, p_c = 1); clamped to [1, 100]. Returns 1.0
+/// when the GEMM finished first or the inputs leave no overlap to explain.
+double fit_coresident_gemm_penalty(double t_gemm, double t_comm_at_ctas, double makespan);
+
+}  // namespace c3sim

@@ -163,6 +163,28 @@ class Session:
                                        C.byref(ms)))
         return ms.value
 
+    def set_comm_curve(self, points):
+        """Measured collective time vs CTA count [(ctas, ms), ...] under this
+        world's link rate; replaces the comm slowdown table in predictions
+        ([] restores it)."""
+        pts = sorted(points)
+        n = len(pts)
+        ct = (C.c_int * max(n, 1))(*[int(c) for c, _ in pts])
+        ms = (C.c_double * max(n, 1))(*[float(t) for _, t in pts])
+        check(lib().c3_session_set_comm_curve(self.h, ct, ms, n))
+
+    def load_coresident(self, json_path):
+        """Co-residency penalties (B200 model extension); None disables."""
+        check(lib().c3_session_load_coresident(self.h, json_path.encode() if json_path else None))
+
+    def predict_alloc(self, strategy, alloc, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms=0.0):
+        """Predicted makespan (ms) of (strategy, alloc); co-resident allocations
+        use the co-resident model."""
+        ms = C.c_double()
+        check(lib().c3_session_predict_alloc(self.h, strategy, C.byref(alloc), t_gemm_ms, t_comm_cu_ms,
+                                             t_comm_dma_ms, C.byref(ms)))
+        return ms.value
+
     def autotune(self, candidates, rounds=3, reduce_max=None, medians=None):
         """candidates: [(strategy, Alloc)] -> (best index, median ms). With
         several ranks pass reduce_max (elementwise max over ranks of a list) so

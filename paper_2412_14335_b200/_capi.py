@@ -114,6 +114,10 @@ SIGNATURES = {
                                 C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     "c3_session_choose": (I, [P, C.c_double, C.c_double, C.c_double, I, C.POINTER(C.c_int),
                               C.POINTER(Alloc), C.POINTER(C.c_double)]),
+    "c3_session_set_comm_curve": (I, [P, C.POINTER(C.c_int), C.POINTER(C.c_double), I]),
+    "c3_session_load_coresident": (I, [P, C.c_char_p]),
+    "c3_session_predict_alloc": (I, [P, I, C.POINTER(Alloc), C.c_double, C.c_double, C.c_double,
+                                     C.POINTER(C.c_double)]),
 }
 
 

@@ -28,6 +28,7 @@
 
 #include "c3cuda_internal.hpp"
 #include "c3sim/conccl.hpp"
+#include "c3sim/coresident.hpp"
 #include "c3sim/errors.hpp"
 #include "c3sim/params_io.hpp"
 #include "c3sim/sim.hpp"
@@ -286,8 +287,12 @@ struct c3_session {
                 ev_ce = nullptr, ev_end = nullptr;
     c3sim::MachineDescriptor md;
     c3sim::SlowdownTableSet tables;
+    c3sim::SlowdownTableSet tables_loaded;  // as loaded (tables' comm class may come from comm_curve)
     c3sim::CoRunPenalty penalties = c3sim::CoRunPenalty::ones();  // c3_session_load_params
     c3sim::C3Scenario scenario;
+    c3sim::CommCurve comm_curve;            // c3_session_set_comm_curve (seconds)
+    bool coresident = false;                // c3_session_load_coresident: model co-residency
+    c3sim::CoResidentParams cores;
 };
 
 namespace {
@@ -913,6 +918,11 @@ int c3_session_load_tables(c3_session* s, const char* csv_path) {
     if (!s || !csv_path) return set_error(C3_ERR_VALIDATION, "c3_session_load_tables: null argument");
     return guarded([&] {
         s->tables = c3sim::load_slowdown_tables(csv_path, s->md.min_cu_grain);
+        s->tables_loaded = s->tables;
+        if (!s->comm_curve.empty()) {
+            const auto cls = c3sim::comm_kernel_class(s->scenario.collective.kind);
+            s->tables.at(cls) = s->comm_curve.as_table(cls, s->md);
+        }
         return C3_OK;
     });
 }
@@ -943,7 +953,81 @@ double predict_makespan(c3_session* s, int st, double t_gemm_ms, double t_comm_c
     return c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff).makespan;
 }
 
+// Collective time (ms) on `ctas` CTAs given its measured full-GPU time: the
+// measured comm curve's shape when set, else the loaded comm table.
+double comm_ms_at(const c3_session* s, int ctas, double t_comm_cu_ms) {
+    if (!s->comm_curve.empty())
+        return t_comm_cu_ms * s->comm_curve.time_at(ctas) / s->comm_curve.time_at(s->md.cus_per_gpu);
+    const auto cls = c3sim::comm_kernel_class(s->scenario.collective.kind);
+    return t_comm_cu_ms * c3sim::slowdown_at(s->tables.at(cls), ctas);
+}
+
+// B200 co-resident prediction (include/c3sim/coresident.hpp): GEMM on all
+// SMs, the SM collective on `ctas` CTAs beside it.
+double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, double t_comm_cu_ms) {
+    const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
+    return c3sim::simulate_coresident(t_gemm_ms * 1e-3, comm_ms_at(s, ctas, t_comm_cu_ms) * 1e-3,
+                                      t_comm_cu_ms * 1e-3, s->md.cus_per_gpu, ctas, gcls, s->cores)
+        .makespan;
+}
+
+bool is_coresident(const c3_session* s, int st, const c3_alloc* a) {
+    return a && st >= C3_C3_BASE && st <= C3_C3_SP_RP && a->backend == C3_BACKEND_CU &&
+           a->cus_gemm + a->cus_comm > s->md.cus_per_gpu;
+}
+
 }  // namespace
+
+int c3_session_set_comm_curve(c3_session* s, const int* ctas, const double* ms, int n) {
+    if (!s || n < 0 || (n > 0 && (!ctas || !ms)))
+        return set_error(C3_ERR_VALIDATION, "c3_session_set_comm_curve: bad argument");
+    return guarded([&] {
+        const auto cls = c3sim::comm_kernel_class(s->scenario.collective.kind);
+        if (n == 0) {
+            s->comm_curve = {};
+            s->tables.at(cls) = s->tables_loaded.at(cls);
+            return C3_OK;
+        }
+        c3sim::CommCurve c;
+        for (int i = 0; i < n; ++i) {
+            c.ctas.push_back(ctas[i]);
+            c.seconds.push_back(ms[i] * 1e-3);
+        }
+        c3sim::validate(c);
+        s->tables.at(cls) = c.as_table(cls, s->md);
+        s->comm_curve = std::move(c);
+        return C3_OK;
+    });
+}
+
+int c3_session_load_coresident(c3_session* s, const char* json_path) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_load_coresident: null session");
+    if (!json_path) {
+        s->coresident = false;
+        return C3_OK;
+    }
+    return guarded([&] {
+        s->cores = c3sim::load_coresident_params(json_path);
+        s->coresident = true;
+        return C3_OK;
+    });
+}
+
+int c3_session_predict_alloc(c3_session* s, int strategy, const c3_alloc* alloc, double t_gemm_ms,
+                             double t_comm_cu_ms, double t_comm_dma_ms, double* predicted_ms) {
+    if (!s || !alloc || !predicted_ms) return set_error(C3_ERR_VALIDATION, "c3_session_predict_alloc: null argument");
+    if (!is_coresident(s, strategy, alloc))
+        return c3_session_predict(s, strategy, t_gemm_ms, t_comm_cu_ms, t_comm_dma_ms, predicted_ms);
+    if (!(t_gemm_ms > 0 && t_comm_cu_ms > 0))
+        return set_error(C3_ERR_VALIDATION, "c3_session_predict_alloc: isolated times must be positive");
+    if (!s->coresident)
+        return set_error(C3_ERR_VALIDATION, "c3_session_predict_alloc: co-resident allocation needs "
+                                            "c3_session_load_coresident");
+    return guarded([&] {
+        *predicted_ms = predict_coresident(s, alloc->cus_comm, t_gemm_ms, t_comm_cu_ms) * 1e3;
+        return C3_OK;
+    });
+}
 
 int c3_session_load_params(c3_session* s, const char* params_json_path) {
     if (!s || !params_json_path) return set_error(C3_ERR_VALIDATION, "c3_session_load_params: null argument");
@@ -993,8 +1077,45 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
                 best_st = st;
             }
         }
+        // B200 co-resident candidates: GEMM on every SM, collective CTAs beside
+        // it. Among them the FEWEST CTAs within 1% of the best prediction win:
+        // past the link-bound plateau extra comm CTAs only add interference the
+        // fluid model does not see (measured: c3_sp on 64 CTAs 10% slower than
+        // on 24, profiles/r01_c3_sweep_link770_cores.csv).
+        int best_cores = 0;
+        if (s->coresident) {
+            std::vector<int> cands = {8, 16, 24, 32, 48, 64};
+            for (int c : s->comm_curve.ctas) cands.push_back(c);
+            std::sort(cands.begin(), cands.end());
+            cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
+            std::vector<std::pair<int, double>> pred;
+            double best_co = 1e300;
+            for (int c : cands) {
+                if (c < 1 || c >= s->md.cus_per_gpu) continue;
+                pred.emplace_back(c, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms));
+                best_co = std::min(best_co, pred.back().second);
+            }
+            for (const auto& [c, m] : pred) {
+                if (m <= best_co * 1.01) {  // ascending c: the first within 1%
+                    if (m < best) {
+                        best = m;
+                        best_st = C3_C3_SP;
+                        best_cores = c;
+                    }
+                    break;
+                }
+            }
+        }
         *strategy = best_st;
         *predicted_ms = best * 1e3;
+        if (best_cores) {
+            alloc->cus_gemm = s->md.cus_per_gpu;
+            alloc->cus_comm = best_cores;
+            alloc->cus_idle = 0;
+            alloc->backend = C3_BACKEND_CU;
+            alloc->comm_first = 1;
+            return C3_OK;
+        }
         c3sim::EfficiencyParams eff;
         eff.comm_launch_overhead_cu = 0.0;
         c3sim::C3Scenario x = s->scenario;

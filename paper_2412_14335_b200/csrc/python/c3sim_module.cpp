@@ -17,6 +17,7 @@
 
 #include "c3sim/calibrate.hpp"
 #include "c3sim/conccl.hpp"
+#include "c3sim/coresident.hpp"
 #include "c3sim/errors.hpp"
 #include "c3sim/exec.hpp"
 #include "c3sim/machine.hpp"
@@ -216,6 +217,25 @@ void add_sim(py::module_& m) {
     m.def("simulate", &cs::simulate, py::arg("scenario"), py::arg("strategy"), py::arg("machine"),
           py::arg("tables"), py::arg("penalties"), py::arg("params"), py::arg("options") = SO{});
     m.def("work_conservation_check", &cs::work_conservation_check);
+
+    // B200 extension: co-residency in the model (c3sim/coresident.hpp)
+    using CC = cs::CommCurve;
+    py::class_<CC>(m, "CommCurve")
+        .def(py::init<>())
+        .def(py::init([](std::vector<int> c, std::vector<double> t) { return CC{std::move(c), std::move(t)}; }),
+             py::arg("ctas"), py::arg("seconds"))
+        .RW(CC, ctas).RW(CC, seconds)
+        .def("time_at", &CC::time_at)
+        .def("as_table", &CC::as_table);
+    using CRP = cs::CoResidentParams;
+    py::class_<CRP>(m, "CoResidentParams")
+        .def(py::init<>())
+        .RW(CRP, gemm_compute_bound).RW(CRP, gemm_memory_bound).RW(CRP, comm);
+    m.def("load_coresident_params", &cs::load_coresident_params);
+    m.def("save_coresident_params", &cs::save_coresident_params);
+    m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),
+          py::arg("t_comm_full"), py::arg("cus"), py::arg("cus_comm"), py::arg("gemm_class"), py::arg("params"));
+    m.def("fit_coresident_gemm_penalty", &cs::fit_coresident_gemm_penalty);
 
     using SR = cs::SweepRow;
     using AR = cs::AggregateRow;

@@ -1,0 +1,104 @@
+"""B200 model extension: co-residency (include/c3sim/coresident.hpp) through
+the product pybind module. CPU only: the fluid-model arithmetic, the measured
+comm curve, the penalty fit (the inverse of the model) and the params file."""
+import math
+import os
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(REPO, "paper_2412_14335_b200", "python"))
+import c3sim  # noqa: E402
+
+CB = c3sim.KernelClass.GEMM_COMPUTE_BOUND
+MB = c3sim.KernelClass.GEMM_MEMORY_BOUND
+
+
+def test_comm_curve_interpolation_and_clamps():
+    c = c3sim.CommCurve([8, 16, 24], [2.0e-3, 1.2e-3, 1.0e-3])
+    assert c.time_at(16) == pytest.approx(1.2e-3)
+    assert c.time_at(20) == pytest.approx(1.1e-3)
+    assert c.time_at(4) == pytest.approx(4.0e-3)    # below the first point: 1/ctas
+    assert c.time_at(148) == pytest.approx(1.0e-3)  # link-bound: flat above the last
+
+
+def test_comm_curve_as_table_is_a_valid_slowdown_table():
+    md = c3sim.load_machine_file(c3sim.data_path("b200-loopback-node.json"))
+    c = c3sim.CommCurve([8, 16, 24], [2.0e-3, 1.2e-3, 1.0e-3])
+    t = c.as_table(c3sim.KernelClass.ALL_GATHER, md)
+    pts = [(p.cus, p.slowdown) for p in t.points]
+    assert pts[-1] == (md.cus_per_gpu, 1.0)
+    assert all(p[0] % md.min_cu_grain == 0 for p in pts)
+    assert all(s >= 1.0 for _, s in pts)
+    assert dict(pts)[8] == pytest.approx(2.0)
+
+
+@pytest.mark.parametrize("bad", [([16, 8], [1e-3, 1e-3]), ([8], [0.0]), ([8, 16], [1e-3])])
+def test_comm_curve_validation(bad):
+    md = c3sim.load_machine_file(c3sim.data_path("b200-loopback-node.json"))
+    with pytest.raises(Exception):
+        c3sim.CommCurve(*bad).as_table(c3sim.KernelClass.ALL_GATHER, md)
+
+
+def test_coresident_unit_penalties_hide_the_shorter_kernel():
+    p = c3sim.CoResidentParams()
+    tl = c3sim.simulate_coresident(2.5e-3, 1.1e-3, 1.1e-3, 148, 24, CB, p)
+    assert tl.makespan == pytest.approx(2.5e-3)
+    assert tl.speedup == pytest.approx(tl.ideal)
+    assert tl.fraction_of_ideal == pytest.approx(1.0)
+    tl = c3sim.simulate_coresident(0.3e-3, 2.0e-3, 2.0e-3, 148, 32, MB, p)  # C-long
+    assert tl.makespan == pytest.approx(2.0e-3)
+
+
+def test_coresident_penalty_closed_form():
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound = 1.2
+    tg, tc = 2.4e-3, 1.0e-3
+    tl = c3sim.simulate_coresident(tg, tc, tc, 148, 24, CB, p)
+    # phase 1 ends with the collective at tc; the GEMM did tc/1.2 of its work
+    assert tl.makespan == pytest.approx(tc + tg - tc / 1.2)
+    assert len(tl.phases) == 2 and tl.phases[0].cus_gemm == 148 and tl.phases[0].cus_comm == 24
+    # the memory-bound penalty is separate
+    assert c3sim.simulate_coresident(tg, tc, tc, 148, 24, MB, p).makespan == pytest.approx(tg)
+
+
+def test_coresident_slower_ctas_stretch_the_collective():
+    p = c3sim.CoResidentParams()
+    # 8 CTAs take 2x the full-GPU collective time; the collective outlives the GEMM
+    tl = c3sim.simulate_coresident(1.0e-3, 2.4e-3, 1.2e-3, 148, 8, CB, p)
+    assert tl.makespan == pytest.approx(2.4e-3)
+    assert tl.serial_time == pytest.approx(2.2e-3)  # t_comm = the full-GPU time
+    assert tl.speedup < 1.0 and tl.fraction_of_ideal == 0.0
+
+
+@pytest.mark.parametrize("pen", [1.0, 1.07, 1.3, 2.0])
+def test_fit_is_the_inverse_of_the_model(pen):
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound = pen
+    tg, tc = 2.5e-3, 1.1e-3
+    mk = c3sim.simulate_coresident(tg, tc, tc, 148, 24, CB, p).makespan
+    assert c3sim.fit_coresident_gemm_penalty(tg, tc, mk) == pytest.approx(pen)
+
+
+def test_fit_degenerate_cases():
+    assert c3sim.fit_coresident_gemm_penalty(1e-3, 2e-3, 2e-3) == 1.0   # collective outlived the GEMM
+    assert c3sim.fit_coresident_gemm_penalty(1e-3, 0.5e-3, 0.4e-3) == 1.0  # faster than possible
+    assert c3sim.fit_coresident_gemm_penalty(1e-3, 0.5e-3, 5e-3) == 100.0
+
+
+def test_params_roundtrip_and_validation(tmp_path):
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound, p.gemm_memory_bound, p.comm = 1.1, 1.3, 1.05
+    f = tmp_path / "cores.json"
+    f.write_text(c3sim.save_coresident_params(p))
+    q = c3sim.load_coresident_params(str(f))
+    assert (q.gemm_compute_bound, q.gemm_memory_bound, q.comm) == (1.1, 1.3, 1.05)
+    f.write_text('{"gemm-compute-bound": 0.9, "gemm-memory-bound": 1.0}')
+    with pytest.raises(Exception):
+        c3sim.load_coresident_params(str(f))
+
+
+def test_shipped_coresident_params_load():
+    q = c3sim.load_coresident_params(c3sim.data_path("b200-coresident.json"))
+    assert 1.0 <= q.gemm_compute_bound < 2.0 and 1.0 <= q.gemm_memory_bound and not math.isnan(q.comm)

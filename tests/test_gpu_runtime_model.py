@@ -1,0 +1,87 @@
+"""GPU: the runtime heuristic with the B200 co-residency model extension
+(c3_session_set_comm_curve / c3_session_load_coresident / c3_session_predict_alloc,
+include/c3sim/coresident.hpp), through the C ABI on a loopback session, checked
+against the same model evaluated by the pybind module on the CPU."""
+import os
+import sys
+
+import pytest
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(REPO, "paper_2412_14335_b200", "python"))
+
+pytestmark = pytest.mark.gpu
+CORES = os.path.join(REPO, "data", "b200-coresident.json")
+
+
+@pytest.fixture(scope="module")
+def c3():
+    import paper_2412_14335_b200 as c3
+    return c3
+
+
+@pytest.fixture()
+def session(c3):
+    w = c3.World(0, 8, 0, loopback=True)
+    s = c3.Session(w, 1024, 1024, 1024, c3.ALL_GATHER, 8 << 20)
+    s.load_tables(os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv"))
+    s.load_params(os.path.join(REPO, "data", "b200-loopback-params.json"))
+    yield w, s
+    s.close()
+    w.close()
+
+
+def test_choose_picks_coresident_from_the_curve(c3, session):
+    import c3sim
+    w, s = session
+    sms = w.info.sm_count
+    s.load_coresident(CORES)
+    # link-bound collective: 1.0 ms from 24 CTAs on, slower below
+    s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
+    st, a, pred = s.choose(3.0, 1.0, 0.0, allow_dma=False)
+    assert st == c3.C3_SP and a.cus_gemm == sms and a.cus_comm == 24 and a.comm_first == 1
+    p = c3sim.load_coresident_params(CORES)
+    want = c3sim.simulate_coresident(3.0e-3, 1.0e-3, 1.0e-3, sms, 24,
+                                     c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
+    assert pred == pytest.approx(want)
+    assert s.predict_alloc(st, a, 3.0, 1.0) == pytest.approx(want)
+    # 16 CTAs: the collective takes 2 ms on them
+    a.cus_comm = 16
+    want16 = c3sim.simulate_coresident(3.0e-3, 2.0e-3, 1.0e-3, sms, 16,
+                                       c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
+    assert s.predict_alloc(c3.C3_SP, a, 3.0, 1.0) == pytest.approx(want16)
+    # a plateau: 32 CTAs a hair faster than 24 -> still the fewest within 1%
+    s.set_comm_curve([(8, 4.0), (24, 1.004), (32, 1.0), (sms, 1.0)])
+    st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
+    assert st == c3.C3_SP and a.cus_comm == 24
+
+
+def test_partitioned_allocations_keep_the_reference_model(c3, session):
+    w, s = session
+    s.load_coresident(CORES)
+    a = s.default_alloc(c3.C3_RP)
+    assert a.cus_gemm + a.cus_comm <= w.info.sm_count
+    assert s.predict_alloc(c3.C3_RP, a, 3.0, 1.0) == pytest.approx(s.predict(c3.C3_RP, 3.0, 1.0))
+
+
+def test_without_coresident_params_choose_is_the_reference_heuristic(c3, session):
+    w, s = session
+    s.load_coresident(None)
+    st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
+    assert a.cus_gemm + a.cus_comm <= w.info.sm_count or st == c3.SERIAL
+    co = s.default_alloc(c3.C3_SP)
+    co.cus_gemm, co.cus_comm = w.info.sm_count, 24
+    with pytest.raises(c3.C3Error):
+        s.predict_alloc(c3.C3_SP, co, 3.0, 1.0)
+
+
+def test_comm_curve_changes_and_restores_reference_predictions(c3, session):
+    _, s = session
+    base = s.predict(c3.C3_RP, 3.0, 1.0)
+    s.set_comm_curve([(8, 8.0), (148, 1.0)])  # a collective that needs many CTAs
+    slow = s.predict(c3.C3_RP, 3.0, 1.0)
+    s.set_comm_curve([])
+    assert s.predict(c3.C3_RP, 3.0, 1.0) == pytest.approx(base)
+    assert slow != pytest.approx(base)
+    with pytest.raises(c3.C3Error):
+        s.set_comm_curve([(16, 1.0), (16, 2.0)])

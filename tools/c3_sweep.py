@@ -7,7 +7,13 @@ interleaved round-robin.
 usage: python tools/c3_sweep.py OUT.csv [rounds] [link_gbps]
 link_gbps > 0 paces every SM collective (and the fused copies) to that NVLink
 rate with the session's link governor (c3_session_set_link_rate), so the
-loopback world has the real node's collective time; 0 = full local speed."""
+loopback world has the real node's collective time; 0 = full local speed.
+
+The co-resident rows also carry t_comm_ctas_ms, the isolated collective on
+that many CTAs (the comm curve), and their model prediction uses the B200
+co-residency extension (c3_session_set_comm_curve + data/b200-coresident.json).
+OUT.picks.csv compares the runtime heuristic's pick (c3_session_choose) with
+the measured best per scenario."""
 import os
 import statistics
 import sys
@@ -28,7 +34,11 @@ def main():
     world = f"loopback-8-link{link:.0f}" if link > 0 else "loopback-8"
     rows = ["scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
             "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
-            "predicted_makespan_s"]
+            "predicted_makespan_s,t_comm_ctas_ms"]
+    picks = ["scenario_id,collective,model_pick,model_cus_comm,model_predicted_ms,model_pick_measured_ms,"
+             "measured_best,measured_best_ms,pick_over_best"]
+    CORES = (16, 24, 32, 64)
+    cores_json = os.path.join(REPO, "data", "b200-coresident.json")
     for name in ("cfg2", "cfg2_448", "cfg3", "cfg4", "cfg4_mb"):
         cfg = CONFIGS[name]
         colls = [cfg["coll"]] + (["all-to-all"] if cfg["coll"] == "all-gather" else [])
@@ -50,10 +60,16 @@ def main():
             # queue; in loopback they are SM copy kernels): full-speed sweep only
             for st in (range(1, 7) if link == 0 else range(1, 5)):
                 jobs[c3.STRATEGY_NAMES[st]] = (st, s.default_alloc(st))
-            for ctas in (16, 32, 64):  # B200 co-resident SM variants
+            for ctas in CORES:  # B200 co-resident SM variants + the comm curve
                 a = s.default_alloc(c3.C3_BASE)
                 a.cus_gemm, a.cus_comm = full, ctas
                 jobs[f"c3_base_coresident{ctas}"] = (c3.C3_BASE, a)
+                a = s.default_alloc(c3.C3_SP)
+                a.cus_gemm, a.cus_comm = full, ctas
+                jobs[f"c3_sp_coresident{ctas}"] = (c3.C3_SP, a)
+                a = s.default_alloc(c3.COMM_ONLY_CU)
+                a.cus_comm = ctas
+                jobs[f"comm_c{ctas}"] = (c3.COMM_ONLY_CU, a)
             if KIND[coll] != c3.REDUCE_SCATTER:
                 try:
                     s.run(c3.FUSED, s.default_alloc(c3.FUSED))
@@ -72,31 +88,57 @@ def main():
             tg = med("gemm", lambda x: x.gemm_end_ms - x.gemm_start_ms)
             tc = med("comm", lambda x: x.comm_end_ms - x.comm_start_ms)
             td = med("comm_dma", lambda x: x.comm_end_ms - x.comm_start_ms)
+            curve = {c: med(f"comm_c{c}", lambda x: x.comm_end_ms - x.comm_start_ms) for c in CORES}
+            s.set_comm_curve(sorted(curve.items()) + [(full, tc)])
+            if os.path.exists(cores_json):
+                s.load_coresident(cores_json)
             ideal = c3.ideal_speedup(tg, tc)
             tax = "G-long" if tg > 1.15 * tc else "C-long" if tc > 1.15 * tg else "GC-equal"
             sid = f"{name}_{cfg['payload'] >> 20}M"
             flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
             rows.append(f"{sid},{coll},{tax},serial,{(tg + tc) / 1e3:.6g},1,{ideal:.6g},0,{tg:.4f},"
                         f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,{world},"
-                        f"{s.predict(c3.SERIAL, tg, tc, td) / 1e3:.6g}")
+                        f"{s.predict(c3.SERIAL, tg, tc, td) / 1e3:.6g},")
+            measured = {}
             for k, (st, al) in jobs.items():
-                if k in ("gemm", "comm", "comm_dma"):
+                if k in ("gemm", "comm", "comm_dma") or k.startswith("comm_c"):
                     continue
-                pred = (s.predict(st, tg, tc, td) / 1e3) if st <= c3.CONCCL_RP and "coresident" not in k \
-                    else float("nan")
+                try:
+                    pred = s.predict_alloc(st, al, tg, tc, td) / 1e3 if st <= c3.CONCCL_RP else float("nan")
+                except c3.C3Error:
+                    pred = float("nan")
                 mk = med(k, lambda x: x.total_ms)
                 gk = med(k, lambda x: x.gemm_end_ms - x.gemm_start_ms)
                 sp = (tg + tc) / mk
                 rows.append(f"{sid},{coll},{tax},{k},{mk / 1e3:.6g},{sp:.6g},{ideal:.6g},"
                             f"{c3.fraction_of_ideal(sp, ideal):.6g},{tg:.4f},{tc:.4f},"
                             f"{flops / gk / 1e9:.1f},{al.cus_gemm},{al.cus_comm},"
-                            f"{['CU', 'DMA', 'TMA'][al.backend]},{world},{pred:.6g}")
+                            f"{['CU', 'DMA', 'TMA'][al.backend]},{world},{pred:.6g},"
+                            f"{curve[al.cus_comm] if 'coresident' in k else ''}")
+                measured[k] = (mk, st, al)
+            # the runtime heuristic's pick vs the measured best
+            st, al, pred = s.choose(tg, tc, td, allow_dma=False)
+            key = next((k for k, (_, s2, a2) in measured.items()
+                        if s2 == st and a2.cus_gemm == al.cus_gemm and a2.cus_comm == al.cus_comm), None)
+            if st == c3.SERIAL:
+                key, pk = "serial", tg + tc
+            else:
+                pk = measured[key][0] if key else float("nan")
+            best = min(measured, key=lambda k: measured[k][0])
+            bm = min(measured[best][0], tg + tc)
+            if tg + tc < measured[best][0]:
+                best = "serial"
+            picks.append(f"{sid},{coll},{key or c3.STRATEGY_NAMES[st]},{al.cus_comm},{pred:.4f},{pk:.4f},"
+                         f"{best},{bm:.4f},{pk / bm:.4f}")
             s.close()
             w.close()
             print(f"{sid} {coll} done", file=sys.stderr, flush=True)
     with open(out_path, "w") as f:
         f.write("\n".join(rows) + "\n")
+    with open(os.path.splitext(out_path)[0] + ".picks.csv", "w") as f:
+        f.write("\n".join(picks) + "\n")
     print("\n".join(rows))
+    print("\n".join(picks))
 
 
 if __name__ == "__main__":
