@@ -1137,8 +1137,11 @@ int c3_session_autotune(c3_session* s, const int* strategies, const c3_alloc* al
     if (!s || !strategies || !allocs || !medians || !best || !best_ms || n < 1 || rounds < 1)
         return set_error(C3_ERR_VALIDATION, "c3_session_autotune: bad argument");
     std::vector<std::vector<double>> t(static_cast<size_t>(n));
-    for (int r = 0; r < rounds; ++r)  // round-robin so clock drift hits all alike
-        for (int i = 0; i < n; ++i) {
+    // round-robin so clock drift hits all alike, starting one candidate later
+    // each round: under the power cap a run's clocks depend on its predecessor
+    for (int r = 0; r < rounds; ++r)
+        for (int j = 0; j < n; ++j) {
+            const int i = (j + r) % n;
             c3_timing tm;
             C3_TRY(c3_session_run(s, strategies[i], &allocs[i], &tm));
             t[static_cast<size_t>(i)].push_back(tm.total_ms);

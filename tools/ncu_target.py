@@ -2,7 +2,8 @@
 GEMM (cfg2 shape by default), loopback all-gather push and reduce-scatter
 pull, and the fused C3 pair GEMM next to the plain pair GEMM (cfg2 + 896 MiB
 all-gather, loopback), all through the C ABI.
-Usage: python tools/ncu_target.py [gemm|ag|rs|fused|all] [M N K]"""
+cublas: torch.matmul (cuBLAS) on the same shape, for a side-by-side capture.
+Usage: python tools/ncu_target.py [gemm|cublas|ag|rs|fused|all] [M N K]"""
 import os
 import sys
 
@@ -23,6 +24,13 @@ if what in ("gemm", "all"):
         w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K)
     torch.cuda.synchronize()
     w.close()
+if what == "cublas":
+    A = torch.randn(M, K, device="cuda", dtype=torch.bfloat16)
+    B = torch.randn(N, K, device="cuda", dtype=torch.bfloat16)
+    Cm = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    for _ in range(2):
+        torch.matmul(A, B.t(), out=Cm)
+    torch.cuda.synchronize()
 if what in ("ag", "rs", "all"):
     n = 8
     wl = c3.World(0, n, 0, loopback=True)
