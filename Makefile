@@ -18,7 +18,7 @@ OBJ      := build/obj
 ARCH     := -gencode arch=compute_100a,code=sm_100a
 
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -Iinclude -I$(JSON_DIR)
-NVFLAGS  := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Iinclude -I$(PKG)/csrc/cuda \
+NVFLAGS  := -std=c++17 -O3 $(ARCH) $(NVCC_EXTRA) -lineinfo -Xcompiler -fPIC -Iinclude -I$(PKG)/csrc/cuda \
             --expt-relaxed-constexpr -ccbin $(CXX) -Xptxas -v
 
 MODEL_SRC := $(wildcard $(PKG)/csrc/model/*.cpp)

@@ -61,10 +61,11 @@ int set_driver_error(CUresult r, const char* what);
 
 // ------------------------------------------------------------------- GEMM
 struct GemmPlan {
-    enum Kind { kWide = 0, kNarrow = 1, kPair = 2 };  // 128x256, 128x128, pair 256x256
+    enum Kind { kWide = 0, kNarrow = 1, kPair = 2, kPair512 = 3 };  // 128x256, 128x128, pair 256x256 / 256x512
     CUtensorMap map_a;     // 128-row boxes
     CUtensorMap map_b128;  // 128-row boxes (pair half tile, narrow kernel)
     CUtensorMap map_b256;  // 256-row boxes (wide kernel)
+    CUtensorMap map_c;     // C stores: 32-row x 64-column boxes, 128B swizzle (pair kernels)
     void* c = nullptr;
     int* counters = nullptr;  // device [tile claims, CTA exits]; zero between launches
     int64_t m = 0, n = 0, k = 0;

@@ -33,7 +33,15 @@ namespace c3k {
 
 namespace {
 
-constexpr int kThreads = 512;
+constexpr int kThreads = 512;  // byte-granular kernels (tiny parity cases)
+// Vector collectives run 256-thread CTAs, two per unit of the caller's CTA
+// budget (n_ctas counts 512-thread equivalents, the unit the slowdown tables
+// and allocations were measured in). A 256-thread CTA fits beside the pair
+// GEMM's CTA (256 x 152 registers) in one SM's 64K registers, where a
+// 512-thread one (16 warps x 56 allocated) does not: the co-resident C3 mode.
+constexpr int kVecThreads = 256;
+constexpr int kCtasPerUnit = 2;
+constexpr int kThreadsRs = kVecThreads;
 constexpr int kUnroll = 4;
 
 // Last-CTA election + cross-rank exit barrier. Called by every thread of every
@@ -75,7 +83,7 @@ __device__ void entry_barrier(const Signals& sig, int self, int n, int slot_base
 // entry, [16,24) reduce-scatter exit, [24,32) copy-engine exit.
 constexpr int kAgExit = 0, kRsEntry = 8, kRsExit = 16;
 
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kVecThreads)
 ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, int n,
                    int64_t nvec, int64_t slot_vec, int copy_self, int stream_l2, float cta_bpns,
                    Signals sig) {
@@ -84,21 +92,21 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
 #pragma unroll
     for (int j = 0; j < C3_MAX_RANKS; ++j)
         dst[j] = j < n ? static_cast<uint4*>(recv.p[j]) + slot_vec * self : nullptr;
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnroll;
     const uint64_t t0 = global_ns();
     double sent = 0.0;  // peer bytes this CTA has pushed (pacing)
-    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll; blk < nvec; blk += step) {
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnroll; blk < nvec; blk += step) {
         if (cta_bpns > 0.f) {
             if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
             __syncthreads();
             const int64_t left = nvec - blk;
-            sent += 16.0 * (n - 1) * static_cast<double>(left < kThreads * kUnroll ? left : kThreads * kUnroll);
+            sent += 16.0 * (n - 1) * static_cast<double>(left < kVecThreads * kUnroll ? left : kVecThreads * kUnroll);
         }
         const int64_t base = blk + threadIdx.x;
         uint4 v[kUnroll];
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
-            const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+            const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
             if (i < nvec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
         }
         // peers in rotated order so the ranks do not all start on the same target
@@ -108,7 +116,7 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
             uint4* d = dst[p];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+                const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
                 if (i < nvec) {
                     if (stream_l2)
                         st_stream_v4(d + i, v[u], pol);
@@ -200,35 +208,35 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
 
 // All-to-all, push form (plan_all_to_all's mapping, conccl.cpp:55-84): slot p
 // of rank `self`'s send buffer goes to slot `self` of rank p's receive buffer.
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kVecThreads)
 a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, int n,
                     int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * kUnroll;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnroll;
     const uint64_t t0 = global_ns();
     double sent = 0.0;
     for (int j = 0; j < n; ++j) {
         const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
         const uint4* src = send + slot_vec * p;
         uint4* dst = static_cast<uint4*>(recv.p[p]) + slot_vec * self;
-        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreads * kUnroll; blk < slot_vec;
+        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnroll; blk < slot_vec;
              blk += step) {
             if (cta_bpns > 0.f && p != self) {
                 if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
                 __syncthreads();
                 const int64_t left = slot_vec - blk;
-                sent += 16.0 * static_cast<double>(left < kThreads * kUnroll ? left : kThreads * kUnroll);
+                sent += 16.0 * static_cast<double>(left < kVecThreads * kUnroll ? left : kVecThreads * kUnroll);
             }
             const int64_t base = blk + threadIdx.x;
             uint4 v[kUnroll];
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+                const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
                 if (i < slot_vec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
             }
 #pragma unroll
             for (int u = 0; u < kUnroll; ++u) {
-                const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+                const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
                 if (i < slot_vec) {
                     if (stream_l2)
                         st_stream_v4(dst + i, v[u], pol);
@@ -263,7 +271,7 @@ __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& v) {
 }
 
 template <int N>
-__global__ void __launch_bounds__(kThreads)
+__global__ void __launch_bounds__(kThreadsRs)
 rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
                    int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
@@ -271,21 +279,21 @@ rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
     const uint4* src[N];
 #pragma unroll
     for (int g = 0; g < N; ++g) src[g] = static_cast<const uint4*>(in.p[g]) + slot_vec * self;
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads * 2;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kThreadsRs * 2;
     const uint64_t t0 = global_ns();
     double pulled = 0.0;  // peer bytes this CTA has read (pacing)
-    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreads * 2; blk < nvec; blk += step) {
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kThreadsRs * 2; blk < nvec; blk += step) {
         if (cta_bpns > 0.f) {
             if (threadIdx.x == 0) link_wait(t0, pulled, cta_bpns);
             __syncthreads();
             const int64_t left = nvec - blk;
-            pulled += 16.0 * (N - 1) * static_cast<double>(left < kThreads * 2 ? left : kThreads * 2);
+            pulled += 16.0 * (N - 1) * static_cast<double>(left < kThreadsRs * 2 ? left : kThreadsRs * 2);
         }
         const int64_t base = blk + threadIdx.x;
         uint4 v[2][N];
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+            const int64_t i = base + static_cast<int64_t>(u) * kThreadsRs;
             if (i < nvec)
 #pragma unroll
                 for (int g = 0; g < N; ++g)
@@ -293,7 +301,7 @@ rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
         }
 #pragma unroll
         for (int u = 0; u < 2; ++u) {
-            const int64_t i = base + static_cast<int64_t>(u) * kThreads;
+            const int64_t i = base + static_cast<int64_t>(u) * kThreadsRs;
             if (i >= nvec) continue;
             float acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
@@ -431,8 +439,8 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
                                                         static_cast<float>(link_bpns / grid), sig);
     } else if ((align & 15) == 0) {
         const int64_t nvec = chunk_bytes / 16;
-        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
-        ag_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnroll, n_ctas * kCtasPerUnit);
+        ag_push_vec_kernel<<<grid, kVecThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
                                                          n, nvec, nvec, in_place ? 0 : 1,
                                                          stream_l2_enabled(),
                                                          static_cast<float>(link_bpns / grid), sig);
@@ -457,8 +465,8 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
     for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
     if ((align & 15) == 0) {
         const int64_t nvec = per_peer_bytes / 16;
-        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * kUnroll, n_ctas);
-        a2a_push_vec_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnroll, n_ctas * kCtasPerUnit);
+        a2a_push_vec_kernel<<<grid, kVecThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
                                                           n, nvec, stream_l2_enabled(),
                                                           static_cast<float>(link_bpns / grid), sig);
     } else {
@@ -481,12 +489,12 @@ int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, i
     for (int g = 0; g < n; ++g) align |= reinterpret_cast<uintptr_t>(in.p[g]);
     if ((align & 15) == 0) {
         const int64_t nvec = count / 8;
-        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreads * 2, n_ctas);
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kThreadsRs * 2, n_ctas * kCtasPerUnit);
         uint4* o = static_cast<uint4*>(out);
         switch (n) {
 #define C3_RS_CASE(N)                                                                          \
     case N:                                                                                    \
-        rs_pull_vec_kernel<N><<<grid, kThreads, 0, stream>>>(                                  \
+        rs_pull_vec_kernel<N><<<grid, kThreadsRs, 0, stream>>>(                                \
             in, o, self, nvec, nvec, stream_l2_enabled(), static_cast<float>(link_bpns / grid), sig); \
         break;
             C3_RS_CASE(1) C3_RS_CASE(2) C3_RS_CASE(3) C3_RS_CASE(4)

@@ -336,18 +336,25 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
         return set_error(C3_ERR_VALIDATION, "gemm: dimension too large");
     if (!counters) return set_error(C3_ERR_VALIDATION, "gemm: missing tile-claim counters");
-    // Kernel choice: CTA-pair 256x256 tiles when there is at least one pair
-    // tile per SM pair; else single-CTA 128x256 tiles, or 128x128 when that
-    // leaves fewer than two tiles per SM (e.g. M=128: 208 -> 416 tiles).
+    // Kernel choice: CTA-pair 256x512, else 256x256 tiles when there is at
+    // least one pair tile per SM pair; else single-CTA 128x256 tiles, or
+    // 128x128 when that leaves fewer than two tiles per SM (e.g. M=128: 208 ->
+    // 416 tiles).
     const int64_t sms = std::max(sm_count, 2);
     const int64_t tm1 = (m + 127) / 128;
     const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
-    plan->kind = m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
+    const int64_t pair512_tiles = ((m + 255) / 256) * ((n + 511) / 512);
+    // 256x512 pair tiles when every SM pair gets one: 25% less L2->SM operand
+    // traffic than 256x256, which the 1 kW power cap turns into clock
+    // (sustained cfg2 / 8192^3 / cfg4: +3% / +4% / +7%, profiles/r01_gemm_pair512_ab.txt)
+    plan->kind = m >= 256 && pair512_tiles >= sms / 2 ? GemmPlan::kPair512
+                 : m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
                  : tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow
                                                      : GemmPlan::kWide;
     if (const char* f = std::getenv("C3_GEMM_KERNEL")) {  // tests force each variant
         const std::string v(f);
         if (v == "pair") plan->kind = GemmPlan::kPair;
+        if (v == "pair512") plan->kind = GemmPlan::kPair512;
         if (v == "wide") plan->kind = GemmPlan::kWide;
         if (v == "narrow") plan->kind = GemmPlan::kNarrow;
     }
@@ -356,6 +363,8 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
         r = encode_kmajor_bf16(&plan->map_b128, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 128);
     if (r == CUDA_SUCCESS)
         r = encode_kmajor_bf16(&plan->map_b256, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 256);
+    if (r == CUDA_SUCCESS)  // C [m, n] in 32-row x 64-column boxes (pair kernels' TMA-store epilogue)
+        r = encode_kmajor_bf16(&plan->map_c, C, static_cast<uint64_t>(m), static_cast<uint64_t>(n), 32);
     if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
     plan->m = m;
     plan->n = n;
@@ -363,8 +372,9 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     plan->c = C;
     plan->counters = counters;
     plan->k_blocks = static_cast<int>((k + gemm::BK - 1) / gemm::BK);
-    const int bm = plan->kind == GemmPlan::kPair ? 256 : 128;
-    const int bn = plan->kind == GemmPlan::kNarrow ? 128 : 256;
+    const bool pair = plan->kind == GemmPlan::kPair || plan->kind == GemmPlan::kPair512;
+    const int bm = pair ? 256 : 128;
+    const int bn = plan->kind == GemmPlan::kNarrow ? 128 : plan->kind == GemmPlan::kPair512 ? 512 : 256;
     plan->tiles_m = static_cast<int>((m + bm - 1) / bm);
     plan->tiles_n = static_cast<int>((n + bn - 1) / bn);
     plan->num_tiles = plan->tiles_m * plan->tiles_n;
@@ -375,9 +385,10 @@ int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStrea
                      const FusedComm* fc) {
     int grid = max_ctas > 0 ? max_ctas : sm_count;
     grid = std::min(grid, sm_count);
-    if (fc && (plan->kind != GemmPlan::kPair || grid < 2))
+    const bool pair = plan->kind == GemmPlan::kPair || plan->kind == GemmPlan::kPair512;
+    if (fc && (!pair || grid < 2))
         return set_error(C3_ERR_UNSUPPORTED, "fused C3 needs the CTA-pair GEMM (M >= 256, enough tiles)");
-    if (plan->kind == GemmPlan::kPair && grid >= 2) {
+    if (pair && grid >= 2) {
         // whole CTA pairs; a fused launch keeps every pair (its copy warps move data)
         grid = fc ? grid / 2 * 2 : std::min(grid / 2, plan->num_tiles) * 2;
         return gemm_pair_launch(plan, grid, stream, fc);

@@ -15,16 +15,18 @@
 //               TMA loads complete_tx on it (peer bit of the address cleared)
 //   empty[s]    both CTAs; the leader's tcgen05.commit multicasts to both
 //   acc_full[b] both CTAs; multicast commit after a tile's last k-block
-//   acc_empty[b] leader; 4 local + 4 remote epilogue-warp arrivals
+//   acc_empty[b] leader; EPI_WARPS local + EPI_WARPS remote epilogue-warp arrivals
 //   tile ring   leader claims tiles (global atomic, one tile ahead), writes
 //               the id into both CTAs' rings (st.shared::cluster) and arrives
 //               on both tile_full; consumers of both CTAs release the slot on
-//               the leader's tile_empty (1 MMA + 4 + 1 peer producer + 4).
+//               the leader's tile_empty (1 MMA + EPI_WARPS + 1 peer producer
+//               + EPI_WARPS).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <string>
 
 #include "c3cuda_internal.hpp"
 #include "ptx.cuh"
@@ -33,12 +35,9 @@ namespace c3k {
 namespace gemm2 {
 
 constexpr int BM = 256;        // pair tile rows (128 per CTA)
-constexpr int BN = 256;        // pair tile cols (B: 128 rows per CTA)
 constexpr int BK = 64;
 constexpr int UK = 16;
-constexpr int STAGES = 6;
-constexpr int ACC_BUFS = 2;
-constexpr int THREADS = 256;
+constexpr int THREADS = 256;  // 256-wide tiles: warps 0-3 roles, 4-7 epilogue
 // Pair-rows per raster band (C3_GEMM_BAND env overrides, dev A/B). Measured
 // DRAM reads per cfg2 launch: band 8 -> 2.39 GB, 16 -> 3.85 GB, 32 -> 12.3 GB
 // (profiles/r01_gemm_band_ab.txt): the L2 is split across the two dies, so a
@@ -46,13 +45,40 @@ constexpr int THREADS = 256;
 constexpr int GROUP_M_DEFAULT = 8;
 constexpr int RING = 4;
 constexpr uint32_t A_STAGE = 128 * BK * 2;  // this CTA's 128 rows of A
-constexpr uint32_t B_STAGE = 128 * BK * 2;  // this CTA's 128 rows of B
-constexpr uint32_t STAGE = A_STAGE + B_STAGE;
-constexpr uint32_t TMEM_COLS = ACC_BUFS * BN;
-constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 512;
+constexpr uint32_t B_HALF = 128 * BK * 2;   // this CTA's 128 rows of one 256-column half of B
+constexpr uint32_t TMEM_COLS = 512;
 // fused C3: two 16 KiB copy buffers in the shared memory the GEMM leaves free
-constexpr uint32_t PIECE = 16 * 1024;
-constexpr uint32_t SMEM_FUSED = SMEM + 2 * PIECE + 64;
+constexpr uint32_t PIECE = 8 * 1024;
+// epilogue staging per warp: 32 rows x 64 bf16 columns
+constexpr uint32_t kEpiWarpStage = 32 * 128;
+
+// Pair tile 256 x BN. BN = 256: two TMEM accumulators (the epilogue of tile i
+// overlaps the MMAs of tile i+1), 6 stages. BN = 512: one accumulator filling
+// all 512 TMEM columns (the epilogue is exposed), 4 stages, but each k-block
+// moves 48 KiB of operands per CTA for 2x the MMA work of a 256-wide tile
+// (64 KiB per 256x256x64 -> 48 KiB): 25% less L2->SM traffic, which under
+// the 1 kW power cap is clock (profiles/r01_ncu_gemm_vs_cublas.txt).
+template <int BN_>
+struct PairCfg {
+    static constexpr int BN = BN_;
+    static constexpr int HALVES = BN / 256;  // N=256 MMAs per k-step
+    static constexpr int STAGES = BN == 256 ? 6 : 4;
+    static constexpr int ACC_BUFS = BN == 256 ? 2 : 1;
+    // epilogue warps (one per TMEM lane quadrant; 8 = two per quadrant, each
+    // half the columns, measured no faster for 512-wide tiles)
+    static constexpr int EPI_WARPS = 4;
+    static constexpr int THREADS = 128 + 32 * EPI_WARPS;
+    static constexpr uint32_t B_STAGE = HALVES * B_HALF;
+    static constexpr uint32_t STAGE = A_STAGE + B_STAGE;
+    // C staging: two tiles per epilogue warp (one when fused: the copy
+    // buffers take the other's shared memory)
+    static constexpr uint32_t EPI_SMEM = EPI_WARPS * kEpiWarpStage;
+    static constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 2 * EPI_SMEM + 512;
+    static constexpr uint32_t SMEM_FUSED = STAGES * STAGE + 1024 + EPI_SMEM + 512 + 2 * PIECE + 64;
+    static_assert(SMEM <= 227 * 1024 && SMEM_FUSED <= 227 * 1024, "shared memory");
+    static_assert(ACC_BUFS * BN <= static_cast<int>(TMEM_COLS), "TMEM");
+    static_assert(BN / (EPI_WARPS / 4) % 128 == 0, "epilogue drains 128 columns per step");
+};
 
 struct Params {
     int m, n, k;
@@ -63,7 +89,6 @@ struct Params {
     int* exit_counter;
     int group_m;
     int pol_a, pol_b;  // L2 policy of the A / B operand loads (policy_by_kind)
-    int pol_c;         // C stores: 0 = plain, else an L2 cache hint (policy_by_kind)
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -193,10 +218,21 @@ __device__ void fused_copy_loop_lsu(const Params& p, int lane) {
     if (fc.link_cta_bpns > 0.f && lane == 0) link_wait(t0, sent, fc.link_cta_bpns);
 }
 
-template <bool FUSED>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(THREADS, 1)
+// <= 152 registers per thread: 256 x 152 = 38K of the SM's 64K leaves room
+// for a collective CTA beside the GEMM's (all-gather / all-to-all: 512 x 50;
+// reduce-scatter: 256 x 96), the B200 co-resident C3 mode.
+// (setmaxnreg would not help: ptxas sizes every path for the launch count.)
+#ifndef C3_PAIR_MAXNREG
+#define C3_PAIR_MAXNREG 152
+#endif
+template <bool FUSED, int BN_>
+__global__ void __cluster_dims__(2, 1, 1) __maxnreg__(C3_PAIR_MAXNREG)
 gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
-                         const __grid_constant__ CUtensorMap map_b, const Params p) {
+                         const __grid_constant__ CUtensorMap map_b,
+                         const __grid_constant__ CUtensorMap map_c, const Params p) {
+    using Cfg = PairCfg<BN_>;
+    constexpr int BN = Cfg::BN, STAGES = Cfg::STAGES, ACC_BUFS = Cfg::ACC_BUFS;
+    constexpr uint32_t B_STAGE = Cfg::B_STAGE, STAGE = Cfg::STAGE;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = reinterpret_cast<uint8_t*>(
         (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~static_cast<uintptr_t>(1023));
@@ -215,7 +251,12 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     uint64_t* lbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [2] copy loads
     uint32_t* progress = reinterpret_cast<uint32_t*>(lbar + 2);   // producer k-blocks issued
     uint32_t* producer_done = progress + 1;
-    uint8_t* copy_buf = smem + STAGES * STAGE + 1024;
+    uint8_t* epi_stage = smem + STAGES * STAGE + 1024;
+#ifndef C3_EPI_BUFS
+#define C3_EPI_BUFS 2
+#endif
+    constexpr int EPI_BUFS = FUSED ? 1 : C3_EPI_BUFS;
+    uint8_t* copy_buf = epi_stage + EPI_BUFS * Cfg::EPI_SMEM;
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -225,17 +266,18 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_a);
         tma_prefetch_desc(&map_b);
+        tma_prefetch_desc(&map_c);
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
         }
         for (int b = 0; b < ACC_BUFS; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 8);
+            mbar_init(&acc_empty[b], 2 * Cfg::EPI_WARPS);
         }
         for (int r = 0; r < RING; ++r) {
             mbar_init(&tile_full[r], 1);
-            mbar_init(&tile_empty[r], 10);
+            mbar_init(&tile_empty[r], 2 + 2 * Cfg::EPI_WARPS);
         }
         if (FUSED) {
             mbar_init(&lbar[0], 1);
@@ -279,12 +321,15 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             int tm, tn;
             tile_coords(p, tile, tm, tn);
             const int a_row = tm * BM + static_cast<int>(rank) * 128;
-            const int b_row = tn * BN + static_cast<int>(rank) * 128;
+            const int b_row = tn * BN + static_cast<int>(rank) * 128;  // + 256 per half
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
                 tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, pol_a);
-                tma_load_2d_pair(smem_b + stage * B_STAGE, &map_b, &full[stage], kb * BK, b_row, pol_b);
+#pragma unroll
+                for (int h = 0; h < Cfg::HALVES; ++h)
+                    tma_load_2d_pair(smem_b + stage * B_STAGE + h * B_HALF, &map_b, &full[stage], kb * BK,
+                                     b_row + h * 256, pol_b);
                 if (FUSED) st_volatile_shared(progress, ld_volatile_shared(progress) + 1);
                 if (++stage == STAGES) {
                     stage = 0;
@@ -303,7 +348,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         }
     } else if (warp == 1 && lane == 0 && leader) {
         // ------------- MMA issuer (leader only) -------------
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, 256);
         const uint32_t a0 = smem_u32(smem_a), b0 = smem_u32(smem_b);
         int stage = 0;
         uint32_t phase = 0;
@@ -325,8 +370,11 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 const uint32_t b_addr = b0 + stage * B_STAGE;
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k)
-                    umma_bf16_pair(d_tmem, smem_desc_k_sw128(a_addr + k * UK * 2),
-                                   smem_desc_k_sw128(b_addr + k * UK * 2), idesc, (kb | k) != 0);
+#pragma unroll
+                    for (int h = 0; h < Cfg::HALVES; ++h)
+                        umma_bf16_pair(d_tmem + h * 256, smem_desc_k_sw128(a_addr + k * UK * 2),
+                                       smem_desc_k_sw128(b_addr + h * B_HALF + k * UK * 2), idesc,
+                                       (kb | k) != 0);
                 umma_commit_pair(&empty[stage], 0x3);
                 if (++stage == STAGES) {
                     stage = 0;
@@ -340,12 +388,14 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             }
         }
     } else if (warp >= 4) {
-        // ------------- epilogue (both CTAs): own 128 rows x 256 columns -------------
-        const int q = warp - 4;
-        const int row_in_tile = static_cast<int>(rank) * 128 + q * 32 + lane;
+        // ------------- epilogue (both CTAs): own 128 rows x BN columns -------------
+        const int q = warp % 4;  // TMEM lane quadrant this warp may access
+        constexpr int COLS = BN / (Cfg::EPI_WARPS / 4);
+        const int c_begin = (warp - 4) / 4 * COLS;
+        uint8_t* stg_base = epi_stage + (warp - 4) * EPI_BUFS * kEpiWarpStage;
+        int stg_i = 0;  // staging tile in use (ring of EPI_BUFS)
         int acc = 0;
         uint32_t acc_phase = 0;
-        const uint64_t pol_c = policy_by_kind(p.pol_c);
         for (int i = 0;; ++i) {
             const int r = i % RING;
             if (leader)
@@ -360,54 +410,76 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 else
                     mbar_arrive_cluster(mapa(smem_u32(&tile_empty[r]), 0));
             }
-            if (tile < 0) break;
+            if (tile < 0) {
+                if (lane == 0) bulk_wait_all();  // this warp's C stores complete
+                break;
+            }
             int tm, tn;
             tile_coords(p, tile, tm, tn);
             mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
-            const int row = tm * BM + row_in_tile;
-            const bool row_ok = row < p.m;
-            __nv_bfloat16* crow = p.c + static_cast<size_t>(row) * p.ldc;
+            // TMEM row `lane` of this warp's quadrant -> packed bf16 -> the
+            // warp's 32 x 64 staging tile in shared memory (16-byte chunks
+            // XOR-swizzled by row: the TMA 128B swizzle) -> one TMA tensor
+            // store per 64 columns (OOB rows/columns clipped by the map). The
+            // TMEM loads of chunk c+64 are issued before chunk c's store, and
+            // the accumulator is released right after the last TMEM load: with
+            // one 512-column accumulator the next tile's MMAs wait for this.
+            const int row0 = tm * BM + static_cast<int>(rank) * 128 + q * 32;  // warp's first row
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(t_row + c, v);
-                tmem_ld_wait();
-                const int col = tn * BN + c;
-                if (!row_ok) continue;
-                if (col + 32 <= p.n) {
-                    uint4* dst = reinterpret_cast<uint4*>(crow + col);
+            // chunk c in registers -> staging tile -> TMA store (lane 0)
+            auto stage_store = [&](const uint32_t (&a)[32], const uint32_t (&b)[32], int c) {
+                uint8_t* stg = stg_base + stg_i * kEpiWarpStage;
+                if (lane == 0) bulk_wait_read<EPI_BUFS - 1>();  // this tile's previous store has read it
+                __syncwarp();
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        uint4 o;
-                        __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
-                        __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-                        __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
-                        o.x = *reinterpret_cast<uint32_t*>(&h0);
-                        o.y = *reinterpret_cast<uint32_t*>(&h1);
-                        o.z = *reinterpret_cast<uint32_t*>(&h2);
-                        o.w = *reinterpret_cast<uint32_t*>(&h3);
-                        if (p.pol_c)
-                            st_stream_v4(dst + j, o, pol_c);
-                        else
-                            dst[j] = o;
-                    }
-                } else {
-#pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t* v = j < 4 ? a + 8 * j : b + 8 * (j - 4);
+                    uint4 o;
+                    o.x = pack_bf16x2(v[0], v[1]);
+                    o.y = pack_bf16x2(v[2], v[3]);
+                    o.z = pack_bf16x2(v[4], v[5]);
+                    o.w = pack_bf16x2(v[6], v[7]);
+                    st_shared_v4(stg + lane * 128 + ((j ^ (lane & 7)) << 4), o);
                 }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) {
-                if (leader)
-                    mbar_arrive(&acc_empty[acc]);
-                else
-                    mbar_arrive_cluster(mapa(smem_u32(&acc_empty[acc]), 0));
+                fence_proxy_async_shared();
+                __syncwarp();
+                if (lane == 0) {
+                    tma_store_2d(&map_c, stg, tn * BN + c, row0);
+                    bulk_commit();
+                }
+                if (++stg_i == EPI_BUFS) stg_i = 0;
+            };
+            // two register sets: the TMEM loads of chunk c+64 are in flight
+            // while chunk c is packed and stored; the accumulator is released
+            // right after the last TMEM load completes
+            uint32_t va0[32], va1[32], vb0[32], vb1[32];
+            tmem_ld_32x32b_x32(t_row + c_begin, va0);
+            tmem_ld_32x32b_x32(t_row + c_begin + 32, va1);
+#pragma unroll 1
+            for (int c = c_begin;; c += 128) {
+                tmem_ld_wait();  // chunk c
+                tmem_ld_32x32b_x32(t_row + c + 64, vb0);
+                tmem_ld_32x32b_x32(t_row + c + 96, vb1);
+                stage_store(va0, va1, c);
+                tmem_ld_wait();  // chunk c + 64
+                const bool last = c + 128 >= c_begin + COLS;
+                if (!last) {
+                    tmem_ld_32x32b_x32(t_row + c + 128, va0);
+                    tmem_ld_32x32b_x32(t_row + c + 160, va1);
+                } else {
+                    tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) {
+                        if (leader)
+                            mbar_arrive(&acc_empty[acc]);
+                        else
+                            mbar_arrive_cluster(mapa(smem_u32(&acc_empty[acc]), 0));
+                    }
+                }
+                stage_store(vb0, vb1, c + 64);
+                if (last) break;
             }
             if (++acc == ACC_BUFS) {
                 acc = 0;
@@ -450,20 +522,30 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 
 }  // namespace gemm2
 
-int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc) {
-    static bool attr_done[2] = {false, false};
-    const int f = fc != nullptr ? 1 : 0;
-    if (!attr_done[f]) {
-        const cudaError_t e =
-            f ? cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel<true>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(gemm2::SMEM_FUSED))
-              : cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel<false>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     static_cast<int>(gemm2::SMEM));
+namespace {
+
+template <bool FUSED, int BN>
+int launch_pair(const GemmPlan* plan, const gemm2::Params& p, int grid, cudaStream_t stream) {
+    using Cfg = gemm2::PairCfg<BN>;
+    constexpr uint32_t smem = FUSED ? Cfg::SMEM_FUSED : Cfg::SMEM;
+    static bool attr_done = false;
+    if (!attr_done) {
+        const cudaError_t e = cudaFuncSetAttribute(gemm2::gemm_bf16_tn_pair_kernel<FUSED, BN>,
+                                                   cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   static_cast<int>(smem));
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm pair)");
-        attr_done[f] = true;
+        attr_done = true;
     }
+    gemm2::gemm_bf16_tn_pair_kernel<FUSED, BN><<<grid, Cfg::THREADS, smem, stream>>>(
+        plan->map_a, plan->map_b128, plan->map_c, p);
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return set_cuda_error(e, "gemm pair launch");
+    return C3_OK;
+}
+
+}  // namespace
+
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc) {
     gemm2::Params p;
     p.m = static_cast<int>(plan->m);
     p.n = static_cast<int>(plan->n);
@@ -482,30 +564,25 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return v > 0 ? v : gemm2::GROUP_M_DEFAULT;
     }();
     p.group_m = band;
-    // L2 policies of the operand loads, "<a><b>" digits (C3_GEMM_POL env, dev A/B)
-    // and of the C stores ("<a><b><c>", c = 0 plain)
+    // L2 policies of the operand loads, "<a><b>" digits (C3_GEMM_POL env, dev A/B;
+    // profiles/r01_gemm_l2_policy_ab.txt)
     static const int pol = [] {
         const char* e = std::getenv("C3_GEMM_POL");
-        return e && e[0] && e[1] && e[2] ? (e[0] - '0') * 100 + (e[1] - '0') * 10 + (e[2] - '0') : 110;
+        return e && e[0] && e[1] ? (e[0] - '0') * 10 + (e[1] - '0') : 11;
     }();
-    p.pol_a = pol / 100;
-    p.pol_b = pol / 10 % 10;
-    p.pol_c = pol % 10;
+    p.pol_a = pol / 10;
+    p.pol_b = pol % 10;
+
+    const bool wide = plan->kind == GemmPlan::kPair512;
     if (fc) {
         if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
         p.fc = *fc;
         p.fc.link_cta_bpns = static_cast<float>(fc->link_bpns / grid);
         p.fc.piece = std::max<int64_t>(16, std::min<int64_t>(fc->piece, gemm2::PIECE)) / 16 * 16;
-        gemm2::gemm_bf16_tn_pair_kernel<true><<<grid, gemm2::THREADS, gemm2::SMEM_FUSED, stream>>>(
-            plan->map_a, plan->map_b128, p);
-    } else {
-        p.fc = FusedComm{};
-        gemm2::gemm_bf16_tn_pair_kernel<false><<<grid, gemm2::THREADS, gemm2::SMEM, stream>>>(
-            plan->map_a, plan->map_b128, p);
+        return wide ? launch_pair<true, 512>(plan, p, grid, stream) : launch_pair<true, 256>(plan, p, grid, stream);
     }
-    const cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return set_cuda_error(e, "gemm pair launch");
-    return C3_OK;
+    p.fc = FusedComm{};
+    return wide ? launch_pair<false, 512>(plan, p, grid, stream) : launch_pair<false, 256>(plan, p, grid, stream);
 }
 
 }  // namespace c3k

@@ -1099,7 +1099,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
                 if (m <= best_co * 1.01) {  // ascending c: the first within 1%
                     if (m < best) {
                         best = m;
-                        best_st = C3_C3_SP;
+                        best_st = C3_C3_BASE;
                         best_cores = c;
                     }
                     break;
@@ -1113,7 +1113,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
             alloc->cus_comm = best_cores;
             alloc->cus_idle = 0;
             alloc->backend = C3_BACKEND_CU;
-            alloc->comm_first = 1;
+            alloc->comm_first = 0;
             return C3_OK;
         }
         c3sim::EfficiencyParams eff;

@@ -86,12 +86,13 @@ def test_gemm_small_full(torch_mod, c3, M, N, K):
     w.close()
 
 
-@pytest.mark.parametrize("kernel", ["pair", "wide", "narrow"])
+@pytest.mark.parametrize("kernel", ["pair", "pair512", "wide", "narrow"])
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 768, 1024), (1000, 2056, 136),
-                                   (300, 520, 200)])
+                                   (300, 520, 200), (768, 1536, 512)])
 def test_gemm_kernel_variants_full(torch_mod, c3, monkeypatch, kernel, M, N, K):
-    """Each GEMM kernel variant (CTA-pair 256x256, single-CTA 128x256 and
-    128x128 tiles), forced, on full outputs including ragged M/N/K tails."""
+    """Each GEMM kernel variant (CTA-pair 256x256 and 256x512, single-CTA
+    128x256 and 128x128 tiles), forced, on full outputs including ragged M/N/K
+    tails."""
     monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
     torch = torch_mod
     w = c3.World()
@@ -331,10 +332,11 @@ def test_session_alltoall_all_strategies(torch_mod, c3, n):
 @pytest.mark.parametrize("collective", [0, 1], ids=["all-gather", "all-to-all"])
 @pytest.mark.parametrize("n", [2, 8])
 @pytest.mark.parametrize("pace,piece", [(0.0, 4096), (0.8, 16384), (0.0, 0)])
-def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace, piece):
+@pytest.mark.parametrize("kernel", ["pair", "pair512"])
+def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace, piece, kernel):
     """C3_FUSED: the collective moved inside the CTA-pair GEMM by its copy warp
     (TMA bulk copies). Every virtual rank's output bit-exact; GEMM in tolerance."""
-    monkeypatch.setenv("C3_GEMM_KERNEL", "pair")
+    monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
     w = c3.World(0, n, 0, loopback=True)
     M, N, K = 512, 1024, 512
     payload = n * ((3 << 16) + 48)  # slots not a multiple of the 16 KiB piece

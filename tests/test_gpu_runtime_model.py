@@ -39,7 +39,7 @@ def test_choose_picks_coresident_from_the_curve(c3, session):
     # link-bound collective: 1.0 ms from 24 CTAs on, slower below
     s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
     st, a, pred = s.choose(3.0, 1.0, 0.0, allow_dma=False)
-    assert st == c3.C3_SP and a.cus_gemm == sms and a.cus_comm == 24 and a.comm_first == 1
+    assert st == c3.C3_BASE and a.cus_gemm == sms and a.cus_comm == 24 and a.comm_first == 0
     p = c3sim.load_coresident_params(CORES)
     want = c3sim.simulate_coresident(3.0e-3, 1.0e-3, 1.0e-3, sms, 24,
                                      c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
@@ -49,11 +49,11 @@ def test_choose_picks_coresident_from_the_curve(c3, session):
     a.cus_comm = 16
     want16 = c3sim.simulate_coresident(3.0e-3, 2.0e-3, 1.0e-3, sms, 16,
                                        c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
-    assert s.predict_alloc(c3.C3_SP, a, 3.0, 1.0) == pytest.approx(want16)
+    assert s.predict_alloc(c3.C3_BASE, a, 3.0, 1.0) == pytest.approx(want16)
     # a plateau: 32 CTAs a hair faster than 24 -> still the fewest within 1%
     s.set_comm_curve([(8, 4.0), (24, 1.004), (32, 1.0), (sms, 1.0)])
     st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
-    assert st == c3.C3_SP and a.cus_comm == 24
+    assert st == c3.C3_BASE and a.cus_comm == 24
 
 
 def test_partitioned_allocations_keep_the_reference_model(c3, session):

@@ -25,7 +25,7 @@ def main():
     by_class = {"cb": [], "mb": []}
     for path in ins:
         for r in csv.DictReader(open(path)):
-            if "coresident" not in r["strategy"]:
+            if not r["strategy"].startswith("c3_base_coresident"):  # the runtime's co-resident mode
                 continue
             tg = float(r["t_gemm_iso_ms"])
             tc = float(r.get("t_comm_ctas_ms") or "nan")
