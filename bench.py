@@ -94,32 +94,43 @@ class ClockSampler:
         self.lines = []
 
     def start(self):
+        """Start polling (every 20 ms) and wait for the first sample, so the
+        short timed region that follows is covered."""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "20"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            deadline = time.perf_counter() + 10.0
+            while not self.lines and time.perf_counter() < deadline and self.proc.poll() is None:
+                time.sleep(0.01)
         except Exception:
             self.proc = None
 
     def _read(self):
         for line in self.proc.stdout:
-            self.lines.append(line.strip())
+            self.lines.append((time.perf_counter(), line.strip()))
 
-    def stop(self):
+    def stop(self, t0=None, t1=None):
+        """Samples taken inside [t0, t1] (perf_counter; the timed region), or
+        the three nearest to it when the region is shorter than the period."""
         if not self.proc:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
+        time.sleep(0.1)
         self.proc.terminate()
         try:
             self.proc.wait(timeout=2)
         except Exception:
             self.proc.kill()
+        lines = self.lines
+        if t0 is not None and t1 is not None and lines:
+            inside = [x for x in lines if t0 <= x[0] <= t1 + 0.03]
+            lines = inside if inside else sorted(lines, key=lambda x: abs(x[0] - (t0 + t1) / 2))[:3]
         sms, maxs, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -375,15 +386,20 @@ def run_ours(args, dist):
     clocks = ClockSampler(device) if dist.rank == 0 else None
     if clocks:
         clocks.start()
+    dist.barrier()
+    for _ in range(2):  # the sampler's start-up took wall time: re-warm the step (all ranks)
+        sess.run(head, head_alloc)
     torch.cuda.synchronize()
+    dist.barrier()
     t0 = time.perf_counter()
     jobs = {"gemm": head_iso["gemm"], comm_key: head_iso[comm_key], "step": (head, head_alloc, link)}
     timed_rows = rounds(jobs, K)
     log("timed region done")
     torch.cuda.synchronize()
     dist.barrier()
-    wall = time.perf_counter() - t0
-    clk = clocks.stop() if clocks else None
+    t1 = time.perf_counter()
+    wall = t1 - t0
+    clk = clocks.stop(t0, t1) if clocks else None
 
     # ---- comparison block (after the timed region, not part of ms_per_step):
     # the full-speed loopback pair and the library baseline, interleaved with

@@ -41,8 +41,11 @@ struct CommCurve {
 
 void validate(const CommCurve& c);
 
-/// Co-residency penalties: residual slowdown of each kernel while both are
-/// resident on the same SMs (1.0 = no interference).
+/// Co-residency penalties (1.0 = no interference): the GEMM's residual
+/// slowdown while a collective runs beside it, and the collective CTA's cost
+/// factor: a CTA sharing its SM with the GEMM moves data like 1/comm isolated
+/// CTAs, so the collective on c co-resident CTAs takes t_comm(c / comm)
+/// (coresident_comm_ctas).
 struct CoResidentParams {
     double gemm_compute_bound = 1.0;
     double gemm_memory_bound = 1.0;
@@ -59,10 +62,14 @@ void validate(const CoResidentParams& p);
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 
+/// Isolated-equivalent CTA count of `cus_comm` co-resident collective CTAs.
+int coresident_comm_ctas(int cus_comm, const CoResidentParams& p);
+
 /// Two-phase fluid prediction of a co-resident run: GEMM on all CUs
-/// (t_gemm seconds alone), collective on cus_comm CTAs (t_comm_at_ctas
-/// seconds alone at that CTA count). serial_time / ideal use t_comm_full,
-/// the collective's isolated time on the whole GPU (the paper's t_comm).
+/// (t_gemm seconds alone), collective on cus_comm CTAs (t_comm_at_ctas =
+/// the isolated collective's time on coresident_comm_ctas(cus_comm) CTAs).
+/// serial_time / ideal use t_comm_full, the collective's isolated time on the
+/// whole GPU (the paper's t_comm).
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
                                 int cus_comm, KernelClass gemm_class, const CoResidentParams& p);
 

@@ -966,7 +966,8 @@ double comm_ms_at(const c3_session* s, int ctas, double t_comm_cu_ms) {
 // SMs, the SM collective on `ctas` CTAs beside it.
 double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, double t_comm_cu_ms) {
     const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
-    return c3sim::simulate_coresident(t_gemm_ms * 1e-3, comm_ms_at(s, ctas, t_comm_cu_ms) * 1e-3,
+    const int eff = c3sim::coresident_comm_ctas(ctas, s->cores);
+    return c3sim::simulate_coresident(t_gemm_ms * 1e-3, comm_ms_at(s, eff, t_comm_cu_ms) * 1e-3,
                                       t_comm_cu_ms * 1e-3, s->md.cus_per_gpu, ctas, gcls, s->cores)
         .makespan;
 }

@@ -83,6 +83,11 @@ std::string save_coresident_params(const CoResidentParams& p) {
     return j.dump(2) + "\n";
 }
 
+int coresident_comm_ctas(int cus_comm, const CoResidentParams& p) {
+    validate(p);
+    return std::max(1, static_cast<int>(std::lround(cus_comm / p.comm)));
+}
+
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
                                 int cus_comm, KernelClass gemm_class, const CoResidentParams& p) {
     validate(p);
@@ -95,7 +100,7 @@ SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_c
     tl.work_comm = t_comm_full;
     // phase 1: both resident; rates in units of each kernel's isolated work
     const double rg = 1.0 / p.gemm(gemm_class);
-    const double rc = (t_comm_full / t_comm_at_ctas) / p.comm;
+    const double rc = t_comm_full / t_comm_at_ctas;
     const double end_g = t_gemm / rg, end_c = t_comm_full / rc;
     const double t1 = std::min(end_g, end_c);
     tl.phases.push_back({0.0, t1, rg, rc, cus, cus_comm});

@@ -236,6 +236,7 @@ void add_sim(py::module_& m) {
     m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),
           py::arg("t_comm_full"), py::arg("cus"), py::arg("cus_comm"), py::arg("gemm_class"), py::arg("params"));
     m.def("fit_coresident_gemm_penalty", &cs::fit_coresident_gemm_penalty);
+    m.def("coresident_comm_ctas", &cs::coresident_comm_ctas);
 
     using SR = cs::SweepRow;
     using AR = cs::AggregateRow;

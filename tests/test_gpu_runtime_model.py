@@ -31,16 +31,28 @@ def session(c3):
     w.close()
 
 
-def test_choose_picks_coresident_from_the_curve(c3, session):
+@pytest.fixture()
+def cores_unit_comm(tmp_path):
+    """Co-resident params with the collective CTA cost factor 1 (the shipped
+    file's fitted factor moves the pick; this test pins the arithmetic)."""
+    import c3sim
+    p = c3sim.load_coresident_params(CORES)
+    p.comm = 1.0
+    f = tmp_path / "cores.json"
+    f.write_text(c3sim.save_coresident_params(p))
+    return str(f)
+
+
+def test_choose_picks_coresident_from_the_curve(c3, session, cores_unit_comm):
     import c3sim
     w, s = session
     sms = w.info.sm_count
-    s.load_coresident(CORES)
+    s.load_coresident(cores_unit_comm)
     # link-bound collective: 1.0 ms from 24 CTAs on, slower below
     s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
     st, a, pred = s.choose(3.0, 1.0, 0.0, allow_dma=False)
     assert st == c3.C3_BASE and a.cus_gemm == sms and a.cus_comm == 24 and a.comm_first == 0
-    p = c3sim.load_coresident_params(CORES)
+    p = c3sim.load_coresident_params(cores_unit_comm)
     want = c3sim.simulate_coresident(3.0e-3, 1.0e-3, 1.0e-3, sms, 24,
                                      c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
     assert pred == pytest.approx(want)
@@ -54,6 +66,21 @@ def test_choose_picks_coresident_from_the_curve(c3, session):
     s.set_comm_curve([(8, 4.0), (24, 1.004), (32, 1.0), (sms, 1.0)])
     st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
     assert st == c3.C3_BASE and a.cus_comm == 24
+
+
+def test_collective_cta_cost_factor_moves_the_pick(c3, session):
+    """With the fitted cost factor p_c, c co-resident CTAs act like c / p_c
+    isolated ones: the pick is the fewest candidate CTAs reaching the plateau."""
+    import c3sim
+    w, s = session
+    sms = w.info.sm_count
+    s.load_coresident(CORES)
+    pc = c3sim.load_coresident_params(CORES).comm
+    s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
+    st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
+    cands = sorted({8, 16, 24, 32, 48, 64})
+    assert st == c3.C3_BASE
+    assert a.cus_comm == next(c for c in cands if round(c / pc) >= 24)
 
 
 def test_partitioned_allocations_keep_the_reference_model(c3, session):

@@ -1,54 +1,95 @@
-"""Fit the B200 co-residency penalties (include/c3sim/coresident.hpp) from a
-measured sweep CSV (tools/c3_sweep.py): for every co-resident row (GEMM on
-every SM, collective CTAs beside it) where the collective finished inside the
-GEMM, solve the model for the GEMM penalty p_g (c3sim.fit_coresident_gemm_penalty,
-p_c = 1) from the isolated GEMM time, the collective's isolated time at that
-CTA count (column t_comm_ctas_ms when present, else rows whose CTA count
-reaches the full-GPU collective time) and the measured makespan; the median
-per GEMM class is written as the params JSON.
+"""Fit the B200 co-residency parameters (include/c3sim/coresident.hpp) from
+measured sweep CSVs (tools/c3_sweep.py, which carries t_comm_ctas_ms: the
+isolated collective on each CTA count).
+
+The runtime's co-resident mode is c3_base with the GEMM on every SM and c
+collective CTAs beside it. Its model has two parameters:
+  p_g  the GEMM's slowdown while the collective runs beside it;
+  p_c  the collective CTA's cost factor: c co-resident CTAs move data like
+       c / p_c isolated CTAs (t_comm = curve(c / p_c)).
+Per scenario the curve is the measured (CTAs, time) points plus the
+full-GPU time; (p_g, p_c) minimise the mean squared relative error of
+c3sim.simulate_coresident against every c3_base_coresident row (grid search).
+Memory-bound GEMM scenarios (cfg4_mb) fit their own p_g.
 
 usage: python tools/calibrate_coresident.py SWEEP.csv [SWEEP2.csv ...] OUT.json"""
 import csv
 import os
-import statistics
 import sys
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, os.path.join(REPO, "paper_2412_14335_b200", "python"))
 import c3sim  # noqa: E402
 
+CB, MB = c3sim.KernelClass.GEMM_COMPUTE_BOUND, c3sim.KernelClass.GEMM_MEMORY_BOUND
+SMS = 148
+
+
+def load(paths):
+    """-> {(path, scenario, collective): {"tg", "tc", "curve", "rows": [(c, makespan)]}}"""
+    scen = {}
+    for path in paths:
+        for r in csv.DictReader(open(path)):
+            if not r["strategy"].startswith("c3_base_coresident") or not r.get("t_comm_ctas_ms"):
+                continue
+            key = (path, r["scenario_id"], r["collective"])
+            d = scen.setdefault(key, {"tg": float(r["t_gemm_iso_ms"]) * 1e-3,
+                                      "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": []})
+            c = int(r["cus_comm"])
+            d["pts"][c] = float(r["t_comm_ctas_ms"]) * 1e-3
+            d["rows"].append((c, float(r["makespan_s"])))
+    for d in scen.values():
+        pts = dict(d["pts"])
+        pts[SMS] = min(d["tc"], min(pts.values()))
+        cs = sorted(pts)
+        d["curve"] = c3sim.CommCurve(cs, [pts[c] for c in cs])
+    return scen
+
+
+def error(scen, cls_of, pg, pc):
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound = p.gemm_memory_bound = pg
+    p.comm = pc
+    err, n = 0.0, 0
+    for key, d in scen.items():
+        cls = cls_of(key)
+        for c, mk in d["rows"]:
+            t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p))
+            pred = c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls, p).makespan
+            err += ((pred - mk) / mk) ** 2
+            n += 1
+    return err / max(n, 1), n
+
+
+def fit(scen, cls_of):
+    best = None
+    for pc in [1.0 + 0.05 * i for i in range(41)]:        # 1.0 .. 3.0
+        for pg in [1.0 + 0.01 * i for i in range(61)]:    # 1.0 .. 1.6
+            e, n = error(scen, cls_of, pg, pc)
+            if best is None or e < best[0]:
+                best = (e, pg, pc, n)
+    return best
+
 
 def main():
     *ins, out = sys.argv[1:]
-    fits = {"C-long": [], "G-long": [], "GC-equal": []}
-    mb = {"cfg4_mb"}  # memory-bound GEMM scenarios (AI < machine op:byte)
-    by_class = {"cb": [], "mb": []}
-    for path in ins:
-        for r in csv.DictReader(open(path)):
-            if not r["strategy"].startswith("c3_base_coresident"):  # the runtime's co-resident mode
-                continue
-            tg = float(r["t_gemm_iso_ms"])
-            tc = float(r.get("t_comm_ctas_ms") or "nan")
-            if tc != tc:  # no per-CTA column: only CTA counts at the full-GPU collective time
-                if int(r["cus_comm"]) < 32:
-                    continue
-                tc = float(r["t_comm_iso_ms"])
-            mk = float(r["makespan_s"]) * 1e3
-            if tc >= tg:  # the collective outlived the GEMM: p_g is not identifiable
-                continue
-            p = c3sim.fit_coresident_gemm_penalty(tg * 1e-3, tc * 1e-3, mk * 1e-3)
-            cls = "mb" if any(r["scenario_id"].startswith(x) for x in mb) else "cb"
-            by_class[cls].append(p)
-            fits[r["taxonomy"]].append(p)
-            print(f"{r['scenario_id']:16s} {r['collective']:15s} {r['strategy']:22s} p_g={p:.3f}")
+    scen = load(ins)
+    is_mb = lambda key: key[1].startswith("cfg4_mb")  # noqa: E731  M=128: memory-bound GEMM
+    cb = {k: v for k, v in scen.items() if not is_mb(k)}
+    mb = {k: v for k, v in scen.items() if is_mb(k)}
+    e_cb, pg_cb, pc, n_cb = fit(cb, lambda k: CB)
+    # memory-bound: p_c shared (a property of the collective CTA), p_g refit
+    best_mb = min(((error(mb, lambda k: MB, pg, pc)[0], pg)
+                   for pg in [1.0 + 0.01 * i for i in range(61)]), default=(0.0, pg_cb))
     prm = c3sim.CoResidentParams()
-    prm.gemm_compute_bound = statistics.median(by_class["cb"]) if by_class["cb"] else 1.0
-    prm.gemm_memory_bound = statistics.median(by_class["mb"]) if by_class["mb"] else prm.gemm_compute_bound
-    prm.comm = 1.0
+    prm.gemm_compute_bound, prm.comm = pg_cb, pc
+    prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     with open(out, "w") as f:
         f.write(c3sim.save_coresident_params(prm))
-    print(f"fitted: compute-bound {prm.gemm_compute_bound:.3f} ({len(by_class['cb'])} rows), "
-          f"memory-bound {prm.gemm_memory_bound:.3f} ({len(by_class['mb'])} rows) -> {out}")
+    print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc:.2f}, rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows)")
+    if mb:
+        print(f"memory-bound:  p_g {best_mb[1]:.2f}, rms rel. error {best_mb[0] ** 0.5:.3f}")
+    print(f"-> {out}")
 
 
 if __name__ == "__main__":
