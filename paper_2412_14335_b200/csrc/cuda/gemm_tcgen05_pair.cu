@@ -16,6 +16,7 @@
 //   empty[s]    both CTAs; the leader's tcgen05.commit multicasts to both
 //   acc_full[b] both CTAs; multicast commit after a tile's last k-block
 //   acc_empty[b] leader; EPI_WARPS local + EPI_WARPS remote epilogue-warp arrivals
+//               (BN 512: one barrier per 256-column half of the accumulator)
 //   tile ring   leader claims tiles (global atomic, one tile ahead), writes
 //               the id into both CTAs' rings (st.shared::cluster) and arrives
 //               on both tile_full; consumers of both CTAs release the slot on
@@ -44,6 +45,7 @@ constexpr int THREADS = 256;  // 256-wide tiles: warps 0-3 roles, 4-7 epilogue
 // band's A slice must stay well under the nominal 126 MB.
 constexpr int GROUP_M_DEFAULT = 8;
 constexpr int RING = 4;
+constexpr int kPreHalf = 2;  // BN 512: k-blocks issued into half 0 before half 1 is free
 constexpr uint32_t A_STAGE = 128 * BK * 2;  // this CTA's 128 rows of A
 constexpr uint32_t B_HALF = 128 * BK * 2;   // this CTA's 128 rows of one 256-column half of B
 constexpr uint32_t TMEM_COLS = 512;
@@ -242,8 +244,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     uint64_t* full = bars;
     uint64_t* empty = bars + STAGES;
     uint64_t* acc_full = bars + 2 * STAGES;
-    uint64_t* acc_empty = acc_full + ACC_BUFS;
-    uint64_t* tile_full = acc_empty + ACC_BUFS;
+    uint64_t* acc_empty = acc_full + ACC_BUFS;  // [2]: per accumulator (BN 256) / per 256-column half (BN 512)
+    uint64_t* tile_full = acc_empty + 2;
     uint64_t* tile_empty = tile_full + RING;
     int* tile_ring = reinterpret_cast<int*>(tile_empty + RING);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + RING);
@@ -273,8 +275,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         }
         for (int b = 0; b < ACC_BUFS; ++b) {
             mbar_init(&acc_full[b], 1);
-            mbar_init(&acc_empty[b], 2 * Cfg::EPI_WARPS);
         }
+        for (int b = 0; b < 2; ++b) mbar_init(&acc_empty[b], 2 * Cfg::EPI_WARPS);
         for (int r = 0; r < RING; ++r) {
             mbar_init(&tile_full[r], 1);
             mbar_init(&tile_empty[r], 2 + 2 * Cfg::EPI_WARPS);
@@ -360,10 +362,50 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int tile = tile_ring[r];
             mbar_arrive(&tile_empty[r]);
             if (tile < 0) break;
-            mbar_wait(&acc_empty[acc], acc_phase ^ 1);
-            tc_fence_after();
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-            for (int kb = 0; kb < p.k_blocks; ++kb) {
+            int kb0 = 0;
+            if constexpr (Cfg::HALVES == 2) {
+                // One 512-column accumulator, released by the epilogue in
+                // 256-column halves: the first PRE k-blocks of the new tile
+                // accumulate into half 0 while half 1 is still being drained.
+                const int pre = p.k_blocks < kPreHalf ? p.k_blocks : kPreHalf;
+                mbar_wait(&acc_empty[0], acc_phase ^ 1);
+                tc_fence_after();
+                int st = stage;
+                uint32_t ph = phase;
+                for (int kb = 0; kb < pre; ++kb) {
+                    mbar_wait(&full[st], ph);
+                    tc_fence_after();
+                    const uint32_t a_addr = a0 + st * A_STAGE, b_addr = b0 + st * B_STAGE;
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k)
+                        umma_bf16_pair(d_tmem, smem_desc_k_sw128(a_addr + k * UK * 2),
+                                       smem_desc_k_sw128(b_addr + k * UK * 2), idesc, (kb | k) != 0);
+                    if (++st == STAGES) {
+                        st = 0;
+                        ph ^= 1;
+                    }
+                }
+                mbar_wait(&acc_empty[1], acc_phase ^ 1);
+                tc_fence_after();
+                for (int kb = 0; kb < pre; ++kb) {  // the same stages, half 1, then release them
+                    const uint32_t a_addr = a0 + stage * A_STAGE, b_addr = b0 + stage * B_STAGE;
+#pragma unroll
+                    for (int k = 0; k < BK / UK; ++k)
+                        umma_bf16_pair(d_tmem + 256, smem_desc_k_sw128(a_addr + k * UK * 2),
+                                       smem_desc_k_sw128(b_addr + B_HALF + k * UK * 2), idesc, (kb | k) != 0);
+                    umma_commit_pair(&empty[stage], 0x3);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                kb0 = pre;
+            } else {
+                mbar_wait(&acc_empty[acc], acc_phase ^ 1);
+                tc_fence_after();
+            }
+            for (int kb = kb0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 const uint32_t a_addr = a0 + stage * A_STAGE;
@@ -464,6 +506,18 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 tmem_ld_32x32b_x32(t_row + c + 96, vb1);
                 stage_store(va0, va1, c);
                 tmem_ld_wait();  // chunk c + 64
+                if constexpr (Cfg::HALVES == 2) {
+                    if (c + 64 == 192) {  // columns 0-255 read: release half 0
+                        tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) {
+                            if (leader)
+                                mbar_arrive(&acc_empty[0]);
+                            else
+                                mbar_arrive_cluster(mapa(smem_u32(&acc_empty[0]), 0));
+                        }
+                    }
+                }
                 const bool last = c + 128 >= c_begin + COLS;
                 if (!last) {
                     tmem_ld_32x32b_x32(t_row + c + 128, va0);
@@ -471,11 +525,12 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 } else {
                     tc_fence_before();
                     __syncwarp();
+                    const int rel = Cfg::HALVES == 2 ? 1 : acc;  // the last half / this accumulator
                     if (lane == 0) {
                         if (leader)
-                            mbar_arrive(&acc_empty[acc]);
+                            mbar_arrive(&acc_empty[rel]);
                         else
-                            mbar_arrive_cluster(mapa(smem_u32(&acc_empty[acc]), 0));
+                            mbar_arrive_cluster(mapa(smem_u32(&acc_empty[rel]), 0));
                     }
                 }
                 stage_store(vb0, vb1, c + 64);
