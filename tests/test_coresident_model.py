@@ -102,3 +102,34 @@ def test_params_roundtrip_and_validation(tmp_path):
 def test_shipped_coresident_params_load():
     q = c3sim.load_coresident_params(c3sim.data_path("b200-coresident.json"))
     assert 1.0 <= q.gemm_compute_bound < 2.0 and 1.0 <= q.gemm_memory_bound and not math.isnan(q.comm)
+
+
+def test_calibration_tool_recovers_known_parameters(tmp_path):
+    """tools/calibrate_coresident.py on a sweep CSV synthesised from the model
+    with known (p_g, p_c) recovers them (grid resolution 0.01 / 0.05)."""
+    import json
+    import subprocess
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound, p.gemm_memory_bound, p.comm = 1.12, 1.12, 1.5
+    hdr = ("scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
+           "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
+           "predicted_makespan_s,t_comm_ctas_ms")
+    rows = [hdr]
+    for sid, tg, tc in (("cfgA_1M", 2.4e-3, 1.1e-3), ("cfgB_1M", 9.0e-3, 2.0e-3), ("cfgC_1M", 2.5e-3, 0.6e-3)):
+        # a link-bound collective: 1/ctas below 24 CTA units, flat from there
+        pts = {c: tc * max(1.0, 24.0 / c) for c in (8, 12, 16, 24, 32, 48, 64)}
+        curve = c3sim.CommCurve(sorted(pts) + [148], [pts[c] for c in sorted(pts)] + [tc])
+        for c in (16, 24, 32, 48, 64):
+            t_at = curve.time_at(c3sim.coresident_comm_ctas(c, p))
+            mk = c3sim.simulate_coresident(tg, t_at, tc, 148, c, CB, p).makespan
+            rows.append(f"{sid},all-gather,G-long,c3_base_coresident{c},{mk},1,1,0,{tg * 1e3},{tc * 1e3},"
+                        f"0,148,{c},CU,synthetic,nan,{pts[c] * 1e3}")
+    src = tmp_path / "sweep.csv"
+    src.write_text("\n".join(rows) + "\n")
+    out = tmp_path / "cores.json"
+    r = subprocess.run([sys.executable, os.path.join(REPO, "tools", "calibrate_coresident.py"), str(src),
+                        str(out)], capture_output=True, text=True, timeout=300)
+    assert r.returncode == 0, r.stderr
+    got = json.loads(out.read_text())
+    assert got["gemm-compute-bound"] == pytest.approx(1.12, abs=0.011)
+    assert got["comm"] == pytest.approx(1.5, abs=0.051)
