@@ -45,7 +45,7 @@ constexpr int THREADS = 256;  // 256-wide tiles: warps 0-3 roles, 4-7 epilogue
 // band's A slice must stay well under the nominal 126 MB.
 constexpr int GROUP_M_DEFAULT = 8;
 constexpr int RING = 4;
-constexpr int kPreHalf = 2;  // BN 512: k-blocks issued into half 0 before half 1 is free
+constexpr int kPreHalf = 4;  // BN 512: k-blocks issued into half 0 before half 1 is free (C3_GEMM_PREHALF; measured 1-4: 92.2 -> 93.1% tensor pipe)
 constexpr uint32_t A_STAGE = 128 * BK * 2;  // this CTA's 128 rows of A
 constexpr uint32_t B_HALF = 128 * BK * 2;   // this CTA's 128 rows of one 256-column half of B
 constexpr uint32_t TMEM_COLS = 512;
@@ -91,6 +91,7 @@ struct Params {
     int* exit_counter;
     int group_m;
     int pol_a, pol_b;  // L2 policy of the A / B operand loads (policy_by_kind)
+    int pre_half;      // BN 512: k-blocks into half 0 before waiting for half 1 (<= STAGES)
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -368,7 +369,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 // One 512-column accumulator, released by the epilogue in
                 // 256-column halves: the first PRE k-blocks of the new tile
                 // accumulate into half 0 while half 1 is still being drained.
-                const int pre = p.k_blocks < kPreHalf ? p.k_blocks : kPreHalf;
+                const int pre = p.k_blocks < p.pre_half ? p.k_blocks : p.pre_half;
                 mbar_wait(&acc_empty[0], acc_phase ^ 1);
                 tc_fence_after();
                 int st = stage;
@@ -627,6 +628,12 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
     }();
     p.pol_a = pol / 10;
     p.pol_b = pol % 10;
+    static const int pre_half = [] {
+        const char* e = std::getenv("C3_GEMM_PREHALF");  // dev A/B
+        const int v = e ? std::atoi(e) : gemm2::kPreHalf;
+        return v < 1 ? 1 : v > gemm2::PairCfg<512>::STAGES ? gemm2::PairCfg<512>::STAGES : v;
+    }();
+    p.pre_half = pre_half;
 
     const bool wide = plan->kind == GemmPlan::kPair512;
     if (fc) {
