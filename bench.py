@@ -271,7 +271,7 @@ def run_ours(args, dist):
                         best_iso)
         if st == c3.FUSED:
             res["note"] = ("collective moved inside the CTA-pair GEMM kernel by its copy warp "
-                           "(TMA bulk copies, 4 KiB pieces); t_comm_iso = SM collective")
+                           "(TMA bulk copies, 8 KiB pieces); t_comm_iso = SM collective")
         res["alloc"] = {"cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm, "cus_idle": a.cus_idle,
                         "backend": ["CU", "DMA", "TMA"][a.backend]}
         if a.backend == c3.BACKEND_DMA and loopback:

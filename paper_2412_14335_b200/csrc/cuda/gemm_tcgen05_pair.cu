@@ -106,16 +106,21 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
 
 // Fused C3 copy engine (warp 3, one thread, FUSED only): this rank's share of
 // the collective moved by the SM's own TMA unit with bulk async copies —
-// global -> 16 KiB shared buffer -> every destination (local or NVLink peer) —
-// double-buffered, and paced so item k of this CTA's n items starts once the
-// CTA's producer has issued k/n * pace of its expected k-blocks. Work items
-// are spread round-robin over the grid. AG: item = (rank v, piece j), one load,
+// global -> shared ring -> every destination (local or NVLink peer). The
+// 2 x PIECE bytes of copy buffer are cut into nb = 2 x PIECE / piece slots
+// (<= kFusedSlots), and loads run nb-1 items ahead of the stores, so an
+// all-to-all (one store per load) is not bound by one load round trip per
+// piece. Item k of this CTA's `mine` items starts once the CTA's producer has
+// issued k/mine * pace of its expected k-blocks (pace > 0). Work items are
+// spread round-robin over the grid. AG: item = (rank v, piece j), one load,
 // n-1 stores; A2A: item = (v, dest q, piece j), one load, one store.
+constexpr int kFusedSlots = 8;
 __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
                                 const uint32_t* progress, const volatile uint32_t* producer_done) {
     const FusedComm& fc = p.fc;
     const uint64_t pol = policy_evict_first();
-    const int64_t piece = fc.piece;  // <= PIECE (the buffer size)
+    const int64_t piece = fc.piece;  // <= PIECE
+    const int nb = static_cast<int>(min(static_cast<int64_t>(kFusedSlots), 2 * PIECE / piece));
     const int64_t pieces = (fc.chunk + piece - 1) / piece;
     const int nv = fc.self_end - fc.self_begin;
     const int64_t per_v = fc.kind == 0 ? pieces : pieces * fc.n;
@@ -124,40 +129,81 @@ __device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
     const int64_t mine = total > blockIdx.x ? (total - blockIdx.x + G - 1) / G : 0;
     // expected producer k-blocks of this CTA over the GEMM (pair tiles / pairs)
     const double est_kb = static_cast<double>((p.num_tiles + G / 2 - 1) / (G / 2)) * p.k_blocks;
+    const int targets = fc.kind == 0 ? (fc.skip_self ? fc.n - 1 : fc.n) : 1;
+    struct Item {
+        int v, q;
+        int64_t off;
+        uint32_t len;
+    };
+    // item k -> (rank, destination, offset): 32-bit division (item counts stay
+    // far below 2^31; a 64-bit division per item was the copy thread's
+    // bottleneck for all-to-all, which has n x the items of an all-gather)
+    const bool small = total < (int64_t{1} << 31);
+    auto item = [&](int64_t k) {
+        const int64_t w = blockIdx.x + k * G;
+        Item it;
+        int64_t r, jj;
+        if (small) {
+            const uint32_t w32 = static_cast<uint32_t>(w), pv = static_cast<uint32_t>(per_v);
+            const uint32_t pc = static_cast<uint32_t>(pieces);
+            it.v = fc.self_begin + static_cast<int>(w32 / pv);
+            const uint32_t r32 = w32 % pv;
+            it.q = fc.kind == 0 ? -1 : static_cast<int>(r32 / pc);
+            r = r32;
+            jj = fc.kind == 0 ? r32 : r32 % pc;
+        } else {
+            it.v = fc.self_begin + static_cast<int>(w / per_v);
+            r = w % per_v;
+            it.q = fc.kind == 0 ? -1 : static_cast<int>(r / pieces);
+            jj = fc.kind == 0 ? r : r % pieces;
+        }
+        it.off = jj * piece;
+        const int64_t left = fc.chunk - it.off;
+        it.len = static_cast<uint32_t>(left < piece ? left : piece);
+        return it;
+    };
+    Item slot[kFusedSlots];  // the item in flight in each buffer slot
+    auto issue_load = [&](int64_t k, int b) {
+        const Item it = item(k);
+        slot[b] = it;
+        const uint8_t* src = fc.src[it.v] + (fc.kind == 0 ? 0 : static_cast<int64_t>(it.q) * fc.chunk) + it.off;
+        mbar_arrive_expect_tx(&lbar[b], it.len);
+        bulk_load(buf + b * piece, src, it.len, &lbar[b], pol);
+    };
+    for (int64_t k = 0; k < nb - 1 && k < mine; ++k) issue_load(k, static_cast<int>(k));
     const uint64_t t0 = global_ns();
     double sent = 0.0;  // peer bytes stored (link emulation)
-    const int targets = fc.kind == 0 ? (fc.skip_self ? fc.n - 1 : fc.n) : 1;
-    int64_t k = 0;
-    for (int64_t w = blockIdx.x; w < total; w += G, ++k) {
-        const int b = static_cast<int>(k & 1);
-        if (k >= 2) bulk_wait_read<1>();  // buffer b's stores (group k-2) done reading
-        if (fc.pace > 0.f && mine > 0) {
+    int b = 0, refill = nb - 1;  // slot of item k, slot of item k + nb - 1
+    uint32_t par = 0;            // mbarrier parity of slot b's current use
+    for (int64_t k = 0; k < mine; ++k) {
+        const Item it = slot[b];
+        if (fc.pace > 0.f) {
             const uint32_t target = static_cast<uint32_t>(est_kb * fc.pace * k / mine);
             while (ld_volatile_shared(progress) < target && !*producer_done) __nanosleep(256);
         }
         if (fc.link_cta_bpns > 0.f) link_wait(t0, sent, fc.link_cta_bpns);
-        const int v = fc.self_begin + static_cast<int>(w / per_v);
-        const int64_t r = w % per_v;
-        const int q = fc.kind == 0 ? -1 : static_cast<int>(r / pieces);
-        const int64_t j = fc.kind == 0 ? r : r % pieces;
-        const int64_t off = j * piece;
-        const int64_t left = fc.chunk - off;
-        const uint32_t len = static_cast<uint32_t>(left < piece ? left : piece);
-        sent += static_cast<double>(len) * (fc.kind == 0 ? targets : (q == v ? 0 : 1));
-        const uint8_t* src = fc.src[v] + (fc.kind == 0 ? 0 : static_cast<int64_t>(q) * fc.chunk) + off;
-        mbar_arrive_expect_tx(&lbar[b], len);
-        bulk_load(buf + b * PIECE, src, len, &lbar[b], pol);
-        mbar_wait(&lbar[b], static_cast<uint32_t>((k >> 1) & 1));
+        sent += static_cast<double>(it.len) * (fc.kind == 0 ? targets : (it.q == it.v ? 0 : 1));
+        mbar_wait(&lbar[b], par);
         if (fc.kind == 0) {
             for (int t = 1; t <= fc.n; ++t) {
-                const int d = (v + t) % fc.n;  // rotated targets
-                if (d == v && fc.skip_self) continue;
-                bulk_store(fc.dst[d] + static_cast<int64_t>(v) * fc.chunk + off, buf + b * PIECE, len, pol);
+                const int d = (it.v + t) % fc.n;  // rotated targets
+                if (d == it.v && fc.skip_self) continue;
+                bulk_store(fc.dst[d] + static_cast<int64_t>(it.v) * fc.chunk + it.off, buf + b * piece, it.len, pol);
             }
         } else {
-            bulk_store(fc.dst[q] + static_cast<int64_t>(v) * fc.chunk + off, buf + b * PIECE, len, pol);
+            bulk_store(fc.dst[it.q] + static_cast<int64_t>(it.v) * fc.chunk + it.off, buf + b * piece, it.len, pol);
         }
         bulk_commit();
+        // refill slot (k-1) % nb (its stores = group k-1) with item k+nb-1
+        if (k + nb - 1 < mine) {
+            bulk_wait_read<1>();
+            issue_load(k + nb - 1, refill);
+        }
+        if (++refill == nb) refill = 0;
+        if (++b == nb) {
+            b = 0;
+            par ^= 1;
+        }
     }
     bulk_wait_all();
     fence_proxy_async_global();
@@ -251,8 +297,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     int* tile_ring = reinterpret_cast<int*>(tile_empty + RING);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + RING);
     // fused C3 state (FUSED only): copy buffers after the ring, 1 KiB aligned
-    uint64_t* lbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [2] copy loads
-    uint32_t* progress = reinterpret_cast<uint32_t*>(lbar + 2);   // producer k-blocks issued
+    uint64_t* lbar = reinterpret_cast<uint64_t*>(tmem_slot + 2);  // [kFusedSlots] copy loads
+    uint32_t* progress = reinterpret_cast<uint32_t*>(lbar + kFusedSlots);  // producer k-blocks issued
     uint32_t* producer_done = progress + 1;
     uint8_t* epi_stage = smem + STAGES * STAGE + 1024;
 #ifndef C3_EPI_BUFS
@@ -283,8 +329,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_init(&tile_empty[r], 2 + 2 * Cfg::EPI_WARPS);
         }
         if (FUSED) {
-            mbar_init(&lbar[0], 1);
-            mbar_init(&lbar[1], 1);
+            for (int b = 0; b < kFusedSlots; ++b) mbar_init(&lbar[b], 1);
             *progress = 0;
             *producer_done = 0;
         }

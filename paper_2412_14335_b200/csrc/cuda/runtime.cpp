@@ -275,7 +275,7 @@ struct c3_session {
     uint32_t* done = nullptr;               // [0] AG counter, [1] RS counter
     uint32_t epoch = 0;
     float fused_pace = 0.0f;                // C3_FUSED: copies finish by this share of the GEMM (0 = unpaced)
-    int64_t fused_piece = 4096;             // C3_FUSED: bytes per bulk copy
+    int64_t fused_piece = 8192;             // C3_FUSED: bytes per bulk copy (the slot size)
     int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
     double link_gbps = 0.0;                 // link emulation: peer-traffic budget per step (0 = off)
     c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
