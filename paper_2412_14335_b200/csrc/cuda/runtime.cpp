@@ -21,6 +21,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <string>
@@ -171,10 +172,27 @@ int green_partition(c3_world* w, int comm_sms, GreenPartition** out) {
 // (every runtime path, including cudaMemcpyBatchAsync with
 // PreferOverlapWithCompute). So the DMA backend is copy-engine only across
 // devices; in a loopback world its "transfers" are SM copies.
+// Batched submission (cudaMemcpyBatchAsync, one call per engine stream with
+// PreferOverlapWithCompute) instead of one cudaMemcpyAsync per transfer:
+// the per-transfer CPU launch overhead the reference's plan_cost charges
+// (conccl.cpp:200-229, cpu_launch_overhead) is paid once per engine.
+// C3_CE_BATCH=0 selects the per-transfer path.
+bool ce_batch_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("C3_CE_BATCH");
+        return !(e != nullptr && std::string(e) == "0");
+    }();
+    return on;
+}
+
 int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, void* const* dst,
            int src_filter, cudaStream_t parent) {
     if (!w->fork_event) C3_CUDA(cudaEventCreateWithFlags(&w->fork_event, cudaEventDisableTiming));
     std::vector<char> used;
+    // per engine stream: the batch (dst, src, size) of its transfers, plan order
+    std::vector<std::vector<void*>> bd, bs;
+    std::vector<std::vector<size_t>> bz;
+    const bool batch = ce_batch_enabled();
     bool forked = false;
     for (int i = 0; i < nt; ++i) {
         const c3_transfer& x = t[i];
@@ -185,15 +203,41 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
             C3_CUDA(cudaEventRecord(w->fork_event, parent));
             forked = true;
         }
-        if (used.size() <= idx) used.resize(idx + 1, 0);
+        if (used.size() <= idx) {
+            used.resize(idx + 1, 0);
+            bd.resize(idx + 1);
+            bs.resize(idx + 1);
+            bz.resize(idx + 1);
+        }
         if (!used[idx]) {
             C3_CUDA(cudaStreamWaitEvent(w->ce_streams[idx], w->fork_event, 0));
             used[idx] = 1;
         }
-        C3_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(dst[x.dst_gpu]) + x.dst_offset,
-                                static_cast<const uint8_t*>(src[x.src_gpu]) + x.src_offset,
-                                static_cast<size_t>(x.length), cudaMemcpyDeviceToDevice,
-                                w->ce_streams[idx]));
+        void* d = static_cast<uint8_t*>(dst[x.dst_gpu]) + x.dst_offset;
+        const void* sp = static_cast<const uint8_t*>(src[x.src_gpu]) + x.src_offset;
+        if (batch) {
+            bd[idx].push_back(d);
+            bs[idx].push_back(const_cast<void*>(sp));
+            bz[idx].push_back(static_cast<size_t>(x.length));
+        } else {
+            C3_CUDA(cudaMemcpyAsync(d, sp, static_cast<size_t>(x.length), cudaMemcpyDeviceToDevice,
+                                    w->ce_streams[idx]));
+        }
+    }
+    if (batch) {
+        cudaMemcpyAttributes attr{};
+        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
+        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
+        size_t attr_idx = 0;
+        for (std::size_t idx = 0; idx < used.size(); ++idx) {
+            if (!used[idx] || bd[idx].empty()) continue;
+            size_t fail = 0;
+            const cudaError_t e = cudaMemcpyBatchAsync(bd[idx].data(), bs[idx].data(), bz[idx].data(),
+                                                       bd[idx].size(), &attr, &attr_idx, 1, &fail,
+                                                       w->ce_streams[idx]);
+            if (e != cudaSuccess)
+                return set_cuda_error(e, ("cudaMemcpyBatchAsync (transfer " + std::to_string(fail) + ")").c_str());
+        }
     }
     for (std::size_t idx = 0; idx < used.size(); ++idx) {
         if (!used[idx]) continue;
