@@ -331,7 +331,7 @@ def test_session_alltoall_all_strategies(torch_mod, c3, n):
 
 @pytest.mark.parametrize("collective", [0, 1], ids=["all-gather", "all-to-all"])
 @pytest.mark.parametrize("n", [2, 8])
-@pytest.mark.parametrize("pace,piece", [(0.0, 4096), (0.8, 16384), (0.0, 0)])
+@pytest.mark.parametrize("pace,piece", [(0.0, 4096), (0.8, 16384), (0.0, 0), (0.0, 2048), (0.5, 1040)])
 @pytest.mark.parametrize("kernel", ["pair", "pair512"])
 def test_fused_c3_bit_exact(torch_mod, c3, monkeypatch, collective, n, pace, piece, kernel):
     """C3_FUSED: the collective moved inside the CTA-pair GEMM by its copy warp
@@ -393,11 +393,12 @@ def test_degenerate_worlds(c3, collective):
 
 
 @pytest.mark.parametrize("collective", [0, 1, 2], ids=["all-gather", "all-to-all", "reduce-scatter"])
-def test_link_rate_emulation_exact_and_paced(torch_mod, c3, monkeypatch, collective):
+@pytest.mark.parametrize("kernel", ["pair", "pair512"])
+def test_link_rate_emulation_exact_and_paced(torch_mod, c3, monkeypatch, collective, kernel):
     """c3_session_set_link_rate: the paced SM collective (and the paced fused
     copies) deliver bit-identical data, and the isolated collective takes the
     link time (n-1)/n * P / rate, independent of the CTA count."""
-    monkeypatch.setenv("C3_GEMM_KERNEL", "pair")  # the fused path needs the CTA-pair GEMM
+    monkeypatch.setenv("C3_GEMM_KERNEL", kernel)  # the fused path needs a CTA-pair GEMM
     n, rate = 8, 200.0  # GB/s: slow enough that pacing, not HBM, sets the time
     payload = n * (8 << 20)  # enough 32 KiB iterations per CTA for the pace to be smooth
     w = c3.World(0, n, 0, loopback=True)
