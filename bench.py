@@ -308,6 +308,16 @@ def run_ours(args, dist):
         sess.set_comm_curve(sorted(curve.items()))
     else:
         t_g_pick, t_c_pick = t_g, iso_comm["cu"]
+        # the collective's time vs CTA units on this world's links (real NVLink
+        # at N>1): the co-residency model's comm curve, measured here rather
+        # than taken from the loopback tables (collective: every rank runs it)
+        curve = {}
+        for ctas in (8, 16, 24, 32, 48, 64):
+            a = sess.default_alloc(c3.COMM_ONLY_CU)
+            a.cus_comm = ctas
+            curve[ctas] = median([r[2] for r in timed(c3.COMM_ONLY_CU, 3, a)])
+        curve[full] = min(t_c_pick, min(curve.values()))
+        sess.set_comm_curve(sorted(curve.items()))
 
     def coresident(st, g, c):
         a = sess.default_alloc(st)
@@ -346,7 +356,7 @@ def run_ours(args, dist):
         cands = [(head, head_alloc)] + (emulated_candidates() if emulate else full_speed_candidates())
         sess.set_link_rate(link)
         meds = []
-        best_i, best_ms = sess.autotune(cands, rounds=5, reduce_max=dist.max_list, medians=meds)
+        best_i, best_ms = sess.autotune(cands, rounds=9, reduce_max=dist.max_list, medians=meds)
         log(f"autotune done: {best_i}")
         tune = {"candidates": [{"strategy": c3.STRATEGY_NAMES[st], "cus_gemm": a.cus_gemm,
                                 "cus_comm": a.cus_comm, "median_ms": ms}
@@ -371,7 +381,7 @@ def run_ours(args, dist):
     if emulate:
         fc = full_speed_candidates()
         sess.set_link_rate(0.0)
-        fi, _ = sess.autotune(fc, rounds=3, reduce_max=dist.max_list)
+        fi, _ = sess.autotune(fc, rounds=5, reduce_max=dist.max_list)
         fs = fc[fi]
 
     # ---- the timed region: K rounds of the headline C3 step, each round also
