@@ -319,29 +319,50 @@ def run_ours(args, dist):
         curve[full] = min(t_c_pick, min(curve.values()))
         sess.set_comm_curve(sorted(curve.items()))
 
-    def coresident(st, g, c):
+    def coresident(st, g, c, pace=0.0):
         a = sess.default_alloc(st)
         a.cus_gemm, a.cus_comm = g, c
+        a.comm_pace_gbps = pace
         return (st, a)
+
+    peer_bytes = (n - 1) / n * cfg["payload"]
+
+    def pace_for(frac, t_gemm_ms, cap):
+        """The rate that spreads the collective over `frac` of the GEMM (GB/s),
+        if below the link rate `cap` (0 = no cap); else 0 (unpaced)."""
+        r = peer_bytes / (frac * t_gemm_ms * 1e-3) / 1e9
+        return r if (cap <= 0 or r < cap) else 0.0
 
     def full_speed_candidates():
         cands = [(c3.SERIAL, sess.default_alloc(c3.SERIAL))]
         for st in (c3.C3_BASE, c3.C3_SP):
             for ctas in (8, 16, 32, 64):
                 cands.append(coresident(st, full, ctas))
+        # B200 extension: the collective paced to spread over the GEMM
+        for frac in (0.6, 0.8):
+            p = pace_for(frac, t_g, 0.0)
+            if p > 0:
+                cands += [coresident(c3.C3_BASE, full, c, p) for c in (16, 32)]
         if dma_ok:
             cands += [(st, sess.default_alloc(st)) for st in (c3.CONCCL, c3.CONCCL_RP)]
         if fused_ok:
             cands.append((c3.FUSED, sess.default_alloc(c3.FUSED)))
         return cands
 
-    def emulated_candidates():
+    def emulated_candidates(co_ctas):
         # the collective paced to the link rate on nvl_ctas CTAs (the SM
         # footprint of a link-bound P2P kernel); fused: the GEMM's copy warps paced
         part = max(8, nvl_ctas)
         cands = [coresident(c3.SERIAL, full, nvl_ctas), coresident(c3.C3_BASE, full, nvl_ctas),
                  coresident(c3.C3_SP, full, nvl_ctas), coresident(c3.C3_RP, full - part, nvl_ctas),
                  coresident(c3.C3_SP_RP, full - part, nvl_ctas)]
+        # B200 extension: the co-resident collective (the model's CTA count)
+        # paced below the link rate, spread over 60% / 80% of the GEMM
+        # (measured: 0.75 -> 0.93 of ideal on cfg2, profiles/r01_pace_probe.txt)
+        for frac in (0.6, 0.8):
+            p = pace_for(frac, t_g_pick, NVLINK_PEER_GBPS)
+            if p > 0:
+                cands.append(coresident(c3.C3_BASE, full, co_ctas, p))
         if fused_ok:
             cands.append((c3.FUSED, sess.default_alloc(c3.FUSED)))
         return cands
@@ -353,13 +374,15 @@ def run_ours(args, dist):
         head, head_alloc, predicted = sess.choose(t_g_pick, t_c_pick, iso_comm["dma"], dma_ok)
         if emulate and head_alloc.cus_gemm + head_alloc.cus_comm <= full:
             head_alloc.cus_comm = nvl_ctas  # the model's split, the collective at NVLink rate
-        cands = [(head, head_alloc)] + (emulated_candidates() if emulate else full_speed_candidates())
+        co_ctas = head_alloc.cus_comm if head_alloc.cus_gemm + head_alloc.cus_comm > full else max(16, nvl_ctas or 16)
+        cands = [(head, head_alloc)] + (emulated_candidates(co_ctas) if emulate else full_speed_candidates())
         sess.set_link_rate(link)
         meds = []
         best_i, best_ms = sess.autotune(cands, rounds=9, reduce_max=dist.max_list, medians=meds)
         log(f"autotune done: {best_i}")
         tune = {"candidates": [{"strategy": c3.STRATEGY_NAMES[st], "cus_gemm": a.cus_gemm,
-                                "cus_comm": a.cus_comm, "median_ms": ms}
+                                "cus_comm": a.cus_comm, "comm_pace_gbps": round(a.comm_pace_gbps, 1),
+                                "median_ms": ms}
                                for (st, a), ms in zip(cands, meds)],
                 "model_pick": c3.STRATEGY_NAMES[head], "model_alloc": {"cus_gemm": head_alloc.cus_gemm,
                                                                       "cus_comm": head_alloc.cus_comm},
@@ -438,7 +461,7 @@ def run_ours(args, dist):
 
     def alloc_dict(a):
         return {"cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm, "cus_idle": a.cus_idle,
-                "backend": ["CU", "DMA", "TMA"][a.backend]}
+                "backend": ["CU", "DMA", "TMA"][a.backend], "comm_pace_gbps": round(a.comm_pace_gbps, 1)}
 
     choice = {"strategy": head_name, "selected_by": "runtime: model prediction (c3_session_choose) + "
               "measured autotune (c3_session_autotune)" if args.strategy == "auto" else "--strategy",

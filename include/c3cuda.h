@@ -108,6 +108,11 @@ typedef struct c3_alloc {
     int32_t cus_gemm, cus_comm, cus_idle;
     int32_t backend;
     int32_t comm_first;
+    /* B200 extension: in a concurrent run, pace the SM (or fused) collective's
+     * peer traffic to this rate in GB/s (the lower of it and the session's
+     * link rate), spreading it over the GEMM instead of bursting it at link
+     * speed (0 = unpaced). Isolated collective runs ignore it. */
+    float comm_pace_gbps;
 } c3_alloc;
 
 /* Device-event timing of one C3 step on this rank, milliseconds from the

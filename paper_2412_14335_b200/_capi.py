@@ -50,7 +50,7 @@ class ScenarioDesc(C.Structure):
 
 class Alloc(C.Structure):
     _fields_ = [("cus_gemm", C.c_int32), ("cus_comm", C.c_int32), ("cus_idle", C.c_int32),
-                ("backend", C.c_int32), ("comm_first", C.c_int32)]
+                ("backend", C.c_int32), ("comm_first", C.c_int32), ("comm_pace_gbps", C.c_float)]
 
 
 class Timing(C.Structure):

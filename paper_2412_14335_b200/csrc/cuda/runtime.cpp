@@ -322,6 +322,7 @@ struct c3_session {
     int64_t fused_piece = 8192;             // C3_FUSED: bytes per bulk copy (the slot size)
     int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
     double link_gbps = 0.0;                 // link emulation: peer-traffic budget per step (0 = off)
+    double run_gbps = 0.0;                  // this run's pacing: link rate, or a concurrent run's comm pace
     c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
     void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
@@ -433,7 +434,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             const Signals sig = make_signals(s, 0);
             for (int v = first; v <= last; ++v) {
                 C3_TRY(launch_allgather_push(v, n, static_cast<uint8_t*>(recv.p[v]) + chunk * v, recv,
-                                             chunk, n_ctas, sig, st, s->link_gbps));
+                                             chunk, n_ctas, sig, st, s->run_gbps));
                 ++*launches;
             }
         } else {
@@ -457,7 +458,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             const Signals sig = make_signals(s, 0);
             for (int v = first; v <= last; ++v) {
                 C3_TRY(launch_alltoall_push(v, n, loop ? s->in[static_cast<size_t>(v)] : s->in[0], recv,
-                                            chunk, n_ctas, sig, st, s->link_gbps));
+                                            chunk, n_ctas, sig, st, s->run_gbps));
                 ++*launches;
             }
         } else {
@@ -482,7 +483,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         const Signals sig = make_signals(s, 1);
         for (int v = first; v <= last; ++v) {
             void* out = loop ? s->out[static_cast<size_t>(v)] : s->out[0];
-            C3_TRY(launch_reduce_scatter_pull(v, n, in, out, count, n_ctas, sig, st, s->link_gbps));
+            C3_TRY(launch_reduce_scatter_pull(v, n, in, out, count, n_ctas, sig, st, s->run_gbps));
             ++*launches;
         }
         return C3_OK;
@@ -1159,6 +1160,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
             alloc->cus_idle = 0;
             alloc->backend = C3_BACKEND_CU;
             alloc->comm_first = 0;
+            alloc->comm_pace_gbps = 0.f;
             return C3_OK;
         }
         c3sim::EfficiencyParams eff;
@@ -1173,6 +1175,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
         alloc->cus_idle = a.cus_idle;
         alloc->backend = a.comm_backend == c3sim::CommBackend::DMA ? C3_BACKEND_DMA : C3_BACKEND_CU;
         alloc->comm_first = a.comm_first ? 1 : 0;
+        alloc->comm_pace_gbps = 0.f;
         return C3_OK;
     });
 }
@@ -1241,11 +1244,11 @@ int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
     const int C = s->md.cus_per_gpu;
     if (strategy >= C3_GEMM_ONLY) {
         *out = {C, strategy == C3_COMM_ONLY_CU ? 32 : 0, 0,
-                strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA : C3_BACKEND_CU, 0};
+                strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA : C3_BACKEND_CU, 0, 0.f};
         return C3_OK;
     }
     if (strategy == C3_FUSED) {
-        *out = {C, 0, 0, C3_BACKEND_TMA, 0};
+        *out = {C, 0, 0, C3_BACKEND_TMA, 0, 0.f};
         return C3_OK;
     }
     if (strategy < C3_SERIAL || strategy > C3_CONCCL_RP)
@@ -1259,6 +1262,7 @@ int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
         out->cus_idle = a.cus_idle;
         out->backend = a.comm_backend == c3sim::CommBackend::DMA ? C3_BACKEND_DMA : C3_BACKEND_CU;
         out->comm_first = a.comm_first ? 1 : 0;
+        out->comm_pace_gbps = 0.f;
         if (strategy == C3_SERIAL) out->cus_comm = C;  // each kernel alone on the whole GPU
         return C3_OK;
     });
@@ -1295,6 +1299,14 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     }
     t->gemm_ctas = gemm_ctas;
     t->comm_ctas = a.backend == C3_BACKEND_CU ? comm_ctas : 0;
+    // pacing of this run's SM / fused collective: the emulated link rate, or
+    // (concurrent runs) the allocation's comm pace when lower
+    s->run_gbps = s->link_gbps;
+    const bool concurrent = strategy != C3_SERIAL && strategy != C3_GEMM_ONLY &&
+                            strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;
+    if (concurrent && a.comm_pace_gbps > 0.f &&
+        (s->run_gbps <= 0.0 || static_cast<double>(a.comm_pace_gbps) < s->run_gbps))
+        s->run_gbps = a.comm_pace_gbps;
     int launches = 0;
 
     if (strategy == C3_FUSED) {
@@ -1308,7 +1320,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         fc.pace = s->fused_pace;
         fc.piece = s->fused_piece;
         fc.mode = s->fused_mode;
-        fc.link_bpns = s->link_gbps;
+        fc.link_bpns = s->run_gbps;
         const bool loop = w->loopback != 0;
         fc.self_begin = loop ? 0 : w->rank;
         fc.self_end = loop ? ((flags & kRunAllRanks) ? s->n : 1) : w->rank + 1;

@@ -130,7 +130,7 @@ def test_gemm_cta_cap_same_result(torch_mod, c3, max_ctas):
     w.close()
 
 
-@pytest.mark.parametrize("M,N,K", [(8192, 28672, 8192), (128, 53248, 16384)])
+@pytest.mark.parametrize("M,N,K", [(8192, 28672, 8192), (128, 53248, 16384), (64, 53248, 16384)])
 def test_gemm_llama_shapes_sampled(torch_mod, c3, M, N, K):
     """BASELINE configs[1]/[3] shapes: sampled entries + full tile-boundary rows/cols."""
     torch = torch_mod
@@ -445,3 +445,38 @@ def test_link_rate_emulation_exact_and_paced(torch_mod, c3, monkeypatch, collect
 
 def _comm_ms(t):
     return t.comm_end_ms - t.comm_start_ms
+
+
+@pytest.mark.parametrize("collective", [0, 2], ids=["all-gather", "reduce-scatter"])
+def test_comm_pace_in_concurrent_runs(torch_mod, c3, collective):
+    """c3_alloc.comm_pace_gbps: a concurrent run paces its collective to the
+    given rate (bit-identical data, the collective stretched to the paced
+    time); the isolated collective with the same allocation ignores it."""
+    n, rate = 8, 100.0
+    payload = n * (4 << 20)
+    w = c3.World(0, n, 0, loopback=True)
+    s = c3.Session(w, 512, 1024, 512, collective, payload)
+    target_ms = (n - 1) / n * payload / (rate * 1e9) * 1e3
+    a = s.default_alloc(c3.C3_BASE)
+    a.cus_gemm, a.cus_comm, a.comm_pace_gbps = w.info.sm_count, 16, rate
+    t = s.run(c3.C3_BASE, a)  # this rank's share: (n-1)/n * payload of peer traffic
+    comm_ms = t.comm_end_ms - t.comm_start_ms
+    assert 0.95 * target_ms <= comm_ms <= 1.5 * target_ms, (comm_ms, target_ms)
+    s.fill(SEED)
+    s.run(c3.C3_BASE, a, all_ranks=True)  # every virtual rank's share, for the data check
+    chunk = payload // n
+    got = np.empty(payload if collective == 0 else chunk // 2 * 2, np.uint8)
+    c3.check(c3.lib().c3_memcpy(got.ctypes.data, s.pointers(0).recv, got.size, 2, None))
+    c3.check(c3.lib().c3_stream_sync(None))
+    if collective == 0:
+        assert np.array_equal(got, orc.expected_allgather(n, chunk, SEED, 2))
+    else:
+        count = chunk // 2
+        host_in = [orc.bf16(n * count, SEED, g, 3) for g in range(n)]
+        assert np.array_equal(got.view(np.uint16), orc.reduce_scatter(host_in, 0, count))
+    iso = s.default_alloc(c3.COMM_ONLY_CU)
+    iso.cus_comm, iso.comm_pace_gbps = 16, rate
+    fast = min(_comm_ms(s.run(c3.COMM_ONLY_CU, iso)) for _ in range(3))
+    assert fast < 0.5 * target_ms
+    s.close()
+    w.close()
