@@ -50,6 +50,10 @@ struct CoResidentParams {
     double gemm_compute_bound = 1.0;
     double gemm_memory_bound = 1.0;
     double comm = 1.0;
+    /// Comm pacing: the GEMM penalty's excess scales with the collective's
+    /// rate as (rate / link rate)^rate_exponent; 1 = linear (pacing neutral),
+    /// > 1 = spreading the collective over the GEMM pays.
+    double rate_exponent = 1.0;
 
     double gemm(KernelClass gemm_class) const {
         return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
@@ -58,7 +62,8 @@ struct CoResidentParams {
 
 void validate(const CoResidentParams& p);
 
-/// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc}.
+/// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc,
+///        "rate-exponent": g (optional, default 1)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 
@@ -70,8 +75,13 @@ int coresident_comm_ctas(int cus_comm, const CoResidentParams& p);
 /// the isolated collective's time on coresident_comm_ctas(cus_comm) CTAs).
 /// serial_time / ideal use t_comm_full, the collective's isolated time on the
 /// whole GPU (the paper's t_comm).
+/// rate_ratio (<= 1): the collective's paced rate over the link rate (1 =
+/// unpaced); the GEMM penalty's excess scales by rate_ratio^rate_exponent.
+/// A paced collective's t_comm_at_ctas is the longer of the curve time and
+/// bytes / paced rate (the caller's).
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
-                                int cus_comm, KernelClass gemm_class, const CoResidentParams& p);
+                                int cus_comm, KernelClass gemm_class, const CoResidentParams& p,
+                                double rate_ratio = 1.0);
 
 /// Penalty p_g that makes simulate_coresident reproduce a measured makespan
 /// (collective finishing first, p_c = 1); clamped to [1, 100]. Returns 1.0

@@ -1007,13 +1007,30 @@ double comm_ms_at(const c3_session* s, int ctas, double t_comm_cu_ms) {
     return t_comm_cu_ms * c3sim::slowdown_at(s->tables.at(cls), ctas);
 }
 
+// This rank's peer bytes per collective (AG / A2A pushed, RS pulled).
+double peer_bytes(const c3_session* s) { return static_cast<double>(s->n - 1) * static_cast<double>(s->chunk); }
+
+// The collective's unpaced rate in GB/s (= bytes/ns): the emulated link rate,
+// else the measured full-GPU time's.
+double link_rate_gbps(const c3_session* s, double t_comm_cu_ms) {
+    return s->link_gbps > 0.0 ? s->link_gbps : peer_bytes(s) / (t_comm_cu_ms * 1e6);
+}
+
 // B200 co-resident prediction (include/c3sim/coresident.hpp): GEMM on all
-// SMs, the SM collective on `ctas` CTAs beside it.
-double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, double t_comm_cu_ms) {
+// SMs, the SM collective on `ctas` CTAs beside it, paced to pace_gbps if > 0.
+double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, double t_comm_cu_ms,
+                          double pace_gbps = 0.0) {
     const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
     const int eff = c3sim::coresident_comm_ctas(ctas, s->cores);
-    return c3sim::simulate_coresident(t_gemm_ms * 1e-3, comm_ms_at(s, eff, t_comm_cu_ms) * 1e-3,
-                                      t_comm_cu_ms * 1e-3, s->md.cus_per_gpu, ctas, gcls, s->cores)
+    double t_at = comm_ms_at(s, eff, t_comm_cu_ms);
+    double ratio = 1.0;
+    const double link = link_rate_gbps(s, t_comm_cu_ms);
+    if (pace_gbps > 0.0 && pace_gbps < link) {
+        ratio = pace_gbps / link;
+        t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));
+    }
+    return c3sim::simulate_coresident(t_gemm_ms * 1e-3, t_at * 1e-3, t_comm_cu_ms * 1e-3, s->md.cus_per_gpu,
+                                      ctas, gcls, s->cores, ratio)
         .makespan;
 }
 
@@ -1070,7 +1087,8 @@ int c3_session_predict_alloc(c3_session* s, int strategy, const c3_alloc* alloc,
         return set_error(C3_ERR_VALIDATION, "c3_session_predict_alloc: co-resident allocation needs "
                                             "c3_session_load_coresident");
     return guarded([&] {
-        *predicted_ms = predict_coresident(s, alloc->cus_comm, t_gemm_ms, t_comm_cu_ms) * 1e3;
+        *predicted_ms =
+            predict_coresident(s, alloc->cus_comm, t_gemm_ms, t_comm_cu_ms, alloc->comm_pace_gbps) * 1e3;
         return C3_OK;
     });
 }
@@ -1152,6 +1170,21 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
                 }
             }
         }
+        // comm pacing of the co-resident pick: the collective spread over
+        // 60% / 80% of the GEMM, when that is below its unpaced rate
+        double best_pace = 0.0;
+        if (best_cores) {
+            const double link = link_rate_gbps(s, t_comm_cu_ms);
+            for (double frac : {0.8, 0.6}) {
+                const double pace = peer_bytes(s) / (frac * t_gemm_ms * 1e6);
+                if (!(pace < link)) continue;
+                const double m = predict_coresident(s, best_cores, t_gemm_ms, t_comm_cu_ms, pace);
+                if (m < best * 0.995) {
+                    best = m;
+                    best_pace = pace;
+                }
+            }
+        }
         *strategy = best_st;
         *predicted_ms = best * 1e3;
         if (best_cores) {
@@ -1160,7 +1193,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
             alloc->cus_idle = 0;
             alloc->backend = C3_BACKEND_CU;
             alloc->comm_first = 0;
-            alloc->comm_pace_gbps = 0.f;
+            alloc->comm_pace_gbps = static_cast<float>(best_pace);
             return C3_OK;
         }
         c3sim::EfficiencyParams eff;

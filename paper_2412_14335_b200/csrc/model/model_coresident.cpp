@@ -51,6 +51,8 @@ SlowdownTable CommCurve::as_table(KernelClass cls, const MachineDescriptor& md) 
 void validate(const CoResidentParams& p) {
     for (double v : {p.gemm_compute_bound, p.gemm_memory_bound, p.comm})
         if (!(v >= 1.0) || !std::isfinite(v)) throw ValidationError("co-resident penalties must be finite and >= 1");
+    if (!(p.rate_exponent > 0) || !std::isfinite(p.rate_exponent))
+        throw ValidationError("co-resident rate exponent must be finite and > 0");
 }
 
 CoResidentParams load_coresident_params(const std::filesystem::path& path) {
@@ -69,6 +71,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.gemm_compute_bound = j.at("gemm-compute-bound").get<double>();
         p.gemm_memory_bound = j.at("gemm-memory-bound").get<double>();
         p.comm = j.value("comm", 1.0);
+        p.rate_exponent = j.value("rate-exponent", 1.0);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -79,7 +82,8 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
 std::string save_coresident_params(const CoResidentParams& p) {
     json j = {{"gemm-compute-bound", p.gemm_compute_bound},
               {"gemm-memory-bound", p.gemm_memory_bound},
-              {"comm", p.comm}};
+              {"comm", p.comm},
+              {"rate-exponent", p.rate_exponent}};
     return j.dump(2) + "\n";
 }
 
@@ -89,17 +93,20 @@ int coresident_comm_ctas(int cus_comm, const CoResidentParams& p) {
 }
 
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
-                                int cus_comm, KernelClass gemm_class, const CoResidentParams& p) {
+                                int cus_comm, KernelClass gemm_class, const CoResidentParams& p,
+                                double rate_ratio) {
     validate(p);
     if (!(t_gemm > 0) || !(t_comm_at_ctas > 0) || !(t_comm_full > 0))
         throw ValidationError("simulate_coresident: isolated times must be positive");
+    if (!(rate_ratio > 0) || rate_ratio > 1.0 + 1e-12)
+        throw ValidationError("simulate_coresident: rate_ratio must be in (0, 1]");
     SimTimeline tl;
     tl.serial_time = t_gemm + t_comm_full;
     tl.ideal = ideal_speedup(t_gemm, t_comm_full);
     tl.work_gemm = t_gemm;
     tl.work_comm = t_comm_full;
     // phase 1: both resident; rates in units of each kernel's isolated work
-    const double rg = 1.0 / p.gemm(gemm_class);
+    const double rg = 1.0 / (1.0 + (p.gemm(gemm_class) - 1.0) * std::pow(rate_ratio, p.rate_exponent));
     const double rc = t_comm_full / t_comm_at_ctas;
     const double end_g = t_gemm / rg, end_c = t_comm_full / rc;
     const double t1 = std::min(end_g, end_c);

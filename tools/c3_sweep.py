@@ -34,9 +34,9 @@ def main():
     world = f"loopback-8-link{link:.0f}" if link > 0 else "loopback-8"
     rows = ["scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
             "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
-            "predicted_makespan_s,t_comm_ctas_ms"]
-    picks = ["scenario_id,collective,model_pick,model_cus_comm,model_predicted_ms,model_pick_measured_ms,"
-             "measured_best,measured_best_ms,pick_over_best"]
+            "predicted_makespan_s,t_comm_ctas_ms,comm_pace_gbps"]
+    picks = ["scenario_id,collective,model_pick,model_cus_comm,model_pace_gbps,model_predicted_ms,"
+             "model_pick_measured_ms,measured_best,measured_best_ms,pick_over_best"]
     CORES = (16, 24, 32, 48, 64)
     cores_json = os.path.join(REPO, "data", "b200-coresident.json")
     for name in ("cfg2", "cfg2_448", "cfg3", "cfg4", "cfg4_mb"):
@@ -60,6 +60,18 @@ def main():
             # queue; in loopback they are SM copy kernels): full-speed sweep only
             for st in (range(1, 7) if link == 0 else range(1, 5)):
                 jobs[c3.STRATEGY_NAMES[st]] = (st, s.default_alloc(st))
+            # comm pacing (B200 extension): the co-resident collective spread
+            # over 60% / 80% of the GEMM (rate from a quick GEMM probe)
+            tg0 = statistics.median(s.run(c3.GEMM_ONLY).total_ms for _ in range(3))
+            peer = (8 - 1) / 8 * cfg["payload"]
+            for ctas in (16, 24):
+                for frac in (0.6, 0.8):
+                    pace = peer / (frac * tg0 * 1e-3) / 1e9
+                    if link > 0 and pace >= link:
+                        continue
+                    a = s.default_alloc(c3.C3_BASE)
+                    a.cus_gemm, a.cus_comm, a.comm_pace_gbps = full, ctas, pace
+                    jobs[f"c3_base_coresident{ctas}_pace{int(frac * 100)}"] = (c3.C3_BASE, a)
             for ctas in CORES:  # B200 co-resident SM variants + the comm curve
                 a = s.default_alloc(c3.C3_BASE)
                 a.cus_gemm, a.cus_comm = full, ctas
@@ -98,7 +110,7 @@ def main():
             flops = 2.0 * cfg["m"] * cfg["n"] * cfg["k"]
             rows.append(f"{sid},{coll},{tax},serial,{(tg + tc) / 1e3:.6g},1,{ideal:.6g},0,{tg:.4f},"
                         f"{tc:.4f},{flops / tg / 1e9:.1f},{full},{full},CU,{world},"
-                        f"{s.predict(c3.SERIAL, tg, tc, td) / 1e3:.6g},")
+                        f"{s.predict(c3.SERIAL, tg, tc, td) / 1e3:.6g},,0.0")
             measured = {}
             for k, (st, al) in jobs.items():
                 if k in ("gemm", "comm", "comm_dma") or k.startswith("comm_c"):
@@ -114,12 +126,15 @@ def main():
                             f"{c3.fraction_of_ideal(sp, ideal):.6g},{tg:.4f},{tc:.4f},"
                             f"{flops / gk / 1e9:.1f},{al.cus_gemm},{al.cus_comm},"
                             f"{['CU', 'DMA', 'TMA'][al.backend]},{world},{pred:.6g},"
-                            f"{curve[al.cus_comm] if 'coresident' in k else ''}")
+                            f"{curve.get(al.cus_comm, '') if 'coresident' in k else ''},{al.comm_pace_gbps:.1f}")
                 measured[k] = (mk, st, al)
             # the runtime heuristic's pick vs the measured best
             st, al, pred = s.choose(tg, tc, td, allow_dma=False)
+            def same_pace(x, y):
+                return (x == 0 and y == 0) or (x > 0 and y > 0 and abs(x - y) <= 0.1 * max(x, y))
             key = next((k for k, (_, s2, a2) in measured.items()
-                        if s2 == st and a2.cus_gemm == al.cus_gemm and a2.cus_comm == al.cus_comm), None)
+                        if s2 == st and a2.cus_gemm == al.cus_gemm and a2.cus_comm == al.cus_comm
+                        and same_pace(a2.comm_pace_gbps, al.comm_pace_gbps)), None)
             if st == c3.SERIAL:
                 key, pk = "serial", tg + tc
             else:
@@ -128,7 +143,8 @@ def main():
             bm = min(measured[best][0], tg + tc)
             if tg + tc < measured[best][0]:
                 best = "serial"
-            picks.append(f"{sid},{coll},{key or c3.STRATEGY_NAMES[st]},{al.cus_comm},{pred:.4f},{pk:.4f},"
+            picks.append(f"{sid},{coll},{key or c3.STRATEGY_NAMES[st]},{al.cus_comm},{al.comm_pace_gbps:.0f},"
+                         f"{pred:.4f},{pk:.4f},"
                          f"{best},{bm:.4f},{pk / bm:.4f}")
             s.close()
             w.close()

@@ -10,7 +10,9 @@ collective CTAs beside it. Its model has two parameters:
 Per scenario the curve is the measured (CTAs, time) points plus the
 full-GPU time; (p_g, p_c) minimise the mean squared relative error of
 c3sim.simulate_coresident against every c3_base_coresident row (grid search).
-Memory-bound GEMM scenarios (cfg4_mb) fit their own p_g.
+Memory-bound GEMM scenarios (cfg4_mb) fit their own p_g. Then the comm-pacing
+exponent g (the penalty's excess scales with (paced rate / link rate)^g) is
+fitted on the paced rows (c3_base_coresident{c}_pace{pct}, comm_pace_gbps).
 
 usage: python tools/calibrate_coresident.py SWEEP.csv [SWEEP2.csv ...] OUT.json"""
 import csv
@@ -30,15 +32,24 @@ def load(paths):
     scen = {}
     for path in paths:
         for r in csv.DictReader(open(path)):
-            if not r["strategy"].startswith("c3_base_coresident") or not r.get("t_comm_ctas_ms"):
+            if not r["strategy"].startswith("c3_base_coresident"):
                 continue
             key = (path, r["scenario_id"], r["collective"])
             d = scen.setdefault(key, {"tg": float(r["t_gemm_iso_ms"]) * 1e-3,
-                                      "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": []})
+                                      "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": [],
+                                      "paced": [], "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M"))})
             c = int(r["cus_comm"])
+            pace = float(r.get("comm_pace_gbps") or 0.0)
+            if pace > 0:
+                d["paced"].append((c, pace, float(r["makespan_s"])))
+                continue
+            if not r.get("t_comm_ctas_ms"):
+                continue
             d["pts"][c] = float(r["t_comm_ctas_ms"]) * 1e-3
             d["rows"].append((c, float(r["makespan_s"])))
     for d in scen.values():
+        if not d["pts"]:
+            continue
         pts = dict(d["pts"])
         pts[SMS] = min(d["tc"], min(pts.values()))
         cs = sorted(pts)
@@ -71,9 +82,27 @@ def fit(scen, cls_of):
     return best
 
 
+def paced_error(scen, cls_of, pg, pc, gamma):
+    """Mean squared relative error of the paced rows under (pg, pc, gamma)."""
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound = p.gemm_memory_bound = pg
+    p.comm, p.rate_exponent = pc, gamma
+    err, n = 0.0, 0
+    for key, d in scen.items():
+        peer = 7 / 8 * d["mib"] * 2 ** 20
+        link = peer / d["tc"] / 1e9  # GB/s of the unpaced collective
+        for c, pace, mk in d["paced"]:
+            ratio = min(1.0, pace / link)
+            t_at = max(d["curve"].time_at(c3sim.coresident_comm_ctas(c, p)), d["tc"] / ratio)
+            pred = c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls_of(key), p, ratio).makespan
+            err += ((pred - mk) / mk) ** 2
+            n += 1
+    return err / max(n, 1), n
+
+
 def main():
     *ins, out = sys.argv[1:]
-    scen = load(ins)
+    scen = {k: v for k, v in load(ins).items() if "curve" in v}
     is_mb = lambda key: key[1].startswith("cfg4_mb")  # noqa: E731  M=128: memory-bound GEMM
     cb = {k: v for k, v in scen.items() if not is_mb(k)}
     mb = {k: v for k, v in scen.items() if is_mb(k)}
@@ -81,8 +110,13 @@ def main():
     # memory-bound: p_c shared (a property of the collective CTA), p_g refit
     best_mb = min(((error(mb, lambda k: MB, pg, pc)[0], pg)
                    for pg in [1.0 + 0.01 * i for i in range(61)]), default=(0.0, pg_cb))
+    gam, n_p = 1.0, 0
+    if any(d["paced"] for d in cb.values()):
+        best_g = min((paced_error(cb, lambda k: CB, pg_cb, pc, g)[0], g) for g in [0.5 + 0.25 * i for i in range(23)])
+        gam, n_p = best_g[1], paced_error(cb, lambda k: CB, pg_cb, pc, best_g[1])[1]
+        print(f"comm pacing: rate exponent {gam:.2f}, rms rel. error {best_g[0] ** 0.5:.3f} ({n_p} rows)")
     prm = c3sim.CoResidentParams()
-    prm.gemm_compute_bound, prm.comm = pg_cb, pc
+    prm.gemm_compute_bound, prm.comm, prm.rate_exponent = pg_cb, pc, gam
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     with open(out, "w") as f:
         f.write(c3sim.save_coresident_params(prm))
