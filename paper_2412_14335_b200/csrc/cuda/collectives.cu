@@ -43,6 +43,14 @@ constexpr int kVecThreads = 256;
 constexpr int kCtasPerUnit = 2;
 constexpr int kThreadsRs = kVecThreads;
 constexpr int kUnroll = 4;
+// all-to-all moves one store per load (all-gather: n-1), so each thread keeps
+// more vectors in flight: 16 (C3_A2A_UNROLL, build-time A/B): co-resident
+// cfg2 all-to-all at 24-48 units 0.23-0.61 -> 0.82-0.88 of ideal
+// (profiles/r01_a2a_unroll.txt)
+#ifndef C3_A2A_UNROLL
+#define C3_A2A_UNROLL 16
+#endif
+constexpr int kUnrollA2a = C3_A2A_UNROLL;
 
 // Last-CTA election + cross-rank exit barrier. Called by every thread of every
 // CTA after its stores; returns after this rank has seen `epoch` from all peers
@@ -212,30 +220,30 @@ __global__ void __launch_bounds__(kVecThreads)
 a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, int n,
                     int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnroll;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnrollA2a;
     const uint64_t t0 = global_ns();
     double sent = 0.0;
     for (int j = 0; j < n; ++j) {
         const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
         const uint4* src = send + slot_vec * p;
         uint4* dst = static_cast<uint4*>(recv.p[p]) + slot_vec * self;
-        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnroll; blk < slot_vec;
+        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnrollA2a; blk < slot_vec;
              blk += step) {
             if (cta_bpns > 0.f && p != self) {
                 if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
                 __syncthreads();
                 const int64_t left = slot_vec - blk;
-                sent += 16.0 * static_cast<double>(left < kVecThreads * kUnroll ? left : kVecThreads * kUnroll);
+                sent += 16.0 * static_cast<double>(left < kVecThreads * kUnrollA2a ? left : kVecThreads * kUnrollA2a);
             }
             const int64_t base = blk + threadIdx.x;
-            uint4 v[kUnroll];
+            uint4 v[kUnrollA2a];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < kUnrollA2a; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
                 if (i < slot_vec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
             }
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < kUnrollA2a; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
                 if (i < slot_vec) {
                     if (stream_l2)
@@ -465,7 +473,7 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
     for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
     if ((align & 15) == 0) {
         const int64_t nvec = per_peer_bytes / 16;
-        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnroll, n_ctas * kCtasPerUnit);
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnrollA2a, n_ctas * kCtasPerUnit);
         a2a_push_vec_kernel<<<grid, kVecThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
                                                           n, nvec, stream_l2_enabled(),
                                                           static_cast<float>(link_bpns / grid), sig);
