@@ -524,6 +524,27 @@ def run_ours(args, dist):
                 traffic = json.load(f).get(f"{cfg['m']}x{cfg['n']}x{cfg['k']}", {}).get("dram_bytes")
         except Exception:
             traffic = None
+    # the GEMM's roofline: tensor-bound when its arithmetic intensity exceeds
+    # the machine's FLOP:byte ratio, else HBM-bound (cfg4_mb, M = 128)
+    gemm_bytes = 2.0 * (cfg["m"] * cfg["k"] + cfg["n"] * cfg["k"] + cfg["m"] * cfg["n"])
+    ratio = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    if flops / gemm_bytes >= ratio:
+        roofline = {"bound": "tensor", "kernel": "gemm_bf16_tn_pair_kernel (tcgen05 cta_group::2)",
+                    "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
+                    "frac": achieved / peaks["bf16_tflops"],
+                    "frac_of_sustained": achieved / peak_sus,
+                    "peak_source": peak_src + " burst bf16 (cuBLAS): the timed region is ~0.1 s "
+                                   "of GEMMs interleaved with collective-only phases, short of the "
+                                   "sustained (4 s back-to-back) regime",
+                    "algorithmic_flops_per_launch": flops, "traffic": traffic}
+    else:
+        gbs = gemm_bytes / (gemm_avg * 1e-3) / 1e9
+        roofline = {"bound": "hbm", "kernel": "gemm_bf16_tn_kernel (tcgen05, single-CTA tiles)",
+                    "achieved": gbs, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                    "frac": gbs / peaks["hbm_gbs"],
+                    "peak_source": peak_src + " HBM copy bandwidth",
+                    "algorithmic_bytes_per_launch": gemm_bytes, "traffic": traffic,
+                    "arithmetic_intensity": flops / gemm_bytes, "machine_flop_per_byte": ratio}
     if emulate:
         world_desc = (f"loopback with NVLink-rate emulation: 8-rank scenario on 1 GPU; this GPU's GEMM "
                       f"and its share of the collective (7 chunk copies into stand-in peer buffers in "
@@ -559,14 +580,7 @@ def run_ours(args, dist):
                    "timed_region_wall_s": wall},
         "loopback_full_speed": full_speed,
         "strategies_full_speed": results,
-        "roofline": {"bound": "tensor", "kernel": "gemm_bf16_tn_pair_kernel (tcgen05 cta_group::2)",
-                     "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                     "frac": achieved / peaks["bf16_tflops"],
-                     "frac_of_sustained": achieved / peak_sus,
-                     "peak_source": peak_src + " burst bf16 (cuBLAS): the timed region is ~0.1 s "
-                                    "of GEMMs interleaved with collective-only phases, short of the "
-                                    "sustained (4 s back-to-back) regime",
-                     "algorithmic_flops_per_launch": flops, "traffic": traffic},
+        "roofline": roofline,
         "e2e": {"value": e2e_speedup, "unit": "x (t_serial / t_concurrent, host buffers)",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "concurrent_ms": e2e_conc, "gemm_ms": e2e_g, "comm_ms": e2e_c},
