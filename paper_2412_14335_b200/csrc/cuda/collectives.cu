@@ -51,6 +51,12 @@ constexpr int kUnroll = 4;
 #define C3_A2A_UNROLL 16
 #endif
 constexpr int kUnrollA2a = C3_A2A_UNROLL;
+// all-gather: 8 vectors in flight per thread (64 registers: still co-resident
+// beside the GEMM; 16 takes 112 and is not), profiles/r01_ag_unroll.txt
+#ifndef C3_AG_UNROLL
+#define C3_AG_UNROLL 8
+#endif
+constexpr int kUnrollAg = C3_AG_UNROLL;
 
 // Last-CTA election + cross-rank exit barrier. Called by every thread of every
 // CTA after its stores; returns after this rank has seen `epoch` from all peers
@@ -100,20 +106,20 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
 #pragma unroll
     for (int j = 0; j < C3_MAX_RANKS; ++j)
         dst[j] = j < n ? static_cast<uint4*>(recv.p[j]) + slot_vec * self : nullptr;
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnroll;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnrollAg;
     const uint64_t t0 = global_ns();
     double sent = 0.0;  // peer bytes this CTA has pushed (pacing)
-    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnroll; blk < nvec; blk += step) {
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnrollAg; blk < nvec; blk += step) {
         if (cta_bpns > 0.f) {
             if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
             __syncthreads();
             const int64_t left = nvec - blk;
-            sent += 16.0 * (n - 1) * static_cast<double>(left < kVecThreads * kUnroll ? left : kVecThreads * kUnroll);
+            sent += 16.0 * (n - 1) * static_cast<double>(left < kVecThreads * kUnrollAg ? left : kVecThreads * kUnrollAg);
         }
         const int64_t base = blk + threadIdx.x;
-        uint4 v[kUnroll];
+        uint4 v[kUnrollAg];
 #pragma unroll
-        for (int u = 0; u < kUnroll; ++u) {
+        for (int u = 0; u < kUnrollAg; ++u) {
             const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
             if (i < nvec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
         }
@@ -123,7 +129,7 @@ ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, in
             if (p == self && !copy_self) continue;
             uint4* d = dst[p];
 #pragma unroll
-            for (int u = 0; u < kUnroll; ++u) {
+            for (int u = 0; u < kUnrollAg; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
                 if (i < nvec) {
                     if (stream_l2)
@@ -447,7 +453,7 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
                                                         static_cast<float>(link_bpns / grid), sig);
     } else if ((align & 15) == 0) {
         const int64_t nvec = chunk_bytes / 16;
-        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnroll, n_ctas * kCtasPerUnit);
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnrollAg, n_ctas * kCtasPerUnit);
         ag_push_vec_kernel<<<grid, kVecThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
                                                          n, nvec, nvec, in_place ? 0 : 1,
                                                          stream_l2_enabled(),
