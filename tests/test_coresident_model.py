@@ -133,3 +133,34 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
     got = json.loads(out.read_text())
     assert got["gemm-compute-bound"] == pytest.approx(1.12, abs=0.011)
     assert got["comm"] == pytest.approx(1.5, abs=0.051)
+
+
+def test_paced_collective_scales_the_gemm_penalty():
+    """rate_ratio r < 1 (comm pacing): the GEMM penalty's excess scales by
+    r^rate_exponent; r = 1 is the unpaced model."""
+    p = c3sim.CoResidentParams()
+    p.gemm_compute_bound, p.rate_exponent = 1.2, 2.0
+    tg, tc = 2.4e-3, 1.0e-3
+    base = c3sim.simulate_coresident(tg, tc, tc, 148, 24, CB, p)
+    assert c3sim.simulate_coresident(tg, tc, tc, 148, 24, CB, p, 1.0).makespan == pytest.approx(base.makespan)
+    # paced to half the rate: the collective takes 2 tc, the penalty excess 0.2 * 0.25
+    tl = c3sim.simulate_coresident(tg, 2 * tc, tc, 148, 24, CB, p, 0.5)
+    pen = 1.0 + 0.2 * 0.25
+    assert tl.makespan == pytest.approx(2 * tc + tg - 2 * tc / pen)
+    assert tl.makespan < base.makespan  # exponent 2 > 1: spreading pays
+    p.rate_exponent = 1.0  # linear: lost GEMM work ~ equal, no clear gain
+    lin = c3sim.simulate_coresident(tg, 2 * tc, tc, 148, 24, CB, p, 0.5)
+    assert lin.makespan == pytest.approx(2 * tc + tg - 2 * tc / 1.1)
+    for bad in (0.0, 1.5):
+        with pytest.raises(Exception):
+            c3sim.simulate_coresident(tg, tc, tc, 148, 24, CB, p, bad)
+
+
+def test_rate_exponent_roundtrip_and_default(tmp_path):
+    p = c3sim.CoResidentParams()
+    p.rate_exponent = 2.75
+    f = tmp_path / "c.json"
+    f.write_text(c3sim.save_coresident_params(p))
+    assert c3sim.load_coresident_params(str(f)).rate_exponent == 2.75
+    f.write_text('{"gemm-compute-bound": 1.1, "gemm-memory-bound": 1.0, "comm": 1.5}')
+    assert c3sim.load_coresident_params(str(f)).rate_exponent == 1.0
