@@ -75,8 +75,9 @@ int coresident_comm_ctas(int cus_comm, const CoResidentParams& p);
 /// the isolated collective's time on coresident_comm_ctas(cus_comm) CTAs).
 /// serial_time / ideal use t_comm_full, the collective's isolated time on the
 /// whole GPU (the paper's t_comm).
-/// rate_ratio (<= 1): the collective's paced rate over the link rate (1 =
-/// unpaced); the GEMM penalty's excess scales by rate_ratio^rate_exponent.
+/// rate_ratio (<= 1): the collective's actual rate beside the GEMM over its
+/// unpaced full-GPU rate (t_comm_full / t_comm_at_ctas: pacing or few CTAs);
+/// the GEMM penalty's excess scales by rate_ratio^rate_exponent.
 /// A paced collective's t_comm_at_ctas is the longer of the curve time and
 /// bytes / paced rate (the caller's).
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,

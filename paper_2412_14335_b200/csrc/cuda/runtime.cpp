@@ -1023,12 +1023,11 @@ double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, doubl
     const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
     const int eff = c3sim::coresident_comm_ctas(ctas, s->cores);
     double t_at = comm_ms_at(s, eff, t_comm_cu_ms);
-    double ratio = 1.0;
     const double link = link_rate_gbps(s, t_comm_cu_ms);
-    if (pace_gbps > 0.0 && pace_gbps < link) {
-        ratio = pace_gbps / link;
-        t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));
-    }
+    if (pace_gbps > 0.0 && pace_gbps < link) t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));
+    // the collective's actual rate relative to its unpaced full-GPU rate: pacing
+    // or too few co-resident CTAs both lower its intensity beside the GEMM
+    const double ratio = std::min(1.0, t_comm_cu_ms / t_at);
     return c3sim::simulate_coresident(t_gemm_ms * 1e-3, t_at * 1e-3, t_comm_cu_ms * 1e-3, s->md.cus_per_gpu,
                                       ctas, gcls, s->cores, ratio)
         .makespan;

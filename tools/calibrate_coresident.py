@@ -1,18 +1,21 @@
 """Fit the B200 co-residency parameters (include/c3sim/coresident.hpp) from
 measured sweep CSVs (tools/c3_sweep.py, which carries t_comm_ctas_ms: the
-isolated collective on each CTA count).
+isolated collective on each CTA count, and comm_pace_gbps for paced rows).
 
 The runtime's co-resident mode is c3_base with the GEMM on every SM and c
-collective CTAs beside it. Its model has two parameters:
-  p_g  the GEMM's slowdown while the collective runs beside it;
-  p_c  the collective CTA's cost factor: c co-resident CTAs move data like
-       c / p_c isolated CTAs (t_comm = curve(c / p_c)).
-Per scenario the curve is the measured (CTAs, time) points plus the
-full-GPU time; (p_g, p_c) minimise the mean squared relative error of
-c3sim.simulate_coresident against every c3_base_coresident row (grid search).
-Memory-bound GEMM scenarios (cfg4_mb) fit their own p_g. Then the comm-pacing
-exponent g (the penalty's excess scales with (paced rate / link rate)^g) is
-fitted on the paced rows (c3_base_coresident{c}_pace{pct}, comm_pace_gbps).
+collective CTA units beside it. The model (the same arithmetic as the
+runtime's predict_coresident) has three parameters:
+  p_g  the GEMM's slowdown beside the collective at its full unpaced rate;
+  p_c  the collective CTA's cost factor: c co-resident units move data like
+       c / p_c isolated units (t = curve(c / p_c));
+  g    the slowdown's excess scales with the collective's actual rate over its
+       unpaced rate, ratio = t_comm_full / t_collective, as ratio^g (pacing or
+       too few CTAs lower the collective's intensity beside the GEMM).
+A paced row's collective takes max(curve(c / p_c), bytes / pace). Per
+scenario the curve is the measured (CTA units, time) points plus the full-GPU
+time. (p_g, p_c, g) minimise the mean squared relative error of
+c3sim.simulate_coresident over every c3_base_coresident row, paced or not
+(grid search); memory-bound GEMM scenarios (cfg4_mb) refit p_g alone.
 
 usage: python tools/calibrate_coresident.py SWEEP.csv [SWEEP2.csv ...] OUT.json"""
 import csv
@@ -25,10 +28,11 @@ import c3sim  # noqa: E402
 
 CB, MB = c3sim.KernelClass.GEMM_COMPUTE_BOUND, c3sim.KernelClass.GEMM_MEMORY_BOUND
 SMS = 148
+N_RANKS = 8
 
 
 def load(paths):
-    """-> {(path, scenario, collective): {"tg", "tc", "curve", "rows": [(c, makespan)]}}"""
+    """-> {(path, scenario, collective): {tg, tc, mib, curve, rows: [(c, pace, makespan)]}}"""
     scen = {}
     for path in paths:
         for r in csv.DictReader(open(path)):
@@ -37,90 +41,70 @@ def load(paths):
             key = (path, r["scenario_id"], r["collective"])
             d = scen.setdefault(key, {"tg": float(r["t_gemm_iso_ms"]) * 1e-3,
                                       "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": [],
-                                      "paced": [], "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M"))})
+                                      "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M"))})
             c = int(r["cus_comm"])
             pace = float(r.get("comm_pace_gbps") or 0.0)
-            if pace > 0:
-                d["paced"].append((c, pace, float(r["makespan_s"])))
-                continue
-            if not r.get("t_comm_ctas_ms"):
-                continue
-            d["pts"][c] = float(r["t_comm_ctas_ms"]) * 1e-3
-            d["rows"].append((c, float(r["makespan_s"])))
-    for d in scen.values():
+            if pace <= 0 and r.get("t_comm_ctas_ms"):
+                d["pts"][c] = float(r["t_comm_ctas_ms"]) * 1e-3
+            d["rows"].append((c, pace, float(r["makespan_s"])))
+    out = {}
+    for key, d in scen.items():
         if not d["pts"]:
             continue
         pts = dict(d["pts"])
         pts[SMS] = min(d["tc"], min(pts.values()))
         cs = sorted(pts)
         d["curve"] = c3sim.CommCurve(cs, [pts[c] for c in cs])
-    return scen
+        out[key] = d
+    return out
 
 
-def error(scen, cls_of, pg, pc):
+def predict(d, c, pace, cls, p):
+    """The runtime's predict_coresident (runtime.cpp) on one row."""
+    t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p))
+    peer = (N_RANKS - 1) / N_RANKS * d["mib"] * 2 ** 20
+    link = peer / d["tc"] / 1e9
+    if 0 < pace < link:
+        t_at = max(t_at, peer / (pace * 1e9))
+    ratio = min(1.0, d["tc"] / t_at)
+    return c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls, p, ratio).makespan
+
+
+def error(scen, cls, pg, pc, g):
     p = c3sim.CoResidentParams()
     p.gemm_compute_bound = p.gemm_memory_bound = pg
-    p.comm = pc
+    p.comm, p.rate_exponent = pc, g
     err, n = 0.0, 0
-    for key, d in scen.items():
-        cls = cls_of(key)
-        for c, mk in d["rows"]:
-            t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p))
-            pred = c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls, p).makespan
-            err += ((pred - mk) / mk) ** 2
-            n += 1
-    return err / max(n, 1), n
-
-
-def fit(scen, cls_of):
-    best = None
-    for pc in [1.0 + 0.05 * i for i in range(41)]:        # 1.0 .. 3.0
-        for pg in [1.0 + 0.01 * i for i in range(61)]:    # 1.0 .. 1.6
-            e, n = error(scen, cls_of, pg, pc)
-            if best is None or e < best[0]:
-                best = (e, pg, pc, n)
-    return best
-
-
-def paced_error(scen, cls_of, pg, pc, gamma):
-    """Mean squared relative error of the paced rows under (pg, pc, gamma)."""
-    p = c3sim.CoResidentParams()
-    p.gemm_compute_bound = p.gemm_memory_bound = pg
-    p.comm, p.rate_exponent = pc, gamma
-    err, n = 0.0, 0
-    for key, d in scen.items():
-        peer = 7 / 8 * d["mib"] * 2 ** 20
-        link = peer / d["tc"] / 1e9  # GB/s of the unpaced collective
-        for c, pace, mk in d["paced"]:
-            ratio = min(1.0, pace / link)
-            t_at = max(d["curve"].time_at(c3sim.coresident_comm_ctas(c, p)), d["tc"] / ratio)
-            pred = c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls_of(key), p, ratio).makespan
-            err += ((pred - mk) / mk) ** 2
+    for d in scen.values():
+        for c, pace, mk in d["rows"]:
+            err += ((predict(d, c, pace, cls, p) - mk) / mk) ** 2
             n += 1
     return err / max(n, 1), n
 
 
 def main():
     *ins, out = sys.argv[1:]
-    scen = {k: v for k, v in load(ins).items() if "curve" in v}
+    scen = load(ins)
     is_mb = lambda key: key[1].startswith("cfg4_mb")  # noqa: E731  M=128: memory-bound GEMM
     cb = {k: v for k, v in scen.items() if not is_mb(k)}
     mb = {k: v for k, v in scen.items() if is_mb(k)}
-    e_cb, pg_cb, pc, n_cb = fit(cb, lambda k: CB)
-    # memory-bound: p_c shared (a property of the collective CTA), p_g refit
-    best_mb = min(((error(mb, lambda k: MB, pg, pc)[0], pg)
-                   for pg in [1.0 + 0.01 * i for i in range(61)]), default=(0.0, pg_cb))
-    gam, n_p = 1.0, 0
-    if any(d["paced"] for d in cb.values()):
-        best_g = min((paced_error(cb, lambda k: CB, pg_cb, pc, g)[0], g) for g in [0.5 + 0.25 * i for i in range(23)])
-        gam, n_p = best_g[1], paced_error(cb, lambda k: CB, pg_cb, pc, best_g[1])[1]
-        print(f"comm pacing: rate exponent {gam:.2f}, rms rel. error {best_g[0] ** 0.5:.3f} ({n_p} rows)")
+    best = None
+    for pc in [1.0 + 0.1 * i for i in range(21)]:             # 1.0 .. 3.0
+        for pg in [1.0 + 0.02 * i for i in range(31)]:        # 1.0 .. 1.6
+            for g in [0.5 * i for i in range(1, 9)]:          # 0.5 .. 4.0
+                e, n = error(cb, CB, pg, pc, g)
+                if best is None or e < best[0]:
+                    best = (e, pg, pc, g, n)
+    e_cb, pg_cb, pc, g, n_cb = best
+    best_mb = min(((error(mb, MB, pg, pc, g)[0], pg) for pg in [1.0 + 0.02 * i for i in range(31)]),
+                  default=(0.0, pg_cb))
     prm = c3sim.CoResidentParams()
-    prm.gemm_compute_bound, prm.comm, prm.rate_exponent = pg_cb, pc, gam
+    prm.gemm_compute_bound, prm.comm, prm.rate_exponent = pg_cb, pc, g
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     with open(out, "w") as f:
         f.write(c3sim.save_coresident_params(prm))
-    print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc:.2f}, rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows)")
+    print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc:.2f}, rate exponent {g:.2f}, "
+          f"rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows, paced and unpaced)")
     if mb:
         print(f"memory-bound:  p_g {best_mb[1]:.2f}, rms rel. error {best_mb[0] ** 0.5:.3f}")
     print(f"-> {out}")
