@@ -59,8 +59,9 @@ def test_choose_picks_coresident_from_the_curve(c3, session, cores_unit_comm):
     assert s.predict_alloc(st, a, 3.0, 1.0) == pytest.approx(want)
     # 16 CTAs: the collective takes 2 ms on them
     a.cus_comm = 16
+    # the collective's actual rate beside the GEMM is half its full rate here
     want16 = c3sim.simulate_coresident(3.0e-3, 2.0e-3, 1.0e-3, sms, 16,
-                                       c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
+                                       c3sim.KernelClass.GEMM_COMPUTE_BOUND, p, 0.5).makespan * 1e3
     assert s.predict_alloc(c3.C3_BASE, a, 3.0, 1.0) == pytest.approx(want16)
     # a plateau: 32 CTAs a hair faster than 24 -> still the fewest within 1%
     s.set_comm_curve([(8, 4.0), (24, 1.004), (32, 1.0), (sms, 1.0)])
@@ -79,8 +80,16 @@ def test_collective_cta_cost_factor_moves_the_pick(c3, session):
     s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
     st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
     cands = sorted({8, 16, 24, 32, 48, 64})
-    assert st == c3.C3_BASE
-    assert a.cus_comm == next(c for c in cands if round(c / pc) >= 24)
+    assert st == c3.C3_BASE and pc > 1.0
+    pred = {}
+    for c in cands:
+        x = s.default_alloc(c3.C3_BASE)
+        x.cus_gemm, x.cus_comm = sms, c
+        pred[c] = s.predict_alloc(c3.C3_BASE, x, 3.0, 1.0)
+    best = min(pred.values())
+    # the fewest CTA units whose prediction is within 1% of the best
+    assert a.cus_comm == next(c for c in cands if pred[c] <= best * 1.01)
+    assert round(a.cus_comm / pc) > 16  # the cost factor pushes the pick past the isolated plateau's 24 / p_c
 
 
 def test_partitioned_allocations_keep_the_reference_model(c3, session):
