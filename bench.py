@@ -356,6 +356,11 @@ def run_ours(args, dist):
         cands = [coresident(c3.SERIAL, full, nvl_ctas), coresident(c3.C3_BASE, full, nvl_ctas),
                  coresident(c3.C3_SP, full, nvl_ctas), coresident(c3.C3_RP, full - part, nvl_ctas),
                  coresident(c3.C3_SP_RP, full - part, nvl_ctas)]
+        # more co-resident CTA units: a co-resident unit moves less than an
+        # isolated one (the model's cost factor), so the rate-matched count is
+        # a floor, not the choice
+        for c in sorted({2 * nvl_ctas, 24, 32} - {nvl_ctas, co_ctas}):
+            cands.append(coresident(c3.C3_BASE, full, c))
         # B200 extension: the co-resident collective (the model's CTA count)
         # paced below the link rate, spread over 60% / 80% of the GEMM
         # (measured: 0.75 -> 0.93 of ideal on cfg2, profiles/r01_pace_probe.txt)
