@@ -50,6 +50,9 @@ struct CoResidentParams {
     double gemm_compute_bound = 1.0;
     double gemm_memory_bound = 1.0;
     double comm = 1.0;
+    /// The cost factor of the all-to-all class (all-to-all and reduce-scatter
+    /// kernels: one store per load, or n loads per store); 0 = `comm`.
+    double comm_all_to_all = 0.0;
     /// Comm pacing: the GEMM penalty's excess scales with the collective's
     /// rate as (rate / link rate)^rate_exponent; 1 = linear (pacing neutral),
     /// > 1 = spreading the collective over the GEMM pays.
@@ -58,17 +61,22 @@ struct CoResidentParams {
     double gemm(KernelClass gemm_class) const {
         return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
     }
+    double comm_factor(KernelClass comm_class) const {
+        return comm_class == KernelClass::AllToAll && comm_all_to_all > 0.0 ? comm_all_to_all : comm;
+    }
 };
 
 void validate(const CoResidentParams& p);
 
 /// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc,
-///        "rate-exponent": g (optional, default 1)}.
+///        "comm-all-to-all": pc (optional), "rate-exponent": g (optional, default 1)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 
-/// Isolated-equivalent CTA count of `cus_comm` co-resident collective CTAs.
-int coresident_comm_ctas(int cus_comm, const CoResidentParams& p);
+/// Isolated-equivalent CTA count of `cus_comm` co-resident collective CTAs
+/// of the given collective kernel class.
+int coresident_comm_ctas(int cus_comm, const CoResidentParams& p,
+                         KernelClass comm_class = KernelClass::AllGather);
 
 /// Two-phase fluid prediction of a co-resident run: GEMM on all CUs
 /// (t_gemm seconds alone), collective on cus_comm CTAs (t_comm_at_ctas =

@@ -1021,7 +1021,8 @@ double link_rate_gbps(const c3_session* s, double t_comm_cu_ms) {
 double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, double t_comm_cu_ms,
                           double pace_gbps = 0.0) {
     const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
-    const int eff = c3sim::coresident_comm_ctas(ctas, s->cores);
+    const int eff = c3sim::coresident_comm_ctas(ctas, s->cores,
+                                                c3sim::comm_kernel_class(s->scenario.collective.kind));
     double t_at = comm_ms_at(s, eff, t_comm_cu_ms);
     const double link = link_rate_gbps(s, t_comm_cu_ms);
     if (pace_gbps > 0.0 && pace_gbps < link) t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));

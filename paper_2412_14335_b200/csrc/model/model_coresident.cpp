@@ -51,6 +51,8 @@ SlowdownTable CommCurve::as_table(KernelClass cls, const MachineDescriptor& md) 
 void validate(const CoResidentParams& p) {
     for (double v : {p.gemm_compute_bound, p.gemm_memory_bound, p.comm})
         if (!(v >= 1.0) || !std::isfinite(v)) throw ValidationError("co-resident penalties must be finite and >= 1");
+    if (!(p.comm_all_to_all == 0.0 || (p.comm_all_to_all >= 1.0 && std::isfinite(p.comm_all_to_all))))
+        throw ValidationError("co-resident all-to-all cost factor must be 0 (= comm) or >= 1");
     if (!(p.rate_exponent > 0) || !std::isfinite(p.rate_exponent))
         throw ValidationError("co-resident rate exponent must be finite and > 0");
 }
@@ -72,6 +74,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.gemm_memory_bound = j.at("gemm-memory-bound").get<double>();
         p.comm = j.value("comm", 1.0);
         p.rate_exponent = j.value("rate-exponent", 1.0);
+        p.comm_all_to_all = j.value("comm-all-to-all", 0.0);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -83,13 +86,14 @@ std::string save_coresident_params(const CoResidentParams& p) {
     json j = {{"gemm-compute-bound", p.gemm_compute_bound},
               {"gemm-memory-bound", p.gemm_memory_bound},
               {"comm", p.comm},
+              {"comm-all-to-all", p.comm_all_to_all},
               {"rate-exponent", p.rate_exponent}};
     return j.dump(2) + "\n";
 }
 
-int coresident_comm_ctas(int cus_comm, const CoResidentParams& p) {
+int coresident_comm_ctas(int cus_comm, const CoResidentParams& p, KernelClass comm_class) {
     validate(p);
-    return std::max(1, static_cast<int>(std::lround(cus_comm / p.comm)));
+    return std::max(1, static_cast<int>(std::lround(cus_comm / p.comm_factor(comm_class))));
 }
 
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,

@@ -105,34 +105,45 @@ def test_shipped_coresident_params_load():
 
 
 def test_calibration_tool_recovers_known_parameters(tmp_path):
-    """tools/calibrate_coresident.py on a sweep CSV synthesised from the model
-    with known (p_g, p_c) recovers them (grid resolution 0.01 / 0.05)."""
+    """tools/calibrate_coresident.py on a sweep CSV synthesised with the
+    runtime's arithmetic from known (p_g, p_c all-gather, p_c all-to-all,
+    rate exponent) recovers them (grid resolution 0.02 / 0.1 / 0.1 / 0.5)."""
     import json
     import subprocess
+    sys.path.insert(0, os.path.join(REPO, "tools"))
+    import calibrate_coresident as cal
     p = c3sim.CoResidentParams()
-    p.gemm_compute_bound, p.gemm_memory_bound, p.comm = 1.12, 1.12, 1.5
+    p.gemm_compute_bound = p.gemm_memory_bound = 1.12
+    p.comm, p.comm_all_to_all, p.rate_exponent = 1.5, 2.0, 1.5
     hdr = ("scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
            "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
-           "predicted_makespan_s,t_comm_ctas_ms")
+           "predicted_makespan_s,t_comm_ctas_ms,comm_pace_gbps")
     rows = [hdr]
-    for sid, tg, tc in (("cfgA_1M", 2.4e-3, 1.1e-3), ("cfgB_1M", 9.0e-3, 2.0e-3), ("cfgC_1M", 2.5e-3, 0.6e-3)):
+    for sid, coll, tg, tc in (("cfgA_896M", "all-gather", 2.4e-3, 1.1e-3), ("cfgB_1664M", "all-gather", 9.0e-3, 2.0e-3),
+                              ("cfgC_896M", "all-to-all", 2.5e-3, 1.1e-3), ("cfgD_896M", "reduce-scatter", 2.4e-3, 1.0e-3)):
         # a link-bound collective: 1/ctas below 24 CTA units, flat from there
-        pts = {c: tc * max(1.0, 24.0 / c) for c in (8, 12, 16, 24, 32, 48, 64)}
-        curve = c3sim.CommCurve(sorted(pts) + [148], [pts[c] for c in sorted(pts)] + [tc])
+        pts = {c: tc * max(1.0, 24.0 / c) for c in (16, 24, 32, 48, 64)}
+        d = {"tg": tg, "tc": tc, "mib": float(sid.rsplit("_", 1)[1].rstrip("M")),
+             "ccls": c3sim.KernelClass.ALL_GATHER if coll == "all-gather" else c3sim.KernelClass.ALL_TO_ALL,
+             "curve": c3sim.CommCurve(sorted(pts) + [148], [pts[c] for c in sorted(pts)] + [tc])}
+        peer = 7 / 8 * d["mib"] * 2 ** 20
         for c in (16, 24, 32, 48, 64):
-            t_at = curve.time_at(c3sim.coresident_comm_ctas(c, p))
-            mk = c3sim.simulate_coresident(tg, t_at, tc, 148, c, CB, p).makespan
-            rows.append(f"{sid},all-gather,G-long,c3_base_coresident{c},{mk},1,1,0,{tg * 1e3},{tc * 1e3},"
-                        f"0,148,{c},CU,synthetic,nan,{pts[c] * 1e3}")
+            for pace in (0.0, peer / (0.8 * tg) / 1e9, peer / (0.6 * tg) / 1e9):
+                mk = cal.predict(d, c, pace, CB, p)
+                tag = "" if pace == 0 else f"_pace{int(pace)}"
+                rows.append(f"{sid},{coll},G-long,c3_base_coresident{c}{tag},{mk},1,1,0,{tg * 1e3},{tc * 1e3},"
+                            f"0,148,{c},CU,synthetic,nan,{pts[c] * 1e3 if pace == 0 else ''},{pace}")
     src = tmp_path / "sweep.csv"
     src.write_text("\n".join(rows) + "\n")
     out = tmp_path / "cores.json"
     r = subprocess.run([sys.executable, os.path.join(REPO, "tools", "calibrate_coresident.py"), str(src),
-                        str(out)], capture_output=True, text=True, timeout=300)
+                        str(out)], capture_output=True, text=True, timeout=600)
     assert r.returncode == 0, r.stderr
     got = json.loads(out.read_text())
     assert got["gemm-compute-bound"] == pytest.approx(1.12, abs=0.011)
     assert got["comm"] == pytest.approx(1.5, abs=0.051)
+    assert got["comm-all-to-all"] == pytest.approx(2.0, abs=0.051)
+    assert got["rate-exponent"] == pytest.approx(1.5, abs=0.01)
 
 
 def test_paced_collective_scales_the_gemm_penalty():

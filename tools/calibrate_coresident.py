@@ -7,7 +7,8 @@ collective CTA units beside it. The model (the same arithmetic as the
 runtime's predict_coresident) has three parameters:
   p_g  the GEMM's slowdown beside the collective at its full unpaced rate;
   p_c  the collective CTA's cost factor: c co-resident units move data like
-       c / p_c isolated units (t = curve(c / p_c));
+       c / p_c isolated units (t = curve(c / p_c)); fitted separately for the
+       all-gather kernel and the all-to-all class (all-to-all, reduce-scatter);
   g    the slowdown's excess scales with the collective's actual rate over its
        unpaced rate, ratio = t_comm_full / t_collective, as ratio^g (pacing or
        too few CTAs lower the collective's intensity beside the GEMM).
@@ -15,7 +16,8 @@ A paced row's collective takes max(curve(c / p_c), bytes / pace). Per
 scenario the curve is the measured (CTA units, time) points plus the full-GPU
 time. (p_g, p_c, g) minimise the mean squared relative error of
 c3sim.simulate_coresident over every c3_base_coresident row, paced or not
-(grid search); memory-bound GEMM scenarios (cfg4_mb) refit p_g alone.
+(grid search: for each (p_g, g) the two p_c are independent); memory-bound
+GEMM scenarios (cfg4_mb) refit p_g alone.
 
 usage: python tools/calibrate_coresident.py SWEEP.csv [SWEEP2.csv ...] OUT.json"""
 import csv
@@ -41,7 +43,9 @@ def load(paths):
             key = (path, r["scenario_id"], r["collective"])
             d = scen.setdefault(key, {"tg": float(r["t_gemm_iso_ms"]) * 1e-3,
                                       "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": [],
-                                      "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M"))})
+                                      "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M")),
+                                      "ccls": c3sim.KernelClass.ALL_GATHER if r["collective"] == "all-gather"
+                                      else c3sim.KernelClass.ALL_TO_ALL})
             c = int(r["cus_comm"])
             pace = float(r.get("comm_pace_gbps") or 0.0)
             if pace <= 0 and r.get("t_comm_ctas_ms"):
@@ -61,7 +65,7 @@ def load(paths):
 
 def predict(d, c, pace, cls, p):
     """The runtime's predict_coresident (runtime.cpp) on one row."""
-    t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p))
+    t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p, d["ccls"]))
     peer = (N_RANKS - 1) / N_RANKS * d["mib"] * 2 ** 20
     link = peer / d["tc"] / 1e9
     if 0 < pace < link:
@@ -70,10 +74,10 @@ def predict(d, c, pace, cls, p):
     return c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls, p, ratio).makespan
 
 
-def error(scen, cls, pg, pc, g):
+def error(scen, cls, pg, pc, g, pc_a2a=None):
     p = c3sim.CoResidentParams()
     p.gemm_compute_bound = p.gemm_memory_bound = pg
-    p.comm, p.rate_exponent = pc, g
+    p.comm, p.comm_all_to_all, p.rate_exponent = pc, pc if pc_a2a is None else pc_a2a, g
     err, n = 0.0, 0
     for d in scen.values():
         for c, pace, mk in d["rows"]:
@@ -88,22 +92,37 @@ def main():
     is_mb = lambda key: key[1].startswith("cfg4_mb")  # noqa: E731  M=128: memory-bound GEMM
     cb = {k: v for k, v in scen.items() if not is_mb(k)}
     mb = {k: v for k, v in scen.items() if is_mb(k)}
+    ag = {k: v for k, v in cb.items() if v["ccls"] == c3sim.KernelClass.ALL_GATHER}
+    a2a = {k: v for k, v in cb.items() if v["ccls"] != c3sim.KernelClass.ALL_GATHER}
+    pcs = [1.0 + 0.1 * i for i in range(21)]                   # 1.0 .. 3.0
     best = None
-    for pc in [1.0 + 0.1 * i for i in range(21)]:             # 1.0 .. 3.0
-        for pg in [1.0 + 0.02 * i for i in range(31)]:        # 1.0 .. 1.6
-            for g in [0.5 * i for i in range(1, 9)]:          # 0.5 .. 4.0
-                e, n = error(cb, CB, pg, pc, g)
-                if best is None or e < best[0]:
-                    best = (e, pg, pc, g, n)
-    e_cb, pg_cb, pc, g, n_cb = best
-    best_mb = min(((error(mb, MB, pg, pc, g)[0], pg) for pg in [1.0 + 0.02 * i for i in range(31)]),
+    for pg in [1.0 + 0.02 * i for i in range(31)]:            # 1.0 .. 1.6
+        for g in [0.5 * i for i in range(1, 9)]:              # 0.5 .. 4.0
+            tot, n, pcs_best = 0.0, 0, []
+            for group in (ag, a2a):
+                if not group:
+                    pcs_best.append(0.0)
+                    continue
+                e, pc, k = min((error(group, CB, pg, pc, g)[0], pc, error(group, CB, pg, pc, g)[1])
+                               for pc in pcs)
+                tot += e * k
+                n += k
+                pcs_best.append(pc)
+            if best is None or tot / n < best[0]:
+                best = (tot / n, pg, pcs_best[0], pcs_best[1], g, n)
+    e_cb, pg_cb, pc_ag, pc_a2a, g, n_cb = best
+    pc = pc_ag or pc_a2a
+    pc_a2a = pc_a2a or pc
+    best_mb = min(((error(mb, MB, pg, pc, g, pc_a2a)[0], pg) for pg in [1.0 + 0.02 * i for i in range(31)]),
                   default=(0.0, pg_cb))
     prm = c3sim.CoResidentParams()
     prm.gemm_compute_bound, prm.comm, prm.rate_exponent = pg_cb, pc, g
+    prm.comm_all_to_all = pc_a2a if pc_a2a and pc_a2a != pc else 0.0
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     with open(out, "w") as f:
         f.write(c3sim.save_coresident_params(prm))
-    print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc:.2f}, rate exponent {g:.2f}, "
+    print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc_ag:.2f} (all-gather) / {pc_a2a:.2f} (all-to-all class), "
+          f"rate exponent {g:.2f}, "
           f"rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows, paced and unpaced)")
     if mb:
         print(f"memory-bound:  p_g {best_mb[1]:.2f}, rms rel. error {best_mb[0] ** 0.5:.3f}")
