@@ -69,14 +69,17 @@ def test_choose_picks_coresident_from_the_curve(c3, session, cores_unit_comm):
     assert st == c3.C3_BASE and a.cus_comm == 24
 
 
-def test_collective_cta_cost_factor_moves_the_pick(c3, session):
-    """With the fitted cost factor p_c, c co-resident CTAs act like c / p_c
-    isolated ones: the pick is the fewest candidate CTAs reaching the plateau."""
+def test_collective_cta_cost_factor_moves_the_pick(c3, session, tmp_path):
+    """With a cost factor p_c > 1, c co-resident CTAs act like c / p_c
+    isolated ones: the pick is the fewest candidate CTAs within 1% of the best."""
     import c3sim
     w, s = session
     sms = w.info.sm_count
-    s.load_coresident(CORES)
-    pc = c3sim.load_coresident_params(CORES).comm
+    prm = c3sim.load_coresident_params(CORES)
+    prm.comm = pc = 1.6  # the all-gather kernel's factor for this session
+    f = tmp_path / "cores.json"
+    f.write_text(c3sim.save_coresident_params(prm))
+    s.load_coresident(str(f))
     s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
     st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
     cands = sorted({8, 16, 24, 32, 48, 64})
