@@ -183,6 +183,48 @@ public:
         return t;
     }
 
+    /// Link-rate emulation for loopback worlds (c3_session_set_link_rate); 0 = off.
+    void set_link_rate(double gbps) {
+        check_status(c3_session_set_link_rate(s_, gbps), "c3_session_set_link_rate");
+    }
+
+    /// The runtime heuristic's inputs: measured interference tables, co-run
+    /// penalties (optional) and the B200 co-residency parameters (optional).
+    void load_model(const std::string& tables_csv, const std::string& params_json = {},
+                    const std::string& coresident_json = {}) {
+        check_status(c3_session_load_tables(s_, tables_csv.c_str()), "c3_session_load_tables");
+        if (!params_json.empty())
+            check_status(c3_session_load_params(s_, params_json.c_str()), "c3_session_load_params");
+        if (!coresident_json.empty())
+            check_status(c3_session_load_coresident(s_, coresident_json.c_str()), "c3_session_load_coresident");
+    }
+
+    /// The collective's measured time (seconds) vs CTA units (co-residency model).
+    void set_comm_curve(const std::vector<std::pair<int, double>>& pts) {
+        std::vector<int> c;
+        std::vector<double> ms;
+        for (const auto& [ctas, sec] : pts) {
+            c.push_back(ctas);
+            ms.push_back(sec * 1e3);
+        }
+        check_status(c3_session_set_comm_curve(s_, c.data(), ms.data(), static_cast<int>(c.size())),
+                     "c3_session_set_comm_curve");
+    }
+
+    /// c3_session_choose on measured isolated times (seconds): the mode and
+    /// allocation the runtime heuristic picks, and its predicted makespan.
+    std::pair<ExecMode, c3_alloc> choose(double t_gemm, double t_comm, double t_comm_dma, bool allow_dma,
+                                         double* predicted = nullptr) {
+        int st = 0;
+        c3_alloc a{};
+        double pred_ms = 0;
+        check_status(c3_session_choose(s_, t_gemm * 1e3, t_comm * 1e3, t_comm_dma * 1e3, allow_dma ? 1 : 0,
+                                       &st, &a, &pred_ms),
+                     "c3_session_choose");
+        if (predicted) *predicted = pred_ms * 1e-3;
+        return {static_cast<ExecMode>(st), a};
+    }
+
 private:
     static int barrier_tramp(void* ctx) {
         try {
@@ -205,6 +247,8 @@ struct ExecOptions {
     /// Override the strategy's own allocation (allocate_cus semantics).
     bool use_alloc = false;
     c3_alloc alloc{};
+    /// Link-rate emulation of the (loopback) collective, GB/s per direction; 0 = off.
+    double link_gbps = 0.0;
 };
 
 struct ExecResult {
@@ -276,6 +320,7 @@ inline void measure_isolated(Session& s, C3Scenario& sc, const ExecOptions& o = 
 inline ExecResult execute(Session& s, const C3Scenario& sc, ExecMode mode, const ExecOptions& o = {}) {
     if (o.reps < 1 || o.warmup < 0) throw ValidationError("execute: reps >= 1 and warmup >= 0 required");
     if (o.fill) s.fill(o.seed);
+    s.set_link_rate(o.link_gbps);
     ExecResult res;
     res.scenario_id = sc.id;
     res.mode = mode;

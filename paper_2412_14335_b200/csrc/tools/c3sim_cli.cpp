@@ -314,16 +314,20 @@ int run_cmd(const Args& a) {
     C3Scenario sc = run_scenario(a);
     std::vector<ExecMode> modes;
     const std::string name = a.get("strategy", "all");
+    const bool autopick = name == "auto";
     if (name == "all") {
         for (Strategy s : kAllStrategies) modes.push_back(to_mode(s));
         modes.push_back(ExecMode::Fused);
-    } else {
+    } else if (!autopick) {
         modes.push_back(exec_mode_from_string(name));
     }
     ExecOptions o;
     o.warmup = std::stoi(a.get("warmup", "6"));
     o.reps = std::stoi(a.get("reps", "9"));
     o.seed = std::stoull(a.get("seed", "20241217"));
+    o.link_gbps = std::stod(a.get("link-gbps", "0"));
+    // explicit allocation (B200: --cus-gemm all SMs + --cus-comm c = co-resident)
+    const bool explicit_alloc = a.has("cus-gemm") || a.has("cus-comm") || a.has("comm-pace-gbps");
 
     // optional model side: predict every strategy from the measured isolated times
     std::optional<Inputs> model;
@@ -331,13 +335,57 @@ int run_cmd(const Args& a) {
 
     World world(0, sc.collective.n_ranks, std::stoi(a.get("device", "0")), /*loopback=*/true);
     Session session(world, sc);
+    std::optional<c3_alloc> picked;
+    if (autopick) {
+        // the runtime heuristic: measured isolated times and comm curve ->
+        // c3_session_choose (reference model + B200 co-residency) -> execute
+        if (!a.has("tables")) throw ValidationError("run --strategy auto needs --tables");
+        session.load_model(a.get("tables"), a.get("params", ""), a.get("coresident", ""));
+        session.fill(o.seed);
+        session.set_link_rate(o.link_gbps);
+        C3Scenario msc = sc;
+        ExecOptions mo = o;
+        measure_isolated(session, msc, mo);
+        std::vector<std::pair<int, double>> curve;
+        for (int c : {8, 16, 24, 32, 48, 64}) {
+            c3_alloc ca = session.default_alloc(ExecMode::CommOnlyCu);
+            ca.cus_comm = c;
+            std::vector<double> ts;
+            for (int r = 0; r < 3 + o.warmup; ++r) {
+                const c3_timing t = session.run(ExecMode::CommOnlyCu, &ca);
+                if (r >= o.warmup) ts.push_back((t.comm_end_ms - t.comm_start_ms) * 1e-3);
+            }
+            curve.emplace_back(c, detail::median(ts));
+        }
+        const int C = session.default_alloc(ExecMode::GemmOnly).cus_gemm;
+        const double tg = msc.gemm.measured_time.value(), tc = msc.collective.measured_time.value();
+        curve.emplace_back(C, std::min(tc, curve.back().second));
+        session.set_comm_curve(curve);
+        const auto [mode, alloc] = session.choose(tg, tc, 0.0, /*allow_dma=*/false);
+        std::cerr << "auto: picked " << to_string(mode) << " cus_gemm " << alloc.cus_gemm << " cus_comm "
+                  << alloc.cus_comm << " pace " << alloc.comm_pace_gbps << " GB/s\n";
+        modes.push_back(mode);
+        picked = alloc;
+        o.fill = false;
+    }
     std::ostringstream csv;
     csv << "scenario_id,collective,strategy,cus_gemm,cus_comm,backend,t_gemm_s,t_comm_s,t_comm_dma_s,"
-           "makespan_s,speedup,ideal,fraction_of_ideal,taxonomy,predicted_makespan_s,predicted_speedup\n";
+           "makespan_s,speedup,ideal,fraction_of_ideal,taxonomy,predicted_makespan_s,predicted_speedup,"
+           "comm_pace_gbps\n";
     json rows = json::array();
     for (ExecMode m : modes) {
         ExecResult r;
         try {
+            if (picked) {
+                o.use_alloc = true;
+                o.alloc = *picked;
+            } else if (explicit_alloc) {
+                o.use_alloc = true;
+                o.alloc = session.default_alloc(m);
+                if (a.has("cus-gemm")) o.alloc.cus_gemm = std::stoi(a.get("cus-gemm"));
+                if (a.has("cus-comm")) o.alloc.cus_comm = std::stoi(a.get("cus-comm"));
+                if (a.has("comm-pace-gbps")) o.alloc.comm_pace_gbps = std::stof(a.get("comm-pace-gbps"));
+            }
             r = execute(session, sc, m, o);
             o.fill = false;  // operands stay resident across strategies
         } catch (const ValidationError& e) {  // e.g. c3_fused on a shape without the pair GEMM
@@ -364,13 +412,15 @@ int run_cmd(const Args& a) {
             << r.gemm_ctas << ',' << r.comm_ctas << ',' << backend << ',' << g12(r.t_gemm) << ','
             << g12(r.t_comm) << ',' << g12(r.t_comm_dma) << ',' << g12(r.makespan) << ','
             << g12(r.speedup) << ',' << g12(r.ideal) << ',' << g12(r.fraction_of_ideal) << ','
-            << to_string(r.taxonomy) << ',' << pred_ms << ',' << pred_sp << '\n';
+            << to_string(r.taxonomy) << ',' << pred_ms << ',' << pred_sp << ',' << g12(r.alloc.comm_pace_gbps)
+            << '\n';
         json row = {{"scenario_id", sc.id}, {"collective", to_string(sc.collective.kind)},
                     {"strategy", to_string(m)}, {"cus_gemm", r.gemm_ctas}, {"cus_comm", r.comm_ctas},
                     {"backend", backend}, {"t_gemm_s", r.t_gemm}, {"t_comm_s", r.t_comm},
                     {"t_comm_dma_s", r.t_comm_dma}, {"makespan_s", r.makespan}, {"speedup", r.speedup},
                     {"ideal", r.ideal}, {"fraction_of_ideal", r.fraction_of_ideal},
-                    {"taxonomy", to_string(r.taxonomy)}, {"steps_s", r.steps}};
+                    {"taxonomy", to_string(r.taxonomy)}, {"steps_s", r.steps},
+                    {"comm_pace_gbps", r.alloc.comm_pace_gbps}};
         if (!pred_ms.empty()) row["predicted_makespan_s"] = pm;
         rows.push_back(row);
     }
@@ -385,7 +435,8 @@ void usage() {
                  "[--zero-interference] [subcommand options]\n"
                  "       c3sim run {--dataset FILE --scenario ID | --m M --n N --k K --ranks R "
                  "--payload-bytes P [--kind all-gather|all-to-all|reduce-scatter]} "
-                 "[--strategy NAME|all] [--warmup W] [--reps K] [--device D] "
+                 "[--strategy NAME|all|auto] [--cus-gemm N] [--cus-comm N] [--comm-pace-gbps X] "
+                 "[--link-gbps X] [--coresident FILE] [--warmup W] [--reps K] [--device D] "
                  "[--machine FILE --tables FILE [--params FILE]] [--format csv|structured-text] "
                  "[--out FILE]\n";
 }

@@ -152,3 +152,34 @@ def test_cli_run_executes_and_predicts(tmp_path):
         assert x["makespan_s"] > 0 and x["t_gemm_s"] > 0 and len(x["steps_s"]) == 3
         if x["strategy"] != "c3_fused":
             assert x["predicted_makespan_s"] > 0
+
+
+@pytest.mark.gpu
+def test_cli_run_auto_and_coresident(tmp_path):
+    """`c3sim run --strategy auto`: the runtime heuristic (measured isolated
+    times and comm curve -> c3_session_choose with the B200 co-residency
+    model) picks and executes; an explicit co-resident, paced allocation runs
+    too. Both at an emulated link rate."""
+    exe = os.path.join(REPO, "paper_2412_14335_b200", "bin", "c3sim")
+    base = [exe, "run", "--m", "2048", "--n", "4096", "--k", "2048", "--ranks", "8",
+            "--payload-bytes", str(64 << 20), "--warmup", "2", "--reps", "3", "--link-gbps", "300",
+            "--format", "structured-text"]
+    out = tmp_path / "auto.json"
+    r = subprocess.run(base + ["--strategy", "auto",
+                               "--tables", os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv"),
+                               "--params", os.path.join(REPO, "data", "b200-loopback-params.json"),
+                               "--coresident", os.path.join(REPO, "data", "b200-coresident.json"),
+                               "--out", str(out)], capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    assert "auto: picked" in r.stderr
+    rows = json.loads(out.read_text())
+    assert len(rows) == 1 and rows[0]["makespan_s"] > 0 and rows[0]["speedup"] > 0
+    out = tmp_path / "co.json"
+    r = subprocess.run(base + ["--strategy", "c3_base", "--cus-gemm", "148", "--cus-comm", "24",
+                               "--comm-pace-gbps", "150", "--out", str(out)],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    row = json.loads(out.read_text())[0]
+    assert row["cus_gemm"] == 148 and row["cus_comm"] == 24 and row["comm_pace_gbps"] == pytest.approx(150)
+    # serial = GEMM + the link-rate collective: (n-1)/n * P at 300 GB/s
+    assert row["t_comm_s"] == pytest.approx(7 / 8 * (64 << 20) / 300e9, rel=0.25)
