@@ -14,6 +14,7 @@
 #include <pybind11/stl/filesystem.h>
 
 #include <cstring>
+#include <optional>
 
 #include "c3sim/calibrate.hpp"
 #include "c3sim/conccl.hpp"
@@ -307,20 +308,33 @@ void add_exec(py::module_& m) {
     m.def(
         "execute",
         [](const cs::C3Scenario& sc, const py::object& strategy, cs::World& w, int warmup, int reps,
-           std::uint64_t seed, const py::object& allgather, const py::object& barrier) {
+           std::uint64_t seed, const py::object& allgather, const py::object& barrier, double link_gbps,
+           std::optional<int> cus_gemm, std::optional<int> cus_comm, std::optional<double> comm_pace_gbps) {
             cs::ExecOptions o;
             o.warmup = warmup;
             o.reps = reps;
             o.seed = seed;
+            o.link_gbps = link_gbps;
             auto t = transport_of(allgather, barrier);
             cs::Session s(w, sc, t.get());
-            return cs::execute(s, sc, mode_of(strategy), o);
+            const cs::ExecMode mode = mode_of(strategy);
+            if (cus_gemm || cus_comm || comm_pace_gbps) {
+                o.use_alloc = true;
+                o.alloc = s.default_alloc(mode);
+                if (cus_gemm) o.alloc.cus_gemm = *cus_gemm;
+                if (cus_comm) o.alloc.cus_comm = *cus_comm;
+                if (comm_pace_gbps) o.alloc.comm_pace_gbps = static_cast<float>(*comm_pace_gbps);
+            }
+            return cs::execute(s, sc, mode, o);
         },
         py::arg("scenario"), py::arg("strategy"), py::arg("world"), py::arg("warmup") = 6,
         py::arg("reps") = 9, py::arg("seed") = 20241217ull, py::arg("allgather") = py::none(),
-        py::arg("barrier") = py::none(),
+        py::arg("barrier") = py::none(), py::arg("link_gbps") = 0.0, py::arg("cus_gemm") = py::none(),
+        py::arg("cus_comm") = py::none(), py::arg("comm_pace_gbps") = py::none(),
         "Run the scenario on this GPU under a strategy (Strategy or name, incl. 'c3_fused'); "
-        "measured seconds and the reference's speedup arithmetic.");
+        "measured seconds and the reference's speedup arithmetic. B200 options: link_gbps "
+        "(NVLink-rate emulation of a loopback world), an explicit allocation (cus_gemm, cus_comm: "
+        "all SMs + c units = co-resident) and comm_pace_gbps (comm pacing).");
     m.def(
         "measure_isolated",
         [](cs::C3Scenario sc, cs::World& w, int warmup, int reps, const py::object& allgather,

@@ -135,6 +135,19 @@ def test_measure_isolated_feeds_the_model():
 
 
 @pytest.mark.gpu
+def test_execute_coresident_paced_at_link_rate():
+    """B200 options of execute(): the co-resident allocation (all SMs + c
+    collective units), comm pacing and NVLink-rate emulation."""
+    w = c3sim.World(0, 8, 0, True)
+    sc = _small_scenario(n=8)
+    r = c3sim.execute(sc, "c3_base", w, warmup=2, reps=3, link_gbps=200.0, cus_gemm=w.sm_count,
+                      cus_comm=16, comm_pace_gbps=100.0)
+    assert r.gemm_ctas == w.sm_count and r.comm_ctas == 16
+    assert r.t_comm == pytest.approx(7 / 8 * (16 << 20) / 200e9, rel=0.25)  # isolated at the link rate
+    assert r.makespan > 0
+
+
+@pytest.mark.gpu
 def test_cli_run_executes_and_predicts(tmp_path):
     out = tmp_path / "run.json"
     exe = os.path.join(REPO, "paper_2412_14335_b200", "bin", "c3sim")
