@@ -367,7 +367,8 @@ def run_ours(args, dist):
         for frac in (0.6, 0.8):
             p = pace_for(frac, t_g_pick, NVLINK_PEER_GBPS)
             if p > 0:
-                cands.append(coresident(c3.C3_BASE, full, co_ctas, p))
+                for c in sorted({co_ctas, 24}):  # 24 units paced: often the sweeps' best
+                    cands.append(coresident(c3.C3_BASE, full, c, p))
         if fused_ok:
             cands.append((c3.FUSED, sess.default_alloc(c3.FUSED)))
         return cands
