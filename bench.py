@@ -591,6 +591,11 @@ def run_ours(args, dist):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "concurrent_ms": e2e_conc, "gemm_ms": e2e_g, "comm_ms": e2e_c},
         "gpu_launches": launches,
+        # the north star's "1 GPU (GEMM only)" line: the isolated GEMM of the
+        # timed rounds (median), as time and TF/s against the measured peaks
+        "gemm_only": {"ms": t_g_timed, "tflops": flops / (t_g_timed * 1e-3) / 1e12,
+                      "frac_of_burst": flops / (t_g_timed * 1e-3) / 1e12 / peaks["bf16_tflops"],
+                      "frac_of_sustained": flops / (t_g_timed * 1e-3) / 1e12 / peak_sus},
         "clocks": clk,
     }
     if emulate:
