@@ -458,7 +458,9 @@ def run_ours(args, dist):
     rows = timed_rows["step"]
     step_ms = [r[0] for r in rows]
     gemm_ms = [r[1] for r in rows]
-    launches = int(sum(r[3] for r in rows))
+    # every launch of ours in the timed region: the C3 steps and the isolated
+    # GEMM / collective runs interleaved with them
+    launches = int(sum(r[3] for job in timed_rows.values() for r in job))
     t_g_timed = median([r[1] for r in timed_rows["gemm"]])
     t_c = median([r[col[comm_key]] for r in timed_rows[comm_key]])
     head_res = summarise(rows, t_g_timed, t_c, t_c)
