@@ -246,9 +246,10 @@ int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc,
 typedef int (*c3_barrier_fn)(void* ctx);
 /* C3_FUSED pacing: the copies of each CTA finish after this share of the
  * GEMM's operand loads (default 0 = as fast as possible); piece_bytes =
- * bytes per bulk copy (16..16384, multiple of 16, used up to the 8 KiB slot
- * size; default 8192: the copy warp's 16 KiB of shared memory is a ring of
- * 16 KiB / piece slots with loads running ahead of stores). piece_bytes = 0
+ * bytes per bulk copy (16..16384, multiple of 16, at most half the copy
+ * ring: 64 KiB beside the 512-wide GEMM, 16 KiB beside the 256-wide one;
+ * loads run ahead of stores). Default: 8 KiB for all-gather, 16 KiB for
+ * all-to-all. piece_bytes = 0
  * selects the LSU mode instead: the copy warp's 32 lanes move 16-byte vectors
  * with plain loads/stores, leaving the TMA unit to the GEMM (pace unused). */
 int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes);

@@ -60,11 +60,13 @@ constexpr uint32_t kEpiWarpStage = 32 * 128;
 // moves 48 KiB of operands per CTA for 2x the MMA work of a 256-wide tile
 // (64 KiB per 256x256x64 -> 48 KiB): 25% less L2->SM traffic, which under
 // the 1 kW power cap is clock (profiles/r01_ncu_gemm_vs_cublas.txt).
-template <int BN_>
+template <int BN_, bool FUSED_ = false>
 struct PairCfg {
     static constexpr int BN = BN_;
     static constexpr int HALVES = BN / 256;  // N=256 MMAs per k-step
-    static constexpr int STAGES = BN == 256 ? 6 : 4;
+    // fused 512-wide: one operand stage fewer buys the copy warp a 64 KiB ring
+    // (the fused all-to-all is latency-bound on its copy slots)
+    static constexpr int STAGES = BN == 256 ? 6 : (FUSED_ ? 3 : 4);
     static constexpr int ACC_BUFS = BN == 256 ? 2 : 1;
     // epilogue warps (one per TMEM lane quadrant; 8 = two per quadrant, each
     // half the columns, measured no faster for 512-wide tiles)
@@ -76,7 +78,9 @@ struct PairCfg {
     // buffers take the other's shared memory)
     static constexpr uint32_t EPI_SMEM = EPI_WARPS * kEpiWarpStage;
     static constexpr uint32_t SMEM = STAGES * STAGE + 1024 + 2 * EPI_SMEM + 512;
-    static constexpr uint32_t SMEM_FUSED = STAGES * STAGE + 1024 + EPI_SMEM + 512 + 2 * PIECE + 64;
+    // fused: the copy warp's slot ring after one staging tile per epilogue warp
+    static constexpr uint32_t COPY_BYTES = BN == 512 && FUSED_ ? 64 * 1024 : 2 * PIECE;
+    static constexpr uint32_t SMEM_FUSED = STAGES * STAGE + 1024 + EPI_SMEM + 512 + COPY_BYTES + 64;
     static_assert(SMEM <= 227 * 1024 && SMEM_FUSED <= 227 * 1024, "shared memory");
     static_assert(ACC_BUFS * BN <= static_cast<int>(TMEM_COLS), "TMEM");
     static_assert(BN / (EPI_WARPS / 4) % 128 == 0, "epilogue drains 128 columns per step");
@@ -115,12 +119,12 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
 // spread round-robin over the grid. AG: item = (rank v, piece j), one load,
 // n-1 stores; A2A: item = (v, dest q, piece j), one load, one store.
 constexpr int kFusedSlots = 8;
-__device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint64_t* lbar,
+__device__ void fused_copy_loop(const Params& p, uint8_t* buf, uint32_t buf_bytes, uint64_t* lbar,
                                 const uint32_t* progress, const volatile uint32_t* producer_done) {
     const FusedComm& fc = p.fc;
     const uint64_t pol = policy_evict_first();
-    const int64_t piece = fc.piece;  // <= PIECE
-    const int nb = static_cast<int>(min(static_cast<int64_t>(kFusedSlots), 2 * PIECE / piece));
+    const int64_t piece = fc.piece;  // <= buf_bytes / 2
+    const int nb = static_cast<int>(min(static_cast<int64_t>(kFusedSlots), static_cast<int64_t>(buf_bytes) / piece));
     const int64_t pieces = (fc.chunk + piece - 1) / piece;
     const int nv = fc.self_end - fc.self_begin;
     const int64_t per_v = fc.kind == 0 ? pieces : pieces * fc.n;
@@ -279,7 +283,7 @@ __global__ void __cluster_dims__(2, 1, 1) __maxnreg__(C3_PAIR_MAXNREG)
 gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                          const __grid_constant__ CUtensorMap map_b,
                          const __grid_constant__ CUtensorMap map_c, const Params p) {
-    using Cfg = PairCfg<BN_>;
+    using Cfg = PairCfg<BN_, FUSED>;
     constexpr int BN = Cfg::BN, STAGES = Cfg::STAGES, ACC_BUFS = Cfg::ACC_BUFS;
     constexpr uint32_t B_STAGE = Cfg::B_STAGE, STAGE = Cfg::STAGE;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -392,7 +396,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             if (p.fc.mode == 1)
                 fused_copy_loop_lsu(p, lane);
             else if (lane == 0)
-                fused_copy_loop(p, copy_buf, lbar, progress, producer_done);
+                fused_copy_loop(p, copy_buf, Cfg::COPY_BYTES, lbar, progress, producer_done);
         }
     } else if (warp == 1 && lane == 0 && leader) {
         // ------------- MMA issuer (leader only) -------------
@@ -414,7 +418,10 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 // One 512-column accumulator, released by the epilogue in
                 // 256-column halves: the first PRE k-blocks of the new tile
                 // accumulate into half 0 while half 1 is still being drained.
-                const int pre = p.k_blocks < p.pre_half ? p.k_blocks : p.pre_half;
+                // at most the ring's stages: the half-1 MMAs of these k-blocks
+                // release their stages, so more would wait on itself
+                const int pre_cap = p.pre_half < STAGES ? p.pre_half : STAGES;
+                const int pre = p.k_blocks < pre_cap ? p.k_blocks : pre_cap;
                 mbar_wait(&acc_empty[0], acc_phase ^ 1);
                 tc_fence_after();
                 int st = stage;
@@ -626,8 +633,10 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
 namespace {
 
 template <bool FUSED, int BN>
-int launch_pair(const GemmPlan* plan, const gemm2::Params& p, int grid, cudaStream_t stream) {
-    using Cfg = gemm2::PairCfg<BN>;
+int launch_pair(const GemmPlan* plan, gemm2::Params p, int grid, cudaStream_t stream) {
+    using Cfg = gemm2::PairCfg<BN, FUSED>;
+    // fused: bytes per bulk copy, at most half the copy ring (>= 2 slots)
+    if (FUSED) p.fc.piece = std::max<int64_t>(16, std::min<int64_t>(p.fc.piece, Cfg::COPY_BYTES / 2)) / 16 * 16;
     constexpr uint32_t smem = FUSED ? Cfg::SMEM_FUSED : Cfg::SMEM;
     static bool attr_done = false;
     if (!attr_done) {
@@ -685,7 +694,7 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
         p.fc = *fc;
         p.fc.link_cta_bpns = static_cast<float>(fc->link_bpns / grid);
-        p.fc.piece = std::max<int64_t>(16, std::min<int64_t>(fc->piece, gemm2::PIECE)) / 16 * 16;
+        p.fc.piece = fc->piece;  // clamped to the variant's copy ring in launch_pair
         return wide ? launch_pair<true, 512>(plan, p, grid, stream) : launch_pair<true, 256>(plan, p, grid, stream);
     }
     p.fc = FusedComm{};

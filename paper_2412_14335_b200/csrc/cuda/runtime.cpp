@@ -319,7 +319,7 @@ struct c3_session {
     uint32_t* done = nullptr;               // [0] AG counter, [1] RS counter
     uint32_t epoch = 0;
     float fused_pace = 0.0f;                // C3_FUSED: copies finish by this share of the GEMM (0 = unpaced)
-    int64_t fused_piece = 8192;             // C3_FUSED: bytes per bulk copy (the slot size)
+    int64_t fused_piece = 0;                // C3_FUSED: bytes per bulk copy; 0 = per collective (AG 8 KiB, A2A 16 KiB)
     int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
     double link_gbps = 0.0;                 // link emulation: peer-traffic budget per step (0 = off)
     double run_gbps = 0.0;                  // this run's pacing: link rate, or a concurrent run's comm pace
@@ -1359,7 +1359,9 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         fc.n = s->n;
         fc.chunk = s->chunk;
         fc.pace = s->fused_pace;
-        fc.piece = s->fused_piece;
+        // all-to-all moves one store per load: bigger pieces amortise the copy
+        // warp's per-item cost (profiles/r01_fused_probe_ring64.txt)
+        fc.piece = s->fused_piece > 0 ? s->fused_piece : (fc.kind == 0 ? 8192 : 16384);
         fc.mode = s->fused_mode;
         fc.link_bpns = s->run_gbps;
         const bool loop = w->loopback != 0;
