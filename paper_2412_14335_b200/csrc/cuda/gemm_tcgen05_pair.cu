@@ -96,8 +96,24 @@ struct Params {
     int group_m;
     int pol_a, pol_b;  // L2 policy of the A / B operand loads (policy_by_kind)
     int pre_half;      // BN 512: k-blocks into half 0 before waiting for half 1 (<= STAGES)
+    // BN 512 tail split: claims u < full_tiles are whole tiles; the last
+    // num_tiles - full_tiles tiles are claimed as two 256-column halves each
+    // (u in [full_tiles, num_units)), so an underfilled last wave takes half a
+    // tile's time. full_tiles = num_units = num_tiles when not split.
+    int full_tiles, num_units;
     FusedComm fc;  // only read by the FUSED instantiation
 };
+
+// claim u -> tile and half (-1 = the whole tile, 0/1 = its 256-column half)
+__device__ __forceinline__ void unit_tile(const Params& p, int u, int& tile, int& half) {
+    if (u < p.full_tiles) {
+        tile = u;
+        half = -1;
+    } else {
+        tile = p.full_tiles + (u - p.full_tiles) / 2;
+        half = (u - p.full_tiles) % 2;
+    }
+}
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
     const int band = p.group_m * p.tiles_n;
@@ -357,7 +373,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int r = i % RING;
             const uint32_t par = (i / RING) & 1;
             if (leader) {
-                if (tile >= p.num_tiles) tile = -1;
+                if (tile >= p.num_units) tile = -1;
                 mbar_wait(&tile_empty[r], par ^ 1);
                 tile_ring[r] = tile;
                 st_cluster_u32(mapa(smem_u32(&tile_ring[r]), 1), static_cast<uint32_t>(tile));
@@ -370,16 +386,19 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             }
             if (tile < 0) break;
             const int next = leader ? atomicAdd(p.tile_counter, 1) : 0;
-            int tm, tn;
-            tile_coords(p, tile, tm, tn);
+            int tm, tn, t_idx, half;
+            unit_tile(p, tile, t_idx, half);
+            tile_coords(p, t_idx, tm, tn);
             const int a_row = tm * BM + static_cast<int>(rank) * 128;
-            const int b_row = tn * BN + static_cast<int>(rank) * 128;  // + 256 per half
+            // + 256 per half; a half tile loads only its own 256 B rows, into slot 0
+            const int b_row = tn * BN + (half > 0 ? 256 : 0) + static_cast<int>(rank) * 128;
+            const int halves = half < 0 ? Cfg::HALVES : 1;
+            const uint32_t stage_tx = 2 * (A_STAGE + halves * B_HALF);
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
-                if (leader) mbar_arrive_expect_tx(&full[stage], 2 * STAGE);
+                if (leader) mbar_arrive_expect_tx(&full[stage], stage_tx);
                 tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, pol_a);
-#pragma unroll
-                for (int h = 0; h < Cfg::HALVES; ++h)
+                for (int h = 0; h < halves; ++h)
                     tma_load_2d_pair(smem_b + stage * B_STAGE + h * B_HALF, &map_b, &full[stage], kb * BK,
                                      b_row + h * 256, pol_b);
                 if (FUSED) st_volatile_shared(progress, ld_volatile_shared(progress) + 1);
@@ -412,9 +431,16 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int tile = tile_ring[r];
             mbar_arrive(&tile_empty[r]);
             if (tile < 0) break;
+            int t_idx, half;
+            unit_tile(p, tile, t_idx, half);
+            const int halves = half < 0 ? Cfg::HALVES : 1;  // a half tile: one N=256 MMA per k-step
             const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
             int kb0 = 0;
-            if constexpr (Cfg::HALVES == 2) {
+            if (Cfg::HALVES == 2 && half >= 0) {
+                mbar_wait(&acc_empty[0], acc_phase ^ 1);
+                mbar_wait(&acc_empty[1], acc_phase ^ 1);
+                tc_fence_after();
+            } else if constexpr (Cfg::HALVES == 2) {
                 // One 512-column accumulator, released by the epilogue in
                 // 256-column halves: the first PRE k-blocks of the new tile
                 // accumulate into half 0 while half 1 is still being drained.
@@ -465,8 +491,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 const uint32_t b_addr = b0 + stage * B_STAGE;
 #pragma unroll
                 for (int k = 0; k < BK / UK; ++k)
-#pragma unroll
-                    for (int h = 0; h < Cfg::HALVES; ++h)
+                    for (int h = 0; h < halves; ++h)
                         umma_bf16_pair(d_tmem + h * 256, smem_desc_k_sw128(a_addr + k * UK * 2),
                                        smem_desc_k_sw128(b_addr + h * B_HALF + k * UK * 2), idesc,
                                        (kb | k) != 0);
@@ -509,8 +534,11 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 if (lane == 0) bulk_wait_all();  // this warp's C stores complete
                 break;
             }
-            int tm, tn;
-            tile_coords(p, tile, tm, tn);
+            int tm, tn, t_idx, half;
+            unit_tile(p, tile, t_idx, half);
+            tile_coords(p, t_idx, tm, tn);
+            const int cols = half < 0 ? COLS : 256;  // a half tile fills accumulator columns 0-255
+            const int col_base = tn * BN + (half > 0 ? 256 : 0);
             mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
             // TMEM row `lane` of this warp's quadrant -> packed bf16 -> the
@@ -541,7 +569,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 fence_proxy_async_shared();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&map_c, stg, tn * BN + c, row0);
+                    tma_store_2d(&map_c, stg, col_base + c, row0);
                     bulk_commit();
                 }
                 if (++stg_i == EPI_BUFS) stg_i = 0;
@@ -571,7 +599,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                         }
                     }
                 }
-                const bool last = c + 128 >= c_begin + COLS;
+                const bool last = c + 128 >= c_begin + cols;
                 if (!last) {
                     tmem_ld_32x32b_x32(t_row + c + 128, va0);
                     tmem_ld_32x32b_x32(t_row + c + 160, va1);
@@ -690,6 +718,21 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
     p.pre_half = pre_half;
 
     const bool wide = plan->kind == GemmPlan::kPair512;
+    // tail split (512-wide): if the last wave is at most half full, its tiles
+    // are claimed as 256-column halves (C3_GEMM_TAILSPLIT=0 turns it off, dev A/B)
+    p.full_tiles = p.num_units = p.num_tiles;
+    static const bool tail_split = [] {
+        const char* e = std::getenv("C3_GEMM_TAILSPLIT");
+        return !(e != nullptr && std::string(e) == "0");
+    }();
+    if (wide && tail_split) {
+        const int pairs = grid / 2;
+        const int rem = pairs > 0 ? p.num_tiles % pairs : 0;
+        if (rem > 0 && 2 * rem <= pairs) {
+            p.full_tiles = p.num_tiles - rem;
+            p.num_units = p.num_tiles + rem;
+        }
+    }
     if (fc) {
         if (fc->chunk % 16 != 0) return set_error(C3_ERR_VALIDATION, "fused C3: slot bytes must be 16-byte multiples");
         p.fc = *fc;

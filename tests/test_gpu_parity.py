@@ -480,3 +480,32 @@ def test_comm_pace_in_concurrent_runs(torch_mod, c3, collective):
     assert fast < 0.5 * target_ms
     s.close()
     w.close()
+
+
+def test_pair512_tail_split_matches_256_wide(torch_mod, c3, monkeypatch):
+    """cfg2's GEMM on the 512-wide pair kernel claims its underfilled last
+    wave as 256-column halves (1792 tiles on 74 pairs: 16 tiles split); the
+    result is bit-identical to the 256-wide pair kernel (same per-element K
+    order), and within the bf16 bar at sampled entries."""
+    torch = torch_mod
+    M, N, K = 8192, 28672, 8192
+    w = c3.World()
+    A = torch.empty(M * K, dtype=torch.int16, device="cuda")
+    B = torch.empty(N * K, dtype=torch.int16, device="cuda")
+    c3.check(c3.lib().c3_fill_bf16(A.data_ptr(), M * K, SEED, 0, 0, None))
+    c3.check(c3.lib().c3_fill_bf16(B.data_ptr(), N * K, SEED, 0, 1, None))
+    out = {}
+    for kernel in ("pair512", "pair"):
+        monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
+        C_ = torch.zeros(M * N, dtype=torch.int16, device="cuda")
+        w.gemm(A.data_ptr(), B.data_ptr(), C_.data_ptr(), M, N, K, 0)
+        torch.cuda.synchronize()
+        out[kernel] = C_
+    assert torch.equal(out["pair512"], out["pair"])
+    # the split tiles are the last 16 of the raster: check their columns' region
+    rng = np.random.default_rng(5)
+    rows = rng.integers(0, M, 1024)
+    cols = rng.integers(N - 4096, N, 1024)
+    gemm_check(out["pair512"].cpu().numpy().view(np.uint16), orc.bf16(M * K, SEED, 0, 0),
+               orc.bf16(N * K, SEED, 0, 1), M, N, K, rows, cols)
+    w.close()
