@@ -363,8 +363,9 @@ def run_ours(args, dist):
             cands.append(coresident(c3.C3_BASE, full, c))
         # B200 extension: the co-resident collective (the model's CTA count)
         # paced below the link rate, spread over 60% / 80% of the GEMM
-        # (measured: 0.75 -> 0.93 of ideal on cfg2, profiles/r01_pace_probe.txt)
-        for frac in (0.6, 0.8):
+        # (measured: 0.75 -> 0.93 of ideal on cfg2, profiles/r01_pace_probe.txt),
+        # over 60% / 80% / 90% of the GEMM
+        for frac in (0.6, 0.8, 0.9):
             p = pace_for(frac, t_g_pick, NVLINK_PEER_GBPS)
             if p > 0:
                 for c in sorted({co_ctas, 24}):  # 24 units paced: often the sweeps' best
