@@ -54,19 +54,23 @@ def _view(ptr, nbytes):
     return torch.as_tensor(_A(ptr, nbytes), device="cuda")
 
 
-def test_allgather_896mib_coresident_with_cfg2_gemm(c3):
+@pytest.mark.parametrize("M,Nn,K,payload,pace", [(8192, 28672, 8192, PAYLOAD, 0.0),
+                                                   (8192, 53248, 16384, 1664 << 20, 250.0)],
+                         ids=["cfg2", "cfg4-paced"])
+def test_allgather_full_size_coresident_with_gemm(c3, M, Nn, K, payload, pace):
+    """cfg2 (896 MiB) and cfg4 (LLaMA-405B, 1664 MiB, the collective paced
+    below the link rate) all-gathers, co-resident beside their GEMMs."""
     w = c3.World(0, N, 0, loopback=True)
-    M, Nn, K = 8192, 28672, 8192
-    s = c3.Session(w, M, Nn, K, c3.ALL_GATHER, PAYLOAD)
+    s = c3.Session(w, M, Nn, K, c3.ALL_GATHER, payload)
     s.fill(SEED)
     a = s.default_alloc(c3.C3_BASE)
-    a.cus_gemm, a.cus_comm = w.info.sm_count, 24
+    a.cus_gemm, a.cus_comm, a.comm_pace_gbps = w.info.sm_count, 24, pace
     s.run(c3.C3_BASE, a, all_ranks=True)
-    chunk = PAYLOAD // N
-    got0 = _d2h(c3, s.pointers(0).recv, PAYLOAD)
+    chunk = payload // N
+    got0 = _d2h(c3, s.pointers(0).recv, payload)
     assert np.array_equal(got0, orc.expected_allgather(N, chunk, SEED, 2))
     for v in range(1, N):
-        assert _dev_equal(c3, s.pointers(v).recv, s.pointers(0).recv, PAYLOAD), f"rank {v}"
+        assert _dev_equal(c3, s.pointers(v).recv, s.pointers(0).recv, payload), f"rank {v}"
     # the GEMM that ran beside it: sampled entries against the fp64 definition
     rng = np.random.default_rng(7)
     rows = rng.integers(0, M, 2048)
