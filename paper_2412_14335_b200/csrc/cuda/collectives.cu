@@ -97,46 +97,45 @@ __device__ void entry_barrier(const Signals& sig, int self, int n, int slot_base
 // entry, [16,24) reduce-scatter exit, [24,32) copy-engine exit.
 constexpr int kAgExit = 0, kRsEntry = 8, kRsExit = 16;
 
+// V: the access width (uint4 = 16 B, u256 = 32 B: LDG/STG .256), U: vectors
+// in flight per thread; nvec / slot_vec count V-sized vectors.
+template <typename V, int U>
 __global__ void __launch_bounds__(kVecThreads)
-ag_push_vec_kernel(const uint4* __restrict__ src, MutPtrTable recv, int self, int n,
+ag_push_vec_kernel(const V* __restrict__ src, MutPtrTable recv, int self, int n,
                    int64_t nvec, int64_t slot_vec, int copy_self, int stream_l2, float cta_bpns,
                    Signals sig) {
     const uint64_t pol = policy_evict_first();
-    uint4* dst[C3_MAX_RANKS];
+    V* dst[C3_MAX_RANKS];
 #pragma unroll
     for (int j = 0; j < C3_MAX_RANKS; ++j)
-        dst[j] = j < n ? static_cast<uint4*>(recv.p[j]) + slot_vec * self : nullptr;
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnrollAg;
+        dst[j] = j < n ? static_cast<V*>(recv.p[j]) + slot_vec * self : nullptr;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * U;
     const uint64_t t0 = global_ns();
     double sent = 0.0;  // peer bytes this CTA has pushed (pacing)
-    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnrollAg; blk < nvec; blk += step) {
+    for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * U; blk < nvec; blk += step) {
         if (cta_bpns > 0.f) {
             if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
             __syncthreads();
             const int64_t left = nvec - blk;
-            sent += 16.0 * (n - 1) * static_cast<double>(left < kVecThreads * kUnrollAg ? left : kVecThreads * kUnrollAg);
+            sent += static_cast<double>(sizeof(V)) * (n - 1) *
+                    static_cast<double>(left < kVecThreads * U ? left : kVecThreads * U);
         }
         const int64_t base = blk + threadIdx.x;
-        uint4 v[kUnrollAg];
+        V v[U];
 #pragma unroll
-        for (int u = 0; u < kUnrollAg; ++u) {
+        for (int u = 0; u < U; ++u) {
             const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
-            if (i < nvec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
+            if (i < nvec) v[u] = ld_vec(src + i, stream_l2 != 0, pol);
         }
         // peers in rotated order so the ranks do not all start on the same target
         for (int j = 1; j <= n; ++j) {
             const int p = (self + j) % n;
             if (p == self && !copy_self) continue;
-            uint4* d = dst[p];
+            V* d = dst[p];
 #pragma unroll
-            for (int u = 0; u < kUnrollAg; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
-                if (i < nvec) {
-                    if (stream_l2)
-                        st_stream_v4(d + i, v[u], pol);
-                    else
-                        st_v4(d + i, v[u]);
-                }
+                if (i < nvec) st_vec(d + i, v[u], stream_l2 != 0, pol);
             }
         }
     }
@@ -222,41 +221,37 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
 
 // All-to-all, push form (plan_all_to_all's mapping, conccl.cpp:55-84): slot p
 // of rank `self`'s send buffer goes to slot `self` of rank p's receive buffer.
+template <typename V, int U>
 __global__ void __launch_bounds__(kVecThreads)
-a2a_push_vec_kernel(const uint4* __restrict__ send, MutPtrTable recv, int self, int n,
+a2a_push_vec_kernel(const V* __restrict__ send, MutPtrTable recv, int self, int n,
                     int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
-    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * kUnrollA2a;
+    const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * U;
     const uint64_t t0 = global_ns();
     double sent = 0.0;
     for (int j = 0; j < n; ++j) {
         const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
-        const uint4* src = send + slot_vec * p;
-        uint4* dst = static_cast<uint4*>(recv.p[p]) + slot_vec * self;
-        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * kUnrollA2a; blk < slot_vec;
-             blk += step) {
+        const V* src = send + slot_vec * p;
+        V* dst = static_cast<V*>(recv.p[p]) + slot_vec * self;
+        for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * U; blk < slot_vec; blk += step) {
             if (cta_bpns > 0.f && p != self) {
                 if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
                 __syncthreads();
                 const int64_t left = slot_vec - blk;
-                sent += 16.0 * static_cast<double>(left < kVecThreads * kUnrollA2a ? left : kVecThreads * kUnrollA2a);
+                sent += static_cast<double>(sizeof(V)) *
+                        static_cast<double>(left < kVecThreads * U ? left : kVecThreads * U);
             }
             const int64_t base = blk + threadIdx.x;
-            uint4 v[kUnrollA2a];
+            V v[U];
 #pragma unroll
-            for (int u = 0; u < kUnrollA2a; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
-                if (i < slot_vec) v[u] = stream_l2 ? ld_stream_v4(src + i, pol) : ld_nc_v4(src + i);
+                if (i < slot_vec) v[u] = ld_vec(src + i, stream_l2 != 0, pol);
             }
 #pragma unroll
-            for (int u = 0; u < kUnrollA2a; ++u) {
+            for (int u = 0; u < U; ++u) {
                 const int64_t i = base + static_cast<int64_t>(u) * kVecThreads;
-                if (i < slot_vec) {
-                    if (stream_l2)
-                        st_stream_v4(dst + i, v[u], pol);
-                    else
-                        st_v4(dst + i, v[u]);
-                }
+                if (i < slot_vec) st_vec(dst + i, v[u], stream_l2 != 0, pol);
             }
         }
     }
@@ -418,6 +413,17 @@ const BulkCfg& bulk_cfg() {
     return c;
 }
 
+// 32-byte (LDG/STG .256) vectors in the all-gather push when aligned: the
+// same bytes in flight with half the instructions (co-resident cfg2 0.78-0.82
+// -> 0.83-0.84 of ideal); C3_COMM_WIDE=0 keeps 16-byte vectors (dev A/B).
+bool wide_vectors() {
+    static const bool on = [] {
+        const char* e = std::getenv("C3_COMM_WIDE");
+        return !(e != nullptr && std::string(e) == "0");
+    }();
+    return on;
+}
+
 int grid_for(int64_t work_items, int threads, int cap) {
     const int64_t g = (work_items + threads - 1) / threads;
     return static_cast<int>(std::max<int64_t>(1, std::min<int64_t>(g, cap)));
@@ -451,13 +457,19 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
                                                         chunk_bytes, in_place ? 0 : 1, bc.piece, bc.nbuf,
                                                         stream_l2_enabled(),
                                                         static_cast<float>(link_bpns / grid), sig);
+    } else if ((align & 31) == 0 && wide_vectors()) {
+        // 32-byte vectors, half as many in flight per thread: the same bytes, half the instructions
+        const int64_t nvec = chunk_bytes / 32;
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * (kUnrollAg / 2), n_ctas * kCtasPerUnit);
+        ag_push_vec_kernel<u256, kUnrollAg / 2><<<grid, kVecThreads, 0, stream>>>(
+            static_cast<const u256*>(send), recv, self, n, nvec, nvec, in_place ? 0 : 1, stream_l2_enabled(),
+            static_cast<float>(link_bpns / grid), sig);
     } else if ((align & 15) == 0) {
         const int64_t nvec = chunk_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnrollAg, n_ctas * kCtasPerUnit);
-        ag_push_vec_kernel<<<grid, kVecThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
-                                                         n, nvec, nvec, in_place ? 0 : 1,
-                                                         stream_l2_enabled(),
-                                                         static_cast<float>(link_bpns / grid), sig);
+        ag_push_vec_kernel<uint4, kUnrollAg><<<grid, kVecThreads, 0, stream>>>(
+            static_cast<const uint4*>(send), recv, self, n, nvec, nvec, in_place ? 0 : 1, stream_l2_enabled(),
+            static_cast<float>(link_bpns / grid), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(chunk_bytes, 1), kThreads, n_ctas);
         ag_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
@@ -477,12 +489,24 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
     if (per_peer_bytes == 0 && !sig.enabled) return C3_OK;
     uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(per_peer_bytes);
     for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
-    if ((align & 15) == 0) {
+    // all-to-all keeps 16-byte vectors by default: 32-byte ones were faster
+    // alone but slower beside the GEMM (0.72 vs 0.80 of ideal, profiles/r01_comm_wide.txt)
+    static const bool wide_a2a = [] {
+        const char* e = std::getenv("C3_COMM_WIDE_A2A");
+        return e != nullptr && std::string(e) == "1";
+    }();
+    if ((align & 31) == 0 && wide_a2a && wide_vectors()) {
+        const int64_t nvec = per_peer_bytes / 32;
+        const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * (kUnrollA2a / 2), n_ctas * kCtasPerUnit);
+        a2a_push_vec_kernel<u256, kUnrollA2a / 2><<<grid, kVecThreads, 0, stream>>>(
+            static_cast<const u256*>(send), recv, self, n, nvec, stream_l2_enabled(),
+            static_cast<float>(link_bpns / grid), sig);
+    } else if ((align & 15) == 0) {
         const int64_t nvec = per_peer_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnrollA2a, n_ctas * kCtasPerUnit);
-        a2a_push_vec_kernel<<<grid, kVecThreads, 0, stream>>>(static_cast<const uint4*>(send), recv, self,
-                                                          n, nvec, stream_l2_enabled(),
-                                                          static_cast<float>(link_bpns / grid), sig);
+        a2a_push_vec_kernel<uint4, kUnrollA2a><<<grid, kVecThreads, 0, stream>>>(
+            static_cast<const uint4*>(send), recv, self, n, nvec, stream_l2_enabled(),
+            static_cast<float>(link_bpns / grid), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(per_peer_bytes, 1), kThreads, n_ctas);
         a2a_push_byte_kernel<<<grid, kThreads, 0, stream>>>(static_cast<const uint8_t*>(send), recv,
