@@ -497,28 +497,30 @@ def run_ours(args, dist):
     L = c3.lib()
 
     def e2e_step(strategy, alloc, rate=0.0):
+        # one step through the host-buffer C ABI call (c3_session_run_host):
+        # A and this rank's collective input copied in from pinned host memory,
+        # the result's first bytes read back, all inside the call
         sess.set_link_rate(rate)
         t0 = time.perf_counter()
-        c3.check(L.c3_memcpy(p.a, pin_a.data_ptr(), p.a_bytes, 1, None))
-        c3.check(L.c3_memcpy(p.send, pin_s.data_ptr(), p.send_bytes, 1, None))
-        c3.check(L.c3_stream_sync(None))
-        sess.run(strategy, alloc)
-        c3.check(L.c3_memcpy(pin_o.data_ptr(), p.c, d2h, 2, None))
-        c3.check(L.c3_stream_sync(None))
+        sess.run_host(strategy, alloc, pin_a.data_ptr(), pin_s.data_ptr(), pin_o.data_ptr(), d2h)
         return (time.perf_counter() - t0) * 1e3
 
+    # serial on host buffers: copies in, GEMM, the collective on the isolated
+    # run's CTAs and rate, result out -- one stream, nothing overlapped
+    ser_alloc = sess.default_alloc(c3.SERIAL)
+    ser_alloc.cus_gemm = full
+    ser_alloc.cus_comm = head_iso["cu"][1].cus_comm if "cu" in head_iso else 32
     for _ in range(2):
         e2e_step(head, head_alloc, link)
-    e2e = {"conc": [], "gemm": [], "comm": []}
-    e2e_jobs = {"conc": (head, head_alloc, link), "gemm": head_iso["gemm"], "comm": head_iso[comm_key]}
+        e2e_step(c3.SERIAL, ser_alloc, link)
+    e2e = {"conc": [], "serial": []}
+    e2e_jobs = {"conc": (head, head_alloc, link), "serial": (c3.SERIAL, ser_alloc, link)}
     names = list(e2e_jobs)
-    for r in range(K):  # interleaved, rotated, like the device-timed rounds
-        for k in names[r % 3:] + names[:r % 3]:
+    for r in range(K):  # interleaved, alternating order
+        for k in names[r % 2:] + names[:r % 2]:
             e2e[k].append(e2e_step(*e2e_jobs[k]))
-    e2e_conc, e2e_g, e2e_c = (median(dist.max_list(e2e[k])) for k in ("conc", "gemm", "comm"))
-    # serial e2e = inputs in, GEMM, collective, result out (copies counted once)
-    io_ms = e2e_g - t_g_timed
-    e2e_speedup = (e2e_g + e2e_c - io_ms) / e2e_conc
+    e2e_conc, e2e_ser = (median(dist.max_list(e2e[k])) for k in ("conc", "serial"))
+    e2e_speedup = e2e_ser / e2e_conc
 
     peaks, peak_src = load_peaks()
     peak_sus = peaks.get("bf16_tflops_sustained", PEAKS_FALLBACK["bf16_tflops_sustained"])
@@ -592,7 +594,9 @@ def run_ours(args, dist):
         "roofline": roofline,
         "e2e": {"value": e2e_speedup, "unit": "x (t_serial / t_concurrent, host buffers)",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                "concurrent_ms": e2e_conc, "gemm_ms": e2e_g, "comm_ms": e2e_c},
+                "concurrent_ms": e2e_conc, "serial_ms": e2e_ser,
+                "call": "c3_session_run_host (pinned host A and collective input in, 4 KiB of C out; "
+                        "concurrent strategies overlap the second input copy with the first kernel)"},
         "gpu_launches": launches,
         # the north star's "1 GPU (GEMM only)" line: the isolated GEMM of the
         # timed rounds (median), as time and TF/s against the measured peaks

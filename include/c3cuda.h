@@ -234,6 +234,16 @@ int c3_session_export(c3_session* s, void* blob_out);
 int c3_session_import(c3_session* s, const void* all_blobs);
 /* One C3 step (synchronous on the host at the end; device-event timed). */
 int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);
+/* One C3 step on HOST buffers (the end-to-end call): the step's inputs are
+ * copied in from host memory (pinned for overlap) and the first `out_bytes`
+ * of C copied back, all inside the step and its timing. `host_a` is A
+ * (M x K bf16), `host_send` this rank's collective input (the `send` /
+ * `send_bytes` of c3_session_pointers); either may be NULL to keep the device
+ * contents. Concurrent strategies copy the first-launched kernel's input
+ * first and overlap the second copy with that kernel; serial and fused copy
+ * both before the GEMM. */
+int c3_session_run_host(c3_session* s, int strategy, const c3_alloc* alloc, const void* host_a,
+                        const void* host_send, void* host_out, int64_t out_bytes, c3_timing* out);
 /* Loopback parity form: every virtual rank's share of the collective runs (the
  * plain call runs rank 0's share only, the per-GPU load of a real world). */
 int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);

@@ -183,6 +183,17 @@ public:
         return t;
     }
 
+    /// One step on host buffers (c3_session_run_host): A and this rank's
+    /// collective input copied in, the first out_bytes of C copied back.
+    c3_timing run_host(ExecMode m, const c3_alloc* alloc, const void* host_a, const void* host_send,
+                       void* host_out, std::int64_t out_bytes) {
+        c3_timing t{};
+        check_status(c3_session_run_host(s_, static_cast<int>(m), alloc, host_a, host_send, host_out,
+                                         out_bytes, &t),
+                     "c3_session_run_host");
+        return t;
+    }
+
     /// Link-rate emulation for loopback worlds (c3_session_set_link_rate); 0 = off.
     void set_link_rate(double gbps) {
         check_status(c3_session_set_link_rate(s_, gbps), "c3_session_set_link_rate");

@@ -215,3 +215,12 @@ class Session:
         fn = lib().c3_session_run_all_ranks if all_ranks else lib().c3_session_run
         check(fn(self.h, strategy, C.byref(alloc) if alloc is not None else None, C.byref(t)))
         return t
+
+    def run_host(self, strategy, alloc, host_a, host_send, host_out=None, out_bytes=0):
+        """One step on host buffers (c3_session_run_host): raw host addresses
+        (ints, pinned memory for overlap) or None for A / the collective input /
+        the result read-back."""
+        t = _capi.Timing()
+        check(lib().c3_session_run_host(self.h, strategy, C.byref(alloc) if alloc is not None else None,
+                                        host_a, host_send, host_out, out_bytes, C.byref(t)))
+        return t

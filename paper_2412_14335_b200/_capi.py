@@ -103,6 +103,7 @@ SIGNATURES = {
     "c3_session_import": (I, [P, P]),
     "c3_session_run": (I, [P, I, C.POINTER(Alloc), C.POINTER(Timing)]),
     "c3_session_run_all_ranks": (I, [P, I, C.POINTER(Alloc), C.POINTER(Timing)]),
+    "c3_session_run_host": (I, [P, I, C.POINTER(Alloc), P, P, P, I64, C.POINTER(Timing)]),
     "c3_session_default_alloc": (I, [P, I, C.POINTER(Alloc)]),
     "c3_session_set_barrier": (I, [P, C.c_void_p, P]),
     "c3_session_set_fused_pace": (I, [P, C.c_float, I]),

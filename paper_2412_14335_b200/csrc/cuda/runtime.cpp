@@ -329,7 +329,7 @@ struct c3_session {
     std::vector<c3_transfer> plan;          // validated ConCCL plan
     cudaStream_t main = nullptr, gemm_s = nullptr, comm_s = nullptr, comm_hi = nullptr;
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
-                ev_ce = nullptr, ev_end = nullptr;
+                ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
     c3sim::MachineDescriptor md;
     c3sim::SlowdownTableSet tables;
     c3sim::SlowdownTableSet tables_loaded;  // as loaded (tables' comm class may come from comm_curve)
@@ -381,6 +381,7 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaStreamCreateWithPriority(&s->comm_hi, cudaStreamNonBlocking, s->w->prio_hi));
     for (cudaEvent_t* e : {&s->ev_start, &s->ev_gs, &s->ev_ge, &s->ev_cs, &s->ev_ce, &s->ev_end})
         C3_CUDA(cudaEventCreate(e));
+    C3_CUDA(cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming));
     return C3_OK;
 }
 
@@ -852,7 +853,7 @@ int c3_session_destroy(c3_session* s) {
         if (p) cudaFree(p);
     for (cudaStream_t st : {s->main, s->gemm_s, s->comm_s, s->comm_hi})
         if (st) cudaStreamDestroy(st);
-    for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end})
+    for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end, s->ev_h2d})
         if (e) cudaEventDestroy(e);
     delete s;
     return C3_OK;
@@ -1309,8 +1310,49 @@ int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
     });
 }
 
+// Host buffers of c3_session_run_host: the step's inputs come from (pinned)
+// host memory and its result goes back, all inside the step.
+struct HostIO {
+    const void* a = nullptr;     // A, M x K bf16
+    const void* send = nullptr;  // this rank's collective input (c3_session_ptrs.send)
+    void* out = nullptr;         // first out_bytes of C
+    int64_t out_bytes = 0;
+};
+
+namespace {
+// this rank's collective input in device memory (c3_session_pointers' send)
+void* session_send(c3_session* s, int64_t* bytes) {
+    const int self = s->w->loopback ? 0 : s->w->rank;
+    if (s->d.collective == C3_ALL_GATHER) {
+        *bytes = s->chunk;
+        return static_cast<uint8_t*>(s->recv[0]) + s->chunk * self;
+    }
+    *bytes = s->d.payload_bytes;
+    return s->in[0];
+}
+
+// Enqueue one H2D copy of the step's inputs on `st` (nothing if no buffer).
+int h2d_a(c3_session* s, const HostIO* io, cudaStream_t st) {
+    if (!io || !io->a) return C3_OK;
+    C3_CUDA(cudaMemcpyAsync(s->a, io->a, static_cast<size_t>(s->d.m * s->d.k * 2), cudaMemcpyDefault, st));
+    return C3_OK;
+}
+int h2d_send(c3_session* s, const HostIO* io, cudaStream_t st) {
+    if (!io || !io->send) return C3_OK;
+    int64_t bytes = 0;
+    void* dst = session_send(s, &bytes);
+    C3_CUDA(cudaMemcpyAsync(dst, io->send, static_cast<size_t>(bytes), cudaMemcpyDefault, st));
+    return C3_OK;
+}
+int d2h_out(c3_session* s, const HostIO* io, cudaStream_t st) {
+    if (!io || !io->out || io->out_bytes <= 0) return C3_OK;
+    C3_CUDA(cudaMemcpyAsync(io->out, s->c, static_cast<size_t>(io->out_bytes), cudaMemcpyDefault, st));
+    return C3_OK;
+}
+}  // namespace
+
 static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_in, int flags,
-                            c3_timing* t) {
+                            c3_timing* t, const HostIO* io = nullptr) {
     if (!s->ready) return set_error(C3_ERR_VALIDATION, "c3_session_run: peers not imported");
     c3_alloc a;
     if (alloc_in)
@@ -1381,10 +1423,13 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         t->gemm_ctas = gemm_ctas;
         C3_CUDA(cudaEventRecord(s->ev_start, s->main));
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
+        C3_TRY(h2d_a(s, io, gs));  // the copy warp reads the send data from the first tile on
+        C3_TRY(h2d_send(s, io, gs));
         C3_CUDA(cudaEventRecord(s->ev_gs, gs));
         C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs, &fc));
         C3_CUDA(cudaEventRecord(s->ev_ge, gs));
         C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ge, 0));
+        C3_TRY(d2h_out(s, io, s->main));
         C3_CUDA(cudaEventRecord(s->ev_end, s->main));
         C3_CUDA(cudaEventSynchronize(s->ev_end));
         C3_CUDA(cudaGetLastError());
@@ -1403,6 +1448,8 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
                                                       : a.backend;
     if (strategy == C3_SERIAL) {
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
+        C3_TRY(h2d_a(s, io, gs));
+        C3_TRY(h2d_send(s, io, gs));
         C3_CUDA(cudaEventRecord(s->ev_gs, gs));
         C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs));
         ++launches;
@@ -1414,6 +1461,17 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     } else {
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
         C3_CUDA(cudaStreamWaitEvent(cs, s->ev_start, 0));
+        if (io) {
+            // Host inputs share one PCIe direction: copy them one after the
+            // other, the first-launched kernel's input first, so that kernel
+            // starts while the other input is still in flight (the second
+            // copy overlaps the first kernel).
+            cudaStream_t first = a.comm_first ? cs : gs, second = a.comm_first ? gs : cs;
+            C3_TRY(a.comm_first ? h2d_send(s, io, first) : h2d_a(s, io, first));
+            C3_CUDA(cudaEventRecord(s->ev_h2d, first));
+            C3_CUDA(cudaStreamWaitEvent(second, s->ev_h2d, 0));
+            C3_TRY(a.comm_first ? h2d_a(s, io, second) : h2d_send(s, io, second));
+        }
         const auto launch_gemm = [&]() -> int {
             C3_CUDA(cudaEventRecord(s->ev_gs, gs));
             if (do_gemm) {
@@ -1439,6 +1497,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ge, 0));
         C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ce, 0));
     }
+    C3_TRY(d2h_out(s, io, s->main));
     C3_CUDA(cudaEventRecord(s->ev_end, s->main));
     C3_CUDA(cudaEventSynchronize(s->ev_end));
     C3_CUDA(cudaGetLastError());
@@ -1459,6 +1518,20 @@ int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing
     if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_run: null argument");
     C3_CUDA(cudaSetDevice(s->w->device));
     return session_run_impl(s, strategy, alloc, 0, out);
+}
+
+int c3_session_run_host(c3_session* s, int strategy, const c3_alloc* alloc, const void* host_a,
+                        const void* host_send, void* host_out, int64_t out_bytes, c3_timing* out) {
+    if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_run_host: null argument");
+    if (out_bytes < 0 || out_bytes > s->d.m * s->d.n * 2 || (out_bytes > 0 && !host_out))
+        return set_error(C3_ERR_VALIDATION, "c3_session_run_host: out_bytes must be in [0, M*N*2] with a buffer");
+    C3_CUDA(cudaSetDevice(s->w->device));
+    HostIO io;
+    io.a = host_a;
+    io.send = host_send;
+    io.out = host_out;
+    io.out_bytes = out_bytes;
+    return session_run_impl(s, strategy, alloc, 0, out, &io);
 }
 
 // Loopback parity helper: run every virtual rank's share of the collective.

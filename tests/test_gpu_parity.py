@@ -509,3 +509,69 @@ def test_pair512_tail_split_matches_256_wide(torch_mod, c3, monkeypatch):
     gemm_check(out["pair512"].cpu().numpy().view(np.uint16), orc.bf16(M * K, SEED, 0, 0),
                orc.bf16(N * K, SEED, 0, 1), M, N, K, rows, cols)
     w.close()
+
+
+def _h2d(c3, ptr, host):
+    c3.check(c3.lib().c3_memcpy(ptr, host.ctypes.data, host.nbytes, 1, None))
+    c3.check(c3.lib().c3_stream_sync(None))
+
+
+def _d2h_np(c3, ptr, nbytes):
+    out = np.empty(nbytes, np.uint8)
+    c3.check(c3.lib().c3_memcpy(out.ctypes.data, ptr, nbytes, 2, None))
+    c3.check(c3.lib().c3_stream_sync(None))
+    return out
+
+
+@pytest.mark.parametrize("collective", [0, 1, 2], ids=["all-gather", "all-to-all", "reduce-scatter"])
+@pytest.mark.parametrize("strategy", ["SERIAL", "C3_BASE", "C3_SP", "CONCCL", "FUSED"])
+def test_run_host_matches_device_run(torch_mod, c3, monkeypatch, collective, strategy):
+    """c3_session_run_host: A and this rank's collective input copied in from
+    pinned host memory, C read back inside the step. The device state after
+    it (C, every virtual rank's receive buffer) and the returned bytes are
+    bit-identical to the device-resident run of the same strategy."""
+    torch = torch_mod
+    if strategy == "FUSED" and collective == 2:
+        pytest.skip("fused C3 moves all-gather / all-to-all data only")
+    if strategy == "FUSED":
+        monkeypatch.setenv("C3_GEMM_KERNEL", "pair")  # fused needs the CTA-pair GEMM
+    st = getattr(c3, strategy)
+    n, M, N, K = 8, 512, 1024, 512
+    payload = n * (1 << 20)
+    w = c3.World(0, n, 0, loopback=True)
+    s = c3.Session(w, M, N, K, collective, payload)
+    s.fill(SEED)
+    p0 = s.pointers(0)
+    a_h = _d2h_np(c3, p0.a, p0.a_bytes)
+    send_h = _d2h_np(c3, p0.send, p0.send_bytes)
+    c_bytes = M * N * 2
+
+    def reset():
+        for v in range(n):
+            pv = s.pointers(v)
+            _h2d(c3, pv.recv, np.zeros(pv.recv_bytes, np.uint8))
+        _h2d(c3, p0.c, np.zeros(c_bytes, np.uint8))
+
+    reset()
+    _h2d(c3, p0.send, send_h)
+    s.run(st, None)
+    c_ref = _d2h_np(c3, p0.c, c_bytes)
+    recv_ref = [_d2h_np(c3, s.pointers(v).recv, s.pointers(v).recv_bytes) for v in range(n)]
+    assert c_ref.any()
+
+    reset()
+    _h2d(c3, p0.a, np.zeros(p0.a_bytes, np.uint8))
+    _h2d(c3, p0.send, np.zeros(p0.send_bytes, np.uint8))
+    pin_a = torch.from_numpy(a_h).pin_memory()
+    pin_s = torch.from_numpy(send_h).pin_memory()
+    pin_o = torch.zeros(c_bytes, dtype=torch.uint8).pin_memory()
+    t = s.run_host(st, None, pin_a.data_ptr(), pin_s.data_ptr(), pin_o.data_ptr(), c_bytes)
+    assert t.total_ms > 0
+    assert np.array_equal(pin_o.numpy(), c_ref)
+    assert np.array_equal(_d2h_np(c3, p0.c, c_bytes), c_ref)
+    for v in range(n):
+        assert np.array_equal(_d2h_np(c3, s.pointers(v).recv, s.pointers(v).recv_bytes), recv_ref[v]), v
+    with pytest.raises(c3.C3Error):
+        s.run_host(st, None, None, None, pin_o.data_ptr(), c_bytes + 2)
+    s.close()
+    w.close()
