@@ -124,7 +124,7 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
                           cudaStream_t stream, double link_bpns = 0.0);
 int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
                          int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream,
-                         double link_bpns = 0.0);
+                         double link_bpns = 0.0, int64_t stride_bytes = -1);  // stride: slot pitch (default = per_peer_bytes)
 int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
                                int n_ctas, const Signals& sig, cudaStream_t stream,
                                double link_bpns = 0.0);

@@ -224,15 +224,15 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
 template <typename V, int U>
 __global__ void __launch_bounds__(kVecThreads)
 a2a_push_vec_kernel(const V* __restrict__ send, MutPtrTable recv, int self, int n,
-                    int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
+                    int64_t slot_vec, int64_t stride_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
     const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * U;
     const uint64_t t0 = global_ns();
     double sent = 0.0;
     for (int j = 0; j < n; ++j) {
         const int p = (self + 1 + j) % n;  // rotated: the ranks start on different targets
-        const V* src = send + slot_vec * p;
-        V* dst = static_cast<V*>(recv.p[p]) + slot_vec * self;
+        const V* src = send + stride_vec * p;
+        V* dst = static_cast<V*>(recv.p[p]) + stride_vec * self;
         for (int64_t blk = static_cast<int64_t>(blockIdx.x) * kVecThreads * U; blk < slot_vec; blk += step) {
             if (cta_bpns > 0.f && p != self) {
                 if (threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
@@ -481,14 +481,19 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
 
 int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
                          int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream,
-                         double link_bpns) {
+                         double link_bpns, int64_t stride_bytes) {
+    if (stride_bytes < 0) stride_bytes = per_peer_bytes;
     if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
         return set_error(C3_ERR_VALIDATION, "alltoall: bad rank/world");
     if (per_peer_bytes < 0) return set_error(C3_ERR_VALIDATION, "alltoall: negative slot");
     if (n_ctas < 1) return set_error(C3_ERR_VALIDATION, "alltoall: n_ctas must be >= 1");
     if (per_peer_bytes == 0 && !sig.enabled) return C3_OK;
-    uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(per_peer_bytes);
+    if (stride_bytes < per_peer_bytes) return set_error(C3_ERR_VALIDATION, "alltoall: stride below the slot");
+    uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(per_peer_bytes) |
+                      static_cast<uintptr_t>(stride_bytes);
     for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
+    if (stride_bytes != per_peer_bytes && (align & 15) != 0)
+        return set_error(C3_ERR_VALIDATION, "alltoall: a strided slot range must be 16-byte aligned");
     // all-to-all keeps 16-byte vectors by default: 32-byte ones were faster
     // alone but slower beside the GEMM (0.72 vs 0.80 of ideal, profiles/r01_comm_wide.txt)
     static const bool wide_a2a = [] {
@@ -499,13 +504,13 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
         const int64_t nvec = per_peer_bytes / 32;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * (kUnrollA2a / 2), n_ctas * kCtasPerUnit);
         a2a_push_vec_kernel<u256, kUnrollA2a / 2><<<grid, kVecThreads, 0, stream>>>(
-            static_cast<const u256*>(send), recv, self, n, nvec, stream_l2_enabled(),
+            static_cast<const u256*>(send), recv, self, n, nvec, stride_bytes / 32, stream_l2_enabled(),
             static_cast<float>(link_bpns / grid), sig);
     } else if ((align & 15) == 0) {
         const int64_t nvec = per_peer_bytes / 16;
         const int grid = grid_for(std::max<int64_t>(nvec, 1), kVecThreads * kUnrollA2a, n_ctas * kCtasPerUnit);
         a2a_push_vec_kernel<uint4, kUnrollA2a><<<grid, kVecThreads, 0, stream>>>(
-            static_cast<const uint4*>(send), recv, self, n, nvec, stream_l2_enabled(),
+            static_cast<const uint4*>(send), recv, self, n, nvec, stride_bytes / 16, stream_l2_enabled(),
             static_cast<float>(link_bpns / grid), sig);
     } else {
         const int grid = grid_for(std::max<int64_t>(per_peer_bytes, 1), kThreads, n_ctas);

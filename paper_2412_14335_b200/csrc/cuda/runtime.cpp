@@ -330,6 +330,8 @@ struct c3_session {
     cudaStream_t main = nullptr, gemm_s = nullptr, comm_s = nullptr, comm_hi = nullptr;
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
                 ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
+    cudaStream_t h2d_s = nullptr;             // c3_session_run_host: the host-input copies
+    cudaEvent_t ev_piece[8] = {};             // ... one per landed piece of the collective's input
     c3sim::MachineDescriptor md;
     c3sim::SlowdownTableSet tables;
     c3sim::SlowdownTableSet tables_loaded;  // as loaded (tables' comm class may come from comm_curve)
@@ -382,6 +384,8 @@ int session_alloc(c3_session* s) {
     for (cudaEvent_t* e : {&s->ev_start, &s->ev_gs, &s->ev_ge, &s->ev_cs, &s->ev_ce, &s->ev_end})
         C3_CUDA(cudaEventCreate(e));
     C3_CUDA(cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming));
+    for (cudaEvent_t& e : s->ev_piece) C3_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    C3_CUDA(cudaStreamCreateWithFlags(&s->h2d_s, cudaStreamNonBlocking));
     return C3_OK;
 }
 
@@ -411,11 +415,16 @@ int host_barrier(c3_session* s, cudaStream_t st) {
 
 // Enqueue this rank's share of the collective on `st`. Returns the number of
 // kernels launched via *launches.
+// `off`/`len` (CU backend only): move bytes [off, off + len) of every slot,
+// the piece of a pipelined host-input step (len < 0: the whole slot).
 int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaStream_t st,
-                       int* launches) {
+                       int* launches, int64_t off = 0, int64_t len = -1) {
     c3_world* w = s->w;
     const int n = s->n;
     const int64_t chunk = s->chunk;
+    const int64_t plen = len < 0 ? chunk : len;
+    if (backend != C3_BACKEND_CU && (off != 0 || plen != chunk))
+        return set_error(C3_ERR_VALIDATION, "slot ranges are for the SM collectives only");
     const bool loop = w->loopback != 0;
     const bool all = loop && (flags & kRunAllRanks);
     const int first = loop ? 0 : w->rank;
@@ -434,8 +443,12 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         if (backend == C3_BACKEND_CU) {
             const Signals sig = make_signals(s, 0);
             for (int v = first; v <= last; ++v) {
-                C3_TRY(launch_allgather_push(v, n, static_cast<uint8_t*>(recv.p[v]) + chunk * v, recv,
-                                             chunk, n_ctas, sig, st, s->run_gbps));
+                // the kernel writes slot v at recv[q] + plen * v: shift the bases
+                // so that lands on recv[q] + chunk * v + off
+                MutPtrTable r = recv;
+                for (int q = 0; q < n; ++q) r.p[q] = static_cast<uint8_t*>(recv.p[q]) + (chunk - plen) * v + off;
+                C3_TRY(launch_allgather_push(v, n, static_cast<uint8_t*>(recv.p[v]) + chunk * v + off, r,
+                                             plen, n_ctas, sig, st, s->run_gbps));
                 ++*launches;
             }
         } else {
@@ -457,9 +470,12 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         }
         if (backend == C3_BACKEND_CU) {
             const Signals sig = make_signals(s, 0);
+            MutPtrTable r = recv;
+            for (int q = 0; q < n; ++q) r.p[q] = static_cast<uint8_t*>(recv.p[q]) + off;
             for (int v = first; v <= last; ++v) {
-                C3_TRY(launch_alltoall_push(v, n, loop ? s->in[static_cast<size_t>(v)] : s->in[0], recv,
-                                            chunk, n_ctas, sig, st, s->run_gbps));
+                C3_TRY(launch_alltoall_push(v, n,
+                                            static_cast<const uint8_t*>(loop ? s->in[static_cast<size_t>(v)] : s->in[0]) + off,
+                                            r, plen, n_ctas, sig, st, s->run_gbps, chunk));
                 ++*launches;
             }
         } else {
@@ -483,8 +499,11 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         for (int p = 0; p < n; ++p) in.p[p] = loop ? s->in[static_cast<size_t>(p)] : s->peer_coll[p];
         const Signals sig = make_signals(s, 1);
         for (int v = first; v <= last; ++v) {
-            void* out = loop ? s->out[static_cast<size_t>(v)] : s->out[0];
-            C3_TRY(launch_reduce_scatter_pull(v, n, in, out, count, n_ctas, sig, st, s->run_gbps));
+            // the kernel reads in[g] + plen * v: shift to in[g] + chunk * v + off
+            PtrTable r = in;
+            for (int g = 0; g < n; ++g) r.p[g] = static_cast<const uint8_t*>(in.p[g]) + (chunk - plen) * v + off;
+            void* out = static_cast<uint8_t*>(loop ? s->out[static_cast<size_t>(v)] : s->out[0]) + off;
+            C3_TRY(launch_reduce_scatter_pull(v, n, r, out, plen / 2, n_ctas, sig, st, s->run_gbps));
             ++*launches;
         }
         return C3_OK;
@@ -853,6 +872,9 @@ int c3_session_destroy(c3_session* s) {
         if (p) cudaFree(p);
     for (cudaStream_t st : {s->main, s->gemm_s, s->comm_s, s->comm_hi})
         if (st) cudaStreamDestroy(st);
+    for (cudaEvent_t e : s->ev_piece)
+        if (e) cudaEventDestroy(e);
+    if (s->h2d_s) cudaStreamDestroy(s->h2d_s);
     for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end, s->ev_h2d})
         if (e) cudaEventDestroy(e);
     delete s;
@@ -1337,6 +1359,37 @@ int h2d_a(c3_session* s, const HostIO* io, cudaStream_t st) {
     C3_CUDA(cudaMemcpyAsync(s->a, io->a, static_cast<size_t>(s->d.m * s->d.k * 2), cudaMemcpyDefault, st));
     return C3_OK;
 }
+// Pieces of the collective's host input in a pipelined concurrent step: each
+// piece's copy is followed by the collective on that piece while the next
+// piece crosses PCIe (C3_H2D_PIECES, default 4; 1 below 4 MiB slots).
+int h2d_pieces(const c3_session* s) {
+    static const int env = [] {
+        const char* e = std::getenv("C3_H2D_PIECES");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? std::min(v, 8) : 4;
+    }();
+    return s->chunk >= (int64_t{4} << 20) ? env : 1;
+}
+void piece_range(const c3_session* s, int pieces, int k, int64_t* off, int64_t* len) {
+    const int64_t pb = (s->chunk / pieces) & ~int64_t{4095};
+    *off = pb * k;
+    *len = k == pieces - 1 ? s->chunk - *off : pb;
+}
+// bytes [off, off + len) of every slot of the collective's input
+int h2d_send_piece(c3_session* s, const HostIO* io, int64_t off, int64_t len, cudaStream_t st) {
+    int64_t bytes = 0;
+    uint8_t* dst = static_cast<uint8_t*>(session_send(s, &bytes));
+    const uint8_t* src = static_cast<const uint8_t*>(io->send);
+    if (s->d.collective == C3_ALL_GATHER) {
+        C3_CUDA(cudaMemcpyAsync(dst + off, src + off, static_cast<size_t>(len), cudaMemcpyDefault, st));
+    } else {
+        const size_t pitch = static_cast<size_t>(s->chunk);
+        C3_CUDA(cudaMemcpy2DAsync(dst + off, pitch, src + off, pitch, static_cast<size_t>(len),
+                                  static_cast<size_t>(s->n), cudaMemcpyDefault, st));
+    }
+    return C3_OK;
+}
+
 int h2d_send(c3_session* s, const HostIO* io, cudaStream_t st) {
     if (!io || !io->send) return C3_OK;
     int64_t bytes = 0;
@@ -1461,16 +1514,38 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     } else {
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
         C3_CUDA(cudaStreamWaitEvent(cs, s->ev_start, 0));
+        // Host inputs (c3_session_run_host) share one PCIe direction: they are
+        // copied back to back on the copy stream, the first-launched kernel's
+        // input first. The collective's input lands in pieces and the SM
+        // collective runs per piece as it lands, so the copies overlap the GEMM
+        // and the collective overlaps the remaining copies.
+        const bool send_in = io && io->send && do_comm;
+        const int pieces = send_in ? (backend == C3_BACKEND_CU ? h2d_pieces(s) : 1) : 0;
         if (io) {
-            // Host inputs share one PCIe direction: copy them one after the
-            // other, the first-launched kernel's input first, so that kernel
-            // starts while the other input is still in flight (the second
-            // copy overlaps the first kernel).
-            cudaStream_t first = a.comm_first ? cs : gs, second = a.comm_first ? gs : cs;
-            C3_TRY(a.comm_first ? h2d_send(s, io, first) : h2d_a(s, io, first));
-            C3_CUDA(cudaEventRecord(s->ev_h2d, first));
-            C3_CUDA(cudaStreamWaitEvent(second, s->ev_h2d, 0));
-            C3_TRY(a.comm_first ? h2d_a(s, io, second) : h2d_send(s, io, second));
+            C3_CUDA(cudaStreamWaitEvent(s->h2d_s, s->ev_start, 0));
+            const auto copy_a = [&]() -> int {
+                if (!io->a) return C3_OK;
+                C3_TRY(h2d_a(s, io, s->h2d_s));
+                C3_CUDA(cudaEventRecord(s->ev_h2d, s->h2d_s));
+                C3_CUDA(cudaStreamWaitEvent(gs, s->ev_h2d, 0));
+                return C3_OK;
+            };
+            const auto copy_send = [&]() -> int {
+                for (int k = 0; k < pieces; ++k) {
+                    int64_t off = 0, len = 0;
+                    piece_range(s, pieces, k, &off, &len);
+                    C3_TRY(h2d_send_piece(s, io, off, len, s->h2d_s));
+                    C3_CUDA(cudaEventRecord(s->ev_piece[k], s->h2d_s));
+                }
+                return C3_OK;
+            };
+            if (a.comm_first) {
+                C3_TRY(copy_send());
+                C3_TRY(copy_a());
+            } else {
+                C3_TRY(copy_a());
+                C3_TRY(copy_send());
+            }
         }
         const auto launch_gemm = [&]() -> int {
             C3_CUDA(cudaEventRecord(s->ev_gs, gs));
@@ -1482,8 +1557,21 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
             return C3_OK;
         };
         const auto launch_comm = [&]() -> int {
+            if (pieces > 0) C3_CUDA(cudaStreamWaitEvent(cs, s->ev_piece[0], 0));
             C3_CUDA(cudaEventRecord(s->ev_cs, cs));
-            if (do_comm) C3_TRY(enqueue_collective(s, backend, comm_ctas, flags, cs, &launches));
+            if (do_comm && pieces > 1) {
+                for (int k = 0; k < pieces; ++k) {
+                    int64_t off = 0, len = 0;
+                    piece_range(s, pieces, k, &off, &len);
+                    if (k > 0) {
+                        C3_CUDA(cudaStreamWaitEvent(cs, s->ev_piece[k], 0));
+                        ++s->epoch;  // every piece is one collective across the ranks
+                    }
+                    C3_TRY(enqueue_collective(s, backend, comm_ctas, flags, cs, &launches, off, len));
+                }
+            } else if (do_comm) {
+                C3_TRY(enqueue_collective(s, backend, comm_ctas, flags, cs, &launches));
+            }
             C3_CUDA(cudaEventRecord(s->ev_ce, cs));
             return C3_OK;
         };

@@ -48,30 +48,53 @@ def _worker(rank, world, port, coll, q):
         strats = [c3.C3_SP, c3.CONCCL, c3.COMM_ONLY_CU, c3.COMM_ONLY_DMA, c3.SERIAL]
         if coll != c3.REDUCE_SCATTER:
             strats.append(c3.FUSED)
-        for strat in strats:
-            s.fill(SEED)
-            d.barrier()  # every rank's inputs are written before anyone reads/pushes
-            t = s.run(strat)
-            d.barrier()  # every rank's collective done before checking
+        def check(s, chunk):
+            payload = world * chunk
             p = s.pointers(0)
             if coll == c3.ALL_GATHER:
                 got = np.empty(payload, np.uint8)
                 c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
                 c3.check(c3.lib().c3_stream_sync(None))
-                ok = np.array_equal(got, orc.expected_allgather(world, chunk, SEED, 2))
-            elif coll == c3.ALL_TO_ALL:
+                return np.array_equal(got, orc.expected_allgather(world, chunk, SEED, 2))
+            if coll == c3.ALL_TO_ALL:
                 got = np.empty(payload, np.uint8)
                 c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
                 c3.check(c3.lib().c3_stream_sync(None))
-                ok = np.array_equal(got, orc.expected_alltoall(world, rank, chunk, SEED, 4))
-            else:
-                count = chunk // 2
-                host_in = [orc.bf16(world * count, SEED, g, 3) for g in range(world)]
-                got = np.empty(count, np.uint16)
-                c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, count * 2, 2, None))
-                c3.check(c3.lib().c3_stream_sync(None))
-                ok = np.array_equal(got, orc.reduce_scatter(host_in, rank, count))
-            results[strat] = (ok, t.total_ms)
+                return np.array_equal(got, orc.expected_alltoall(world, rank, chunk, SEED, 4))
+            count = chunk // 2
+            host_in = [orc.bf16(world * count, SEED, g, 3) for g in range(world)]
+            got = np.empty(count, np.uint16)
+            c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, count * 2, 2, None))
+            c3.check(c3.lib().c3_stream_sync(None))
+            return np.array_equal(got, orc.reduce_scatter(host_in, rank, count))
+
+        for strat in strats:
+            s.fill(SEED)
+            d.barrier()  # every rank's inputs are written before anyone reads/pushes
+            t = s.run(strat)
+            d.barrier()  # every rank's collective done before checking
+            results[strat] = (check(s, chunk), t.total_ms)
+        # host-buffer step (c3_session_run_host) with slots large enough for the
+        # pipelined form: the collective's input lands in pieces, one collective
+        # (one epoch of peer flags) per piece
+        import torch
+        big = (4 << 20) + 4096 * 3 + 16 * 5
+        s2 = c3.Session(w, M, N, K, coll, world * big)
+        s2.import_handles(d.allgather_bytes(s2.export_handles()))
+        s2.set_barrier(d.barrier)
+        for strat in (c3.C3_BASE, c3.C3_SP):
+            s2.fill(SEED)
+            p2 = s2.pointers(0)
+            host = torch.empty(p2.send_bytes, dtype=torch.uint8).pin_memory()
+            c3.check(c3.lib().c3_memcpy(host.data_ptr(), p2.send, p2.send_bytes, 2, None))
+            zeros = np.zeros(p2.send_bytes, np.uint8)
+            c3.check(c3.lib().c3_memcpy(p2.send, zeros.ctypes.data, p2.send_bytes, 1, None))
+            c3.check(c3.lib().c3_stream_sync(None))
+            d.barrier()
+            t = s2.run_host(strat, None, None, host.data_ptr())
+            d.barrier()
+            results[("host", strat)] = (check(s2, big), t.total_ms)
+        s2.close()
         s.close()
         w.close()
         d.close()
