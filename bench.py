@@ -596,7 +596,7 @@ def run_ours(args, dist):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "concurrent_ms": e2e_conc, "serial_ms": e2e_ser,
                 "call": "c3_session_run_host (pinned host A and collective input in, 4 KiB of C out; "
-                        "concurrent strategies overlap the second input copy with the first kernel)"},
+                        "the concurrent step lands the collective input in pieces and runs the collective per piece, overlapping PCIe with the GEMM)"},
         "gpu_launches": launches,
         # the north star's "1 GPU (GEMM only)" line: the isolated GEMM of the
         # timed rounds (median), as time and TF/s against the measured peaks
