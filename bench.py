@@ -46,9 +46,9 @@ from paper_2412_14335_b200.dist import Dist  # noqa: E402
 MIB = 1 << 20
 # BASELINE.json configs: (M, N, K), collective, payload per rank
 CONFIGS = {
-    "cfg1": dict(desc="configs[0] on the GPU: GEMM 1024x1024x1024 (bf16 here; fp32 in the CPU "
-                      "reference) || 16 MiB all-gather", m=1024, n=1024, k=1024,
-                 coll="all-gather", payload=16 * MIB),
+    "cfg1": dict(desc="configs[0] on the GPU: fp32 GEMM 1024x1024x1024 (TF32 tensor cores, fp32 "
+                      "accumulate and output) || 16 MiB all-gather", m=1024, n=1024, k=1024,
+                 coll="all-gather", payload=16 * MIB, dtype_bytes=4),
     "cfg2": dict(desc="LLaMA-70B FSDP layer: FFN up-proj GEMM 8192x28672x8192 bf16 || "
                       "next-layer weight all-gather 896 MiB (gate+up) across 8 GPUs",
                  m=8192, n=28672, k=8192, coll="all-gather", payload=896 * MIB),
@@ -177,7 +177,8 @@ def run_ours(args, dist):
     world = c3.World(dist.rank, n, device, loopback=loopback)
     coll = {"all-gather": c3.ALL_GATHER, "all-to-all": c3.ALL_TO_ALL,
             "reduce-scatter": c3.REDUCE_SCATTER}[cfg["coll"]]
-    sess = c3.Session(world, cfg["m"], cfg["n"], cfg["k"], coll, cfg["payload"])
+    elem = cfg.get("dtype_bytes", 2)
+    sess = c3.Session(world, cfg["m"], cfg["n"], cfg["k"], coll, cfg["payload"], dtype_bytes=elem)
     if not loopback:
         sess.import_handles(dist.allgather_bytes(sess.export_handles()))
     log("session ready")
@@ -537,12 +538,16 @@ def run_ours(args, dist):
             traffic = None
     # the GEMM's roofline: tensor-bound when its arithmetic intensity exceeds
     # the machine's FLOP:byte ratio, else HBM-bound (cfg4_mb, M = 128)
-    gemm_bytes = 2.0 * (cfg["m"] * cfg["k"] + cfg["n"] * cfg["k"] + cfg["m"] * cfg["n"])
-    ratio = peaks["bf16_tflops"] * 1e12 / (peaks["hbm_gbs"] * 1e9)
+    gemm_bytes = float(elem) * (cfg["m"] * cfg["k"] + cfg["n"] * cfg["k"] + cfg["m"] * cfg["n"])
+    # TF32 (fp32 GEMM) runs at half the bf16 dense rate
+    tc_peak = peaks["bf16_tflops"] / (2.0 if elem == 4 else 1.0)
+    ratio = tc_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
     if flops / gemm_bytes >= ratio:
-        roofline = {"bound": "tensor", "kernel": "gemm_bf16_tn_pair_kernel (tcgen05 cta_group::2)",
-                    "achieved": achieved, "peak": peaks["bf16_tflops"], "unit": "TFLOP/s",
-                    "frac": achieved / peaks["bf16_tflops"],
+        roofline = {"bound": "tensor",
+                    "kernel": ("gemm_bf16_tn_kernel<*, F32> (tcgen05 kind::tf32)" if elem == 4
+                               else "gemm_bf16_tn_pair_kernel (tcgen05 cta_group::2)"),
+                    "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
+                    "frac": achieved / tc_peak,
                     "frac_of_sustained": achieved / peak_sus,
                     "peak_source": peak_src + " burst bf16 (cuBLAS): the timed region is ~0.1 s "
                                    "of GEMMs interleaved with collective-only phases, short of the "
@@ -574,7 +579,8 @@ def run_ours(args, dist):
         "n_gpus": dist.world, "steps": K, "warmup": W,
         "ms_per_step": sum(step_ms) / len(step_ms), "ms_per_step_median": t_conc,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "bf16", "data": "synthetic (counter-hash bf16 U(-1,1)/8 and byte labels)",
+        "dtype": "fp32 (TF32 tensor cores)" if elem == 4 else "bf16",
+        "data": "synthetic (counter-hash bf16 U(-1,1)/8 and byte labels)",
         "config": {"workload": f"{args.config}: {cfg['desc']}", "strategy": head_name,
                    "strategy_choice": choice,
                    "collective": cfg["coll"], "payload_bytes": cfg["payload"],

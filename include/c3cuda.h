@@ -101,6 +101,9 @@ typedef struct c3_scenario_desc {
     int32_t collective;
     int32_t n_ranks;
     int64_t payload_bytes;
+    /* GemmKernel::dtype_bytes (workload.hpp:18-25): 0 or 2 = bf16 in/out;
+     * 4 = fp32 in/out on the TF32 tensor cores (configs[0]) */
+    int32_t dtype_bytes;
 } c3_scenario_desc;
 
 /* c3sim::Allocation (sim.hpp:25-31), in SMs. */
@@ -161,11 +164,17 @@ int c3_ipc_close(c3_world* w, void* peer_ptr);
  * Counter-hash data shared bit-for-bit with oracle/c3oracle.c. */
 int c3_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor, void* stream);
 int c3_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor, void* stream);
+/* fp32 buffer of the same values as c3_fill_bf16 (bf16 values widened, exact) */
+int c3_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, void* stream);
 
 /* ------------------------------------------------------------------ GEMM
  * Executes c3sim::GemmKernel (workload.hpp:18-25) whose cost
  * roofline_gemm_time (workload.hpp:62-63) models; max_ctas caps the
  * persistent grid = the GEMM's SM allocation (Allocation::cus_gemm). */
+/* fp32 A, B, C on the TF32 tensor cores (tcgen05.mma kind::tf32, fp32
+ * accumulate): operands are read with a 10-bit mantissa. K, N multiples of 4. */
+int c3_gemm_f32(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
+                int max_ctas, void* stream);
 int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
                  int64_t k, int max_ctas, void* stream);
 

@@ -131,9 +131,10 @@ private:
 class Session {
 public:
     Session(World& w, const C3Scenario& sc, const HostTransport* transport = nullptr) {
-        if (sc.gemm.dtype_bytes != 2)
-            throw ValidationError("execute: the B200 GEMM is bf16 (dtype_bytes 2), scenario '" + sc.id +
-                                  "' has dtype_bytes " + std::to_string(sc.gemm.dtype_bytes));
+        if (sc.gemm.dtype_bytes != 2 && sc.gemm.dtype_bytes != 4)
+            throw ValidationError("execute: the B200 GEMM is bf16 (dtype_bytes 2) or fp32 on the TF32 tensor "
+                                  "cores (4), scenario '" + sc.id + "' has dtype_bytes " +
+                                  std::to_string(sc.gemm.dtype_bytes));
         const c3_world_info wi = w.info();
         if (sc.collective.n_ranks != wi.n_ranks)
             throw ValidationError("execute: scenario '" + sc.id + "' has n_ranks " +
@@ -143,7 +144,7 @@ public:
             throw ValidationError("execute: a multi-process world needs a HostTransport");
         const c3_scenario_desc d{sc.gemm.m, sc.gemm.n, sc.gemm.k,
                                  static_cast<int32_t>(sc.collective.kind), sc.collective.n_ranks,
-                                 sc.collective.payload_bytes};
+                                 sc.collective.payload_bytes, static_cast<int32_t>(sc.gemm.dtype_bytes)};
         check_status(c3_session_create(w.get(), &d, &s_), "c3_session_create");
         n_ranks_ = wi.n_ranks;
         if (!wi.loopback && wi.n_ranks > 1) {

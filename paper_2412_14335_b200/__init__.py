@@ -71,8 +71,10 @@ class World:
             check(lib().c3_world_destroy(self.h))
             self.h = C.c_void_p()
 
-    def gemm(self, a, b, c, m, n, k, max_ctas=0, stream=None):
-        check(lib().c3_gemm_bf16(self.h, a, b, c, m, n, k, max_ctas, stream))
+    def gemm(self, a, b, c, m, n, k, max_ctas=0, stream=None, dtype_bytes=2):
+        """C = A B^T: bf16 (dtype_bytes 2) or fp32 on the TF32 tensor cores (4)."""
+        fn = lib().c3_gemm_f32 if dtype_bytes == 4 else lib().c3_gemm_bf16
+        check(fn(self.h, a, b, c, m, n, k, max_ctas, stream))
 
     def allgather_p2p(self, self_rank, send, recv_ptrs, chunk_bytes, n_ctas=32, stream=None):
         check(lib().c3_allgather_p2p(self.h, self_rank, send, ptr_array(recv_ptrs), chunk_bytes,
@@ -94,9 +96,9 @@ class World:
 class Session:
     """One C3 scenario's operands, executed under a strategy (c3_session_*)."""
 
-    def __init__(self, world, m, n, k, collective, payload_bytes):
+    def __init__(self, world, m, n, k, collective, payload_bytes, dtype_bytes=2):
         self.world = world
-        d = _capi.ScenarioDesc(m, n, k, collective, world.n_ranks, payload_bytes)
+        d = _capi.ScenarioDesc(m, n, k, collective, world.n_ranks, payload_bytes, dtype_bytes)
         self.desc = d
         self.h = C.c_void_p()
         check(lib().c3_session_create(world.h, C.byref(d), C.byref(self.h)))

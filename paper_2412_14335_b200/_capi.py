@@ -45,7 +45,7 @@ class WorldInfo(C.Structure):
 
 class ScenarioDesc(C.Structure):
     _fields_ = [("m", C.c_int64), ("n", C.c_int64), ("k", C.c_int64), ("collective", C.c_int32),
-                ("n_ranks", C.c_int32), ("payload_bytes", C.c_int64)]
+                ("n_ranks", C.c_int32), ("payload_bytes", C.c_int64), ("dtype_bytes", C.c_int32)]
 
 
 class Alloc(C.Structure):
@@ -86,8 +86,10 @@ SIGNATURES = {
     "c3_ipc_import": (I, [P, P, PP]),
     "c3_ipc_close": (I, [P, P]),
     "c3_fill_bf16": (I, [P, I64, U64, I, I, P]),
+    "c3_fill_f32": (I, [P, I64, U64, I, I, P]),
     "c3_fill_labels": (I, [P, I64, U64, I, I, P]),
     "c3_gemm_bf16": (I, [P, P, P, P, I64, I64, I64, I, P]),
+    "c3_gemm_f32": (I, [P, P, P, P, I64, I64, I64, I, P]),
     "c3_allgather_p2p": (I, [P, I, P, PP, I64, I, P]),
     "c3_alltoall_p2p": (I, [P, I, P, PP, I64, I, P]),
     "c3_reduce_scatter_p2p": (I, [P, I, PP, P, I64, I, P]),

@@ -70,10 +70,11 @@ struct GemmPlan {
     int* counters = nullptr;  // device [tile claims, CTA exits]; zero between launches
     int64_t m = 0, n = 0, k = 0;
     Kind kind = kWide;
+    int elem = 2;  // 2: bf16 (kind::f16); 4: fp32 in/out on the TF32 tensor cores (single-CTA kernels)
     int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;  // of the chosen kernel
 };
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k, int* counters, int sm_count);
+                   int64_t k, int* counters, int sm_count, int elem_bytes = 2);
 struct FusedComm;
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
                      const FusedComm* fc = nullptr);
@@ -128,6 +129,8 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
 int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
                                int n_ctas, const Signals& sig, cudaStream_t stream,
                                double link_bpns = 0.0);
+// fp32 buffer holding the same bf16 values widened (the fp32 GEMM's inputs)
+int launch_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, cudaStream_t stream);
 int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor,
                      cudaStream_t stream);
 int launch_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor,

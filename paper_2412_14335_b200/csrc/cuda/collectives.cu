@@ -354,13 +354,20 @@ __device__ __forceinline__ uint64_t hash64(uint64_t x) {
 
 __device__ __forceinline__ uint64_t label_word(uint64_t key, uint64_t w) { return hash64(key ^ w); }
 
-__global__ void fill_bf16_kernel(__nv_bfloat16* dst, int64_t count, uint64_t key) {
+// T = __nv_bfloat16, or float: the same bf16 values widened (exact) for the
+// fp32 GEMM's inputs
+template <typename T>
+__global__ void fill_bf16_kernel(T* dst, int64_t count, uint64_t key) {
     const int64_t step = static_cast<int64_t>(gridDim.x) * blockDim.x;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < count; i += step) {
         const uint64_t h = label_word(key, static_cast<uint64_t>(i));
         const int32_t r24 = static_cast<int32_t>(h >> 40);
         const float u = static_cast<float>(r24 - (1 << 23)) * (1.0f / 8388608.0f);
-        dst[i] = __float2bfloat16_rn(u * 0.125f);
+        const __nv_bfloat16 b = __float2bfloat16_rn(u * 0.125f);
+        if constexpr (sizeof(T) == 4)
+            dst[i] = __bfloat162float(b);
+        else
+            dst[i] = b;
     }
 }
 
@@ -558,6 +565,14 @@ int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tens
     if (count <= 0) return C3_OK;
     fill_bf16_kernel<<<grid_for(count, 256, 148 * 16), 256, 0, stream>>>(
         static_cast<__nv_bfloat16*>(dst), count, label_key(seed, rank, tensor));
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, cudaStream_t stream) {
+    if (count <= 0) return C3_OK;
+    fill_bf16_kernel<<<grid_for(count, 256, 148 * 16), 256, 0, stream>>>(static_cast<float*>(dst), count,
+                                                                         label_key(seed, rank, tensor));
     C3_CUDA(cudaGetLastError());
     return C3_OK;
 }

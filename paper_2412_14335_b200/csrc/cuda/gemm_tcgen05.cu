@@ -1,8 +1,13 @@
-// Persistent bf16 GEMM for sm_100a: TMA -> shared memory (mbarrier ring) ->
+// Persistent GEMM for sm_100a: TMA -> shared memory (mbarrier ring) ->
 // tcgen05.mma (single-thread issue, fp32 accumulators in TMEM, double
-// buffered) -> tcgen05.ld epilogue -> bf16 global stores.
+// buffered) -> tcgen05.ld epilogue -> global stores.
 //
-//   C[M,N] = A[M,K] * B[N,K]^T      (A, B K-major bf16; C row-major bf16)
+//   C[M,N] = A[M,K] * B[N,K]^T      (A, B K-major; C row-major)
+//
+// bf16 in / bf16 out (kind::f16), or fp32 in / fp32 out on the TF32 tensor
+// cores (kind::tf32, F32 = true): configs[0]'s fp32 GEMM. Both move 128-byte
+// K rows per stage (64 bf16 or 32 fp32 elements) and issue 4 MMAs of 32 bytes
+// of K each, so the pipeline is the same.
 //
 // This is the "compute" half of a C3 pair (reference GemmKernel,
 // /root/reference/proj/include/c3sim/workload.hpp:18-25; its cost model
@@ -39,6 +44,7 @@ namespace gemm {
 constexpr int BM = 128;          // UMMA M (one CTA)
 constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
 constexpr int UK = 16;           // UMMA K for 16-bit inputs
+constexpr int BK_F32 = 32;       // one 128-byte swizzle atom of fp32 (TF32 MMAs of K = 8)
 constexpr int ACC_BUFS = 2;
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;      // tile raster: 16 M-tiles per band for L2 reuse
@@ -57,7 +63,7 @@ struct Cfg {
 struct Params {
     int m, n, k;
     int tiles_m, tiles_n, num_tiles, k_blocks;
-    __nv_bfloat16* c;
+    void* c;  // bf16, or fp32 for the TF32 kernel
     int ldc;
     int* tile_counter;  // claims; reset to 0 by the last CTA to exit
     int* exit_counter;
@@ -72,11 +78,12 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
     tn = in_band / rows;
 }
 
-template <int BN>
+template <int BN, bool F32>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, const Params p) {
     using K = Cfg<BN>;
+    constexpr int BKE = F32 ? BK_F32 : BK;  // K elements per stage (128 bytes per row)
     constexpr int STAGES = K::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms.
@@ -142,8 +149,8 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             for (int kb = 0; kb < p.k_blocks; ++kb) {
                 mbar_wait(&empty[stage], phase ^ 1);
                 mbar_arrive_expect_tx(&full[stage], K::STAGE);
-                tma_load_2d(smem_a + stage * K::A_STAGE, &map_a, &full[stage], kb * BK, tm * BM, keep);
-                tma_load_2d(smem_b + stage * K::B_STAGE, &map_b, &full[stage], kb * BK, tn * BN, keep);
+                tma_load_2d(smem_a + stage * K::A_STAGE, &map_a, &full[stage], kb * BKE, tm * BM, keep);
+                tma_load_2d(smem_b + stage * K::B_STAGE, &map_b, &full[stage], kb * BKE, tn * BN, keep);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -153,7 +160,7 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
+        constexpr uint32_t idesc = F32 ? idesc_tf32_f32(BM, BN) : idesc_bf16_f32(BM, BN);
         const uint32_t a0 = smem_u32(smem_a), b0 = smem_u32(smem_b);
         int stage = 0;
         uint32_t phase = 0;
@@ -174,10 +181,15 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                 const uint32_t a_addr = a0 + stage * K::A_STAGE;
                 const uint32_t b_addr = b0 + stage * K::B_STAGE;
 #pragma unroll
-                for (int k = 0; k < BK / UK; ++k) {
-                    // advancing K inside the 128-byte swizzle atom = +32 B per UMMA_K
-                    umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * UK * 2),
-                              smem_desc_k_sw128(b_addr + k * UK * 2), idesc, (kb | k) != 0);
+                for (int k = 0; k < 4; ++k) {
+                    // advancing K inside the 128-byte swizzle atom = +32 B per MMA
+                    // (16 bf16 or 8 tf32 elements)
+                    if constexpr (F32)
+                        umma_tf32(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
+                                  idesc, (kb | k) != 0);
+                    else
+                        umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
+                                  idesc, (kb | k) != 0);
                 }
                 umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
                 if (++stage == STAGES) {
@@ -210,7 +222,6 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             tc_fence_after();
             const int row = tm * BM + row_in_tile;
             const bool row_ok = row < p.m;
-            __nv_bfloat16* crow = p.c + static_cast<size_t>(row) * p.ldc;
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
                                    static_cast<uint32_t>(acc * BN);
 #pragma unroll 1
@@ -219,7 +230,20 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                 tmem_ld_32x32b_x32(t_row + c, v);
                 tmem_ld_wait();
                 const int col = tn * BN + c;
-                if (row_ok) {
+                if (!row_ok) continue;
+                if constexpr (F32) {
+                    float* crow = static_cast<float*>(p.c) + static_cast<size_t>(row) * p.ldc;
+                    if (col + 32 <= p.n) {
+                        uint4* dst = reinterpret_cast<uint4*>(crow + col);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col + j < p.n) crow[col + j] = __uint_as_float(v[j]);
+                    }
+                } else {
+                    __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(p.c) + static_cast<size_t>(row) * p.ldc;
                     if (col + 32 <= p.n) {
                         uint4* dst = reinterpret_cast<uint4*>(crow + col);
 #pragma unroll
@@ -275,25 +299,28 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
 
 namespace {
 
+// K-major [rows, k] operand in boxes of one 128-byte swizzle row (64 bf16 or
+// 32 fp32 elements) x box_rows
 CUresult encode_kmajor_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, uint64_t k,
-                            uint32_t box_rows) {
+                            uint32_t box_rows, int elem = 2) {
     const cuuint64_t dims[2] = {k, rows};
-    const cuuint64_t strides[1] = {k * 2};
-    const cuuint32_t box[2] = {static_cast<cuuint32_t>(gemm::BK), box_rows};
+    const cuuint64_t strides[1] = {k * static_cast<uint64_t>(elem)};
+    const cuuint32_t box[2] = {static_cast<cuuint32_t>(128 / elem), box_rows};
     const cuuint32_t estr[2] = {1, 1};
     if (!drv().TensorMapEncodeTiled) return CUDA_ERROR_NOT_SUPPORTED;
-    return drv().TensorMapEncodeTiled(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(ptr),
+    return drv().TensorMapEncodeTiled(map, elem == 4 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16,
+                                      2, const_cast<void*>(ptr),
                                       dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                                       CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-template <int BN>
+template <int BN, bool F32>
 int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStream_t stream) {
     using K = gemm::Cfg<BN>;
     static bool attr_done = false;
     if (!attr_done) {
-        const cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel<BN>,
+        const cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel<BN, F32>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(K::SMEM));
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
@@ -307,7 +334,7 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStre
     p.tiles_n = static_cast<int>((plan->n + BN - 1) / BN);
     p.num_tiles = p.tiles_m * p.tiles_n;
     p.k_blocks = plan->k_blocks;
-    p.c = static_cast<__nv_bfloat16*>(plan->c);
+    p.c = plan->c;
     p.ldc = static_cast<int>(plan->n);
     static const bool static_sched = [] {
         const char* e = std::getenv("C3_GEMM_SCHED");  // development A/B switch
@@ -316,7 +343,7 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStre
     p.tile_counter = static_sched ? nullptr : plan->counters;
     p.exit_counter = plan->counters + 1;
     grid = std::min(grid, p.num_tiles);
-    gemm::gemm_bf16_tn_kernel<BN><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, map_b, p);
+    gemm::gemm_bf16_tn_kernel<BN, F32><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, map_b, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
     return C3_OK;
@@ -327,10 +354,13 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStre
 int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc);
 
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k, int* counters, int sm_count) {
+                   int64_t k, int* counters, int sm_count, int elem_bytes) {
+    if (elem_bytes != 2 && elem_bytes != 4)
+        return set_error(C3_ERR_VALIDATION, "gemm: element size must be 2 (bf16) or 4 (fp32 on TF32 tensor cores)");
+    const int64_t row_elems = 16 / elem_bytes;
     if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
-    if (k % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: K must be a multiple of 8 (16-byte rows)");
-    if (n % 8 != 0) return set_error(C3_ERR_VALIDATION, "gemm: N must be a multiple of 8 (16-byte rows)");
+    if (k % row_elems != 0) return set_error(C3_ERR_VALIDATION, "gemm: K rows must be a multiple of 16 bytes");
+    if (n % row_elems != 0) return set_error(C3_ERR_VALIDATION, "gemm: N rows must be a multiple of 16 bytes");
     if ((reinterpret_cast<uintptr_t>(A) | reinterpret_cast<uintptr_t>(B) | reinterpret_cast<uintptr_t>(C)) & 15)
         return set_error(C3_ERR_VALIDATION, "gemm: operands must be 16-byte aligned");
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
@@ -351,19 +381,24 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
                  : m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
                  : tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow
                                                      : GemmPlan::kWide;
-    if (const char* f = std::getenv("C3_GEMM_KERNEL")) {  // tests force each variant
+    if (elem_bytes == 4)  // the TF32 path is the single-CTA kernel
+        plan->kind = tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow : GemmPlan::kWide;
+    if (const char* f = std::getenv("C3_GEMM_KERNEL"); f && elem_bytes == 2) {  // tests force each variant
         const std::string v(f);
         if (v == "pair") plan->kind = GemmPlan::kPair;
         if (v == "pair512") plan->kind = GemmPlan::kPair512;
         if (v == "wide") plan->kind = GemmPlan::kWide;
         if (v == "narrow") plan->kind = GemmPlan::kNarrow;
     }
-    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), 128);
+    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), 128,
+                                    elem_bytes);
     if (r == CUDA_SUCCESS)  // 128-row B boxes: the pair kernel's half tile and the narrow kernel
-        r = encode_kmajor_bf16(&plan->map_b128, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 128);
+        r = encode_kmajor_bf16(&plan->map_b128, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 128,
+                               elem_bytes);
     if (r == CUDA_SUCCESS)
-        r = encode_kmajor_bf16(&plan->map_b256, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 256);
-    if (r == CUDA_SUCCESS)  // C [m, n] in 32-row x 64-column boxes (pair kernels' TMA-store epilogue)
+        r = encode_kmajor_bf16(&plan->map_b256, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 256,
+                               elem_bytes);
+    if (r == CUDA_SUCCESS && elem_bytes == 2)  // C [m, n] in 32-row x 64-column boxes (pair kernels' TMA-store epilogue)
         r = encode_kmajor_bf16(&plan->map_c, C, static_cast<uint64_t>(m), static_cast<uint64_t>(n), 32);
     if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
     plan->m = m;
@@ -371,7 +406,9 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     plan->k = k;
     plan->c = C;
     plan->counters = counters;
-    plan->k_blocks = static_cast<int>((k + gemm::BK - 1) / gemm::BK);
+    plan->elem = elem_bytes;
+    const int bke = elem_bytes == 4 ? gemm::BK_F32 : gemm::BK;
+    plan->k_blocks = static_cast<int>((k + bke - 1) / bke);
     const bool pair = plan->kind == GemmPlan::kPair || plan->kind == GemmPlan::kPair512;
     const int bm = pair ? 256 : 128;
     const int bn = plan->kind == GemmPlan::kNarrow ? 128 : plan->kind == GemmPlan::kPair512 ? 512 : 256;
@@ -393,8 +430,12 @@ int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStrea
         grid = fc ? grid / 2 * 2 : std::min(grid / 2, plan->num_tiles) * 2;
         return gemm_pair_launch(plan, grid, stream, fc);
     }
-    if (plan->kind == GemmPlan::kWide) return launch_bn<256>(plan, plan->map_b256, grid, stream);
-    return launch_bn<128>(plan, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap
+    if (plan->elem == 4) {
+        if (plan->kind == GemmPlan::kWide) return launch_bn<256, true>(plan, plan->map_b256, grid, stream);
+        return launch_bn<128, true>(plan, plan->map_b128, grid, stream);
+    }
+    if (plan->kind == GemmPlan::kWide) return launch_bn<256, false>(plan, plan->map_b256, grid, stream);
+    return launch_bn<128, false>(plan, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap
 }
 
 }  // namespace c3k

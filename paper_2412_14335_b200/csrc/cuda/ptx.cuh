@@ -120,6 +120,17 @@ __device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t a_desc, uint
         : "memory");
 }
 
+// kind::tf32: fp32 operands in shared memory read as TF32 (10-bit mantissa), fp32 accumulate
+__device__ __forceinline__ void umma_tf32(uint32_t d_tmem, uint64_t a_desc, uint64_t b_desc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(a_desc), "l"(b_desc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+
 // Arrive on `bar` once every previously issued tcgen05 op of this thread is done.
 __device__ __forceinline__ void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
@@ -164,6 +175,15 @@ __host__ __device__ constexpr uint32_t idesc_bf16_f32(uint32_t m, uint32_t n) {
     return (1u << 4)             // D format F32
            | (1u << 7)           // A format BF16
            | (1u << 10)          // B format BF16
+           | ((n >> 3) << 17)    // N / 8
+           | ((m >> 4) << 24);   // M / 16
+}
+
+// kind::tf32 instruction descriptor: A/B format 2 = TF32, D = F32, both K-major
+__host__ __device__ constexpr uint32_t idesc_tf32_f32(uint32_t m, uint32_t n) {
+    return (1u << 4)             // D format F32
+           | (2u << 7)           // A format TF32
+           | (2u << 10)          // B format TF32
            | ((n >> 3) << 17)    // N / 8
            | ((m >> 4) << 24);   // M / 16
 }

@@ -304,6 +304,7 @@ struct c3_session {
     int vr = 1;             // virtual ranks held by this process
     int n = 1;              // collective ranks
     int64_t chunk = 0;      // payload / n (bytes)
+    int elem = 2;           // GEMM element bytes: 2 bf16, 4 fp32 (TF32 tensor cores)
     GemmPlan gemm;
     int* gemm_counters = nullptr;
     void *a = nullptr, *b = nullptr, *c = nullptr;
@@ -346,13 +347,13 @@ namespace {
 
 int session_alloc(c3_session* s) {
     const c3_scenario_desc& d = s->d;
-    C3_CUDA(cudaMalloc(&s->a, static_cast<size_t>(d.m * d.k * 2)));
-    C3_CUDA(cudaMalloc(&s->b, static_cast<size_t>(d.n * d.k * 2)));
-    C3_CUDA(cudaMalloc(&s->c, static_cast<size_t>(d.m * d.n * 2)));
+    C3_CUDA(cudaMalloc(&s->a, static_cast<size_t>(d.m * d.k * s->elem)));
+    C3_CUDA(cudaMalloc(&s->b, static_cast<size_t>(d.n * d.k * s->elem)));
+    C3_CUDA(cudaMalloc(&s->c, static_cast<size_t>(d.m * d.n * s->elem)));
     C3_CUDA(cudaMalloc(&s->gemm_counters, 2 * sizeof(int)));
     C3_CUDA(cudaMemset(s->gemm_counters, 0, 2 * sizeof(int)));
     C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k, s->gemm_counters,
-                          s->w->prop.multiProcessorCount));
+                          s->w->prop.multiProcessorCount, s->elem));
     const size_t payload = static_cast<size_t>(d.payload_bytes);
     for (int v = 0; v < s->vr; ++v) {
         void* p = nullptr;
@@ -672,19 +673,33 @@ int c3_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor, 
     return launch_fill_bf16(dst, count, seed, rank, tensor, static_cast<cudaStream_t>(stream));
 }
 
+int c3_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, void* stream) {
+    return launch_fill_f32(dst, count, seed, rank, tensor, static_cast<cudaStream_t>(stream));
+}
+
 int c3_fill_labels(void* dst, int64_t bytes, uint64_t seed, int rank, int tensor, void* stream) {
     return launch_fill_labels(dst, bytes, seed, rank, tensor, static_cast<cudaStream_t>(stream));
 }
 
-int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                 int64_t k, int max_ctas, void* stream) {
-    if (!w) return set_error(C3_ERR_VALIDATION, "c3_gemm_bf16: null world");
+static int world_gemm(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
+                      int max_ctas, void* stream, int elem) {
+    if (!w) return set_error(C3_ERR_VALIDATION, "gemm: null world");
     GemmPlan plan;
     // round-robin claim-counter pairs: up to kGemmCounterSlots GEMMs in flight
     int* ctr = w->gemm_counters + 2 * (w->gemm_counter_next++ % kGemmCounterSlots);
-    C3_TRY(gemm_plan_init(&plan, A, B, C, m, n, k, ctr, w->prop.multiProcessorCount));
+    C3_TRY(gemm_plan_init(&plan, A, B, C, m, n, k, ctr, w->prop.multiProcessorCount, elem));
     return gemm_plan_launch(&plan, max_ctas, w->prop.multiProcessorCount,
                             static_cast<cudaStream_t>(stream));
+}
+
+int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
+                 int64_t k, int max_ctas, void* stream) {
+    return world_gemm(w, A, B, C, m, n, k, max_ctas, stream, 2);
+}
+
+int c3_gemm_f32(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
+                int max_ctas, void* stream) {
+    return world_gemm(w, A, B, C, m, n, k, max_ctas, stream, 4);
 }
 
 int c3_allgather_p2p(c3_world* w, int self, const void* send, void* const* recv,
@@ -807,7 +822,10 @@ int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** ou
         return set_error(C3_ERR_VALIDATION, "collective: payload_bytes must be divisible by n_ranks");
     if (d.collective == C3_REDUCE_SCATTER && (d.payload_bytes / d.n_ranks) % 2)
         return set_error(C3_ERR_VALIDATION, "reduce-scatter: per-rank slot must hold whole bf16 elements");
+    if (d.dtype_bytes != 0 && d.dtype_bytes != 2 && d.dtype_bytes != 4)
+        return set_error(C3_ERR_VALIDATION, "c3_session_create: dtype_bytes must be 2 (bf16) or 4 (fp32)");
     auto* s = new c3_session;
+    s->elem = d.dtype_bytes == 4 ? 4 : 2;
     s->w = w;
     s->d = d;
     s->n = d.n_ranks;
@@ -829,7 +847,7 @@ int c3_session_create(c3_world* w, const c3_scenario_desc* desc, c3_session** ou
         sc.gemm.m = d.m;
         sc.gemm.n = d.n;
         sc.gemm.k = d.k;
-        sc.gemm.dtype_bytes = 2;
+        sc.gemm.dtype_bytes = s->elem;
         sc.collective.kind = d.collective == C3_ALL_GATHER   ? c3sim::CollectiveKind::AllGather
                              : d.collective == C3_ALL_TO_ALL ? c3sim::CollectiveKind::AllToAll
                                                              : c3sim::CollectiveKind::ReduceScatter;
@@ -889,9 +907,9 @@ int c3_session_pointers(const c3_session* s, int v, c3_session_ptrs* o) {
     o->a = s->a;
     o->b = s->b;
     o->c = s->c;
-    o->a_bytes = d.m * d.k * 2;
-    o->b_bytes = d.n * d.k * 2;
-    o->c_bytes = d.m * d.n * 2;
+    o->a_bytes = d.m * d.k * s->elem;
+    o->b_bytes = d.n * d.k * s->elem;
+    o->c_bytes = d.m * d.n * s->elem;
     const size_t sv = static_cast<size_t>(v);
     const int self = s->w->loopback ? v : s->w->rank;
     if (d.collective == C3_ALL_GATHER) {
@@ -921,8 +939,9 @@ int c3_session_fill(c3_session* s, uint64_t seed) {
     const c3_scenario_desc& d = s->d;
     cudaStream_t st = s->main;
     const int r0 = s->w->loopback ? 0 : s->w->rank;
-    C3_TRY(launch_fill_bf16(s->a, d.m * d.k, seed, r0, 0, st));
-    C3_TRY(launch_fill_bf16(s->b, d.n * d.k, seed, r0, 1, st));
+    const auto fill = s->elem == 4 ? launch_fill_f32 : launch_fill_bf16;
+    C3_TRY(fill(s->a, d.m * d.k, seed, r0, 0, st));
+    C3_TRY(fill(s->b, d.n * d.k, seed, r0, 1, st));
     for (int v = 0; v < s->vr; ++v) {
         const int rank = s->w->loopback ? v : s->w->rank;
         const size_t sv = static_cast<size_t>(v);
@@ -1356,7 +1375,7 @@ void* session_send(c3_session* s, int64_t* bytes) {
 // Enqueue one H2D copy of the step's inputs on `st` (nothing if no buffer).
 int h2d_a(c3_session* s, const HostIO* io, cudaStream_t st) {
     if (!io || !io->a) return C3_OK;
-    C3_CUDA(cudaMemcpyAsync(s->a, io->a, static_cast<size_t>(s->d.m * s->d.k * 2), cudaMemcpyDefault, st));
+    C3_CUDA(cudaMemcpyAsync(s->a, io->a, static_cast<size_t>(s->d.m * s->d.k * s->elem), cudaMemcpyDefault, st));
     return C3_OK;
 }
 // Pieces of the collective's host input in a pipelined concurrent step: each
@@ -1611,8 +1630,8 @@ int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing
 int c3_session_run_host(c3_session* s, int strategy, const c3_alloc* alloc, const void* host_a,
                         const void* host_send, void* host_out, int64_t out_bytes, c3_timing* out) {
     if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_run_host: null argument");
-    if (out_bytes < 0 || out_bytes > s->d.m * s->d.n * 2 || (out_bytes > 0 && !host_out))
-        return set_error(C3_ERR_VALIDATION, "c3_session_run_host: out_bytes must be in [0, M*N*2] with a buffer");
+    if (out_bytes < 0 || out_bytes > s->d.m * s->d.n * s->elem || (out_bytes > 0 && !host_out))
+        return set_error(C3_ERR_VALIDATION, "c3_session_run_host: out_bytes must be in [0, size of C] with a buffer");
     C3_CUDA(cudaSetDevice(s->w->device));
     HostIO io;
     io.a = host_a;

@@ -578,3 +578,107 @@ def test_run_host_matches_device_run(torch_mod, c3, monkeypatch, collective, str
         s.run_host(st, None, None, None, pin_o.data_ptr(), c_bytes + 2)
     s.close()
     w.close()
+
+
+# ---------------------------------------------------------------- fp32 / TF32
+# configs[0] is an fp32 GEMM. The product runs it on the
+# TF32 tensor cores (tcgen05.mma kind::tf32, fp32 accumulate, fp32 out).
+# Stated tolerances:
+#   * inputs representable in bf16 (the synthetic fill): TF32 reads them
+#     exactly and every product is exact in fp32, so only the fp32
+#     accumulation differs from the fp64 definition:
+#         |C - C_ref| <= 2^-19 |C_ref| + K 2^-22 (|A||B|)[i,j]
+#   * general fp32 inputs: each operand loses up to 2^-10 relative in the
+#     TF32 read, so  |C - C_ref| <= 2^-9 (|A||B|)[i,j] + K 2^-22 (|A||B|)[i,j]
+
+def _f32_check(got, A64, B64, K, exact_inputs):
+    ref = A64 @ B64.T
+    mag = np.abs(A64) @ np.abs(B64).T
+    tol = (2.0 ** -19 * np.abs(ref) if exact_inputs else 2.0 ** -9 * mag) + K * 2.0 ** -22 * mag
+    err = np.abs(got.astype(np.float64) - ref)
+    assert np.all(err <= tol), (float(err.max()), float((err / np.maximum(mag, 1e-30)).max()))
+
+
+def test_fill_f32_matches_oracle(torch_mod, c3):
+    torch = torch_mod
+    w = c3.World()
+    for count in (1, 7, 4096, 1 << 20):
+        t = torch.empty(count, dtype=torch.float32, device="cuda")
+        c3.check(c3.lib().c3_fill_f32(t.data_ptr(), count, SEED, 3, 1, None))
+        assert np.array_equal(t.cpu().numpy(), orc.bf16_to_f32(orc.bf16(count, SEED, 3, 1)))
+    w.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(1024, 1024, 1024), (128, 256, 32), (300, 520, 200), (1000, 2056, 136),
+                                   (64, 1024, 512), (2048, 4096, 1024)])
+def test_gemm_f32_tf32_full(torch_mod, c3, M, N, K):
+    """c3_gemm_f32 on the synthetic (bf16-valued) fp32 inputs, every entry."""
+    torch = torch_mod
+    w = c3.World()
+    A = torch.empty(M * K, dtype=torch.float32, device="cuda")
+    B = torch.empty(N * K, dtype=torch.float32, device="cuda")
+    Cm = torch.full((M * N,), float("nan"), dtype=torch.float32, device="cuda")
+    c3.check(c3.lib().c3_fill_f32(A.data_ptr(), M * K, SEED, 0, 0, None))
+    c3.check(c3.lib().c3_fill_f32(B.data_ptr(), N * K, SEED, 0, 1, None))
+    w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
+    torch.cuda.synchronize()
+    A64 = orc.bf16_to_f32(orc.bf16(M * K, SEED, 0, 0)).astype(np.float64).reshape(M, K)
+    B64 = orc.bf16_to_f32(orc.bf16(N * K, SEED, 0, 1)).astype(np.float64).reshape(N, K)
+    _f32_check(Cm.cpu().numpy().reshape(M, N), A64, B64, K, True)
+    w.close()
+
+
+@pytest.mark.parametrize("M,N,K", [(512, 768, 1000), (300, 520, 204)])
+def test_gemm_f32_general_inputs(torch_mod, c3, M, N, K):
+    """General fp32 inputs (normal, wide exponent range): the TF32 bound."""
+    torch = torch_mod
+    w = c3.World()
+    g = torch.Generator().manual_seed(3)
+    Ah = torch.randn(M, K, generator=g) * torch.exp2(torch.randint(-6, 7, (M, 1), generator=g).float())
+    Bh = torch.randn(N, K, generator=g)
+    A, B = Ah.cuda(), Bh.cuda()
+    Cm = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
+    torch.cuda.synchronize()
+    _f32_check(Cm.cpu().numpy(), Ah.double().numpy(), Bh.double().numpy(), K, False)
+    w.close()
+
+
+def test_gemm_f32_rejects_unaligned(c3, torch_mod):
+    w = c3.World()
+    t = torch_mod.empty(64 * 64, dtype=torch_mod.float32, device="cuda")
+    with pytest.raises(c3.C3Error):
+        w.gemm(t.data_ptr(), t.data_ptr(), t.data_ptr(), 8, 8, 6, dtype_bytes=4)  # K rows of 24 bytes
+    w.close()
+
+
+@pytest.mark.parametrize("strategy", ["SERIAL", "C3_BASE", "C3_SP", "CONCCL"])
+def test_cfg1_fp32_session(torch_mod, c3, strategy):
+    """configs[0] end to end: fp32 GEMM 1024^3 (TF32 tensor cores) with a
+    16 MiB all-gather at world 2: the all-gather bit-exact, every GEMM entry
+    within the stated bound, through the host-buffer call as well."""
+    torch = torch_mod
+    n, M, N, K, payload = 2, 1024, 1024, 1024, 16 << 20
+    w = c3.World(0, n, 0, loopback=True)
+    s = c3.Session(w, M, N, K, c3.ALL_GATHER, payload, dtype_bytes=4)
+    s.fill(SEED)
+    p = s.pointers(0)
+    assert p.a_bytes == M * K * 4 and p.c_bytes == M * N * 4
+    s.run(getattr(c3, strategy), None, all_ranks=True)
+    got = np.empty(payload, np.uint8)
+    c3.check(c3.lib().c3_memcpy(got.ctypes.data, p.recv, payload, 2, None))
+    c3.check(c3.lib().c3_stream_sync(None))
+    assert np.array_equal(got, orc.expected_allgather(n, payload // n, SEED, 2))
+    A64 = orc.bf16_to_f32(orc.bf16(M * K, SEED, 0, 0)).astype(np.float64).reshape(M, K)
+    B64 = orc.bf16_to_f32(orc.bf16(N * K, SEED, 0, 1)).astype(np.float64).reshape(N, K)
+    cm = np.empty(M * N, np.float32)
+    c3.check(c3.lib().c3_memcpy(cm.ctypes.data, p.c, M * N * 4, 2, None))
+    c3.check(c3.lib().c3_stream_sync(None))
+    _f32_check(cm.reshape(M, N), A64, B64, K, True)
+    # host buffers: A in from pinned memory, all of C back
+    a_h = torch.from_numpy(A64.astype(np.float32).ravel().view(np.uint8).copy()).pin_memory()
+    out = torch.zeros(M * N * 4, dtype=torch.uint8).pin_memory()
+    s.run_host(getattr(c3, strategy), None, a_h.data_ptr(), None, out.data_ptr(), M * N * 4)
+    assert np.array_equal(out.numpy().view(np.float32), cm)
+    s.close()
+    w.close()
