@@ -116,6 +116,24 @@ def test_execute_loopback(strategy):
 
 
 @pytest.mark.gpu
+@pytest.mark.parametrize("strategy", ["serial", "c3_sp", "conccl"])
+def test_execute_fp32_configs0(strategy):
+    """configs[0] (fp32 GEMM 1024^3 || 16 MiB all-gather, world 2) through
+    execute(): GemmKernel::dtype_bytes 4 runs on the TF32 tensor cores; fused
+    C3 is bf16-only and refuses it."""
+    s = _small_scenario(m=1024, nn=1024)
+    s.gemm.dtype_bytes = 4
+    w = c3sim.World(0, 2, 0, True)
+    r = c3sim.execute(s, strategy, w, warmup=2, reps=3)
+    assert r.t_gemm > 0 and r.t_comm > 0 and r.makespan > 0
+    with pytest.raises(c3sim.UnsupportedError):
+        c3sim.execute(s, "c3_fused", w, warmup=1, reps=1)
+    s.gemm.dtype_bytes = 8
+    with pytest.raises(c3sim.ValidationError):
+        c3sim.execute(s, strategy, w, warmup=1, reps=1)
+
+
+@pytest.mark.gpu
 def test_fused_on_a_small_gemm_is_unsupported():
     w = c3sim.World(0, 2, 0, True)
     with pytest.raises(c3sim.UnsupportedError):
