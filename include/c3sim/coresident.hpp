@@ -57,6 +57,12 @@ struct CoResidentParams {
     /// rate as (rate / link rate)^rate_exponent; 1 = linear (pacing neutral),
     /// > 1 = spreading the collective over the GEMM pays.
     double rate_exponent = 1.0;
+    /// The all-gather kernel stores each loaded vector n-1 times, so with few
+    /// ranks it behaves like the all-to-all class: with this set, beside a
+    /// compute-bound GEMM its factor is comm + (comm_all_to_all - comm) / (n-1)^2
+    /// (measured: n = 2 / 4 / 8 fit 1.8 / 1.1 / 1.0, profiles/r01_size_sweep.csv).
+    /// Beside a memory-bound GEMM (single-CTA tiles, light issue load) it stays `comm`.
+    bool all_gather_by_ranks = false;
 
     double gemm(KernelClass gemm_class) const {
         return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
@@ -64,19 +70,31 @@ struct CoResidentParams {
     double comm_factor(KernelClass comm_class) const {
         return comm_class == KernelClass::AllToAll && comm_all_to_all > 0.0 ? comm_all_to_all : comm;
     }
+    /// n_ranks <= 1: no rank dependence (the class factor above).
+    double comm_factor(KernelClass comm_class, int n_ranks, KernelClass gemm_class) const {
+        if (comm_class != KernelClass::AllGather || !all_gather_by_ranks || n_ranks <= 1 ||
+            gemm_class == KernelClass::GemmMemoryBound)
+            return comm_factor(comm_class);
+        const double a2a = comm_all_to_all > 0.0 ? comm_all_to_all : comm;
+        const double s = n_ranks - 1;
+        return comm + (a2a - comm) / (s * s);
+    }
 };
 
 void validate(const CoResidentParams& p);
 
 /// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc,
-///        "comm-all-to-all": pc (optional), "rate-exponent": g (optional, default 1)}.
+///        "comm-all-to-all": pc (optional), "rate-exponent": g (optional, default 1),
+///        "all-gather-by-ranks": bool (optional, default false)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 
 /// Isolated-equivalent CTA count of `cus_comm` co-resident collective CTAs
-/// of the given collective kernel class.
+/// of the given collective kernel class (n_ranks > 1 and the GEMM's class:
+/// the rank-dependent all-gather factor, CoResidentParams::all_gather_by_ranks).
 int coresident_comm_ctas(int cus_comm, const CoResidentParams& p,
-                         KernelClass comm_class = KernelClass::AllGather);
+                         KernelClass comm_class = KernelClass::AllGather, int n_ranks = 0,
+                         KernelClass gemm_class = KernelClass::GemmComputeBound);
 
 /// Two-phase fluid prediction of a co-resident run: GEMM on all CUs
 /// (t_gemm seconds alone), collective on cus_comm CTAs (t_comm_at_ctas =

@@ -1064,7 +1064,7 @@ double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, doubl
                           double pace_gbps = 0.0) {
     const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
     const int eff = c3sim::coresident_comm_ctas(ctas, s->cores,
-                                                c3sim::comm_kernel_class(s->scenario.collective.kind));
+                                                c3sim::comm_kernel_class(s->scenario.collective.kind), s->n, gcls);
     double t_at = comm_ms_at(s, eff, t_comm_cu_ms);
     const double link = link_rate_gbps(s, t_comm_cu_ms);
     if (pace_gbps > 0.0 && pace_gbps < link) t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));
@@ -1203,7 +1203,9 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
             for (int pass = 0; pass < 2 && pred.empty(); ++pass) {
                 for (int c : cands) {
                     if (c < 1 || c >= s->md.cus_per_gpu) continue;
-                    const int eff = c3sim::coresident_comm_ctas(c, s->cores, ccls);
+                    const int eff = c3sim::coresident_comm_ctas(
+                        c, s->cores, ccls, s->n,
+                        c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md)));
                     if (pass == 0 && comm_ms_at(s, eff, t_comm_cu_ms) > 1.03 * t_comm_cu_ms) continue;
                     pred.emplace_back(c, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms));
                     best_co = std::min(best_co, pred.back().second);

@@ -75,6 +75,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.comm = j.value("comm", 1.0);
         p.rate_exponent = j.value("rate-exponent", 1.0);
         p.comm_all_to_all = j.value("comm-all-to-all", 0.0);
+        p.all_gather_by_ranks = j.value("all-gather-by-ranks", false);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -88,12 +89,14 @@ std::string save_coresident_params(const CoResidentParams& p) {
               {"comm", p.comm},
               {"comm-all-to-all", p.comm_all_to_all},
               {"rate-exponent", p.rate_exponent}};
+    if (p.all_gather_by_ranks) j["all-gather-by-ranks"] = true;
     return j.dump(2) + "\n";
 }
 
-int coresident_comm_ctas(int cus_comm, const CoResidentParams& p, KernelClass comm_class) {
+int coresident_comm_ctas(int cus_comm, const CoResidentParams& p, KernelClass comm_class, int n_ranks,
+                         KernelClass gemm_class) {
     validate(p);
-    return std::max(1, static_cast<int>(std::lround(cus_comm / p.comm_factor(comm_class))));
+    return std::max(1, static_cast<int>(std::lround(cus_comm / p.comm_factor(comm_class, n_ranks, gemm_class))));
 }
 
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,

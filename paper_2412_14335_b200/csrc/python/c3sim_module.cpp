@@ -232,7 +232,7 @@ void add_sim(py::module_& m) {
     py::class_<CRP>(m, "CoResidentParams")
         .def(py::init<>())
         .RW(CRP, gemm_compute_bound).RW(CRP, gemm_memory_bound).RW(CRP, comm).RW(CRP, comm_all_to_all)
-        .RW(CRP, rate_exponent);
+        .RW(CRP, rate_exponent).RW(CRP, all_gather_by_ranks);
     m.def("load_coresident_params", &cs::load_coresident_params);
     m.def("save_coresident_params", &cs::save_coresident_params);
     m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),
@@ -240,7 +240,8 @@ void add_sim(py::module_& m) {
           py::arg("rate_ratio") = 1.0);
     m.def("fit_coresident_gemm_penalty", &cs::fit_coresident_gemm_penalty);
     m.def("coresident_comm_ctas", &cs::coresident_comm_ctas, py::arg("cus_comm"), py::arg("params"),
-          py::arg("comm_class") = cs::KernelClass::AllGather);
+          py::arg("comm_class") = cs::KernelClass::AllGather, py::arg("n_ranks") = 0,
+          py::arg("gemm_class") = cs::KernelClass::GemmComputeBound);
 
     using SR = cs::SweepRow;
     using AR = cs::AggregateRow;

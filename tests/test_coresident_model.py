@@ -115,6 +115,7 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
     p = c3sim.CoResidentParams()
     p.gemm_compute_bound = p.gemm_memory_bound = 1.12
     p.comm, p.comm_all_to_all, p.rate_exponent = 1.5, 2.0, 1.5
+    p.all_gather_by_ranks = True  # as the tool fits
     hdr = ("scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
            "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
            "predicted_makespan_s,t_comm_ctas_ms,comm_pace_gbps")
@@ -123,7 +124,7 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
                               ("cfgC_896M", "all-to-all", 2.5e-3, 1.1e-3), ("cfgD_896M", "reduce-scatter", 2.4e-3, 1.0e-3)):
         # a link-bound collective: 1/ctas below 24 CTA units, flat from there
         pts = {c: tc * max(1.0, 24.0 / c) for c in (16, 24, 32, 48, 64)}
-        d = {"tg": tg, "tc": tc, "mib": float(sid.rsplit("_", 1)[1].rstrip("M")),
+        d = {"tg": tg, "tc": tc, "mib": float(sid.rsplit("_", 1)[1].rstrip("M")), "n": 8,
              "ccls": c3sim.KernelClass.ALL_GATHER if coll == "all-gather" else c3sim.KernelClass.ALL_TO_ALL,
              "curve": c3sim.CommCurve(sorted(pts) + [148], [pts[c] for c in sorted(pts)] + [tc])}
         peer = 7 / 8 * d["mib"] * 2 ** 20
@@ -144,6 +145,26 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
     assert got["comm"] == pytest.approx(1.5, abs=0.051)
     assert got["comm-all-to-all"] == pytest.approx(2.0, abs=0.051)
     assert got["rate-exponent"] == pytest.approx(1.5, abs=0.01)
+    assert got["all-gather-by-ranks"] is True
+
+
+def test_all_gather_factor_by_ranks():
+    """all_gather_by_ranks: beside a compute-bound GEMM the all-gather CTA's
+    factor is comm + (comm_all_to_all - comm) / (n-1)^2 (n = 2: the all-to-all
+    one); beside a memory-bound GEMM, and with the flag off, it is `comm`."""
+    p = c3sim.CoResidentParams()
+    p.comm, p.comm_all_to_all = 1.0, 2.1
+    AG, A2A = c3sim.KernelClass.ALL_GATHER, c3sim.KernelClass.ALL_TO_ALL
+    assert c3sim.coresident_comm_ctas(64, p, AG, 2, CB) == 64  # flag off
+    p.all_gather_by_ranks = True
+    assert c3sim.coresident_comm_ctas(63, p, AG, 2, CB) == 30   # 63 / 2.1
+    assert c3sim.coresident_comm_ctas(64, p, AG, 4, CB) == round(64 / (1.0 + 1.1 / 9))
+    assert c3sim.coresident_comm_ctas(64, p, AG, 8, CB) == round(64 / (1.0 + 1.1 / 49))
+    assert c3sim.coresident_comm_ctas(64, p, AG, 2, c3sim.KernelClass.GEMM_MEMORY_BOUND) == 64
+    assert c3sim.coresident_comm_ctas(63, p, A2A, 2, CB) == 30
+    assert c3sim.coresident_comm_ctas(64, p, AG) == 64  # no world size: the class factor
+    txt = c3sim.save_coresident_params(p)
+    assert '"all-gather-by-ranks": true' in txt
 
 
 def test_paced_collective_scales_the_gemm_penalty():

@@ -9,6 +9,9 @@ runtime's predict_coresident) has three parameters:
   p_c  the collective CTA's cost factor: c co-resident units move data like
        c / p_c isolated units (t = curve(c / p_c)); fitted separately for the
        all-gather kernel and the all-to-all class (all-to-all, reduce-scatter);
+  (the all-gather factor beside a compute-bound GEMM moves toward the
+  all-to-all one as the world shrinks: p_c + (p_c,a2a - p_c) / (n-1)^2,
+  CoResidentParams::all_gather_by_ranks; rows carry n_ranks, default 8)
   g    the slowdown's excess scales with the collective's actual rate over its
        unpaced rate, ratio = t_comm_full / t_collective, as ratio^g (pacing or
        too few CTAs lower the collective's intensity beside the GEMM).
@@ -44,6 +47,7 @@ def load(paths):
             d = scen.setdefault(key, {"tg": float(r["t_gemm_iso_ms"]) * 1e-3,
                                       "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": [],
                                       "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M")),
+                                      "n": int(r.get("n_ranks") or N_RANKS),
                                       "ccls": c3sim.KernelClass.ALL_GATHER if r["collective"] == "all-gather"
                                       else c3sim.KernelClass.ALL_TO_ALL})
             c = int(r["cus_comm"])
@@ -65,8 +69,8 @@ def load(paths):
 
 def predict(d, c, pace, cls, p):
     """The runtime's predict_coresident (runtime.cpp) on one row."""
-    t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p, d["ccls"]))
-    peer = (N_RANKS - 1) / N_RANKS * d["mib"] * 2 ** 20
+    t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p, d["ccls"], d["n"], cls))
+    peer = (d["n"] - 1) / d["n"] * d["mib"] * 2 ** 20
     link = peer / d["tc"] / 1e9
     if 0 < pace < link:
         t_at = max(t_at, peer / (pace * 1e9))
@@ -78,6 +82,7 @@ def error(scen, cls, pg, pc, g, pc_a2a=None):
     p = c3sim.CoResidentParams()
     p.gemm_compute_bound = p.gemm_memory_bound = pg
     p.comm, p.comm_all_to_all, p.rate_exponent = pc, pc if pc_a2a is None else pc_a2a, g
+    p.all_gather_by_ranks = True  # the all-gather factor tends to the all-to-all one as n -> 2
     err, n = 0.0, 0
     for d in scen.values():
         for c, pace, mk in d["rows"]:
@@ -89,7 +94,7 @@ def error(scen, cls, pg, pc, g, pc_a2a=None):
 def main():
     *ins, out = sys.argv[1:]
     scen = load(ins)
-    is_mb = lambda key: key[1].startswith("cfg4_mb")  # noqa: E731  M=128: memory-bound GEMM
+    is_mb = lambda key: key[1].startswith("cfg4_mb") or "_mb_" in key[1]  # noqa: E731  M=128: memory-bound
     cb = {k: v for k, v in scen.items() if not is_mb(k)}
     mb = {k: v for k, v in scen.items() if is_mb(k)}
     ag = {k: v for k, v in cb.items() if v["ccls"] == c3sim.KernelClass.ALL_GATHER}
@@ -98,16 +103,17 @@ def main():
     best = None
     for pg in [1.0 + 0.02 * i for i in range(31)]:            # 1.0 .. 1.6
         for g in [0.5 * i for i in range(1, 9)]:              # 0.5 .. 4.0
-            tot, n, pcs_best = 0.0, 0, []
-            for group in (ag, a2a):
+            tot, n, pcs_best = 0.0, 0, [0.0, 0.0]
+            # the all-to-all class first: the all-gather factor at small n leans on it
+            for gi, group in ((1, a2a), (0, ag)):
                 if not group:
-                    pcs_best.append(0.0)
                     continue
-                e, pc, k = min((error(group, CB, pg, pc, g)[0], pc, error(group, CB, pg, pc, g)[1])
-                               for pc in pcs)
+                fixed = pcs_best[1] or None
+                e, pc, k = min((error(group, CB, pg, pc, g, fixed if gi == 0 else None)[0], pc,
+                                error(group, CB, pg, pc, g, fixed if gi == 0 else None)[1]) for pc in pcs)
                 tot += e * k
                 n += k
-                pcs_best.append(pc)
+                pcs_best[gi] = pc
             if best is None or tot / n < best[0]:
                 best = (tot / n, pg, pcs_best[0], pcs_best[1], g, n)
     e_cb, pg_cb, pc_ag, pc_a2a, g, n_cb = best
@@ -118,6 +124,7 @@ def main():
     prm = c3sim.CoResidentParams()
     prm.gemm_compute_bound, prm.comm, prm.rate_exponent = pg_cb, pc, g
     prm.comm_all_to_all = pc_a2a if pc_a2a and pc_a2a != pc else 0.0
+    prm.all_gather_by_ranks = True
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     with open(out, "w") as f:
         f.write(c3sim.save_coresident_params(prm))
