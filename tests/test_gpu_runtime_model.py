@@ -38,6 +38,7 @@ def cores_unit_comm(tmp_path):
     import c3sim
     p = c3sim.load_coresident_params(CORES)
     p.comm = 1.0
+    p.all_gather_by_ranks = False  # factor exactly 1 at any world size
     f = tmp_path / "cores.json"
     f.write_text(c3sim.save_coresident_params(p))
     return str(f)
@@ -77,6 +78,7 @@ def test_collective_cta_cost_factor_moves_the_pick(c3, session, tmp_path):
     sms = w.info.sm_count
     prm = c3sim.load_coresident_params(CORES)
     prm.comm = pc = 1.6  # the all-gather kernel's factor for this session
+    prm.all_gather_by_ranks = False
     f = tmp_path / "cores.json"
     f.write_text(c3sim.save_coresident_params(prm))
     s.load_coresident(str(f))
