@@ -76,8 +76,17 @@ struct GemmPlan {
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
                    int64_t k, int* counters, int sm_count, int elem_bytes = 2);
 struct FusedComm;
+// A rows that land while the GEMM runs (c3_session_run_host): flag[b] reaches
+// `epoch` once rows [b * rows_per_flag, (b + 1) * rows_per_flag) of A are in
+// device memory (a stream memop after each piece's copy). The CTA-pair GEMM's
+// TMA producers wait on their tile's band before loading it.
+struct RowGate {
+    const uint32_t* flags = nullptr;
+    uint32_t epoch = 0;
+    int rows_per_flag = 0;
+};
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
-                     const FusedComm* fc = nullptr);
+                     const FusedComm* fc = nullptr, const RowGate* gate = nullptr);
 
 // ------------------------------------------------------------ collectives
 // Cross-process completion signalling for the SM-driven collectives.

@@ -351,7 +351,8 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStre
 
 }  // namespace
 
-int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc);
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc,
+                     const RowGate* gate);
 
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
                    int64_t k, int* counters, int sm_count, int elem_bytes) {
@@ -419,7 +420,7 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
 }
 
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
-                     const FusedComm* fc) {
+                     const FusedComm* fc, const RowGate* gate) {
     int grid = max_ctas > 0 ? max_ctas : sm_count;
     grid = std::min(grid, sm_count);
     const bool pair = plan->kind == GemmPlan::kPair || plan->kind == GemmPlan::kPair512;
@@ -428,12 +429,13 @@ int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStrea
     if (pair && grid >= 2) {
         // whole CTA pairs; a fused launch keeps every pair (its copy warps move data)
         grid = fc ? grid / 2 * 2 : std::min(grid / 2, plan->num_tiles) * 2;
-        return gemm_pair_launch(plan, grid, stream, fc);
+        return gemm_pair_launch(plan, grid, stream, fc, gate);
     }
     if (plan->elem == 4) {
         if (plan->kind == GemmPlan::kWide) return launch_bn<256, true>(plan, plan->map_b256, grid, stream);
         return launch_bn<128, true>(plan, plan->map_b128, grid, stream);
     }
+    if (gate && gate->flags) return set_error(C3_ERR_UNSUPPORTED, "row-gated GEMM needs the CTA-pair kernel");
     if (plan->kind == GemmPlan::kWide) return launch_bn<256, false>(plan, plan->map_b256, grid, stream);
     return launch_bn<128, false>(plan, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap
 }

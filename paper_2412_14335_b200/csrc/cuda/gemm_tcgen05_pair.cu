@@ -101,8 +101,21 @@ struct Params {
     // (u in [full_tiles, num_units)), so an underfilled last wave takes half a
     // tile's time. full_tiles = num_units = num_tiles when not split.
     int full_tiles, num_units;
+    RowGate gate;  // A rows landing during the launch (flags == nullptr: all resident)
     FusedComm fc;  // only read by the FUSED instantiation
 };
+
+// Wait until A's row band `band` has landed (RowGate). Bounded: after 2 s the
+// producer proceeds (wrong data, caught by the caller's checks) rather than
+// hang the GPU on a flag that never comes.
+__device__ __forceinline__ void wait_row_band(const RowGate& g, int band) {
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_sys(g.flags + band) < g.epoch) {
+        if (global_ns() - t0 > 2000000000ull) break;
+        __nanosleep(500);
+    }
+    fence_proxy_async_global();  // the TMA loads that follow read what the flag published
+}
 
 // claim u -> tile and half (-1 = the whole tile, 0/1 = its 256-column half)
 __device__ __forceinline__ void unit_tile(const Params& p, int u, int& tile, int& half) {
@@ -368,6 +381,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint64_t pol_b = policy_by_kind(p.pol_b);
         int stage = 0;
         uint32_t phase = 0;
+        int band_ready = -1;  // A row bands known resident (they land in order)
         int tile = leader ? atomicAdd(p.tile_counter, 1) : 0;
         for (int i = 0;; ++i) {
             const int r = i % RING;
@@ -390,6 +404,13 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             unit_tile(p, tile, t_idx, half);
             tile_coords(p, t_idx, tm, tn);
             const int a_row = tm * BM + static_cast<int>(rank) * 128;
+            if (p.gate.flags != nullptr) {
+                const int band = a_row / p.gate.rows_per_flag;
+                if (band > band_ready) {
+                    wait_row_band(p.gate, band);
+                    band_ready = band;
+                }
+            }
             // + 256 per half; a half tile loads only its own 256 B rows, into slot 0
             const int b_row = tn * BN + (half > 0 ? 256 : 0) + static_cast<int>(rank) * 128;
             const int halves = half < 0 ? Cfg::HALVES : 1;
@@ -683,8 +704,12 @@ int launch_pair(const GemmPlan* plan, gemm2::Params p, int grid, cudaStream_t st
 
 }  // namespace
 
-int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc) {
+int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc,
+                     const RowGate* gate) {
     gemm2::Params p;
+    p.gate = gate ? *gate : RowGate{};
+    if (p.gate.flags && p.gate.rows_per_flag < 128)
+        return set_error(C3_ERR_VALIDATION, "row gate: rows_per_flag must be >= 128");
     p.m = static_cast<int>(plan->m);
     p.n = static_cast<int>(plan->n);
     p.k = static_cast<int>(plan->k);

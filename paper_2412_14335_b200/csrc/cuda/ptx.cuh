@@ -347,6 +347,7 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
 }
 __device__ __forceinline__ void fence_sys() { asm volatile("fence.acq_rel.sys;" ::: "memory"); }
 
+
 // Link-rate governor (NVLink emulation in loopback worlds, c3_session_set_link_rate):
 // the caller has moved `sent` bytes since `t0` at a budget of `bytes_per_ns`;
 // sleep until that volume fits under the budget. Global timer, so the pace does

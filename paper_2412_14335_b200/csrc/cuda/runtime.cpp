@@ -332,6 +332,8 @@ struct c3_session {
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
                 ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
     cudaStream_t h2d_s = nullptr;             // c3_session_run_host: the host-input copies
+    uint32_t* a_flags = nullptr;              // ... A row bands landed (RowGate), kMaxAPieces words
+    uint32_t a_epoch = 0;
     cudaEvent_t ev_piece[8] = {};             // ... one per landed piece of the collective's input
     c3sim::MachineDescriptor md;
     c3sim::SlowdownTableSet tables;
@@ -387,6 +389,8 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming));
     for (cudaEvent_t& e : s->ev_piece) C3_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     C3_CUDA(cudaStreamCreateWithFlags(&s->h2d_s, cudaStreamNonBlocking));
+    C3_CUDA(cudaMalloc(&s->a_flags, 64 * sizeof(uint32_t)));
+    C3_CUDA(cudaMemset(s->a_flags, 0, 64 * sizeof(uint32_t)));
     return C3_OK;
 }
 
@@ -893,6 +897,7 @@ int c3_session_destroy(c3_session* s) {
     for (cudaEvent_t e : s->ev_piece)
         if (e) cudaEventDestroy(e);
     if (s->h2d_s) cudaStreamDestroy(s->h2d_s);
+    if (s->a_flags) cudaFree(s->a_flags);
     for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end, s->ev_h2d})
         if (e) cudaEventDestroy(e);
     delete s;
@@ -1396,6 +1401,22 @@ void piece_range(const c3_session* s, int pieces, int k, int64_t* off, int64_t* 
     *off = pb * k;
     *len = k == pieces - 1 ? s->chunk - *off : pb;
 }
+// A in row bands (C3_H2D_A_PIECES, default 4; multiples of the pair tile's
+// 256 rows): the CTA-pair GEMM starts on the first band while the rest cross
+// PCIe (RowGate). 0 bands = A copied whole before the GEMM (other kernels).
+int a_row_bands(const c3_session* s, int* rows_per_band) {
+    static const int env = [] {
+        const char* e = std::getenv("C3_H2D_A_PIECES");
+        const int v = e ? std::atoi(e) : 0;
+        return v > 0 ? std::min(v, 32) : 4;
+    }();
+    const bool pair = s->gemm.kind == GemmPlan::kPair || s->gemm.kind == GemmPlan::kPair512;
+    if (!pair || env < 2 || !drv().StreamWriteValue32) return 0;
+    const int64_t rows = ((s->d.m + env - 1) / env + 255) / 256 * 256;
+    *rows_per_band = static_cast<int>(rows);
+    return static_cast<int>((s->d.m + rows - 1) / rows);
+}
+
 // bytes [off, off + len) of every slot of the collective's input
 int h2d_send_piece(c3_session* s, const HostIO* io, int64_t off, int64_t len, cudaStream_t st) {
     int64_t bytes = 0;
@@ -1542,10 +1563,29 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         // and the collective overlaps the remaining copies.
         const bool send_in = io && io->send && do_comm;
         const int pieces = send_in ? (backend == C3_BACKEND_CU ? h2d_pieces(s) : 1) : 0;
+        RowGate gate;
+        const int a_bands = io && io->a && do_gemm && !rp ? a_row_bands(s, &gate.rows_per_flag) : 0;
+        if (a_bands > 0) {
+            gate.flags = s->a_flags;
+            gate.epoch = ++s->a_epoch;
+        }
         if (io) {
             C3_CUDA(cudaStreamWaitEvent(s->h2d_s, s->ev_start, 0));
             const auto copy_a = [&]() -> int {
                 if (!io->a) return C3_OK;
+                if (a_bands > 0) {  // in row bands, each published by a flag the GEMM waits on
+                    const size_t row_bytes = static_cast<size_t>(s->d.k * s->elem);
+                    for (int b = 0; b < a_bands; ++b) {
+                        const int64_t r0 = static_cast<int64_t>(b) * gate.rows_per_flag;
+                        const int64_t nr = std::min<int64_t>(gate.rows_per_flag, s->d.m - r0);
+                        C3_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(s->a) + r0 * row_bytes,
+                                                static_cast<const uint8_t*>(io->a) + r0 * row_bytes,
+                                                static_cast<size_t>(nr) * row_bytes, cudaMemcpyDefault, s->h2d_s));
+                        C3_CU(StreamWriteValue32, reinterpret_cast<CUstream>(s->h2d_s),
+                              reinterpret_cast<CUdeviceptr>(s->a_flags + b), gate.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+                    }
+                    return C3_OK;
+                }
                 C3_TRY(h2d_a(s, io, s->h2d_s));
                 C3_CUDA(cudaEventRecord(s->ev_h2d, s->h2d_s));
                 C3_CUDA(cudaStreamWaitEvent(gs, s->ev_h2d, 0));
@@ -1571,7 +1611,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         const auto launch_gemm = [&]() -> int {
             C3_CUDA(cudaEventRecord(s->ev_gs, gs));
             if (do_gemm) {
-                C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs));
+                C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs, nullptr, a_bands > 0 ? &gate : nullptr));
                 ++launches;
             }
             C3_CUDA(cudaEventRecord(s->ev_ge, gs));

@@ -682,3 +682,38 @@ def test_cfg1_fp32_session(torch_mod, c3, strategy):
     assert np.array_equal(out.numpy().view(np.float32), cm)
     s.close()
     w.close()
+
+
+@pytest.mark.parametrize("kernel", ["pair", "pair512"])
+@pytest.mark.parametrize("strategy", ["C3_BASE", "C3_SP", "GEMM_ONLY"])
+@pytest.mark.parametrize("M,a_pieces", [(1024, "4"), (1000, "3"), (2048, "8")])
+def test_run_host_row_gated_gemm(torch_mod, c3, monkeypatch, kernel, strategy, M, a_pieces):
+    """c3_session_run_host with the CTA-pair GEMM: A lands in row bands, each
+    published by a stream-memop flag the GEMM's TMA producers wait on, so the
+    GEMM starts on the first band. C must be bit-identical to the
+    device-resident run (ragged last band included)."""
+    torch = torch_mod
+    monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
+    monkeypatch.setenv("C3_H2D_A_PIECES", a_pieces)  # read once per process: the first value sticks
+    st = getattr(c3, strategy)
+    n, N, K = 8, 1536, 512
+    payload = n * (5 << 20)
+    w = c3.World(0, n, 0, loopback=True)
+    s = c3.Session(w, M, N, K, c3.ALL_GATHER, payload)
+    s.fill(SEED)
+    p0 = s.pointers(0)
+    a_h = _d2h_np(c3, p0.a, p0.a_bytes)
+    send_h = _d2h_np(c3, p0.send, p0.send_bytes)
+    c_bytes = M * N * 2
+    s.run(st, None)
+    c_ref = _d2h_np(c3, p0.c, c_bytes)
+    for rep in range(3):  # repeated steps: the flags' epochs advance
+        _h2d(c3, p0.c, np.zeros(c_bytes, np.uint8))
+        _h2d(c3, p0.a, np.zeros(p0.a_bytes, np.uint8))
+        pin_a = torch.from_numpy(a_h).pin_memory()
+        pin_s = torch.from_numpy(send_h).pin_memory()
+        pin_o = torch.zeros(c_bytes, dtype=torch.uint8).pin_memory()
+        s.run_host(st, None, pin_a.data_ptr(), pin_s.data_ptr(), pin_o.data_ptr(), c_bytes)
+        assert np.array_equal(pin_o.numpy(), c_ref), rep
+    s.close()
+    w.close()
