@@ -1394,6 +1394,8 @@ int h2d_pieces(const c3_session* s) {
         const int v = e ? std::atoi(e) : 0;
         return v > 0 ? std::min(v, 8) : 4;
     }();
+    // strided all-to-all slot ranges need 16-byte slots (launch_alltoall_push)
+    if (s->d.collective == C3_ALL_TO_ALL && s->chunk % 16 != 0) return 1;
     return s->chunk >= (int64_t{4} << 20) ? env : 1;
 }
 void piece_range(const c3_session* s, int pieces, int k, int64_t* off, int64_t* len) {

@@ -525,7 +525,7 @@ def _d2h_np(c3, ptr, nbytes):
 
 @pytest.mark.parametrize("collective", [0, 1, 2], ids=["all-gather", "all-to-all", "reduce-scatter"])
 @pytest.mark.parametrize("strategy", ["SERIAL", "C3_BASE", "C3_SP", "CONCCL", "FUSED"])
-@pytest.mark.parametrize("slot_mib", [1, 5])
+@pytest.mark.parametrize("slot_mib", [1, 5, "5odd"])
 def test_run_host_matches_device_run(torch_mod, c3, monkeypatch, collective, strategy, slot_mib):
     """c3_session_run_host: A and this rank's collective input copied in from
     pinned host memory, C read back inside the step. The device state after
@@ -536,11 +536,16 @@ def test_run_host_matches_device_run(torch_mod, c3, monkeypatch, collective, str
     torch = torch_mod
     if strategy == "FUSED" and collective == 2:
         pytest.skip("fused C3 moves all-gather / all-to-all data only")
+    if strategy == "FUSED" and slot_mib == "5odd":
+        pytest.skip("fused C3 needs 16-byte slots")
     if strategy == "FUSED":
         monkeypatch.setenv("C3_GEMM_KERNEL", "pair")  # fused needs the CTA-pair GEMM
     st = getattr(c3, strategy)
     n, M, N, K = 8, 512, 1024, 512
-    payload = n * ((slot_mib << 20) + 4096 * 3 + 16 * 5)  # pieces of 4 KiB multiples + a remainder
+    if slot_mib == "5odd":  # slots not 16-byte aligned (the all-to-all keeps one piece)
+        payload = n * ((5 << 20) + 4096 * 3 + 2 * 5)
+    else:
+        payload = n * ((slot_mib << 20) + 4096 * 3 + 16 * 5)  # pieces of 4 KiB multiples + a remainder
     w = c3.World(0, n, 0, loopback=True)
     s = c3.Session(w, M, N, K, collective, payload)
     s.fill(SEED)
