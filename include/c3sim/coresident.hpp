@@ -63,6 +63,10 @@ struct CoResidentParams {
     /// (measured: n = 2 / 4 / 8 fit 1.8 / 1.1 / 1.0, profiles/r01_size_sweep.csv).
     /// Beside a memory-bound GEMM (single-CTA tiles, light issue load) it stays `comm`.
     bool all_gather_by_ranks = false;
+    /// The collective CTA's factor beside a memory-bound GEMM (single-CTA
+    /// tiles: light issue and register pressure), any collective class;
+    /// 0 = the class factor. Measured ~1.0 (RMS 30% -> 12% over 228 rows).
+    double comm_memory_bound = 0.0;
 
     double gemm(KernelClass gemm_class) const {
         return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
@@ -72,6 +76,7 @@ struct CoResidentParams {
     }
     /// n_ranks <= 1: no rank dependence (the class factor above).
     double comm_factor(KernelClass comm_class, int n_ranks, KernelClass gemm_class) const {
+        if (gemm_class == KernelClass::GemmMemoryBound && comm_memory_bound > 0.0) return comm_memory_bound;
         if (comm_class != KernelClass::AllGather || !all_gather_by_ranks || n_ranks <= 1 ||
             gemm_class == KernelClass::GemmMemoryBound)
             return comm_factor(comm_class);
@@ -85,7 +90,8 @@ void validate(const CoResidentParams& p);
 
 /// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc,
 ///        "comm-all-to-all": pc (optional), "rate-exponent": g (optional, default 1),
-///        "all-gather-by-ranks": bool (optional, default false)}.
+///        "all-gather-by-ranks": bool (optional, default false),
+///        "comm-memory-bound": pc (optional, 0 = the class factor)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 

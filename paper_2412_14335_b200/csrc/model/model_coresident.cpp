@@ -53,6 +53,8 @@ void validate(const CoResidentParams& p) {
         if (!(v >= 1.0) || !std::isfinite(v)) throw ValidationError("co-resident penalties must be finite and >= 1");
     if (!(p.comm_all_to_all == 0.0 || (p.comm_all_to_all >= 1.0 && std::isfinite(p.comm_all_to_all))))
         throw ValidationError("co-resident all-to-all cost factor must be 0 (= comm) or >= 1");
+    if (!(p.comm_memory_bound == 0.0 || (p.comm_memory_bound >= 1.0 && std::isfinite(p.comm_memory_bound))))
+        throw ValidationError("co-resident memory-bound cost factor must be 0 (= class factor) or >= 1");
     if (!(p.rate_exponent > 0) || !std::isfinite(p.rate_exponent))
         throw ValidationError("co-resident rate exponent must be finite and > 0");
 }
@@ -76,6 +78,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.rate_exponent = j.value("rate-exponent", 1.0);
         p.comm_all_to_all = j.value("comm-all-to-all", 0.0);
         p.all_gather_by_ranks = j.value("all-gather-by-ranks", false);
+        p.comm_memory_bound = j.value("comm-memory-bound", 0.0);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -90,6 +93,7 @@ std::string save_coresident_params(const CoResidentParams& p) {
               {"comm-all-to-all", p.comm_all_to_all},
               {"rate-exponent", p.rate_exponent}};
     if (p.all_gather_by_ranks) j["all-gather-by-ranks"] = true;
+    if (p.comm_memory_bound > 0.0) j["comm-memory-bound"] = p.comm_memory_bound;
     return j.dump(2) + "\n";
 }
 

@@ -146,6 +146,22 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
     assert got["comm-all-to-all"] == pytest.approx(2.0, abs=0.051)
     assert got["rate-exponent"] == pytest.approx(1.5, abs=0.01)
     assert got["all-gather-by-ranks"] is True
+    assert got["comm-memory-bound"] == 1.0
+
+
+def test_comm_factor_beside_memory_bound_gemm():
+    """comm_memory_bound: beside a memory-bound GEMM every collective class
+    uses that factor; 0 keeps the class factor."""
+    p = c3sim.CoResidentParams()
+    p.comm, p.comm_all_to_all = 1.0, 2.1
+    A2A, MBc = c3sim.KernelClass.ALL_TO_ALL, c3sim.KernelClass.GEMM_MEMORY_BOUND
+    assert c3sim.coresident_comm_ctas(42, p, A2A, 8, MBc) == 20
+    p.comm_memory_bound = 1.0
+    assert c3sim.coresident_comm_ctas(42, p, A2A, 8, MBc) == 42
+    assert c3sim.coresident_comm_ctas(42, p, A2A, 8, CB) == 20
+    p.comm_memory_bound = 0.5
+    with pytest.raises(Exception):
+        c3sim.coresident_comm_ctas(42, p, A2A, 8, MBc)
 
 
 def test_all_gather_factor_by_ranks():
