@@ -84,6 +84,7 @@ struct RowGate {
     const uint32_t* flags = nullptr;
     uint32_t epoch = 0;
     int rows_per_flag = 0;
+    uint32_t* timed_out = nullptr;  // set to 1 by a producer whose bounded wait expired
 };
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
                      const FusedComm* fc = nullptr, const RowGate* gate = nullptr);

@@ -106,12 +106,15 @@ struct Params {
 };
 
 // Wait until A's row band `band` has landed (RowGate). Bounded: after 2 s the
-// producer proceeds (wrong data, caught by the caller's checks) rather than
-// hang the GPU on a flag that never comes.
+// producer records the timeout and proceeds (the host then fails the step)
+// rather than hang the GPU on a flag that never comes.
 __device__ __forceinline__ void wait_row_band(const RowGate& g, int band) {
     const uint64_t t0 = global_ns();
     while (ld_acquire_sys(g.flags + band) < g.epoch) {
-        if (global_ns() - t0 > 2000000000ull) break;
+        if (global_ns() - t0 > 2000000000ull) {
+            if (g.timed_out) atomicExch(g.timed_out, 1u);  // the host fails the step loudly
+            break;
+        }
         __nanosleep(500);
     }
     fence_proxy_async_global();  // the TMA loads that follow read what the flag published

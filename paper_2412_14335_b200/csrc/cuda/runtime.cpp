@@ -332,7 +332,7 @@ struct c3_session {
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
                 ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
     cudaStream_t h2d_s = nullptr;             // c3_session_run_host: the host-input copies
-    uint32_t* a_flags = nullptr;              // ... A row bands landed (RowGate), kMaxAPieces words
+    uint32_t* a_flags = nullptr;              // ... A row bands landed (RowGate); word 63: gate timed out
     uint32_t a_epoch = 0;
     cudaEvent_t ev_piece[8] = {};             // ... one per landed piece of the collective's input
     c3sim::MachineDescriptor md;
@@ -1406,6 +1406,7 @@ void piece_range(const c3_session* s, int pieces, int k, int64_t* off, int64_t* 
 // A in row bands (C3_H2D_A_PIECES, default 4; multiples of the pair tile's
 // 256 rows): the CTA-pair GEMM starts on the first band while the rest cross
 // PCIe (RowGate). 0 bands = A copied whole before the GEMM (other kernels).
+constexpr int kGateTimeoutWord = 63;  // a_flags[63]; bands use words [0, 32)
 int a_row_bands(const c3_session* s, int* rows_per_band) {
     static const int env = [] {
         const char* e = std::getenv("C3_H2D_A_PIECES");
@@ -1543,6 +1544,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     const int backend = strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA
                         : strategy == C3_COMM_ONLY_CU ? C3_BACKEND_CU
                                                       : a.backend;
+    bool gated = false;  // A arrives in row bands the GEMM waits on (RowGate)
     if (strategy == C3_SERIAL) {
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
         C3_TRY(h2d_a(s, io, gs));
@@ -1570,6 +1572,8 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         if (a_bands > 0) {
             gate.flags = s->a_flags;
             gate.epoch = ++s->a_epoch;
+            gate.timed_out = s->a_flags + kGateTimeoutWord;
+            gated = true;
         }
         if (io) {
             C3_CUDA(cudaStreamWaitEvent(s->h2d_s, s->ev_start, 0));
@@ -1652,6 +1656,14 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     C3_CUDA(cudaEventRecord(s->ev_end, s->main));
     C3_CUDA(cudaEventSynchronize(s->ev_end));
     C3_CUDA(cudaGetLastError());
+    if (gated) {
+        uint32_t to = 0;
+        C3_CUDA(cudaMemcpy(&to, s->a_flags + kGateTimeoutWord, sizeof to, cudaMemcpyDeviceToHost));
+        if (to != 0) {
+            C3_CUDA(cudaMemset(s->a_flags + kGateTimeoutWord, 0, sizeof to));
+            return set_error(C3_ERR_CUDA, "c3_session_run_host: A row band never landed (row gate timed out)");
+        }
+    }
     t->gemm_start_ms = elapsed(s->ev_start, s->ev_gs);
     t->gemm_end_ms = elapsed(s->ev_start, s->ev_ge);
     t->comm_start_ms = elapsed(s->ev_start, s->ev_cs);
