@@ -1567,6 +1567,10 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         // and the collective overlaps the remaining copies.
         const bool send_in = io && io->send && do_comm;
         const int pieces = send_in ? (backend == C3_BACKEND_CU ? h2d_pieces(s) : 1) : 0;
+        // comm pacing spreads a device-resident collective over the GEMM; a
+        // collective whose input arrives over PCIe in pieces is already spread,
+        // and pacing each piece from its own start would only stretch the tail
+        if (pieces > 1) s->run_gbps = s->link_gbps;
         RowGate gate;
         const int a_bands = io && io->a && do_gemm && !rp ? a_row_bands(s, &gate.rows_per_flag) : 0;
         if (a_bands > 0) {
