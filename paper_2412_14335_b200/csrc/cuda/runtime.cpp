@@ -1387,12 +1387,13 @@ int h2d_a(c3_session* s, const HostIO* io, cudaStream_t st) {
 }
 // Pieces of the collective's host input in a pipelined concurrent step: each
 // piece's copy is followed by the collective on that piece while the next
-// piece crosses PCIe (C3_H2D_PIECES, default 4; 1 below 4 MiB slots).
+// piece crosses PCIe (C3_H2D_PIECES, default 8: the last piece's collective is
+// the exposed tail; 1 below 4 MiB slots). profiles/r01_e2e_pieces.txt
 int h2d_pieces(const c3_session* s) {
     static const int env = [] {
         const char* e = std::getenv("C3_H2D_PIECES");
         const int v = e ? std::atoi(e) : 0;
-        return v > 0 ? std::min(v, 8) : 4;
+        return v > 0 ? std::min(v, 8) : 8;
     }();
     // strided all-to-all slot ranges need 16-byte slots (launch_alltoall_push)
     if (s->d.collective == C3_ALL_TO_ALL && s->chunk % 16 != 0) return 1;
