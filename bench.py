@@ -353,10 +353,13 @@ def run_ours(args, dist):
     def emulated_candidates(co_ctas):
         # the collective paced to the link rate on nvl_ctas CTAs (the SM
         # footprint of a link-bound P2P kernel); fused: the GEMM's copy warps paced
-        part = max(8, nvl_ctas)
+        # green-context partitions come in multiples of the SM grain (8 on
+        # B200): the comm group is the rate-matched count rounded up to it
+        g = max(1, world.info.sm_grain)
+        part = -(-max(8, nvl_ctas) // g) * g
         cands = [coresident(c3.SERIAL, full, nvl_ctas), coresident(c3.C3_BASE, full, nvl_ctas),
-                 coresident(c3.C3_SP, full, nvl_ctas), coresident(c3.C3_RP, full - part, nvl_ctas),
-                 coresident(c3.C3_SP_RP, full - part, nvl_ctas)]
+                 coresident(c3.C3_SP, full, nvl_ctas), coresident(c3.C3_RP, full - part, part),
+                 coresident(c3.C3_SP_RP, full - part, part)]
         # more co-resident CTA units: a co-resident unit moves less than an
         # isolated one (the model's cost factor), so the rate-matched count is
         # a floor, not the choice

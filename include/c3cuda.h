@@ -37,6 +37,10 @@ extern "C" {
 #define C3_ERR_CUDA 100
 #define C3_ERR_DRIVER 101
 #define C3_ERR_UNSUPPORTED 102
+/* A bounded device-side cross-rank wait expired (C3_WAIT_TIMEOUT_MS, default
+ * 2000): a peer process is dead or ran a mismatched step. The step's results
+ * are undefined; destroy the session. */
+#define C3_ERR_TIMEOUT 103
 
 #define C3_MAX_RANKS 8
 #define C3_IPC_HANDLE_BYTES 64
@@ -256,12 +260,18 @@ int c3_session_run_host(c3_session* s, int strategy, const c3_alloc* alloc, cons
 /* Loopback parity form: every virtual rank's share of the collective runs (the
  * plain call runs rank 0's share only, the per-GPU load of a real world). */
 int c3_session_run_all_ranks(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);
-/* Cross-rank completion of the copy-engine collective is host-side (the
- * copies are host-issued, as in the paper's ConCCL): a multi-process session
- * running a DMA strategy calls `fn(ctx)` (e.g. a torch.distributed barrier)
- * once per step after its own copies drained, and before the local reduce of
- * a reduce-scatter. Return 0 on success. Not needed for loopback worlds or
- * the SM (P2P) collectives, which signal through peer flags on the device. */
+/* Cross-rank completion is device-side for every backend: the SM
+ * collectives signal through peer flag words; the copy-engine collectives
+ * (conccl / conccl_rp) write a delivery flag into each destination rank's
+ * signal words from every engine stream after its copies (stream memop), and
+ * the receiver waits on the device (a one-warp kernel, or the reduce-scatter's
+ * local reduce) — nothing blocks the host, so the GEMM is launched at once.
+ * All-gather / all-to-all (SM, fused or copy-engine) first pass an entry
+ * barrier: no rank writes into a peer's receive buffer before that peer has
+ * entered the same step. The copy-engine reduce-scatter stages into two
+ * buffers by step parity. Every wait is bounded (c3_session_set_wait_timeout;
+ * C3_ERR_TIMEOUT). c3_session_set_barrier is kept for source compatibility:
+ * the callback is no longer called. */
 typedef int (*c3_barrier_fn)(void* ctx);
 /* C3_FUSED pacing: the copies of each CTA finish after this share of the
  * GEMM's operand loads (default 0 = as fast as possible); piece_bytes =
@@ -282,6 +292,9 @@ int c3_session_set_fused_pace(c3_session* s, float pace, int piece_bytes);
  * transfers are not paced. */
 int c3_session_set_link_rate(c3_session* s, double gbps);
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx);
+/* Bound of every device-side cross-rank wait of this session, in ms
+ * (default 2000, or C3_WAIT_TIMEOUT_MS). */
+int c3_session_set_wait_timeout(c3_session* s, double ms);
 /* Runtime heuristic (the paper's strategy choice, on the product model layer):
  * load measured interference tables (reference SlowdownTable CSV,
  * interference.hpp:57-61; data/b200-*-slowdown-tables.csv), then predict every

@@ -126,8 +126,8 @@ class Session:
         check(lib().c3_session_import(self.h, C.create_string_buffer(joined, len(joined))))
 
     def set_barrier(self, fn):
-        """Host barrier for copy-engine collectives across processes:
-        fn() -> None (e.g. torch.distributed.barrier)."""
+        """Kept for source compatibility: cross-rank completion of every
+        backend is device-side now and the callback is not called."""
         def _cb(_ctx):
             try:
                 fn()
@@ -136,6 +136,11 @@ class Session:
                 return 1
         self._barrier_cb = _capi.BARRIER_FN(_cb)  # keep alive
         check(lib().c3_session_set_barrier(self.h, C.cast(self._barrier_cb, C.c_void_p), None))
+
+    def set_wait_timeout(self, ms):
+        """Bound (ms) of every device-side cross-rank wait; an expired wait
+        fails the step with C3Error code 103 (Timeout)."""
+        check(lib().c3_session_set_wait_timeout(self.h, float(ms)))
 
     def load_tables(self, csv_path):
         check(lib().c3_session_load_tables(self.h, csv_path.encode()))

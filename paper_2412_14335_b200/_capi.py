@@ -15,7 +15,7 @@ CLI = os.path.join(_HERE, "bin", "c3sim")
 
 C3_OK = 0
 ERR_NAMES = {2: "IoError", 3: "UnknownEntityError", 4: "ValidationError", 5: "FitError",
-             100: "CudaError", 101: "DriverError", 102: "Unsupported"}
+             100: "CudaError", 101: "DriverError", 102: "Unsupported", 103: "Timeout"}
 
 ALL_GATHER, ALL_TO_ALL, REDUCE_SCATTER = 0, 1, 2
 SERIAL, C3_BASE, C3_SP, C3_RP, C3_SP_RP, CONCCL, CONCCL_RP = range(7)
@@ -108,6 +108,7 @@ SIGNATURES = {
     "c3_session_run_host": (I, [P, I, C.POINTER(Alloc), P, P, P, I64, C.POINTER(Timing)]),
     "c3_session_default_alloc": (I, [P, I, C.POINTER(Alloc)]),
     "c3_session_set_barrier": (I, [P, C.c_void_p, P]),
+    "c3_session_set_wait_timeout": (I, [P, C.c_double]),
     "c3_session_set_fused_pace": (I, [P, C.c_float, I]),
     "c3_session_set_link_rate": (I, [P, C.c_double]),
     "c3_session_load_tables": (I, [P, C.c_char_p]),

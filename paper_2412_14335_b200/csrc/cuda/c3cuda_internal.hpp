@@ -84,26 +84,52 @@ struct RowGate {
     const uint32_t* flags = nullptr;
     uint32_t epoch = 0;
     int rows_per_flag = 0;
-    uint32_t* timed_out = nullptr;  // set to 1 by a producer whose bounded wait expired
+    uint32_t* timed_out = nullptr;  // error word: kWaitRowGate once a producer's bounded wait expired
 };
 int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStream_t stream,
                      const FusedComm* fc = nullptr, const RowGate* gate = nullptr);
 
 // ------------------------------------------------------------ collectives
-// Cross-process completion signalling for the SM-driven collectives.
-// `mine` is this rank's flag array (C3_MAX_RANKS x 2 words: [entry, exit]
-// per source rank), `peers[p]` rank p's array (peer-mapped). `done` is a
-// device counter (one per launch site) used to elect the last CTA.
+// Cross-process completion signalling. Every session owns a signal array of
+// kSigWords u32 words; rank p's array is peer-mapped. A slot is C3_MAX_RANKS
+// words, word [slot + g] is written by rank g only (st.release.sys, or a
+// stream memop after a copy-engine batch) with the step's epoch; readers poll
+// with ld.acquire.sys. Epochs only grow, so nothing is ever reset.
+constexpr int kSigWords = 64;
+constexpr int kSigPushExit = 0;    // all-gather / all-to-all push: my stores into you are done
+constexpr int kSigRsEntry = 8;     // reduce-scatter pull: my input is ready
+constexpr int kSigRsExit = 16;     // reduce-scatter pull: I finished reading your input
+constexpr int kSigCeDone = 24;     // copy engines: my copies into your buffer have landed
+constexpr int kSigPushEntry = 32;  // push / copy-engine entry: your previous result may be overwritten
+constexpr int kFusedExitSlot = 40; // fused C3: my copy warps' stores into you are done
+constexpr int kSigFusedEntry = 48; // fused C3 entry
+// Error word codes (Signals::err, mapped host memory the host reads after a step)
+constexpr uint32_t kWaitEntry = 1, kWaitExit = 2, kWaitCeDone = 3, kWaitFusedExit = 4,
+                   kWaitFusedEntry = 5, kWaitRowGate = 6;
+// Default bound of every device-side cross-rank wait (C3_WAIT_TIMEOUT_MS).
+constexpr uint64_t kDefaultWaitNs = 2000000000ull;
+
+// `mine` is this rank's flag array, `peers[p]` rank p's (peer-mapped). `done`
+// is a device counter (one per launch site) used to elect the last CTA.
 struct Signals {
     uint32_t* mine = nullptr;
     uint32_t* peers[C3_MAX_RANKS] = {};
     uint32_t* done = nullptr;
-    uint32_t epoch = 0;
+    uint32_t epoch = 0;        // exit / delivery epoch
+    uint32_t entry_epoch = 0;  // entry barrier epoch
     bool enabled = false;
+    int self = 0;  // this rank (the kernels' data-indexing `self` may differ: local reduce)
+    // entry: wait until every peer wrote >= epoch into mine[entry_slot + p]
+    // (entry_post: first post epoch into peers[p][entry_slot + self]; false =
+    // wait only, for flags written by the peers' copy-engine streams).
+    int entry_slot = -1;
+    bool entry_post = true;
+    int exit_slot = -1;  // last-CTA exit barrier slot (-1: none)
+    uint32_t* err = nullptr;  // set to a kWait* code when a wait expires
+    uint64_t timeout_ns = kDefaultWaitNs;
 };
 
 // Fused C3 (collective moved by the GEMM's own copy warp + TMA unit).
-constexpr int kFusedExitSlot = 40;  // signal-array words [40,48)
 struct FusedComm {
     int enabled = 0;
     int kind = 0;                    // 0 all-gather, 1 all-to-all
@@ -139,6 +165,13 @@ int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& r
 int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, int64_t count,
                                int n_ctas, const Signals& sig, cudaStream_t stream,
                                double link_bpns = 0.0);
+// One-thread kernel running only Signals' entry part (post and/or wait on
+// entry_slot): the copy-engine path's entry barrier and its wait for the
+// peers' delivery flags. Occupies one warp of one SM while it polls.
+int launch_signal_wait(const Signals& sig, int n, cudaStream_t stream);
+// Fallback when stream memops are unavailable: store `value` into each of
+// `count` (peer-mapped) words with st.release.sys, after the stream's prior work.
+int launch_flag_store(uint32_t* const* words, int count, uint32_t value, cudaStream_t stream);
 // fp32 buffer holding the same bf16 values widened (the fp32 GEMM's inputs)
 int launch_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, cudaStream_t stream);
 int launch_fill_bf16(void* dst, int64_t count, uint64_t seed, int rank, int tensor,

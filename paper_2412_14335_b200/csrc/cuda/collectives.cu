@@ -58,44 +58,60 @@ constexpr int kUnrollA2a = C3_A2A_UNROLL;
 #endif
 constexpr int kUnrollAg = C3_AG_UNROLL;
 
+// Bounded wait of one thread until every peer's word [slot + p] of this
+// rank's signal array reached the epoch. A peer that never arrives (dead,
+// or running a mismatched collective) trips the timeout: the thread records
+// `code` in the session's error word and returns, so the step ends and the
+// host fails it instead of the GPU hanging.
+__device__ void wait_peers(const Signals& sig, int n, int slot, uint32_t epoch, uint32_t code) {
+    wait_words_bounded(sig.mine, slot, sig.self, n, epoch, sig.timeout_ns, sig.err, code);
+}
+
 // Last-CTA election + cross-rank exit barrier. Called by every thread of every
 // CTA after its stores; returns after this rank has seen `epoch` from all peers
 // (only the elected CTA waits; the other CTAs exit).
-__device__ void exit_barrier(const Signals& sig, int self, int n, int slot_base) {
+__device__ void exit_barrier(const Signals& sig, int n) {
     __syncthreads();
-    if (threadIdx.x != 0) return;
+    if (threadIdx.x != 0 || sig.exit_slot < 0) return;
     fence_sys();
     const uint32_t ticket = atomicAdd(sig.done, 1u);
     if (ticket != gridDim.x - 1) return;
     fence_sys();
     for (int p = 0; p < n; ++p)
-        if (p != self) st_release_sys(sig.peers[p] + slot_base + self, sig.epoch);
-    for (int p = 0; p < n; ++p)
-        if (p != self)
-            while (ld_acquire_sys(sig.mine + slot_base + p) < sig.epoch) {
-            }
+        if (p != sig.self) st_release_sys(sig.peers[p] + sig.exit_slot + sig.self, sig.epoch);
+    wait_peers(sig, n, sig.exit_slot, sig.epoch, kWaitExit);
     *sig.done = 0;  // next launch on this stream starts from zero
 }
 
-// Entry barrier: every peer has reached this collective (its inputs are ready).
-__device__ void entry_barrier(const Signals& sig, int self, int n, int slot_base) {
+// Entry barrier: every peer has reached this collective (its inputs are
+// ready, or its receive buffer may be overwritten). Block 0 posts; every
+// CTA's thread 0 waits. With entry_post false it only waits (flags written
+// by the peers' copy-engine streams after their copies into this rank).
+__device__ void entry_barrier(const Signals& sig, int n) {
+    if (sig.entry_slot < 0) return;
     if (threadIdx.x == 0) {
-        if (blockIdx.x == 0) {
+        if (blockIdx.x == 0 && sig.entry_post) {
             fence_sys();
             for (int p = 0; p < n; ++p)
-                if (p != self) st_release_sys(sig.peers[p] + slot_base + self, sig.epoch);
+                if (p != sig.self) st_release_sys(sig.peers[p] + sig.entry_slot + sig.self, sig.entry_epoch);
         }
-        for (int p = 0; p < n; ++p)
-            if (p != self)
-                while (ld_acquire_sys(sig.mine + slot_base + p) < sig.epoch) {
-                }
+        wait_peers(sig, n, sig.entry_slot, sig.entry_epoch, sig.entry_post ? kWaitEntry : kWaitCeDone);
     }
     __syncthreads();
 }
 
-// Signal-array layout (words): [0,8) all-gather exit, [8,16) reduce-scatter
-// entry, [16,24) reduce-scatter exit, [24,32) copy-engine exit.
-constexpr int kAgExit = 0, kRsEntry = 8, kRsExit = 16;
+__global__ void __launch_bounds__(32) signal_wait_kernel(Signals sig, int n) {
+    entry_barrier(sig, n);
+}
+
+struct FlagWords {
+    uint32_t* w[C3_MAX_RANKS];
+};
+__global__ void __launch_bounds__(32) flag_store_kernel(FlagWords f, int count, uint32_t value) {
+    if (threadIdx.x != 0) return;
+    fence_sys();
+    for (int i = 0; i < count; ++i) st_release_sys(f.w[i], value);
+}
 
 // V: the access width (uint4 = 16 B, u256 = 32 B: LDG/STG .256), U: vectors
 // in flight per thread; nvec / slot_vec count V-sized vectors.
@@ -104,6 +120,7 @@ __global__ void __launch_bounds__(kVecThreads)
 ag_push_vec_kernel(const V* __restrict__ src, MutPtrTable recv, int self, int n,
                    int64_t nvec, int64_t slot_vec, int copy_self, int stream_l2, float cta_bpns,
                    Signals sig) {
+    if (sig.enabled) entry_barrier(sig, n);  // peers' receive buffers are free
     const uint64_t pol = policy_evict_first();
     V* dst[C3_MAX_RANKS];
 #pragma unroll
@@ -140,7 +157,7 @@ ag_push_vec_kernel(const V* __restrict__ src, MutPtrTable recv, int self, int n,
         }
     }
     if (cta_bpns > 0.f && threadIdx.x == 0) link_wait(t0, sent, cta_bpns);  // the last bytes' link time
-    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+    if (sig.enabled) exit_barrier(sig, n);
 }
 
 // All-gather, push form on the SM's TMA unit: one thread per CTA streams this
@@ -151,6 +168,7 @@ constexpr int kBulkMaxBufs = 8;
 __global__ void __launch_bounds__(32)
 ag_push_bulk_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self, int n, int64_t chunk,
                     int copy_self, int piece, int nbuf, int stream_l2, float cta_bpns, Signals sig) {
+    if (sig.enabled) entry_barrier(sig, n);  // peers' receive buffers are free
     extern __shared__ __align__(128) uint8_t bulk_buf[];
     __shared__ __align__(8) uint64_t bar[kBulkMaxBufs];
     if (threadIdx.x == 0) {
@@ -200,7 +218,7 @@ ag_push_bulk_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
         if (cta_bpns > 0.f) link_wait(t0, sent, cta_bpns);
         (void)targets;
     }
-    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+    if (sig.enabled) exit_barrier(sig, n);
 }
 
 // Byte-granular fallback shape for chunks that are not 16-byte multiples or
@@ -208,6 +226,7 @@ ag_push_bulk_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
 __global__ void __launch_bounds__(kThreads)
 ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self, int n,
                     int64_t chunk, int copy_self, Signals sig) {
+    if (sig.enabled) entry_barrier(sig, n);  // peers' receive buffers are free
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < chunk; i += step) {
         const uint8_t v = src[i];
@@ -216,7 +235,7 @@ ag_push_byte_kernel(const uint8_t* __restrict__ src, MutPtrTable recv, int self,
             static_cast<uint8_t*>(recv.p[p])[chunk * self + i] = v;
         }
     }
-    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+    if (sig.enabled) exit_barrier(sig, n);
 }
 
 // All-to-all, push form (plan_all_to_all's mapping, conccl.cpp:55-84): slot p
@@ -225,6 +244,7 @@ template <typename V, int U>
 __global__ void __launch_bounds__(kVecThreads)
 a2a_push_vec_kernel(const V* __restrict__ send, MutPtrTable recv, int self, int n,
                     int64_t slot_vec, int64_t stride_vec, int stream_l2, float cta_bpns, Signals sig) {
+    if (sig.enabled) entry_barrier(sig, n);  // peers' receive buffers are free
     const uint64_t pol = policy_evict_first();
     const int64_t step = static_cast<int64_t>(gridDim.x) * kVecThreads * U;
     const uint64_t t0 = global_ns();
@@ -256,17 +276,18 @@ a2a_push_vec_kernel(const V* __restrict__ send, MutPtrTable recv, int self, int 
         }
     }
     if (cta_bpns > 0.f && threadIdx.x == 0) link_wait(t0, sent, cta_bpns);
-    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+    if (sig.enabled) exit_barrier(sig, n);
 }
 
 __global__ void __launch_bounds__(kThreads)
 a2a_push_byte_kernel(const uint8_t* __restrict__ send, MutPtrTable recv, int self, int n,
                      int64_t slot, Signals sig) {
+    if (sig.enabled) entry_barrier(sig, n);  // peers' receive buffers are free
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads;
     for (int p = 0; p < n; ++p)
         for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < slot; i += step)
             static_cast<uint8_t*>(recv.p[p])[slot * self + i] = send[slot * p + i];
-    if (sig.enabled) exit_barrier(sig, self, n, kAgExit);
+    if (sig.enabled) exit_barrier(sig, n);
 }
 
 __device__ __forceinline__ void acc_bf16x8(float (&acc)[8], const uint4& v) {
@@ -284,7 +305,7 @@ __global__ void __launch_bounds__(kThreadsRs)
 rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
                    int64_t slot_vec, int stream_l2, float cta_bpns, Signals sig) {
     const uint64_t pol = policy_evict_first();
-    if (sig.enabled) entry_barrier(sig, self, N, kRsEntry);
+    if (sig.enabled) entry_barrier(sig, N);
     const uint4* src[N];
 #pragma unroll
     for (int g = 0; g < N; ++g) src[g] = static_cast<const uint4*>(in.p[g]) + slot_vec * self;
@@ -326,13 +347,13 @@ rs_pull_vec_kernel(PtrTable in, uint4* __restrict__ out, int self, int64_t nvec,
         }
     }
     if (cta_bpns > 0.f && threadIdx.x == 0) link_wait(t0, pulled, cta_bpns);
-    if (sig.enabled) exit_barrier(sig, self, N, kRsExit);
+    if (sig.enabled) exit_barrier(sig, N);
 }
 
 __global__ void __launch_bounds__(kThreads)
 rs_pull_scalar_kernel(PtrTable in, __nv_bfloat16* __restrict__ out, int self, int n, int64_t count,
                       Signals sig) {
-    if (sig.enabled) entry_barrier(sig, self, n, kRsEntry);
+    if (sig.enabled) entry_barrier(sig, n);
     const int64_t step = static_cast<int64_t>(gridDim.x) * kThreads;
     for (int64_t i = static_cast<int64_t>(blockIdx.x) * kThreads + threadIdx.x; i < count; i += step) {
         float acc = 0.f;
@@ -340,7 +361,7 @@ rs_pull_scalar_kernel(PtrTable in, __nv_bfloat16* __restrict__ out, int self, in
             acc = __fadd_rn(acc, __bfloat162float(static_cast<const __nv_bfloat16*>(in.p[g])[count * self + i]));
         out[i] = __float2bfloat16_rn(acc);
     }
-    if (sig.enabled) exit_barrier(sig, self, n, kRsExit);
+    if (sig.enabled) exit_barrier(sig, n);
 }
 
 // ------------------------------------------------------ synthetic inputs ---
@@ -556,6 +577,23 @@ int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, i
         rs_pull_scalar_kernel<<<grid, kThreads, 0, stream>>>(in, static_cast<__nv_bfloat16*>(out),
                                                              self, n, count, sig);
     }
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_signal_wait(const Signals& sig, int n, cudaStream_t stream) {
+    if (!sig.enabled || sig.entry_slot < 0 || n < 2) return C3_OK;
+    signal_wait_kernel<<<1, 32, 0, stream>>>(sig, n);
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
+int launch_flag_store(uint32_t* const* words, int count, uint32_t value, cudaStream_t stream) {
+    if (count <= 0) return C3_OK;
+    if (count > C3_MAX_RANKS) return set_error(C3_ERR_VALIDATION, "flag_store: too many words");
+    FlagWords f{};
+    for (int i = 0; i < count; ++i) f.w[i] = words[i];
+    flag_store_kernel<<<1, 32, 0, stream>>>(f, count, value);
     C3_CUDA(cudaGetLastError());
     return C3_OK;
 }

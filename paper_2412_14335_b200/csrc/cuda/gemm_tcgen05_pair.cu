@@ -112,7 +112,7 @@ __device__ __forceinline__ void wait_row_band(const RowGate& g, int band) {
     const uint64_t t0 = global_ns();
     while (ld_acquire_sys(g.flags + band) < g.epoch) {
         if (global_ns() - t0 > 2000000000ull) {
-            if (g.timed_out) atomicExch(g.timed_out, 1u);  // the host fails the step loudly
+            if (g.timed_out) st_release_sys(g.timed_out, kWaitRowGate);  // the host fails the step loudly
             break;
         }
         __nanosleep(500);
@@ -436,6 +436,20 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         if (FUSED) st_volatile_shared(producer_done, 1);
     } else if (FUSED && warp == 3) {
         if (p.fc.enabled) {
+            // across processes: no copy warp stores into a peer's receive buffer
+            // before that peer reached this step (its previous result is free)
+            const Signals& sig = p.fc.sig;
+            if (sig.enabled && lane == 0) {
+                if (blockIdx.x == 0) {
+                    fence_sys();
+                    for (int q = 0; q < p.fc.n; ++q)
+                        if (q != p.fc.self_begin)
+                            st_release_sys(sig.peers[q] + kSigFusedEntry + p.fc.self_begin, sig.entry_epoch);
+                }
+                wait_words_bounded(sig.mine, kSigFusedEntry, p.fc.self_begin, p.fc.n, sig.entry_epoch, sig.timeout_ns,
+                                   sig.err, kWaitFusedEntry);
+            }
+            __syncwarp();
             if (p.fc.mode == 1)
                 fused_copy_loop_lsu(p, lane);
             else if (lane == 0)
@@ -663,10 +677,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             fence_sys();
             for (int q = 0; q < p.fc.n; ++q)
                 if (q != p.fc.self_begin) st_release_sys(sig.peers[q] + kFusedExitSlot + p.fc.self_begin, sig.epoch);
-            for (int q = 0; q < p.fc.n; ++q)
-                if (q != p.fc.self_begin)
-                    while (ld_acquire_sys(sig.mine + kFusedExitSlot + q) < sig.epoch) {
-                    }
+            wait_words_bounded(sig.mine, kFusedExitSlot, p.fc.self_begin, p.fc.n, sig.epoch, sig.timeout_ns,
+                               sig.err, kWaitFusedExit);
             *sig.done = 0;
         }
     }

@@ -365,6 +365,28 @@ __device__ __forceinline__ void link_wait(uint64_t t0, double sent, float bytes_
     }
 }
 
+// Bounded cross-rank wait: until words[slot + p] >= epoch for every rank
+// p != self of n (this rank's signal array, written by the peers). After
+// timeout_ns the waiter records `code` in *err (mapped host word; may be
+// null) and gives up, so a dead or mismatched peer fails the step instead of
+// hanging the GPU. Returns false on timeout.
+__device__ __forceinline__ bool wait_words_bounded(const uint32_t* words, int slot, int self, int n,
+                                                   uint32_t epoch, uint64_t timeout_ns, uint32_t* err,
+                                                   uint32_t code) {
+    const uint64_t t0 = global_ns();
+    for (int p = 0; p < n; ++p) {
+        if (p == self) continue;
+        while (ld_acquire_sys(words + slot + p) < epoch) {
+            if (global_ns() - t0 > timeout_ns) {
+                if (err) st_release_sys(err, code);
+                return false;
+            }
+            __nanosleep(64);
+        }
+    }
+    return true;
+}
+
 // 16-byte streaming load that bypasses L1 allocation; 16-byte store.
 __device__ __forceinline__ uint4 ld_nc_v4(const uint4* p) {
     uint4 v;

@@ -185,13 +185,41 @@ bool ce_batch_enabled() {
     return on;
 }
 
+// Delivery flags of a multi-process copy-engine collective: after the copies
+// on one engine stream, word [kSigCeDone + self] of every destination rank's
+// signal array gets the step's epoch, so the receiver learns on the device
+// that this rank's bytes have landed (no host barrier, nothing blocks the
+// host before the GEMM is launched). A stream memop (cuStreamWriteValue32,
+// which fences the stream's prior writes) when the driver has it, else a
+// one-thread st.release.sys kernel.
+struct CeDeliver {
+    const Signals* sig = nullptr;  // peers' signal arrays, epoch, this rank
+};
+
+int ce_signal(const CeDeliver& dv, const std::vector<int>& dsts, cudaStream_t st) {
+    const Signals& g = *dv.sig;
+    uint32_t* words[C3_MAX_RANKS];
+    int cnt = 0;
+    for (int d : dsts)
+        if (d != g.self) words[cnt++] = g.peers[d] + kSigCeDone + g.self;
+    if (cnt == 0) return C3_OK;
+    if (drv().StreamWriteValue32) {
+        for (int i = 0; i < cnt; ++i)
+            C3_CU(StreamWriteValue32, reinterpret_cast<CUstream>(st), reinterpret_cast<CUdeviceptr>(words[i]),
+                  g.epoch, CU_STREAM_WRITE_VALUE_DEFAULT);
+        return C3_OK;
+    }
+    return launch_flag_store(words, cnt, g.epoch, st);
+}
+
 int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, void* const* dst,
-           int src_filter, cudaStream_t parent) {
+           int src_filter, cudaStream_t parent, const CeDeliver* deliver = nullptr) {
     if (!w->fork_event) C3_CUDA(cudaEventCreateWithFlags(&w->fork_event, cudaEventDisableTiming));
     std::vector<char> used;
     // per engine stream: the batch (dst, src, size) of its transfers, plan order
     std::vector<std::vector<void*>> bd, bs;
     std::vector<std::vector<size_t>> bz;
+    std::vector<std::vector<int>> dst_ranks;  // destinations per engine stream (delivery flags)
     const bool batch = ce_batch_enabled();
     bool forked = false;
     for (int i = 0; i < nt; ++i) {
@@ -208,11 +236,14 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
             bd.resize(idx + 1);
             bs.resize(idx + 1);
             bz.resize(idx + 1);
+            dst_ranks.resize(idx + 1);
         }
         if (!used[idx]) {
             C3_CUDA(cudaStreamWaitEvent(w->ce_streams[idx], w->fork_event, 0));
             used[idx] = 1;
         }
+        auto& dr = dst_ranks[idx];
+        if (std::find(dr.begin(), dr.end(), x.dst_gpu) == dr.end()) dr.push_back(x.dst_gpu);
         void* d = static_cast<uint8_t*>(dst[x.dst_gpu]) + x.dst_offset;
         const void* sp = static_cast<const uint8_t*>(src[x.src_gpu]) + x.src_offset;
         if (batch) {
@@ -241,6 +272,7 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
     }
     for (std::size_t idx = 0; idx < used.size(); ++idx) {
         if (!used[idx]) continue;
+        if (deliver) C3_TRY(ce_signal(*deliver, dst_ranks[idx], w->ce_streams[idx]));
         C3_CUDA(cudaEventRecord(w->ce_events[idx], w->ce_streams[idx]));
         C3_CUDA(cudaStreamWaitEvent(parent, w->ce_events[idx], 0));
     }
@@ -294,8 +326,15 @@ c3sim::SlowdownTableSet default_tables(const c3sim::MachineDescriptor& md) {
 // ---------------------------------------------------------------- session
 
 namespace {
-constexpr int kSigWords = 64;  // signal array: see collectives.cu for the layout
 constexpr int kRunAllRanks = 1;
+// Every step advances the session's epoch by this stride, whatever its
+// collective launches: a pipelined host-input step runs up to kEpochStride
+// pieces, piece k of P signalling epoch base + stride - (P - 1 - k), and a
+// whole-slot collective signals the top epoch. A rank that runs one
+// collective and a peer that runs P pieces therefore stay consistent: the top
+// epoch is only reached once every piece is done (the epoch must
+// not depend on per-call arguments).
+constexpr uint32_t kEpochStride = 8;
 }  // namespace
 
 struct c3_session {
@@ -318,7 +357,12 @@ struct c3_session {
     std::vector<void*> imported;            // to close on destroy
     uint32_t* sig = nullptr;                // local signal array
     uint32_t* done = nullptr;               // [0] AG counter, [1] RS counter
-    uint32_t epoch = 0;
+    uint32_t epoch = 0;                     // top epoch of the current step (multiple of kEpochStride)
+    int piece_k = 0, piece_n = 1;           // piece of the collective being enqueued (make_signals)
+    uint64_t step_index = 0;                // steps run (copy-engine staging parity)
+    uint32_t* err_host = nullptr;           // mapped pinned word: kWait* code of an expired device wait
+    uint32_t* err_dev = nullptr;            // ... its device alias
+    uint64_t wait_ns = kDefaultWaitNs;      // bound of every device-side cross-rank wait
     float fused_pace = 0.0f;                // C3_FUSED: copies finish by this share of the GEMM (0 = unpaced)
     int64_t fused_piece = 0;                // C3_FUSED: bytes per bulk copy; 0 = per collective (AG 8 KiB, A2A 16 KiB)
     int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
@@ -332,7 +376,7 @@ struct c3_session {
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
                 ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
     cudaStream_t h2d_s = nullptr;             // c3_session_run_host: the host-input copies
-    uint32_t* a_flags = nullptr;              // ... A row bands landed (RowGate); word 63: gate timed out
+    uint32_t* a_flags = nullptr;              // ... A row bands landed (RowGate)
     uint32_t a_epoch = 0;
     cudaEvent_t ev_piece[8] = {};             // ... one per landed piece of the collective's input
     c3sim::MachineDescriptor md;
@@ -346,6 +390,9 @@ struct c3_session {
 };
 
 namespace {
+
+bool multi_process(const c3_session* s) { return !s->w->loopback && s->n > 1; }
+int staging_buffers(const c3_session* s) { return multi_process(s) ? 2 : 1; }
 
 int session_alloc(c3_session* s) {
     const c3_scenario_desc& d = s->d;
@@ -372,7 +419,10 @@ int session_alloc(c3_session* s) {
             s->in.push_back(p);
             C3_CUDA(cudaMalloc(&p, std::max<size_t>(static_cast<size_t>(s->chunk), 16)));
             s->out.push_back(p);
-            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload, 16)));
+            // multi-process copy-engine reduce-scatter: two staging buffers,
+            // used by step parity, so a peer one step ahead never writes into
+            // the slots this rank's local reduce is still reading
+            C3_CUDA(cudaMalloc(&p, std::max<size_t>(payload * static_cast<size_t>(staging_buffers(s)), 16)));
             s->staging.push_back(p);
         }
     }
@@ -391,35 +441,77 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaStreamCreateWithFlags(&s->h2d_s, cudaStreamNonBlocking));
     C3_CUDA(cudaMalloc(&s->a_flags, 64 * sizeof(uint32_t)));
     C3_CUDA(cudaMemset(s->a_flags, 0, 64 * sizeof(uint32_t)));
+    // error word of the device-side waits: mapped pinned host memory, so the
+    // host reads it after the step's event without a copy
+    C3_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&s->err_host), 64, cudaHostAllocMapped));
+    *s->err_host = 0;
+    C3_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&s->err_dev), s->err_host, 0));
+    if (const char* e = std::getenv("C3_WAIT_TIMEOUT_MS")) {
+        const double ms = std::atof(e);
+        if (ms > 0) s->wait_ns = static_cast<uint64_t>(ms * 1e6);
+    }
     return C3_OK;
 }
 
-Signals make_signals(c3_session* s, int which) {
+// What a collective launch signals across processes (collectives.cu layout).
+enum class SigUse {
+    Push,    // AG / A2A push: entry (receivers free) + exit (stores landed)
+    Rs,      // RS pull: entry (inputs ready) + exit (inputs read)
+    Fused,   // fused C3: fixed slots inside the GEMM kernel
+    CeEntry, // copy-engine AG / A2A: receivers free (post + wait), before the copies
+    CeDone,  // copy-engine: wait for every peer's delivery flags (written by its CE streams)
+};
+
+// Epochs of a step (kEpochStride): the step's top epoch E = s->epoch and its
+// base E - stride + 1. A collective split into P pieces (host-input steps)
+// runs piece k with s->piece_k = k, s->piece_n = P; a whole-slot one with
+// k = 0, P = 1. Entry of a push (receivers free) happens once per step, at the
+// base epoch; entry of a pull (inputs up to piece k ready) at E - (P-1-k); the
+// exit barrier only at the last piece, at E. Ranks that split the same step
+// differently therefore neither deadlock nor pass early.
+Signals make_signals(c3_session* s, SigUse use) {
     Signals g;
     if (s->w->loopback || s->n == 1) return g;
     g.enabled = true;
     g.mine = s->sig;
     for (int p = 0; p < s->n; ++p) g.peers[p] = s->peer_sig[p];
-    g.done = s->done + which;
-    g.epoch = s->epoch;
+    const uint32_t top = s->epoch, base = s->epoch - kEpochStride + 1;
+    const bool first = s->piece_k == 0, last = s->piece_k == s->piece_n - 1;
+    g.epoch = top;
+    g.entry_epoch = base;
+    g.self = s->w->rank;
+    g.err = s->err_dev;
+    g.timeout_ns = s->wait_ns;
+    switch (use) {
+        case SigUse::Push:
+            g.done = s->done + 0;
+            g.entry_slot = first ? kSigPushEntry : -1;
+            g.exit_slot = last ? kSigPushExit : -1;
+            break;
+        case SigUse::Rs:
+            g.done = s->done + 1;
+            g.entry_slot = kSigRsEntry;
+            g.entry_epoch = top - static_cast<uint32_t>(s->piece_n - 1 - s->piece_k);
+            g.exit_slot = last ? kSigRsExit : -1;
+            break;
+        case SigUse::Fused:
+            g.done = s->done + 2;
+            break;
+        case SigUse::CeEntry:
+            g.entry_slot = kSigPushEntry;
+            break;
+        case SigUse::CeDone:
+            g.entry_slot = kSigCeDone;
+            g.entry_post = false;
+            g.entry_epoch = top;
+            break;
+    }
     return g;
 }
 
-// Host barrier across ranks for the copy-engine path: the copies are
-// host-issued (as in the paper's ConCCL) and so is their cross-rank
-// completion; `local` work on `st` is drained first. No stream-wait memops:
-// a blocked cuStreamWaitValue32 can hold a hardware queue other work needs.
-int host_barrier(c3_session* s, cudaStream_t st) {
-    if (s->w->loopback || s->n == 1) return C3_OK;
-    if (!s->barrier) return set_error(C3_ERR_VALIDATION, "copy-engine collective across processes needs "
-                                                         "c3_session_set_barrier");
-    C3_CUDA(cudaStreamSynchronize(st));
-    if (s->barrier(s->barrier_ctx) != 0) return set_error(C3_ERR_IO, "host barrier callback failed");
-    return C3_OK;
-}
-
 // Enqueue this rank's share of the collective on `st`. Returns the number of
-// kernels launched via *launches.
+// kernels launched via *launches. Nothing here blocks the host: every
+// cross-rank dependency is a device-side flag wait (bounded, see Signals).
 // `off`/`len` (CU backend only): move bytes [off, off + len) of every slot,
 // the piece of a pipelined host-input step (len < 0: the whole slot).
 int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaStream_t st,
@@ -435,6 +527,26 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
     const int first = loop ? 0 : w->rank;
     const int last = loop ? (all ? n - 1 : 0) : w->rank;
     if (n == 1) return C3_OK;
+    // copy-engine collectives across processes: delivery flags per engine
+    // stream, and (AG / A2A, which write into the peers' result buffers) an
+    // entry barrier before the copies
+    const Signals ce_done = make_signals(s, SigUse::CeDone);
+    CeDeliver dv;
+    dv.sig = &ce_done;
+    const CeDeliver* deliver = ce_done.enabled ? &dv : nullptr;
+    const auto ce_entry = [&]() -> int {
+        const Signals e = make_signals(s, SigUse::CeEntry);
+        if (!e.enabled) return C3_OK;
+        C3_TRY(launch_signal_wait(e, n, st));
+        ++*launches;
+        return C3_OK;
+    };
+    const auto ce_wait_delivered = [&]() -> int {
+        if (!ce_done.enabled) return C3_OK;
+        C3_TRY(launch_signal_wait(ce_done, n, st));
+        ++*launches;
+        return C3_OK;
+    };
     if (s->d.collective == C3_ALL_GATHER) {
         MutPtrTable recv{};
         std::vector<const void*> src(static_cast<size_t>(n));
@@ -446,7 +558,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             src[static_cast<size_t>(p)] = static_cast<uint8_t*>(base) + chunk * p;
         }
         if (backend == C3_BACKEND_CU) {
-            const Signals sig = make_signals(s, 0);
+            const Signals sig = make_signals(s, SigUse::Push);
             for (int v = first; v <= last; ++v) {
                 // the kernel writes slot v at recv[q] + plen * v: shift the bases
                 // so that lands on recv[q] + chunk * v + off
@@ -457,10 +569,12 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
                 ++*launches;
             }
         } else {
-            // completion across ranks: every rank's outgoing copies done = all
-            // data delivered (host barrier at the end of the step, outside timing)
+            // plan_all_gather (conccl.cpp:24-53) on the copy engines; the step
+            // ends once every peer's chunk has landed here (delivery flags)
+            C3_TRY(ce_entry());
             C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
-                          all ? -1 : first, st));
+                          all ? -1 : first, st, deliver));
+            C3_TRY(ce_wait_delivered());
         }
         return C3_OK;
     }
@@ -474,7 +588,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             src[static_cast<size_t>(p)] = loop ? s->in[static_cast<size_t>(p)] : s->in[0];
         }
         if (backend == C3_BACKEND_CU) {
-            const Signals sig = make_signals(s, 0);
+            const Signals sig = make_signals(s, SigUse::Push);
             MutPtrTable r = recv;
             for (int q = 0; q < n; ++q) r.p[q] = static_cast<uint8_t*>(recv.p[q]) + off;
             for (int v = first; v <= last; ++v) {
@@ -486,14 +600,16 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         } else {
             // plan_all_to_all (conccl.cpp:55-84) on the copy engines; the self
             // slot is a local copy, not part of the plan
+            C3_TRY(ce_entry());
             C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
-                          all ? -1 : first, st));
+                          all ? -1 : first, st, deliver));
             for (int v = first; v <= last; ++v) {
                 const size_t lv = loop ? static_cast<size_t>(v) : 0;
                 C3_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(s->recv[lv]) + chunk * v,
                                         static_cast<const uint8_t*>(s->in[lv]) + chunk * v,
                                         static_cast<size_t>(chunk), cudaMemcpyDeviceToDevice, st));
             }
+            C3_TRY(ce_wait_delivered());
         }
         return C3_OK;
     }
@@ -502,7 +618,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
     if (backend == C3_BACKEND_CU) {
         PtrTable in{};
         for (int p = 0; p < n; ++p) in.p[p] = loop ? s->in[static_cast<size_t>(p)] : s->peer_coll[p];
-        const Signals sig = make_signals(s, 1);
+        const Signals sig = make_signals(s, SigUse::Rs);
         for (int v = first; v <= last; ++v) {
             // the kernel reads in[g] + plen * v: shift to in[g] + chunk * v + off
             PtrTable r = in;
@@ -513,26 +629,28 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         }
         return C3_OK;
     }
-    // copy phase: rank g's slot p -> rank p's staging slot g (plan_reduce_scatter)
+    // copy phase: rank g's slot p -> rank p's staging slot g (plan_reduce_scatter),
+    // into the staging buffer of this step's parity (multi-process)
+    const int64_t par = multi_process(s) ? static_cast<int64_t>(s->step_index % 2) * s->d.payload_bytes : 0;
     std::vector<const void*> src(static_cast<size_t>(n));
     std::vector<void*> dst(static_cast<size_t>(n));
     for (int p = 0; p < n; ++p) {
         src[static_cast<size_t>(p)] = loop ? s->in[static_cast<size_t>(p)] : s->peer_coll[p];
-        dst[static_cast<size_t>(p)] = loop ? s->staging[static_cast<size_t>(p)] : s->peer_staging[p];
+        dst[static_cast<size_t>(p)] =
+            static_cast<uint8_t*>(loop ? s->staging[static_cast<size_t>(p)] : s->peer_staging[p]) + par;
     }
     if (!loop) src[static_cast<size_t>(w->rank)] = s->in[0];
     C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
-                  all ? -1 : first, st));
-    C3_TRY(host_barrier(s, st));  // every peer's slot has landed in my staging
-    // local reduce of the n slots (own slot straight from the input)
+                  all ? -1 : first, st, deliver));
+    // local reduce of the n slots (own slot straight from the input); across
+    // processes its CTAs first wait for every peer's delivery flag
     for (int v = first; v <= last; ++v) {
         PtrTable slots{};
         const size_t lv = loop ? static_cast<size_t>(v) : 0;
         for (int g = 0; g < n; ++g)
             slots.p[g] = g == v ? static_cast<const uint8_t*>(s->in[lv]) + chunk * v
-                                : static_cast<const uint8_t*>(s->staging[lv]) + chunk * g;
-        C3_TRY(launch_reduce_scatter_pull(0, n, slots, s->out[lv], count, std::max(1, n_ctas),
-                                          Signals{}, st));
+                                : static_cast<const uint8_t*>(s->staging[lv]) + par + chunk * g;
+        C3_TRY(launch_reduce_scatter_pull(0, n, slots, s->out[lv], count, std::max(1, n_ctas), ce_done, st));
         ++*launches;
     }
     return C3_OK;
@@ -898,6 +1016,7 @@ int c3_session_destroy(c3_session* s) {
         if (e) cudaEventDestroy(e);
     if (s->h2d_s) cudaStreamDestroy(s->h2d_s);
     if (s->a_flags) cudaFree(s->a_flags);
+    if (s->err_host) cudaFreeHost(s->err_host);
     for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end, s->ev_h2d})
         if (e) cudaEventDestroy(e);
     delete s;
@@ -1322,6 +1441,13 @@ int c3_session_set_link_rate(c3_session* s, double gbps) {
     return C3_OK;
 }
 
+int c3_session_set_wait_timeout(c3_session* s, double ms) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_wait_timeout: null session");
+    if (!(ms > 0.0)) return set_error(C3_ERR_VALIDATION, "wait timeout must be > 0 ms");
+    s->wait_ns = static_cast<uint64_t>(ms * 1e6);
+    return C3_OK;
+}
+
 int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
     if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_barrier: null session");
     s->barrier = fn;
@@ -1390,11 +1516,8 @@ int h2d_a(c3_session* s, const HostIO* io, cudaStream_t st) {
 // piece crosses PCIe (C3_H2D_PIECES, default 8: the last piece's collective is
 // the exposed tail; 1 below 4 MiB slots). profiles/r01_e2e_pieces.txt
 int h2d_pieces(const c3_session* s) {
-    static const int env = [] {
-        const char* e = std::getenv("C3_H2D_PIECES");
-        const int v = e ? std::atoi(e) : 0;
-        return v > 0 ? std::min(v, 8) : 8;
-    }();
+    const char* e = std::getenv("C3_H2D_PIECES");
+    const int env = e && std::atoi(e) > 0 ? std::min(std::atoi(e), static_cast<int>(kEpochStride)) : 8;
     // strided all-to-all slot ranges need 16-byte slots (launch_alltoall_push)
     if (s->d.collective == C3_ALL_TO_ALL && s->chunk % 16 != 0) return 1;
     return s->chunk >= (int64_t{4} << 20) ? env : 1;
@@ -1407,13 +1530,10 @@ void piece_range(const c3_session* s, int pieces, int k, int64_t* off, int64_t* 
 // A in row bands (C3_H2D_A_PIECES, default 4; multiples of the pair tile's
 // 256 rows): the CTA-pair GEMM starts on the first band while the rest cross
 // PCIe (RowGate). 0 bands = A copied whole before the GEMM (other kernels).
-constexpr int kGateTimeoutWord = 63;  // a_flags[63]; bands use words [0, 32)
 int a_row_bands(const c3_session* s, int* rows_per_band) {
-    static const int env = [] {
-        const char* e = std::getenv("C3_H2D_A_PIECES");
-        const int v = e ? std::atoi(e) : 0;
-        return v > 0 ? std::min(v, 32) : 4;
-    }();
+    // read per call (a test may change it between steps; getenv is cheap)
+    const char* e = std::getenv("C3_H2D_A_PIECES");
+    const int env = e && std::atoi(e) > 0 ? std::min(std::atoi(e), 32) : 4;
     const bool pair = s->gemm.kind == GemmPlan::kPair || s->gemm.kind == GemmPlan::kPair512;
     if (!pair || env < 2 || !drv().StreamWriteValue32) return 0;
     const int64_t rows = ((s->d.m + env - 1) / env + 255) / 256 * 256;
@@ -1450,6 +1570,31 @@ int d2h_out(c3_session* s, const HostIO* io, cudaStream_t st) {
 }
 }  // namespace
 
+namespace {
+const char* wait_error_text(uint32_t code) {
+    switch (code) {
+        case kWaitEntry: return "a peer never reached the collective's entry barrier";
+        case kWaitExit: return "a peer never finished the collective (exit barrier)";
+        case kWaitCeDone: return "a peer's copy-engine deliveries never landed";
+        case kWaitFusedExit: return "a peer never finished the fused collective";
+        case kWaitFusedEntry: return "a peer never reached the fused collective";
+        case kWaitRowGate: return "an A row band never landed (row gate)";
+        default: return "a device-side wait expired";
+    }
+}
+int check_wait_error(c3_session* s) {
+    const uint32_t code = *static_cast<volatile uint32_t*>(s->err_host);
+    if (code == 0) return C3_OK;
+    *static_cast<volatile uint32_t*>(s->err_host) = 0;
+    // drain the copies so nothing still reads the caller's host buffers
+    cudaStreamSynchronize(s->h2d_s);
+    for (cudaStream_t st : s->w->ce_streams) cudaStreamSynchronize(st);
+    return set_error(C3_ERR_TIMEOUT, std::string("c3_session_run: ") + wait_error_text(code) + " (epoch " +
+                                         std::to_string(s->epoch) + ", bound " + std::to_string(s->wait_ns / 1000000) +
+                                         " ms)");
+}
+}  // namespace
+
 static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_in, int flags,
                             c3_timing* t, const HostIO* io = nullptr) {
     if (!s->ready) return set_error(C3_ERR_VALIDATION, "c3_session_run: peers not imported");
@@ -1461,7 +1606,10 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     c3_world* w = s->w;
     const int C = w->prop.multiProcessorCount;
     std::memset(t, 0, sizeof *t);
-    ++s->epoch;
+    s->epoch += kEpochStride;
+    s->piece_k = 0;
+    s->piece_n = 1;
+    ++s->step_index;
 
     cudaStream_t gs = s->gemm_s, cs = s->comm_s;
     int gemm_ctas = std::max(1, std::min(a.cus_gemm > 0 ? a.cus_gemm : C, C));
@@ -1469,15 +1617,24 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     const bool sp = strategy == C3_C3_SP || strategy == C3_C3_SP_RP;
     const bool rp = strategy == C3_C3_RP || strategy == C3_C3_SP_RP;
     if (sp) cs = s->comm_hi;
-    if (rp && w->green_ok) {
+    if (rp) {
+        // the SM partition is the strategy (allocate_cus, sim.cpp:40-100): no
+        // silent fallback to CTA caps, and no silent rounding of the split
+        if (!w->green_ok)
+            return set_error(C3_ERR_UNSUPPORTED, "c3_rp / c3_sp_rp need green contexts, unavailable on this device");
+        if (w->green_grain > 0 && comm_ctas % w->green_grain != 0)
+            return set_error(C3_ERR_VALIDATION, "c3_rp / c3_sp_rp: cus_comm " + std::to_string(comm_ctas) +
+                                                    " is not a multiple of the green-context SM grain " +
+                                                    std::to_string(w->green_grain));
         GreenPartition* gp = nullptr;
-        if (green_partition(w, comm_ctas, &gp) == C3_OK) {
-            gs = reinterpret_cast<cudaStream_t>(gp->gemm_stream);
-            cs = reinterpret_cast<cudaStream_t>(gp->comm_stream);
-            comm_ctas = gp->comm_sms;
-            gemm_ctas = std::min(gemm_ctas, gp->gemm_sms);
-            t->partition = 1;
-        }
+        C3_TRY(green_partition(w, comm_ctas, &gp));
+        if (gp->comm_sms != comm_ctas)
+            return set_error(C3_ERR_VALIDATION, "c3_rp: the driver granted " + std::to_string(gp->comm_sms) +
+                                                    " SMs for a request of " + std::to_string(comm_ctas));
+        gs = reinterpret_cast<cudaStream_t>(gp->gemm_stream);
+        cs = reinterpret_cast<cudaStream_t>(gp->comm_stream);
+        gemm_ctas = std::min(gemm_ctas, gp->gemm_sms);
+        t->partition = 1;
     }
     t->gemm_ctas = gemm_ctas;
     t->comm_ctas = a.backend == C3_BACKEND_CU ? comm_ctas : 0;
@@ -1517,7 +1674,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
             }
         }
         if (!loop && s->n > 1) {
-            fc.sig = make_signals(s, 2);
+            fc.sig = make_signals(s, SigUse::Fused);
         }
         t->gemm_ctas = gemm_ctas;
         C3_CUDA(cudaEventRecord(s->ev_start, s->main));
@@ -1536,7 +1693,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         t->gemm_end_ms = t->comm_end_ms = elapsed(s->ev_start, s->ev_ge);
         t->total_ms = elapsed(s->ev_start, s->ev_end);
         t->launches = 1;
-        return C3_OK;
+        return check_wait_error(s);
     }
 
     C3_CUDA(cudaEventRecord(s->ev_start, s->main));
@@ -1577,7 +1734,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         if (a_bands > 0) {
             gate.flags = s->a_flags;
             gate.epoch = ++s->a_epoch;
-            gate.timed_out = s->a_flags + kGateTimeoutWord;
+            gate.timed_out = s->err_dev;
             gated = true;
         }
         if (io) {
@@ -1635,10 +1792,10 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
                 for (int k = 0; k < pieces; ++k) {
                     int64_t off = 0, len = 0;
                     piece_range(s, pieces, k, &off, &len);
-                    if (k > 0) {
-                        C3_CUDA(cudaStreamWaitEvent(cs, s->ev_piece[k], 0));
-                        ++s->epoch;  // every piece is one collective across the ranks
-                    }
+                    if (k > 0) C3_CUDA(cudaStreamWaitEvent(cs, s->ev_piece[k], 0));
+                    // every piece is one collective across the ranks (epochs: make_signals)
+                    s->piece_k = k;
+                    s->piece_n = pieces;
                     C3_TRY(enqueue_collective(s, backend, comm_ctas, flags, cs, &launches, off, len));
                 }
             } else if (do_comm) {
@@ -1661,23 +1818,15 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     C3_CUDA(cudaEventRecord(s->ev_end, s->main));
     C3_CUDA(cudaEventSynchronize(s->ev_end));
     C3_CUDA(cudaGetLastError());
-    if (gated) {
-        uint32_t to = 0;
-        C3_CUDA(cudaMemcpy(&to, s->a_flags + kGateTimeoutWord, sizeof to, cudaMemcpyDeviceToHost));
-        if (to != 0) {
-            C3_CUDA(cudaMemset(s->a_flags + kGateTimeoutWord, 0, sizeof to));
-            return set_error(C3_ERR_CUDA, "c3_session_run_host: A row band never landed (row gate timed out)");
-        }
-    }
+    // a bounded device-side wait expired: a peer is dead or ran a mismatched
+    // step, or (row gate) a band of A never landed
+    C3_TRY(check_wait_error(s));
+    (void)gated;
     t->gemm_start_ms = elapsed(s->ev_start, s->ev_gs);
     t->gemm_end_ms = elapsed(s->ev_start, s->ev_ge);
     t->comm_start_ms = elapsed(s->ev_start, s->ev_cs);
     t->comm_end_ms = elapsed(s->ev_start, s->ev_ce);
     t->total_ms = elapsed(s->ev_start, s->ev_end);
-    // copy-engine collectives complete across ranks at a host barrier after
-    // the step (each rank's device time is its own copies; callers take the
-    // max over ranks, which is when every chunk has landed)
-    if (do_comm && backend == C3_BACKEND_DMA) C3_TRY(host_barrier(s, s->main));
     t->launches = launches;
     return C3_OK;
 }

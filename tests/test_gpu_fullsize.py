@@ -125,13 +125,24 @@ def test_alltoall_896mib_sampled_slots(c3):
     w.close()
 
 
-def test_reduce_scatter_896mib_sampled_elements(c3):
+@pytest.mark.parametrize("mode", ["sm_pull", "copy_engine", "conccl_cfg3"])
+def test_reduce_scatter_896mib_sampled_elements(c3, mode):
+    """cfg3's 896 MiB reduce-scatter: the SM pull, the copy-engine plan
+    (plan_reduce_scatter transpose into staging + local reduce), and the whole
+    conccl C3 step beside the cfg3 weight-grad GEMM."""
     w = c3.World(0, N, 0, loopback=True)
-    s = c3.Session(w, 256, 256, 256, c3.REDUCE_SCATTER, PAYLOAD)
+    mnk = (8192, 28672, 8192) if mode == "conccl_cfg3" else (256, 256, 256)
+    s = c3.Session(w, *mnk, c3.REDUCE_SCATTER, PAYLOAD)
     s.fill(SEED)
-    a = s.default_alloc(c3.COMM_ONLY_CU)
-    a.cus_comm = 148
-    s.run(c3.COMM_ONLY_CU, a, all_ranks=True)
+    if mode == "sm_pull":
+        a = s.default_alloc(c3.COMM_ONLY_CU)
+        a.cus_comm = 148
+        s.run(c3.COMM_ONLY_CU, a, all_ranks=True)
+    elif mode == "copy_engine":
+        s.run(c3.COMM_ONLY_DMA, s.default_alloc(c3.COMM_ONLY_DMA), all_ranks=True)
+    else:
+        t = s.run(c3.CONCCL, s.default_alloc(c3.CONCCL), all_ranks=True)
+        assert t.gemm_ctas == 148 and t.comm_ctas == 0
     count = PAYLOAD // N // 2
     rng = np.random.default_rng(13)
     idx = np.unique(rng.integers(0, count, 256))

@@ -250,6 +250,9 @@ def test_session_all_strategies_loopback(torch_mod, c3, collective, n):
         t = s.run(strat, all_ranks=True)
         torch.cuda.synchronize()
         assert t.total_ms > 0
+        if strat in (c3.C3_RP, c3.C3_SP_RP):
+            # the SM partition really is a green-context split (no CTA-cap fallback)
+            assert t.partition == 1 and t.comm_ctas % w.info.sm_grain == 0, (t.partition, t.comm_ctas)
         if strat != c3.COMM_ONLY_CU and strat != c3.COMM_ONLY_DMA:
             p = s.pointers(0)
             Cbits = np.empty(M * N, np.uint16)
@@ -369,6 +372,24 @@ def test_fused_rejects_reduce_scatter(c3):
     with pytest.raises(c3.C3Error) as e:
         s.run(c3.FUSED)
     assert e.value.code == 102
+    s.close()
+    w.close()
+
+
+def test_green_partition_rejects_unrealisable_split(c3):
+    """c3_rp with an SM split the green-context grain cannot realise is an
+    error, not a silent rounding (the driver grants multiples of the grain)."""
+    w = c3.World(0, 2, 0, loopback=True)
+    assert w.info.green_ctx == 1 and w.info.sm_grain >= 1
+    s = c3.Session(w, 256, 256, 64, 0, 2 * 4096)
+    a = s.default_alloc(c3.C3_RP)
+    assert a.cus_comm % w.info.sm_grain == 0
+    if w.info.sm_grain > 1:
+        a.cus_comm = w.info.sm_grain + 1
+        a.cus_gemm = w.info.sm_count - a.cus_comm
+        with pytest.raises(c3.C3Error) as e:
+            s.run(c3.C3_RP, a)
+        assert e.value.code == 4
     s.close()
     w.close()
 

@@ -2,7 +2,9 @@
 exchange CUDA-IPC handles of their session buffers over gloo, and run the
 non-loopback code path — P2P kernels that signal completion through peer
 flag words (st.release.sys / ld.acquire.sys), and the copy-engine executor
-with its host barrier — checked bit-exactly against the oracle.
+with its device-side delivery flags (stream memops after each engine's
+copies, waited on by a one-warp kernel / the local reduce) — checked
+bit-exactly against the oracle.
 
 This is the same code a one-process-per-GPU torchrun world executes; only the
 peer mapping is same-device IPC instead of NVLink (the box gives one GPU).
@@ -43,7 +45,8 @@ def _worker(rank, world, port, coll, q):
         payload = world * chunk
         s = c3.Session(w, M, N, K, coll, payload)
         s.import_handles(d.allgather_bytes(s.export_handles()))
-        s.set_barrier(d.barrier)
+        # no host barrier callback: cross-rank completion is device-side for
+        # every backend, copy engines included (delivery flags)
         results = {}
         strats = [c3.C3_SP, c3.CONCCL, c3.COMM_ONLY_CU, c3.COMM_ONLY_DMA, c3.SERIAL]
         if coll != c3.REDUCE_SCATTER:
@@ -74,6 +77,19 @@ def _worker(rank, world, port, coll, q):
             t = s.run(strat)
             d.barrier()  # every rank's collective done before checking
             results[strat] = (check(s, chunk), t.total_ms)
+            if strat == c3.CONCCL:
+                # the copy phase no longer blocks the host: the GEMM is launched
+                # (and starts) before the collective, copies included, completes
+                results["conccl_overlap"] = (t.gemm_start_ms < t.comm_end_ms, t.total_ms)
+        # back-to-back steps with no host synchronisation between the ranks:
+        # the entry barriers / staging parity keep every step's data intact
+        for strat in (c3.C3_SP, c3.CONCCL):
+            s.fill(SEED)
+            d.barrier()
+            for _ in range(3):
+                s.run(strat)
+            d.barrier()
+            results[("b2b", strat)] = (check(s, chunk), 0.0)
         # host-buffer step (c3_session_run_host) with slots large enough for the
         # pipelined form: the collective's input lands in pieces, one collective
         # (one epoch of peer flags) per piece
@@ -81,8 +97,7 @@ def _worker(rank, world, port, coll, q):
         big = (4 << 20) + 4096 * 3 + 16 * 5
         s2 = c3.Session(w, M, N, K, coll, world * big)
         s2.import_handles(d.allgather_bytes(s2.export_handles()))
-        s2.set_barrier(d.barrier)
-        for strat in (c3.C3_BASE, c3.C3_SP):
+        for strat in (c3.C3_BASE, c3.C3_SP, "mixed"):
             s2.fill(SEED)
             p2 = s2.pointers(0)
             host = torch.empty(p2.send_bytes, dtype=torch.uint8).pin_memory()
@@ -90,8 +105,18 @@ def _worker(rank, world, port, coll, q):
             zeros = np.zeros(p2.send_bytes, np.uint8)
             c3.check(c3.lib().c3_memcpy(p2.send, zeros.ctypes.data, p2.send_bytes, 1, None))
             c3.check(c3.lib().c3_stream_sync(None))
-            d.barrier()
-            t = s2.run_host(strat, None, None, host.data_ptr())
+            if strat == "mixed":
+                # rank 0 lands its input in pieces (one collective per piece),
+                # rank 1 keeps it on the device (one whole-slot collective): the
+                # per-step epoch stride keeps both consistent
+                if rank == 1:
+                    c3.check(c3.lib().c3_memcpy(p2.send, host.data_ptr(), p2.send_bytes, 1, None))
+                    c3.check(c3.lib().c3_stream_sync(None))
+                d.barrier()
+                t = s2.run_host(c3.C3_SP, None, None, host.data_ptr() if rank == 0 else None)
+            else:
+                d.barrier()
+                t = s2.run_host(strat, None, None, host.data_ptr())
             d.barrier()
             results[("host", strat)] = (check(s2, big), t.total_ms)
         s2.close()
@@ -182,3 +207,57 @@ def test_exec_api_two_processes_one_gpu(strategy):
     # execute() reports the max over ranks: both ranks agree on every number
     assert out[0][1] == out[1][1]
     assert out[0][1][0] > 0 and len(out[0][1][1]) == 3
+
+
+def _dead_peer_worker(rank, world, port, coll, strategy, q):
+    """Rank 1 maps its buffers but never runs the step: rank 0's bounded
+    device-side waits must expire and fail the step (C3_ERR_TIMEOUT), not
+    hang the GPU."""
+    try:
+        os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
+                           "MASTER_ADDR": "127.0.0.1", "MASTER_PORT": str(port)})
+        import time
+
+        import paper_2412_14335_b200 as c3
+        from paper_2412_14335_b200.dist import Dist
+        d = Dist()
+        w = c3.World(rank, world, 0, loopback=False)
+        s = c3.Session(w, 256, 256, 256, coll, world * (256 << 10))
+        s.import_handles(d.allgather_bytes(s.export_handles()))
+        s.fill(SEED)
+        s.set_wait_timeout(300.0)
+        d.barrier()
+        res = None
+        if rank == 0:
+            t0 = time.perf_counter()
+            try:
+                s.run(strategy)
+                res = ("no error", time.perf_counter() - t0)
+            except c3.C3Error as e:
+                res = (e.code, time.perf_counter() - t0, str(e))
+        d.barrier()  # rank 1 stays alive (its memory mapped) until rank 0 is done
+        s.close()
+        w.close()
+        d.close()
+        q.put((rank, res, None))
+    except Exception as e:
+        q.put((rank, None, repr(e)))
+
+
+@pytest.mark.parametrize("coll,strategy", [(0, 2), (2, 2), (0, 5), (2, 5)],
+                         ids=["ag-sm", "rs-sm", "ag-ce", "rs-ce"])
+def test_dead_peer_is_an_error_not_a_hang(coll, strategy):
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_dead_peer_worker, args=(r, world, port, coll, strategy, q))
+             for r in range(world)]
+    for p in procs:
+        p.start()
+    out = dict((r, (res, err)) for r, res, err in (q.get(timeout=240) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+    assert out[0][1] is None and out[1][1] is None, out
+    res = out[0][0]
+    assert res[0] == 103, res  # C3_ERR_TIMEOUT
+    assert res[1] < 30.0, res  # bounded: the 300 ms waits expired, no hang
