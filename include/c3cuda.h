@@ -68,6 +68,13 @@ extern "C" {
 #define C3_GEMM_ONLY 100 /* isolated GEMM */
 #define C3_COMM_ONLY_CU 101 /* isolated SM-driven collective */
 #define C3_COMM_ONLY_DMA 102 /* isolated copy-engine collective */
+/* serial kernels (GEMM, then the SM collective on the isolated run's CTAs)
+ * with the host copies of c3_session_run_host overlapped as well as they can
+ * be without overlapping the two kernels: A lands in row bands the GEMM waits
+ * on, the collective's input crosses PCIe during the GEMM, C goes back while
+ * the collective runs. The conservative serial baseline of the end-to-end
+ * metric (a plain C3_SERIAL step does every copy and kernel in sequence). */
+#define C3_SERIAL_OVERLAP_IO 103
 
 /* c3sim::CommBackend (interference.hpp:14). */
 #define C3_BACKEND_CU 0
@@ -254,7 +261,9 @@ int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing
  * `send_bytes` of c3_session_pointers); either may be NULL to keep the device
  * contents. Concurrent strategies copy the first-launched kernel's input
  * first and overlap the second copy with that kernel; serial and fused copy
- * both before the GEMM. */
+ * both before the GEMM. C (up to out_bytes) goes back once the GEMM ends: on
+ * its own stream beside the collective for concurrent strategies and
+ * C3_SERIAL_OVERLAP_IO, after everything for C3_SERIAL. */
 int c3_session_run_host(c3_session* s, int strategy, const c3_alloc* alloc, const void* host_a,
                         const void* host_send, void* host_out, int64_t out_bytes, c3_timing* out);
 /* Loopback parity form: every virtual rank's share of the collective runs (the

@@ -212,24 +212,6 @@ static double now_s(void) {
     return (double)ts.tv_sec + 1e-9 * (double)ts.tv_nsec;
 }
 
-typedef struct {
-    const c3o_transfer* t;
-    int n_t, n;
-    void* const* src;
-    int64_t src_bytes;
-    void* const* dst;
-    int64_t dst_bytes;
-    double elapsed;
-} replay_job;
-
-static void* replay_thread(void* arg) {
-    replay_job* j = (replay_job*)arg;
-    const double t0 = now_s();
-    c3o_replay_plan(j->t, j->n_t, j->n, j->src, j->src_bytes, j->dst, j->dst_bytes);
-    j->elapsed = now_s() - t0;
-    return NULL;
-}
-
 static int cmp_double(const void* a, const void* b) {
     const double x = *(const double*)a, y = *(const double*)b;
     return x < y ? -1 : x > y;
@@ -240,37 +222,79 @@ static double median(double* v, int n) {
     return n % 2 ? v[n / 2] : 0.5 * (v[n / 2 - 1] + v[n / 2]);
 }
 
-int c3o_cpu_c3(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_transfer* t,
-               int n_transfers, int n_ranks, int64_t src_bytes, int64_t dst_bytes, int warmup,
-               int iters, double* out) {
-    if (iters < 1 || n_ranks < 1) return -1;
+/* Reduce-scatter second phase on the host, every rank: out_r[i] = sum over g
+ * of (g == r ? src_r[r slot] : dst_r[g slot])[i], fp32 in rank order, one
+ * bf16 rounding (the same arithmetic as c3o_reduce_scatter_bf16). */
+static void reduce_local_all(int n, int64_t slot_bytes, void* const* src, void* const* dst, uint16_t* out) {
+    const int64_t count = slot_bytes / 2;
+    for (int r = 0; r < n; ++r) {
+        for (int64_t i = 0; i < count; ++i) {
+            float acc = 0.0f;
+            for (int g = 0; g < n; ++g) {
+                /* own slot straight from the input, the others from staging */
+                const uint16_t* sl = (const uint16_t*)(g == r ? src[r] : dst[r]) + (int64_t)g * count;
+                acc += c3o_bf16_to_f32(sl[i]);
+            }
+            out[i] = c3o_f32_to_bf16_rne(acc); /* timing only: every rank reuses one buffer */
+        }
+    }
+}
+
+typedef struct {
+    const c3o_transfer* t;
+    int n_t, n, kind;
+    void* const* src;
+    int64_t src_bytes;
+    void* const* dst;
+    int64_t dst_bytes;
+    uint16_t* rs_out;
+} comm_job;
+
+static void run_comm(const comm_job* j) {
+    c3o_replay_plan(j->t, j->n_t, j->n, j->src, j->src_bytes, j->dst, j->dst_bytes);
+    if (j->kind == 2) reduce_local_all(j->n, j->src_bytes / j->n, j->src, j->dst, j->rs_out);
+}
+
+static void* comm_thread(void* arg) {
+    run_comm((const comm_job*)arg);
+    return NULL;
+}
+
+int c3o_cpu_c3_kind(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_transfer* t,
+                    int n_transfers, int n_ranks, int64_t src_bytes, int64_t dst_bytes, int kind,
+                    int warmup, int iters, double* out) {
+    if (iters < 1 || n_ranks < 1 || kind < 0 || kind > 2) return -1;
     float* A = (float*)malloc((size_t)(M * K) * sizeof(float));
     float* B = (float*)malloc((size_t)(N * K) * sizeof(float));
     float* C = (float*)malloc((size_t)(M * N) * sizeof(float));
     void** src = (void**)calloc((size_t)n_ranks, sizeof(void*));
     void** dst = (void**)calloc((size_t)n_ranks, sizeof(void*));
+    uint16_t* rs_out = kind == 2 ? (uint16_t*)malloc((size_t)(src_bytes / n_ranks)) : NULL;
     for (int64_t i = 0; i < M * K; ++i) A[i] = c3o_bf16_to_f32(c3o_bf16_value(20241217, 0, 0, (uint64_t)i));
     for (int64_t i = 0; i < N * K; ++i) B[i] = c3o_bf16_to_f32(c3o_bf16_value(20241217, 0, 1, (uint64_t)i));
     for (int r = 0; r < n_ranks; ++r) {
         src[r] = malloc((size_t)src_bytes);
         dst[r] = malloc((size_t)dst_bytes);
-        c3o_fill_labels(src[r], src_bytes, 20241217, r, 2);
+        if (kind == 2)
+            c3o_fill_bf16((uint16_t*)src[r], src_bytes / 2, 20241217, r, 3);
+        else
+            c3o_fill_labels(src[r], src_bytes, 20241217, r, kind == 0 ? 2 : 4);
         memset(dst[r], 0, (size_t)dst_bytes);
     }
     double* tg = (double*)malloc(sizeof(double) * (size_t)iters);
     double* tc = (double*)malloc(sizeof(double) * (size_t)iters);
     double* tb = (double*)malloc(sizeof(double) * (size_t)iters);
-    replay_job job = {t, n_transfers, n_ranks, src, src_bytes, dst, dst_bytes, 0.0};
+    comm_job job = {t, n_transfers, n_ranks, kind, src, src_bytes, dst, dst_bytes, rs_out};
     for (int it = -warmup; it < iters; ++it) {
         double t0 = now_s();
         c3o_gemm_f32(A, B, C, M, N, K, gemm_threads);
         const double g = now_s() - t0;
         t0 = now_s();
-        c3o_replay_plan(t, n_transfers, n_ranks, src, src_bytes, dst, dst_bytes);
+        run_comm(&job);
         const double c = now_s() - t0;
         pthread_t th;
         t0 = now_s();
-        pthread_create(&th, NULL, replay_thread, &job);
+        pthread_create(&th, NULL, comm_thread, &job);
         c3o_gemm_f32(A, B, C, M, N, K, gemm_threads);
         pthread_join(th, NULL);
         const double b = now_s() - t0;
@@ -289,6 +313,7 @@ int c3o_cpu_c3(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_tran
     }
     free(src);
     free(dst);
+    free(rs_out);
     free(A);
     free(B);
     free(C);
@@ -296,4 +321,11 @@ int c3o_cpu_c3(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_tran
     free(tc);
     free(tb);
     return 0;
+}
+
+int c3o_cpu_c3(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_transfer* t,
+               int n_transfers, int n_ranks, int64_t src_bytes, int64_t dst_bytes, int warmup,
+               int iters, double* out) {
+    return c3o_cpu_c3_kind(M, N, K, gemm_threads, t, n_transfers, n_ranks, src_bytes, dst_bytes, 0, warmup,
+                           iters, out);
 }

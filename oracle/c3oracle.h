@@ -99,6 +99,12 @@ void c3o_gemm_f32(const float* A, const float* B, float* C, int64_t M, int64_t N
 int c3o_cpu_c3(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_transfer* t,
                int n_transfers, int n_ranks, int64_t src_bytes, int64_t dst_bytes, int warmup,
                int iters, double* out);
+/* The same for any collective kind (0 all-gather, 1 all-to-all, 2
+ * reduce-scatter = the all-to-all plan into staging + a local fp32 reduce of
+ * every rank's slots on the communication thread). */
+int c3o_cpu_c3_kind(int64_t M, int64_t N, int64_t K, int gemm_threads, const c3o_transfer* t,
+                    int n_transfers, int n_ranks, int64_t src_bytes, int64_t dst_bytes, int kind,
+                    int warmup, int iters, double* out);
 
 #ifdef __cplusplus
 }

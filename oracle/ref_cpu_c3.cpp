@@ -11,9 +11,13 @@
 //   * the reference simulate() prediction for the same scenario on the
 //     machine file given (speedup/ideal/fraction for c3_base and conccl).
 //
-// usage: c3sim_ref_cpu_c3 M N K n_ranks payload_bytes threads warmup iters machine.json
+// usage: c3sim_ref_cpu_c3 M N K n_ranks payload_bytes threads warmup iters machine.json [kind]
+// kind: all-gather (default; plan_all_gather), all-to-all or reduce-scatter
+// (plan_all_to_all, conccl.cpp:55-84 -- the reduce-scatter copy phase -- then a
+// local fp32 reduce).
 // prints one JSON object.
 #include <cstdio>
+#include <stdexcept>
 #include <string>
 #include <thread>
 #include <vector>
@@ -39,14 +43,18 @@ int main(int argc, char** argv) {
     if (threads <= 0) threads = std::max(1u, std::thread::hardware_concurrency());
     try {
         const MachineDescriptor md = load_machine_file(argv[9]);
-        const TransferPlan plan = plan_all_gather(n, payload / n, md);
+        const std::string kind = argc > 10 ? argv[10] : "all-gather";
+        const int k = kind == "all-gather" ? 0 : kind == "all-to-all" ? 1 : kind == "reduce-scatter" ? 2 : -1;
+        if (k < 0) throw std::runtime_error("unknown collective kind " + kind);
+        const TransferPlan plan =
+            k == 0 ? plan_all_gather(n, payload / n, md) : plan_all_to_all(n, payload / n, md);
         std::vector<c3o_transfer> ts;
         for (const auto& t : plan.transfers)
             ts.push_back({t.src_gpu, t.dst_gpu, t.src_offset, t.dst_offset, t.length, t.engine_id,
                           t.seq});
         double out[3] = {0, 0, 0};
-        if (c3o_cpu_c3(M, N, K, threads, ts.data(), (int)ts.size(), n, plan.buffers.src_bytes,
-                       plan.buffers.dst_bytes, warmup, iters, out) != 0)
+        if (c3o_cpu_c3_kind(M, N, K, threads, ts.data(), (int)ts.size(), n, plan.buffers.src_bytes,
+                            plan.buffers.dst_bytes, k, warmup, iters, out) != 0)
             return 4;
         const double serial = out[0] + out[1];
         const double speedup = serial / out[2];
@@ -55,8 +63,8 @@ int main(int argc, char** argv) {
         std::printf(
             "{\"t_gemm_s\": %.9g, \"t_comm_s\": %.9g, \"t_concurrent_s\": %.9g, "
             "\"speedup\": %.9g, \"ideal\": %.9g, \"fraction_of_ideal\": %.9g, "
-            "\"threads\": %d, \"transfers\": %zu}\n",
-            out[0], out[1], out[2], speedup, ideal, frac, threads, ts.size());
+            "\"threads\": %d, \"transfers\": %zu, \"kind\": \"%s\", \"warmup\": %d, \"iters\": %d}\n",
+            out[0], out[1], out[2], speedup, ideal, frac, threads, ts.size(), kind.c_str(), warmup, iters);
     } catch (const std::exception& e) {
         std::fprintf(stderr, "ref_cpu_c3: %s\n", e.what());
         return 4;

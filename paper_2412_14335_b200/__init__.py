@@ -13,6 +13,7 @@ import ctypes as C
 from . import _capi
 from ._capi import (ALL_GATHER, ALL_TO_ALL, REDUCE_SCATTER, SERIAL, C3_BASE, C3_SP, C3_RP,
                     C3_SP_RP, CONCCL, CONCCL_RP, FUSED, GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA,
+                    SERIAL_OVERLAP_IO,
                     STRATEGY_NAMES, BACKEND_CU, BACKEND_DMA, BACKEND_TMA, C3Error, check, lib,
                     ptr_array)
 

@@ -20,7 +20,7 @@ ERR_NAMES = {2: "IoError", 3: "UnknownEntityError", 4: "ValidationError", 5: "Fi
 ALL_GATHER, ALL_TO_ALL, REDUCE_SCATTER = 0, 1, 2
 SERIAL, C3_BASE, C3_SP, C3_RP, C3_SP_RP, CONCCL, CONCCL_RP = range(7)
 FUSED = 7  # B200 extension: collective moved inside the GEMM kernel by its TMA unit
-GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA = 100, 101, 102
+GEMM_ONLY, COMM_ONLY_CU, COMM_ONLY_DMA, SERIAL_OVERLAP_IO = 100, 101, 102, 103
 STRATEGY_NAMES = ["serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp",
                   "c3_fused"]
 BACKEND_CU, BACKEND_DMA, BACKEND_TMA = 0, 1, 2

@@ -376,6 +376,8 @@ struct c3_session {
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
                 ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
     cudaStream_t h2d_s = nullptr;             // c3_session_run_host: the host-input copies
+    cudaStream_t d2h_s = nullptr;             // ... the result read-back (C), beside the collective
+    cudaEvent_t ev_d2h = nullptr;
     uint32_t* a_flags = nullptr;              // ... A row bands landed (RowGate)
     uint32_t a_epoch = 0;
     cudaEvent_t ev_piece[8] = {};             // ... one per landed piece of the collective's input
@@ -439,6 +441,8 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaEventCreateWithFlags(&s->ev_h2d, cudaEventDisableTiming));
     for (cudaEvent_t& e : s->ev_piece) C3_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     C3_CUDA(cudaStreamCreateWithFlags(&s->h2d_s, cudaStreamNonBlocking));
+    C3_CUDA(cudaStreamCreateWithFlags(&s->d2h_s, cudaStreamNonBlocking));
+    C3_CUDA(cudaEventCreateWithFlags(&s->ev_d2h, cudaEventDisableTiming));
     C3_CUDA(cudaMalloc(&s->a_flags, 64 * sizeof(uint32_t)));
     C3_CUDA(cudaMemset(s->a_flags, 0, 64 * sizeof(uint32_t)));
     // error word of the device-side waits: mapped pinned host memory, so the
@@ -1015,6 +1019,8 @@ int c3_session_destroy(c3_session* s) {
     for (cudaEvent_t e : s->ev_piece)
         if (e) cudaEventDestroy(e);
     if (s->h2d_s) cudaStreamDestroy(s->h2d_s);
+    if (s->d2h_s) cudaStreamDestroy(s->d2h_s);
+    if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
     if (s->a_flags) cudaFree(s->a_flags);
     if (s->err_host) cudaFreeHost(s->err_host);
     for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end, s->ev_h2d})
@@ -1458,6 +1464,10 @@ int c3_session_set_barrier(c3_session* s, c3_barrier_fn fn, void* ctx) {
 int c3_session_default_alloc(c3_session* s, int strategy, c3_alloc* out) {
     if (!s || !out) return set_error(C3_ERR_VALIDATION, "c3_session_default_alloc: null argument");
     const int C = s->md.cus_per_gpu;
+    if (strategy == C3_SERIAL_OVERLAP_IO) {
+        *out = {C, C, 0, C3_BACKEND_CU, 0, 0.f};
+        return C3_OK;
+    }
     if (strategy >= C3_GEMM_ONLY) {
         *out = {C, strategy == C3_COMM_ONLY_CU ? 32 : 0, 0,
                 strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA : C3_BACKEND_CU, 0, 0.f};
@@ -1641,7 +1651,8 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     // pacing of this run's SM / fused collective: the emulated link rate, or
     // (concurrent runs) the allocation's comm pace when lower
     s->run_gbps = s->link_gbps;
-    const bool concurrent = strategy != C3_SERIAL && strategy != C3_GEMM_ONLY &&
+    const bool serial_io = strategy == C3_SERIAL_OVERLAP_IO;
+    const bool concurrent = strategy != C3_SERIAL && strategy != C3_GEMM_ONLY && !serial_io &&
                             strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;
     if (concurrent && a.comm_pace_gbps > 0.f &&
         (s->run_gbps <= 0.0 || static_cast<double>(a.comm_pace_gbps) < s->run_gbps))
@@ -1700,8 +1711,9 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     const bool do_gemm = strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;
     const bool do_comm = strategy != C3_GEMM_ONLY;
     const int backend = strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA
-                        : strategy == C3_COMM_ONLY_CU ? C3_BACKEND_CU
-                                                      : a.backend;
+                        : strategy == C3_COMM_ONLY_CU || serial_io ? C3_BACKEND_CU
+                                                                    : a.backend;
+    if (serial_io) a.comm_first = 0;  // GEMM first, the collective after it
     bool gated = false;  // A arrives in row bands the GEMM waits on (RowGate)
     if (strategy == C3_SERIAL) {
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
@@ -1715,6 +1727,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         C3_TRY(enqueue_collective(s, C3_BACKEND_CU, comm_ctas, flags, gs, &launches));
         C3_CUDA(cudaEventRecord(s->ev_ce, gs));
         C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ce, 0));
+        C3_TRY(d2h_out(s, io, s->main));  // one stream: after everything
     } else {
         C3_CUDA(cudaStreamWaitEvent(gs, s->ev_start, 0));
         C3_CUDA(cudaStreamWaitEvent(cs, s->ev_start, 0));
@@ -1724,7 +1737,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         // collective runs per piece as it lands, so the copies overlap the GEMM
         // and the collective overlaps the remaining copies.
         const bool send_in = io && io->send && do_comm;
-        const int pieces = send_in ? (backend == C3_BACKEND_CU ? h2d_pieces(s) : 1) : 0;
+        const int pieces = send_in ? (backend == C3_BACKEND_CU && !serial_io ? h2d_pieces(s) : 1) : 0;
         // comm pacing spreads a device-resident collective over the GEMM; a
         // collective whose input arrives over PCIe in pieces is already spread,
         // and pacing each piece from its own start would only stretch the tail
@@ -1787,6 +1800,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         };
         const auto launch_comm = [&]() -> int {
             if (pieces > 0) C3_CUDA(cudaStreamWaitEvent(cs, s->ev_piece[0], 0));
+            if (serial_io) C3_CUDA(cudaStreamWaitEvent(cs, s->ev_ge, 0));  // kernels in sequence
             C3_CUDA(cudaEventRecord(s->ev_cs, cs));
             if (do_comm && pieces > 1) {
                 for (int k = 0; k < pieces; ++k) {
@@ -1813,8 +1827,14 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         }
         C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ge, 0));
         C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_ce, 0));
+        if (io && io->out && io->out_bytes > 0) {
+            // C goes back as soon as the GEMM is done, beside the collective
+            C3_CUDA(cudaStreamWaitEvent(s->d2h_s, s->ev_ge, 0));
+            C3_TRY(d2h_out(s, io, s->d2h_s));
+            C3_CUDA(cudaEventRecord(s->ev_d2h, s->d2h_s));
+            C3_CUDA(cudaStreamWaitEvent(s->main, s->ev_d2h, 0));
+        }
     }
-    C3_TRY(d2h_out(s, io, s->main));
     C3_CUDA(cudaEventRecord(s->ev_end, s->main));
     C3_CUDA(cudaEventSynchronize(s->ev_end));
     C3_CUDA(cudaGetLastError());

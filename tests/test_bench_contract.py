@@ -29,6 +29,13 @@ def test_reference_arm_contract():
     cb = d["cpu_baseline"]
     assert {"value", "unit", "cores", "kind", "sample"} <= set(cb) and cb["cores"] >= 1
     assert "workload" in d["config"]
+    # the reference arm reports the steps it really ran and our arm's config
+    assert d["steps"] == 2 and d["warmup"] == 3
+    sys.path.insert(0, REPO)
+    import bench
+    from types import SimpleNamespace
+    assert d["config"] == bench.bench_config(SimpleNamespace(config="cfg1"), 1)
+    assert d["unit"] == d["e2e"]["unit"] == bench.UNIT
 
 
 @pytest.mark.gpu
@@ -45,5 +52,11 @@ def test_our_arm_contract():
     assert {"sm_mhz", "sm_max_mhz", "reasons"} <= set(d["clocks"])
     cb = d["cpu_baseline"]
     assert {"value", "unit", "cores", "kind", "sample"} <= set(cb)
-    assert d["config"]["strategy_choice"]["strategy"] in (
+    from types import SimpleNamespace
+    sys.path.insert(0, REPO)
+    import bench
+    assert d["config"] == bench.bench_config(SimpleNamespace(config="cfg1"), 1)
+    assert d["e2e"]["unit"] == d["unit"]
+    assert d["e2e"]["d2h_bytes_per_step"] == 1024 * 1024 * 4  # the whole fp32 C
+    assert d["details"]["strategy_choice"]["strategy"] in (
         "serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp", "c3_fused")

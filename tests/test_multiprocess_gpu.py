@@ -161,7 +161,7 @@ def test_bench_two_ranks_shared_device(tmp_path):
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads(r.stdout.strip().splitlines()[-1])
     assert line["n_gpus"] == 2 and line["value"] > 0 and line["gpu_launches"] >= 1
-    assert "CUDA-IPC" in line["config"]["world"]
+    assert "CUDA-IPC" in line["details"]["world"]
 
 
 def _exec_worker(rank, world, port, strategy, q):
