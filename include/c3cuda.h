@@ -252,6 +252,22 @@ int c3_session_fill(c3_session* s, uint64_t seed);
 #define C3_SESSION_HANDLE_BYTES (4 * C3_IPC_HANDLE_BYTES)
 int c3_session_export(c3_session* s, void* blob_out);
 int c3_session_import(c3_session* s, const void* all_blobs);
+/* Host-staged copy-engine proxy (loopback worlds of >= 2 ranks; one-GPU
+ * measurement of the ConCCL path): every peer's buffers of the DMA backend
+ * become pinned host memory, so this GPU's share of the copy-engine
+ * collective -- its n-1 outgoing transfers (D2H) and the n-1 incoming ones
+ * (H2D, on a second bank of engine streams) -- runs on the copy engines over
+ * PCIe instead of as same-device SM copies. Per-GPU HBM
+ * traffic is the real node's; the rate is PCIe's, not NVLink's. Applies to the
+ * plain c3_session_run (this rank's share), DMA strategies only; peer q's
+ * host buffers (chunk bytes each: its own data, filled by c3_session_fill,
+ * and what this rank sent it) are returned by c3_session_proxy_buffers. */
+int c3_session_set_ce_proxy(c3_session* s, int on);
+int c3_session_proxy_buffers(c3_session* s, int peer, void** host_send, void** host_recv);
+/* Diagnostic: occupy every SM with one spinning CTA (most of its shared
+ * memory, so nothing else fits beside it) for `ms` milliseconds on `stream`:
+ * work that still completes meanwhile needs no SM (copy-engine proof). */
+int c3_sm_hog(c3_world* w, double ms, void* stream);
 /* One C3 step (synchronous on the host at the end; device-event timed). */
 int c3_session_run(c3_session* s, int strategy, const c3_alloc* alloc, c3_timing* out);
 /* One C3 step on HOST buffers (the end-to-end call): the step's inputs are

@@ -109,6 +109,9 @@ SIGNATURES = {
     "c3_session_default_alloc": (I, [P, I, C.POINTER(Alloc)]),
     "c3_session_set_barrier": (I, [P, C.c_void_p, P]),
     "c3_session_set_wait_timeout": (I, [P, C.c_double]),
+    "c3_session_set_ce_proxy": (I, [P, I]),
+    "c3_session_proxy_buffers": (I, [P, I, PP, PP]),
+    "c3_sm_hog": (I, [P, C.c_double, P]),
     "c3_session_set_fused_pace": (I, [P, C.c_float, I]),
     "c3_session_set_link_rate": (I, [P, C.c_double]),
     "c3_session_load_tables": (I, [P, C.c_char_p]),

@@ -169,6 +169,7 @@ int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, i
 // entry_slot): the copy-engine path's entry barrier and its wait for the
 // peers' delivery flags. Occupies one warp of one SM while it polls.
 int launch_signal_wait(const Signals& sig, int n, cudaStream_t stream);
+int launch_sm_hog(int sm_count, double ms, cudaStream_t stream);
 // Fallback when stream memops are unavailable: store `value` into each of
 // `count` (peer-mapped) words with st.release.sys, after the stream's prior work.
 int launch_flag_store(uint32_t* const* words, int count, uint32_t value, cudaStream_t stream);

@@ -581,6 +581,28 @@ int launch_reduce_scatter_pull(int self, int n, const PtrTable& in, void* out, i
     return C3_OK;
 }
 
+// Diagnostic SM hog: every thread of every CTA spins on the global timer.
+// 1024-thread CTAs with 100 KB of shared memory, two per SM, fill each SM's
+// thread slots and most of its shared memory, so no other CTA can be resident.
+__global__ void __launch_bounds__(1024) sm_hog_kernel(uint64_t ns) {
+    extern __shared__ uint8_t hog_smem[];
+    const uint64_t t0 = global_ns();
+    while (global_ns() - t0 < ns) __nanosleep(1000);
+    if (threadIdx.x == 0) hog_smem[0] = 0;
+}
+
+int launch_sm_hog(int sm_count, double ms, cudaStream_t stream) {
+    constexpr int kSmem = 100 * 1024;
+    static bool attr = false;
+    if (!attr) {
+        C3_CUDA(cudaFuncSetAttribute(sm_hog_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, kSmem));
+        attr = true;
+    }
+    sm_hog_kernel<<<2 * sm_count, 1024, kSmem, stream>>>(static_cast<uint64_t>(ms * 1e6));
+    C3_CUDA(cudaGetLastError());
+    return C3_OK;
+}
+
 int launch_signal_wait(const Signals& sig, int n, cudaStream_t stream) {
     if (!sig.enabled || sig.entry_slot < 0 || n < 2) return C3_OK;
     signal_wait_kernel<<<1, 32, 0, stream>>>(sig, n);

@@ -121,9 +121,12 @@ int probe_green(c3_world* w) {
     return 1;
 }
 
-int ce_stream(c3_world* w, int engine, std::size_t* idx_out) {
+// Copy-engine stream of `engine` (mod the device's async engine count); with
+// inbound = true the second bank of streams (the host-staged proxy's H2D
+// half, so the two PCIe directions run side by side).
+int ce_stream(c3_world* w, int engine, std::size_t* idx_out, bool inbound = false) {
     const int n_eng = std::max(1, w->prop.asyncEngineCount);
-    const std::size_t idx = static_cast<std::size_t>(engine % n_eng);
+    const std::size_t idx = static_cast<std::size_t>(engine % n_eng + (inbound ? n_eng : 0));
     while (w->ce_streams.size() <= idx) {
         cudaStream_t s;
         cudaEvent_t e;
@@ -212,8 +215,11 @@ int ce_signal(const CeDeliver& dv, const std::vector<int>& dsts, cudaStream_t st
     return launch_flag_store(words, cnt, g.epoch, st);
 }
 
+// Transfers selected: src_gpu == src_filter, or (dst_filter >= 0) dst_gpu ==
+// dst_filter; every transfer when both filters are < 0. Copies whose
+// destination is dst_filter use the inbound stream bank.
 int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, void* const* dst,
-           int src_filter, cudaStream_t parent, const CeDeliver* deliver = nullptr) {
+           int src_filter, cudaStream_t parent, const CeDeliver* deliver = nullptr, int dst_filter = -1) {
     if (!w->fork_event) C3_CUDA(cudaEventCreateWithFlags(&w->fork_event, cudaEventDisableTiming));
     std::vector<char> used;
     // per engine stream: the batch (dst, src, size) of its transfers, plan order
@@ -224,9 +230,10 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
     bool forked = false;
     for (int i = 0; i < nt; ++i) {
         const c3_transfer& x = t[i];
-        if ((src_filter >= 0 && x.src_gpu != src_filter) || x.length <= 0) continue;
+        const bool pick = (src_filter < 0 && dst_filter < 0) || x.src_gpu == src_filter || x.dst_gpu == dst_filter;
+        if (!pick || x.length <= 0) continue;
         std::size_t idx = 0;
-        C3_TRY(ce_stream(w, x.engine_id, &idx));
+        C3_TRY(ce_stream(w, x.engine_id, &idx, dst_filter >= 0 && x.dst_gpu == dst_filter));
         if (!forked) {
             C3_CUDA(cudaEventRecord(w->fork_event, parent));
             forked = true;
@@ -251,7 +258,7 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
             bs[idx].push_back(const_cast<void*>(sp));
             bz[idx].push_back(static_cast<size_t>(x.length));
         } else {
-            C3_CUDA(cudaMemcpyAsync(d, sp, static_cast<size_t>(x.length), cudaMemcpyDeviceToDevice,
+            C3_CUDA(cudaMemcpyAsync(d, sp, static_cast<size_t>(x.length), cudaMemcpyDefault,
                                     w->ce_streams[idx]));
         }
     }
@@ -372,6 +379,12 @@ struct c3_session {
     void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
     std::vector<c3_transfer> plan;          // validated ConCCL plan
+    // host-staged copy-engine proxy (loopback, c3_session_set_ce_proxy): the
+    // DMA backend's peers are pinned host buffers, one chunk each: the peer's
+    // own data (source of its inbound copies) and what this rank sends it
+    bool ce_proxy = false;
+    void* proxy_send[C3_MAX_RANKS] = {};
+    void* proxy_recv[C3_MAX_RANKS] = {};
     cudaStream_t main = nullptr, gemm_s = nullptr, comm_s = nullptr, comm_hi = nullptr;
     cudaEvent_t ev_start = nullptr, ev_gs = nullptr, ev_ge = nullptr, ev_cs = nullptr,
                 ev_ce = nullptr, ev_end = nullptr, ev_h2d = nullptr;
@@ -551,6 +564,11 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         ++*launches;
         return C3_OK;
     };
+    // host-staged proxy (rank 0's share of a loopback world): rank 0's copies
+    // to peer q land in q's pinned host buffer (D2H), q's copies to rank 0 come
+    // from it (H2D), so every byte of this GPU's share crosses a copy engine
+    const bool proxy = loop && s->ce_proxy && !all && backend == C3_BACKEND_DMA;
+    const int dst_filter = proxy ? 0 : -1;
     if (s->d.collective == C3_ALL_GATHER) {
         MutPtrTable recv{};
         std::vector<const void*> src(static_cast<size_t>(n));
@@ -575,9 +593,14 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         } else {
             // plan_all_gather (conccl.cpp:24-53) on the copy engines; the step
             // ends once every peer's chunk has landed here (delivery flags)
+            if (proxy)
+                for (int q = 1; q < n; ++q) {
+                    src[static_cast<size_t>(q)] = s->proxy_send[q];  // plan src_offset = 0
+                    dst[static_cast<size_t>(q)] = s->proxy_recv[q];  // rank 0's slot: dst_offset = 0
+                }
             C3_TRY(ce_entry());
             C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
-                          all ? -1 : first, st, deliver));
+                          all ? -1 : first, st, deliver, dst_filter));
             C3_TRY(ce_wait_delivered());
         }
         return C3_OK;
@@ -604,9 +627,14 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
         } else {
             // plan_all_to_all (conccl.cpp:55-84) on the copy engines; the self
             // slot is a local copy, not part of the plan
+            if (proxy)
+                for (int q = 1; q < n; ++q) {
+                    src[static_cast<size_t>(q)] = s->proxy_send[q];  // q's send slot 0 (src_offset 0)
+                    dst[static_cast<size_t>(q)] = s->proxy_recv[q];  // rank 0's slot (dst_offset 0)
+                }
             C3_TRY(ce_entry());
             C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
-                          all ? -1 : first, st, deliver));
+                          all ? -1 : first, st, deliver, dst_filter));
             for (int v = first; v <= last; ++v) {
                 const size_t lv = loop ? static_cast<size_t>(v) : 0;
                 C3_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(s->recv[lv]) + chunk * v,
@@ -644,8 +672,13 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
             static_cast<uint8_t*>(loop ? s->staging[static_cast<size_t>(p)] : s->peer_staging[p]) + par;
     }
     if (!loop) src[static_cast<size_t>(w->rank)] = s->in[0];
+    if (proxy)
+        for (int q = 1; q < n; ++q) {
+            src[static_cast<size_t>(q)] = s->proxy_send[q];  // q's input slot 0 (src_offset 0)
+            dst[static_cast<size_t>(q)] = s->proxy_recv[q];  // rank 0's slot (dst_offset 0)
+        }
     C3_TRY(ce_run(w, s->plan.data(), static_cast<int>(s->plan.size()), src.data(), dst.data(),
-                  all ? -1 : first, st, deliver));
+                  all ? -1 : first, st, deliver, dst_filter));
     // local reduce of the n slots (own slot straight from the input); across
     // processes its CTAs first wait for every peer's delivery flag
     for (int v = first; v <= last; ++v) {
@@ -1023,6 +1056,10 @@ int c3_session_destroy(c3_session* s) {
     if (s->ev_d2h) cudaEventDestroy(s->ev_d2h);
     if (s->a_flags) cudaFree(s->a_flags);
     if (s->err_host) cudaFreeHost(s->err_host);
+    for (int q = 0; q < C3_MAX_RANKS; ++q) {
+        if (s->proxy_send[q]) cudaFreeHost(s->proxy_send[q]);
+        if (s->proxy_recv[q]) cudaFreeHost(s->proxy_recv[q]);
+    }
     for (cudaEvent_t e : {s->ev_start, s->ev_gs, s->ev_ge, s->ev_cs, s->ev_ce, s->ev_end, s->ev_h2d})
         if (e) cudaEventDestroy(e);
     delete s;
@@ -1086,7 +1123,59 @@ int c3_session_fill(c3_session* s, uint64_t seed) {
             C3_TRY(launch_fill_bf16(s->in[sv], d.payload_bytes / 2, seed, rank, 3, st));
         }
     }
+    if (s->ce_proxy && s->chunk > 0) {
+        // each proxy peer's own data (the oracle's labels / values of rank q):
+        // generated on the device, staged into its pinned host buffer
+        void* tmp = nullptr;
+        C3_CUDA(cudaMalloc(&tmp, static_cast<size_t>(s->chunk)));
+        for (int q = 1; q < s->n; ++q) {
+            if (d.collective == C3_ALL_GATHER)
+                C3_TRY(launch_fill_labels(tmp, s->chunk, seed, q, 2, st));
+            else if (d.collective == C3_ALL_TO_ALL)
+                C3_TRY(launch_fill_labels(tmp, s->chunk, seed, q, 4, st));  // q's send slot 0
+            else
+                C3_TRY(launch_fill_bf16(tmp, s->chunk / 2, seed, q, 3, st));  // q's input slot 0
+            C3_CUDA(cudaMemcpyAsync(s->proxy_send[q], tmp, static_cast<size_t>(s->chunk), cudaMemcpyDefault, st));
+            C3_CUDA(cudaStreamSynchronize(st));
+            std::memset(s->proxy_recv[q], 0, static_cast<size_t>(s->chunk));
+        }
+        C3_CUDA(cudaFree(tmp));
+    }
     C3_CUDA(cudaStreamSynchronize(st));
+    return C3_OK;
+}
+
+int c3_sm_hog(c3_world* w, double ms, void* stream) {
+    if (!w || !(ms > 0.0) || ms > 10000.0) return set_error(C3_ERR_VALIDATION, "c3_sm_hog: ms must be in (0, 10000]");
+    C3_CUDA(cudaSetDevice(w->device));
+    return launch_sm_hog(w->prop.multiProcessorCount, ms, static_cast<cudaStream_t>(stream));
+}
+
+int c3_session_set_ce_proxy(c3_session* s, int on) {
+    if (!s) return set_error(C3_ERR_VALIDATION, "c3_session_set_ce_proxy: null session");
+    if (!on) {
+        s->ce_proxy = false;
+        return C3_OK;
+    }
+    if (!s->w->loopback || s->n < 2)
+        return set_error(C3_ERR_VALIDATION, "c3_session_set_ce_proxy: needs a loopback world of >= 2 ranks");
+    C3_CUDA(cudaSetDevice(s->w->device));
+    const size_t bytes = static_cast<size_t>(std::max<int64_t>(s->chunk, 16));
+    for (int q = 1; q < s->n; ++q) {
+        if (!s->proxy_send[q]) C3_CUDA(cudaHostAlloc(&s->proxy_send[q], bytes, cudaHostAllocPortable));
+        if (!s->proxy_recv[q]) C3_CUDA(cudaHostAlloc(&s->proxy_recv[q], bytes, cudaHostAllocPortable));
+        std::memset(s->proxy_recv[q], 0, bytes);
+    }
+    s->ce_proxy = true;
+    return C3_OK;
+}
+
+int c3_session_proxy_buffers(c3_session* s, int peer, void** host_send, void** host_recv) {
+    if (!s || !host_send || !host_recv) return set_error(C3_ERR_VALIDATION, "c3_session_proxy_buffers: null argument");
+    if (!s->ce_proxy || peer < 1 || peer >= s->n)
+        return set_error(C3_ERR_VALIDATION, "c3_session_proxy_buffers: no proxy buffer for that peer");
+    *host_send = s->proxy_send[peer];
+    *host_recv = s->proxy_recv[peer];
     return C3_OK;
 }
 
