@@ -138,6 +138,12 @@ class Session:
         self._barrier_cb = _capi.BARRIER_FN(_cb)  # keep alive
         check(lib().c3_session_set_barrier(self.h, C.cast(self._barrier_cb, C.c_void_p), None))
 
+    def set_ce_proxy(self, on=True):
+        """Host-staged copy-engine proxy (loopback): the DMA backend's peers
+        become pinned host buffers, so this GPU's share of the plan runs on
+        the copy engines over PCIe. Call before fill()."""
+        check(lib().c3_session_set_ce_proxy(self.h, int(bool(on))))
+
     def set_wait_timeout(self, ms):
         """Bound (ms) of every device-side cross-rank wait; an expired wait
         fails the step with C3Error code 103 (Timeout)."""

@@ -1164,6 +1164,7 @@ int c3_session_set_ce_proxy(c3_session* s, int on) {
     for (int q = 1; q < s->n; ++q) {
         if (!s->proxy_send[q]) C3_CUDA(cudaHostAlloc(&s->proxy_send[q], bytes, cudaHostAllocPortable));
         if (!s->proxy_recv[q]) C3_CUDA(cudaHostAlloc(&s->proxy_recv[q], bytes, cudaHostAllocPortable));
+        std::memset(s->proxy_send[q], 0, bytes);  // c3_session_fill writes peer q's data
         std::memset(s->proxy_recv[q], 0, bytes);
     }
     s->ce_proxy = true;

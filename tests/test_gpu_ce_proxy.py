@@ -91,8 +91,8 @@ def test_copy_engines_need_no_sm(c3):
     n, chunk = 8, 16 << 20
     w = c3.World(0, n, 0, loopback=True)
     s = c3.Session(w, 256, 256, 256, c3.ALL_GATHER, n * chunk)
-    s.fill(SEED)
     c3.check(c3.lib().c3_session_set_ce_proxy(s.h, 1))
+    s.fill(SEED)  # also fills the proxy peers' host buffers
     s.run(c3.COMM_ONLY_DMA)  # warm: streams, batches
     hog_ms = 400.0
     side = torch.cuda.Stream()
