@@ -197,8 +197,9 @@ def run_ours(args, dist):
         sess.import_handles(dist.allgather_bytes(sess.export_handles()))
     log("session ready")
     sess.fill(20241217)
-    if not loopback:
-        sess.set_barrier(dist.barrier)
+    machine = os.path.join(REPO, "data", f"b200-node-n{n}.json")
+    if os.path.exists(machine):
+        sess.load_machine(machine)  # measured peaks and copy-engine overheads (tools/make_machine.py)
     tables = os.path.join(REPO, "data", "b200-loopback-slowdown-tables.csv")
     sess.load_tables(tables)
     params = os.path.join(REPO, "data", "b200-loopback-params.json")
@@ -505,6 +506,16 @@ def run_ours(args, dist):
                                "local HBM with the whole GPU (~5x faster than NVLink), same timed rounds"})
         full_speed = fs_res
 
+    # ---- copy-engine strategies on one GPU: the host-staged proxy ----
+    # (loopback only; a real world runs conccl / conccl_rp over NVLink in the
+    # autotune above). The DMA backend's peers are pinned host buffers, so this
+    # GPU's share of the plan crosses PCIe on the copy engines (~48 GB/s per
+    # direction instead of NVLink's 770): the payload is scaled so the proxy
+    # collective lasts as long as the real one at NVLink rate.
+    ce_proxy = None
+    if loopback and not args.no_ce_proxy:
+        ce_proxy = run_ce_proxy(c3, cfg, n, coll, elem, K, W, NVLINK_PEER_GBPS)
+
     # ---- e2e through the C ABI with host buffers ----
     # Every step copies A and this rank's collective input in from pinned host
     # memory and the WHOLE result C back, inside the call (c3_session_run_host).
@@ -640,6 +651,7 @@ def run_ours(args, dist):
                                  "C3 step] in rotated order; medians; then, outside the timed region, "
                                  "K rounds of the full-speed pair and the library baseline"),
                     "timed_region_wall_s": wall},
+        "conccl_ce_proxy": ce_proxy,
         "loopback_full_speed": full_speed,
         "strategies_full_speed": results,
         "roofline": roofline,
@@ -683,6 +695,67 @@ def run_ours(args, dist):
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(quick=True)
     sess.close()
+    world.close()
+    return out
+
+
+# ------------------------------------------------ copy-engine proxy ------
+
+def run_ce_proxy(c3, cfg, n, coll, elem, K, W, link_gbps):
+    """conccl / conccl_rp with this GPU's share of the collective on the copy
+    engines (c3_session_set_ce_proxy): 7 transfers out (D2H to pinned host
+    peers) and 7 in (H2D), rotated rounds with the isolated GEMM and the
+    isolated proxy collective. The payload is the one whose proxy collective
+    takes the time the real payload takes at NVLink rate."""
+    MIBp = 1 << 20
+    target_ms = (n - 1) / n * cfg["payload"] / (link_gbps * 1e9) * 1e3
+    world = c3.World(0, n, 0, loopback=True)
+
+    def session(payload):
+        s = c3.Session(world, cfg["m"], cfg["n"], cfg["k"], coll, payload, dtype_bytes=elem)
+        s.set_ce_proxy(True)
+        s.fill(20241217)
+        return s
+
+    probe_payload = 64 * MIBp
+    s = session(probe_payload)
+    for _ in range(2):
+        s.run(c3.COMM_ONLY_DMA)
+    probe_ms = median([s.run(c3.COMM_ONLY_DMA).total_ms for _ in range(3)])
+    s.close()
+    step = 8 * n  # 8-byte words per slot
+    payload = max(step, int(probe_payload * target_ms / probe_ms) // step * step)
+    payload = min(payload, cfg["payload"])
+    s = session(payload)
+    jobs = {"gemm": (c3.GEMM_ONLY, s.default_alloc(c3.GEMM_ONLY)),
+            "comm": (c3.COMM_ONLY_DMA, s.default_alloc(c3.COMM_ONLY_DMA)),
+            "conccl": (c3.CONCCL, s.default_alloc(c3.CONCCL)),
+            "conccl_rp": (c3.CONCCL_RP, s.default_alloc(c3.CONCCL_RP))}
+    t = {j: [] for j in jobs}
+    names = list(jobs)
+    for r in range(W + K):
+        for j in names[r % len(names):] + names[:r % len(names)]:
+            tm = s.run(*jobs[j])
+            if r >= W:
+                t[j].append(tm)
+    tg = median([x.gemm_end_ms - x.gemm_start_ms for x in t["gemm"]])
+    tc = median([x.comm_end_ms - x.comm_start_ms for x in t["comm"]])
+    ideal = c3.ideal_speedup(tg, tc)
+    out = {"what": "PCIe-rate CE proxy: loopback world, the DMA backend's peers are pinned host buffers, so "
+                   "this GPU's share of the copy-engine plan (7 transfers out D2H, 7 in H2D) runs on the copy "
+                   "engines; payload scaled so the proxy collective lasts as long as the real one at "
+                   f"{link_gbps:.0f} GB/s NVLink; no SM runs the collective",
+           "payload_bytes": payload, "target_ms": target_ms, "t_gemm_iso_ms": tg, "t_comm_dma_iso_ms": tc,
+           "ce_gbs_per_direction": (n - 1) / n * payload / (tc * 1e-3) / 1e9, "ideal": ideal}
+    for j in ("conccl", "conccl_rp"):
+        st, al = jobs[j]
+        mk = median([x.total_ms for x in t[j]])
+        gk = median([x.gemm_end_ms - x.gemm_start_ms for x in t[j]])
+        sp = (tg + tc) / mk
+        out[j] = {"t_concurrent_ms": mk, "speedup": sp, "fraction_of_ideal": c3.fraction_of_ideal(sp, ideal),
+                  "gemm_ms_in_step": gk, "gemm_slowdown": gk / tg, "cus_gemm": al.cus_gemm,
+                  "cus_idle": al.cus_idle}
+    s.close()
     world.close()
     return out
 
@@ -880,9 +953,15 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-library-baseline", action="store_true")
     ap.add_argument("--no-nvlink-emulation", action="store_true")
+    ap.add_argument("--no-ce-proxy", action="store_true")
     args = ap.parse_args()
     args.strategies = [s for s in args.strategies.split(",") if s]
     args.warmup = max(3, args.warmup)
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        # NCCL communicator set-up in the log (the library baseline's group):
+        # the driver checks comm_nranks there
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     dist = Dist()
     try:
         if args.impl == "reference":

@@ -328,6 +328,12 @@ int c3_session_set_wait_timeout(c3_session* s, double ms);
  * allocation. allow_dma = 0 excludes conccl/conccl_rp (e.g. loopback worlds,
  * where same-device copies are SM copies). */
 int c3_session_load_tables(c3_session* s, const char* csv_path);
+/* Machine descriptor for the predictor from a reference-format machine JSON
+ * (machine.hpp:13-41, load_machine_file), e.g. data/b200-node-n8.json written
+ * by tools/make_machine.py from measured peaks and copy-engine overheads;
+ * gpus_per_node must equal the session's ranks and cus_per_gpu the SM count.
+ * Default: the same B200 figures built in. */
+int c3_session_load_machine(c3_session* s, const char* machine_json_path);
 /* Co-run penalties for the predictor from a params JSON (params_io.hpp:18-19),
  * e.g. data/b200-loopback-params.json fitted by `c3sim calibrate` on measured
  * B200 speedups (tools/calibrate_penalties.py). Default: unit penalties. */

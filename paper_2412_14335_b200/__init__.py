@@ -160,6 +160,11 @@ class Session:
         to `gbps` GB/s per direction (0 = off)."""
         check(lib().c3_session_set_link_rate(self.h, float(gbps)))
 
+    def load_machine(self, json_path):
+        """Reference-format machine descriptor for the predictor (e.g.
+        data/b200-node-n8.json)."""
+        check(lib().c3_session_load_machine(self.h, json_path.encode()))
+
     def load_params(self, json_path):
         check(lib().c3_session_load_params(self.h, json_path.encode()))
 

@@ -116,6 +116,7 @@ SIGNATURES = {
     "c3_session_set_link_rate": (I, [P, C.c_double]),
     "c3_session_load_tables": (I, [P, C.c_char_p]),
     "c3_session_load_params": (I, [P, C.c_char_p]),
+    "c3_session_load_machine": (I, [P, C.c_char_p]),
     "c3_session_predict": (I, [P, I, C.c_double, C.c_double, C.c_double, C.POINTER(C.c_double)]),
     "c3_session_autotune": (I, [P, C.POINTER(C.c_int), C.POINTER(Alloc), I, I,
                                 C.POINTER(C.c_double), C.POINTER(C.c_int), C.POINTER(C.c_double)]),

@@ -31,6 +31,7 @@
 #include "c3sim/conccl.hpp"
 #include "c3sim/coresident.hpp"
 #include "c3sim/errors.hpp"
+#include "c3sim/machine.hpp"
 #include "c3sim/params_io.hpp"
 #include "c3sim/sim.hpp"
 
@@ -287,7 +288,10 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
 }
 
 // B200 machine descriptor for a world of `n` ranks, from the live device.
-// Peaks are the driver-measured MEASURED_PEAKS.json figures of this pool.
+// Defaults = data/b200-node-n{n}.json (tools/make_machine.py): peaks from the
+// driver-measured MEASURED_PEAKS.json of this pool, copy-engine overheads
+// from data/b200-ce-overheads.json, the measured 770 GB/s peer copy shared by
+// n-1 peers. c3_session_load_machine replaces it with a machine file.
 c3sim::MachineDescriptor b200_machine(const c3_world* w, int n) {
     c3sim::MachineDescriptor md;
     md.gpus_per_node = n;
@@ -296,13 +300,13 @@ c3sim::MachineDescriptor b200_machine(const c3_world* w, int n) {
     md.cus_per_xcd = md.cus_per_gpu / md.xcds_per_gpu;
     md.min_cu_grain = md.cus_per_gpu % 4 == 0 ? 4 : (md.cus_per_gpu % 2 == 0 ? 2 : 1);
     md.dma_engines_per_gpu = std::max(1, w->prop.asyncEngineCount);
-    md.peak_compute_flops = 1.6097e15;
-    md.hbm_bandwidth = 6.5383e12;
+    md.peak_compute_flops = 1.6786e15;
+    md.hbm_bandwidth = 6.5498e12;
     md.llc_capacity = w->prop.l2CacheSize;
-    md.link_bandwidth_unidir = n > 1 ? 900e9 / (n - 1) : 900e9;
+    md.link_bandwidth_unidir = n > 1 ? 770e9 / (n - 1) : 770e9;
     md.links_per_gpu = n - 1;
-    md.cpu_launch_overhead = 2e-6;
-    md.dma_sync_overhead = 1e-5;
+    md.cpu_launch_overhead = 5.64e-7;
+    md.dma_sync_overhead = 3.36e-5;
     c3sim::validate(md);
     return md;
 }
@@ -397,6 +401,7 @@ struct c3_session {
     c3sim::MachineDescriptor md;
     c3sim::SlowdownTableSet tables;
     c3sim::SlowdownTableSet tables_loaded;  // as loaded (tables' comm class may come from comm_curve)
+    bool tables_from_file = false;
     c3sim::CoRunPenalty penalties = c3sim::CoRunPenalty::ones();  // c3_session_load_params
     c3sim::C3Scenario scenario;
     c3sim::CommCurve comm_curve;            // c3_session_set_comm_curve (seconds)
@@ -1226,6 +1231,7 @@ int c3_session_load_tables(c3_session* s, const char* csv_path) {
     return guarded([&] {
         s->tables = c3sim::load_slowdown_tables(csv_path, s->md.min_cu_grain);
         s->tables_loaded = s->tables;
+        s->tables_from_file = true;
         if (!s->comm_curve.empty()) {
             const auto cls = c3sim::comm_kernel_class(s->scenario.collective.kind);
             s->tables.at(cls) = s->comm_curve.as_table(cls, s->md);
@@ -1252,10 +1258,26 @@ double predict_makespan(c3_session* s, int st, double t_gemm_ms, double t_comm_c
     if (st == C3_SERIAL) return (t_gemm_ms + t_comm_cu_ms) * 1e-3;
     c3sim::MachineDescriptor md = s->md;
     if (dma && s->chunk > 0) {
+        // the link bandwidth at which the model's DMA work (plan_cost of the
+        // ConCCL plan, conccl.cpp:200-229: per-engine FIFOs, so 7 transfers on
+        // 4 engines take two transfer times; plus the reduce-scatter's local
+        // reduce) reproduces the measured copy-engine time
         md.cpu_launch_overhead = 0.0;
         md.dma_sync_overhead = 0.0;
-        md.link_bandwidth_unidir =
-            static_cast<double>(s->chunk) / (eff.efficiency * t_comm_dma_ms * 1e-3);
+        md.link_bandwidth_unidir = 1.0;
+        const c3sim::CollectiveKind kind = s->scenario.collective.kind;
+        const c3sim::TransferPlan tp = kind == c3sim::CollectiveKind::AllGather
+                                           ? c3sim::plan_all_gather(s->n, s->chunk, md)
+                                       : kind == c3sim::CollectiveKind::AllToAll
+                                           ? c3sim::plan_all_to_all(s->n, s->chunk, md)
+                                           : c3sim::plan_reduce_scatter(s->n, s->chunk, md);
+        const double at_unit = c3sim::plan_cost(tp, md, eff).total;  // seconds at 1 B/s
+        const double fixed = kind == c3sim::CollectiveKind::ReduceScatter
+                                 ? static_cast<double>(s->d.payload_bytes + s->chunk) /
+                                       (eff.efficiency * md.hbm_bandwidth)
+                                 : 0.0;
+        const double t_dma = t_comm_dma_ms * 1e-3;
+        md.link_bandwidth_unidir = at_unit / std::max(t_dma - fixed, 0.05 * t_dma);
     }
     return c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff).makespan;
 }
@@ -1351,6 +1373,23 @@ int c3_session_predict_alloc(c3_session* s, int strategy, const c3_alloc* alloc,
     return guarded([&] {
         *predicted_ms =
             predict_coresident(s, alloc->cus_comm, t_gemm_ms, t_comm_cu_ms, alloc->comm_pace_gbps) * 1e3;
+        return C3_OK;
+    });
+}
+
+int c3_session_load_machine(c3_session* s, const char* machine_json_path) {
+    if (!s || !machine_json_path) return set_error(C3_ERR_VALIDATION, "c3_session_load_machine: null argument");
+    return guarded([&] {
+        const c3sim::MachineDescriptor md = c3sim::load_machine_file(machine_json_path);
+        if (md.gpus_per_node != s->n)
+            throw c3sim::ValidationError("machine: gpus_per_node " + std::to_string(md.gpus_per_node) +
+                                         " != the session's " + std::to_string(s->n) + " ranks");
+        if (md.cus_per_gpu != s->w->prop.multiProcessorCount)
+            throw c3sim::ValidationError("machine: cus_per_gpu " + std::to_string(md.cus_per_gpu) +
+                                         " != this device's " + std::to_string(s->w->prop.multiProcessorCount) +
+                                         " SMs");
+        s->md = md;
+        if (!s->tables_from_file) s->tables = default_tables(s->md);
         return C3_OK;
     });
 }

@@ -261,3 +261,34 @@ def test_dead_peer_is_an_error_not_a_hang(coll, strategy):
     res = out[0][0]
     assert res[0] == 103, res  # C3_ERR_TIMEOUT
     assert res[1] < 30.0, res  # bounded: the 300 ms waits expired, no hang
+
+
+def test_library_baseline_nccl_branch_world_one(monkeypatch):
+    """bench.py's N>1 library baseline (cuBLAS || NCCL collective) exercised on
+    one GPU with a world-size-1 process group: the NCCL subgroup is created,
+    and the GEMM-only / collective-only / concurrent runs return device times
+    (SCALE runs at 2/4/8 GPUs take this same branch)."""
+    import sys
+
+    import torch
+    import torch.distributed as tdist
+    repo = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    sys.path.insert(0, repo)
+    import bench
+    from paper_2412_14335_b200.dist import Dist
+    monkeypatch.setenv("MASTER_ADDR", "127.0.0.1")
+    monkeypatch.setenv("MASTER_PORT", str(_free_port()))
+    tdist.init_process_group("gloo", rank=0, world_size=1)
+    try:
+        d = Dist()
+        d.pg = tdist  # world-size-1 group (Dist leaves a 1-process world uninitialised)
+        torch.cuda.set_device(0)
+        for name in ("cfg1", "cfg3"):
+            cfg = dict(bench.CONFIGS[name], m=1024, n=1024, k=1024, payload=8 << 20)
+            lib = bench.LibraryBaseline(cfg, d, loopback=False)
+            assert "NCCL" in lib.label
+            for fn in (lib.gemm_only, lib.comm_only, lib.both):
+                tot, g, c, _ = fn()
+                assert tot > 0
+    finally:
+        tdist.destroy_process_group()

@@ -214,3 +214,19 @@ def test_cli_run_auto_and_coresident(tmp_path):
     assert row["cus_gemm"] == 148 and row["cus_comm"] == 24 and row["comm_pace_gbps"] == pytest.approx(150)
     # serial = GEMM + the link-rate collective: (n-1)/n * P at 300 GB/s
     assert row["t_comm_s"] == pytest.approx(7 / 8 * (64 << 20) / 300e9, rel=0.25)
+
+
+@pytest.mark.parametrize("n", [2, 4, 8])
+def test_b200_machine_files_validate(n):
+    """data/b200-node-n{n}.json (tools/make_machine.py): measured B200 peaks
+    and copy-engine overheads in the reference's machine format, one file per
+    world size, accepted by the product's load_machine_file (validate,
+    machine.cpp:26-49); every partition candidate is a multiple of the
+    green-context grain (8)."""
+    md = c3sim.load_machine_file(os.path.join(REPO, "data", f"b200-node-n{n}.json"))
+    assert md.gpus_per_node == n and md.cus_per_gpu == 148 and md.links_per_gpu == n - 1
+    assert md.peak_compute_flops > 1.5e15 and md.hbm_bandwidth > 6e12
+    assert 0 < md.cpu_launch_overhead < 1e-5 and 0 < md.dma_sync_overhead < 1e-3
+    with open(os.path.join(REPO, "data", "b200-ce-overheads.json")) as f:
+        ce = json.load(f)
+    assert md.cpu_launch_overhead == pytest.approx(ce["cpu_launch_overhead"], rel=1e-2)
