@@ -1,5 +1,5 @@
 """Full-speed loopback collective throughput vs CTA count (dev aid).
-python tools/comm_ab.py [ag|a2a|rs] [payload_MiB] -> one line per CTA count:
+python tools/dev/comm_ab.py [ag|a2a|rs] [payload_MiB] -> one line per CTA count:
 median ms, per-GPU HBM bytes (read + write) / time, and fraction of the
 measured HBM copy peak (MEASURED_PEAKS.json)."""
 import json
@@ -7,7 +7,7 @@ import os
 import statistics
 import sys
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 import paper_2412_14335_b200 as c3  # noqa: E402
 

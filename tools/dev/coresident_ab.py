@@ -1,12 +1,12 @@
 """Co-resident C3 (GEMM on all SMs + comm CTAs beside it) on the cfg2 loopback
 session, interleaved rounds, for the collective implementation selected by the
 environment (C3_COMM_IMPL etc.). Dev probe.
-python tools/coresident_ab.py [ag|a2a|rs] [link_gbps (0 = full speed)] [ctas,...]"""
+python tools/dev/coresident_ab.py [ag|a2a|rs] [link_gbps (0 = full speed)] [ctas,...]"""
 import os
 import statistics
 import sys
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 import paper_2412_14335_b200 as c3  # noqa: E402
 

@@ -1,13 +1,13 @@
 """Timeline of one host-buffer C3 step (c3_session_run_host) on cfg2: the
 device-event times of the GEMM and the collective and the call's wall time,
 for the A row-band / collective-piece settings in the environment
-(C3_H2D_A_PIECES, C3_H2D_PIECES). Dev probe: python tools/e2e_probe.py [reps]"""
+(C3_H2D_A_PIECES, C3_H2D_PIECES). Dev probe: python tools/dev/e2e_probe.py [reps]"""
 import os
 import statistics
 import sys
 import time
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 import torch  # noqa: E402
 

@@ -1,10 +1,10 @@
 """C3_FUSED vs co-resident c3_base on the cfg2 loopback session at a link rate
-(dev probe): python tools/fused_probe.py [ag|a2a] [link_gbps] [pieces,...]"""
+(dev probe): python tools/dev/fused_probe.py [ag|a2a] [link_gbps] [pieces,...]"""
 import os
 import statistics
 import sys
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 import paper_2412_14335_b200 as c3  # noqa: E402
 

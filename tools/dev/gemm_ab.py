@@ -1,6 +1,6 @@
-"""A/B GEMM timing in one process (dev aid): python tools/gemm_ab.py M N K [reps]."""
+"""A/B GEMM timing in one process (dev aid): python tools/dev/gemm_ab.py M N K [reps]."""
 import os, sys, statistics
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch
 import paper_2412_14335_b200 as c3
 M, N, K = (int(x) for x in sys.argv[1:4])

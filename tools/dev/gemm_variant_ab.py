@@ -3,12 +3,12 @@
   burst      one launch per variant, interleaved, 20 rounds (cool GPU);
   sustained  each variant back to back for ~0.4 s, alternating, 3 rounds
              (the 1 kW power cap engages, as in bench.py's timed region).
-usage: python tools/gemm_variant_ab.py M N K [variants=pair,pair512,cublas]"""
+usage: python tools/dev/gemm_variant_ab.py M N K [variants=pair,pair512,cublas]"""
 import os
 import statistics
 import sys
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import torch  # noqa: E402
 
 import paper_2412_14335_b200 as c3  # noqa: E402

@@ -1,12 +1,12 @@
 """Does pacing the collective below the link rate (spreading it over the
 GEMM) shorten the co-resident C3 step? cfg2 loopback, c3_base on all SMs +
 c CTA units; serial reference at the link rate. Dev probe.
-python tools/pace_probe.py [ag|a2a|rs] [ctas] [rates,...]"""
+python tools/dev/pace_probe.py [ag|a2a|rs] [ctas] [rates,...]"""
 import os
 import statistics
 import sys
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 import paper_2412_14335_b200 as c3  # noqa: E402
 

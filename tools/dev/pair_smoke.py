@@ -1,7 +1,7 @@
 """Hang-guarded first run of the CTA-pair GEMM: one small and one cfg2 launch,
 checked against cuBLAS (dev aid)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 os.environ["C3_GEMM_KERNEL"] = sys.argv[1] if len(sys.argv) > 1 else "pair"
 import torch
 import paper_2412_14335_b200 as c3

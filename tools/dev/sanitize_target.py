@@ -1,6 +1,6 @@
 """Small invocations of every kernel family for compute-sanitizer (dev aid)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 os.environ.setdefault("C3_GEMM_KERNEL", "pair")
 import paper_2412_14335_b200 as c3
 for coll in (c3.ALL_GATHER, c3.ALL_TO_ALL, c3.REDUCE_SCATTER):

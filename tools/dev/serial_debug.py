@@ -1,6 +1,6 @@
 """Raw per-step rows for isolated vs serial steps in different round orders (dev aid)."""
 import os, sys
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import paper_2412_14335_b200 as c3
 w = c3.World(0, 8, 0, loopback=True)
 s = c3.Session(w, 8192, 28672, 8192, c3.ALL_GATHER, 896 << 20)

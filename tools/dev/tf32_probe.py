@@ -1,11 +1,11 @@
 """fp32 GEMM on the TF32 tensor cores (c3_gemm_f32) against cuBLAS TF32
 (torch.matmul with allow_tf32) on the same device buffers: interleaved,
-event-timed medians. Dev probe: python tools/tf32_probe.py [M N K]"""
+event-timed medians. Dev probe: python tools/dev/tf32_probe.py [M N K]"""
 import os
 import statistics
 import sys
 
-REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+REPO = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 sys.path.insert(0, REPO)
 import torch  # noqa: E402
 
