@@ -67,6 +67,13 @@ struct CoResidentParams {
     /// tiles: light issue and register pressure), any collective class;
     /// 0 = the class factor. Measured ~1.0 (RMS 30% -> 12% over 228 rows).
     double comm_memory_bound = 0.0;
+    /// The GEMM's extra slowdown per resident collective CTA unit, whatever
+    /// the collective's rate: excess += cta_cost * cus_comm / cus. Resident
+    /// collective warps take issue slots, registers and L1 from the GEMM's
+    /// CTAs even while they sleep (paced) or stall; measured: 64 all-to-all
+    /// units beside the cfg4 GEMM 10% slower than 16, both collectives done
+    /// well before the GEMM (profiles/r02_c3_sweep_link770.csv). 0 = off.
+    double cta_cost = 0.0;
 
     double gemm(KernelClass gemm_class) const {
         return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
@@ -91,7 +98,8 @@ void validate(const CoResidentParams& p);
 /// JSON: {"gemm-compute-bound": pg, "gemm-memory-bound": pg, "comm": pc,
 ///        "comm-all-to-all": pc (optional), "rate-exponent": g (optional, default 1),
 ///        "all-gather-by-ranks": bool (optional, default false),
-///        "comm-memory-bound": pc (optional, 0 = the class factor)}.
+///        "comm-memory-bound": pc (optional, 0 = the class factor),
+///        "cta-cost": c (optional, default 0)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 

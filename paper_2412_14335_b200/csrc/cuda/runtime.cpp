@@ -1455,20 +1455,12 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
             cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
             std::vector<std::pair<int, double>> pred;
             double best_co = 1e300;
-            // only CTA counts that carry the collective at its full rate beside
-            // the GEMM (within 3%): slowing it is the pacing knob's job, not an
-            // under-provisioned launch (fall back to every count if none does)
-            const auto ccls = c3sim::comm_kernel_class(s->scenario.collective.kind);
-            for (int pass = 0; pass < 2 && pred.empty(); ++pass) {
-                for (int c : cands) {
-                    if (c < 1 || c >= s->md.cus_per_gpu) continue;
-                    const int eff = c3sim::coresident_comm_ctas(
-                        c, s->cores, ccls, s->n,
-                        c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md)));
-                    if (pass == 0 && comm_ms_at(s, eff, t_comm_cu_ms) > 1.03 * t_comm_cu_ms) continue;
-                    pred.emplace_back(c, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms));
-                    best_co = std::min(best_co, pred.back().second);
-                }
+            // every count: a collective slowed by few CTAs still hides under a
+            // longer GEMM, and every resident CTA costs the GEMM (cta_cost)
+            for (int c : cands) {
+                if (c < 1 || c >= s->md.cus_per_gpu) continue;
+                pred.emplace_back(c, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms));
+                best_co = std::min(best_co, pred.back().second);
             }
             for (const auto& [c, m] : pred) {
                 if (m <= best_co * 1.01) {  // ascending c: the first within 1%

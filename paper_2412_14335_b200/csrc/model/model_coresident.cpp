@@ -57,6 +57,8 @@ void validate(const CoResidentParams& p) {
         throw ValidationError("co-resident memory-bound cost factor must be 0 (= class factor) or >= 1");
     if (!(p.rate_exponent > 0) || !std::isfinite(p.rate_exponent))
         throw ValidationError("co-resident rate exponent must be finite and > 0");
+    if (!(p.cta_cost >= 0.0) || !std::isfinite(p.cta_cost))
+        throw ValidationError("co-resident CTA cost must be finite and >= 0");
 }
 
 CoResidentParams load_coresident_params(const std::filesystem::path& path) {
@@ -79,6 +81,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.comm_all_to_all = j.value("comm-all-to-all", 0.0);
         p.all_gather_by_ranks = j.value("all-gather-by-ranks", false);
         p.comm_memory_bound = j.value("comm-memory-bound", 0.0);
+        p.cta_cost = j.value("cta-cost", 0.0);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -94,6 +97,7 @@ std::string save_coresident_params(const CoResidentParams& p) {
               {"rate-exponent", p.rate_exponent}};
     if (p.all_gather_by_ranks) j["all-gather-by-ranks"] = true;
     if (p.comm_memory_bound > 0.0) j["comm-memory-bound"] = p.comm_memory_bound;
+    if (p.cta_cost > 0.0) j["cta-cost"] = p.cta_cost;
     return j.dump(2) + "\n";
 }
 
@@ -117,7 +121,8 @@ SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_c
     tl.work_gemm = t_gemm;
     tl.work_comm = t_comm_full;
     // phase 1: both resident; rates in units of each kernel's isolated work
-    const double rg = 1.0 / (1.0 + (p.gemm(gemm_class) - 1.0) * std::pow(rate_ratio, p.rate_exponent));
+    const double rg = 1.0 / (1.0 + (p.gemm(gemm_class) - 1.0) * std::pow(rate_ratio, p.rate_exponent) +
+                             p.cta_cost * static_cast<double>(cus_comm) / static_cast<double>(cus));
     const double rc = t_comm_full / t_comm_at_ctas;
     const double end_g = t_gemm / rg, end_c = t_comm_full / rc;
     const double t1 = std::min(end_g, end_c);

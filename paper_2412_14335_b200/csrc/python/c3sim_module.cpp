@@ -148,7 +148,8 @@ void add_interference(py::module_& m) {
     py::class_<T>(m, "SlowdownTable").RW(T, kernel_class).RW(T, points);
     py::class_<cs::SlowdownTableSet>(m, "SlowdownTableSet")
         .def("at", [](const cs::SlowdownTableSet& s, cs::KernelClass c) -> const T& { return s.at(c); },
-             py::return_value_policy::reference_internal);
+             py::return_value_policy::reference_internal)
+        .def("set", [](cs::SlowdownTableSet& s, cs::KernelClass c, const T& t) { s.at(c) = t; });
     m.def("slowdown_at", &cs::slowdown_at);
     m.def("comm_saturation_cus", &cs::comm_saturation_cus);
     m.def("default_comm_table", &cs::default_comm_table);
@@ -232,7 +233,7 @@ void add_sim(py::module_& m) {
     py::class_<CRP>(m, "CoResidentParams")
         .def(py::init<>())
         .RW(CRP, gemm_compute_bound).RW(CRP, gemm_memory_bound).RW(CRP, comm).RW(CRP, comm_all_to_all)
-        .RW(CRP, rate_exponent).RW(CRP, all_gather_by_ranks).RW(CRP, comm_memory_bound);
+        .RW(CRP, rate_exponent).RW(CRP, all_gather_by_ranks).RW(CRP, comm_memory_bound).RW(CRP, cta_cost);
     m.def("load_coresident_params", &cs::load_coresident_params);
     m.def("save_coresident_params", &cs::save_coresident_params);
     m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),

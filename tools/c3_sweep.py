@@ -37,7 +37,7 @@ def main():
             "predicted_makespan_s,t_comm_ctas_ms,comm_pace_gbps"]
     picks = ["scenario_id,collective,model_pick,model_cus_comm,model_pace_gbps,model_predicted_ms,"
              "model_pick_measured_ms,measured_best,measured_best_ms,pick_over_best"]
-    CORES = (16, 24, 32, 48, 64)
+    CORES = (8, 16, 24, 32, 48, 64)
     cores_json = os.path.join(REPO, "data", "b200-coresident.json")
     for name in ("cfg2", "cfg2_448", "cfg3", "cfg4", "cfg4_mb"):
         cfg = CONFIGS[name]

@@ -78,12 +78,50 @@ def predict(d, c, pace, cls, p):
     return c3sim.simulate_coresident(d["tg"], t_at, d["tc"], SMS, c, cls, p, ratio).makespan
 
 
-def error(scen, cls, pg, pc, g, pc_a2a=None):
+def params(pg, pc, g, pc_a2a=None, cta=0.0):
     p = c3sim.CoResidentParams()
     p.gemm_compute_bound = p.gemm_memory_bound = pg
     p.comm, p.comm_all_to_all, p.rate_exponent = pc, pc if pc_a2a is None else pc_a2a, g
     p.all_gather_by_ranks = True  # the all-gather factor tends to the all-to-all one as n -> 2
     p.comm_memory_bound = 1.0     # beside a memory-bound GEMM the collective CTAs lose ~nothing
+    p.cta_cost = cta
+    return p
+
+
+def pick_regret(d, cls, p):
+    """The runtime's co-resident choice (c3_session_choose: every CTA count,
+    the fewest within 1% of the best prediction, then comm pacing over 80% /
+    60% of the GEMM if predicted 0.5% better) against the measured best row of
+    the scenario; None when the pick was not among the measured rows."""
+    meas = {(c, round(pace)): mk for c, pace, mk in d["rows"]}
+    if not meas:
+        return None
+    peer = (d["n"] - 1) / d["n"] * d["mib"] * 2 ** 20
+    link = peer / d["tc"] / 1e9
+    cands = sorted(set([8, 16, 24, 32, 48, 64]) | {c for c in d["pts"]})
+    pred = [(c, predict(d, c, 0.0, cls, p)) for c in cands]
+    best = min(m for _, m in pred)
+    c_pick = next(c for c, m in pred if m <= best * 1.01)
+    pick, pick_m = (c_pick, 0.0), min(m for c, m in pred if c == c_pick)
+    for frac in (0.8, 0.6):
+        pace = peer / (frac * d["tg"]) / 1e9
+        if pace < link:
+            m = predict(d, c_pick, pace, cls, p)
+            if m < pick_m * 0.995:
+                pick, pick_m = (c_pick, pace), m
+    # the measured row of that (c, pace): paced rows were run at frac of a GEMM probe
+    key = None
+    for (c, pr), mk in meas.items():
+        if c == pick[0] and ((pr == 0 and pick[1] == 0) or (pr > 0 and pick[1] > 0 and
+                                                             abs(pr - pick[1]) <= 0.15 * pick[1])):
+            key = (c, pr)
+    if key is None:
+        return None
+    return meas[key] / min(meas.values()) - 1.0
+
+
+def error(scen, cls, pg, pc, g, pc_a2a=None, cta=0.0):
+    p = params(pg, pc, g, pc_a2a, cta)
     err, n = 0.0, 0
     for d in scen.values():
         for c, pace, mk in d["rows"]:
@@ -101,26 +139,40 @@ def main():
     ag = {k: v for k, v in cb.items() if v["ccls"] == c3sim.KernelClass.ALL_GATHER}
     a2a = {k: v for k, v in cb.items() if v["ccls"] != c3sim.KernelClass.ALL_GATHER}
     pcs = [1.0 + 0.1 * i for i in range(21)]                   # 1.0 .. 3.0
-    best = None
-    for pg in [1.0 + 0.02 * i for i in range(31)]:            # 1.0 .. 1.6
-        for g in [0.5 * i for i in range(1, 9)]:              # 0.5 .. 4.0
-            tot, n, pcs_best = 0.0, 0, [0.0, 0.0]
-            # the all-to-all class first: the all-gather factor at small n leans on it
-            for gi, group in ((1, a2a), (0, ag)):
-                if not group:
-                    continue
-                fixed = pcs_best[1] or None
-                e, pc, k = min((error(group, CB, pg, pc, g, fixed if gi == 0 else None)[0], pc,
-                                error(group, CB, pg, pc, g, fixed if gi == 0 else None)[1]) for pc in pcs)
-                tot += e * k
-                n += k
-                pcs_best[gi] = pc
-            if best is None or tot / n < best[0]:
-                best = (tot / n, pg, pcs_best[0], pcs_best[1], g, n)
-    e_cb, pg_cb, pc_ag, pc_a2a, g, n_cb = best
+    fits = []
+    for cta in [0.0, 0.05, 0.1, 0.15, 0.2, 0.3, 0.4, 0.5]:
+        for pg in [1.0 + 0.02 * i for i in range(31)]:        # 1.0 .. 1.6
+            for g in [0.5 * i for i in range(1, 13)]:         # 0.5 .. 6.0
+                tot, n, pcs_best = 0.0, 0, [0.0, 0.0]
+                # the all-to-all class first: the all-gather factor at small n leans on it
+                for gi, group in ((1, a2a), (0, ag)):
+                    if not group:
+                        continue
+                    fixed = pcs_best[1] or None
+                    e, pc, k = min((error(group, CB, pg, pc, g, fixed if gi == 0 else None, cta)[0], pc,
+                                    error(group, CB, pg, pc, g, fixed if gi == 0 else None, cta)[1])
+                                   for pc in pcs)
+                    tot += e * k
+                    n += k
+                    pcs_best[gi] = pc
+                fits.append((tot / n, pg, pcs_best[0], pcs_best[1], g, n, cta))
+    # among the fits within 25% of the lowest mean squared error, the one whose
+    # co-resident pick (the runtime's choice rule) is worst-case closest to the
+    # measured best: the model exists to pick, not to fit
+    fits.sort()
+    near = [f for f in fits if f[0] <= 1.25 * fits[0][0]]
+
+    def worst_regret(f):
+        e, pg, pc_ag, pc_a2a, g, n, cta = f
+        p = params(pg, pc_ag or pc_a2a, g, pc_a2a or pc_ag, cta)
+        r = [pick_regret(d, CB, p) for d in cb.values()]
+        r = [x for x in r if x is not None]
+        return (max(r) if r else 0.0, e)
+    best = min(near, key=worst_regret)
+    e_cb, pg_cb, pc_ag, pc_a2a, g, n_cb, cta = best
     pc = pc_ag or pc_a2a
     pc_a2a = pc_a2a or pc
-    best_mb = min(((error(mb, MB, pg, pc, g, pc_a2a)[0], pg) for pg in [1.0 + 0.02 * i for i in range(31)]),
+    best_mb = min(((error(mb, MB, pg, pc, g, pc_a2a, cta)[0], pg) for pg in [1.0 + 0.02 * i for i in range(31)]),
                   default=(0.0, pg_cb))
     prm = c3sim.CoResidentParams()
     prm.gemm_compute_bound, prm.comm, prm.rate_exponent = pg_cb, pc, g
@@ -128,10 +180,17 @@ def main():
     prm.all_gather_by_ranks = True
     prm.comm_memory_bound = 1.0
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
+    prm.cta_cost = cta
+    regrets = {}
+    for key, d in scen.items():
+        r = pick_regret(d, MB if is_mb(key) else CB, prm)
+        regrets[f"{os.path.basename(key[0])}:{key[1]}/{key[2]}"] = r
     with open(out, "w") as f:
         f.write(c3sim.save_coresident_params(prm))
+    for k, r in sorted(regrets.items()):
+        print(f"  pick regret {k}: " + ("n/a (pick not measured)" if r is None else f"{100 * r:.1f}%"))
     print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc_ag:.2f} (all-gather) / {pc_a2a:.2f} (all-to-all class), "
-          f"rate exponent {g:.2f}, "
+          f"rate exponent {g:.2f}, cta cost {cta:.2f}, "
           f"rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows, paced and unpaced)")
     if mb:
         print(f"memory-bound:  p_g {best_mb[1]:.2f}, rms rel. error {best_mb[0] ** 0.5:.3f}")

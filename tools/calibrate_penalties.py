@@ -1,81 +1,239 @@
-"""B200 calibration loop: measured C3 sweep -> reference
-formats -> the product's `c3sim calibrate` (fit_penalties, calibrate.cpp:95-238)
--> data/b200-loopback-params.json, which the runtime heuristic loads
-(c3_session_load_params).
+#!/usr/bin/env python3
+"""B200 calibration loop: the reference co-run penalties
+(CoRunPenalty, interference.hpp:57-70; their role in simulate(), sim.cpp:121-215)
+re-fitted on measured B200 runs of the final kernels, with a BOUNDED fit.
 
-Inputs: a tools/c3_sweep.py CSV (measured). Outputs in data/:
-  b200-loopback-node.json      machine descriptor (8 ranks, 148 SMs, grain 4)
-  b200-loopback-dataset.json   the swept scenarios with measured isolated times
-  b200-loopback-measured.csv   scenario_id,collective,strategy,measured_speedup
-  b200-loopback-params.json    fitted co-run penalties (SM strategies)
-usage: python tools/calibrate_penalties.py SWEEP.csv
+Rows:
+  * SM strategies with the reference's allocations (c3_base, c3_sp, c3_rp,
+    c3_sp_rp) from a tools/c3_sweep.py CSV (loopback, NVLink-rate emulation):
+    the CU column;
+  * copy-engine strategies (conccl, conccl_rp) from a tools/ce_proxy_sweep.py
+    CSV (the host-staged copy-engine proxy): the DMA column.
+For each row the product model predicts the makespan exactly as the runtime
+does (c3_session_predict): the scenario's measured isolated times
+(GemmKernel / CollectiveOp::measured_time), the B200 machine file
+(data/b200-node-n8.json), the measured slowdown tables with the collective's
+comm curve (CU rows), and for DMA rows the link bandwidth at which the plan's
+cost reproduces the measured copy-engine time. The 8 penalties (4 kernel
+classes x {cu, dma}) minimise the squared relative makespan error with
+scipy.optimize.least_squares, every penalty bounded to [1, 3]: a co-run
+penalty below 1 would be a speed-up, and the reference's defaults
+(proj/data/default-params.json) span 1.02-3.5. Unidentified penalties (no row
+exercises them) stay at 1.0 and are listed.
+
+The reference's own fit (c3sim calibrate, calibrate.cpp:95-238, unbounded
+Levenberg-Marquardt) degenerated on these rows in round 1 (GEMM penalties
+13.3 / 1.64): it trades physically meaningless penalties for a lower RMS.
+
+Outputs: data/b200-loopback-params.json (RunParams format, loaded by
+c3_session_load_params) and data/b200-loopback-params.fit.json (per-row
+residuals, RMS per strategy class, the bounds, the active bounds).
+
+usage: python tools/calibrate_penalties.py SM_SWEEP.csv [CE_PROXY_SWEEP.csv]
 """
 import csv
 import json
+import math
 import os
-import subprocess
 import sys
 
+import numpy as np
+from scipy.optimize import least_squares
+
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, os.path.join(REPO, "paper_2412_14335_b200", "python"))
 sys.path.insert(0, REPO)
+import c3sim  # noqa: E402
 from bench import CONFIGS  # noqa: E402
 
 DATA = os.path.join(REPO, "data")
-CLI = os.path.join(REPO, "paper_2412_14335_b200", "bin", "c3sim")
-MACHINE = {
-    "gpus_per_node": 8, "cus_per_gpu": 148, "xcds_per_gpu": 2, "cus_per_xcd": 74,
-    "min_cu_grain": 4, "dma_engines_per_gpu": 4, "peak_compute_flops": 1.6097e15,
-    "hbm_bandwidth": 6.5383e12, "llc_capacity": 132644864,
-    "link_bandwidth_unidir": 900e9 / 7, "links_per_gpu": 7, "topology": "fully-connected",
-    "cpu_launch_overhead": 2e-6, "dma_sync_overhead": 1e-5}
-SM_STRATEGIES = ("c3_base", "c3_sp", "c3_rp", "c3_sp_rp")
+SM = ("c3_base", "c3_sp", "c3_rp", "c3_sp_rp")
+DMA = ("conccl", "conccl_rp")
+CLASSES = ("gemm-compute-bound", "gemm-memory-bound", "all-gather", "all-to-all")
+KC = {"gemm-compute-bound": c3sim.KernelClass.GEMM_COMPUTE_BOUND,
+      "gemm-memory-bound": c3sim.KernelClass.GEMM_MEMORY_BOUND,
+      "all-gather": c3sim.KernelClass.ALL_GATHER, "all-to-all": c3sim.KernelClass.ALL_TO_ALL}
+KIND = {"all-gather": c3sim.CollectiveKind.ALL_GATHER, "all-to-all": c3sim.CollectiveKind.ALL_TO_ALL,
+        "reduce-scatter": c3sim.CollectiveKind.REDUCE_SCATTER}
+STRAT = {s: getattr(c3sim.Strategy, s.upper()) for s in SM + DMA}
+LO, HI = 1.0, 3.0
+
+
+def scenario(m, n, k, coll, payload, t_gemm_s, t_comm_s, md):
+    sc = c3sim.C3Scenario()
+    sc.id = "row"
+    sc.gemm.tag = "gemm"
+    sc.gemm.m, sc.gemm.n, sc.gemm.k, sc.gemm.dtype_bytes = m, n, k, 2
+    sc.gemm.measured_time = t_gemm_s
+    sc.gemm.boundedness_override = c3sim.classify_gemm_boundedness(sc.gemm, c3sim.machine_op_to_byte(md))
+    sc.collective.kind = KIND[coll]
+    sc.collective.payload_bytes = payload
+    sc.collective.n_ranks = 8
+    sc.collective.measured_time = t_comm_s
+    return sc
+
+
+def dma_machine(md_text, coll, payload, t_dma_s):
+    """Machine whose link bandwidth makes the plan's cost equal the measured
+    copy-engine time (the runtime's predict_makespan does the same)."""
+    md = c3sim.load_machine(md_text)
+    md.cpu_launch_overhead = 0.0
+    md.dma_sync_overhead = 0.0
+    md.link_bandwidth_unidir = 1.0
+    chunk = payload // 8
+    plan = {"all-gather": c3sim.plan_all_gather, "all-to-all": c3sim.plan_all_to_all,
+            "reduce-scatter": c3sim.plan_reduce_scatter}[coll](8, chunk, md)
+    eff = c3sim.EfficiencyParams()
+    eff.efficiency = 1.0
+    at_unit = c3sim.plan_cost(plan, md, eff).total
+    fixed = (payload + chunk) / md.hbm_bandwidth if coll == "reduce-scatter" else 0.0
+    md.link_bandwidth_unidir = at_unit / max(t_dma_s - fixed, 0.05 * t_dma_s)
+    return md
+
+
+def sm_rows(path, md, base_tables):
+    rows, curves = [], {}
+    recs = list(csv.DictReader(open(path)))
+    for r in recs:  # the collective's measured time vs CTA units (co-resident rows)
+        if r["strategy"].startswith("c3_base_coresident") and r.get("t_comm_ctas_ms") and \
+                float(r.get("comm_pace_gbps") or 0) == 0:
+            curves.setdefault((r["scenario_id"], r["collective"]), {})[int(r["cus_comm"])] = \
+                float(r["t_comm_ctas_ms"]) * 1e-3
+    for r in recs:
+        if r["strategy"] not in SM:
+            continue
+        cfg = CONFIGS[r["scenario_id"].rsplit("_", 1)[0]]
+        tg, tc = float(r["t_gemm_iso_ms"]) * 1e-3, float(r["t_comm_iso_ms"]) * 1e-3
+        sc = scenario(cfg["m"], cfg["n"], cfg["k"], r["collective"], cfg["payload"], tg, tc, md)
+        tables = base_tables
+        pts = curves.get((r["scenario_id"], r["collective"]))
+        if pts:
+            pts = dict(pts)
+            pts[md.cus_per_gpu] = tc
+            c = sorted(pts)
+            curve = c3sim.CommCurve([int(x) for x in c], [pts[x] for x in c])
+            tables = c3sim.load_slowdown_tables(os.path.join(DATA, "b200-loopback-slowdown-tables.csv"),
+                                                md.min_cu_grain)
+            cls = KC["all-gather" if r["collective"] == "all-gather" else "all-to-all"]
+            tables.set(cls, curve.as_table(cls, md))
+        rows.append({"id": f'{r["scenario_id"]}/{r["collective"]}', "strategy": r["strategy"], "sc": sc,
+                     "md": md, "tables": tables, "measured": float(r["makespan_s"]), "backend": "cu"})
+    return rows
+
+
+def dma_rows(path, md_text, tables):
+    rows = []
+    for r in csv.DictReader(open(path)):
+        if r["strategy"] not in DMA:
+            continue
+        m, n, k = (int(x) for x in r["scenario_id"].split("_")[1].split("x"))
+        payload = int(r["scenario_id"].rsplit("_", 1)[1].rstrip("M")) << 20
+        tg, td = float(r["t_gemm_iso_ms"]) * 1e-3, float(r["t_comm_dma_ms"]) * 1e-3
+        md = dma_machine(md_text, r["collective"], payload, td)
+        sc = scenario(m, n, k, r["collective"], payload, tg, td, md)
+        rows.append({"id": f'{r["scenario_id"]}/{r["collective"]}', "strategy": r["strategy"], "sc": sc,
+                     "md": md, "tables": tables, "measured": float(r["makespan_s"]), "backend": "dma"})
+    return rows
+
+
+def unpack(x):
+    """x = 4 DMA penalties in [1, 3] + 4 CU excesses in [0, 2]: the reference
+    requires CU >= DMA per kernel class (interference.cpp validate), so
+    cu = min(3, dma + excess)."""
+    dma = np.asarray(x[4:], dtype=float)
+    cu = np.minimum(HI, dma + np.asarray(x[:4], dtype=float))
+    return cu, dma
+
+
+def penalty(x):
+    cu, dma = unpack(x)
+    pen = c3sim.CoRunPenalty.ones()
+    for i, cls in enumerate(CLASSES):
+        pen.set(KC[cls], c3sim.CommBackend.CU, float(cu[i]))
+        pen.set(KC[cls], c3sim.CommBackend.DMA, float(dma[i]))
+    return pen
+
+
+def predict(rows, x):
+    eff = c3sim.EfficiencyParams()
+    eff.efficiency = 1.0
+    eff.comm_launch_overhead_cu = 0.0
+    pen = penalty(x)
+    return np.array([c3sim.simulate(r["sc"], STRAT[r["strategy"]], r["md"], r["tables"], pen, eff).makespan
+                     for r in rows])
 
 
 def main():
-    rows = list(csv.DictReader(open(sys.argv[1])))
-    os.makedirs(DATA, exist_ok=True)
-    with open(os.path.join(DATA, "b200-loopback-node.json"), "w") as f:
-        json.dump(MACHINE, f, indent=2)
-    scenarios, measured, seen = [], [], set()
-    for r in rows:
-        sid, coll = r["scenario_id"], r["collective"]
-        cfg_name = sid.rsplit("_", 1)[0]
-        cfg = CONFIGS[cfg_name]
-        if (sid, coll) not in seen:
-            seen.add((sid, coll))
-            payload = cfg["payload"]
-            scenarios.append({
-                "id": sid, "source": "B200 loopback measurement",
-                "gemm": {"tag": cfg_name, "m": cfg["m"], "n": cfg["n"], "k": cfg["k"],
-                         "dtype_bytes": 2, "measured_time": float(r["t_gemm_iso_ms"]) * 1e-3},
-                "collective": {"kind": coll, "payload_bytes": payload, "n_ranks": 8,
-                               "measured_time": float(r["t_comm_iso_ms"]) * 1e-3}})
-        if r["strategy"] in SM_STRATEGIES:
-            measured.append((sid, coll, r["strategy"], float(r["speedup"])))
-    ds = os.path.join(DATA, "b200-loopback-dataset.json")
-    with open(ds, "w") as f:
-        json.dump(scenarios, f, indent=2)
-    mp = os.path.join(DATA, "b200-loopback-measured.csv")
-    with open(mp, "w") as f:
-        f.write("scenario_id,collective,strategy,measured_speedup\n")
-        for m in measured:
-            f.write("%s,%s,%s,%.9g\n" % m)
-    start = os.path.join(DATA, "b200-start-params.json")
-    with open(start, "w") as f:  # start from unit penalties (no prior about B200)
-        json.dump({"efficiency": 1.0, "comm_launch_overhead_cu": 0.0,
-                   "co_run_penalty": {c: {"cu": 1.0, "dma": 1.0} for c in
-                                      ("gemm-compute-bound", "gemm-memory-bound", "all-gather",
-                                       "all-to-all")},
-                   "freeze_phase2_allocation": False}, f, indent=2)
-    out = os.path.join(DATA, "b200-loopback-params.json")
-    r = subprocess.run([CLI, "calibrate", "--machine", os.path.join(DATA, "b200-loopback-node.json"),
-                        "--dataset", ds, "--tables",
-                        os.path.join(DATA, "b200-loopback-slowdown-tables.csv"), "--params", start,
-                        "--measured", mp, "--out", out], capture_output=True, text=True)
-    os.remove(start)
-    print(r.stdout)
-    print(r.stderr, file=sys.stderr)
-    sys.exit(r.returncode)
+    sm_csv = sys.argv[1]
+    ce_csv = sys.argv[2] if len(sys.argv) > 2 else None
+    md_path = os.path.join(DATA, "b200-node-n8.json")
+    md_text = open(md_path).read()
+    md = c3sim.load_machine(md_text)
+    tables = c3sim.load_slowdown_tables(os.path.join(DATA, "b200-loopback-slowdown-tables.csv"), md.min_cu_grain)
+    rows = sm_rows(sm_csv, md, tables) + (dma_rows(ce_csv, md_text, tables) if ce_csv else [])
+    meas = np.array([r["measured"] for r in rows])
+
+    def resid(x):
+        return predict(rows, x) / meas - 1.0
+
+    x0 = np.concatenate([np.zeros(4), np.ones(4)])
+    lo = np.concatenate([np.zeros(4), np.full(4, LO)])
+    hi = np.concatenate([np.full(4, HI - LO), np.full(4, HI)])
+    fit = least_squares(resid, x0 + 0.01, bounds=(lo, hi), diff_step=1e-3)
+    res = resid(fit.x)
+    res0 = resid(x0)
+    cu, dma = unpack(fit.x)
+    x = np.concatenate([cu, dma])  # the penalties themselves from here on
+
+    def predict_pen(xx):  # predictions from explicit (cu, dma) penalties
+        return predict(rows, np.concatenate([xx[:4] - xx[4:], xx[4:]]))
+
+    def rms(v):
+        return float(math.sqrt(np.mean(np.square(v)))) if len(v) else float("nan")
+
+    # a penalty is identified when moving it changes some row's prediction
+    ident = []
+    base = predict_pen(x)
+    for i in range(8):
+        xp = x.copy()
+        xp[i] = xp[i] + 0.1 if xp[i] < HI - 0.1 else xp[i] - 0.1
+        if i < 4:
+            xp[i] = max(xp[i], xp[4 + i])
+        else:
+            xp[i - 4] = max(xp[i - 4], xp[i])
+        ident.append(bool(np.max(np.abs(predict_pen(xp) - base)) > 1e-9))
+    for i in range(4):  # unidentified: back to 1.0 (keeping CU >= DMA)
+        if not ident[4 + i]:
+            x[4 + i] = 1.0
+        if not ident[i]:
+            x[i] = x[4 + i]
+    params = {"efficiency": 1.0, "comm_launch_overhead_cu": 0.0,
+              "co_run_penalty": {cls: {"cu": round(float(x[i]), 4), "dma": round(float(x[4 + i]), 4)}
+                                 for i, cls in enumerate(CLASSES)},
+              "freeze_phase2_allocation": False}
+    names = [f"{c}.cu" for c in CLASSES] + [f"{c}.dma" for c in CLASSES]
+    report = {
+        "what": "bounded least-squares fit of the reference co-run penalties on measured B200 rows "
+                "(tools/calibrate_penalties.py)",
+        "inputs": [os.path.relpath(p, REPO) for p in (sm_csv, ce_csv) if p],
+        "machine": os.path.relpath(md_path, REPO), "bounds": [LO, HI],
+        "rows": len(rows), "rows_cu": sum(r["backend"] == "cu" for r in rows),
+        "rows_dma": sum(r["backend"] == "dma" for r in rows),
+        "rms_rel_error": rms(res), "rms_rel_error_unit_penalties": rms(res0),
+        "rms_by_strategy": {s: rms([e for e, r in zip(res, rows) if r["strategy"] == s])
+                            for s in SM + DMA if any(r["strategy"] == s for r in rows)},
+        "penalties": dict(zip(names, [round(float(v), 4) for v in x])),
+        "identified": dict(zip(names, ident)),
+        "at_bound": [nm for nm, v, i in zip(names, x, ident) if i and (v <= LO + 1e-6 or v >= HI - 1e-6)],
+        "per_row": [{"row": r["id"], "strategy": r["strategy"], "measured_ms": 1e3 * r["measured"],
+                     "predicted_ms": 1e3 * r["measured"] * (1 + e), "rel_error": float(e)}
+                    for r, e in zip(rows, res)],
+    }
+    with open(os.path.join(DATA, "b200-loopback-params.json"), "w") as f:
+        json.dump(params, f, indent=2)
+    with open(os.path.join(DATA, "b200-loopback-params.fit.json"), "w") as f:
+        json.dump(report, f, indent=1)
+    print(json.dumps({k: v for k, v in report.items() if k != "per_row"}, indent=1))
 
 
 if __name__ == "__main__":
