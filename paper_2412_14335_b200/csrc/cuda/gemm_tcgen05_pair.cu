@@ -102,6 +102,11 @@ struct Params {
     // tile's time. full_tiles = num_units = num_tiles when not split.
     int full_tiles, num_units;
     RowGate gate;  // A rows landing during the launch (flags == nullptr: all resident)
+    // dev A/B only (C3_GEMM_DEV, results invalid when set): bit 0 every tile
+    // loads the operands of tile (0, 0) (L2-resident: the cost of DRAM traffic),
+    // bit 1 the epilogue releases the accumulator without draining it (the
+    // cost of the exposed TMEM drain)
+    int dev;
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -406,6 +411,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             int tm, tn, t_idx, half;
             unit_tile(p, tile, t_idx, half);
             tile_coords(p, t_idx, tm, tn);
+            if (p.dev & 1) tm = tn = 0;
             const int a_row = tm * BM + static_cast<int>(rank) * 128;
             if (p.gate.flags != nullptr) {
                 const int band = a_row / p.gate.rows_per_flag;
@@ -579,6 +585,22 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int col_base = tn * BN + (half > 0 ? 256 : 0);
             mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
+            if (p.dev & 2) {  // dev: release without draining
+                __syncwarp();
+                if (lane == 0)
+                    for (int h = 0; h < (Cfg::HALVES == 2 ? 2 : 1); ++h) {
+                        const int rel = Cfg::HALVES == 2 ? h : acc;
+                        if (leader)
+                            mbar_arrive(&acc_empty[rel]);
+                        else
+                            mbar_arrive_cluster(mapa(smem_u32(&acc_empty[rel]), 0));
+                    }
+                if (++acc == ACC_BUFS) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
+                continue;
+            }
             // TMEM row `lane` of this warp's quadrant -> packed bf16 -> the
             // warp's 32 x 64 staging tile in shared memory (16-byte chunks
             // XOR-swizzled by row: the TMA 128B swizzle) -> one TMA tensor
@@ -756,6 +778,11 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return v < 1 ? 1 : v > gemm2::PairCfg<512>::STAGES ? gemm2::PairCfg<512>::STAGES : v;
     }();
     p.pre_half = pre_half;
+    static const int dev = [] {
+        const char* e = std::getenv("C3_GEMM_DEV");  // dev A/B only: results invalid
+        return e ? std::atoi(e) : 0;
+    }();
+    p.dev = dev;
 
     const bool wide = plan->kind == GemmPlan::kPair512;
     // tail split (512-wide): if the last wave is at most half full, its tiles
