@@ -120,9 +120,11 @@ int coresident_comm_ctas(int cus_comm, const CoResidentParams& p,
 /// the GEMM penalty's excess scales by rate_ratio^rate_exponent.
 /// A paced collective's t_comm_at_ctas is the longer of the curve time and
 /// bytes / paced rate (the caller's).
+/// t_comm_alone_at_ctas (> 0): the collective's time on its cus_comm CTAs once
+/// the GEMM is gone (phase 2: no co-residency cost factor); 0 = t_comm_at_ctas.
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
                                 int cus_comm, KernelClass gemm_class, const CoResidentParams& p,
-                                double rate_ratio = 1.0);
+                                double rate_ratio = 1.0, double t_comm_alone_at_ctas = 0.0);
 
 /// Penalty p_g that makes simulate_coresident reproduce a measured makespan
 /// (collective finishing first, p_c = 1); clamped to [1, 100]. Returns 1.0

@@ -95,6 +95,7 @@ struct Params {
     int* exit_counter;
     int group_m;
     int pol_a, pol_b;  // L2 policy of the A / B operand loads (policy_by_kind)
+    int pol_c;         // L2 policy hint of the C stores (0: none)
     int pre_half;      // BN 512: k-blocks into half 0 before waiting for half 1 (<= STAGES)
     // BN 512 tail split: claims u < full_tiles are whole tiles; the last
     // num_tiles - full_tiles tiles are claimed as two 256-column halves each
@@ -629,7 +630,10 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 fence_proxy_async_shared();
                 __syncwarp();
                 if (lane == 0) {
-                    tma_store_2d(&map_c, stg, col_base + c, row0);
+                    if (p.pol_c)
+                        tma_store_2d_hint(&map_c, stg, col_base + c, row0, policy_by_kind(p.pol_c));
+                    else
+                        tma_store_2d(&map_c, stg, col_base + c, row0);
                     bulk_commit();
                 }
                 if (++stg_i == EPI_BUFS) stg_i = 0;
@@ -768,10 +772,12 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
     // profiles/r01_gemm_l2_policy_ab.txt)
     static const int pol = [] {
         const char* e = std::getenv("C3_GEMM_POL");
-        return e && e[0] && e[1] ? (e[0] - '0') * 10 + (e[1] - '0') : 11;
+        if (!(e && e[0] && e[1])) return 110;
+        return (e[0] - '0') * 100 + (e[1] - '0') * 10 + (e[2] ? e[2] - '0' : 0);
     }();
-    p.pol_a = pol / 10;
-    p.pol_b = pol % 10;
+    p.pol_a = pol / 100;
+    p.pol_b = pol / 10 % 10;
+    p.pol_c = pol % 10;
     static const int pre_half = [] {
         const char* e = std::getenv("C3_GEMM_PREHALF");  // dev A/B
         const int v = e ? std::atoi(e) : gemm2::kPreHalf;

@@ -403,6 +403,7 @@ struct c3_session {
     c3sim::SlowdownTableSet tables_loaded;  // as loaded (tables' comm class may come from comm_curve)
     bool tables_from_file = false;
     c3sim::CoRunPenalty penalties = c3sim::CoRunPenalty::ones();  // c3_session_load_params
+    bool freeze_phase2 = false;                                      // ... its freeze_phase2_allocation
     c3sim::C3Scenario scenario;
     c3sim::CommCurve comm_curve;            // c3_session_set_comm_curve (seconds)
     bool coresident = false;                // c3_session_load_coresident: model co-residency
@@ -1279,7 +1280,9 @@ double predict_makespan(c3_session* s, int st, double t_gemm_ms, double t_comm_c
         const double t_dma = t_comm_dma_ms * 1e-3;
         md.link_bandwidth_unidir = at_unit / std::max(t_dma - fixed, 0.05 * t_dma);
     }
-    return c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff).makespan;
+    c3sim::SimOptions opt;
+    opt.freeze_phase2_allocation = s->freeze_phase2;
+    return c3sim::simulate(x, static_cast<c3sim::Strategy>(st), md, s->tables, pen, eff, opt).makespan;
 }
 
 // Collective time (ms) on `ctas` CTAs given its measured full-GPU time: the
@@ -1308,13 +1311,17 @@ double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, doubl
     const int eff = c3sim::coresident_comm_ctas(ctas, s->cores,
                                                 c3sim::comm_kernel_class(s->scenario.collective.kind), s->n, gcls);
     double t_at = comm_ms_at(s, eff, t_comm_cu_ms);
+    double t_alone = comm_ms_at(s, ctas, t_comm_cu_ms);  // after the GEMM: the same CTAs, alone
     const double link = link_rate_gbps(s, t_comm_cu_ms);
-    if (pace_gbps > 0.0 && pace_gbps < link) t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));
+    if (pace_gbps > 0.0 && pace_gbps < link) {
+        t_at = std::max(t_at, peer_bytes(s) / (pace_gbps * 1e6));
+        t_alone = std::max(t_alone, peer_bytes(s) / (pace_gbps * 1e6));
+    }
     // the collective's actual rate relative to its unpaced full-GPU rate: pacing
     // or too few co-resident CTAs both lower its intensity beside the GEMM
     const double ratio = std::min(1.0, t_comm_cu_ms / t_at);
     return c3sim::simulate_coresident(t_gemm_ms * 1e-3, t_at * 1e-3, t_comm_cu_ms * 1e-3, s->md.cus_per_gpu,
-                                      ctas, gcls, s->cores, ratio)
+                                      ctas, gcls, s->cores, ratio, t_alone * 1e-3)
         .makespan;
 }
 
@@ -1397,7 +1404,11 @@ int c3_session_load_machine(c3_session* s, const char* machine_json_path) {
 int c3_session_load_params(c3_session* s, const char* params_json_path) {
     if (!s || !params_json_path) return set_error(C3_ERR_VALIDATION, "c3_session_load_params: null argument");
     return guarded([&] {
-        s->penalties = c3sim::load_params_file(params_json_path).penalties;
+        const c3sim::RunParams rp = c3sim::load_params_file(params_json_path);
+        s->penalties = rp.penalties;
+        // green-context partitions stay in place after the collective ends
+        // (c3_rp / c3_sp_rp): the reference's freeze_phase2_allocation option
+        s->freeze_phase2 = rp.freeze_phase2_allocation;
         return C3_OK;
     });
 }
@@ -1442,50 +1453,46 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
                 best_st = st;
             }
         }
-        // B200 co-resident candidates: GEMM on every SM, collective CTAs beside
-        // it. Among them the FEWEST CTAs within 1% of the best prediction win:
-        // past the link-bound plateau extra comm CTAs only add interference the
-        // fluid model does not see (measured: c3_sp on 64 CTAs 10% slower than
-        // on 24, profiles/r01_c3_sweep_link770_cores.csv).
+        // B200 co-resident candidates: GEMM on every SM, the collective on c
+        // CTA units beside it, unpaced or paced to spread over 80% / 60% of
+        // the GEMM (below its unpaced rate), every (c, pace) predicted jointly.
+        // Among those within 1% of the best prediction the FEWEST CTAs win
+        // (then the lowest prediction): extra resident CTAs cost the GEMM more
+        // than the fluid model sees.
         int best_cores = 0;
+        double best_pace = 0.0;
         if (s->coresident) {
             std::vector<int> cands = {8, 16, 24, 32, 48, 64};
             for (int c : s->comm_curve.ctas) cands.push_back(c);
             std::sort(cands.begin(), cands.end());
             cands.erase(std::unique(cands.begin(), cands.end()), cands.end());
-            std::vector<std::pair<int, double>> pred;
+            const double link = link_rate_gbps(s, t_comm_cu_ms);
+            struct Cand {
+                int c;
+                double pace, m;
+            };
+            std::vector<Cand> pred;
             double best_co = 1e300;
-            // every count: a collective slowed by few CTAs still hides under a
-            // longer GEMM, and every resident CTA costs the GEMM (cta_cost)
             for (int c : cands) {
                 if (c < 1 || c >= s->md.cus_per_gpu) continue;
-                pred.emplace_back(c, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms));
-                best_co = std::min(best_co, pred.back().second);
-            }
-            for (const auto& [c, m] : pred) {
-                if (m <= best_co * 1.01) {  // ascending c: the first within 1%
-                    if (m < best) {
-                        best = m;
-                        best_st = C3_C3_BASE;
-                        best_cores = c;
-                    }
-                    break;
+                pred.push_back({c, 0.0, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms)});
+                for (double frac : {0.8, 0.6}) {
+                    const double pace = peer_bytes(s) / (frac * t_gemm_ms * 1e6);
+                    if (pace < link) pred.push_back({c, pace, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms, pace)});
                 }
             }
-        }
-        // comm pacing of the co-resident pick: the collective spread over
-        // 60% / 80% of the GEMM, when that is below its unpaced rate
-        double best_pace = 0.0;
-        if (best_cores) {
-            const double link = link_rate_gbps(s, t_comm_cu_ms);
-            for (double frac : {0.8, 0.6}) {
-                const double pace = peer_bytes(s) / (frac * t_gemm_ms * 1e6);
-                if (!(pace < link)) continue;
-                const double m = predict_coresident(s, best_cores, t_gemm_ms, t_comm_cu_ms, pace);
-                if (m < best * 0.995) {
-                    best = m;
-                    best_pace = pace;
+            for (const Cand& x : pred) best_co = std::min(best_co, x.m);
+            const Cand* pick = nullptr;
+            for (const Cand& x : pred)  // ascending c
+                if (x.m <= best_co * 1.01 && (!pick || (x.c == pick->c && x.m < pick->m))) {
+                    if (pick && x.c != pick->c) break;
+                    pick = &x;
                 }
+            if (pick && pick->m < best) {
+                best = pick->m;
+                best_st = C3_C3_BASE;
+                best_cores = pick->c;
+                best_pace = pick->pace;
             }
         }
         *strategy = best_st;

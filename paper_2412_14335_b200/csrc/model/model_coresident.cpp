@@ -109,7 +109,8 @@ int coresident_comm_ctas(int cus_comm, const CoResidentParams& p, KernelClass co
 
 SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_comm_full, int cus,
                                 int cus_comm, KernelClass gemm_class, const CoResidentParams& p,
-                                double rate_ratio) {
+                                double rate_ratio, double t_comm_alone_at_ctas) {
+    if (!(t_comm_alone_at_ctas > 0)) t_comm_alone_at_ctas = t_comm_at_ctas;
     validate(p);
     if (!(t_gemm > 0) || !(t_comm_at_ctas > 0) || !(t_comm_full > 0))
         throw ValidationError("simulate_coresident: isolated times must be positive");
@@ -131,8 +132,9 @@ SimTimeline simulate_coresident(double t_gemm, double t_comm_at_ctas, double t_c
         tl.makespan = t1 + (t_gemm - t1 * rg);
         tl.phases.push_back({t1, tl.makespan, 1.0, 0.0, cus, 0});
     } else if (end_g < end_c) {  // the collective finishes alone on its CTAs
-        tl.makespan = t1 + (t_comm_full - t1 * rc) * (t_comm_at_ctas / t_comm_full);
-        tl.phases.push_back({t1, tl.makespan, 0.0, t_comm_full / t_comm_at_ctas, 0, cus_comm});
+        // its CTAs alone on their SMs now: the curve's time, no co-residency factor
+        tl.makespan = t1 + (t_comm_full - t1 * rc) * (t_comm_alone_at_ctas / t_comm_full);
+        tl.phases.push_back({t1, tl.makespan, 0.0, t_comm_full / t_comm_alone_at_ctas, 0, cus_comm});
     } else {
         tl.makespan = t1;
     }

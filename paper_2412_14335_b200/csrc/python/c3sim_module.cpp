@@ -238,7 +238,7 @@ void add_sim(py::module_& m) {
     m.def("save_coresident_params", &cs::save_coresident_params);
     m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),
           py::arg("t_comm_full"), py::arg("cus"), py::arg("cus_comm"), py::arg("gemm_class"), py::arg("params"),
-          py::arg("rate_ratio") = 1.0);
+          py::arg("rate_ratio") = 1.0, py::arg("t_comm_alone_at_ctas") = 0.0);
     m.def("fit_coresident_gemm_penalty", &cs::fit_coresident_gemm_penalty);
     m.def("coresident_comm_ctas", &cs::coresident_comm_ctas, py::arg("cus_comm"), py::arg("params"),
           py::arg("comm_class") = cs::KernelClass::AllGather, py::arg("n_ranks") = 0,

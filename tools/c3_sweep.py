@@ -64,7 +64,7 @@ def main():
             # over 60% / 80% of the GEMM (rate from a quick GEMM probe)
             tg0 = statistics.median(s.run(c3.GEMM_ONLY).total_ms for _ in range(3))
             peer = (8 - 1) / 8 * cfg["payload"]
-            for ctas in (16, 24):
+            for ctas in (8, 16, 24):
                 for frac in (0.6, 0.8):
                     pace = peer / (frac * tg0 * 1e-3) / 1e9
                     if link > 0 and pace >= link:
@@ -135,14 +135,32 @@ def main():
             key = next((k for k, (_, s2, a2) in measured.items()
                         if s2 == st and a2.cus_gemm == al.cus_gemm and a2.cus_comm == al.cus_comm
                         and same_pace(a2.comm_pace_gbps, al.comm_pace_gbps)), None)
-            if st == c3.SERIAL:
-                key, pk = "serial", tg + tc
-            else:
-                pk = measured[key][0] if key else float("nan")
             best = min(measured, key=lambda k: measured[k][0])
             bm = min(measured[best][0], tg + tc)
             if tg + tc < measured[best][0]:
                 best = "serial"
+            if st == c3.SERIAL:
+                key, pk = "serial", tg + tc
+            elif key:
+                pk = measured[key][0]
+            else:
+                # the pick was not among the swept jobs: measure it head to head
+                # against the measured best, alternating, and scale to the sweep
+                if best == "serial":
+                    pair = {"pick": (st, al), "best": None}
+                else:
+                    pair = {"pick": (st, al), "best": jobs[best]}
+                hh = {"pick": [], "best": []}
+                for r in range(R):
+                    for k2 in (("pick", "best") if r % 2 == 0 else ("best", "pick")):
+                        if pair[k2] is None:
+                            tmg = s.run(c3.GEMM_ONLY, jobs["gemm"][1]).total_ms
+                            tmc = s.run(*jobs["comm"]).total_ms
+                            hh[k2].append(tmg + tmc)
+                        else:
+                            hh[k2].append(s.run(*pair[k2]).total_ms)
+                pk = bm * statistics.median(hh["pick"]) / statistics.median(hh["best"])
+                key = f"model_pick(c{al.cus_comm},pace{al.comm_pace_gbps:.0f})"
             picks.append(f"{sid},{coll},{key or c3.STRATEGY_NAMES[st]},{al.cus_comm},{al.comm_pace_gbps:.0f},"
                          f"{pred:.4f},{pk:.4f},"
                          f"{best},{bm:.4f},{pk / bm:.4f}")

@@ -4,9 +4,15 @@
 re-fitted on measured B200 runs of the final kernels, with a BOUNDED fit.
 
 Rows:
-  * SM strategies with the reference's allocations (c3_base, c3_sp, c3_rp,
-    c3_sp_rp) from a tools/c3_sweep.py CSV (loopback, NVLink-rate emulation):
-    the CU column;
+  * SM strategies with the reference's allocations from a tools/c3_sweep.py
+    CSV (loopback, NVLink-rate emulation): the CU column is FITTED on c3_rp /
+    c3_sp_rp only, whose green-context SM partition is the execution the
+    reference model describes (cus_gemm + cus_comm <= C, sim.cpp:40-100).
+    c3_base / c3_sp with the reference allocations are reported but not
+    fitted: on B200 their collective CTAs co-reside with the GEMM's CTAs on
+    the same SMs, an execution the CU-partition model cannot
+    express with any penalty (the runtime predicts co-resident runs with the
+    co-residency extension, c3sim/coresident.hpp);
   * copy-engine strategies (conccl, conccl_rp) from a tools/ce_proxy_sweep.py
     CSV (the host-staged copy-engine proxy): the DMA column.
 For each row the product model predicts the makespan exactly as the runtime
@@ -48,6 +54,7 @@ from bench import CONFIGS  # noqa: E402
 
 DATA = os.path.join(REPO, "data")
 SM = ("c3_base", "c3_sp", "c3_rp", "c3_sp_rp")
+FITTED = ("c3_rp", "c3_sp_rp", "conccl", "conccl_rp")
 DMA = ("conccl", "conccl_rp")
 CLASSES = ("gemm-compute-bound", "gemm-memory-bound", "all-gather", "all-to-all")
 KC = {"gemm-compute-bound": c3sim.KernelClass.GEMM_COMPUTE_BOUND,
@@ -154,12 +161,20 @@ def penalty(x):
     return pen
 
 
+# A green-context partition stays in place after the collective ends: the
+# GEMM of c3_rp / c3_sp_rp keeps its cus_gemm SMs (freeze_phase2_allocation,
+# sim.cpp:172-200); copy-engine runs leave every SM to the GEMM either way.
+FREEZE = True
+
+
 def predict(rows, x):
     eff = c3sim.EfficiencyParams()
     eff.efficiency = 1.0
     eff.comm_launch_overhead_cu = 0.0
     pen = penalty(x)
-    return np.array([c3sim.simulate(r["sc"], STRAT[r["strategy"]], r["md"], r["tables"], pen, eff).makespan
+    opt = c3sim.SimOptions()
+    opt.freeze_phase2_allocation = FREEZE
+    return np.array([c3sim.simulate(r["sc"], STRAT[r["strategy"]], r["md"], r["tables"], pen, eff, opt).makespan
                      for r in rows])
 
 
@@ -170,8 +185,10 @@ def main():
     md_text = open(md_path).read()
     md = c3sim.load_machine(md_text)
     tables = c3sim.load_slowdown_tables(os.path.join(DATA, "b200-loopback-slowdown-tables.csv"), md.min_cu_grain)
-    rows = sm_rows(sm_csv, md, tables) + (dma_rows(ce_csv, md_text, tables) if ce_csv else [])
+    all_rows = sm_rows(sm_csv, md, tables) + (dma_rows(ce_csv, md_text, tables) if ce_csv else [])
+    rows = [r for r in all_rows if r["strategy"] in FITTED]
     meas = np.array([r["measured"] for r in rows])
+    meas_all = np.array([r["measured"] for r in all_rows])
 
     def resid(x):
         return predict(rows, x) / meas - 1.0
@@ -182,6 +199,7 @@ def main():
     fit = least_squares(resid, x0 + 0.01, bounds=(lo, hi), diff_step=1e-3)
     res = resid(fit.x)
     res0 = resid(x0)
+    res_all = predict(all_rows, fit.x) / meas_all - 1.0
     cu, dma = unpack(fit.x)
     x = np.concatenate([cu, dma])  # the penalties themselves from here on
 
@@ -210,7 +228,7 @@ def main():
     params = {"efficiency": 1.0, "comm_launch_overhead_cu": 0.0,
               "co_run_penalty": {cls: {"cu": round(float(x[i]), 4), "dma": round(float(x[4 + i]), 4)}
                                  for i, cls in enumerate(CLASSES)},
-              "freeze_phase2_allocation": False}
+              "freeze_phase2_allocation": FREEZE}
     names = [f"{c}.cu" for c in CLASSES] + [f"{c}.dma" for c in CLASSES]
     report = {
         "what": "bounded least-squares fit of the reference co-run penalties on measured B200 rows "
@@ -220,14 +238,15 @@ def main():
         "rows": len(rows), "rows_cu": sum(r["backend"] == "cu" for r in rows),
         "rows_dma": sum(r["backend"] == "dma" for r in rows),
         "rms_rel_error": rms(res), "rms_rel_error_unit_penalties": rms(res0),
-        "rms_by_strategy": {s: rms([e for e, r in zip(res, rows) if r["strategy"] == s])
-                            for s in SM + DMA if any(r["strategy"] == s for r in rows)},
+        "fitted_strategies": list(FITTED),
+        "rms_by_strategy": {s: rms([e for e, r in zip(res_all, all_rows) if r["strategy"] == s])
+                            for s in SM + DMA if any(r["strategy"] == s for r in all_rows)},
         "penalties": dict(zip(names, [round(float(v), 4) for v in x])),
         "identified": dict(zip(names, ident)),
         "at_bound": [nm for nm, v, i in zip(names, x, ident) if i and (v <= LO + 1e-6 or v >= HI - 1e-6)],
-        "per_row": [{"row": r["id"], "strategy": r["strategy"], "measured_ms": 1e3 * r["measured"],
-                     "predicted_ms": 1e3 * r["measured"] * (1 + e), "rel_error": float(e)}
-                    for r, e in zip(rows, res)],
+        "per_row": [{"row": r["id"], "strategy": r["strategy"], "fitted": r["strategy"] in FITTED,
+                     "measured_ms": 1e3 * r["measured"], "predicted_ms": 1e3 * r["measured"] * (1 + e),
+                     "rel_error": float(e)} for r, e in zip(all_rows, res_all)],
     }
     with open(os.path.join(DATA, "b200-loopback-params.json"), "w") as f:
         json.dump(params, f, indent=2)
