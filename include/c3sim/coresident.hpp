@@ -74,6 +74,19 @@ struct CoResidentParams {
     /// units beside the cfg4 GEMM 10% slower than 16, both collectives done
     /// well before the GEMM (profiles/r02_c3_sweep_link770.csv). 0 = off.
     double cta_cost = 0.0;
+    /// The reduce-scatter pull's CTA factor (n loads and an fp32 sum per
+    /// store: heavier beside the GEMM than the all-to-all push of its kernel
+    /// class); 0 = the all-to-all class factor. Applied by for_kind().
+    double comm_reduce_scatter = 0.0;
+
+    /// These parameters as seen by a collective of `kind`: a reduce-scatter
+    /// uses comm_reduce_scatter as its all-to-all class factor when set.
+    CoResidentParams for_kind(CollectiveKind kind) const {
+        CoResidentParams q = *this;
+        if (kind == CollectiveKind::ReduceScatter && comm_reduce_scatter > 0.0)
+            q.comm_all_to_all = comm_reduce_scatter;
+        return q;
+    }
 
     double gemm(KernelClass gemm_class) const {
         return gemm_class == KernelClass::GemmMemoryBound ? gemm_memory_bound : gemm_compute_bound;
@@ -99,7 +112,8 @@ void validate(const CoResidentParams& p);
 ///        "comm-all-to-all": pc (optional), "rate-exponent": g (optional, default 1),
 ///        "all-gather-by-ranks": bool (optional, default false),
 ///        "comm-memory-bound": pc (optional, 0 = the class factor),
-///        "cta-cost": c (optional, default 0)}.
+///        "cta-cost": c (optional, default 0),
+///        "comm-reduce-scatter": pc (optional, 0 = the all-to-all class factor)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 

@@ -1308,7 +1308,8 @@ double link_rate_gbps(const c3_session* s, double t_comm_cu_ms) {
 double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, double t_comm_cu_ms,
                           double pace_gbps = 0.0) {
     const auto gcls = c3sim::gemm_kernel_class(s->scenario.gemm, c3sim::machine_op_to_byte(s->md));
-    const int eff = c3sim::coresident_comm_ctas(ctas, s->cores,
+    const c3sim::CoResidentParams cores = s->cores.for_kind(s->scenario.collective.kind);
+    const int eff = c3sim::coresident_comm_ctas(ctas, cores,
                                                 c3sim::comm_kernel_class(s->scenario.collective.kind), s->n, gcls);
     double t_at = comm_ms_at(s, eff, t_comm_cu_ms);
     double t_alone = comm_ms_at(s, ctas, t_comm_cu_ms);  // after the GEMM: the same CTAs, alone
@@ -1321,7 +1322,7 @@ double predict_coresident(const c3_session* s, int ctas, double t_gemm_ms, doubl
     // or too few co-resident CTAs both lower its intensity beside the GEMM
     const double ratio = std::min(1.0, t_comm_cu_ms / t_at);
     return c3sim::simulate_coresident(t_gemm_ms * 1e-3, t_at * 1e-3, t_comm_cu_ms * 1e-3, s->md.cus_per_gpu,
-                                      ctas, gcls, s->cores, ratio, t_alone * 1e-3)
+                                      ctas, gcls, cores, ratio, t_alone * 1e-3)
         .makespan;
 }
 

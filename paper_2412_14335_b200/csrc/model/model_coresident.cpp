@@ -57,6 +57,8 @@ void validate(const CoResidentParams& p) {
         throw ValidationError("co-resident memory-bound cost factor must be 0 (= class factor) or >= 1");
     if (!(p.rate_exponent > 0) || !std::isfinite(p.rate_exponent))
         throw ValidationError("co-resident rate exponent must be finite and > 0");
+    if (!(p.comm_reduce_scatter == 0.0 || (p.comm_reduce_scatter >= 1.0 && std::isfinite(p.comm_reduce_scatter))))
+        throw ValidationError("co-resident reduce-scatter cost factor must be 0 (= all-to-all class) or >= 1");
     if (!(p.cta_cost >= 0.0) || !std::isfinite(p.cta_cost))
         throw ValidationError("co-resident CTA cost must be finite and >= 0");
 }
@@ -82,6 +84,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.all_gather_by_ranks = j.value("all-gather-by-ranks", false);
         p.comm_memory_bound = j.value("comm-memory-bound", 0.0);
         p.cta_cost = j.value("cta-cost", 0.0);
+        p.comm_reduce_scatter = j.value("comm-reduce-scatter", 0.0);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -98,6 +101,7 @@ std::string save_coresident_params(const CoResidentParams& p) {
     if (p.all_gather_by_ranks) j["all-gather-by-ranks"] = true;
     if (p.comm_memory_bound > 0.0) j["comm-memory-bound"] = p.comm_memory_bound;
     if (p.cta_cost > 0.0) j["cta-cost"] = p.cta_cost;
+    if (p.comm_reduce_scatter > 0.0) j["comm-reduce-scatter"] = p.comm_reduce_scatter;
     return j.dump(2) + "\n";
 }
 

@@ -233,7 +233,8 @@ void add_sim(py::module_& m) {
     py::class_<CRP>(m, "CoResidentParams")
         .def(py::init<>())
         .RW(CRP, gemm_compute_bound).RW(CRP, gemm_memory_bound).RW(CRP, comm).RW(CRP, comm_all_to_all)
-        .RW(CRP, rate_exponent).RW(CRP, all_gather_by_ranks).RW(CRP, comm_memory_bound).RW(CRP, cta_cost);
+        .RW(CRP, rate_exponent).RW(CRP, all_gather_by_ranks).RW(CRP, comm_memory_bound).RW(CRP, cta_cost)
+        .RW(CRP, comm_reduce_scatter).def("for_kind", &CRP::for_kind);
     m.def("load_coresident_params", &cs::load_coresident_params);
     m.def("save_coresident_params", &cs::save_coresident_params);
     m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),

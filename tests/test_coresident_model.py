@@ -107,14 +107,15 @@ def test_shipped_coresident_params_load():
 def test_calibration_tool_recovers_known_parameters(tmp_path):
     """tools/calibrate_coresident.py on a sweep CSV synthesised with the
     runtime's arithmetic from known (p_g, p_c all-gather, p_c all-to-all,
-    rate exponent) recovers them (grid resolution 0.02 / 0.1 / 0.1 / 0.5)."""
+    rate exponent) recovers them (values on the tool's grid: 0.04 / 0.2 / 0.2
+    / {0.5, 1, 2, 3, 4, 6})."""
     import json
     import subprocess
     sys.path.insert(0, os.path.join(REPO, "tools"))
     import calibrate_coresident as cal
     p = c3sim.CoResidentParams()
     p.gemm_compute_bound = p.gemm_memory_bound = 1.12
-    p.comm, p.comm_all_to_all, p.rate_exponent = 1.5, 2.0, 1.5
+    p.comm, p.comm_all_to_all, p.rate_exponent = 1.6, 2.0, 2.0
     p.all_gather_by_ranks = True  # as the tool fits
     hdr = ("scenario_id,collective,taxonomy,strategy,makespan_s,speedup,ideal,fraction_of_ideal,"
            "t_gemm_iso_ms,t_comm_iso_ms,gemm_tflops_in_step,cus_gemm,cus_comm,backend,world,"
@@ -125,6 +126,8 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
         # a link-bound collective: 1/ctas below 24 CTA units, flat from there
         pts = {c: tc * max(1.0, 24.0 / c) for c in (16, 24, 32, 48, 64)}
         d = {"tg": tg, "tc": tc, "mib": float(sid.rsplit("_", 1)[1].rstrip("M")), "n": 8,
+             "kind": {"all-gather": c3sim.CollectiveKind.ALL_GATHER, "all-to-all": c3sim.CollectiveKind.ALL_TO_ALL,
+                      "reduce-scatter": c3sim.CollectiveKind.REDUCE_SCATTER}[coll],
              "ccls": c3sim.KernelClass.ALL_GATHER if coll == "all-gather" else c3sim.KernelClass.ALL_TO_ALL,
              "curve": c3sim.CommCurve(sorted(pts) + [148], [pts[c] for c in sorted(pts)] + [tc])}
         peer = 7 / 8 * d["mib"] * 2 ** 20
@@ -142,9 +145,11 @@ def test_calibration_tool_recovers_known_parameters(tmp_path):
     assert r.returncode == 0, r.stderr
     got = json.loads(out.read_text())
     assert got["gemm-compute-bound"] == pytest.approx(1.12, abs=0.011)
-    assert got["comm"] == pytest.approx(1.5, abs=0.051)
+    assert got["comm"] == pytest.approx(1.6, abs=0.051)
     assert got["comm-all-to-all"] == pytest.approx(2.0, abs=0.051)
-    assert got["rate-exponent"] == pytest.approx(1.5, abs=0.01)
+    assert got["rate-exponent"] == pytest.approx(2.0, abs=0.01)
+    # the reduce-scatter rows were made with the all-to-all factor
+    assert got.get("comm-reduce-scatter", 2.0) == pytest.approx(2.0, abs=0.21)
     assert got["all-gather-by-ranks"] is True
     assert got["comm-memory-bound"] == 1.0
 
@@ -212,3 +217,46 @@ def test_rate_exponent_roundtrip_and_default(tmp_path):
     assert c3sim.load_coresident_params(str(f)).rate_exponent == 2.75
     f.write_text('{"gemm-compute-bound": 1.1, "gemm-memory-bound": 1.0, "comm": 1.5}')
     assert c3sim.load_coresident_params(str(f)).rate_exponent == 1.0
+
+
+def test_round2_extensions_cta_cost_phase2_and_reduce_scatter_factor(tmp_path):
+    """cta_cost: every resident collective CTA unit slows the GEMM, paced or
+    not; phase 2: once the GEMM is done the collective's CTAs run alone (the
+    curve time, no co-residency factor); comm_reduce_scatter: the pull's own
+    CTA factor, applied through for_kind."""
+    p = c3sim.CoResidentParams()
+    tg, tc = 2.4e-3, 1.0e-3
+    base = c3sim.simulate_coresident(tg, tc, tc, 148, 16, CB, p).makespan
+    p.cta_cost = 0.3
+    m16 = c3sim.simulate_coresident(tg, tc, tc, 148, 16, CB, p).makespan
+    m64 = c3sim.simulate_coresident(tg, tc, tc, 148, 64, CB, p).makespan
+    assert base < m16 < m64
+    # GEMM rate during phase 1: 1 / (1 + 0.3 * c / 148)
+    assert m16 == pytest.approx(tc + tg - tc / (1 + 0.3 * 16 / 148))
+    # C-long: the collective outlives the GEMM; after it, its CTAs run at the
+    # alone-rate, not at the co-resident (derated) one
+    q = c3sim.CoResidentParams()
+    slow = c3sim.simulate_coresident(0.3e-3, 4.0e-3, 2.0e-3, 148, 8, MB, q).makespan
+    fast = c3sim.simulate_coresident(0.3e-3, 4.0e-3, 2.0e-3, 148, 8, MB, q, 1.0, 2.0e-3).makespan
+    assert fast == pytest.approx(0.3e-3 + (2.0e-3 - 0.3e-3 * 2.0e-3 / 4.0e-3) * 2.0e-3 / 2.0e-3)
+    assert fast < slow
+    # the reduce-scatter factor and its JSON round trip
+    q.comm_all_to_all = 2.0
+    q.comm_reduce_scatter = 3.5
+    rs = q.for_kind(c3sim.CollectiveKind.REDUCE_SCATTER)
+    a2a = q.for_kind(c3sim.CollectiveKind.ALL_TO_ALL)
+    assert rs.comm_all_to_all == 3.5 and a2a.comm_all_to_all == 2.0
+    assert c3sim.coresident_comm_ctas(24, rs, c3sim.KernelClass.ALL_TO_ALL) == 7
+    q.cta_cost = 0.1
+    path = tmp_path / "cores.json"
+    path.write_text(c3sim.save_coresident_params(q))
+    back = c3sim.load_coresident_params(str(path))
+    assert back.comm_reduce_scatter == 3.5 and back.cta_cost == pytest.approx(0.1)
+
+
+def test_shipped_coresident_params_are_the_fit():
+    """data/b200-coresident.json: written by tools/calibrate_coresident.py from
+    the r02 NVLink-rate sweeps; physically ordered factors."""
+    p = c3sim.load_coresident_params(c3sim.data_path("b200-coresident.json"))
+    assert 1.0 <= p.gemm_compute_bound <= 3.0 and 1.0 <= p.gemm_memory_bound <= 3.0
+    assert 1.0 <= p.comm <= p.comm_all_to_all <= p.comm_reduce_scatter <= 6.0

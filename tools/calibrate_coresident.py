@@ -48,6 +48,10 @@ def load(paths):
                                       "tc": float(r["t_comm_iso_ms"]) * 1e-3, "pts": {}, "rows": [],
                                       "mib": float(r["scenario_id"].rsplit("_", 1)[1].rstrip("M")),
                                       "n": int(r.get("n_ranks") or N_RANKS),
+                                      "kind": {"all-gather": c3sim.CollectiveKind.ALL_GATHER,
+                                               "all-to-all": c3sim.CollectiveKind.ALL_TO_ALL,
+                                               "reduce-scatter": c3sim.CollectiveKind.REDUCE_SCATTER}[
+                                          r["collective"]],
                                       "ccls": c3sim.KernelClass.ALL_GATHER if r["collective"] == "all-gather"
                                       else c3sim.KernelClass.ALL_TO_ALL})
             c = int(r["cus_comm"])
@@ -69,6 +73,7 @@ def load(paths):
 
 def predict(d, c, pace, cls, p):
     """The runtime's predict_coresident (runtime.cpp) on one row."""
+    p = p.for_kind(d["kind"])
     t_at = d["curve"].time_at(c3sim.coresident_comm_ctas(c, p, d["ccls"], d["n"], cls))
     t_alone = d["curve"].time_at(c)
     peer = (d["n"] - 1) / d["n"] * d["mib"] * 2 ** 20
@@ -166,6 +171,19 @@ def main():
         return (round(max(r), 3) if r else 0.0, e)
     best = min(near, key=worst_regret)
     e_cb, pg_cb, pc_ag, pc_a2a, g, n_cb, cta = best
+    # the reduce-scatter pull's own CTA factor (n loads + a sum per store),
+    # by worst-case pick regret then error over the reduce-scatter scenarios
+    rs = {k: v for k, v in cb.items() if v["kind"] == c3sim.CollectiveKind.REDUCE_SCATTER}
+    pc_rs = 0.0
+    if rs:
+        def rs_score(x):
+            p = params(pg_cb, pc_ag or pc_a2a, g, pc_a2a or pc_ag, cta)
+            p.comm_reduce_scatter = x
+            r = [pick_regret(d, CB, p) for d in rs.values()]
+            r = [v for v in r if v is not None]
+            err = sum(((predict(d, c, pace, CB, p) - mk) / mk) ** 2 for d in rs.values() for c, pace, mk in d["rows"])
+            return (round(max(r), 3) if r else 0.0, err)
+        pc_rs = min([1.0 + 0.2 * i for i in range(16)], key=rs_score)
     pc = pc_ag or pc_a2a
     pc_a2a = pc_a2a or pc
     def mb_error(pg, pcm):
@@ -186,6 +204,7 @@ def main():
     prm.comm_memory_bound = best_mb[2]
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     prm.cta_cost = cta
+    prm.comm_reduce_scatter = pc_rs
     regrets = {}
     for key, d in scen.items():
         r = pick_regret(d, MB if is_mb(key) else CB, prm)
@@ -195,7 +214,7 @@ def main():
     for k, r in sorted(regrets.items()):
         print(f"  pick regret {k}: " + ("n/a (pick not measured)" if r is None else f"{100 * r:.1f}%"))
     print(f"compute-bound: p_g {pg_cb:.2f}, p_c {pc_ag:.2f} (all-gather) / {pc_a2a:.2f} (all-to-all class), "
-          f"rate exponent {g:.2f}, cta cost {cta:.2f}, "
+          f"reduce-scatter {pc_rs:.2f}, rate exponent {g:.2f}, cta cost {cta:.2f}, "
           f"rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows, paced and unpaced)")
     if mb:
         print(f"memory-bound:  p_g {best_mb[1]:.2f}, p_c {best_mb[2]:.2f}, rms rel. error {best_mb[0] ** 0.5:.3f}")

@@ -32,7 +32,7 @@ def main():
             if rnd == 0:
                 r = subprocess.run(
                     ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
-                     "lts__t_bytes.sum", "--clock-control", "none", "-k", "regex:gemm", "-s", "2", "-c", "1",
+                     "lts__t_bytes.sum", "--clock-control", "none", "-k", "regex:gemm", "-s", "1", "-c", "1",
                      sys.executable, os.path.join(REPO, "tools", "ncu_target.py"), "gemm", str(m), str(n), str(k)],
                     env=env, capture_output=True, text=True)
                 for name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
