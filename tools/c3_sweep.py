@@ -62,7 +62,9 @@ def main():
                 jobs[c3.STRATEGY_NAMES[st]] = (st, s.default_alloc(st))
             # comm pacing (B200 extension): the co-resident collective spread
             # over 60% / 80% of the GEMM (rate from a quick GEMM probe)
-            tg0 = statistics.median(s.run(c3.GEMM_ONLY).total_ms for _ in range(3))
+            for _ in range(5):  # warm: the pace is set from the steady GEMM time, as the runtime's choice is
+                s.run(c3.GEMM_ONLY)
+            tg0 = statistics.median(s.run(c3.GEMM_ONLY).total_ms for _ in range(5))
             peer = (8 - 1) / 8 * cfg["payload"]
             for ctas in (8, 16, 24):
                 for frac in (0.6, 0.8):
