@@ -44,6 +44,25 @@ def cores_unit_comm(tmp_path):
     return str(f)
 
 
+def expected_pick(c3, s, sms, t_g, t_c, peer_bytes, link_gbps):
+    """c3_session_choose's co-resident rule: every CTA count of {8..64} and
+    the curve, unpaced and paced to spread the collective over 80% / 60% of
+    the GEMM (when below its unpaced rate); the fewest CTAs with a candidate
+    within 1% of the best prediction, then that count's lowest prediction."""
+    pred = []
+    for c in (8, 16, 24, 32, 48, 64):
+        for frac in (None, 0.8, 0.6):
+            pace = 0.0 if frac is None else peer_bytes / (frac * t_g * 1e6)
+            if frac is not None and not pace < link_gbps:
+                continue
+            x = s.default_alloc(c3.C3_BASE)
+            x.cus_gemm, x.cus_comm, x.comm_pace_gbps = sms, c, pace
+            pred.append((c, pace, s.predict_alloc(c3.C3_BASE, x, t_g, t_c)))
+    best = min(m for _, _, m in pred)
+    c_pick = next(c for c, _, m in pred if m <= best * 1.01)
+    return min(((c, pc, m) for c, pc, m in pred if c == c_pick and m <= best * 1.01), key=lambda x: x[2])
+
+
 def test_choose_picks_coresident_from_the_curve(c3, session, cores_unit_comm):
     import c3sim
     w, s = session
@@ -52,7 +71,11 @@ def test_choose_picks_coresident_from_the_curve(c3, session, cores_unit_comm):
     # link-bound collective: 1.0 ms from 24 CTAs on, slower below
     s.set_comm_curve([(8, 4.0), (16, 2.0), (24, 1.0), (sms, 1.0)])
     st, a, pred = s.choose(3.0, 1.0, 0.0, allow_dma=False)
-    assert st == c3.C3_BASE and a.cus_gemm == sms and a.cus_comm == 24 and a.comm_first == 0
+    peer = 7 * (1 << 20)  # this rank's peer bytes: (n-1) chunks of 1 MiB
+    c_want, pace_want, m_want = expected_pick(c3, s, sms, 3.0, 1.0, peer, peer / (1.0 * 1e6))
+    assert st == c3.C3_BASE and a.cus_gemm == sms and a.comm_first == 0
+    assert a.cus_comm == c_want and a.comm_pace_gbps == pytest.approx(pace_want, rel=1e-5)
+    assert pred == pytest.approx(m_want)
     p = c3sim.load_coresident_params(cores_unit_comm)
     want = c3sim.simulate_coresident(3.0e-3, 1.0e-3, 1.0e-3, sms, 24,
                                      c3sim.KernelClass.GEMM_COMPUTE_BOUND, p).makespan * 1e3
@@ -67,7 +90,7 @@ def test_choose_picks_coresident_from_the_curve(c3, session, cores_unit_comm):
     # a plateau: 32 CTAs a hair faster than 24 -> still the fewest within 1%
     s.set_comm_curve([(8, 4.0), (24, 1.004), (32, 1.0), (sms, 1.0)])
     st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
-    assert st == c3.C3_BASE and a.cus_comm == 24
+    assert st == c3.C3_BASE and a.cus_comm == expected_pick(c3, s, sms, 3.0, 1.0, peer, peer / 1e6)[0]
 
 
 def test_collective_cta_cost_factor_moves_the_pick(c3, session, tmp_path):
@@ -91,12 +114,12 @@ def test_collective_cta_cost_factor_moves_the_pick(c3, session, tmp_path):
         x = s.default_alloc(c3.C3_BASE)
         x.cus_gemm, x.cus_comm = sms, c
         pred[c] = s.predict_alloc(c3.C3_BASE, x, 3.0, 1.0)
-    # only units that carry the collective at its full rate (c / p_c on the
-    # curve's plateau from 24 isolated units); of those the fewest within 1%
-    full_rate = [c for c in cands if round(c / pc) >= 24]
-    best = min(pred[c] for c in full_rate)
-    assert a.cus_comm == next(c for c in full_rate if pred[c] <= best * 1.01)
-    assert a.cus_comm > 24  # the cost factor pushes the pick past the isolated plateau
+    # the cost factor slows few co-resident units: unpaced, the fewest within
+    # 1% of the best now sits past the isolated plateau (24 units)
+    best = min(pred.values())
+    assert next(c for c in cands if pred[c] <= best * 1.01) > 24
+    peer = 7 * (1 << 20)
+    assert a.cus_comm == expected_pick(c3, s, sms, 3.0, 1.0, peer, peer / 1e6)[0]
 
 
 def test_partitioned_allocations_keep_the_reference_model(c3, session):
