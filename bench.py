@@ -412,6 +412,8 @@ def run_ours(args, dist):
             head_alloc = realisable(head, head_alloc)
         co_ctas = head_alloc.cus_comm if head_alloc.cus_gemm + head_alloc.cus_comm > full else max(16, nvl_ctas or 16)
         cands = [(head, head_alloc)] + (emulated_candidates(co_ctas) if emulate else full_speed_candidates())
+        if args.no_green:  # ncu cannot profile kernels on green-context streams
+            cands = [c for c in cands if c[0] not in (c3.C3_RP, c3.C3_SP_RP)] or [(c3.SERIAL, sess.default_alloc(c3.SERIAL))]
         sess.set_link_rate(link)
         meds = []
         best_i, best_ms = sess.autotune(cands, rounds=9, reduce_max=dist.max_list, medians=meds)
@@ -975,8 +977,12 @@ def main():
     ap.add_argument("--no-library-baseline", action="store_true")
     ap.add_argument("--no-nvlink-emulation", action="store_true")
     ap.add_argument("--no-ce-proxy", action="store_true")
+    ap.add_argument("--no-green", action="store_true",
+                    help="no green-context (c3_rp / c3_sp_rp) runs: for ncu, which cannot profile them")
     args = ap.parse_args()
     args.strategies = [s for s in args.strategies.split(",") if s]
+    if args.no_green:
+        args.strategies = [s for s in args.strategies if s not in ("c3_rp", "c3_sp_rp")]
     args.warmup = max(3, args.warmup)
     if int(os.environ.get("WORLD_SIZE", "1")) > 1:
         # NCCL communicator set-up in the log (the library baseline's group):
