@@ -108,9 +108,6 @@ struct Params {
     // bit 1 the epilogue releases the accumulator without draining it (the
     // cost of the exposed TMEM drain)
     int dev;
-    // k-blocks ahead of the shared-memory loads at which the producer pulls
-    // its operand boxes into L2 (0: off): DRAM latency off the smem ring
-    int prefetch;
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -428,38 +425,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int b_row = tn * BN + (half > 0 ? 256 : 0) + static_cast<int>(rank) * 128;
             const int halves = half < 0 ? Cfg::HALVES : 1;
             const uint32_t stage_tx = 2 * (A_STAGE + halves * B_HALF);
-            // L2 prefetch (C3_GEMM_PREFETCH = D k-blocks, dev A/B): each CTA pulls
-            // its own rows of k-block kb + D into L2 as it loads kb; over its
-            // tile's last D k-blocks the leader pulls the first D k-blocks of
-            // the next tile it claimed (all 256 A rows and BN B rows: the
-            // follower does not know that tile yet)
-            int n_arow = -1, n_brow = 0, n_halves = 0;
-            if (p.prefetch > 0 && leader && next < p.num_units) {
-                int ntm, ntn, nt_idx, nhalf;
-                unit_tile(p, next, nt_idx, nhalf);
-                tile_coords(p, nt_idx, ntm, ntn);
-                n_arow = ntm * BM;
-                n_brow = ntn * BN + (nhalf > 0 ? 256 : 0);
-                n_halves = nhalf < 0 ? Cfg::HALVES : 1;
-            }
-            if (p.prefetch > 0 && i == 0)
-                for (int kb = 0; kb < p.prefetch && kb < p.k_blocks; ++kb) {
-                    tma_prefetch_l2_2d(&map_a, kb * BK, a_row);
-                    for (int h = 0; h < halves; ++h) tma_prefetch_l2_2d(&map_b, kb * BK, b_row + h * 256);
-                }
             for (int kb = 0; kb < p.k_blocks; ++kb) {
-                if (p.prefetch > 0) {
-                    const int pk = kb + p.prefetch;
-                    if (pk < p.k_blocks) {
-                        tma_prefetch_l2_2d(&map_a, pk * BK, a_row);
-                        for (int h = 0; h < halves; ++h) tma_prefetch_l2_2d(&map_b, pk * BK, b_row + h * 256);
-                    } else if (n_arow >= 0 && pk - p.k_blocks < p.k_blocks) {
-                        const int nk = (pk - p.k_blocks) * BK;
-                        for (int r2 = 0; r2 < 2; ++r2) tma_prefetch_l2_2d(&map_a, nk, n_arow + r2 * 128);
-                        for (int h = 0; h < n_halves; ++h)
-                            for (int r2 = 0; r2 < 2; ++r2) tma_prefetch_l2_2d(&map_b, nk, n_brow + h * 256 + r2 * 128);
-                    }
-                }
                 mbar_wait(&empty[stage], phase ^ 1);
                 if (leader) mbar_arrive_expect_tx(&full[stage], stage_tx);
                 tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, pol_a);
@@ -823,11 +789,6 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return e ? std::atoi(e) : 0;
     }();
     p.dev = dev;
-    static const int prefetch = [] {
-        const char* e = std::getenv("C3_GEMM_PREFETCH");  // k-blocks of L2 prefetch ahead (dev A/B)
-        return e ? std::max(0, std::atoi(e)) : 0;
-    }();
-    p.prefetch = prefetch;
 
     const bool wide = plan->kind == GemmPlan::kPair512;
     // tail split (512-wide): if the last wave is at most half full, its tiles
