@@ -235,16 +235,23 @@ def run_ours(args, dist):
     iso_modes["cu"][1].cus_comm = full
     col = {"gemm": 1, "cu": 2, "dma": 2}
 
+    import random
+    order_rng = random.Random(20241217)  # same sequence on every rank
+
     def rounds(jobs, n):
         """n round-robin rounds over jobs {name: (strategy, alloc) | callable};
         per-job rows [total, gemm, comm, launches] (device ms, max over ranks)."""
         out = {k: [] for k in jobs}
         names = list(jobs)
         for r in range(n):
-            # rotate the order each round: under the 1 kW power cap a job's
-            # clocks depend on its predecessor, so no job may always follow
-            # the same one (measured: a fixed order skewed isolated GEMM times)
-            for name in names[r % len(names):] + names[:r % len(names)]:
+            # a fresh order every round: under the 1 kW power cap a job's
+            # clocks depend on its predecessor (measured: a fixed order skewed
+            # isolated GEMM times by 10%). A cyclic rotation still gives every
+            # job the same predecessor within a round, so the order is a
+            # seeded permutation, identical on every rank
+            order = list(names)
+            order_rng.shuffle(order)
+            for name in order:
                 job = jobs[name]
                 out[name] += [job()] if callable(job) else timed(*job[:1], 1, *job[1:])
         return out
@@ -567,8 +574,10 @@ def run_ours(args, dist):
             e2e_step(*job)
     e2e = {k: [] for k in e2e_jobs}
     names = list(e2e_jobs)
-    for r in range(K):  # interleaved, rotated order
-        for k in names[r % 3:] + names[:r % 3]:
+    for r in range(K):  # interleaved, a fresh seeded order per round
+        order = list(names)
+        order_rng.shuffle(order)
+        for k in order:
             e2e[k].append(e2e_step(*e2e_jobs[k]))
     e2e_ms = {k: median(dist.max_list(v)) for k, v in e2e.items()}
     e2e_speedup = e2e_ms["serial"] / e2e_ms["conc"]
@@ -623,7 +632,7 @@ def run_ours(args, dist):
     else:
         world_desc = f"{n} GPUs, CUDA-IPC peer memory"
     # per-round paired speedups: each round's C3 step against the isolated
-    # GEMM and collective of the SAME round (rotated order, so each step is
+    # GEMM and collective of the SAME round (seeded per-round order, so each step is
     # bracketed by isolated runs under the same power state), and the spread
     # of the headline over three blocks of rounds
     g_rows, c_rows = timed_rows["gemm"], timed_rows[comm_key]
@@ -665,8 +674,9 @@ def run_ours(args, dist):
                                     "full_speed_sweep_gemm": t_g, "full_speed_sweep_comm_cu": iso_comm["cu"],
                                     "full_speed_sweep_comm_dma": iso_comm["dma"]},
                     "protocol": ("W warm-up, then K rounds of [isolated GEMM, isolated collective, "
-                                 "C3 step] in rotated order; medians; then, outside the timed region, "
-                                 "K rounds of the full-speed pair and the library baseline"),
+                                 "C3 step], each round in a fresh seeded order; medians; then, outside "
+                                 "the timed region, >= 15 such rounds of the full-speed pair and the "
+                                 "library baseline"),
                     "timed_region_wall_s": wall},
         "conccl_ce_proxy": ce_proxy,
         "loopback_full_speed": full_speed,
@@ -714,7 +724,7 @@ def run_ours(args, dist):
             "paired_ratio_min_max": [min(paired), max(paired)], "rounds": len(paired),
             "ratio_of_medians": tb_l / ours_full,
             "compared_with": "loopback_full_speed" if full_speed else "headline",
-            "note": "both concurrent steps in the same rotated comparison rounds (after the timed region)"}
+            "note": "both concurrent steps in the same comparison rounds, fresh seeded order per round (after the timed region)"}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(quick=True)
     sess.close()
@@ -756,8 +766,12 @@ def run_ce_proxy(c3, cfg, n, coll, elem, K, W, link_gbps):
             "conccl_rp": (c3.CONCCL_RP, s.default_alloc(c3.CONCCL_RP))}
     t = {j: [] for j in jobs}
     names = list(jobs)
+    import random
+    rng = random.Random(20241217)
     for r in range(W + K):
-        for j in names[r % len(names):] + names[:r % len(names)]:
+        order = list(names)
+        rng.shuffle(order)
+        for j in order:
             tm = s.run(*jobs[j])
             if r >= W:
                 t[j].append(tm)
