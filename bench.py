@@ -598,6 +598,12 @@ def run_ours(args, dist):
     # the GEMM's roofline: tensor-bound when its arithmetic intensity exceeds
     # the machine's FLOP:byte ratio, else HBM-bound (cfg4_mb, M = 128)
     gemm_bytes = float(elem) * (cfg["m"] * cfg["k"] + cfg["n"] * cfg["k"] + cfg["m"] * cfg["n"])
+    # this GPU's collective HBM bytes per step: AG reads its chunk and takes
+    # n-1 incoming chunks; A2A reads n-1 outgoing slots and takes n-1 incoming;
+    # RS: its n input slots are read (one by each rank) and its slot written
+    chunk_b = cfg["payload"] / n
+    comm_hbm_bytes = {"all-gather": n * chunk_b, "all-to-all": 2 * (n - 1) * chunk_b,
+                      "reduce-scatter": (n + 1) * chunk_b}[cfg["coll"]]
     # TF32 (fp32 GEMM) runs at half the bf16 dense rate
     tc_peak = peaks["bf16_tflops"] / (2.0 if elem == 4 else 1.0)
     ratio = tc_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
@@ -619,7 +625,12 @@ def run_ours(args, dist):
                     "frac": gbs / peaks["hbm_gbs"],
                     "peak_source": peak_src + " HBM copy bandwidth",
                     "algorithmic_bytes_per_launch": gemm_bytes, "traffic": traffic,
-                    "arithmetic_intensity": flops / gemm_bytes, "machine_flop_per_byte": ratio}
+                    "arithmetic_intensity": flops / gemm_bytes, "machine_flop_per_byte": ratio,
+                    # the same GEMM alone in the timed rounds: inside the step the
+                    # co-resident collective draws HBM too (its own bytes below)
+                    "frac_isolated": gemm_bytes / (t_g_timed * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                    "collective_hbm_bytes_per_step": comm_hbm_bytes,
+                    "step_hbm_frac": (gemm_bytes + comm_hbm_bytes) / (t_conc * 1e-3) / 1e9 / peaks["hbm_gbs"]}
     if emulate:
         world_desc = (f"loopback with NVLink-rate emulation: 8-rank scenario on 1 GPU; this GPU's GEMM "
                       f"and its share of the collective (7 chunk copies into stand-in peer buffers in "
