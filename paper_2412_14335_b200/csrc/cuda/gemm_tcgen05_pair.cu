@@ -108,6 +108,9 @@ struct Params {
     // bit 1 the epilogue releases the accumulator without draining it (the
     // cost of the exposed TMEM drain)
     int dev;
+    // suspend-time hint (ns) of the epilogue's wait for a finished accumulator
+    // (a whole tile's mainloop): 0 = plain try_wait loop
+    uint32_t epi_sleep_ns;
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -584,7 +587,10 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             tile_coords(p, t_idx, tm, tn);
             const int cols = half < 0 ? COLS : 256;  // a half tile fills accumulator columns 0-255
             const int col_base = tn * BN + (half > 0 ? 256 : 0);
-            mbar_wait(&acc_full[acc], acc_phase);
+            if (p.epi_sleep_ns)
+                mbar_wait_sleep(&acc_full[acc], acc_phase, p.epi_sleep_ns);
+            else
+                mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
             if (p.dev & 2) {  // dev: release without draining
                 __syncwarp();
@@ -789,6 +795,11 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return e ? std::atoi(e) : 0;
     }();
     p.dev = dev;
+    static const uint32_t epi_sleep = [] {
+        const char* e = std::getenv("C3_GEMM_EPI_SLEEP");  // dev A/B
+        return e ? static_cast<uint32_t>(std::max(0, std::atoi(e))) : 0u;
+    }();
+    p.epi_sleep_ns = epi_sleep;
 
     const bool wide = plan->kind == GemmPlan::kPair512;
     // tail split (512-wide): if the last wave is at most half full, its tiles

@@ -47,6 +47,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
+// The same wait for long waits (an epilogue waiting out a whole tile's
+// mainloop): try_wait with a suspend-time hint, so the waiting warp sleeps in
+// the barrier unit instead of re-issuing the probe; hint_ns = 0 = mbar_wait.
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+    asm volatile(
+        "{\n\t.reg .pred P;\n"
+        "WAITS_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
+        "@!P bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity), "r"(hint_ns)
+        : "memory");
+}
+
 // ------------------------------------------------------------------ TMA ---
 
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {

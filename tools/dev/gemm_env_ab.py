@@ -32,15 +32,16 @@ def main():
             if rnd == 0:
                 r = subprocess.run(
                     ["ncu", "--metrics", "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum,"
-                     "lts__t_bytes.sum", "--clock-control", "none", "-k", "regex:gemm", "-s", "1", "-c", "1",
+                     "lts__t_bytes.sum,smsp__inst_executed.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed", "--clock-control", "none", "-k", "regex:gemm", "-s", "1", "-c", "1",
                      sys.executable, os.path.join(REPO, "tools", "ncu_target.py"), "gemm", str(m), str(n), str(k)],
                     env=env, capture_output=True, text=True)
                 for name in ("dram__bytes_read.sum", "dram__bytes_write.sum", "gpu__time_duration.sum",
-                             "lts__t_bytes.sum"):
+                             "lts__t_bytes.sum", "smsp__inst_executed.sum",
+                             "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed"):
                     mm = re.search(re.escape(name) + r"\s+(\S+)\s+([\d.,]+)", r.stdout)
                     if mm:
                         unit, val = mm.group(1), float(mm.group(2).replace(",", ""))
-                        scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
+                        scale = {"inst": 1, "%": 1, "byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12,
                                  "ns": 1e-6, "us": 1e-3, "ms": 1.0, "msecond": 1.0, "usecond": 1e-3}.get(unit, 1)
                         row[name] = val * scale
             code = CHILD.format(repo=REPO, m=m, n=n, k=k, cublas=False)
