@@ -47,17 +47,34 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// The same wait for long waits (an epilogue waiting out a whole tile's
-// mainloop): try_wait with a suspend-time hint, so the waiting warp sleeps in
-// the barrier unit instead of re-issuing the probe; hint_ns = 0 = mbar_wait.
-__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity, uint32_t hint_ns) {
+// One probe of an mbarrier phase (no loop): true once the phase completed.
+__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
+    uint32_t ok;
     asm volatile(
-        "{\n\t.reg .pred P;\n"
-        "WAITS_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%0], %1, %2;\n\t"
-        "@!P bra WAITS_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity), "r"(hint_ns)
+        "{\n\t.reg .pred P;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, P;\n}"
+        : "=r"(ok)
+        : "r"(smem_u32(bar)), "r"(parity)
         : "memory");
+    return ok != 0;
+}
+
+// The same wait with exponential nanosleep backoff between probes (32 ns
+// doubling up to max_ns): for waits that last a whole tile (the epilogue) or
+// many k-blocks (the producer on a full ring), where a hot try_wait loop
+// re-issues the probe tens of millions of times per launch (profiles: 60% of
+// the pair GEMM's instructions). max_ns = 0 = mbar_wait.
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t max_ns) {
+    if (max_ns == 0) {
+        mbar_wait(bar, parity);
+        return;
+    }
+    uint32_t ns = 32;
+    while (!mbar_try(bar, parity)) {
+        __nanosleep(ns);
+        ns = ns * 2 < max_ns ? ns * 2 : max_ns;
+    }
 }
 
 // ------------------------------------------------------------------ TMA ---
