@@ -108,10 +108,6 @@ struct Params {
     // bit 1 the epilogue releases the accumulator without draining it (the
     // cost of the exposed TMEM drain)
     int dev;
-    // nanosleep backoff caps (ns) of the epilogue's wait for a finished
-    // accumulator (a whole tile's mainloop) and of the producer's wait for a
-    // free stage; 0 = a plain try_wait loop
-    uint32_t epi_sleep_ns, prod_sleep_ns;
     FusedComm fc;  // only read by the FUSED instantiation
 };
 
@@ -430,7 +426,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int halves = half < 0 ? Cfg::HALVES : 1;
             const uint32_t stage_tx = 2 * (A_STAGE + halves * B_HALF);
             for (int kb = 0; kb < p.k_blocks; ++kb) {
-                mbar_wait_backoff(&empty[stage], phase ^ 1, p.prod_sleep_ns);
+                mbar_wait(&empty[stage], phase ^ 1);
                 if (leader) mbar_arrive_expect_tx(&full[stage], stage_tx);
                 tma_load_2d_pair(smem_a + stage * A_STAGE, &map_a, &full[stage], kb * BK, a_row, pol_a);
                 for (int h = 0; h < halves; ++h)
@@ -588,7 +584,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             tile_coords(p, t_idx, tm, tn);
             const int cols = half < 0 ? COLS : 256;  // a half tile fills accumulator columns 0-255
             const int col_base = tn * BN + (half > 0 ? 256 : 0);
-            mbar_wait_backoff(&acc_full[acc], acc_phase, p.epi_sleep_ns);
+            mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
             if (p.dev & 2) {  // dev: release without draining
                 __syncwarp();
@@ -793,16 +789,6 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return e ? std::atoi(e) : 0;
     }();
     p.dev = dev;
-    static const uint32_t epi_sleep = [] {
-        const char* e = std::getenv("C3_GEMM_EPI_SLEEP");  // dev A/B
-        return e ? static_cast<uint32_t>(std::max(0, std::atoi(e))) : 0u;
-    }();
-    p.epi_sleep_ns = epi_sleep;
-    static const uint32_t prod_sleep = [] {
-        const char* e = std::getenv("C3_GEMM_PROD_SLEEP");  // dev A/B
-        return e ? static_cast<uint32_t>(std::max(0, std::atoi(e))) : 0u;
-    }();
-    p.prod_sleep_ns = prod_sleep;
 
     const bool wide = plan->kind == GemmPlan::kPair512;
     // tail split (512-wide): if the last wave is at most half full, its tiles

@@ -47,36 +47,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         : "memory");
 }
 
-// One probe of an mbarrier phase (no loop): true once the phase completed.
-__device__ __forceinline__ bool mbar_try(uint64_t* bar, uint32_t parity) {
-    uint32_t ok;
-    asm volatile(
-        "{\n\t.reg .pred P;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, P;\n}"
-        : "=r"(ok)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
-    return ok != 0;
-}
-
-// The same wait with exponential nanosleep backoff between probes (32 ns
-// doubling up to max_ns): for waits that last a whole tile (the epilogue) or
-// many k-blocks (the producer on a full ring), where a hot try_wait loop
-// re-issues the probe tens of millions of times per launch (profiles: 60% of
-// the pair GEMM's instructions). max_ns = 0 = mbar_wait.
-__device__ __forceinline__ void mbar_wait_backoff(uint64_t* bar, uint32_t parity, uint32_t max_ns) {
-    if (max_ns == 0) {
-        mbar_wait(bar, parity);
-        return;
-    }
-    uint32_t ns = 32;
-    while (!mbar_try(bar, parity)) {
-        __nanosleep(ns);
-        ns = ns * 2 < max_ns ? ns * 2 : max_ns;
-    }
-}
-
 // ------------------------------------------------------------------ TMA ---
 
 __device__ __forceinline__ void tma_prefetch_desc(const CUtensorMap* map) {
