@@ -48,7 +48,7 @@ MIB = 1 << 20
 CONFIGS = {
     "cfg1": dict(desc="configs[0] on the GPU: fp32 GEMM 1024x1024x1024 (TF32 tensor cores, fp32 "
                       "accumulate and output) || 16 MiB all-gather", m=1024, n=1024, k=1024,
-                 coll="all-gather", payload=16 * MIB, dtype_bytes=4),
+                 coll="all-gather", payload=16 * MIB, dtype_bytes=4, ranks=2),
     "cfg2": dict(desc="LLaMA-70B FSDP layer: FFN up-proj GEMM 8192x28672x8192 bf16 || "
                       "next-layer weight all-gather 896 MiB (gate+up) across 8 GPUs",
                  m=8192, n=28672, k=8192, coll="all-gather", payload=896 * MIB),
@@ -75,7 +75,7 @@ def bench_config(args, world):
     """The workload both arms (ours and --impl reference) run, identical
     between them: static facts only (run-time choices go to `details`)."""
     cfg = CONFIGS[args.config]
-    n = 8 if world == 1 else world
+    n = cfg.get("ranks", 8) if world == 1 else world
     return {"workload": f"{args.config}: {cfg['desc']}", "gemm_mnk": [cfg["m"], cfg["n"], cfg["k"]],
             "gemm_dtype": "fp32" if cfg.get("dtype_bytes", 2) == 4 else "bf16",
             "collective": cfg["coll"], "payload_bytes": cfg["payload"], "ranks": n,
@@ -182,7 +182,7 @@ def run_ours(args, dist):
     import paper_2412_14335_b200 as c3
 
     cfg = CONFIGS[args.config]
-    n = 8 if dist.world == 1 else dist.world
+    n = cfg.get("ranks", 8) if dist.world == 1 else dist.world
     loopback = dist.world == 1
     # C3_SHARED_DEVICE=1: every rank on device 0 (exercises the multi-process
     # IPC path on a one-GPU box; not a performance configuration)
@@ -526,7 +526,7 @@ def run_ours(args, dist):
         fs_c = median([r[2] for r in cmp_rows["fs_comm"]])
         fs_res = summarise(cmp_rows["fs_step"], median([r[1] for r in cmp_rows["gemm"]]), fs_c, fs_c)
         fs_res.update({"strategy": c3.STRATEGY_NAMES[fs[0]], "alloc": alloc_dict(fs[1]),
-                       "what": "loopback at full local speed: the collective's 7 chunk copies run on "
+                       "what": f"loopback at full local speed: the collective's {n - 1} chunk copies run on "
                                "local HBM with the whole GPU (~5x faster than NVLink), same timed rounds"})
         full_speed = fs_res
 
@@ -632,14 +632,14 @@ def run_ours(args, dist):
                     "collective_hbm_bytes_per_step": comm_hbm_bytes,
                     "step_hbm_frac": (gemm_bytes + comm_hbm_bytes) / (t_conc * 1e-3) / 1e9 / peaks["hbm_gbs"]}
     if emulate:
-        world_desc = (f"loopback with NVLink-rate emulation: 8-rank scenario on 1 GPU; this GPU's GEMM "
-                      f"and its share of the collective (7 chunk copies into stand-in peer buffers in "
+        world_desc = (f"loopback with NVLink-rate emulation: {n}-rank scenario on 1 GPU; this GPU's GEMM "
+                      f"and its share of the collective ({n - 1} chunk copies into stand-in peer buffers in "
                       f"local HBM), the collective's peer traffic paced on the global timer to "
                       f"{NVLINK_PEER_GBPS:.0f} GB/s per direction (c3_session_set_link_rate), i.e. "
                       f"(n-1)/n*P/{NVLINK_PEER_GBPS:.0f} GB/s = {nvl_target:.3f} ms, on {nvl_ctas} CTAs "
                       f"(fewest that reach the rate); full-speed loopback in `loopback_full_speed`")
     elif loopback:
-        world_desc = "loopback: 8-rank collective emulated on 1 GPU (peer buffers in local HBM, no NVLink)"
+        world_desc = f"loopback: {n}-rank collective emulated on 1 GPU (peer buffers in local HBM, no NVLink)"
     else:
         world_desc = f"{n} GPUs, CUDA-IPC peer memory"
     # per-round paired speedups: each round's C3 step against the isolated
@@ -850,7 +850,7 @@ class LibraryBaseline:
         self.A = torch.randn(cfg["m"], cfg["k"], device=dev, dtype=torch.bfloat16)
         self.B = torch.randn(cfg["n"], cfg["k"], device=dev, dtype=torch.bfloat16)
         self.C = torch.empty(cfg["m"], cfg["n"], device=dev, dtype=torch.bfloat16)
-        n = 8 if loopback else dist.world
+        n = cfg.get("ranks", 8) if loopback else dist.world
         chunk = cfg["payload"] // n
         self.s_g, self.s_c = torch.cuda.Stream(), torch.cuda.Stream()
         self.ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
@@ -861,7 +861,7 @@ class LibraryBaseline:
             def comm():
                 for p in range(1, n):
                     dst[p * chunk:(p + 1) * chunk].copy_(src)
-            self.label = ("cuBLAS (torch.matmul) || torch device copies of 7 chunks "
+            self.label = (f"cuBLAS (torch.matmul) || torch device copies of {n - 1} chunks "
                           "(loopback; SM copy kernels)")
         else:
             import torch.distributed as tdist
@@ -956,7 +956,7 @@ def run_reference(args, dist):
     adds the local fp32 reduce). Exactly `warmup` + `steps` iterations run;
     rank 0 only (the other ranks exit without work)."""
     cfg = CONFIGS[args.config]
-    n = 8 if dist.world == 1 else dist.world
+    n = cfg.get("ranks", 8) if dist.world == 1 else dist.world
     scale = max(1, cfg["m"] // REF_TOKENS)
     m = cfg["m"] // scale
     payload = cfg["payload"] // scale
