@@ -105,7 +105,7 @@ def pick_regret(d, cls, p):
         return None
     peer = (d["n"] - 1) / d["n"] * d["mib"] * 2 ** 20
     link = peer / d["tc"] / 1e9
-    cands = sorted(set([8, 16, 24, 32, 48, 64]) | {c for c in d["pts"]})
+    cands = [c for c in sorted(set([8, 16, 24, 32, 48, 64]) | {c for c in d["pts"]}) if c >= min(d["pts"])]
     pred = []
     for c in cands:
         pred.append((c, 0.0, predict(d, c, 0.0, cls, p)))
@@ -163,10 +163,13 @@ def main():
     fits.sort()
     near = [f for f in fits if f[0] <= 1.5 ** 2 * fits[0][0]]
 
+    # picks are scored on the BASELINE scenarios (tools/c3_sweep.py rows,
+    # scenario ids "cfg*"); other inputs (e.g. tools/size_sweep.py at world 2
+    # / 4) constrain the fit through the error only
     def worst_regret(f):
         e, pg, pc_ag, pc_a2a, g, n, cta = f
         p = params(pg, pc_ag, g, pc_a2a, cta)
-        r = [pick_regret(d, CB, p) for d in cb.values()]
+        r = [pick_regret(d, CB, p) for k, d in cb.items() if k[1].startswith("cfg")]
         r = [x for x in r if x is not None]
         return (round(max(r), 3) if r else 0.0, e)
     best = min(near, key=worst_regret)
