@@ -1474,10 +1474,10 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
             };
             std::vector<Cand> pred;
             double best_co = 1e300;
-            // no counts below the comm curve's first measured point: its time
-            // there is an extrapolation, and too few co-resident CTAs fall
+            // no counts below 16 unless the comm curve measured them: the curve's
+            // time there is an extrapolation, and too few co-resident CTAs fall
             // behind even a paced collective's rate (size sweep, world 2)
-            const int min_c = s->comm_curve.empty() ? 1 : s->comm_curve.ctas.front();
+            const int min_c = s->comm_curve.empty() ? 1 : std::min(16, s->comm_curve.ctas.front());
             for (int c : cands) {
                 if (c < min_c || c >= s->md.cus_per_gpu) continue;
                 pred.push_back({c, 0.0, predict_coresident(s, c, t_gemm_ms, t_comm_cu_ms)});

@@ -105,7 +105,7 @@ def pick_regret(d, cls, p):
         return None
     peer = (d["n"] - 1) / d["n"] * d["mib"] * 2 ** 20
     link = peer / d["tc"] / 1e9
-    cands = [c for c in sorted(set([8, 16, 24, 32, 48, 64]) | {c for c in d["pts"]}) if c >= min(d["pts"])]
+    cands = [c for c in sorted(set([8, 16, 24, 32, 48, 64]) | {c for c in d["pts"]}) if c >= min(16, min(d["pts"]))]
     pred = []
     for c in cands:
         pred.append((c, 0.0, predict(d, c, 0.0, cls, p)))
