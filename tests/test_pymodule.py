@@ -230,3 +230,33 @@ def test_b200_machine_files_validate(n):
     with open(os.path.join(REPO, "data", "b200-ce-overheads.json")) as f:
         ce = json.load(f)
     assert md.cpu_launch_overhead == pytest.approx(ce["cpu_launch_overhead"], rel=1e-2)
+
+
+def test_bounded_penalty_fit_is_physical(tmp_path):
+    """tools/calibrate_penalties.py on the committed round-2 rows: every
+    penalty in [1, 3], CU >= DMA per kernel class, the fitted rows' RMS under
+    10%, and its output reloads as reference-format params."""
+    import shutil
+    root = tmp_path / "repo"
+    for d in ("tools", "data", "profiles"):
+        (root / d).mkdir(parents=True)
+    shutil.copy(os.path.join(REPO, "tools", "calibrate_penalties.py"), root / "tools")
+    shutil.copy(os.path.join(REPO, "bench.py"), root)
+    for f in ("b200-node-n8.json", "b200-loopback-slowdown-tables.csv"):
+        shutil.copy(os.path.join(REPO, "data", f), root / "data")
+    for f in ("r02_c3_sweep_link770.csv", "r02_ce_proxy_sweep.csv"):
+        shutil.copy(os.path.join(REPO, "profiles", f), root / "profiles")
+    os.symlink(os.path.join(REPO, "paper_2412_14335_b200"), root / "paper_2412_14335_b200")
+    r = subprocess.run([sys.executable, str(root / "tools" / "calibrate_penalties.py"),
+                        str(root / "profiles" / "r02_c3_sweep_link770.csv"),
+                        str(root / "profiles" / "r02_ce_proxy_sweep.csv")],
+                       capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    rep = json.loads((root / "data" / "b200-loopback-params.fit.json").read_text())
+    pen = rep["penalties"]
+    assert all(1.0 <= v <= 3.0 for v in pen.values()), pen
+    for cls in ("gemm-compute-bound", "gemm-memory-bound", "all-gather", "all-to-all"):
+        assert pen[f"{cls}.cu"] >= pen[f"{cls}.dma"] - 1e-9
+    assert rep["rms_rel_error"] < 0.10 and rep["rows_dma"] > 0
+    rp = c3sim.load_params_file(str(root / "data" / "b200-loopback-params.json"))
+    assert rp.freeze_phase2_allocation
