@@ -737,7 +737,7 @@ def run_ours(args, dist):
             "compared_with": "loopback_full_speed" if full_speed else "headline",
             "note": "both concurrent steps in the same comparison rounds, fresh seeded order per round (after the timed region)"}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(quick=True)
+        out["cpu_baseline"] = cpu_baseline(cfg, n)
     sess.close()
     world.close()
     return out
@@ -930,16 +930,31 @@ def ref_cpu_c3(m, n, k, ranks, payload, warmup, iters, kind="all-gather"):
     return json.loads(r.stdout)
 
 
-def cpu_baseline(quick=True):
-    """configs[0] on the host cores: fp32 GEMM 1024^3 || 16 MiB all-gather at
-    world 2 (the reference planner's transfers, memcpy replay)."""
-    res = ref_cpu_c3(1024, 1024, 1024, 2, 16 * MIB, 2 if quick else 6, 3 if quick else 9)
+def ref_sample(cfg, n):
+    """The bounded CPU sample of a config: M cut to REF_TOKENS rows and the
+    payload by the same factor -> (m, payload, scale)."""
+    scale = max(1, cfg["m"] // REF_TOKENS)
+    m = cfg["m"] // scale
+    payload = cfg["payload"] // scale
+    payload -= payload % (8 * n)
+    return m, payload, scale
+
+
+def cpu_baseline(cfg, n, warmup=1, iters=9):
+    """The reference's CPU path timed on this box's host cores, on a bounded
+    sample of the SAME workload as the GPU line (about 10-30 s of CPU work):
+    fp32 GEMM of REF_TOKENS rows on all host threads || the reference
+    planner's transfers for the config's collective replayed by memcpy on one
+    more thread (oracle/_ref driving the oracle/c3oracle.c restatement)."""
+    m, payload, scale = ref_sample(cfg, n)
+    res = ref_cpu_c3(m, cfg["n"], cfg["k"], n, payload, warmup, iters, cfg["coll"])
     return {"value": res["speedup"], "unit": UNIT,
             "cores": res["threads"], "kind": "port",
             "fraction_of_ideal_pct": 100 * res["fraction_of_ideal"],
-            "sample": ("configs[0]: fp32 GEMM 1024x1024x1024 on all host threads || 16 MiB "
-                       "all-gather (reference plan_all_gather, world 2) replayed by memcpy on one "
-                       "thread; oracle/c3oracle.c restatement driven by oracle/_ref; medians"),
+            "sample": (f"1/{scale} of the workload's tokens and payload: fp32 GEMM {m}x{cfg['n']}x{cfg['k']} "
+                       f"on all {res['threads']} host threads || {cfg['coll']} of {payload / MIB:.1f} MiB over {n} "
+                       f"host ranks (reference planner's transfers by memcpy on one thread); {warmup} warm-up + "
+                       f"{iters} iterations, medians"),
             "t_gemm_ms": 1e3 * res["t_gemm_s"], "t_comm_ms": 1e3 * res["t_comm_s"],
             "t_concurrent_ms": 1e3 * res["t_concurrent_s"]}
 
@@ -957,10 +972,7 @@ def run_reference(args, dist):
     rank 0 only (the other ranks exit without work)."""
     cfg = CONFIGS[args.config]
     n = cfg.get("ranks", 8) if dist.world == 1 else dist.world
-    scale = max(1, cfg["m"] // REF_TOKENS)
-    m = cfg["m"] // scale
-    payload = cfg["payload"] // scale
-    payload -= payload % (8 * n)
+    m, payload, scale = ref_sample(cfg, n)
     t0 = time.perf_counter()
     res = ref_cpu_c3(m, cfg["n"], cfg["k"], n, payload, args.warmup, args.steps, cfg["coll"])
     wall = time.perf_counter() - t0
