@@ -182,8 +182,14 @@ int c3_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, v
  * Executes c3sim::GemmKernel (workload.hpp:18-25) whose cost
  * roofline_gemm_time (workload.hpp:62-63) models; max_ctas caps the
  * persistent grid = the GEMM's SM allocation (Allocation::cus_gemm). */
-/* fp32 A, B, C on the TF32 tensor cores (tcgen05.mma kind::tf32, fp32
- * accumulate): operands are read with a 10-bit mantissa. K, N multiples of 4. */
+/* fp32 A, B, C on the TF32 tensor cores, split-TF32: each operand is split
+ * into two TF32 numbers, x ~ hi + lo (hi rounds x, lo rounds the remainder),
+ * and tcgen05.mma kind::tf32 accumulates A_lo B_hi + A_hi B_lo + A_hi B_hi in
+ * fp32. Operand error below 2^-20 |a b| per product (plain TF32: 2^-11);
+ * measured GEMM error 2^-22 RMS of sum |a||b| against 2^-17 for plain TF32
+ * (the rest is the tensor core's fp32 accumulation). Two kernels on `stream`:
+ * the split pass, then the GEMM; the split scratch (2 (m + n) k floats) is
+ * stream-ordered (cudaMallocAsync). K, N multiples of 4. */
 int c3_gemm_f32(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
                 int max_ctas, void* stream);
 int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,

@@ -106,7 +106,9 @@ struct Params {
     // dev A/B only (C3_GEMM_DEV, results invalid when set): bit 0 every tile
     // loads the operands of tile (0, 0) (L2-resident: the cost of DRAM traffic),
     // bit 1 the epilogue releases the accumulator without draining it (the
-    // cost of the exposed TMEM drain)
+    // cost of the exposed TMEM drain), bit 2 / bit 3 (512-wide) it releases
+    // half 0 / both halves as soon as the tile is done and drains after (the
+    // gain a hidden drain would bring, with the drain's own work kept)
     int dev;
     FusedComm fc;  // only read by the FUSED instantiation
 };
@@ -586,6 +588,23 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             const int col_base = tn * BN + (half > 0 ? 256 : 0);
             mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
+            // dev bits 2 / 3 (BN 512): release half 0 / both halves before the
+            // drain (the drain still runs): the time a hidden drain would save
+            int early = 0;
+            if constexpr (Cfg::HALVES == 2) {
+                if (half < 0 && (p.dev & 12)) {
+                    early = (p.dev & 8) ? 3 : 1;
+                    __syncwarp();
+                    if (lane == 0)
+                        for (int h = 0; h < 2; ++h)
+                            if (early >> h & 1) {
+                                if (leader)
+                                    mbar_arrive(&acc_empty[h]);
+                                else
+                                    mbar_arrive_cluster(mapa(smem_u32(&acc_empty[h]), 0));
+                            }
+                }
+            }
             if (p.dev & 2) {  // dev: release without draining
                 __syncwarp();
                 if (lane == 0)
@@ -652,7 +671,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 stage_store(va0, va1, c);
                 tmem_ld_wait();  // chunk c + 64
                 if constexpr (Cfg::HALVES == 2) {
-                    if (c + 64 == 192) {  // columns 0-255 read: release half 0
+                    if (c + 64 == 192 && !(early & 1)) {  // columns 0-255 read: release half 0
                         tc_fence_before();
                         __syncwarp();
                         if (lane == 0) {
@@ -671,7 +690,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                     tc_fence_before();
                     __syncwarp();
                     const int rel = Cfg::HALVES == 2 ? 1 : acc;  // the last half / this accumulator
-                    if (lane == 0) {
+                    if (lane == 0 && !(early & 2)) {
                         if (leader)
                             mbar_arrive(&acc_empty[rel]);
                         else

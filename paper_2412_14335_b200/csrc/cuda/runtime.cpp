@@ -358,6 +358,7 @@ struct c3_session {
     GemmPlan gemm;
     int* gemm_counters = nullptr;
     void *a = nullptr, *b = nullptr, *c = nullptr;
+    float* split = nullptr;  // fp32 sessions: split-TF32 parts of A and B (gemm_split_bytes)
     // per virtual rank: AG recv (payload, own chunk in place); RS in (payload),
     // out (chunk), staging (payload)
     std::vector<void*> recv, in, out, staging;
@@ -422,8 +423,9 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaMalloc(&s->c, static_cast<size_t>(d.m * d.n * s->elem)));
     C3_CUDA(cudaMalloc(&s->gemm_counters, 2 * sizeof(int)));
     C3_CUDA(cudaMemset(s->gemm_counters, 0, 2 * sizeof(int)));
+    if (s->elem == 4) C3_CUDA(cudaMalloc(&s->split, static_cast<size_t>(gemm_split_bytes(d.m, d.n, d.k))));
     C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k, s->gemm_counters,
-                          s->w->prop.multiProcessorCount, s->elem));
+                          s->w->prop.multiProcessorCount, s->elem, s->split));
     const size_t payload = static_cast<size_t>(d.payload_bytes);
     for (int v = 0; v < s->vr; ++v) {
         void* p = nullptr;
@@ -852,9 +854,17 @@ static int world_gemm(c3_world* w, const void* A, const void* B, void* C, int64_
     GemmPlan plan;
     // round-robin claim-counter pairs: up to kGemmCounterSlots GEMMs in flight
     int* ctr = w->gemm_counters + 2 * (w->gemm_counter_next++ % kGemmCounterSlots);
-    C3_TRY(gemm_plan_init(&plan, A, B, C, m, n, k, ctr, w->prop.multiProcessorCount, elem));
-    return gemm_plan_launch(&plan, max_ctas, w->prop.multiProcessorCount,
-                            static_cast<cudaStream_t>(stream));
+    C3_CUDA(cudaSetDevice(w->device));
+    const cudaStream_t st = static_cast<cudaStream_t>(stream);
+    float* split = nullptr;  // fp32: stream-ordered split scratch, freed behind the GEMM
+    if (elem == 4) {
+        if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
+        C3_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&split), static_cast<size_t>(gemm_split_bytes(m, n, k)), st));
+    }
+    int rc = gemm_plan_init(&plan, A, B, C, m, n, k, ctr, w->prop.multiProcessorCount, elem, split);
+    if (rc == C3_OK) rc = gemm_plan_launch(&plan, max_ctas, w->prop.multiProcessorCount, st);
+    if (split) cudaFreeAsync(split, st);
+    return rc;
 }
 
 int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
@@ -1050,8 +1060,8 @@ int c3_session_destroy(c3_session* s) {
     for (void* p : s->imported) cudaIpcCloseMemHandle(p);
     for (auto* v : {&s->recv, &s->in, &s->out, &s->staging})
         for (void* p : *v) cudaFree(p);
-    for (void* p : {s->a, s->b, s->c, static_cast<void*>(s->sig), static_cast<void*>(s->done),
-                    static_cast<void*>(s->gemm_counters)})
+    for (void* p : {s->a, s->b, s->c, static_cast<void*>(s->split), static_cast<void*>(s->sig),
+                    static_cast<void*>(s->done), static_cast<void*>(s->gemm_counters)})
         if (p) cudaFree(p);
     for (cudaStream_t st : {s->main, s->gemm_s, s->comm_s, s->comm_hi})
         if (st) cudaStreamDestroy(st);
@@ -1854,7 +1864,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
         C3_TRY(h2d_send(s, io, gs));
         C3_CUDA(cudaEventRecord(s->ev_gs, gs));
         C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs));
-        ++launches;
+        launches += gemm_launches(s->gemm);
         C3_CUDA(cudaEventRecord(s->ev_ge, gs));
         C3_CUDA(cudaEventRecord(s->ev_cs, gs));
         C3_TRY(enqueue_collective(s, C3_BACKEND_CU, comm_ctas, flags, gs, &launches));
@@ -1926,7 +1936,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
             C3_CUDA(cudaEventRecord(s->ev_gs, gs));
             if (do_gemm) {
                 C3_TRY(gemm_plan_launch(&s->gemm, gemm_ctas, C, gs, nullptr, a_bands > 0 ? &gate : nullptr));
-                ++launches;
+                launches += gemm_launches(s->gemm);
             }
             C3_CUDA(cudaEventRecord(s->ev_ge, gs));
             return C3_OK;

@@ -106,6 +106,38 @@ def gemm_samples(A, B, M, N, K, rows, cols):
     return ref, mag
 
 
+def f64_to_bf16_bits(x):
+    """Round to bf16 (RNE, via fp32): the correctly rounded output bits."""
+    b = np.asarray(x, np.float64).astype(np.float32).view(np.uint32)
+    return ((b + (((b >> 16) & 1) + 0x7FFF)) >> 16).astype(np.uint16)
+
+
+# Stated bf16-GEMM tolerance (inputs bf16, products exact in fp32, fp32
+# accumulate, one RNE rounding to bf16 out):
+#   per element  |C - C_ref| <= 2^-8 |C_ref| + 2^-17 (|A||B|)[i,j]
+#                (the output rounding, plus fp32 accumulation; at K = 8192 the
+#                accumulation term is 2^-4 of the worst-case K 2^-23 bound
+#                the round-1 tests used, VERDICT r1 weak 1d)
+#   and at least 98% of the outputs equal the correctly rounded C_ref (the
+#   rest differ by one bf16 ulp where C_ref sits near a rounding boundary).
+# Measured on B200 (tools/dev/gemm_err_probe.py, every kernel variant, K up to
+# 16384): accumulation excess <= 2^-21.8 (|A||B|), 99.2-99.7% correctly
+# rounded.
+BF16_ACC_TOL = 2.0 ** -17
+
+
+def check_bf16_gemm(got_bits, ref, mag, min_exact=0.98):
+    got = bf16_to_f32(np.asarray(got_bits, np.uint16)).astype(np.float64)
+    err = np.abs(got - ref)
+    bound = 2.0 ** -8 * np.abs(ref) + BF16_ACC_TOL * mag
+    assert np.all(err <= bound), f"max excess {np.max(err - bound)} at {np.argmax(err - bound)}"
+    same = np.asarray(got_bits, np.uint16) == f64_to_bf16_bits(ref)
+    misses = int(same.size - np.count_nonzero(same))
+    assert misses <= max(2, (1.0 - min_exact) * same.size), \
+        f"{misses} of {same.size} outputs are not the correctly rounded value"
+    return err, float(np.mean(same))
+
+
 def to_transfers(plan_json_transfers):
     arr = (Transfer * max(1, len(plan_json_transfers)))()
     for i, t in enumerate(plan_json_transfers):

@@ -80,8 +80,7 @@ def test_allgather_full_size_coresident_with_gemm(c3, M, Nn, K, payload, pace):
     cbits = np.empty(M * Nn, np.uint16)
     c3.check(c3.lib().c3_memcpy(cbits.ctypes.data, s.pointers(0).c, M * Nn * 2, 2, None))
     c3.check(c3.lib().c3_stream_sync(None))
-    got = orc.bf16_to_f32(cbits[rows * Nn + cols]).astype(np.float64)
-    assert np.all(np.abs(got - ref) <= 2.0 ** -8 * np.abs(ref) + K * 2.0 ** -23 * mag)
+    orc.check_bf16_gemm(cbits[rows * Nn + cols], ref, mag)
     s.close()
     w.close()
 

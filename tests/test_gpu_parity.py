@@ -43,11 +43,10 @@ def to_host_u8(t, nbytes):
 
 
 def gemm_check(c_bits, A, B, M, N, K, rows, cols):
+    """The stated bf16 tolerance (tests/_oracle.py check_bf16_gemm) on the
+    sampled entries, and the relative RMS error."""
     ref, mag = orc.gemm_samples(A, B, M, N, K, rows, cols)
-    got = orc.bf16_to_f32(c_bits[rows * N + cols]).astype(np.float64)
-    err = np.abs(got - ref)
-    bound = 2.0 ** -8 * np.abs(ref) + K * 2.0 ** -23 * mag
-    assert np.all(err <= bound), f"max excess {np.max(err - bound)} at {np.argmax(err - bound)}"
+    err, _ = orc.check_bf16_gemm(c_bits[rows * N + cols], ref, mag)
     rel_rms = np.sqrt(np.mean(err ** 2)) / max(np.sqrt(np.mean(ref ** 2)), 1e-30)
     assert rel_rms <= 2.0 ** -8, rel_rms
     return rel_rms
@@ -607,22 +606,35 @@ def test_run_host_matches_device_run(torch_mod, c3, monkeypatch, collective, str
 
 
 # ---------------------------------------------------------------- fp32 / TF32
-# configs[0] is an fp32 GEMM. The product runs it on the
-# TF32 tensor cores (tcgen05.mma kind::tf32, fp32 accumulate, fp32 out).
-# Stated tolerances:
-#   * inputs representable in bf16 (the synthetic fill): TF32 reads them
-#     exactly and every product is exact in fp32, so only the fp32
-#     accumulation differs from the fp64 definition:
-#         |C - C_ref| <= 2^-19 |C_ref| + K 2^-22 (|A||B|)[i,j]
-#   * general fp32 inputs: each operand loses up to 2^-10 relative in the
-#     TF32 read, so  |C - C_ref| <= 2^-9 (|A||B|)[i,j] + K 2^-22 (|A||B|)[i,j]
+# configs[0] is an fp32 GEMM. The product runs it at fp32
+# accuracy on the TF32 tensor cores: split-TF32 (c3_gemm_f32, c3cuda.h), each
+# operand x ~ hi + lo with hi the TF32 rounding of x and lo that of the
+# remainder, three kind::tf32 K segments A_lo B_hi + A_hi B_lo + A_hi B_hi,
+# fp32 accumulate. Stated tolerances:
+#   * inputs representable in bf16 (the synthetic fill): lo = 0 and every
+#     product is exact in fp32, so only the fp32 accumulation differs from the
+#     fp64 definition:
+#         |C - C_ref| <= 2^-19 |C_ref| + 2^-17 (|A||B|)[i,j]
+#   * general fp32 inputs: |x - hi| <= 2^-11 |x|, |x - hi - lo| <= 2^-22 |x|,
+#     so the dropped A_lo B_lo and the remainders cost at most 2^-20 |a b| per
+#     product (unbiased):
+#         |C - C_ref| <= 2^-18 (|A||B|)[i,j]
+#     and an RMS error (normalised by (|A||B|)) <= 2^-20. Measured on B200
+#     (tools/dev/gemm_err_probe.py, 512x768x4096, normalised by (|A||B|)):
+#     split-TF32 RMS 2^-22.0, max 2^-19.5; plain TF32 (cuBLAS) RMS 2^-17.1,
+#     max 2^-14.8; host fp32 (numpy) RMS 2^-26.7. The gap to the host is the
+#     tensor core's own fp32 accumulation (the bf16 kernels show the same
+#     2^-22 accumulation excess).
 
 def _f32_check(got, A64, B64, K, exact_inputs):
     ref = A64 @ B64.T
     mag = np.abs(A64) @ np.abs(B64).T
-    tol = (2.0 ** -19 * np.abs(ref) if exact_inputs else 2.0 ** -9 * mag) + K * 2.0 ** -22 * mag
+    tol = 2.0 ** -19 * np.abs(ref) + 2.0 ** -17 * mag if exact_inputs else 2.0 ** -18 * mag
     err = np.abs(got.astype(np.float64) - ref)
     assert np.all(err <= tol), (float(err.max()), float((err / np.maximum(mag, 1e-30)).max()))
+    if not exact_inputs:  # split-TF32 accuracy, not TF32's (2^-17 RMS)
+        rms = float(np.sqrt(np.mean((err / mag) ** 2)))
+        assert rms <= 2.0 ** -20, rms
 
 
 def test_fill_f32_matches_oracle(torch_mod, c3):
@@ -654,9 +666,10 @@ def test_gemm_f32_tf32_full(torch_mod, c3, M, N, K):
     w.close()
 
 
-@pytest.mark.parametrize("M,N,K", [(512, 768, 1000), (300, 520, 204)])
+@pytest.mark.parametrize("M,N,K", [(512, 768, 1000), (300, 520, 204), (1024, 1024, 1024)])
 def test_gemm_f32_general_inputs(torch_mod, c3, M, N, K):
-    """General fp32 inputs (normal, wide exponent range): the TF32 bound."""
+    """General fp32 inputs (normal, wide exponent range): the split-TF32
+    bound, 32x below plain TF32's error."""
     torch = torch_mod
     w = c3.World()
     g = torch.Generator().manual_seed(3)
@@ -680,7 +693,7 @@ def test_gemm_f32_rejects_unaligned(c3, torch_mod):
 
 @pytest.mark.parametrize("strategy", ["SERIAL", "C3_BASE", "C3_SP", "CONCCL"])
 def test_cfg1_fp32_session(torch_mod, c3, strategy):
-    """configs[0] end to end: fp32 GEMM 1024^3 (TF32 tensor cores) with a
+    """configs[0] end to end: fp32 GEMM 1024^3 (split-TF32) with a
     16 MiB all-gather at world 2: the all-gather bit-exact, every GEMM entry
     within the stated bound, through the host-buffer call as well."""
     torch = torch_mod
@@ -720,7 +733,7 @@ def test_run_host_row_gated_gemm(torch_mod, c3, monkeypatch, kernel, strategy, M
     device-resident run (ragged last band included)."""
     torch = torch_mod
     monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
-    monkeypatch.setenv("C3_H2D_A_PIECES", a_pieces)  # read once per process: the first value sticks
+    monkeypatch.setenv("C3_H2D_A_PIECES", a_pieces)  # read per call (a_row_bands)
     st = getattr(c3, strategy)
     n, N, K = 8, 1536, 512
     payload = n * (5 << 20)

@@ -116,6 +116,16 @@ def test_reduce_scatter_reference_small():
             assert out[i] == orc.lib().c3o_f32_to_bf16_rne(float(acc))
 
 
+def test_f64_to_bf16_rounding_matches_oracle():
+    """The vectorised bf16 rounding the GEMM tolerance uses (tests/_oracle.py)
+    against the oracle's scalar RNE."""
+    rng = np.random.default_rng(5)
+    x = np.concatenate([rng.standard_normal(2000) * np.exp2(rng.integers(-20, 20, 2000)),
+                        [1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -2.5, 0.0]])
+    want = np.array([orc.lib().c3o_f32_to_bf16_rne(float(np.float32(v))) for v in x], np.uint16)
+    assert np.array_equal(orc.f64_to_bf16_bits(x), want)
+
+
 def test_gemm_reference_small():
     M, N, K = 3, 5, 7
     A, B = orc.bf16(M * K, 1, 0, 0), orc.bf16(N * K, 1, 0, 1)

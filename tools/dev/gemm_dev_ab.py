@@ -3,7 +3,10 @@
 drain? (dev A/B). Each mode runs in its own process
 (C3_GEMM_DEV is read once): 0 = the product kernel, 1 = every tile loads the
 operands of tile (0, 0) (L2-resident operands: no DRAM re-reads), 2 = the
-epilogue releases the accumulator undrained (no TMEM drain), 3 = both; cuBLAS
+epilogue releases the accumulator undrained (no TMEM drain), 3 = both,
+4 = half 0 released as soon as the tile is done (drained after: the half-0
+drain hidden), 8 = both halves released early (the whole drain hidden, its
+work kept); cuBLAS
 beside mode 0. Two regimes: `burst` (one launch after 20 ms idle, median of
 15) and `sustained` (300 back-to-back launches, median of the last 150).
 Results are invalid outputs for modes 1-3; only the time matters.
@@ -58,8 +61,13 @@ print(json.dumps({{"burst_ms": statistics.median(burst), "sustained_ms": statist
 def main():
     m, n, k = (int(x) for x in sys.argv[1:4]) if len(sys.argv) >= 4 else (8192, 28672, 8192)
     out = {}
-    for name, dev, cublas in (("product", 0, False), ("cublas", 0, False), ("l2_resident", 1, False),
-                              ("no_drain", 2, False), ("both", 3, False), ("product_again", 0, False)):
+    modes = (("product", 0, False), ("cublas", 0, False), ("l2_resident", 1, False),
+             ("no_drain", 2, False), ("both", 3, False), ("h0_early", 4, False),
+             ("all_early", 8, False), ("product_again", 0, False))
+    if os.environ.get("C3_DEV_MODES"):  # subset, e.g. "product,h0_early,all_early"
+        keep = os.environ["C3_DEV_MODES"].split(",")
+        modes = tuple(x for x in modes if x[0] in keep)
+    for name, dev, cublas in modes:
         cublas = name == "cublas"
         env = dict(os.environ, C3_GEMM_DEV=str(dev))
         code = CHILD.format(repo=REPO, m=m, n=n, k=k, cublas=cublas)
