@@ -256,23 +256,49 @@ def run_ours(args, dist):
                 out[name] += [job()] if callable(job) else timed(*job[:1], 1, *job[1:])
         return out
 
+    dropped = []
+
+    def viable(cands):
+        """Run each (strategy, alloc) once on every rank and keep those that
+        succeeded on ALL ranks: a strategy the platform cannot run (say, a
+        driver without cross-device batched copies) is dropped on every rank
+        alike and reported, instead of ending the run. A failing step's peers
+        give up after the bounded device waits (C3_ERR_TIMEOUT), so every rank
+        reaches the vote."""
+        bad = []
+        for st, a in cands:
+            try:
+                sess.run(st, a)
+                bad.append(0.0)
+            except c3.C3Error as e:
+                log(f"candidate {c3.STRATEGY_NAMES[st]} failed: {e}")
+                bad.append(1.0)
+        bad = dist.max_list(bad) if bad else []
+        for (st, a), b in zip(cands, bad):
+            if b:
+                dropped.append({"strategy": c3.STRATEGY_NAMES[st], "cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm})
+        return [c for c, b in zip(cands, bad) if not b]
+
+    if not viable([iso_modes["dma"]]):  # no copy-engine collective on this platform
+        del iso_modes["dma"]
+        dma_ok = False
     rounds(iso_modes, W)  # warm-up
     log("isolated warm-up done")
     strat_jobs = {}
     for st in strategies:
         if st != c3.SERIAL:
-            strat_jobs[c3.STRATEGY_NAMES[st]] = (st, sess.default_alloc(st))
+            cand = viable([(st, sess.default_alloc(st))])
+            if cand:
+                strat_jobs[c3.STRATEGY_NAMES[st]] = cand[0]
     # B200 extension: collective fused into the CTA-pair GEMM (TMA bulk copies)
     fused_ok = coll != c3.REDUCE_SCATTER
-    if fused_ok:
-        try:
-            sess.run(c3.FUSED, sess.default_alloc(c3.FUSED))
-        except c3.C3Error:
-            fused_ok = False  # shape not on the CTA-pair kernel
+    if fused_ok:  # not every shape is on the CTA-pair kernel
+        fused_ok = bool(viable([(c3.FUSED, sess.default_alloc(c3.FUSED))]))
     if fused_ok:
         strat_jobs["c3_fused"] = (c3.FUSED, sess.default_alloc(c3.FUSED))
     sweep_rows = rounds({**iso_modes, **strat_jobs}, K)
-    iso_comm = {k: median([r[col[k]] for r in sweep_rows[k]]) for k in ("cu", "dma")}
+    iso_comm = {k: median([r[col[k]] for r in sweep_rows[k]]) for k in ("cu", "dma") if k in sweep_rows}
+    iso_comm.setdefault("dma", iso_comm["cu"])  # dropped (details.dropped_candidates): unused, dma_ok is off
     log("strategy sweep done")
     t_g = median([r[1] for r in sweep_rows["gemm"]])
 
@@ -422,6 +448,7 @@ def run_ours(args, dist):
         if args.no_green:  # ncu cannot profile kernels on green-context streams
             cands = [c for c in cands if c[0] not in (c3.C3_RP, c3.C3_SP_RP)] or [(c3.SERIAL, sess.default_alloc(c3.SERIAL))]
         sess.set_link_rate(link)
+        cands = viable(cands) or [(c3.SERIAL, sess.default_alloc(c3.SERIAL))]
         meds = []
         best_i, best_ms = sess.autotune(cands, rounds=9, reduce_max=dist.max_list, medians=meds)
         log(f"autotune done: {best_i}")
@@ -448,8 +475,8 @@ def run_ours(args, dist):
     # full-speed loopback head (secondary line), picked by a short autotune
     fs = None
     if emulate:
-        fc = full_speed_candidates()
         sess.set_link_rate(0.0)
+        fc = viable(full_speed_candidates()) or [(c3.SERIAL, sess.default_alloc(c3.SERIAL))]
         fi, _ = sess.autotune(fc, rounds=5, reduce_max=dist.max_list)
         fs = fc[fi]
 
@@ -486,9 +513,14 @@ def run_ours(args, dist):
     lib = None
     if os.environ.get("C3_SHARED_DEVICE"):
         args.no_library_baseline = True  # NCCL cannot place two ranks on one device
+    lib_error = None
     if not args.no_library_baseline:
-        lib = LibraryBaseline(cfg, dist, loopback)
-        rounds({"lg": lib.gemm_only, "lc": lib.comm_only, "lb": lib.both}, W)
+        try:
+            lib = LibraryBaseline(cfg, dist, loopback)
+            rounds({"lg": lib.gemm_only, "lc": lib.comm_only, "lb": lib.both}, W)
+        except Exception as e:  # e.g. NCCL unavailable: the headline stands without it
+            lib, lib_error = None, f"{type(e).__name__}: {e}"[:300]
+            log(f"library baseline failed: {lib_error}")
     cmp_jobs = {}
     if fs:
         cmp_jobs.update({"gemm": iso_modes["gemm"], "fs_comm": iso_modes["cu"], "fs_step": fs})
@@ -633,6 +665,21 @@ def run_ours(args, dist):
                     "frac_isolated": gemm_bytes / (t_g_timed * 1e-3) / 1e9 / peaks["hbm_gbs"],
                     "collective_hbm_bytes_per_step": comm_hbm_bytes,
                     "step_hbm_frac": (gemm_bytes + comm_hbm_bytes) / (t_conc * 1e-3) / 1e9 / peaks["hbm_gbs"]}
+    # the C3 pair's roofline: the step can finish no sooner than
+    # its GEMM at the tensor (or HBM) peak, its collective's peer bytes at the
+    # link rate, or the pair's combined HBM bytes at the HBM peak
+    link_gbs = NVLINK_PEER_GBPS if emulate else 900.0
+    t_tensor = flops / (tc_peak * 1e12) * 1e3
+    t_link = (n - 1) / n * cfg["payload"] / (link_gbs * 1e9) * 1e3
+    t_hbm = (gemm_bytes + comm_hbm_bytes) / (peaks["hbm_gbs"] * 1e9) * 1e3
+    t_roof = max(t_tensor, t_link, t_hbm)
+    c3_roofline = {"makespan_ms": t_roof, "measured_ms": t_conc, "frac": t_roof / t_conc,
+                   "bound": {t_tensor: "tensor", t_link: "link", t_hbm: "hbm"}[t_roof],
+                   "terms_ms": {"gemm_at_tensor_peak": t_tensor, "collective_at_link_rate": t_link,
+                                "pair_hbm_bytes_at_hbm_peak": t_hbm},
+                   "link_gbs": link_gbs,
+                   "what": "max(F / tensor peak, (n-1)/n P / link, (B_gemm + B_comm,HBM) / HBM peak) / measured "
+                           "C3 step (SURVEY 8(d)); link = the emulated 770 GB/s at N=1, 900 GB/s at N>1"}
     if emulate:
         world_desc = (f"loopback with NVLink-rate emulation: {n}-rank scenario on 1 GPU; this GPU's GEMM "
                       f"and its share of the collective ({n - 1} chunk copies into stand-in peer buffers in "
@@ -686,6 +733,7 @@ def run_ours(args, dist):
                                     "comm_ctas": head_iso["cu"][1].cus_comm if comm_key == "cu" else 0,
                                     "full_speed_sweep_gemm": t_g, "full_speed_sweep_comm_cu": iso_comm["cu"],
                                     "full_speed_sweep_comm_dma": iso_comm["dma"]},
+                    "dropped_candidates": dropped,
                     "protocol": ("W warm-up, then K rounds of [isolated GEMM, isolated collective, "
                                  "C3 step], each round in a fresh seeded order; medians; then, outside "
                                  "the timed region, >= 15 such rounds of the full-speed pair and the "
@@ -695,6 +743,7 @@ def run_ours(args, dist):
         "loopback_full_speed": full_speed,
         "strategies_full_speed": results,
         "roofline": roofline,
+        "c3_roofline": c3_roofline,
         "e2e": {"value": e2e_speedup, "unit": UNIT,
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                 "concurrent_ms": e2e_ms["conc"], "serial_ms": e2e_ms["serial"],
@@ -738,6 +787,8 @@ def run_ours(args, dist):
             "ratio_of_medians": tb_l / ours_full,
             "compared_with": "loopback_full_speed" if full_speed else "headline",
             "note": "both concurrent steps in the same comparison rounds, fresh seeded order per round (after the timed region)"}
+    elif lib_error:
+        out["library_baseline"] = {"unavailable": lib_error}
     if dist.rank == 0 and dist.world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(cfg, n)
     sess.close()
