@@ -15,6 +15,8 @@
 //               TMA loads complete_tx on it (peer bit of the address cleared)
 //   empty[s]    both CTAs; the leader's tcgen05.commit multicasts to both
 //   acc_full[b] both CTAs; multicast commit after a tile's last k-block
+//   acc_h0      both CTAs (BN 512); multicast commit once half 0 of the tile is
+//               final: with the tail lag, L k-blocks before half 1 is
 //   acc_empty[b] leader; EPI_WARPS local + EPI_WARPS remote epilogue-warp arrivals
 //               (BN 512: one barrier per 256-column half of the accumulator)
 //   tile ring   leader claims tiles (global atomic, one tile ahead), writes
@@ -46,6 +48,13 @@ constexpr int THREADS = 256;  // 256-wide tiles: warps 0-3 roles, 4-7 epilogue
 constexpr int GROUP_M_DEFAULT = 8;
 constexpr int RING = 4;
 constexpr int kPreHalf = 4;  // BN 512: k-blocks issued into half 0 before half 1 is free (C3_GEMM_PREHALF; measured 1-4: 92.2 -> 93.1% tensor pipe)
+// BN 512 tail lag (C3_GEMM_TAILLAG): the last L k-blocks of a tile run half 0
+// first and half 1 after, so half 0 is final (and its drain starts) L k-blocks
+// of MMA work before the tile ends. With the pre k-blocks at the next tile's
+// start this hides the drain of both halves behind MMAs; without it the next
+// tile waited for the whole half-0 drain (profiles/r02_gemm_drain_release_ab.txt:
+// releasing the accumulator early is worth 0.8% burst / 2% sustained on cfg2).
+constexpr int kTailLag = 4;
 constexpr uint32_t A_STAGE = 128 * BK * 2;  // this CTA's 128 rows of A
 constexpr uint32_t B_HALF = 128 * BK * 2;   // this CTA's 128 rows of one 256-column half of B
 constexpr uint32_t TMEM_COLS = 512;
@@ -97,6 +106,7 @@ struct Params {
     int pol_a, pol_b;  // L2 policy of the A / B operand loads (policy_by_kind)
     int pol_c;         // L2 policy hint of the C stores (0: none)
     int pre_half;      // BN 512: k-blocks into half 0 before waiting for half 1 (<= STAGES)
+    int tail_lag;      // BN 512: last k-blocks whose half-1 MMAs follow the half-0 ones (<= STAGES)
     // BN 512 tail split: claims u < full_tiles are whole tiles; the last
     // num_tiles - full_tiles tiles are claimed as two 256-column halves each
     // (u in [full_tiles, num_units)), so an underfilled last wave takes half a
@@ -336,7 +346,8 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
     uint64_t* empty = bars + STAGES;
     uint64_t* acc_full = bars + 2 * STAGES;
     uint64_t* acc_empty = acc_full + ACC_BUFS;  // [2]: per accumulator (BN 256) / per 256-column half (BN 512)
-    uint64_t* tile_full = acc_empty + 2;
+    uint64_t* acc_h0 = acc_empty + 2;           // BN 512: half 0 of the tile final
+    uint64_t* tile_full = acc_h0 + 1;
     uint64_t* tile_empty = tile_full + RING;
     int* tile_ring = reinterpret_cast<int*>(tile_empty + RING);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + RING);
@@ -368,6 +379,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_init(&acc_full[b], 1);
         }
         for (int b = 0; b < 2; ++b) mbar_init(&acc_empty[b], 2 * Cfg::EPI_WARPS);
+        mbar_init(acc_h0, 1);
         for (int r = 0; r < RING; ++r) {
             mbar_init(&tile_full[r], 1);
             mbar_init(&tile_empty[r], 2 + 2 * Cfg::EPI_WARPS);
@@ -531,7 +543,12 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 mbar_wait(&acc_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
             }
-            for (int kb = kb0; kb < p.k_blocks; ++kb) {
+            // BN 512 whole tiles: the last `lag` k-blocks run half 0, then half 1
+            int lag = 0;
+            if constexpr (Cfg::HALVES == 2) {
+                if (half < 0) lag = min(min(p.tail_lag, p.k_blocks - kb0), STAGES);
+            }
+            for (int kb = kb0; kb < p.k_blocks - lag; ++kb) {
                 mbar_wait(&full[stage], phase);
                 tc_fence_after();
                 const uint32_t a_addr = a0 + stage * A_STAGE;
@@ -546,6 +563,45 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
+                }
+            }
+            if constexpr (Cfg::HALVES == 2) {
+                if (lag > 0) {
+                    // half 0 of the last `lag` k-blocks (their stages stay held) ...
+                    int st = stage;
+                    uint32_t ph = phase;
+                    for (int j = 0; j < lag; ++j) {
+                        const int kb = p.k_blocks - lag + j;
+                        mbar_wait(&full[st], ph);
+                        tc_fence_after();
+                        const uint32_t a_addr = a0 + st * A_STAGE, b_addr = b0 + st * B_STAGE;
+#pragma unroll
+                        for (int k = 0; k < BK / UK; ++k)
+                            umma_bf16_pair(d_tmem, smem_desc_k_sw128(a_addr + k * UK * 2),
+                                           smem_desc_k_sw128(b_addr + k * UK * 2), idesc, (kb | k) != 0);
+                        if (++st == STAGES) {
+                            st = 0;
+                            ph ^= 1;
+                        }
+                    }
+                    umma_commit_pair(acc_h0, 0x3);  // half 0 final: its drain overlaps what follows
+                    // ... then half 1 of the same k-blocks, releasing the stages
+                    for (int j = 0; j < lag; ++j) {
+                        const int kb = p.k_blocks - lag + j;
+                        const uint32_t a_addr = a0 + stage * A_STAGE, b_addr = b0 + stage * B_STAGE;
+#pragma unroll
+                        for (int k = 0; k < BK / UK; ++k)
+                            umma_bf16_pair(d_tmem + 256, smem_desc_k_sw128(a_addr + k * UK * 2),
+                                           smem_desc_k_sw128(b_addr + B_HALF + k * UK * 2), idesc,
+                                           (kb | k) != 0);
+                        umma_commit_pair(&empty[stage], 0x3);
+                        if (++stage == STAGES) {
+                            stage = 0;
+                            phase ^= 1;
+                        }
+                    }
+                } else {
+                    umma_commit_pair(acc_h0, 0x3);  // half 0 final with the whole tile
                 }
             }
             umma_commit_pair(&acc_full[acc], 0x3);
@@ -586,8 +642,19 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
             tile_coords(p, t_idx, tm, tn);
             const int cols = half < 0 ? COLS : 256;  // a half tile fills accumulator columns 0-255
             const int col_base = tn * BN + (half > 0 ? 256 : 0);
-            mbar_wait(&acc_full[acc], acc_phase);
+            // BN 512: half 0 may be final before half 1 (tail lag); the wait
+            // for half 1 comes before its first TMEM load
+            bool h1_ready = Cfg::HALVES != 2;
+            if constexpr (Cfg::HALVES == 2)
+                mbar_wait(acc_h0, acc_phase);
+            else
+                mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
+            if (!h1_ready && (p.dev & 14)) {  // dev modes: the whole tile first
+                mbar_wait(&acc_full[acc], acc_phase);
+                tc_fence_after();
+                h1_ready = true;
+            }
             // dev bits 2 / 3 (BN 512): release half 0 / both halves before the
             // drain (the drain still runs): the time a hidden drain would save
             int early = 0;
@@ -684,6 +751,11 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 }
                 const bool last = c + 128 >= c_begin + cols;
                 if (!last) {
+                    if (!h1_ready && c + 128 == 256) {  // half 1's first columns next
+                        mbar_wait(&acc_full[acc], acc_phase);
+                        tc_fence_after();
+                        h1_ready = true;
+                    }
                     tmem_ld_32x32b_x32(t_row + c + 128, va0);
                     tmem_ld_32x32b_x32(t_row + c + 160, va1);
                 } else {
@@ -803,6 +875,12 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
         return v < 1 ? 1 : v > gemm2::PairCfg<512>::STAGES ? gemm2::PairCfg<512>::STAGES : v;
     }();
     p.pre_half = pre_half;
+    static const int tail_lag = [] {
+        const char* e = std::getenv("C3_GEMM_TAILLAG");  // dev A/B: 0 = half 1 alongside half 0 to the end
+        const int v = e ? std::atoi(e) : gemm2::kTailLag;
+        return v < 0 ? 0 : v;
+    }();
+    p.tail_lag = tail_lag;
     static const int dev = [] {
         const char* e = std::getenv("C3_GEMM_DEV");  // dev A/B only: results invalid
         return e ? std::atoi(e) : 0;
