@@ -1,6 +1,6 @@
 // ConCCL collective decomposition: transfer plans, their exact validator and
 // their event cost model. These plans are what the B200 copy-engine executor
-// (csrc/cuda/ce_exec.cpp) runs, transfer by transfer.
+// (csrc/cuda/runtime.cpp ce_run) runs: one batched submission per engine.
 //
 // Reference semantics (/root/reference/proj):
 //   plan_all_gather   src/conccl.cpp:24-53   (peer-indexed engine, per-engine seq)
