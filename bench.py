@@ -46,8 +46,8 @@ from paper_2412_14335_b200.dist import Dist  # noqa: E402
 MIB = 1 << 20
 # BASELINE.json configs: (M, N, K), collective, payload per rank
 CONFIGS = {
-    "cfg1": dict(desc="configs[0] on the GPU: fp32 GEMM 1024x1024x1024 (fp32 accuracy: split-TF32 on "
-                      "the tensor cores, fp32 accumulate and output) || 16 MiB all-gather", m=1024, n=1024, k=1024,
+    "cfg1": dict(desc="configs[0] on the GPU: fp32 GEMM 1024x1024x1024 (split-TF32 on the tensor "
+                      "cores, fp32 accumulate and output) || 16 MiB all-gather", m=1024, n=1024, k=1024,
                  coll="all-gather", payload=16 * MIB, dtype_bytes=4, ranks=2),
     "cfg2": dict(desc="LLaMA-70B FSDP layer: FFN up-proj GEMM 8192x28672x8192 bf16 || "
                       "next-layer weight all-gather 896 MiB (gate+up) across 8 GPUs",
@@ -715,7 +715,7 @@ def run_ours(args, dist):
         "n_gpus": dist.world, "steps": K, "warmup": W,
         "ms_per_step": sum(step_ms) / len(step_ms), "ms_per_step_median": t_conc,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
-        "dtype": "fp32 (split-TF32 tensor cores, fp32 accuracy)" if elem == 4 else "bf16",
+        "dtype": "fp32 (split-TF32 on the tensor cores)" if elem == 4 else "bf16",
         "data": "synthetic (counter-hash bf16 U(-1,1)/8 and byte labels)",
         "config": bench_config(args, dist.world),
         "spread": {"paired_round_speedups": {"median": median(paired), "min": min(paired), "max": max(paired),

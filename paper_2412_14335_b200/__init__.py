@@ -73,7 +73,7 @@ class World:
             self.h = C.c_void_p()
 
     def gemm(self, a, b, c, m, n, k, max_ctas=0, stream=None, dtype_bytes=2):
-        """C = A B^T: bf16 (dtype_bytes 2) or fp32 at fp32 accuracy (4: split-TF32 on the tensor cores)."""
+        """C = A B^T: bf16 (dtype_bytes 2) or fp32 (4: split-TF32 on the tensor cores, see c3cuda.h)."""
         fn = lib().c3_gemm_f32 if dtype_bytes == 4 else lib().c3_gemm_bf16
         check(fn(self.h, a, b, c, m, n, k, max_ctas, stream))
 

@@ -87,7 +87,7 @@ def test_gemm_small_full(torch_mod, c3, M, N, K):
 
 @pytest.mark.parametrize("kernel", ["pair", "pair512", "wide", "narrow"])
 @pytest.mark.parametrize("M,N,K", [(256, 256, 64), (512, 768, 1024), (1000, 2056, 136),
-                                   (300, 520, 200), (768, 1536, 512)])
+                                   (300, 520, 200), (768, 1536, 512), (512, 1024, 320), (512, 1024, 448)])
 def test_gemm_kernel_variants_full(torch_mod, c3, monkeypatch, kernel, M, N, K):
     """Each GEMM kernel variant (CTA-pair 256x256 and 256x512, single-CTA
     128x256 and 128x128 tiles), forced, on full outputs including ragged M/N/K
@@ -680,6 +680,29 @@ def test_gemm_f32_general_inputs(torch_mod, c3, M, N, K):
     w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
     torch.cuda.synchronize()
     _f32_check(Cm.cpu().numpy(), Ah.double().numpy(), Bh.double().numpy(), K, False)
+    w.close()
+
+
+def test_gemm_f32_stream_ordered_back_to_back(torch_mod, c3):
+    """c3_gemm_f32 on a side stream, several calls back to back with no host
+    sync between them: each call's split scratch is stream-ordered
+    (cudaMallocAsync / cudaFreeAsync), so no call sees another's split."""
+    torch = torch_mod
+    w = c3.World()
+    M, N, K = 256, 384, 512
+    g = torch.Generator().manual_seed(11)
+    As = [torch.randn(M, K, generator=g) for _ in range(4)]
+    Bs = [torch.randn(N, K, generator=g) for _ in range(4)]
+    Ad, Bd = [a.cuda() for a in As], [b.cuda() for b in Bs]
+    Cs = [torch.empty(M, N, dtype=torch.float32, device="cuda") for _ in range(4)]
+    side = torch.cuda.Stream()
+    side.wait_stream(torch.cuda.current_stream())
+    for i in range(4):
+        w.gemm(Ad[i].data_ptr(), Bd[i].data_ptr(), Cs[i].data_ptr(), M, N, K, dtype_bytes=4,
+               stream=side.cuda_stream)
+    side.synchronize()
+    for i in range(4):
+        _f32_check(Cs[i].cpu().numpy(), As[i].double().numpy(), Bs[i].double().numpy(), K, False)
     w.close()
 
 
