@@ -78,6 +78,13 @@ struct CoResidentParams {
     /// store: heavier beside the GEMM than the all-to-all push of its kernel
     /// class); 0 = the all-to-all class factor. Applied by for_kind().
     double comm_reduce_scatter = 0.0;
+    /// With all_gather_by_ranks: the all-gather factor at n = 2, the limit the
+    /// rank-dependent factor tends to (its one peer means one store per load,
+    /// but the all-gather kernel's 32-byte vectors and 4 in flight per thread
+    /// lose more beside the GEMM than the all-to-all push); 0 = comm_all_to_all.
+    /// Fitted on the world-2 / 4 size sweep (profiles/r02_size_sweep_final.csv:
+    /// 4.0 against the all-to-all's 2.4, pick regret at world 2 9.3% -> ~1%).
+    double comm_all_gather_two_ranks = 0.0;
 
     /// These parameters as seen by a collective of `kind`: a reduce-scatter
     /// uses comm_reduce_scatter as its all-to-all class factor when set.
@@ -100,9 +107,11 @@ struct CoResidentParams {
         if (comm_class != KernelClass::AllGather || !all_gather_by_ranks || n_ranks <= 1 ||
             gemm_class == KernelClass::GemmMemoryBound)
             return comm_factor(comm_class);
-        const double a2a = comm_all_to_all > 0.0 ? comm_all_to_all : comm;
+        const double two = comm_all_gather_two_ranks > 0.0 ? comm_all_gather_two_ranks
+                           : comm_all_to_all > 0.0         ? comm_all_to_all
+                                                           : comm;
         const double s = n_ranks - 1;
-        return comm + (a2a - comm) / (s * s);
+        return comm + (two - comm) / (s * s);
     }
 };
 
@@ -113,7 +122,8 @@ void validate(const CoResidentParams& p);
 ///        "all-gather-by-ranks": bool (optional, default false),
 ///        "comm-memory-bound": pc (optional, 0 = the class factor),
 ///        "cta-cost": c (optional, default 0),
-///        "comm-reduce-scatter": pc (optional, 0 = the all-to-all class factor)}.
+///        "comm-reduce-scatter": pc (optional, 0 = the all-to-all class factor),
+///        "comm-all-gather-2": pc (optional, 0 = the all-to-all class factor)}.
 CoResidentParams load_coresident_params(const std::filesystem::path& path);
 std::string save_coresident_params(const CoResidentParams& p);
 

@@ -59,6 +59,9 @@ void validate(const CoResidentParams& p) {
         throw ValidationError("co-resident rate exponent must be finite and > 0");
     if (!(p.comm_reduce_scatter == 0.0 || (p.comm_reduce_scatter >= 1.0 && std::isfinite(p.comm_reduce_scatter))))
         throw ValidationError("co-resident reduce-scatter cost factor must be 0 (= all-to-all class) or >= 1");
+    if (!(p.comm_all_gather_two_ranks == 0.0 ||
+          (p.comm_all_gather_two_ranks >= 1.0 && std::isfinite(p.comm_all_gather_two_ranks))))
+        throw ValidationError("co-resident two-rank all-gather cost factor must be 0 (= all-to-all class) or >= 1");
     if (!(p.cta_cost >= 0.0) || !std::isfinite(p.cta_cost))
         throw ValidationError("co-resident CTA cost must be finite and >= 0");
 }
@@ -85,6 +88,7 @@ CoResidentParams load_coresident_params(const std::filesystem::path& path) {
         p.comm_memory_bound = j.value("comm-memory-bound", 0.0);
         p.cta_cost = j.value("cta-cost", 0.0);
         p.comm_reduce_scatter = j.value("comm-reduce-scatter", 0.0);
+        p.comm_all_gather_two_ranks = j.value("comm-all-gather-2", 0.0);
     } catch (const json::exception& e) {
         throw ValidationError("co-resident params: " + std::string(e.what()));
     }
@@ -102,6 +106,7 @@ std::string save_coresident_params(const CoResidentParams& p) {
     if (p.comm_memory_bound > 0.0) j["comm-memory-bound"] = p.comm_memory_bound;
     if (p.cta_cost > 0.0) j["cta-cost"] = p.cta_cost;
     if (p.comm_reduce_scatter > 0.0) j["comm-reduce-scatter"] = p.comm_reduce_scatter;
+    if (p.comm_all_gather_two_ranks > 0.0) j["comm-all-gather-2"] = p.comm_all_gather_two_ranks;
     return j.dump(2) + "\n";
 }
 

@@ -234,7 +234,7 @@ void add_sim(py::module_& m) {
         .def(py::init<>())
         .RW(CRP, gemm_compute_bound).RW(CRP, gemm_memory_bound).RW(CRP, comm).RW(CRP, comm_all_to_all)
         .RW(CRP, rate_exponent).RW(CRP, all_gather_by_ranks).RW(CRP, comm_memory_bound).RW(CRP, cta_cost)
-        .RW(CRP, comm_reduce_scatter).def("for_kind", &CRP::for_kind);
+        .RW(CRP, comm_reduce_scatter).RW(CRP, comm_all_gather_two_ranks).def("for_kind", &CRP::for_kind);
     m.def("load_coresident_params", &cs::load_coresident_params);
     m.def("save_coresident_params", &cs::save_coresident_params);
     m.def("simulate_coresident", &cs::simulate_coresident, py::arg("t_gemm"), py::arg("t_comm_at_ctas"),

@@ -188,6 +188,30 @@ def test_all_gather_factor_by_ranks():
     assert '"all-gather-by-ranks": true' in txt
 
 
+def test_all_gather_two_rank_factor():
+    """comm_all_gather_two_ranks replaces the all-to-all factor as the n = 2
+    limit of the rank-dependent all-gather factor (the all-to-all class keeps
+    its own); it round-trips through the params JSON and must be 0 or >= 1."""
+    p = c3sim.CoResidentParams()
+    p.comm, p.comm_all_to_all, p.all_gather_by_ranks = 1.0, 2.1, True
+    p.comm_all_gather_two_ranks = 5.5
+    AG, A2A = c3sim.KernelClass.ALL_GATHER, c3sim.KernelClass.ALL_TO_ALL
+    assert c3sim.coresident_comm_ctas(55, p, AG, 2, CB) == 10            # 55 / 5.5
+    assert c3sim.coresident_comm_ctas(64, p, AG, 4, CB) == round(64 / (1.0 + 4.5 / 9))
+    assert c3sim.coresident_comm_ctas(64, p, AG, 8, CB) == round(64 / (1.0 + 4.5 / 49))
+    assert c3sim.coresident_comm_ctas(63, p, A2A, 2, CB) == 30          # all-to-all: 63 / 2.1
+    txt = c3sim.save_coresident_params(p)
+    assert '"comm-all-gather-2": 5.5' in txt
+    p.comm_all_gather_two_ranks = 0.5
+    with pytest.raises(Exception):
+        c3sim.coresident_comm_ctas(42, p, AG, 2, CB)
+
+
+def test_shipped_coresident_params_load():
+    prm = c3sim.load_coresident_params(os.path.join(REPO, "data", "b200-coresident.json"))
+    assert prm.all_gather_by_ranks and prm.comm_all_gather_two_ranks >= 1.0
+
+
 def test_paced_collective_scales_the_gemm_penalty():
     """rate_ratio r < 1 (comm pacing): the GEMM penalty's excess scales by
     r^rate_exponent; r = 1 is the unpaced model."""

@@ -22,7 +22,13 @@ c3sim.simulate_coresident over every c3_base_coresident row, paced or not
 (grid search: for each (p_g, g) the two p_c are independent); memory-bound
 GEMM scenarios (cfg4_mb) refit p_g alone.
 
-usage: python tools/calibrate_coresident.py SWEEP.csv [SWEEP2.csv ...] OUT.json"""
+The two-rank all-gather factor (CoResidentParams::comm_all_gather_two_ranks,
+the n = 2 limit of the rank-dependent factor) is fitted last, on the world-2
+and world-4 all-gather rows beside compute-bound GEMMs (tools/size_sweep.py):
+within 1.5x of the lowest RMS error, the lowest mean pick regret. --two-ranks-only BASE.json keeps every
+other parameter of BASE.json and fits only that term.
+
+usage: python tools/calibrate_coresident.py [--two-ranks-only BASE.json] SWEEP.csv [SWEEP2.csv ...] OUT.json"""
 import csv
 import os
 import sys
@@ -138,8 +144,51 @@ def error(scen, cls, pg, pc, g, pc_a2a=None, cta=0.0):
     return err / max(n, 1), n
 
 
+def fit_two_ranks(scen, prm):
+    """comm_all_gather_two_ranks on the world-2 / 4 all-gather rows beside
+    compute-bound GEMMs: among the values within 1.5x of the lowest RMS error,
+    the lowest mean pick regret."""
+    few = {k: d for k, d in scen.items() if d["n"] in (2, 4) and d["ccls"] == c3sim.KernelClass.ALL_GATHER
+           and not (k[1].startswith("cfg4_mb") or "_mb_" in k[1])}
+    if not few:
+        return prm.comm_all_gather_two_ranks, None
+
+    def score(f):
+        q = c3sim.CoResidentParams()
+        for name in ("gemm_compute_bound", "gemm_memory_bound", "comm", "comm_all_to_all", "rate_exponent",
+                     "all_gather_by_ranks", "comm_memory_bound", "cta_cost", "comm_reduce_scatter"):
+            setattr(q, name, getattr(prm, name))
+        q.comm_all_gather_two_ranks = f
+        r = [pick_regret(d, CB, q) for d in few.values()]
+        r = [x for x in r if x is not None]
+        err = [((predict(d, c, pace, CB, q) - mk) / mk) ** 2 for d in few.values() for c, pace, mk in d["rows"]]
+        return (round(sum(r) / len(r), 3) if r else 0.0, sum(err) / max(len(err), 1)), r
+    grid = [0.0] + [1.0 + 0.25 * i for i in range(21)]  # 0 (= the all-to-all factor), 1.0 .. 6.0
+    scored = {f: score(f) for f in grid}
+    # as the main fit: among the points within 1.5x of the lowest RMS error,
+    # the lowest mean pick regret
+    lo = min(v[0][1] for v in scored.values())
+    best = min((f for f, v in scored.items() if v[0][1] <= 1.5 ** 2 * lo), key=lambda f: scored[f][0])
+    (mean_r, mse), regrets = scored[best]
+    return best, {"rows": sum(len(d["rows"]) for d in few.values()), "scenarios": len(few),
+                  "mean_pick_regret": mean_r, "max_pick_regret": max(regrets) if regrets else None,
+                  "rms": mse ** 0.5}
+
+
 def main():
-    *ins, out = sys.argv[1:]
+    args = sys.argv[1:]
+    if args and args[0] == "--two-ranks-only":
+        base, *ins, out = args[1:]
+        scen = load(ins)
+        prm = c3sim.load_coresident_params(base)
+        f, rep = fit_two_ranks(scen, prm)
+        prm.comm_all_gather_two_ranks = f
+        with open(out, "w") as fh:
+            fh.write(c3sim.save_coresident_params(prm))
+        print(f"two-rank all-gather factor {f:.2f} (0 = all-to-all class): {rep}")
+        print(f"-> {out}")
+        return
+    *ins, out = args
     scen = load(ins)
     is_mb = lambda key: key[1].startswith("cfg4_mb") or "_mb_" in key[1]  # noqa: E731  M=128: memory-bound
     cb = {k: v for k, v in scen.items() if not is_mb(k)}
@@ -208,6 +257,7 @@ def main():
     prm.gemm_memory_bound = best_mb[1] if mb else pg_cb
     prm.cta_cost = cta
     prm.comm_reduce_scatter = pc_rs
+    prm.comm_all_gather_two_ranks, two_rep = fit_two_ranks(scen, prm)
     regrets = {}
     for key, d in scen.items():
         r = pick_regret(d, MB if is_mb(key) else CB, prm)
@@ -221,6 +271,7 @@ def main():
           f"rms rel. error {e_cb ** 0.5:.3f} ({n_cb} rows, paced and unpaced)")
     if mb:
         print(f"memory-bound:  p_g {best_mb[1]:.2f}, p_c {best_mb[2]:.2f}, rms rel. error {best_mb[0] ** 0.5:.3f}")
+    print(f"two-rank all-gather factor {prm.comm_all_gather_two_ranks:.2f}: {two_rep}")
     print(f"-> {out}")
 
 
