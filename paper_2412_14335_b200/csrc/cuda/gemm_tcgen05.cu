@@ -145,9 +145,15 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
         const uint64_t keep = policy_evict_last();
         int stage = 0;
         uint32_t phase = 0;
-        // dynamic claiming, or static round-robin when no counter is given
+        // dynamic claiming, or static round-robin when no counter is given.
+        // The first tile is the CTA's own (blockIdx.x) and only the later ones
+        // are claimed: the claim runs one tile ahead, so with claimed first
+        // tiles the CTAs that start first took two tiles each before the last
+        // ones started (a collective launched beside the GEMM staggers the
+        // starts): configs[0]'s 64-tile GEMM then took two tile times
+        // (tools/dev/cfg1_probe.py: 49 -> 73 us beside the collective)
         const bool dyn = p.tile_counter != nullptr;
-        int tile = dyn ? atomicAdd(p.tile_counter, 1) : static_cast<int>(blockIdx.x);
+        int tile = static_cast<int>(blockIdx.x);
         for (int i = 0;; ++i) {
             const int r = i % TILE_RING;
             if (tile >= p.num_tiles) tile = -1;
@@ -156,7 +162,8 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             mbar_arrive(&tile_full[r]);  // release: consumers read tile_ring[r] after their wait
             if (tile < 0) break;
             // claim the next tile now; its round trip overlaps this tile's loads
-            const int next = dyn ? atomicAdd(p.tile_counter, 1) : tile + static_cast<int>(gridDim.x);
+            const int next = dyn ? static_cast<int>(gridDim.x) + atomicAdd(p.tile_counter, 1)
+                                 : tile + static_cast<int>(gridDim.x);
             int tm, tn;
             tile_coords(p, tile, tm, tn);
             for (int kb = 0; kb < p.k_blocks; ++kb) {

@@ -405,7 +405,11 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
         int stage = 0;
         uint32_t phase = 0;
         int band_ready = -1;  // A row bands known resident (they land in order)
-        int tile = leader ? atomicAdd(p.tile_counter, 1) : 0;
+        // the pair's first unit is its own (blockIdx.x / 2), later ones are
+        // claimed one ahead: claimed first units let the pairs that start first
+        // take two each before the last ones started (gemm_tcgen05.cu)
+        const int pairs = static_cast<int>(gridDim.x / 2);
+        int tile = leader ? static_cast<int>(blockIdx.x / 2) : 0;
         for (int i = 0;; ++i) {
             const int r = i % RING;
             const uint32_t par = (i / RING) & 1;
@@ -422,7 +426,7 @@ gemm_bf16_tn_pair_kernel(const __grid_constant__ CUtensorMap map_a,
                 mbar_arrive_cluster(mapa(smem_u32(&tile_empty[r]), 0));
             }
             if (tile < 0) break;
-            const int next = leader ? atomicAdd(p.tile_counter, 1) : 0;
+            const int next = leader ? pairs + atomicAdd(p.tile_counter, 1) : 0;
             int tm, tn, t_idx, half;
             unit_tile(p, tile, t_idx, half);
             tile_coords(p, t_idx, tm, tn);
