@@ -189,7 +189,9 @@ int c3_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, v
  * measured GEMM error 2^-22 RMS of sum |a||b| against 2^-17 for plain TF32
  * (the rest is the tensor core's fp32 accumulation). Two kernels on `stream`:
  * the split pass, then the GEMM; the split scratch (2 (m + n) k floats) is
- * stream-ordered (cudaMallocAsync). K, N multiples of 4. */
+ * stream-ordered (cudaMallocAsync). Infinities and NaNs propagate; finite
+ * inputs within half a TF32 ulp of FLT_MAX round to infinity in the split.
+ * K, N multiples of 4. */
 int c3_gemm_f32(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
                 int max_ctas, void* stream);
 int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,

@@ -341,8 +341,15 @@ __global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restric
         // both parts rounded to nearest TF32 (10 explicit mantissa bits), so
         // the MMA reads them exactly whatever its own TF32 conversion does, and
         // the residuals are unbiased: |v - hi| <= 2^-11 |v|, |v - hi - lo| <= 2^-22 |v|
+        // Infinities and NaNs pass through whole (lo = 0), so they propagate as
+        // in an fp32 GEMM; rounding cannot carry a NaN payload into the sign.
         auto tf32_rn = [](float v) { return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u); };
         auto split = [&](float v, float& vh, float& vl) {
+            if ((__float_as_uint(v) & 0x7F800000u) == 0x7F800000u) {
+                vh = v;
+                vl = 0.0f;
+                return;
+            }
             vh = tf32_rn(v);
             vl = tf32_rn(v - vh);  // v - vh is exact (Sterbenz)
         };

@@ -706,6 +706,28 @@ def test_gemm_f32_stream_ordered_back_to_back(torch_mod, c3):
     w.close()
 
 
+def test_gemm_f32_propagates_inf_and_nan(torch_mod, c3):
+    """The split keeps infinities and NaNs whole (a NaN payload must not round
+    into a signed zero): they propagate into their rows as in an fp32 GEMM."""
+    torch = torch_mod
+    w = c3.World()
+    M, N, K = 128, 128, 64
+    A = torch.ones(M, K)
+    B = torch.ones(N, K) * 0.5
+    A[3, 5] = float("inf")
+    A[7, 9] = float("nan")
+    A.view(torch.int32)[11, 2] = 0x7FFFFFFF  # NaN with every payload bit set
+    Ad, Bd = A.cuda(), B.cuda()
+    Cm = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    w.gemm(Ad.data_ptr(), Bd.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
+    torch.cuda.synchronize()
+    C = Cm.cpu()
+    assert torch.isinf(C[3]).all() and (C[3] > 0).all()
+    assert torch.isnan(C[7]).all() and torch.isnan(C[11]).all()
+    assert torch.equal(C[0], torch.full((N,), 32.0))
+    w.close()
+
+
 def test_gemm_f32_rejects_unaligned(c3, torch_mod):
     w = c3.World()
     t = torch_mod.empty(64 * 64, dtype=torch_mod.float32, device="cuda")
