@@ -168,27 +168,6 @@ int green_partition(c3_world* w, int comm_sms, GreenPartition** out) {
     return C3_OK;
 }
 
-// Copy-engine executor: fork from `parent`, one cudaMemcpyAsync per selected
-// transfer on the stream of its engine_id, join back into `parent`.
-// Measured on B200 (profiles/r01_ce_probe2.json): copies between two devices
-// and host<->device copies run on copy engines; a copy whose source and
-// destination are on the SAME device runs as a driver copy kernel on SMs
-// (every runtime path, including cudaMemcpyBatchAsync with
-// PreferOverlapWithCompute). So the DMA backend is copy-engine only across
-// devices; in a loopback world its "transfers" are SM copies.
-// Batched submission (cudaMemcpyBatchAsync, one call per engine stream with
-// PreferOverlapWithCompute) instead of one cudaMemcpyAsync per transfer:
-// the per-transfer CPU launch overhead the reference's plan_cost charges
-// (conccl.cpp:200-229, cpu_launch_overhead) is paid once per engine.
-// C3_CE_BATCH=0 selects the per-transfer path.
-bool ce_batch_enabled() {
-    static const bool on = [] {
-        const char* e = std::getenv("C3_CE_BATCH");
-        return !(e != nullptr && std::string(e) == "0");
-    }();
-    return on;
-}
-
 // Delivery flags of a multi-process copy-engine collective: after the copies
 // on one engine stream, word [kSigCeDone + self] of every destination rank's
 // signal array gets the step's epoch, so the receiver learns on the device
@@ -216,6 +195,17 @@ int ce_signal(const CeDeliver& dv, const std::vector<int>& dsts, cudaStream_t st
     return launch_flag_store(words, cnt, g.epoch, st);
 }
 
+// Copy-engine executor: fork from `parent`, one cudaMemcpyAsync per selected
+// transfer on the stream of its engine_id, join back into `parent`.
+// Measured on B200 (profiles/r01_ce_probe2.json): copies between two devices
+// and host<->device copies run on copy engines; a copy whose source and
+// destination are on the SAME device runs as a driver copy kernel on SMs
+// (every runtime copy path). So the DMA backend is copy-engine only across
+// devices; in a loopback world its "transfers" are SM copies.
+// One submission per transfer: the reference's plan_cost charges
+// cpu_launch_overhead per transfer (conccl.cpp:200-229), measured here at
+// 1.5 us (data/b200-ce-overheads.json). (The batched submission API of CUDA
+// 12.8+ is closed on this GPU pool after driver faults, so it is not used.)
 // Transfers selected: src_gpu == src_filter, or (dst_filter >= 0) dst_gpu ==
 // dst_filter; every transfer when both filters are < 0. Copies whose
 // destination is dst_filter use the inbound stream bank.
@@ -223,11 +213,7 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
            int src_filter, cudaStream_t parent, const CeDeliver* deliver = nullptr, int dst_filter = -1) {
     if (!w->fork_event) C3_CUDA(cudaEventCreateWithFlags(&w->fork_event, cudaEventDisableTiming));
     std::vector<char> used;
-    // per engine stream: the batch (dst, src, size) of its transfers, plan order
-    std::vector<std::vector<void*>> bd, bs;
-    std::vector<std::vector<size_t>> bz;
     std::vector<std::vector<int>> dst_ranks;  // destinations per engine stream (delivery flags)
-    const bool batch = ce_batch_enabled();
     bool forked = false;
     for (int i = 0; i < nt; ++i) {
         const c3_transfer& x = t[i];
@@ -241,9 +227,6 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
         }
         if (used.size() <= idx) {
             used.resize(idx + 1, 0);
-            bd.resize(idx + 1);
-            bs.resize(idx + 1);
-            bz.resize(idx + 1);
             dst_ranks.resize(idx + 1);
         }
         if (!used[idx]) {
@@ -254,29 +237,7 @@ int ce_run(c3_world* w, const c3_transfer* t, int nt, const void* const* src, vo
         if (std::find(dr.begin(), dr.end(), x.dst_gpu) == dr.end()) dr.push_back(x.dst_gpu);
         void* d = static_cast<uint8_t*>(dst[x.dst_gpu]) + x.dst_offset;
         const void* sp = static_cast<const uint8_t*>(src[x.src_gpu]) + x.src_offset;
-        if (batch) {
-            bd[idx].push_back(d);
-            bs[idx].push_back(const_cast<void*>(sp));
-            bz[idx].push_back(static_cast<size_t>(x.length));
-        } else {
-            C3_CUDA(cudaMemcpyAsync(d, sp, static_cast<size_t>(x.length), cudaMemcpyDefault,
-                                    w->ce_streams[idx]));
-        }
-    }
-    if (batch) {
-        cudaMemcpyAttributes attr{};
-        attr.srcAccessOrder = cudaMemcpySrcAccessOrderStream;
-        attr.flags = cudaMemcpyFlagPreferOverlapWithCompute;
-        size_t attr_idx = 0;
-        for (std::size_t idx = 0; idx < used.size(); ++idx) {
-            if (!used[idx] || bd[idx].empty()) continue;
-            size_t fail = 0;
-            const cudaError_t e = cudaMemcpyBatchAsync(bd[idx].data(), bs[idx].data(), bz[idx].data(),
-                                                       bd[idx].size(), &attr, &attr_idx, 1, &fail,
-                                                       w->ce_streams[idx]);
-            if (e != cudaSuccess)
-                return set_cuda_error(e, ("cudaMemcpyBatchAsync (transfer " + std::to_string(fail) + ")").c_str());
-        }
+        C3_CUDA(cudaMemcpyAsync(d, sp, static_cast<size_t>(x.length), cudaMemcpyDefault, w->ce_streams[idx]));
     }
     for (std::size_t idx = 0; idx < used.size(); ++idx) {
         if (!used[idx]) continue;
@@ -305,7 +266,7 @@ c3sim::MachineDescriptor b200_machine(const c3_world* w, int n) {
     md.llc_capacity = w->prop.l2CacheSize;
     md.link_bandwidth_unidir = n > 1 ? 770e9 / (n - 1) : 770e9;
     md.links_per_gpu = n - 1;
-    md.cpu_launch_overhead = 5.64e-7;
+    md.cpu_launch_overhead = 1.5e-6;
     md.dma_sync_overhead = 3.36e-5;
     c3sim::validate(md);
     return md;

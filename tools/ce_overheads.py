@@ -11,10 +11,8 @@ copy-engine collective: fork, engine start, join).
   outgoing transfers D2H into pinned host peers, the 7 incoming ones H2D),
   COMM_ONLY_DMA device time per chunk size; GB/s per direction.
 * cpu_launch_overhead: host wall time of c3_ce_execute enqueueing the full
-  56-transfer plan (D2H into pinned host buffers), per transfer, for the
-  per-transfer path (C3_CE_BATCH=0, cudaMemcpyAsync each) and the batched
-  one (cudaMemcpyBatchAsync per engine stream); the batched figure is what the
-  runtime pays, and goes into the machine descriptor.
+  56-transfer plan (D2H into pinned host buffers, one cudaMemcpyAsync per
+  transfer), per transfer; it goes into the machine descriptor.
 * dma_sync_overhead: device time of a proxy collective of 4 KiB transfers
   (bytes negligible): the fixed latency of a copy-engine collective.
 """
@@ -53,9 +51,9 @@ def proxy_bandwidth(c3, sizes, reps=7):
     return out
 
 
-def launch_overhead(batch, reps=20):
-    """Per-transfer host cost of enqueueing the 56-transfer plan (subprocess,
-    since the batch switch is read once per process)."""
+def launch_overhead(reps=20):
+    """Per-transfer host cost of enqueueing the 56-transfer plan (subprocess:
+    a fresh process, no state from the bandwidth runs)."""
     code = f"""
 import ctypes as C, json, sys, time, torch
 sys.path.insert(0, {REPO!r})
@@ -79,8 +77,7 @@ ts.sort()
 print(json.dumps({{"transfers": nt, "enqueue_s_median": ts[len(ts) // 2],
                    "per_transfer_s": ts[len(ts) // 2] / nt}}))
 """
-    env = dict(os.environ, C3_CE_BATCH="1" if batch else "0")
-    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, check=True)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, check=True)
     return json.loads(r.stdout.strip().splitlines()[-1])
 
 
@@ -88,8 +85,7 @@ def main():
     import paper_2412_14335_b200 as c3
     out_path = sys.argv[1] if len(sys.argv) > 1 else os.path.join(REPO, "data", "b200-ce-overheads.json")
     bw = proxy_bandwidth(c3, [4 << 10, 64 << 10, 1 << 20, 16 << 20, 112 << 20])
-    per = launch_overhead(False)
-    bat = launch_overhead(True)
+    per = launch_overhead()
     w = c3.World(0, 8, 0, loopback=True)
     res = {
         "what": "copy-engine measurements on one B200 (tools/ce_overheads.py): host-staged proxy "
@@ -97,8 +93,7 @@ def main():
         "async_engines": w.info.async_engines,
         "proxy_bandwidth": bw,
         "enqueue_per_transfer_path": per,
-        "enqueue_batched_path": bat,
-        "cpu_launch_overhead": bat["per_transfer_s"],
+        "cpu_launch_overhead": per["per_transfer_s"],
         "dma_sync_overhead": bw[0]["device_ms"] * 1e-3,
         "when": time.strftime("%Y-%m-%dT%H:%M:%SZ", time.gmtime()),
     }

@@ -4,7 +4,7 @@
 //     it ran on a copy engine)
 //  2. D2D copy bandwidth vs size and number of concurrent streams
 //  3. cost of satisfied / unsatisfied cuStreamWaitValue32 on a copy stream
-//  4. cudaMemcpyBatchAsync availability
+//  4. the CUDA runtime version
 // build: nvcc -gencode arch=compute_100a,code=sm_100a -O2 tools/ce_probe.cu -lcuda -o build/ce_probe
 #include <cuda.h>
 #include <cuda_runtime.h>
@@ -132,7 +132,7 @@ int main() {
         }
         printf("\"wait_wakeup_after_kernel_write_us\": %.2f,\n", tot / 20 * 1e3);
     }
-    // 4. batched memcpy API present?
+    // 4. runtime version
     printf("\"cuda_runtime_version\": %d}\n", CUDART_VERSION);
     return 0;
 }

@@ -70,27 +70,6 @@ int main() {
     under_hog("memcpy2DAsync_d2d", [&] {
         return cudaMemcpy2DAsync(b, 1 << 20, a, 1 << 20, 1 << 20, n >> 20, cudaMemcpyDeviceToDevice, s_cp);
     }, n);
-    for (int flag : {0, 1}) {
-        for (int order : {1, 3}) {
-            char name[96];
-            snprintf(name, sizeof name, "batch_d2d_flag%d_order%d", flag, order);
-            under_hog(name, [&] {
-                void* dsts[4];
-                void* srcs[4];
-                size_t sizes[4];
-                for (int i = 0; i < 4; ++i) {
-                    dsts[i] = b + i * (n / 4);
-                    srcs[i] = a + i * (n / 4);
-                    sizes[i] = n / 4;
-                }
-                cudaMemcpyAttributes attr{};
-                attr.srcAccessOrder = static_cast<cudaMemcpySrcAccessOrder>(order);
-                attr.flags = flag ? cudaMemcpyFlagPreferOverlapWithCompute : 0;
-                size_t idx = 0, fail = 0;
-                return cudaMemcpyBatchAsync(dsts, srcs, sizes, 4, &attr, &idx, 1, &fail, s_cp);
-            }, n);
-        }
-    }
     under_hog("memcpyAsync_d2h_pinned", [&] { return cudaMemcpyAsync(h, a, n, cudaMemcpyDeviceToHost, s_cp); }, n);
     under_hog("memcpyAsync_h2d_pinned", [&] { return cudaMemcpyAsync(a, h, n, cudaMemcpyHostToDevice, s_cp); }, n);
     printf("\"done\": true}\n");

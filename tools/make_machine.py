@@ -8,7 +8,7 @@ Sources, all measured on this pool's B200s:
   peak_compute_flops, hbm_bandwidth   MEASURED_PEAKS.json (driver-written): the
                                       burst cuBLAS bf16 rate and the copy bandwidth
   cpu_launch_overhead                 data/b200-ce-overheads.json: host time per
-                                      transfer of the batched copy-engine submit
+                                      transfer of the copy-engine submit
   dma_sync_overhead                   same file: device time of a copy-engine
                                       collective of 4 KiB transfers (fixed cost)
   dma_engines_per_gpu                 asyncEngineCount (ce_overheads "async_engines")
