@@ -66,27 +66,26 @@ struct GemmPlan {
     CUtensorMap map_b128;  // 128-row boxes (pair half tile, narrow kernel)
     CUtensorMap map_b256;  // 256-row boxes (wide kernel)
     CUtensorMap map_c;     // C stores: 32-row x 64-column boxes, 128B swizzle (pair kernels)
-    // fp32 (elem 4): split-TF32. Every launch first splits A and B into two
-    // TF32 numbers each, x ~ hi + lo (hi rounds x, lo the remainder), into `split` = [A_hi | A_lo | B_hi | B_lo]; the TF32 kernel then runs
-    // three K segments, A_lo B_hi + A_hi B_lo + A_hi B_hi, in one fp32
-    // accumulator. map_a / map_b* address the hi parts, the *_lo maps the lo.
-    CUtensorMap map_a_lo, map_b128_lo, map_b256_lo;
-    const void* src_a = nullptr;  // fp32: the caller's A and B (split per launch)
-    const void* src_b = nullptr;
-    float* split = nullptr;
+    // fp32 (elem 4): split-TF32 inside the SM (gemm_f32.cu): map_a / map_b128
+    // address the raw fp32 operands; f32_ws holds the per-tile arrival words and,
+    // with split-K (f32_splits > 1), the partial tiles (gemm_f32_workspace_bytes)
+    void* f32_ws = nullptr;
+    int f32_splits = 1;
     void* c = nullptr;
     int* counters = nullptr;  // device [tile claims, CTA exits]; zero between launches
     int64_t m = 0, n = 0, k = 0;
     Kind kind = kWide;
-    int elem = 2;  // 2: bf16 (kind::f16); 4: fp32 in/out, split-TF32 on the tensor cores (single-CTA kernels)
-    int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;  // of the chosen kernel (fp32: per K segment)
+    int elem = 2;  // 2: bf16 (kind::f16); 4: fp32 in/out, split-TF32 on the tensor cores
+    int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;  // of the chosen kernel
 };
-// fp32 plans need split scratch of this many bytes (2 (m + n) k floats)
-inline int64_t gemm_split_bytes(int64_t m, int64_t n, int64_t k) { return 2 * (m + n) * k * 4; }
-// kernels one gemm_plan_launch issues (fp32: the split, then the GEMM)
-inline int gemm_launches(const GemmPlan& p) { return p.elem == 4 ? 2 : 1; }
+// fp32 plans: split-K parts, and the workspace bytes (zeroed once; the kernel
+// leaves its arrival words at zero)
+int gemm_f32_splits(int64_t m, int64_t n, int64_t k, int sm_count);
+int64_t gemm_f32_workspace_bytes(int64_t m, int64_t n, int64_t k, int sm_count);
+// kernels one gemm_plan_launch issues
+inline int gemm_launches(const GemmPlan&) { return 1; }
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k, int* counters, int sm_count, int elem_bytes = 2, float* split_scratch = nullptr);
+                   int64_t k, int* counters, int sm_count, int elem_bytes = 2, void* f32_ws = nullptr);
 struct FusedComm;
 // A rows that land while the GEMM runs (c3_session_run_host): flag[b] reaches
 // `epoch` once rows [b * rows_per_flag, (b + 1) * rows_per_flag) of A are in

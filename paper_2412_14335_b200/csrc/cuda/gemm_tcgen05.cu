@@ -4,16 +4,8 @@
 //
 //   C[M,N] = A[M,K] * B[N,K]^T      (A, B K-major; C row-major)
 //
-// bf16 in / bf16 out (kind::f16), or fp32 in / fp32 out (F32 = true):
-// configs[0]'s fp32 GEMM, as split-TF32 on the tensor cores. The TF32 MMA
-// reads 10 mantissa bits, so each operand is split into two TF32 numbers,
-// x ~ hi + lo (split_tf32_kernel, one pass before the GEMM: hi rounds x, lo
-// rounds the remainder), and the K loop runs three segments into one fp32
-// accumulator: A_lo B_hi + A_hi B_lo + A_hi B_hi (the dropped A_lo B_lo and
-// the remainders lo misses are below 2^-20 |a b| per product and unbiased:
-// fp32-GEMM accuracy; plain TF32 is 2^-11). Both kinds move 128-byte K rows per stage
-// (64 bf16 or 32 fp32 elements) and issue 4 MMAs of 32 bytes of K each, so the
-// pipeline is the same.
+// bf16 in / bf16 out (kind::f16). The fp32 GEMM (configs[0]) is
+// gemm_f32.cu: split-TF32 inside the SM.
 //
 // This is the "compute" half of a C3 pair (reference GemmKernel,
 // /root/reference/proj/include/c3sim/workload.hpp:18-25; its cost model
@@ -50,7 +42,6 @@ namespace gemm {
 constexpr int BM = 128;          // UMMA M (one CTA)
 constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
 constexpr int UK = 16;           // UMMA K for 16-bit inputs
-constexpr int BK_F32 = 32;       // one 128-byte swizzle atom of fp32 (TF32 MMAs of K = 8)
 constexpr int ACC_BUFS = 2;
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;      // tile raster: 16 M-tiles per band for L2 reuse
@@ -69,8 +60,7 @@ struct Cfg {
 struct Params {
     int m, n, k;
     int tiles_m, tiles_n, num_tiles, k_blocks;
-    int kb_seg;  // F32: k-blocks per split segment (k_blocks = 3 kb_seg)
-    void* c;  // bf16, or fp32 for the TF32 kernel
+    void* c;  // bf16
     int ldc;
     int* tile_counter;  // claims; reset to 0 by the last CTA to exit
     int* exit_counter;
@@ -85,14 +75,11 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
     tn = in_band / rows;
 }
 
-template <int BN, bool F32>
+template <int BN>
 __global__ void __launch_bounds__(THREADS, 1)
 gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
-                    const __grid_constant__ CUtensorMap map_b,
-                    const __grid_constant__ CUtensorMap map_a_lo,  // F32 only: A_lo, B_lo
-                    const __grid_constant__ CUtensorMap map_b_lo, const Params p) {
+                    const __grid_constant__ CUtensorMap map_b, const Params p) {
     using K = Cfg<BN>;
-    constexpr int BKE = F32 ? BK_F32 : BK;  // K elements per stage (128 bytes per row)
     constexpr int STAGES = K::STAGES;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1024-byte alignment for the 128B-swizzle atoms.
@@ -116,10 +103,6 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_a);
         tma_prefetch_desc(&map_b);
-        if constexpr (F32) {
-            tma_prefetch_desc(&map_a_lo);
-            tma_prefetch_desc(&map_b_lo);
-        }
         for (int s = 0; s < STAGES; ++s) {
             mbar_init(&full[s], 1);
             mbar_init(&empty[s], 1);
@@ -167,20 +150,10 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             int tm, tn;
             tile_coords(p, tile, tm, tn);
             for (int kb = 0; kb < p.k_blocks; ++kb) {
-                // F32: segment 0 = (A_lo, B_hi), 1 = (A_hi, B_lo), 2 = (A_hi, B_hi)
-                const CUtensorMap* ma = &map_a;
-                const CUtensorMap* mb = &map_b;
-                int kk = kb;
-                if constexpr (F32) {
-                    const int seg = kb / p.kb_seg;
-                    kk = kb - seg * p.kb_seg;
-                    if (seg == 0) ma = &map_a_lo;
-                    if (seg == 1) mb = &map_b_lo;
-                }
                 mbar_wait(&empty[stage], phase ^ 1);
                 mbar_arrive_expect_tx(&full[stage], K::STAGE);
-                tma_load_2d(smem_a + stage * K::A_STAGE, ma, &full[stage], kk * BKE, tm * BM, keep);
-                tma_load_2d(smem_b + stage * K::B_STAGE, mb, &full[stage], kk * BKE, tn * BN, keep);
+                tma_load_2d(smem_a + stage * K::A_STAGE, &map_a, &full[stage], kb * BK, tm * BM, keep);
+                tma_load_2d(smem_b + stage * K::B_STAGE, &map_b, &full[stage], kb * BK, tn * BN, keep);
                 if (++stage == STAGES) {
                     stage = 0;
                     phase ^= 1;
@@ -190,7 +163,7 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
         }
     } else if (warp == 1 && lane == 0) {
         // ---------------- MMA issuer ----------------
-        constexpr uint32_t idesc = F32 ? idesc_tf32_f32(BM, BN) : idesc_bf16_f32(BM, BN);
+        constexpr uint32_t idesc = idesc_bf16_f32(BM, BN);
         const uint32_t a0 = smem_u32(smem_a), b0 = smem_u32(smem_b);
         int stage = 0;
         uint32_t phase = 0;
@@ -212,14 +185,9 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                 const uint32_t b_addr = b0 + stage * K::B_STAGE;
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
-                    // advancing K inside the 128-byte swizzle atom = +32 B per MMA
-                    // (16 bf16 or 8 tf32 elements)
-                    if constexpr (F32)
-                        umma_tf32(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
-                                  idesc, (kb | k) != 0);
-                    else
-                        umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
-                                  idesc, (kb | k) != 0);
+                    // advancing K inside the 128-byte swizzle atom = +32 B (16 bf16) per MMA
+                    umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
+                              idesc, (kb | k) != 0);
                 }
                 umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
                 if (++stage == STAGES) {
@@ -261,39 +229,26 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                 tmem_ld_wait();
                 const int col = tn * BN + c;
                 if (!row_ok) continue;
-                if constexpr (F32) {
-                    float* crow = static_cast<float*>(p.c) + static_cast<size_t>(row) * p.ldc;
-                    if (col + 32 <= p.n) {
-                        uint4* dst = reinterpret_cast<uint4*>(crow + col);
+                __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(p.c) + static_cast<size_t>(row) * p.ldc;
+                if (col + 32 <= p.n) {
+                    uint4* dst = reinterpret_cast<uint4*>(crow + col);
 #pragma unroll
-                        for (int j = 0; j < 8; ++j) dst[j] = make_uint4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col + j < p.n) crow[col + j] = __uint_as_float(v[j]);
+                    for (int j = 0; j < 4; ++j) {
+                        uint4 o;
+                        __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
+                        __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
+                        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
+                        __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
+                        o.x = *reinterpret_cast<uint32_t*>(&h0);
+                        o.y = *reinterpret_cast<uint32_t*>(&h1);
+                        o.z = *reinterpret_cast<uint32_t*>(&h2);
+                        o.w = *reinterpret_cast<uint32_t*>(&h3);
+                        dst[j] = o;
                     }
                 } else {
-                    __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(p.c) + static_cast<size_t>(row) * p.ldc;
-                    if (col + 32 <= p.n) {
-                        uint4* dst = reinterpret_cast<uint4*>(crow + col);
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            uint4 o;
-                            __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
-                            __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-                            __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-                            __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
-                            o.x = *reinterpret_cast<uint32_t*>(&h0);
-                            o.y = *reinterpret_cast<uint32_t*>(&h1);
-                            o.z = *reinterpret_cast<uint32_t*>(&h2);
-                            o.w = *reinterpret_cast<uint32_t*>(&h3);
-                            dst[j] = o;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(__uint_as_float(v[j]));
-                    }
+                    for (int j = 0; j < 32; ++j)
+                        if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(__uint_as_float(v[j]));
                 }
             }
             tc_fence_before();
@@ -323,45 +278,6 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
     }
 }
 
-// x ~ hi + lo, hi = the TF32 rounding of x, lo = the TF32 rounding of the
-// remainder; A and B in one grid-stride pass of 16-byte vectors
-__global__ void __launch_bounds__(256) split_tf32_kernel(const float4* __restrict__ a, int64_t na4,
-                                                         const float4* __restrict__ b, int64_t nb4,
-                                                         float4* __restrict__ out) {
-    // out = [A_hi (na4) | A_lo (na4) | B_hi (nb4) | B_lo (nb4)]
-    const int64_t total = na4 + nb4;
-    for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<int64_t>(gridDim.x) * blockDim.x) {
-        const bool in_a = i < na4;
-        const int64_t j = in_a ? i : i - na4;
-        const int64_t n4 = in_a ? na4 : nb4;
-        float4* hi = out + (in_a ? 0 : 2 * na4) + j;
-        const float4 x = in_a ? a[j] : b[j];
-        float4 h, l;
-        // both parts rounded to nearest TF32 (10 explicit mantissa bits), so
-        // the MMA reads them exactly whatever its own TF32 conversion does, and
-        // the residuals are unbiased: |v - hi| <= 2^-11 |v|, |v - hi - lo| <= 2^-22 |v|
-        // Infinities and NaNs pass through whole (lo = 0), so they propagate as
-        // in an fp32 GEMM; rounding cannot carry a NaN payload into the sign.
-        auto tf32_rn = [](float v) { return __uint_as_float((__float_as_uint(v) + 0x1000u) & 0xFFFFE000u); };
-        auto split = [&](float v, float& vh, float& vl) {
-            if ((__float_as_uint(v) & 0x7F800000u) == 0x7F800000u) {
-                vh = v;
-                vl = 0.0f;
-                return;
-            }
-            vh = tf32_rn(v);
-            vl = tf32_rn(v - vh);  // v - vh is exact (Sterbenz)
-        };
-        split(x.x, h.x, l.x);
-        split(x.y, h.y, l.y);
-        split(x.z, h.z, l.z);
-        split(x.w, h.w, l.w);
-        hi[0] = h;
-        hi[n4] = l;
-    }
-}
-
 }  // namespace gemm
 
 // ----------------------------------------------------------------- host ---
@@ -384,13 +300,12 @@ CUresult encode_kmajor_bf16(CUtensorMap* map, const void* ptr, uint64_t rows, ui
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-template <int BN, bool F32>
-int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, const CUtensorMap& map_b_lo, int grid,
-              cudaStream_t stream) {
+template <int BN>
+int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStream_t stream) {
     using K = gemm::Cfg<BN>;
     static bool attr_done = false;
     if (!attr_done) {
-        const cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel<BN, F32>,
+        const cudaError_t e = cudaFuncSetAttribute(gemm::gemm_bf16_tn_kernel<BN>,
                                                    cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                    static_cast<int>(K::SMEM));
         if (e != cudaSuccess) return set_cuda_error(e, "cudaFuncSetAttribute(gemm)");
@@ -403,8 +318,7 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, const CUtensorMap&
     p.tiles_m = static_cast<int>((plan->m + gemm::BM - 1) / gemm::BM);
     p.tiles_n = static_cast<int>((plan->n + BN - 1) / BN);
     p.num_tiles = p.tiles_m * p.tiles_n;
-    p.kb_seg = plan->k_blocks;
-    p.k_blocks = F32 ? 3 * plan->k_blocks : plan->k_blocks;
+    p.k_blocks = plan->k_blocks;
     p.c = plan->c;
     p.ldc = static_cast<int>(plan->n);
     static const bool static_sched = [] {
@@ -414,8 +328,7 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, const CUtensorMap&
     p.tile_counter = static_sched ? nullptr : plan->counters;
     p.exit_counter = plan->counters + 1;
     grid = std::min(grid, p.num_tiles);
-    gemm::gemm_bf16_tn_kernel<BN, F32><<<grid, gemm::THREADS, K::SMEM, stream>>>(
-        plan->map_a, map_b, F32 ? plan->map_a_lo : plan->map_a, map_b_lo, p);
+    gemm::gemm_bf16_tn_kernel<BN><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, map_b, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
     return C3_OK;
@@ -425,13 +338,14 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, const CUtensorMap&
 
 int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const FusedComm* fc,
                      const RowGate* gate);
+int gemm_f32_launch(const GemmPlan* plan, int grid, cudaStream_t stream);
 
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k, int* counters, int sm_count, int elem_bytes, float* split_scratch) {
+                   int64_t k, int* counters, int sm_count, int elem_bytes, void* f32_ws) {
     if (elem_bytes != 2 && elem_bytes != 4)
         return set_error(C3_ERR_VALIDATION, "gemm: element size must be 2 (bf16) or 4 (fp32, split-TF32)");
-    if (elem_bytes == 4 && !split_scratch)
-        return set_error(C3_ERR_VALIDATION, "gemm: an fp32 plan needs split scratch (gemm_split_bytes)");
+    if (elem_bytes == 4 && !f32_ws)
+        return set_error(C3_ERR_VALIDATION, "gemm: an fp32 plan needs a workspace (gemm_f32_workspace_bytes)");
     const int64_t row_elems = 16 / elem_bytes;
     if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
     if (k % row_elems != 0) return set_error(C3_ERR_VALIDATION, "gemm: K rows must be a multiple of 16 bytes");
@@ -456,8 +370,8 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
                  : m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
                  : tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow
                                                      : GemmPlan::kWide;
-    if (elem_bytes == 4)  // the TF32 path is the single-CTA kernel
-        plan->kind = tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow : GemmPlan::kWide;
+    if (elem_bytes == 4)  // fp32: 128 x 128 tiles of the split-TF32 kernel (gemm_f32.cu)
+        plan->kind = GemmPlan::kNarrow;
     if (const char* f = std::getenv("C3_GEMM_KERNEL"); f && elem_bytes == 2) {  // tests force each variant
         const std::string v(f);
         if (v == "pair") plan->kind = GemmPlan::kPair;
@@ -465,32 +379,20 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
         if (v == "wide") plan->kind = GemmPlan::kWide;
         if (v == "narrow") plan->kind = GemmPlan::kNarrow;
     }
-    // fp32: the maps address the split parts, [A_hi | A_lo | B_hi | B_lo]
-    plan->src_a = A;
-    plan->src_b = B;
-    plan->split = elem_bytes == 4 ? split_scratch : nullptr;
-    const void* a_hi = elem_bytes == 4 ? static_cast<const void*>(split_scratch) : A;
-    const void* b_hi = elem_bytes == 4 ? static_cast<const void*>(split_scratch + 2 * m * k) : B;
-    CUresult r = encode_kmajor_bf16(&plan->map_a, a_hi, static_cast<uint64_t>(m), static_cast<uint64_t>(k), 128,
+    // fp32: the raw operands (the split happens in shared memory)
+    plan->f32_ws = elem_bytes == 4 ? f32_ws : nullptr;
+    plan->f32_splits = elem_bytes == 4 ? gemm_f32_splits(m, n, k, sm_count) : 1;
+    CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), 128,
                                     elem_bytes);
     if (r == CUDA_SUCCESS)  // 128-row B boxes: the pair kernel's half tile and the narrow kernel
-        r = encode_kmajor_bf16(&plan->map_b128, b_hi, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 128,
+        r = encode_kmajor_bf16(&plan->map_b128, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 128,
                                elem_bytes);
+    if (r == CUDA_SUCCESS && elem_bytes == 2)
+        r = encode_kmajor_bf16(&plan->map_b256, B, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 256);
+    // C [m, n] in 32-row boxes of one 128-byte swizzle row (64 bf16 / 32 fp32
+    // columns): the TMA-store epilogues of the pair kernels and the fp32 kernel
     if (r == CUDA_SUCCESS)
-        r = encode_kmajor_bf16(&plan->map_b256, b_hi, static_cast<uint64_t>(n), static_cast<uint64_t>(k), 256,
-                               elem_bytes);
-    if (r == CUDA_SUCCESS && elem_bytes == 4) {
-        r = encode_kmajor_bf16(&plan->map_a_lo, split_scratch + m * k, static_cast<uint64_t>(m),
-                               static_cast<uint64_t>(k), 128, 4);
-        if (r == CUDA_SUCCESS)
-            r = encode_kmajor_bf16(&plan->map_b128_lo, split_scratch + 2 * m * k + n * k, static_cast<uint64_t>(n),
-                                   static_cast<uint64_t>(k), 128, 4);
-        if (r == CUDA_SUCCESS)
-            r = encode_kmajor_bf16(&plan->map_b256_lo, split_scratch + 2 * m * k + n * k, static_cast<uint64_t>(n),
-                                   static_cast<uint64_t>(k), 256, 4);
-    }
-    if (r == CUDA_SUCCESS && elem_bytes == 2)  // C [m, n] in 32-row x 64-column boxes (pair kernels' TMA-store epilogue)
-        r = encode_kmajor_bf16(&plan->map_c, C, static_cast<uint64_t>(m), static_cast<uint64_t>(n), 32);
+        r = encode_kmajor_bf16(&plan->map_c, C, static_cast<uint64_t>(m), static_cast<uint64_t>(n), 32, elem_bytes);
     if (r != CUDA_SUCCESS) return set_driver_error(r, "cuTensorMapEncodeTiled");
     plan->m = m;
     plan->n = n;
@@ -498,7 +400,7 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     plan->c = C;
     plan->counters = counters;
     plan->elem = elem_bytes;
-    const int bke = elem_bytes == 4 ? gemm::BK_F32 : gemm::BK;
+    const int bke = elem_bytes == 4 ? 32 : gemm::BK;  // 128-byte K rows
     plan->k_blocks = static_cast<int>((k + bke - 1) / bke);
     const bool pair = plan->kind == GemmPlan::kPair || plan->kind == GemmPlan::kPair512;
     const int bm = pair ? 256 : 128;
@@ -523,20 +425,11 @@ int gemm_plan_launch(const GemmPlan* plan, int max_ctas, int sm_count, cudaStrea
     }
     if (plan->elem == 4) {
         if (gate && gate->flags) return set_error(C3_ERR_UNSUPPORTED, "row-gated GEMM needs the CTA-pair kernel");
-        // split A and B (the whole GPU: the pass is HBM-bound and short), then the GEMM
-        const int64_t na4 = plan->m * plan->k / 4, nb4 = plan->n * plan->k / 4;
-        const int64_t blocks = std::min<int64_t>((na4 + nb4 + 255) / 256, 4 * static_cast<int64_t>(sm_count));
-        gemm::split_tf32_kernel<<<static_cast<int>(blocks), 256, 0, stream>>>(
-            static_cast<const float4*>(plan->src_a), na4, static_cast<const float4*>(plan->src_b), nb4,
-            reinterpret_cast<float4*>(plan->split));
-        C3_CUDA(cudaGetLastError());
-        if (plan->kind == GemmPlan::kWide)
-            return launch_bn<256, true>(plan, plan->map_b256, plan->map_b256_lo, grid, stream);
-        return launch_bn<128, true>(plan, plan->map_b128, plan->map_b128_lo, grid, stream);
+        return gemm_f32_launch(plan, grid, stream);
     }
     if (gate && gate->flags) return set_error(C3_ERR_UNSUPPORTED, "row-gated GEMM needs the CTA-pair kernel");
-    if (plan->kind == GemmPlan::kWide) return launch_bn<256, false>(plan, plan->map_b256, plan->map_b256, grid, stream);
-    return launch_bn<128, false>(plan, plan->map_b128, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap
+    if (plan->kind == GemmPlan::kWide) return launch_bn<256>(plan, plan->map_b256, grid, stream);
+    return launch_bn<128>(plan, plan->map_b128, grid, stream);  // narrow, or a 1-SM cap
 }
 
 }  // namespace c3k

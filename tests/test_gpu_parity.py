@@ -609,12 +609,14 @@ def test_run_host_matches_device_run(torch_mod, c3, monkeypatch, collective, str
 # configs[0] is an fp32 GEMM. The product runs it at fp32
 # accuracy on the TF32 tensor cores: split-TF32 (c3_gemm_f32, c3cuda.h), each
 # operand x ~ hi + lo with hi the TF32 rounding of x and lo that of the
-# remainder, three kind::tf32 K segments A_lo B_hi + A_hi B_lo + A_hi B_hi,
+# remainder, three kind::tf32 MMAs per K step A_lo B_hi + A_hi B_lo + A_hi B_hi,
 # fp32 accumulate. Stated tolerances:
 #   * inputs representable in bf16 (the synthetic fill): lo = 0 and every
 #     product is exact in fp32, so only the fp32 accumulation differs from the
 #     fp64 definition:
 #         |C - C_ref| <= 2^-19 |C_ref| + 2^-17 (|A||B|)[i,j]
+#   (split inside the SM by converter warps, gemm_f32.cu; split-K with a
+#   fixed-order sum of the partials when the tiles are fewer than the SMs)
 #   * general fp32 inputs: |x - hi| <= 2^-11 |x|, |x - hi - lo| <= 2^-22 |x|,
 #     so the dropped A_lo B_lo and the remainders cost at most 2^-20 |a b| per
 #     product (unbiased):
@@ -685,8 +687,8 @@ def test_gemm_f32_general_inputs(torch_mod, c3, M, N, K):
 
 def test_gemm_f32_stream_ordered_back_to_back(torch_mod, c3):
     """c3_gemm_f32 on a side stream, several calls back to back with no host
-    sync between them: each call's split scratch is stream-ordered
-    (cudaMallocAsync / cudaFreeAsync), so no call sees another's split."""
+    sync between them: each call's workspace is stream-ordered
+    (cudaMallocAsync / cudaFreeAsync), so no call sees another's partials."""
     torch = torch_mod
     w = c3.World()
     M, N, K = 256, 384, 512
@@ -706,25 +708,57 @@ def test_gemm_f32_stream_ordered_back_to_back(torch_mod, c3):
     w.close()
 
 
-def test_gemm_f32_propagates_inf_and_nan(torch_mod, c3):
-    """The split keeps infinities and NaNs whole (a NaN payload must not round
-    into a signed zero): they propagate into their rows as in an fp32 GEMM."""
+@pytest.mark.parametrize("K", [64, 256])  # 256: split-K (4 parts) over the slow path
+def test_gemm_f32_propagates_inf_and_nan(torch_mod, c3, K):
+    """Infinities and NaNs follow IEEE fp32 GEMM semantics: every product
+    a*b is formed once (inf * finite = inf, inf * 0 = NaN, inf * inf = inf,
+    -inf + inf = NaN), and a finite input next to FLT_MAX stays finite."""
     torch = torch_mod
     w = c3.World()
-    M, N, K = 128, 128, 64
+    M, N = 128, 128
     A = torch.ones(M, K)
     B = torch.ones(N, K) * 0.5
     A[3, 5] = float("inf")
     A[7, 9] = float("nan")
     A.view(torch.int32)[11, 2] = 0x7FFFFFFF  # NaN with every payload bit set
+    A[13, 20] = float("inf")
+    B[4, 20] = float("inf")  # inf * inf in C[13, 4]; 1 * inf down column 4
+    A[17, 1] = -float("inf")  # -inf row, NaN at column 4 (-inf + inf)
+    A[21, 30] = float("inf")
+    B[9, 30] = 0.0  # inf * 0 = NaN at C[21, 9]
+    A[25, 0] = 3.4e38  # finite: its TF32 rounding would overflow
     Ad, Bd = A.cuda(), B.cuda()
     Cm = torch.empty(M, N, dtype=torch.float32, device="cuda")
     w.gemm(Ad.data_ptr(), Bd.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
     torch.cuda.synchronize()
-    C = Cm.cpu()
-    assert torch.isinf(C[3]).all() and (C[3] > 0).all()
-    assert torch.isnan(C[7]).all() and torch.isnan(C[11]).all()
-    assert torch.equal(C[0], torch.full((N,), 32.0))
+    C = Cm.cpu().double().numpy()
+    with np.errstate(invalid="ignore", over="ignore"):
+        ref = A.double().numpy() @ B.double().numpy().T
+    assert np.array_equal(np.isnan(C), np.isnan(ref))
+    assert np.array_equal(np.isposinf(C), np.isposinf(ref)) and np.array_equal(np.isneginf(C), np.isneginf(ref))
+    fin = np.isfinite(ref)
+    assert np.all(np.abs(C[fin] - ref[fin]) <= 2.0 ** -20 * np.abs(ref[fin]))
+    assert np.isposinf(C[13, 4]) and np.isnan(C[17, 4]) and np.isnan(C[21, 9]) and np.isfinite(C[25, 0])
+    w.close()
+
+
+def test_gemm_f32_split_k_is_bit_reproducible(torch_mod, c3):
+    """configs[0]'s shape runs split-K (the last-arriving part sums the
+    partials in fixed order), so repeated calls are bitwise identical."""
+    torch = torch_mod
+    w = c3.World()
+    M = N = K = 1024
+    g = torch.Generator().manual_seed(5)
+    A, B = torch.randn(M, K, generator=g).cuda(), torch.randn(N, K, generator=g).cuda()
+    outs = []
+    for _ in range(4):
+        Cm = torch.empty(M, N, dtype=torch.float32, device="cuda")
+        w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
+        outs.append(Cm)
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o.view(torch.int32), outs[0].view(torch.int32))
+    _f32_check(outs[0].cpu().numpy(), A.cpu().double().numpy(), B.cpu().double().numpy(), K, False)
     w.close()
 
 

@@ -3,7 +3,8 @@ GEMM (cfg2 shape by default), loopback all-gather push and reduce-scatter
 pull, and the fused C3 pair GEMM next to the plain pair GEMM (cfg2 + 896 MiB
 all-gather, loopback), all through the C ABI.
 cublas: torch.matmul (cuBLAS) on the same shape, for a side-by-side capture.
-Usage: python tools/ncu_target.py [gemm|cublas|ag|rs|fused|all] [M N K]"""
+f32: the split-TF32 fp32 GEMM (configs[0]: 1024^3 by default with this mode).
+Usage: python tools/ncu_target.py [gemm|cublas|ag|rs|fused|f32|all] [M N K]"""
 import os
 import sys
 
@@ -22,6 +23,17 @@ if what in ("gemm", "all"):
     Cm = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
     for _ in range(2):
         w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K)
+    torch.cuda.synchronize()
+    w.close()
+if what == "f32":
+    if len(sys.argv) < 5:
+        M = N = K = 1024
+    w = c3.World()
+    A = torch.randn(M, K, device="cuda")
+    B = torch.randn(N, K, device="cuda")
+    Cm = torch.empty(M, N, device="cuda")
+    for _ in range(3):
+        w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, dtype_bytes=4)
     torch.cuda.synchronize()
     w.close()
 if what == "cublas":
