@@ -642,8 +642,8 @@ def run_ours(args, dist):
     ratio = tc_peak * 1e12 / (peaks["hbm_gbs"] * 1e9)
     if flops / gemm_bytes >= ratio:
         roofline = {"bound": "tensor",
-                    "kernel": ("gemm_bf16_tn_kernel<*, F32> (split-TF32, tcgen05 kind::tf32; peak = "
-                               "bf16 / 2 / 3)" if elem == 4
+                    "kernel": ("gemm_f32_split_kernel (split-TF32 in shared memory, tcgen05 kind::tf32, "
+                               "split-K; peak = bf16 / 2 / 3)" if elem == 4
                                else "gemm_bf16_tn_pair_kernel (tcgen05 cta_group::2)"),
                     "achieved": achieved, "peak": tc_peak, "unit": "TFLOP/s",
                     "frac": achieved / tc_peak,

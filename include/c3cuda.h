@@ -183,15 +183,16 @@ int c3_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, v
  * roofline_gemm_time (workload.hpp:62-63) models; max_ctas caps the
  * persistent grid = the GEMM's SM allocation (Allocation::cus_gemm). */
 /* fp32 A, B, C on the TF32 tensor cores, split-TF32: each operand is split
- * into two TF32 numbers, x ~ hi + lo (hi rounds x, lo rounds the remainder),
- * and tcgen05.mma kind::tf32 accumulates A_lo B_hi + A_hi B_lo + A_hi B_hi in
- * fp32. Operand error below 2^-20 |a b| per product (plain TF32: 2^-11);
- * measured GEMM error 2^-22 RMS of sum |a||b| against 2^-17 for plain TF32
- * (the rest is the tensor core's fp32 accumulation). Two kernels on `stream`:
- * the split pass, then the GEMM; the split scratch (2 (m + n) k floats) is
- * stream-ordered (cudaMallocAsync). Infinities and NaNs propagate; finite
- * inputs within half a TF32 ulp of FLT_MAX round to infinity in the split.
- * K, N multiples of 4. */
+ * into two TF32 numbers, x ~ hi + lo (hi = x as the tensor core reads it,
+ * truncated to TF32; lo the rounded remainder), and tcgen05.mma kind::tf32
+ * accumulates A_lo B_hi + A_hi B_lo + A_hi B_hi in fp32. The split happens in
+ * shared memory inside the one GEMM kernel; split-K (two parts for 1024^3)
+ * adds the parts in a fixed order, so results are bit-reproducible.
+ * Operand error below 2^-20 |a b| per product (plain TF32: 2^-11); measured
+ * GEMM error 2^-23 RMS of sum |a||b| against 2^-17 for plain TF32. A
+ * stream-ordered workspace (cudaMallocAsync) holds the split-K arrival
+ * words. Infinities and NaNs follow IEEE fp32 GEMM semantics (each product
+ * formed once). K, N multiples of 4. */
 int c3_gemm_f32(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
                 int max_ctas, void* stream);
 int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
