@@ -15,3 +15,16 @@ for coll in (c3.ALL_GATHER, c3.ALL_TO_ALL, c3.REDUCE_SCATTER):
     s.close()
     w.close()
 print("sanitize target done")
+if os.environ.get("C3_SANITIZE_F32", "1") == "1":
+    # the fp32 split-TF32 kernel: split-K S = 4 and 3 (workspace), S = 1, S = 2 (TMA add), a non-finite stage
+    import torch
+    w = c3.World()
+    for (M, N, K) in ((256, 256, 256), (300, 520, 200), (512, 1024, 64), (1024, 1024, 128)):
+        A = torch.randn(M, K, device="cuda")
+        B = torch.randn(N, K, device="cuda")
+        A[1, 3] = float("inf")
+        C = torch.empty(M, N, device="cuda")
+        w.gemm(A.data_ptr(), B.data_ptr(), C.data_ptr(), M, N, K, dtype_bytes=4)
+    torch.cuda.synchronize()
+    w.close()
+    print("sanitize f32 done")

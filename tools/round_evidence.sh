@@ -20,3 +20,6 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --
   python bench.py --steps 3 --warmup 3 --no-green --no-cpu-baseline > "$OUT/bench_under_ncu.log" 2>&1; echo "ncu launches rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:gemm_bf16_tn_pair -s 1 -c 1 \
   -o "$OUT/ncu_gemm_cfg2" python tools/ncu_target.py gemm 8192 28672 8192 > "$OUT/ncu_full.log" 2>&1; echo "ncu full rc=$?"
+for tool in memcheck synccheck racecheck; do
+  C3_SANITIZE_F32=1 timeout 900 compute-sanitizer --tool $tool python tools/dev/sanitize_target.py > "$OUT/sanitizer_$tool.txt" 2>&1; echo "sanitizer $tool rc=$?"
+done
