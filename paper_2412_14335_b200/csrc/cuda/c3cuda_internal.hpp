@@ -66,10 +66,13 @@ struct GemmPlan {
     CUtensorMap map_b128;  // 128-row boxes (pair half tile, narrow kernel)
     CUtensorMap map_b256;  // 256-row boxes (wide kernel)
     CUtensorMap map_c;     // C stores: 32-row x 64-column boxes, 128B swizzle (pair kernels)
-    // fp32 (elem 4): split-TF32 inside the SM (gemm_f32.cu): map_a / map_b128
-    // address the raw fp32 operands; f32_ws holds the per-tile arrival words and,
-    // with split-K (f32_splits > 1), the partial tiles (gemm_f32_workspace_bytes)
-    void* f32_ws = nullptr;
+    // Workspace (gemm_workspace_bytes, zeroed once; the kernels leave their
+    // arrival words at zero). fp32 (elem 4, gemm_f32.cu, map_a / map_b128 on the
+    // raw operands): the split-K arrival words (and partials for > 2 parts).
+    // bf16 single-CTA kinds: the stream-K tail's arrival words and partials for
+    // up to sk_capacity tail tiles (nullptr: no stream-K).
+    void* ws = nullptr;
+    int sk_capacity = 0;
     int f32_splits = 1;
     void* c = nullptr;
     int* counters = nullptr;  // device [tile claims, CTA exits]; zero between launches
@@ -78,14 +81,18 @@ struct GemmPlan {
     int elem = 2;  // 2: bf16 (kind::f16); 4: fp32 in/out, split-TF32 on the tensor cores
     int tiles_m = 0, tiles_n = 0, num_tiles = 0, k_blocks = 0;  // of the chosen kernel
 };
-// fp32 plans: split-K parts, and the workspace bytes (zeroed once; the kernel
-// leaves its arrival words at zero)
+// fp32 plans: split-K parts and workspace bytes
 int gemm_f32_splits(int64_t m, int64_t n, int64_t k, int sm_count);
 int64_t gemm_f32_workspace_bytes(int64_t m, int64_t n, int64_t k, int sm_count);
+// a plan's kernel kind, and the workspace bytes its plan wants (0: none)
+GemmPlan::Kind gemm_kind(int64_t m, int64_t n, int elem_bytes, int sm_count);
+int64_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int elem_bytes, int sm_count);
+// stream-K arrival words (done, ready) for `cap` tail tiles, 256-byte aligned
+inline int64_t gemm_sk_counter_bytes(int cap) { return (2 * static_cast<int64_t>(cap) * 4 + 255) / 256 * 256; }
 // kernels one gemm_plan_launch issues
 inline int gemm_launches(const GemmPlan&) { return 1; }
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k, int* counters, int sm_count, int elem_bytes = 2, void* f32_ws = nullptr);
+                   int64_t k, int* counters, int sm_count, int elem_bytes = 2, void* ws = nullptr);
 struct FusedComm;
 // A rows that land while the GEMM runs (c3_session_run_host): flag[b] reaches
 // `epoch` once rows [b * rows_per_flag, (b + 1) * rows_per_flag) of A are in

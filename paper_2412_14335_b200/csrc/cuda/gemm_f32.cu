@@ -586,9 +586,9 @@ int gemm_f32_launch(const GemmPlan* plan, int grid, cudaStream_t stream) {
     p.num_units = p.num_tiles * p.splits;
     p.c = static_cast<float*>(plan->c);
     p.ldc = static_cast<int>(plan->n);
-    p.tile_done = reinterpret_cast<int*>(plan->f32_ws);
+    p.tile_done = reinterpret_cast<int*>(plan->ws);
     p.tile_ready = p.tile_done + p.num_tiles;
-    p.ws = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(plan->f32_ws) +
+    p.ws = reinterpret_cast<float4*>(reinterpret_cast<uint8_t*>(plan->ws) +
                                      (2 * static_cast<int64_t>(p.num_tiles) * 4 + 255) / 256 * 256);
     p.tile_counter = plan->counters;
     p.exit_counter = plan->counters + 1;

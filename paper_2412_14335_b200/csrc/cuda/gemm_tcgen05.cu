@@ -64,7 +64,55 @@ struct Params {
     int ldc;
     int* tile_counter;  // claims; reset to 0 by the last CTA to exit
     int* exit_counter;
+    // Stream-K tail (sk_segs > 0): claims u < full_units are whole tiles; the
+    // k-blocks of the last num_tiles - full_units tiles are cut into sk_segs
+    // equal segments (u = full_units + s) shorter than a tile, so a segment
+    // is one or two pieces, and long enough that a tile is at most
+    // kSkMaxPieces. The decomposition depends on the SM count only, not on
+    // the launched grid, so a CTA cap changes no output bit. The piece
+    // of a tile that arrives last finishes it: the others publish fp32
+    // partials, it sums all in piece order (its own from TMEM) and rounds to
+    // bf16 once.
+    int full_units, num_units, sk_segs;
+    int64_t sk_kb;      // k-blocks of the tail
+    float4* sk_ws;      // [tail tile][kSkMaxPieces][BN / 4][BM] fp32 partials
+    int* sk_done;       // [tail tile] pieces arrived  (zero between launches)
+    int* sk_ready;      // [tail tile] partials published (zero between launches)
 };
+constexpr int kSkMaxPieces = 4;
+
+struct Piece {
+    int tile, kb0, kb1;
+    int idx, count;  // this piece's index among its tile's pieces, and their number
+};
+
+// stream-K segment starts floor(s L / G), s = 1..G-1, at or below tail k-block x
+__device__ __forceinline__ int64_t sk_cuts_le(const Params& p, int64_t x) {
+    return min(static_cast<int64_t>(p.sk_segs - 1), ((x + 1) * p.sk_segs - 1) / p.sk_kb);
+}
+
+// the pieces of claim u (1 or 2)
+__device__ __forceinline__ int unit_pieces(const Params& p, int u, Piece (&pc)[2]) {
+    if (u < p.full_units) {
+        pc[0] = {u, 0, p.k_blocks, 0, 1};
+        return 1;
+    }
+    const int64_t s = u - p.full_units;
+    int64_t pos = s * p.sk_kb / p.sk_segs;
+    const int64_t end = (s + 1) * p.sk_kb / p.sk_segs;
+    int n = 0;
+    while (pos < end && n < 2) {
+        const int t = static_cast<int>(pos / p.k_blocks);
+        const int64_t base = static_cast<int64_t>(t) * p.k_blocks;
+        const int64_t stop = min(end, base + p.k_blocks);
+        const int64_t before = sk_cuts_le(p, base);  // cuts at or before the tile's start
+        pc[n++] = {p.full_units + t, static_cast<int>(pos - base), static_cast<int>(stop - base),
+                   static_cast<int>(sk_cuts_le(p, pos) - before),
+                   static_cast<int>(1 + sk_cuts_le(p, base + p.k_blocks - 1) - before)};
+        pos = stop;
+    }
+    return n;
+}
 
 __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, int& tn) {
     const int band = GROUP_M * p.tiles_n;
@@ -75,8 +123,14 @@ __device__ __forceinline__ void tile_coords(const Params& p, int tile, int& tm, 
     tn = in_band / rows;
 }
 
+// <= 136 registers per thread (as before the stream-K tail): a co-resident
+// collective CTA still fits beside the GEMM's in the SM's register file (the
+// memory-bound GEMM of configs[3])
+#ifndef C3_NARROW_MAXNREG
+#define C3_NARROW_MAXNREG 136
+#endif
 template <int BN>
-__global__ void __launch_bounds__(THREADS, 1)
+__global__ void __maxnreg__(C3_NARROW_MAXNREG)
 gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                     const __grid_constant__ CUtensorMap map_b, const Params p) {
     using K = Cfg<BN>;
@@ -96,6 +150,7 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
     uint64_t* tile_empty = tile_full + TILE_RING;
     int* tile_ring = reinterpret_cast<int*>(tile_empty + TILE_RING);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_ring + TILE_RING);
+    uint32_t* sk_flag = tmem_slot + 1;  // stream-K: this piece arrived first (epilogue warps)
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
@@ -139,24 +194,28 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
         int tile = static_cast<int>(blockIdx.x);
         for (int i = 0;; ++i) {
             const int r = i % TILE_RING;
-            if (tile >= p.num_tiles) tile = -1;
+            if (tile >= p.num_units) tile = -1;
             mbar_wait(&tile_empty[r], ((i / TILE_RING) & 1) ^ 1);
             tile_ring[r] = tile;
             mbar_arrive(&tile_full[r]);  // release: consumers read tile_ring[r] after their wait
             if (tile < 0) break;
-            // claim the next tile now; its round trip overlaps this tile's loads
+            // claim the next unit now; its round trip overlaps this one's loads
             const int next = dyn ? static_cast<int>(gridDim.x) + atomicAdd(p.tile_counter, 1)
                                  : tile + static_cast<int>(gridDim.x);
-            int tm, tn;
-            tile_coords(p, tile, tm, tn);
-            for (int kb = 0; kb < p.k_blocks; ++kb) {
-                mbar_wait(&empty[stage], phase ^ 1);
-                mbar_arrive_expect_tx(&full[stage], K::STAGE);
-                tma_load_2d(smem_a + stage * K::A_STAGE, &map_a, &full[stage], kb * BK, tm * BM, keep);
-                tma_load_2d(smem_b + stage * K::B_STAGE, &map_b, &full[stage], kb * BK, tn * BN, keep);
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
+            Piece pc[2];
+            const int np = unit_pieces(p, tile, pc);
+            for (int pi = 0; pi < np; ++pi) {
+                int tm, tn;
+                tile_coords(p, pc[pi].tile, tm, tn);
+                for (int kb = pc[pi].kb0; kb < pc[pi].kb1; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    mbar_arrive_expect_tx(&full[stage], K::STAGE);
+                    tma_load_2d(smem_a + stage * K::A_STAGE, &map_a, &full[stage], kb * BK, tm * BM, keep);
+                    tma_load_2d(smem_b + stage * K::B_STAGE, &map_b, &full[stage], kb * BK, tn * BN, keep);
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
             }
             tile = next;
@@ -175,30 +234,34 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             const int tile = tile_ring[r];
             mbar_arrive(&tile_empty[r]);
             if (tile < 0) break;
-            mbar_wait(&acc_empty[acc], acc_phase ^ 1);
-            tc_fence_after();
-            const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
-            for (int kb = 0; kb < p.k_blocks; ++kb) {
-                mbar_wait(&full[stage], phase);
+            Piece pc[2];
+            const int np = unit_pieces(p, tile, pc);
+            for (int pi = 0; pi < np; ++pi) {
+                mbar_wait(&acc_empty[acc], acc_phase ^ 1);
                 tc_fence_after();
-                const uint32_t a_addr = a0 + stage * K::A_STAGE;
-                const uint32_t b_addr = b0 + stage * K::B_STAGE;
+                const uint32_t d_tmem = tmem_base + static_cast<uint32_t>(acc * BN);
+                for (int kb = pc[pi].kb0; kb < pc[pi].kb1; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t a_addr = a0 + stage * K::A_STAGE;
+                    const uint32_t b_addr = b0 + stage * K::B_STAGE;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    // advancing K inside the 128-byte swizzle atom = +32 B (16 bf16) per MMA
-                    umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
-                              idesc, (kb | k) != 0);
+                    for (int k = 0; k < 4; ++k) {
+                        // advancing K inside the 128-byte swizzle atom = +32 B (16 bf16) per MMA
+                        umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
+                                  idesc, (kb != pc[pi].kb0 || k != 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
+                    if (++stage == STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
                 }
-                umma_commit(&empty[stage]);  // frees the smem slot when these MMAs retire
-                if (++stage == STAGES) {
-                    stage = 0;
-                    phase ^= 1;
+                umma_commit(&acc_full[acc]);  // accumulator tile (piece) complete
+                if (++acc == ACC_BUFS) {
+                    acc = 0;
+                    acc_phase ^= 1;
                 }
-            }
-            umma_commit(&acc_full[acc]);  // accumulator tile complete
-            if (++acc == ACC_BUFS) {
-                acc = 0;
-                acc_phase ^= 1;
             }
         }
     } else if (warp >= 4) {
@@ -214,48 +277,135 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
             __syncwarp();
             if (lane == 0) mbar_arrive(&tile_empty[r]);
             if (tile < 0) break;
-            int tm, tn;
-            tile_coords(p, tile, tm, tn);
-            mbar_wait(&acc_full[acc], acc_phase);
-            tc_fence_after();
-            const int row = tm * BM + row_in_tile;
-            const bool row_ok = row < p.m;
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
-                                   static_cast<uint32_t>(acc * BN);
-#pragma unroll 1
-            for (int c = 0; c < BN; c += 32) {
-                uint32_t v[32];
-                tmem_ld_32x32b_x32(t_row + c, v);
-                tmem_ld_wait();
-                const int col = tn * BN + c;
-                if (!row_ok) continue;
+            Piece pc[2];
+            const int np = unit_pieces(p, tile, pc);
+            for (int pi = 0; pi < np; ++pi) {
+                int tm, tn;
+                tile_coords(p, pc[pi].tile, tm, tn);
+                mbar_wait(&acc_full[acc], acc_phase);
+                tc_fence_after();
+                const int row = tm * BM + row_in_tile;
+                const bool row_ok = row < p.m;
+                const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) +
+                                       static_cast<uint32_t>(acc * BN);
                 __nv_bfloat16* crow = static_cast<__nv_bfloat16*>(p.c) + static_cast<size_t>(row) * p.ldc;
-                if (col + 32 <= p.n) {
-                    uint4* dst = reinterpret_cast<uint4*>(crow + col);
+                // 32 fp32 columns -> bf16 (one rounding) -> this row of C
+                auto store32 = [&](const float (&f)[32], int col) {
+                    if (!row_ok) return;
+                    if (col + 32 <= p.n) {
+                        uint4* dst = reinterpret_cast<uint4*>(crow + col);
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        uint4 o;
-                        __nv_bfloat162 h0 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 0]), __uint_as_float(v[8 * j + 1]));
-                        __nv_bfloat162 h1 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 2]), __uint_as_float(v[8 * j + 3]));
-                        __nv_bfloat162 h2 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 4]), __uint_as_float(v[8 * j + 5]));
-                        __nv_bfloat162 h3 = __floats2bfloat162_rn(__uint_as_float(v[8 * j + 6]), __uint_as_float(v[8 * j + 7]));
-                        o.x = *reinterpret_cast<uint32_t*>(&h0);
-                        o.y = *reinterpret_cast<uint32_t*>(&h1);
-                        o.z = *reinterpret_cast<uint32_t*>(&h2);
-                        o.w = *reinterpret_cast<uint32_t*>(&h3);
-                        dst[j] = o;
+                        for (int j = 0; j < 4; ++j)
+                            dst[j] = make_uint4(pack_bf16x2(__float_as_uint(f[8 * j]), __float_as_uint(f[8 * j + 1])),
+                                                pack_bf16x2(__float_as_uint(f[8 * j + 2]), __float_as_uint(f[8 * j + 3])),
+                                                pack_bf16x2(__float_as_uint(f[8 * j + 4]), __float_as_uint(f[8 * j + 5])),
+                                                pack_bf16x2(__float_as_uint(f[8 * j + 6]), __float_as_uint(f[8 * j + 7])));
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(f[j]);
                     }
-                } else {
+                };
+                const bool whole = pc[pi].kb0 == 0 && pc[pi].kb1 == p.k_blocks;
+                if (whole) {
+#pragma unroll 1
+                    for (int c = 0; c < BN; c += 32) {
+                        uint32_t v[32];
+                        tmem_ld_32x32b_x32(t_row + c, v);
+                        tmem_ld_wait();
+                        float f[32];
 #pragma unroll
-                    for (int j = 0; j < 32; ++j)
-                        if (col + j < p.n) crow[col + j] = __float2bfloat16_rn(__uint_as_float(v[j]));
+                        for (int j = 0; j < 32; ++j) f[j] = __uint_as_float(v[j]);
+                        store32(f, tn * BN + c);
+                    }
+                    tc_fence_before();
+                    mbar_arrive(&acc_empty[acc]);
+                } else {
+                    // a stream-K tile in pieces: every piece but the last to arrive
+                    // publishes its fp32 partial; the last waits for them (their
+                    // epilogues already counted, and wait on nothing), sums all in
+                    // piece order (its own from TMEM) and rounds once: the result
+                    // does not depend on arrival order
+                    const Piece& pce = pc[pi];
+                    const int tt = pce.tile - p.full_units;
+                    named_bar_sync(1, 128);  // every epilogue thread read the previous sk_flag
+                    if (threadIdx.x == 128)
+                        st_shared_u32(sk_flag, atomicAdd(p.sk_done + tt, 1) == pce.count - 1 ? 1u : 0u);
+                    named_bar_sync(1, 128);
+                    const size_t slot_f4 = static_cast<size_t>(BN / 4) * BM;
+                    float4* slots = p.sk_ws + static_cast<size_t>(tt) * kSkMaxPieces * slot_f4 + row_in_tile;
+                    if (!ld_volatile_shared(sk_flag)) {
+                        float4* mine = slots + pce.idx * slot_f4;
+#pragma unroll 1
+                        for (int c = 0; c < BN; c += 32) {
+                            uint32_t v[32];
+                            tmem_ld_32x32b_x32(t_row + c, v);
+                            tmem_ld_wait();
+#pragma unroll
+                            for (int j = 0; j < 8; ++j)
+                                mine[(c / 4 + j) * BM] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                                     __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                        }
+                        tc_fence_before();
+                        mbar_arrive(&acc_empty[acc]);
+                        __threadfence();  // the partial is visible before it is counted ready
+                        named_bar_sync(1, 128);
+                        if (threadIdx.x == 128) atomicAdd(p.sk_ready + tt, 1);
+                    } else {
+                        if (threadIdx.x == 128)
+                            while (ld_acquire_gpu(p.sk_ready + tt) < pce.count - 1) __nanosleep(64);
+                        named_bar_sync(1, 128);
+                        __threadfence();
+#pragma unroll 1
+                        for (int c = 0; c < BN; c += 32) {
+                            uint32_t v[32];
+                            tmem_ld_32x32b_x32(t_row + c, v);
+                            tmem_ld_wait();
+                            float f[32];
+                            // fixed order: piece 0, 1, ... (own at its index); each
+                            // other piece's 8 vectors as one batch of loads
+#pragma unroll
+                            for (int q_idx = 0; q_idx < kSkMaxPieces; ++q_idx) {
+                                if (q_idx >= pce.count) continue;
+                                float4 t[8];
+                                if (q_idx == pce.idx) {
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j)
+                                        t[j] = make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                                                           __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+                                } else {
+#pragma unroll
+                                    for (int j = 0; j < 8; ++j) t[j] = ld_cg_f4(slots + q_idx * slot_f4 + (c / 4 + j) * BM);
+                                }
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    if (q_idx == 0) {
+                                        f[4 * j] = t[j].x;
+                                        f[4 * j + 1] = t[j].y;
+                                        f[4 * j + 2] = t[j].z;
+                                        f[4 * j + 3] = t[j].w;
+                                    } else {
+                                        f[4 * j] += t[j].x;
+                                        f[4 * j + 1] += t[j].y;
+                                        f[4 * j + 2] += t[j].z;
+                                        f[4 * j + 3] += t[j].w;
+                                    }
+                                }
+                            }
+                            store32(f, tn * BN + c);
+                        }
+                        tc_fence_before();
+                        mbar_arrive(&acc_empty[acc]);
+                        if (threadIdx.x == 128) {  // for the next launch (no one else touches them now)
+                            p.sk_done[tt] = 0;
+                            p.sk_ready[tt] = 0;
+                        }
+                    }
                 }
-            }
-            tc_fence_before();
-            mbar_arrive(&acc_empty[acc]);
-            if (++acc == ACC_BUFS) {
-                acc = 0;
-                acc_phase ^= 1;
+                if (++acc == ACC_BUFS) {
+                    acc = 0;
+                    acc_phase ^= 1;
+                }
             }
         }
     }
@@ -327,7 +477,40 @@ int launch_bn(const GemmPlan* plan, const CUtensorMap& map_b, int grid, cudaStre
     }();
     p.tile_counter = static_sched ? nullptr : plan->counters;
     p.exit_counter = plan->counters + 1;
-    grid = std::min(grid, p.num_tiles);
+    // Stream-K tail: when the tiles leave the last wave of the full GPU partly
+    // empty, that wave's k-blocks are spread evenly over one segment per SM.
+    // Decided from the SM count alone (not the grid), so the result bits do
+    // not depend on the CTA cap. Segments of g >= (k - 1) / 3 k-blocks keep a
+    // tile to at most kSkMaxPieces pieces (C3_GEMM_STREAMK=0: off, dev A/B).
+    // Compute-bound GEMMs only (>= 200 FLOP per operand/output byte): a
+    // memory-bound one's last wave already streams at the HBM rate with fewer
+    // SMs, and the fix-up only adds traffic (measured, ncu: 256x4096x16384
+    // 81.7 -> 56.4 us; 128x53248x16384 279.6 -> 284.3 us, so off there).
+    static const bool streamk = [] {
+        const char* e = std::getenv("C3_GEMM_STREAMK");
+        return !(e != nullptr && std::string(e) == "0");
+    }();
+    const int segs = plan->sk_capacity;
+    const int waves = p.num_tiles / segs, tail = p.num_tiles - waves * segs;
+    const int64_t seg_kb = static_cast<int64_t>(tail) * p.k_blocks / segs;
+    p.full_units = p.num_units = p.num_tiles;
+    p.sk_segs = 0;
+    p.sk_kb = 0;
+    const double flops = 2.0 * static_cast<double>(plan->m) * plan->n * plan->k;
+    const double bytes = 2.0 * (static_cast<double>(plan->m) * plan->k + static_cast<double>(plan->n) * plan->k +
+                                static_cast<double>(plan->m) * plan->n);
+    const bool compute_bound = flops >= 200.0 * bytes;
+    if (streamk && compute_bound && plan->ws && tail > 0 && p.k_blocks >= 2 && seg_kb >= 1 &&
+        p.k_blocks - 2 < 3 * seg_kb) {
+        p.full_units = waves * segs;
+        p.sk_segs = segs;
+        p.num_units = p.full_units + segs;
+        p.sk_kb = static_cast<int64_t>(tail) * p.k_blocks;
+        p.sk_done = static_cast<int*>(plan->ws);
+        p.sk_ready = p.sk_done + plan->sk_capacity;
+        p.sk_ws = reinterpret_cast<float4*>(static_cast<uint8_t*>(plan->ws) + gemm_sk_counter_bytes(plan->sk_capacity));
+    }
+    grid = std::min(grid, p.num_units);
     gemm::gemm_bf16_tn_kernel<BN><<<grid, gemm::THREADS, K::SMEM, stream>>>(plan->map_a, map_b, p);
     const cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return set_cuda_error(e, "gemm launch");
@@ -340,12 +523,48 @@ int gemm_pair_launch(const GemmPlan* plan, int grid, cudaStream_t stream, const 
                      const RowGate* gate);
 int gemm_f32_launch(const GemmPlan* plan, int grid, cudaStream_t stream);
 
+// Kernel choice: CTA-pair 256x512, else 256x256 tiles when there is at least
+// one pair tile per SM pair; else single-CTA 128x256 tiles, or 128x128 when
+// that leaves fewer than two tiles per SM (e.g. M=128: 208 -> 416 tiles).
+// 256x512 pair tiles when every SM pair gets one: 25% less L2->SM operand
+// traffic than 256x256, which the 1 kW power cap turns into clock
+// (sustained cfg2 / 8192^3 / cfg4: +3% / +4% / +7%, profiles/r01_gemm_pair512_ab.txt).
+// fp32: 128 x 128 tiles of the split-TF32 kernel (gemm_f32.cu).
+GemmPlan::Kind gemm_kind(int64_t m, int64_t n, int elem_bytes, int sm_count) {
+    if (elem_bytes == 4) return GemmPlan::kNarrow;
+    const int64_t sms = std::max(sm_count, 2);
+    const int64_t tm1 = (m + 127) / 128;
+    const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
+    const int64_t pair512_tiles = ((m + 255) / 256) * ((n + 511) / 512);
+    GemmPlan::Kind kind = m >= 256 && pair512_tiles >= sms / 2 ? GemmPlan::kPair512
+                          : m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
+                          : tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow
+                                                              : GemmPlan::kWide;
+    if (const char* f = std::getenv("C3_GEMM_KERNEL")) {  // tests force each variant
+        const std::string v(f);
+        if (v == "pair") kind = GemmPlan::kPair;
+        if (v == "pair512") kind = GemmPlan::kPair512;
+        if (v == "wide") kind = GemmPlan::kWide;
+        if (v == "narrow") kind = GemmPlan::kNarrow;
+    }
+    return kind;
+}
+
+int64_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int elem_bytes, int sm_count) {
+    if (elem_bytes == 4) return gemm_f32_workspace_bytes(m, n, k, sm_count);
+    const GemmPlan::Kind kind = gemm_kind(m, n, elem_bytes, sm_count);
+    if (kind != GemmPlan::kNarrow && kind != GemmPlan::kWide) return 0;
+    const int64_t bn = kind == GemmPlan::kNarrow ? 128 : 256;
+    // stream-K: a partial per tail tile, fewer tail tiles than CTAs (<= SMs)
+    return gemm_sk_counter_bytes(sm_count) + static_cast<int64_t>(sm_count) * gemm::kSkMaxPieces * gemm::BM * bn * 4;
+}
+
 int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_t m, int64_t n,
-                   int64_t k, int* counters, int sm_count, int elem_bytes, void* f32_ws) {
+                   int64_t k, int* counters, int sm_count, int elem_bytes, void* ws) {
     if (elem_bytes != 2 && elem_bytes != 4)
         return set_error(C3_ERR_VALIDATION, "gemm: element size must be 2 (bf16) or 4 (fp32, split-TF32)");
-    if (elem_bytes == 4 && !f32_ws)
-        return set_error(C3_ERR_VALIDATION, "gemm: an fp32 plan needs a workspace (gemm_f32_workspace_bytes)");
+    if (elem_bytes == 4 && !ws)
+        return set_error(C3_ERR_VALIDATION, "gemm: an fp32 plan needs a workspace (gemm_workspace_bytes)");
     const int64_t row_elems = 16 / elem_bytes;
     if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
     if (k % row_elems != 0) return set_error(C3_ERR_VALIDATION, "gemm: K rows must be a multiple of 16 bytes");
@@ -355,32 +574,10 @@ int gemm_plan_init(GemmPlan* plan, const void* A, const void* B, void* C, int64_
     if (m > INT32_MAX || n > INT32_MAX || k > INT32_MAX)
         return set_error(C3_ERR_VALIDATION, "gemm: dimension too large");
     if (!counters) return set_error(C3_ERR_VALIDATION, "gemm: missing tile-claim counters");
-    // Kernel choice: CTA-pair 256x512, else 256x256 tiles when there is at
-    // least one pair tile per SM pair; else single-CTA 128x256 tiles, or
-    // 128x128 when that leaves fewer than two tiles per SM (e.g. M=128: 208 ->
-    // 416 tiles).
-    const int64_t sms = std::max(sm_count, 2);
-    const int64_t tm1 = (m + 127) / 128;
-    const int64_t pair_tiles = ((m + 255) / 256) * ((n + 255) / 256);
-    const int64_t pair512_tiles = ((m + 255) / 256) * ((n + 511) / 512);
-    // 256x512 pair tiles when every SM pair gets one: 25% less L2->SM operand
-    // traffic than 256x256, which the 1 kW power cap turns into clock
-    // (sustained cfg2 / 8192^3 / cfg4: +3% / +4% / +7%, profiles/r01_gemm_pair512_ab.txt)
-    plan->kind = m >= 256 && pair512_tiles >= sms / 2 ? GemmPlan::kPair512
-                 : m >= 256 && pair_tiles >= sms / 2 ? GemmPlan::kPair
-                 : tm1 * ((n + 255) / 256) < 2 * sms ? GemmPlan::kNarrow
-                                                     : GemmPlan::kWide;
-    if (elem_bytes == 4)  // fp32: 128 x 128 tiles of the split-TF32 kernel (gemm_f32.cu)
-        plan->kind = GemmPlan::kNarrow;
-    if (const char* f = std::getenv("C3_GEMM_KERNEL"); f && elem_bytes == 2) {  // tests force each variant
-        const std::string v(f);
-        if (v == "pair") plan->kind = GemmPlan::kPair;
-        if (v == "pair512") plan->kind = GemmPlan::kPair512;
-        if (v == "wide") plan->kind = GemmPlan::kWide;
-        if (v == "narrow") plan->kind = GemmPlan::kNarrow;
-    }
+    plan->kind = gemm_kind(m, n, elem_bytes, sm_count);
     // fp32: the raw operands (the split happens in shared memory)
-    plan->f32_ws = elem_bytes == 4 ? f32_ws : nullptr;
+    plan->ws = ws;  // fp32: split-K words; bf16 single-CTA kinds: stream-K (nullptr: off)
+    plan->sk_capacity = std::max(sm_count, 2);
     plan->f32_splits = elem_bytes == 4 ? gemm_f32_splits(m, n, k, sm_count) : 1;
     CUresult r = encode_kmajor_bf16(&plan->map_a, A, static_cast<uint64_t>(m), static_cast<uint64_t>(k), 128,
                                     elem_bytes);

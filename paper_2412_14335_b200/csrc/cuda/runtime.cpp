@@ -319,7 +319,7 @@ struct c3_session {
     GemmPlan gemm;
     int* gemm_counters = nullptr;
     void *a = nullptr, *b = nullptr, *c = nullptr;
-    void* f32_ws = nullptr;  // fp32 sessions: the split-TF32 GEMM's workspace (gemm_f32_workspace_bytes)
+    void* gemm_ws = nullptr;  // the GEMM plan's workspace (gemm_workspace_bytes: fp32 split-K, bf16 stream-K)
     // per virtual rank: AG recv (payload, own chunk in place); RS in (payload),
     // out (chunk), staging (payload)
     std::vector<void*> recv, in, out, staging;
@@ -384,13 +384,13 @@ int session_alloc(c3_session* s) {
     C3_CUDA(cudaMalloc(&s->c, static_cast<size_t>(d.m * d.n * s->elem)));
     C3_CUDA(cudaMalloc(&s->gemm_counters, 2 * sizeof(int)));
     C3_CUDA(cudaMemset(s->gemm_counters, 0, 2 * sizeof(int)));
-    if (s->elem == 4) {
-        const size_t ws = static_cast<size_t>(gemm_f32_workspace_bytes(d.m, d.n, d.k, s->w->prop.multiProcessorCount));
-        C3_CUDA(cudaMalloc(&s->f32_ws, ws));
-        C3_CUDA(cudaMemset(s->f32_ws, 0, ws));
+    const size_t ws = static_cast<size_t>(gemm_workspace_bytes(d.m, d.n, d.k, s->elem, s->w->prop.multiProcessorCount));
+    if (ws > 0) {
+        C3_CUDA(cudaMalloc(&s->gemm_ws, ws));
+        C3_CUDA(cudaMemset(s->gemm_ws, 0, ws));
     }
     C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k, s->gemm_counters,
-                          s->w->prop.multiProcessorCount, s->elem, s->f32_ws));
+                          s->w->prop.multiProcessorCount, s->elem, s->gemm_ws));
     const size_t payload = static_cast<size_t>(d.payload_bytes);
     for (int v = 0; v < s->vr; ++v) {
         void* p = nullptr;
@@ -821,10 +821,10 @@ static int world_gemm(c3_world* w, const void* A, const void* B, void* C, int64_
     int* ctr = w->gemm_counters + 2 * (w->gemm_counter_next++ % kGemmCounterSlots);
     C3_CUDA(cudaSetDevice(w->device));
     const cudaStream_t st = static_cast<cudaStream_t>(stream);
-    void* ws = nullptr;  // fp32: stream-ordered workspace, zeroed, freed behind the GEMM
-    if (elem == 4) {
-        if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
-        const size_t bytes = static_cast<size_t>(gemm_f32_workspace_bytes(m, n, k, w->prop.multiProcessorCount));
+    void* ws = nullptr;  // stream-ordered workspace (fp32 split-K, bf16 stream-K), zeroed, freed behind the GEMM
+    if (m < 1 || n < 1 || k < 1) return set_error(C3_ERR_VALIDATION, "gemm: dimensions must be >= 1");
+    const size_t bytes = static_cast<size_t>(gemm_workspace_bytes(m, n, k, elem, w->prop.multiProcessorCount));
+    if (bytes > 0) {
         C3_CUDA(cudaMallocAsync(&ws, bytes, st));
         C3_CUDA(cudaMemsetAsync(ws, 0, bytes, st));
     }
@@ -1027,7 +1027,7 @@ int c3_session_destroy(c3_session* s) {
     for (void* p : s->imported) cudaIpcCloseMemHandle(p);
     for (auto* v : {&s->recv, &s->in, &s->out, &s->staging})
         for (void* p : *v) cudaFree(p);
-    for (void* p : {s->a, s->b, s->c, s->f32_ws, static_cast<void*>(s->sig),
+    for (void* p : {s->a, s->b, s->c, s->gemm_ws, static_cast<void*>(s->sig),
                     static_cast<void*>(s->done), static_cast<void*>(s->gemm_counters)})
         if (p) cudaFree(p);
     for (cudaStream_t st : {s->main, s->gemm_s, s->comm_s, s->comm_hi})

@@ -110,6 +110,38 @@ def test_gemm_kernel_variants_full(torch_mod, c3, monkeypatch, kernel, M, N, K):
     w.close()
 
 
+@pytest.mark.parametrize("M,N,K,kernel", [(256, 4096, 2048, None), (512, 2048, 1024, "narrow"),
+                                          (1024, 8192, 1024, "wide"), (128, 53248, 512, None)])
+def test_gemm_stream_k_tail(torch_mod, c3, monkeypatch, M, N, K, kernel):
+    """Compute-bound single-CTA GEMMs whose last wave on the full GPU is partly
+    empty (64 128x128 tiles; 64 forced-narrow; 256 forced-wide 128x256 tiles):
+    that wave's k-blocks are spread over one segment per SM, a tile cut into
+    up to four pieces finished by the piece that arrives last (fp32 partials
+    summed in piece order, one bf16 rounding). The memory-bound M = 128 shape
+    keeps whole tiles. Every output checked; bit-identical across runs and
+    across CTA caps (the decomposition depends on the SM count only)."""
+    if kernel:
+        monkeypatch.setenv("C3_GEMM_KERNEL", kernel)
+    torch = torch_mod
+    w = c3.World()
+    A = torch.empty(M * K, dtype=torch.int16, device="cuda")
+    B = torch.empty(N * K, dtype=torch.int16, device="cuda")
+    c3.check(c3.lib().c3_fill_bf16(A.data_ptr(), M * K, SEED, 0, 0, None))
+    c3.check(c3.lib().c3_fill_bf16(B.data_ptr(), N * K, SEED, 0, 1, None))
+    Ah, Bh = orc.bf16(M * K, SEED, 0, 0), orc.bf16(N * K, SEED, 0, 1)
+    rows, cols = np.meshgrid(np.arange(M), np.arange(N), indexing="ij")
+    outs = []
+    for cap in (0, 0, 140, 37):
+        Cm = torch.zeros(M * N, dtype=torch.int16, device="cuda")
+        w.gemm(A.data_ptr(), B.data_ptr(), Cm.data_ptr(), M, N, K, cap)
+        outs.append(Cm)
+    torch.cuda.synchronize()
+    for o in outs[1:]:
+        assert torch.equal(o, outs[0])
+    gemm_check(outs[0].cpu().numpy().view(np.uint16), Ah, Bh, M, N, K, rows.ravel(), cols.ravel())
+    w.close()
+
+
 @pytest.mark.parametrize("max_ctas", [1, 7, 148])
 def test_gemm_cta_cap_same_result(torch_mod, c3, max_ctas):
     """The CTA cap (SM allocation) must not change a single output bit."""
