@@ -82,7 +82,7 @@ struct Params {
     int* tile_ready;  // splits > 1: per-tile partials published (zero between launches)
     int* tile_counter;
     int* exit_counter;
-    unsigned long long* dbg;  // dev only (C3_F32_DBG = device address): per-CTA globaltimer stamps [8]
+    unsigned long long* dbg;  // dev timeline only (built with -DC3_F32_TIMELINE): per-CTA stamps [8]
     int dev;  // dev A/B only (C3_F32_DEV, results invalid when set): bit 0 converters skip the
               // split (arrive at once), bit 1 no MMAs (commits only)
 };
@@ -141,8 +141,14 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
 
     const int warp = threadIdx.x / 32;
     const int lane = threadIdx.x % 32;
+#ifdef C3_F32_TIMELINE
     unsigned long long* dbg = p.dbg ? p.dbg + blockIdx.x * 8 : nullptr;
-    if (dbg && threadIdx.x == 0) dbg[0] = global_ns();
+#define F32_STAMP(cond, slot) \
+    if (dbg && (cond)) dbg[slot] = global_ns()
+#else
+#define F32_STAMP(cond, slot)
+#endif
+    F32_STAMP(threadIdx.x == 0, 0);
 
     if (warp == 0 && lane == 0) {
         tma_prefetch_desc(&map_a);
@@ -171,7 +177,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem_base = *tmem_slot;
-    if (dbg && threadIdx.x == 0) dbg[1] = global_ns();
+    F32_STAMP(threadIdx.x == 0, 1);
 
     if (warp == 0 && lane == 0) {
         // ---------------- unit claimer + TMA producer ----------------
@@ -308,7 +314,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
             for (int kb = x.kb0; kb < x.kb1; ++kb) {
                 mbar_wait(&conv[stage], phase);
                 tc_fence_after();
-                if (dbg && kb == x.kb0 && i == 0) dbg[2] = global_ns();
+                F32_STAMP(kb == x.kb0 && i == 0, 2);
                 const bool slow = ld_volatile_shared(&nf_flag[stage]) != 0;
                 const uint32_t a_hi = smem_u32(stage_base + stage * STAGE), b_hi = a_hi + A_BYTES;
                 const uint32_t a_lo = smem_u32(lo_base + lo * STAGE), b_lo = a_lo + A_BYTES;
@@ -338,7 +344,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                 if (++lo == LO_BUFS) lo = 0;
             }
             umma_commit(&acc_full[acc]);
-            if (dbg && i == 0) dbg[3] = global_ns();
+            F32_STAMP(i == 0, 3);
             if (++acc == ACC_BUFS) {
                 acc = 0;
                 acc_phase ^= 1;
@@ -365,7 +371,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
             const Unit x = unit_of(p, u);
             mbar_wait(&acc_full[acc], acc_phase);
             tc_fence_after();
-            if (dbg && threadIdx.x == 128 && i == 0) dbg[4] = global_ns();
+            F32_STAMP(threadIdx.x == 128 && i == 0, 4);
             const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
             // chunk c of this warp's rows (registers) -> swizzled staging -> one TMA
             // store, or a TMA fp32 add into C (OOB rows / columns clipped by the map)
@@ -418,7 +424,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                             while (ld_acquire_gpu(p.tile_ready + x.tile) < 1) __nanosleep(64);
                         named_bar_sync(kBarEpi, 128);
                         fence_proxy_async_global();  // the acquire above orders this warp's TMA adds
-                        if (dbg && threadIdx.x == 128 && i == 0) dbg[5] = global_ns();
+                        F32_STAMP(threadIdx.x == 128 && i == 0, 5);
                     }
 #pragma unroll 1
                     for (int c = 0; c < BN; c += 32) {
@@ -440,7 +446,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                     } else if (threadIdx.x == 128) {  // for the next launch (no one else touches them now)
                         p.tile_done[x.tile] = 0;
                         p.tile_ready[x.tile] = 0;
-                        if (dbg && i == 0) dbg[6] = global_ns();
+                        F32_STAMP(i == 0, 6);
                     }
                 } else if (!is_last) {
                     // partial tile, float4 (chunk, j) of row r at [(chunk * 8 + j) * BM + r]:
@@ -467,7 +473,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                         while (ld_acquire_gpu(p.tile_ready + x.tile) < p.splits - 1) __nanosleep(64);
                     named_bar_sync(kBarEpi, 128);
                     __threadfence();
-                    if (dbg && threadIdx.x == 128 && i == 0) dbg[5] = global_ns();
+                    F32_STAMP(threadIdx.x == 128 && i == 0, 5);
 #pragma unroll 1
                     for (int c = 0; c < BN; c += 32) {
                         uint32_t v[32];
@@ -517,7 +523,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                         p.tile_done[x.tile] = 0;
                         p.tile_ready[x.tile] = 0;
                     }
-                    if (dbg && threadIdx.x == 128 && i == 0) dbg[6] = global_ns();
+                    F32_STAMP(threadIdx.x == 128 && i == 0, 6);
                 }
             }
             if (++acc == ACC_BUFS) {
@@ -529,7 +535,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
 
     tc_fence_before();
     __syncthreads();
-    if (dbg && threadIdx.x == 0) dbg[7] = global_ns();
+    F32_STAMP(threadIdx.x == 0, 7);
     if (warp == 2) {
         tc_fence_after();
         tmem_dealloc<ACC_BUFS * BN>(tmem_base);
@@ -597,8 +603,12 @@ int gemm_f32_launch(const GemmPlan* plan, int grid, cudaStream_t stream) {
         return e ? std::atoi(e) : 0;
     }();
     p.dev = dev;
-    const char* dbg = std::getenv("C3_F32_DBG");  // dev timeline (read per launch)
+    p.dbg = nullptr;
+#ifdef C3_F32_TIMELINE
+    // dev timeline builds only: stamps go to the device address in C3_F32_DBG
+    const char* dbg = std::getenv("C3_F32_DBG");
     p.dbg = dbg ? reinterpret_cast<unsigned long long*>(std::strtoull(dbg, nullptr, 0)) : nullptr;
+#endif
     grid = std::min(grid, p.num_units);
     gemm_f32_split_kernel<<<grid, THREADS, SMEM, stream>>>(plan->map_a, plan->map_b128, plan->map_c, p);
     const cudaError_t e = cudaGetLastError();

@@ -1,5 +1,6 @@
 #!/usr/bin/env python3
-"""fp32 split-TF32 GEMM per-CTA timeline (dev aid): globaltimer stamps the
+"""fp32 split-TF32 GEMM per-CTA timeline (dev aid; needs a build with
+NVCC_EXTRA=-DC3_F32_TIMELINE, e.g. `make cuda NVCC_EXTRA=-DC3_F32_TIMELINE`): globaltimer stamps the
 kernel writes when C3_F32_DBG holds a device address (gemm_f32.cu):
 0 entry, 1 setup done, 2 first stage converted (MMA side), 3 first unit's
 MMAs issued, 4 its accumulator ready (epilogue), 5 (last part) the other partials ready,
