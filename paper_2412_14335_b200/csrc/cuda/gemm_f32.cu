@@ -18,9 +18,11 @@
 // Split-K: when the 128x128 tiles are fewer than the SMs (1024^3: 64 tiles),
 // each tile's K range is cut into S parts (units = tiles x S, claimed like the
 // bf16 kernels' tiles). A part's epilogue counts itself in the tile's arrival
-// word. S = 2 (configs[0]): the first part stores into C and counts itself
-// ready, the second waits for that and adds its part into C with vector
-// reductions (two terms commute: bit-reproducible). S > 2: every part but the
+// word. S = 2 (configs[0]): the part whose epilogue reaches the tile first
+// zeroes the C tile while the main loops run, and both parts add into it with TMA reductions,
+// in whichever order they finish: (0 + p0) + p1 = (0 + p1) + p0 (fp32 addition
+// commutes), so the result is bit-reproducible and no part waits for the
+// other's result. S > 2: every part but the
 // last writes its fp32 partial to a workspace and counts it ready; the last
 // sums the S parts in the fixed order 0..S-1, its own straight from TMEM. The
 // waits cannot deadlock whatever the grid: the parts waited for are already
@@ -369,10 +371,6 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                 break;
             }
             const Unit x = unit_of(p, u);
-            mbar_wait(&acc_full[acc], acc_phase);
-            tc_fence_after();
-            F32_STAMP(threadIdx.x == 128 && i == 0, 4);
-            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
             // chunk c of this warp's rows (registers) -> swizzled staging -> one TMA
             // store, or a TMA fp32 add into C (OOB rows / columns clipped by the map)
             auto stage_out = [&](const uint32_t (&v)[32], int c, bool add) {
@@ -395,6 +393,33 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                 }
                 if (++stg_i == EPI_BUFS) stg_i = 0;
             };
+            if (p.splits == 2) {
+                // the part whose epilogue reaches the tile first (the epilogue
+                // warps are idle during the main loop) zeroes its C tile; both
+                // parts then add into it (below). Nobody waits on a part that
+                // has not started: the zeroing part is already here.
+                named_bar_sync(kBarEpi, 128);  // every thread read the previous unit's last_flag
+                if (threadIdx.x == 128)
+                    st_shared_u32(last_flag, atomicCAS(p.tile_ready + x.tile, 0, 1) == 0 ? 1u : 0u);
+                named_bar_sync(kBarEpi, 128);
+                if (ld_volatile_shared(last_flag)) {
+                    uint32_t zero[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) zero[j] = 0u;
+                    for (int c = 0; c < BN; c += 32) stage_out(zero, c, false);
+                    if (lane == 0) {
+                        bulk_wait_all();  // the zeros are in C
+                        fence_proxy_async_global();
+                    }
+                    __threadfence();
+                    named_bar_sync(kBarEpi, 128);
+                    if (threadIdx.x == 128) atomicExch(p.tile_ready + x.tile, 2);
+                }
+            }
+            mbar_wait(&acc_full[acc], acc_phase);
+            tc_fence_after();
+            F32_STAMP(threadIdx.x == 128 && i == 0, 4);
+            const uint32_t t_row = tmem_base + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(acc * BN);
             if (p.splits == 1) {
 #pragma unroll 1
                 for (int c = 0; c < BN; c += 32) {
@@ -405,8 +430,32 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                 }
                 tc_fence_before();
                 mbar_arrive(&acc_empty[acc]);
+            } else if (p.splits == 2) {
+                // both parts add into the zeroed tile: C = (0 + p_a) + p_b = p0 + p1
+                // whichever adds first (fp32 addition commutes), so no part waits
+                // for the other's result, only for the zeroing
+                if (threadIdx.x == 128)
+                    while (ld_acquire_gpu(p.tile_ready + x.tile) < 2) __nanosleep(64);
+                named_bar_sync(kBarEpi, 128);
+                if (lane == 0) fence_proxy_async_global();  // the acquire above orders this warp's TMA adds
+                F32_STAMP(threadIdx.x == 128 && i == 0, 5);
+#pragma unroll 1
+                for (int c = 0; c < BN; c += 32) {
+                    uint32_t v[32];
+                    tmem_ld_32x32b_x32(t_row + c, v);
+                    tmem_ld_wait();
+                    stage_out(v, c, true);
+                }
+                tc_fence_before();
+                mbar_arrive(&acc_empty[acc]);
+                if (threadIdx.x == 128 && atomicAdd(p.tile_done + x.tile, 1) == 1) {
+                    // the second part to finish: both passed their waits, reset for the next launch
+                    p.tile_done[x.tile] = 0;
+                    p.tile_ready[x.tile] = 0;
+                    F32_STAMP(i == 0, 6);
+                }
             } else {
-                // split-K: count in first (see the header)
+                // split-K, S > 2: count in first (see the header)
                 named_bar_sync(kBarEpi, 128);  // every thread read the previous unit's last_flag
                 if (threadIdx.x == 128) {
                     const int before = atomicAdd(p.tile_done + x.tile, 1);
@@ -415,40 +464,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                 named_bar_sync(kBarEpi, 128);
                 const size_t tile_f4 = static_cast<size_t>(BN / 4) * BM;  // float4 per partial tile
                 const bool is_last = ld_volatile_shared(last_flag) != 0;
-                if (p.splits == 2) {
-                    // the first part stores into C and counts itself ready; the
-                    // second adds into C with TMA reductions. Two terms: C = p0 + p1
-                    // whichever arrived first (fp32 addition commutes)
-                    if (is_last) {
-                        if (threadIdx.x == 128)
-                            while (ld_acquire_gpu(p.tile_ready + x.tile) < 1) __nanosleep(64);
-                        named_bar_sync(kBarEpi, 128);
-                        fence_proxy_async_global();  // the acquire above orders this warp's TMA adds
-                        F32_STAMP(threadIdx.x == 128 && i == 0, 5);
-                    }
-#pragma unroll 1
-                    for (int c = 0; c < BN; c += 32) {
-                        uint32_t v[32];
-                        tmem_ld_32x32b_x32(t_row + c, v);
-                        tmem_ld_wait();
-                        stage_out(v, c, is_last);
-                    }
-                    tc_fence_before();
-                    mbar_arrive(&acc_empty[acc]);
-                    if (!is_last) {
-                        if (lane == 0) {
-                            bulk_wait_all();  // this warp's stores are performed
-                            fence_proxy_async_global();
-                        }
-                        __threadfence();
-                        named_bar_sync(kBarEpi, 128);
-                        if (threadIdx.x == 128) atomicAdd(p.tile_ready + x.tile, 1);
-                    } else if (threadIdx.x == 128) {  // for the next launch (no one else touches them now)
-                        p.tile_done[x.tile] = 0;
-                        p.tile_ready[x.tile] = 0;
-                        F32_STAMP(i == 0, 6);
-                    }
-                } else if (!is_last) {
+                if (!is_last) {
                     // partial tile, float4 (chunk, j) of row r at [(chunk * 8 + j) * BM + r]:
                     // a warp's 32 rows are 512 contiguous bytes per store
                     float4* mine = p.ws + static_cast<size_t>(u) * tile_f4;
