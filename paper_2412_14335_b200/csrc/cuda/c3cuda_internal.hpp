@@ -174,9 +174,11 @@ struct MutPtrTable {
 
 // link_bpns > 0: pace the launch's peer traffic to that many bytes/ns in total
 // (= GB/s; NVLink emulation in loopback worlds, c3_session_set_link_rate).
+// solo: the collective has the GPU to itself (no GEMM beside it), so an
+// unpaced one on many CTAs may take the TMA bulk-copy kernel (collectives.cu).
 int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
                           int64_t chunk_bytes, int n_ctas, const Signals& sig,
-                          cudaStream_t stream, double link_bpns = 0.0);
+                          cudaStream_t stream, double link_bpns = 0.0, bool solo = false);
 int launch_alltoall_push(int self, int n, const void* send, const MutPtrTable& recv,
                          int64_t per_peer_bytes, int n_ctas, const Signals& sig, cudaStream_t stream,
                          double link_bpns = 0.0, int64_t stride_bytes = -1);  // stride: slot pitch (default = per_peer_bytes)

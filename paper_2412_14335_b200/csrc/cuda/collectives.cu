@@ -423,17 +423,25 @@ int stream_l2_enabled() {
     return on;
 }
 
-// Bulk-copy (TMA) all-gather: C3_COMM_IMPL=bulk selects it, C3_COMM_PIECE /
-// C3_COMM_NBUF size its shared-memory ring (dev A/B).
+// Bulk-copy (TMA) all-gather. Measured (profiles/r01_comm_impl_ab.txt): alone
+// on the whole GPU it moves the loopback all-gather at 0.87 of the HBM peak
+// against the LSU push's 0.72-0.75, but beside the GEMM its bulk copies starve
+// behind the GEMM's TMA operand loads. So it is used when the collective runs
+// alone, unpaced, on >= kBulkSoloUnits CTA units (the isolated collective and
+// the serial step at full speed); C3_COMM_IMPL=bulk forces it everywhere and
+// C3_COMM_IMPL=lsu never (dev A/B), C3_COMM_PIECE / C3_COMM_NBUF size its
+// shared-memory ring.
+constexpr int kBulkSoloUnits = 64;
 struct BulkCfg {
-    bool on;
+    bool on, off;
     int piece, nbuf;
 };
 const BulkCfg& bulk_cfg() {
     static const BulkCfg c = [] {
-        BulkCfg b{false, 16384, 4};
+        BulkCfg b{false, false, 16384, 4};
         const char* e = std::getenv("C3_COMM_IMPL");
         b.on = e != nullptr && std::string(e) == "bulk";
+        b.off = e != nullptr && std::string(e) == "lsu";
         if (const char* p = std::getenv("C3_COMM_PIECE")) b.piece = std::max(16, std::atoi(p) / 16 * 16);
         if (const char* q = std::getenv("C3_COMM_NBUF")) b.nbuf = std::min(kBulkMaxBufs, std::max(2, std::atoi(q)));
         return b;
@@ -461,7 +469,7 @@ int grid_for(int64_t work_items, int threads, int cap) {
 
 int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& recv,
                           int64_t chunk_bytes, int n_ctas, const Signals& sig,
-                          cudaStream_t stream, double link_bpns) {
+                          cudaStream_t stream, double link_bpns, bool solo) {
     if (n < 1 || n > C3_MAX_RANKS || self < 0 || self >= n)
         return set_error(C3_ERR_VALIDATION, "allgather: bad rank/world");
     if (chunk_bytes < 0) return set_error(C3_ERR_VALIDATION, "allgather: negative chunk");
@@ -471,7 +479,8 @@ int launch_allgather_push(int self, int n, const void* send, const MutPtrTable& 
     uintptr_t align = reinterpret_cast<uintptr_t>(send) | static_cast<uintptr_t>(chunk_bytes);
     for (int p = 0; p < n; ++p) align |= reinterpret_cast<uintptr_t>(recv.p[p]);
     if (chunk_bytes == 0 && !sig.enabled) return C3_OK;
-    if ((align & 15) == 0 && bulk_cfg().on) {
+    const bool bulk = bulk_cfg().on || (!bulk_cfg().off && solo && link_bpns <= 0.0 && n_ctas >= kBulkSoloUnits);
+    if ((align & 15) == 0 && bulk) {
         const BulkCfg& bc = bulk_cfg();
         const size_t smem = static_cast<size_t>(bc.piece) * bc.nbuf;
         static bool attr = false;

@@ -341,6 +341,7 @@ struct c3_session {
     int fused_mode = 0;                     // C3_FUSED: 0 TMA bulk copies, 1 LSU vectors
     double link_gbps = 0.0;                 // link emulation: peer-traffic budget per step (0 = off)
     double run_gbps = 0.0;                  // this run's pacing: link rate, or a concurrent run's comm pace
+    bool solo_comm = false;                 // this run's collective has the GPU to itself (no GEMM beside it)
     c3_barrier_fn barrier = nullptr;        // host barrier across ranks (copy-engine path)
     void* barrier_ctx = nullptr;
     bool ready = false;                     // peers imported (or loopback)
@@ -560,7 +561,7 @@ int enqueue_collective(c3_session* s, int backend, int n_ctas, int flags, cudaSt
                 MutPtrTable r = recv;
                 for (int q = 0; q < n; ++q) r.p[q] = static_cast<uint8_t*>(recv.p[q]) + (chunk - plen) * v + off;
                 C3_TRY(launch_allgather_push(v, n, static_cast<uint8_t*>(recv.p[v]) + chunk * v + off, r,
-                                             plen, n_ctas, sig, st, s->run_gbps));
+                                             plen, n_ctas, sig, st, s->run_gbps, s->solo_comm));
                 ++*launches;
             }
         } else {
@@ -1820,6 +1821,7 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     C3_CUDA(cudaEventRecord(s->ev_start, s->main));
     const bool do_gemm = strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;
     const bool do_comm = strategy != C3_GEMM_ONLY;
+    s->solo_comm = strategy == C3_COMM_ONLY_CU || strategy == C3_SERIAL;
     const int backend = strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA
                         : strategy == C3_COMM_ONLY_CU || serial_io ? C3_BACKEND_CU
                                                                     : a.backend;
