@@ -87,6 +87,9 @@ int64_t gemm_f32_workspace_bytes(int64_t m, int64_t n, int64_t k, int sm_count);
 // a plan's kernel kind, and the workspace bytes its plan wants (0: none)
 GemmPlan::Kind gemm_kind(int64_t m, int64_t n, int elem_bytes, int sm_count);
 int64_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int elem_bytes, int sm_count);
+// the leading bytes of that workspace that must be zero before a plan's first
+// launch (the arrival words; the partials need no initial value)
+int64_t gemm_workspace_zero_bytes(int64_t m, int64_t n, int64_t k, int elem_bytes, int sm_count);
 // stream-K arrival words (done, ready) for `cap` tail tiles, 256-byte aligned
 inline int64_t gemm_sk_counter_bytes(int cap) { return (2 * static_cast<int64_t>(cap) * 4 + 255) / 256 * 256; }
 // kernels one gemm_plan_launch issues

@@ -550,6 +550,14 @@ GemmPlan::Kind gemm_kind(int64_t m, int64_t n, int elem_bytes, int sm_count) {
     return kind;
 }
 
+int64_t gemm_workspace_zero_bytes(int64_t m, int64_t n, int64_t k, int elem_bytes, int sm_count) {
+    if (elem_bytes == 4) {
+        const int64_t tiles = ((m + 127) / 128) * ((n + 127) / 128);  // the fp32 kernel's 128 x 128 tiles
+        return std::min(gemm_f32_workspace_bytes(m, n, k, sm_count), (2 * tiles * 4 + 255) / 256 * 256);
+    }
+    return gemm_workspace_bytes(m, n, k, elem_bytes, sm_count) > 0 ? gemm_sk_counter_bytes(sm_count) : 0;
+}
+
 int64_t gemm_workspace_bytes(int64_t m, int64_t n, int64_t k, int elem_bytes, int sm_count) {
     if (elem_bytes == 4) return gemm_f32_workspace_bytes(m, n, k, sm_count);
     const GemmPlan::Kind kind = gemm_kind(m, n, elem_bytes, sm_count);

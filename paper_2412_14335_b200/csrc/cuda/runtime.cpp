@@ -388,7 +388,9 @@ int session_alloc(c3_session* s) {
     const size_t ws = static_cast<size_t>(gemm_workspace_bytes(d.m, d.n, d.k, s->elem, s->w->prop.multiProcessorCount));
     if (ws > 0) {
         C3_CUDA(cudaMalloc(&s->gemm_ws, ws));
-        C3_CUDA(cudaMemset(s->gemm_ws, 0, ws));
+        C3_CUDA(cudaMemset(s->gemm_ws, 0,
+                           static_cast<size_t>(gemm_workspace_zero_bytes(d.m, d.n, d.k, s->elem,
+                                                                         s->w->prop.multiProcessorCount))));
     }
     C3_TRY(gemm_plan_init(&s->gemm, s->a, s->b, s->c, d.m, d.n, d.k, s->gemm_counters,
                           s->w->prop.multiProcessorCount, s->elem, s->gemm_ws));
@@ -827,7 +829,8 @@ static int world_gemm(c3_world* w, const void* A, const void* B, void* C, int64_
     const size_t bytes = static_cast<size_t>(gemm_workspace_bytes(m, n, k, elem, w->prop.multiProcessorCount));
     if (bytes > 0) {
         C3_CUDA(cudaMallocAsync(&ws, bytes, st));
-        C3_CUDA(cudaMemsetAsync(ws, 0, bytes, st));
+        C3_CUDA(cudaMemsetAsync(
+            ws, 0, static_cast<size_t>(gemm_workspace_zero_bytes(m, n, k, elem, w->prop.multiProcessorCount)), st));
     }
     int rc = gemm_plan_init(&plan, A, B, C, m, n, k, ctr, w->prop.multiProcessorCount, elem, ws);
     if (rc == C3_OK) rc = gemm_plan_launch(&plan, max_ctas, w->prop.multiProcessorCount, st);
