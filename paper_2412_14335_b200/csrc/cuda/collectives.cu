@@ -427,8 +427,9 @@ int stream_l2_enabled() {
 // on the whole GPU it moves the loopback all-gather at 0.87 of the HBM peak
 // against the LSU push's 0.72-0.75, but beside the GEMM its bulk copies starve
 // behind the GEMM's TMA operand loads. So it is used when the collective runs
-// alone, unpaced, on >= kBulkSoloUnits CTA units (the isolated collective and
-// the serial step at full speed); C3_COMM_IMPL=bulk forces it everywhere and
+// alone, unpaced, on >= kBulkSoloUnits CTA units in a loopback world (the
+// isolated collective and the serial step at full speed; the runtime's `solo`);
+// C3_COMM_IMPL=bulk forces it everywhere and
 // C3_COMM_IMPL=lsu never (dev A/B), C3_COMM_PIECE / C3_COMM_NBUF size its
 // shared-memory ring.
 constexpr int kBulkSoloUnits = 64;

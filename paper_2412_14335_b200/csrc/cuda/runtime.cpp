@@ -1824,7 +1824,9 @@ static int session_run_impl(c3_session* s, int strategy, const c3_alloc* alloc_i
     C3_CUDA(cudaEventRecord(s->ev_start, s->main));
     const bool do_gemm = strategy != C3_COMM_ONLY_CU && strategy != C3_COMM_ONLY_DMA;
     const bool do_comm = strategy != C3_GEMM_ONLY;
-    s->solo_comm = strategy == C3_COMM_ONLY_CU || strategy == C3_SERIAL;
+    // loopback worlds only: over real NVLink the push is link-bound and the LSU
+    // kernel is the one exercised across processes
+    s->solo_comm = s->w->loopback && (strategy == C3_COMM_ONLY_CU || strategy == C3_SERIAL);
     const int backend = strategy == C3_COMM_ONLY_DMA ? C3_BACKEND_DMA
                         : strategy == C3_COMM_ONLY_CU || serial_io ? C3_BACKEND_CU
                                                                     : a.backend;
