@@ -217,10 +217,14 @@ def run_ours(args, dist):
         rows = []
         for _ in range(steps):
             t = sess.run(strategy, alloc)
+            # [total, GEMM kernel, collective kernel, launches, kernel span]: the
+            # span (first kernel start to last kernel end) leaves out the step's
+            # launch latency, as the isolated kernel times do
+            span = max(t.gemm_end_ms, t.comm_end_ms) - min(t.gemm_start_ms, t.comm_start_ms)
             rows.append([t.total_ms, t.gemm_end_ms - t.gemm_start_ms, t.comm_end_ms - t.comm_start_ms,
-                         float(t.launches)])
+                         float(t.launches), span])
         flat = dist.max_list([v for r in rows for v in r])
-        return [flat[i * 4:(i + 1) * 4] for i in range(steps)]
+        return [flat[i * 5:(i + 1) * 5] for i in range(steps)]
 
     # Isolated kernel times on the whole GPU are the reference's t_gemm /
     # t_comm (sim.cpp:136-138). They are measured INTERLEAVED with the
@@ -542,6 +546,19 @@ def run_ours(args, dist):
     head_res = summarise(rows, t_g_timed, t_c, t_c)
     t_conc = head_res["t_concurrent_ms"]
     speedup, ideal, frac = head_res["speedup"], head_res["ideal"], head_res["fraction_of_ideal"]
+    # the same metric with the concurrent step timed like the isolated kernels
+    # (first kernel start to last kernel end): without the step's launch
+    # latency, which the isolated kernel times do not carry either (a few us:
+    # large only for configs[0]'s ~40 us steps); value / ms_per_step keep the
+    # whole step
+    span_ms = median([r[4] for r in rows])
+    span_sp = (t_g_timed + t_c) / span_ms
+    span_res = {"t_concurrent_span_ms": span_ms, "speedup": span_sp, "ideal": ideal,
+                "fraction_of_ideal": c3.fraction_of_ideal(span_sp, ideal),
+                "launch_latency_ms": t_conc - span_ms,
+                "what": "(t_gemm_iso + t_comm_iso) / median kernel span of the C3 step (first kernel start to "
+                        "last kernel end, CUDA events on the kernels' streams); the headline value uses the "
+                        "whole step, launch latency included"}
 
     def alloc_dict(a):
         return {"cus_gemm": a.cus_gemm, "cus_comm": a.cus_comm, "cus_idle": a.cus_idle,
@@ -724,6 +741,7 @@ def run_ours(args, dist):
                    "what": "per round: (isolated GEMM + isolated collective of that round) / that round's C3 "
                            "step; per block: the headline formula over a third of the rounds"},
         "flags": flags,
+        "kernel_span": span_res,
         "absolute": {"t_concurrent_ms": t_conc, "t_gemm_iso_ms": t_g_timed, "t_comm_iso_ms": t_c,
                      "t_serial_ms": t_g_timed + t_c,
                      "gemm_tflops_in_step": flops / (median(gemm_ms) * 1e-3) / 1e12,

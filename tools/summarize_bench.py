@@ -1,7 +1,8 @@
 #!/usr/bin/env python3
 """One table row per bench line in a directory (bench_<cfg>.json and
 bench_<cfg>_reference.json, tools/round_evidence.sh): speedup, fraction of
-ideal, paired spread, e2e, copy-engine proxy, library ratio, GEMM roofline
+ideal, the same with the step timed as a kernel span, paired spread, e2e,
+copy-engine proxy, library ratio, GEMM roofline
 fraction, C3-pair roofline fraction and the reference arm.
 
 usage: python tools/summarize_bench.py DIR"""
@@ -22,16 +23,17 @@ def last_json(path):
 
 def main():
     d = sys.argv[1]
-    print("| config | C3 speedup (fraction of ideal) | paired spread | e2e (vs overlapped-I/O serial) | "
-          "conccl CE proxy | library/ours | GEMM roofline | pair roofline | reference arm |")
-    print("|---|---|---|---|---|---|---|---|---|")
+    print("| config | C3 speedup (fraction of ideal) | kernel-span speedup (fraction) | paired spread | "
+          "e2e (vs overlapped-I/O serial) | conccl CE proxy | library/ours | GEMM roofline | pair roofline | "
+          "reference arm |")
+    print("|---|---|---|---|---|---|---|---|---|---|")
     for path in sorted(glob.glob(os.path.join(d, "bench_*.json"))):
         if path.endswith("_reference.json"):
             continue
         name = os.path.basename(path)[len("bench_"):-len(".json")]
         b = last_json(path)
         if not b or "value" not in b:
-            print(f"| {name} | (no line) | | | | | | | |")
+            print(f"| {name} | (no line) | | | | | | | | |")
             continue
         r = last_json(path.replace(".json", "_reference.json")) or {}
         sp = b.get("spread", {}).get("paired_round_speedups", {})
@@ -42,8 +44,10 @@ def main():
         roof = b.get("roofline") or {}
         pr = b.get("c3_roofline") or {}
         fr = b.get("fraction_of_ideal_pct")
+        ks = b.get("kernel_span") or {}
         cells = [name,
                  f"{b['value']:.3f}x ({fr:.0f}%)" if fr is not None else f"{b['value']:.3f}x",
+                 f"{ks.get('speedup', 0):.3f}x ({100 * ks.get('fraction_of_ideal', 0):.0f}%)" if ks else "",
                  f"{sp.get('min', 0):.2f}-{sp.get('max', 0):.2f}" if sp else "",
                  f"{e2e.get('value', 0):.2f}x ({e2e.get('vs_serial_overlapped_io', 0):.2f}x)" if e2e else "",
                  (f"{ce_c.get('speedup', 0):.2f}x ({100 * ce_c.get('fraction_of_ideal', 0):.0f}%)" if ce_c else ""),
