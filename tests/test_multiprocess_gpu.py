@@ -120,6 +120,18 @@ def _worker(rank, world, port, coll, q):
             d.barrier()
             results[("host", strat)] = (check(s2, big), t.total_ms)
         s2.close()
+        if coll == c3.ALL_GATHER:
+            # configs[0]'s session kind across processes: fp32 GEMM (split-TF32,
+            # split-K) beside the all-gather, every strategy that runs the SM path
+            s3 = c3.Session(w, 1024, 1024, 1024, coll, payload, dtype_bytes=4)
+            s3.import_handles(d.allgather_bytes(s3.export_handles()))
+            for strat in (c3.C3_BASE, c3.C3_SP, c3.SERIAL, c3.CONCCL):
+                s3.fill(SEED)
+                d.barrier()
+                t = s3.run(strat)
+                d.barrier()
+                results[("f32", strat)] = (check(s3, chunk), t.total_ms)
+            s3.close()
         s.close()
         w.close()
         d.close()
