@@ -435,7 +435,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                 // whichever adds first (fp32 addition commutes), so no part waits
                 // for the other's result, only for the zeroing
                 if (threadIdx.x == 128)
-                    while (ld_acquire_gpu(p.tile_ready + x.tile) < 2) __nanosleep(64);
+                    wait_ge_gpu(p.tile_ready + x.tile, 2);
                 named_bar_sync(kBarEpi, 128);
                 if (lane == 0) fence_proxy_async_global();  // the acquire above orders this warp's TMA adds
                 F32_STAMP(threadIdx.x == 128 && i == 0, 5);
@@ -486,7 +486,7 @@ gemm_f32_split_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_co
                     if (threadIdx.x == 128) atomicAdd(p.tile_ready + x.tile, 1);
                 } else {
                     if (threadIdx.x == 128)
-                        while (ld_acquire_gpu(p.tile_ready + x.tile) < p.splits - 1) __nanosleep(64);
+                        wait_ge_gpu(p.tile_ready + x.tile, p.splits - 1);
                     named_bar_sync(kBarEpi, 128);
                     __threadfence();
                     F32_STAMP(threadIdx.x == 128 && i == 0, 5);

@@ -353,7 +353,7 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                         if (threadIdx.x == 128) atomicAdd(p.sk_ready + tt, 1);
                     } else {
                         if (threadIdx.x == 128)
-                            while (ld_acquire_gpu(p.sk_ready + tt) < pce.count - 1) __nanosleep(64);
+                            wait_ge_gpu(p.sk_ready + tt, pce.count - 1);
                         named_bar_sync(1, 128);
                         __threadfence();
 #pragma unroll 1

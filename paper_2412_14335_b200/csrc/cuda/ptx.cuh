@@ -513,6 +513,23 @@ __device__ __forceinline__ int ld_acquire_gpu(const int* p) {
     asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
     return v;
 }
+// Wait until *p >= target (gpu-scope acquire) for a word another CTA of the
+// same kernel publishes. The GEMMs' split-K / stream-K protocols only wait
+// on parts already in their epilogues, so this returns in microseconds; should
+// that ever fail, the kernel traps after 2 s (a launch error for the host)
+// instead of hanging the GPU.
+__device__ __forceinline__ void wait_ge_gpu(const int* p, int target) {
+    uint64_t t0 = 0;
+    for (int spins = 0; ld_acquire_gpu(p) < target; ++spins) {
+        if ((spins & 1023) == 1023) {
+            uint64_t now;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+            if (t0 == 0) t0 = now;
+            else if (now - t0 > 2000000000ull) __trap();
+        }
+        __nanosleep(64);
+    }
+}
 __device__ __forceinline__ void st_shared_u32(void* p, uint32_t v) {
     asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(p)), "r"(v) : "memory");
 }
