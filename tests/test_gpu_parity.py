@@ -740,7 +740,7 @@ def test_gemm_f32_stream_ordered_back_to_back(torch_mod, c3):
     w.close()
 
 
-@pytest.mark.parametrize("K", [64, 256])  # 256: split-K (4 parts) over the slow path
+@pytest.mark.parametrize("K", [64, 128, 192, 256])  # split-K 1, 2 (TMA adds), 3 and 4 (workspace) parts
 def test_gemm_f32_propagates_inf_and_nan(torch_mod, c3, K):
     """Infinities and NaNs follow IEEE fp32 GEMM semantics: every product
     a*b is formed once (inf * finite = inf, inf * 0 = NaN, inf * inf = inf,
