@@ -142,7 +142,7 @@ class ClockSampler:
         if t0 is not None and t1 is not None and lines:
             inside = [x for x in lines if t0 <= x[0] <= t1 + 0.03]
             lines = inside if inside else sorted(lines, key=lambda x: abs(x[0] - (t0 + t1) / 2))[:3]
-        sms, maxs, reasons = [], [], set()
+        sms, maxs, watts, reasons = [], [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for _, ln in lines:
             parts = [p.strip() for p in ln.split(",")]
@@ -151,6 +151,10 @@ class ClockSampler:
             try:
                 sms.append(float(parts[0]))
                 maxs.append(float(parts[1]))
+                try:
+                    watts.append(float(parts[2]))
+                except ValueError:
+                    pass
             except ValueError:
                 continue
             for nm, v in zip(names, parts[3:7]):
@@ -159,6 +163,7 @@ class ClockSampler:
         loaded = [s for s in sms if s > 300] or sms
         return {"sm_mhz": statistics.median(loaded) if loaded else None,
                 "sm_max_mhz": max(maxs) if maxs else None,
+                "power_w": statistics.median(watts) if watts else None,
                 "reasons": sorted(reasons), "samples": len(sms)}
 
 
