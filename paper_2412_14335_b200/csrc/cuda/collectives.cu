@@ -42,7 +42,6 @@ constexpr int kThreads = 512;  // byte-granular kernels (tiny parity cases)
 constexpr int kVecThreads = 256;
 constexpr int kCtasPerUnit = 2;
 constexpr int kThreadsRs = kVecThreads;
-constexpr int kUnroll = 4;
 // all-to-all moves one store per load (all-gather: n-1), so each thread keeps
 // more vectors in flight: 16 (C3_A2A_UNROLL, build-time A/B): co-resident
 // cfg2 all-to-all at 24-48 units 0.23-0.61 -> 0.82-0.88 of ideal

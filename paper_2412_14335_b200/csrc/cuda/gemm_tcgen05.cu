@@ -41,7 +41,6 @@ namespace gemm {
 
 constexpr int BM = 128;          // UMMA M (one CTA)
 constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
-constexpr int UK = 16;           // UMMA K for 16-bit inputs
 constexpr int ACC_BUFS = 2;
 constexpr int THREADS = 256;
 constexpr int GROUP_M = 16;      // tile raster: 16 M-tiles per band for L2 reuse
@@ -247,7 +246,7 @@ gemm_bf16_tn_kernel(const __grid_constant__ CUtensorMap map_a,
                     const uint32_t b_addr = b0 + stage * K::B_STAGE;
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
-                        // advancing K inside the 128-byte swizzle atom = +32 B (16 bf16) per MMA
+                        // advancing K inside the 128-byte swizzle atom = +32 B (16 bf16, one UMMA K) per MMA
                         umma_bf16(d_tmem, smem_desc_k_sw128(a_addr + k * 32), smem_desc_k_sw128(b_addr + k * 32),
                                   idesc, (kb != pc[pi].kb0 || k != 0) ? 1u : 0u);
                     }

@@ -40,7 +40,6 @@ namespace gemm2 {
 constexpr int BM = 256;        // pair tile rows (128 per CTA)
 constexpr int BK = 64;
 constexpr int UK = 16;
-constexpr int THREADS = 256;  // 256-wide tiles: warps 0-3 roles, 4-7 epilogue
 // Pair-rows per raster band (C3_GEMM_BAND env overrides, dev A/B). Measured
 // DRAM reads per cfg2 launch: band 8 -> 2.39 GB, 16 -> 3.85 GB, 32 -> 12.3 GB
 // (profiles/r01_gemm_band_ab.txt): the L2 is split across the two dies, so a
