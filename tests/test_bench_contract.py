@@ -58,5 +58,8 @@ def test_our_arm_contract():
     assert d["config"] == bench.bench_config(SimpleNamespace(config="cfg1"), 1)
     assert d["e2e"]["unit"] == d["unit"]
     assert d["e2e"]["d2h_bytes_per_step"] == 1024 * 1024 * 4  # the whole fp32 C
+    ks = d["kernel_span"]  # the metric with the step timed as a kernel span, beside the headline
+    assert ks["t_concurrent_span_ms"] > 0 and ks["t_concurrent_span_ms"] <= d["ms_per_step_median"] + 1e-9
+    assert ks["speedup"] >= d["value"] - 1e-9 and "power_w" in d["clocks"]
     assert d["details"]["strategy_choice"]["strategy"] in (
         "serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp", "c3_fused")
