@@ -22,6 +22,12 @@
 // end, with claiming the other SMs absorb the work (measured: profiles/
 // r01_strategy_grid_*.json).
 //
+// Stream-K tail (compute-bound shapes whose last wave on the full GPU is
+// partly empty): the claims after the whole tiles are equal k-block segments
+// of the remaining tiles, one per SM; a tile cut into pieces is finished by
+// the piece that arrives last (fixed-order fp32 fix-up, one bf16 rounding).
+// See Params::full_units and the epilogue; profiles/r02g_streamk_ab.txt.
+//
 // Warp roles (256 threads): warp 0 = tile claimer + TMA producer (one
 // thread), warp 1 = MMA issuer (one thread), warp 2 = TMEM allocator,
 // warps 4..7 = epilogue (warp 4+q reads TMEM lanes 32q..32q+31 = tile rows).
