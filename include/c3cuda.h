@@ -195,6 +195,10 @@ int c3_fill_f32(void* dst, int64_t count, uint64_t seed, int rank, int tensor, v
  * formed once). K, N multiples of 4. */
 int c3_gemm_f32(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n, int64_t k,
                 int max_ctas, void* stream);
+/* bf16 A, B, C. The result bits do not depend on max_ctas (a compute-bound
+ * shape on the single-CTA kernels runs a stream-K tail decomposed by the SM
+ * count, with a fixed-order fix-up); those shapes take a stream-ordered
+ * workspace on `stream`. */
 int c3_gemm_bf16(c3_world* w, const void* A, const void* B, void* C, int64_t m, int64_t n,
                  int64_t k, int max_ctas, void* stream);
 
