@@ -198,7 +198,7 @@ def _ag_buffers(torch, n, chunk):
     return bufs
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 7, 8])
 @pytest.mark.parametrize("chunk", [1, 3, 16, 4096, 1000 * 16 + 7, 8 << 20])
 def test_allgather_p2p_bit_exact(torch_mod, c3, n, chunk):
     torch = torch_mod
@@ -214,7 +214,7 @@ def test_allgather_p2p_bit_exact(torch_mod, c3, n, chunk):
     w.close()
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 3, 4, 7, 8])
 @pytest.mark.parametrize("chunk", [1, 3, 4096, 8 << 20])
 def test_allgather_ce_plan_bit_exact(torch_mod, c3, n, chunk):
     """Copy-engine executor runs the product's validated plan_all_gather."""
@@ -233,7 +233,7 @@ def test_allgather_ce_plan_bit_exact(torch_mod, c3, n, chunk):
     w.close()
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 3, 4, 5, 7, 8])
 @pytest.mark.parametrize("count", [1, 5, 8, 4096, 123456, 1 << 22])
 def test_reduce_scatter_p2p_bit_exact(torch_mod, c3, n, count):
     torch = torch_mod
@@ -265,7 +265,7 @@ SESSION_STRATS = list(range(7)) + [100, 101, 102]
 
 
 @pytest.mark.parametrize("collective", [0, 2])
-@pytest.mark.parametrize("n", [2, 8])
+@pytest.mark.parametrize("n", [2, 3, 8])
 def test_session_all_strategies_loopback(torch_mod, c3, collective, n):
     """Every strategy executes the full C3 pair; the collective's output is
     bit-exact for every virtual rank and the GEMM is within tolerance."""
@@ -315,7 +315,7 @@ def test_session_all_strategies_loopback(torch_mod, c3, collective, n):
     w.close()
 
 
-@pytest.mark.parametrize("n", [2, 4, 8])
+@pytest.mark.parametrize("n", [2, 3, 4, 7, 8])
 @pytest.mark.parametrize("slot", [1, 5, 4096, 1 << 20])
 def test_alltoall_p2p_and_ce_bit_exact(torch_mod, c3, n, slot):
     """All-to-all (reference plan_all_to_all semantics, §8(f) F1): P2P push and
