@@ -1416,6 +1416,9 @@ int c3_session_predict(c3_session* s, int strategy, double t_gemm_ms, double t_c
 // partition_heuristic (strategy.cpp:48-94). The DMA backend's link bandwidth
 // is set so that plan_cost reproduces the measured copy-engine time. Serial
 // wins when no concurrent strategy is predicted to beat it.
+// a B200 co-resident pick must predict at least this much below serial
+constexpr double kCoresidentMargin = 0.02;
+
 int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, double t_comm_dma_ms,
                       int allow_dma, int* strategy, c3_alloc* alloc, double* predicted_ms) {
     if (!s || !strategy || !alloc || !predicted_ms)
@@ -1425,6 +1428,7 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
     return guarded([&] {
         const bool use_dma = allow_dma && t_comm_dma_ms > 0;
         double best = (t_gemm_ms + std::min(t_comm_cu_ms, use_dma ? t_comm_dma_ms : t_comm_cu_ms)) * 1e-3;
+        const double serial = best;
         int best_st = C3_SERIAL;
         for (int st = C3_C3_BASE; st <= C3_CONCCL_RP; ++st) {
             const bool dma = st == C3_CONCCL || st == C3_CONCCL_RP;
@@ -1474,7 +1478,12 @@ int c3_session_choose(c3_session* s, double t_gemm_ms, double t_comm_cu_ms, doub
                     if (pick && x.c != pick->c) break;
                     pick = &x;
                 }
-            if (pick && pick->m < best) {
+            // and it must beat serial by more than the co-residency model's error
+            // (RMS ~4.7%): a collective that is a few % of the GEMM (full local
+            // speed, small payloads) gains at most those few %, and a co-resident
+            // or slow-paced collective there measured up to 6% SLOWER than serial
+            // (profiles/r02p_layer_pipeline.csv, full-speed rows)
+            if (pick && pick->m < best && pick->m < serial * (1.0 - kCoresidentMargin)) {
                 best = pick->m;
                 best_st = C3_C3_BASE;
                 best_cores = pick->c;
