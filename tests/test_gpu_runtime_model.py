@@ -155,3 +155,20 @@ def test_comm_curve_changes_and_restores_reference_predictions(c3, session):
     assert slow != pytest.approx(base)
     with pytest.raises(c3.C3Error):
         s.set_comm_curve([(16, 1.0), (16, 2.0)])
+
+
+def test_choose_keeps_serial_when_the_coresident_gain_is_within_the_model_error(c3, session, cores_unit_comm):
+    """A collective that is ~1% of the GEMM can save at most ~1%: below the
+    co-residency model's error (the 2% margin of c3_session_choose), so the
+    heuristic keeps serial rather than gamble a co-resident or slow-paced pick
+    that measured up to 6% slower at full speed."""
+    w, s = session
+    sms = w.info.sm_count
+    s.load_coresident(cores_unit_comm)
+    s.set_comm_curve([(16, 0.03), (sms, 0.03)])
+    st, a, pred = s.choose(3.0, 0.03, 0.0, allow_dma=False)
+    assert st == c3.SERIAL, (st, a.cus_comm, pred)
+    # the same GEMM with a collective a third of its length: a co-resident pick
+    s.set_comm_curve([(16, 1.0), (sms, 1.0)])
+    st, a, _ = s.choose(3.0, 1.0, 0.0, allow_dma=False)
+    assert st == c3.C3_BASE and a.cus_comm > 0
