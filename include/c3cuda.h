@@ -367,7 +367,8 @@ int c3_session_predict(c3_session* s, int strategy, double t_gemm_ms, double t_c
  * the SM collective on c CTAs beside it) for c in {8,16,24,32,48,64} and the
  * curve's points, and returns it as C3_C3_BASE (GEMM launched first, the
  * collective's CTAs beside it) with cus_gemm = all SMs, cus_comm = c when it
- * is fastest. NULL path disables. */
+ * is fastest and predicts at least 2% below serial (the co-residency model's
+ * error; a smaller predicted gain keeps serial). NULL path disables. */
 int c3_session_set_comm_curve(c3_session* s, const int* ctas, const double* ms, int n);
 int c3_session_load_coresident(c3_session* s, const char* json_path);
 /* Prediction for an explicit allocation: co-resident allocations (CU backend,
