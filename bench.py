@@ -65,6 +65,9 @@ CONFIGS = {
     "cfg4_mb": dict(desc="LLaMA-405B small-token (memory-bound) GEMM 128x53248x16384 || "
                          "all-gather 1664 MiB",
                     m=128, n=53248, k=16384, coll="all-gather", payload=1664 * MIB),
+    "cfg4_mb64": dict(desc="LLaMA-405B small-token (memory-bound) GEMM 64x53248x16384 || "
+                           "all-gather 1664 MiB (configs[3]'s M = 64 case)",
+                      m=64, n=53248, k=16384, coll="all-gather", payload=1664 * MIB),
 }
 PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
 METRIC = "C3 speedup over serial and % of ideal speedup (GEMM+all-gather) at 2/4/8 B200"

@@ -11,7 +11,7 @@ mkdir -p "$OUT"
 timeout 1500 python -m pytest tests -m gpu -q > "$OUT/gputest.log" 2>&1; echo "pytest rc=$?"; tail -2 "$OUT/gputest.log"
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > "$OUT/smoke.log" 2>&1; echo "smoke rc=$?"
 timeout 900 python bench.py > "$OUT/bench_default.json" 2> "$OUT/bench_default.err"; echo "bench rc=$?"
-for c in cfg2_448 cfg3 cfg4 cfg4_mb cfg2_a2a cfg1; do
+for c in cfg2_448 cfg3 cfg4 cfg4_mb cfg4_mb64 cfg2_a2a cfg1; do
   timeout 900 python bench.py --config $c > "$OUT/bench_$c.json" 2> "$OUT/bench_$c.err"; echo "bench $c rc=$?"
   timeout 600 python bench.py --config $c --impl reference > "$OUT/bench_${c}_reference.json" 2>> "$OUT/bench_$c.err"
 done
