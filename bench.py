@@ -82,7 +82,8 @@ def bench_config(args, world):
     return {"workload": f"{args.config}: {cfg['desc']}", "gemm_mnk": [cfg["m"], cfg["n"], cfg["k"]],
             "gemm_dtype": "fp32" if cfg.get("dtype_bytes", 2) == 4 else "bf16",
             "collective": cfg["coll"], "payload_bytes": cfg["payload"], "ranks": n,
-            "l2": "inputs > 126 MB L2 (no flush needed)" if cfg["m"] * cfg["k"] * 2 > (126 << 20)
+            "l2": "inputs > 126 MB L2 (no flush needed)"
+                  if cfg.get("dtype_bytes", 2) * (cfg["m"] + cfg["n"]) * cfg["k"] > (126 << 20)
                   else "GEMM operands fit L2; collective buffers do not"}
 
 
