@@ -63,3 +63,18 @@ def test_our_arm_contract():
     assert ks["speedup"] >= d["value"] - 1e-9 and "power_w" in d["clocks"]
     assert d["details"]["strategy_choice"]["strategy"] in (
         "serial", "c3_base", "c3_sp", "c3_rp", "c3_sp_rp", "conccl", "conccl_rp", "c3_fused")
+
+
+def test_bench_configs_static_and_l2_rule():
+    """Every BASELINE config's static `config` (shared by both arms) names
+    its workload, and says whether the timed steps flush the L2: only inputs
+    that fit the 126 MB L2 (configs[0]) are flushed."""
+    sys.path.insert(0, REPO)
+    import bench
+    from types import SimpleNamespace
+    for name, cfg in bench.CONFIGS.items():
+        c = bench.bench_config(SimpleNamespace(config=name), 1)
+        assert c["workload"].startswith(name + ":") and c["gemm_mnk"] == [cfg["m"], cfg["n"], cfg["k"]]
+        assert c["ranks"] == cfg.get("ranks", 8) and c["payload_bytes"] == cfg["payload"]
+        assert ("flushed" in c["l2"]) == bench.l2_resident(cfg)
+    assert bench.l2_resident(bench.CONFIGS["cfg1"]) and not bench.l2_resident(bench.CONFIGS["cfg2"])
