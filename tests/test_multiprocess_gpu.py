@@ -7,7 +7,9 @@ copies, waited on by a one-warp kernel / the local reduce) — checked
 bit-exactly against the oracle.
 
 This is the same code a one-process-per-GPU torchrun world executes; only the
-peer mapping is same-device IPC instead of NVLink (the box gives one GPU).
+peer mapping is same-device IPC instead of NVLink (the box gives one GPU). On
+a box with as many GPUs as ranks, every rank takes its own device, and the
+same tests run over NVLink peers (`_device`).
 Kernels of the two processes time-slice on the device, so barrier waits here
 cost scheduler slices: this test checks correctness, not speed.
 """
@@ -30,6 +32,12 @@ def _free_port():
     return p
 
 
+def _device(rank, world):
+    """Rank r on GPU r when the box has a GPU per rank, else all on GPU 0."""
+    import torch
+    return rank if torch.cuda.device_count() >= world else 0
+
+
 def _worker(rank, world, port, coll, q):
     try:
         os.environ.update({"RANK": str(rank), "WORLD_SIZE": str(world), "LOCAL_RANK": str(rank),
@@ -38,7 +46,7 @@ def _worker(rank, world, port, coll, q):
         from paper_2412_14335_b200.dist import Dist
         from tests import _oracle as orc
         d = Dist()
-        w = c3.World(rank, world, 0, loopback=False)
+        w = c3.World(rank, world, _device(rank, world), loopback=False)
         os.environ["C3_GEMM_KERNEL"] = "pair"  # the fused path needs the CTA-pair GEMM
         M, N, K = 512, 1024, 256
         chunk = 256 << 10
@@ -188,7 +196,7 @@ def _exec_worker(rank, world, port, strategy, q):
         import c3sim
         from paper_2412_14335_b200.dist import Dist
         d = Dist()
-        w = c3sim.World(rank, world, 0, False)
+        w = c3sim.World(rank, world, _device(rank, world), False)
         s = c3sim.C3Scenario()
         s.id = "mp"
         s.gemm.m, s.gemm.n, s.gemm.k, s.gemm.dtype_bytes = 512, 1024, 256, 2
@@ -233,7 +241,7 @@ def _dead_peer_worker(rank, world, port, coll, strategy, q):
         import paper_2412_14335_b200 as c3
         from paper_2412_14335_b200.dist import Dist
         d = Dist()
-        w = c3.World(rank, world, 0, loopback=False)
+        w = c3.World(rank, world, _device(rank, world), loopback=False)
         s = c3.Session(w, 256, 256, 256, coll, world * (256 << 10))
         s.import_handles(d.allgather_bytes(s.export_handles()))
         s.fill(SEED)
